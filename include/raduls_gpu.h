@@ -1,0 +1,151 @@
+/*
+ * raduls_gpu.h — C-ABI of the B200-native MSD record sort (libraduls_gpu.so).
+ *
+ * Drop-in for the reference entry point
+ *     void raduls::sort(uint8_t* data, size_t n, const RecordLayout& layout,
+ *                       const SchedulerConfig& cfg = {});
+ * (/root/reference/proj/include/raduls/scheduler.hpp:56-61,
+ *  /root/reference/proj/src/scheduler.cpp:40-45)
+ * in the (input buffer, temp buffer, n_recs, rec_size, key_size) shape named by
+ * BASELINE.json. Plain pointers and sizes only; no exceptions cross the ABI.
+ *
+ * Record model (reference layout.hpp:1-81): a record is rec_size bytes
+ * (8, 16, 24 or 32); the key is its first key_size bytes (1..rec_size), most
+ * significant byte first, compared as memcmp. The reference accepts only
+ * key_size 8 or 16 (layout.hpp:22-27); this library also takes any other
+ * key_size <= rec_size (e.g. 24, BASELINE config C4).
+ *
+ * Result: records ordered non-decreasingly by key, in the caller's buffer.
+ * The sort is stable (equal keys keep their input order). The reference's MSD
+ * is not stable (Shell/introsort tails, small_sorts.hpp:166-167), so for
+ * equal keys only the key sequence and the per-run record multiset are
+ * comparable — which is the parity definition.
+ *
+ * Status codes (errors are reported before any write to `data`):
+ */
+#ifndef RADULS_GPU_H
+#define RADULS_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    RADULS_GPU_OK = 0,
+    RADULS_GPU_EINVAL = 1,   /* bad layout, misaligned pointer, n*rec_size overflow
+                                (reference: std::invalid_argument, dispatch.hpp:37-39) */
+    RADULS_GPU_ENOMEM = 2,   /* device/pinned allocation failed, input untouched
+                                (reference: raduls::resource_error, record_array.hpp:21-28) */
+    RADULS_GPU_ECUDA = 3,    /* a CUDA runtime call failed */
+    RADULS_GPU_ENCCL = 4,    /* reserved for the multi-GPU exchange */
+    RADULS_GPU_EINTERNAL = 5 /* planner capacity invariant violated (bug) */
+};
+
+/* Human-readable text for a status code. */
+const char* raduls_gpu_strerror(int code);
+
+/* 1 if (rec_size, key_size) is supported, else 0. */
+int raduls_gpu_layout_valid(uint32_t rec_size, uint32_t key_size);
+
+/* Library/ABI version, e.g. 0x000100 for 0.1.0. */
+uint32_t raduls_gpu_version(void);
+
+/*
+ * Device-resident sort (replaces raduls::sort; scheduler.hpp:60-61).
+ *   d_data : n_recs*rec_size bytes of device memory (16-B aligned for rec_size
+ *            16/32, 8-B aligned for 8/24); sorted in place.
+ *   d_tmp  : scratch of the same size, or NULL: the library then allocates it
+ *            (cudaMallocAsync on `stream`) and frees it before returning, like
+ *            the reference's internal aux array (msd_sorter.hpp:52).
+ *   stream : a cudaStream_t (NULL = legacy default stream).
+ * The call blocks until the sort has completed on `stream` (the MSD planner
+ * reads a few counters back per level), mirroring the synchronous reference.
+ * Calls on the same device are serialised (one shared workspace per device).
+ */
+int raduls_gpu_sort(void* d_data, void* d_tmp, uint64_t n_recs, uint32_t rec_size,
+                    uint32_t key_size, void* stream);
+
+/*
+ * Host drop-in mirroring raduls::sort(data, n, layout, cfg): `data` is host
+ * memory (any alignment); H2D -> device sort -> D2H. `tmp` is ignored (the
+ * device scratch is library-owned); pass NULL.
+ */
+int raduls_gpu_sort_host(uint8_t* data, uint8_t* tmp, uint64_t n_recs, uint32_t rec_size,
+                         uint32_t key_size);
+
+/* Accounting of the most recent sort on the calling thread's device. */
+typedef struct {
+    uint32_t levels;            /* planner levels executed */
+    uint32_t scatter_launches;  /* k_scatter launches */
+    uint64_t hist_records;      /* records read by histogram passes (k_histo_all + k_seg_hist) */
+    uint64_t scatter_records;   /* records moved by scatter passes (1 read + 1 write each) */
+    uint64_t local_records;     /* records moved by local sorts */
+    uint64_t copy_records;      /* records moved by copy-back */
+    uint64_t fallback_groups;   /* local-sort groups that needed the full-key fallback */
+    uint64_t skipped_levels;    /* segment-levels skipped as constant digits (e) */
+} raduls_gpu_stats;
+
+int raduls_gpu_last_stats(raduls_gpu_stats* out);
+
+/*
+ * Building blocks (tests, benchmarks and the multi-GPU driver). All device
+ * pointers; asynchronous on `stream` unless noted.
+ */
+
+/* One stable single-digit split of d_src into d_dst by record byte
+ * `key_byte_offset` (reference radix_split, kernels.hpp:157-167);
+ * h_counts (host, 256 u64, may be NULL) receives the digit histogram.
+ * Synchronous. */
+int raduls_gpu_split(const void* d_src, void* d_dst, uint64_t n_recs, uint32_t rec_size,
+                     uint32_t key_byte_offset, uint64_t* h_counts, void* stream);
+
+/* Histograms of record bytes 0..min(key_size,8)-1 (reference build_histogram,
+ * kernels.hpp:71-77) and AND/OR of every 64-bit record word. Synchronous.
+ * h_hist: host [8][256] u64; h_andor: host [8] u64 (and at 2w, or at 2w+1). */
+int raduls_gpu_histogram(const void* d_data, uint64_t n_recs, uint32_t rec_size,
+                         uint32_t key_size, uint64_t* h_hist, uint64_t* h_andor, void* stream);
+
+/* SURVEY.md §8(d) generator; dist 0 uniform, 1 = C3 skew. Record i gets
+ * global index index_base + i. */
+int raduls_gpu_generate(void* d_out, uint64_t n_recs, uint32_t rec_size, uint32_t key_size,
+                        uint32_t dist, uint64_t seed, uint64_t index_base, void* stream);
+
+/* array_digest (reference verify.cpp:37-50). Synchronous. */
+int raduls_gpu_digest(const void* d_data, uint64_t n_recs, uint32_t rec_size, uint64_t* lo,
+                      uint64_t* hi, void* stream);
+
+/* check_sorted (reference verify.cpp:27-35): *violations = number of adjacent
+ * inversions, *first = first one (or UINT64_MAX). Synchronous. */
+int raduls_gpu_check_sorted(const void* d_data, uint64_t n_recs, uint32_t rec_size,
+                            uint32_t key_size, uint64_t* violations, uint64_t* first,
+                            void* stream);
+
+/*
+ * Multi-GPU key-range partition; one process per GPU,
+ * exchange done by the caller (NCCL all-to-all).
+ *
+ * raduls_gpu_prefix_histogram: d_hist (device, 65536 u64, accumulated into)
+ *   counts records by the 16-bit big-endian value of key bytes
+ *   (prefix_byte, prefix_byte+1) — bytes at or beyond key_size read as 0.
+ * raduls_gpu_partition: stable scatter of d_src into d_dst grouped by
+ *   destination rank = d_bucket_rank[16-bit prefix] (< n_ranks <= 256);
+ *   h_rank_counts (host, n_ranks u64) receives the per-rank record counts.
+ *   Synchronous.
+ */
+int raduls_gpu_prefix_histogram(const void* d_data, uint64_t n_recs, uint32_t rec_size,
+                                uint32_t key_size, uint32_t prefix_byte, uint64_t* d_hist,
+                                void* stream);
+int raduls_gpu_partition(const void* d_src, void* d_dst, uint64_t n_recs, uint32_t rec_size,
+                         uint32_t key_size, uint32_t prefix_byte, const uint32_t* d_bucket_rank,
+                         uint32_t n_ranks, uint64_t* h_rank_counts, void* stream);
+
+/* Release the cached per-device workspace (optional). */
+void raduls_gpu_release(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RADULS_GPU_H */

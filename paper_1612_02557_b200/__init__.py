@@ -1,0 +1,28 @@
+"""B200-native MSD radix sort of fixed-size records (RADULS, arXiv 1612.02557).
+
+The product is ``libraduls_gpu.so`` (C-ABI: ``include/raduls_gpu.h``; CUDA
+kernels for sm_100a plus the C++ level planner under ``csrc/``). This package
+is the thin Python mirror of the reference's interface used by tests, the
+benchmark and the multi-GPU driver.
+"""
+from .raduls import (  # noqa: F401
+    DIST_SKEW,
+    DIST_UNIFORM,
+    BigBinFraction,
+    CudaError,
+    RecordLayout,
+    ResourceError,
+    SchedulerConfig,
+    TinyPolicy,
+    check_sorted,
+    digest,
+    generate,
+    histogram,
+    last_stats,
+    local_capacity,
+    sort,
+    sort_device,
+    split,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,100 @@
+"""ctypes binding of libraduls_gpu.so (C-ABI in include/raduls_gpu.h).
+
+There is no CPU fallback: if the shared library is missing or cannot be
+loaded, every entry point raises. The library is loaded from this package
+directory only (never from site-packages), so the driver can see which .so
+the tests and the bench actually used.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libraduls_gpu.so")
+
+OK, EINVAL, ENOMEM, ECUDA, ENCCL, EINTERNAL = 0, 1, 2, 3, 4, 5
+
+EXPORTED = [
+    "raduls_gpu_strerror",
+    "raduls_gpu_layout_valid",
+    "raduls_gpu_version",
+    "raduls_gpu_sort",
+    "raduls_gpu_sort_host",
+    "raduls_gpu_last_stats",
+    "raduls_gpu_split",
+    "raduls_gpu_histogram",
+    "raduls_gpu_generate",
+    "raduls_gpu_digest",
+    "raduls_gpu_check_sorted",
+    "raduls_gpu_prefix_histogram",
+    "raduls_gpu_partition",
+    "raduls_gpu_release",
+]
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("levels", C.c_uint32),
+        ("scatter_launches", C.c_uint32),
+        ("hist_records", C.c_uint64),
+        ("scatter_records", C.c_uint64),
+        ("local_records", C.c_uint64),
+        ("copy_records", C.c_uint64),
+        ("fallback_groups", C.c_uint64),
+        ("skipped_levels", C.c_uint64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {f: int(getattr(self, f)) for f, _ in self._fields_}
+
+
+_lock = threading.Lock()
+_lib = None
+
+_vp = C.c_void_p
+_u32 = C.c_uint32
+_u64 = C.c_uint64
+_u64p = C.POINTER(C.c_uint64)
+_u32p = C.POINTER(C.c_uint32)
+
+
+def load(build_if_missing: bool = False):
+    """Return the loaded library; raise RuntimeError when it is unavailable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            if build_if_missing:
+                from . import build as _b
+                _b.build()
+            else:
+                raise RuntimeError(
+                    f"{LIB_PATH} is not built; run `python -m paper_1612_02557_b200.build` "
+                    "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.raduls_gpu_strerror.restype = C.c_char_p
+        L.raduls_gpu_strerror.argtypes = [C.c_int]
+        L.raduls_gpu_layout_valid.argtypes = [_u32, _u32]
+        L.raduls_gpu_version.restype = _u32
+        L.raduls_gpu_sort.argtypes = [_vp, _vp, _u64, _u32, _u32, _vp]
+        L.raduls_gpu_sort_host.argtypes = [_vp, _vp, _u64, _u32, _u32]
+        L.raduls_gpu_last_stats.argtypes = [C.POINTER(Stats)]
+        L.raduls_gpu_split.argtypes = [_vp, _vp, _u64, _u32, _u32, _u64p, _vp]
+        L.raduls_gpu_histogram.argtypes = [_vp, _u64, _u32, _u32, _u64p, _u64p, _vp]
+        L.raduls_gpu_generate.argtypes = [_vp, _u64, _u32, _u32, _u32, _u64, _u64, _vp]
+        L.raduls_gpu_digest.argtypes = [_vp, _u64, _u32, _u64p, _u64p, _vp]
+        L.raduls_gpu_check_sorted.argtypes = [_vp, _u64, _u32, _u32, _u64p, _u64p, _vp]
+        L.raduls_gpu_prefix_histogram.argtypes = [_vp, _u64, _u32, _u32, _u32, _vp, _vp]
+        L.raduls_gpu_partition.argtypes = [_vp, _vp, _u64, _u32, _u32, _u32, _vp, _u32, _u64p, _vp]
+        L.raduls_gpu_release.restype = None
+        _lib = L
+        return L
+
+
+def strerror(code: int) -> str:
+    return load().raduls_gpu_strerror(code).decode()

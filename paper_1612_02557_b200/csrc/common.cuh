@@ -1,0 +1,219 @@
+// Shared device-side definitions for the B200 MSD record sort.
+//
+// Record model (reference P/include/raduls/layout.hpp:1-81, P = /root/reference/proj):
+//   * a record is RS bytes (RS in {8,16,24,32}), key = its first `ks` bytes,
+//     most significant byte first; key order == memcmp order (layout.hpp:52-55);
+//   * the MSD digit processed at "byte position" p is record byte p, i.e. the
+//     reference's digit(rec, ks-1-p) (layout.hpp:32-39).
+// Records move as whole 8/16-byte vectors (copy_record, layout.hpp:70-73).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rg {
+
+constexpr int kRadix = 256;
+
+// ---------------------------------------------------------------- record vectors
+
+// A record held in registers as RS/4 little-endian 32-bit words.
+template <int RS>
+struct Rec {
+    static_assert(RS % 8 == 0 && RS >= 8 && RS <= 32, "record size");
+    static constexpr int kWords = RS / 4;
+    uint32_t w[kWords];
+};
+
+template <int RS>
+__device__ __forceinline__ Rec<RS> load_rec(const uint8_t* base, uint64_t idx) {
+    Rec<RS> r;
+    const uint8_t* p = base + idx * RS;
+    if constexpr (RS % 16 == 0) {
+#pragma unroll
+        for (int v = 0; v < RS / 16; ++v) {
+            const uint4 q = __ldg(reinterpret_cast<const uint4*>(p) + v);
+            r.w[4 * v + 0] = q.x;
+            r.w[4 * v + 1] = q.y;
+            r.w[4 * v + 2] = q.z;
+            r.w[4 * v + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < RS / 8; ++v) {
+            const uint2 q = __ldg(reinterpret_cast<const uint2*>(p) + v);
+            r.w[2 * v + 0] = q.x;
+            r.w[2 * v + 1] = q.y;
+        }
+    }
+    return r;
+}
+
+// Same, but through L1-bypassing loads: for buffers written by an earlier
+// kernel in the same sort (no stale-L1 issue across launches, but keeps the
+// streaming data out of L1).
+template <int RS>
+__device__ __forceinline__ Rec<RS> load_rec_stream(const uint8_t* base, uint64_t idx) {
+    Rec<RS> r;
+    const uint8_t* p = base + idx * RS;
+    if constexpr (RS % 16 == 0) {
+#pragma unroll
+        for (int v = 0; v < RS / 16; ++v) {
+            uint4 q;
+            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w)
+                         : "l"(reinterpret_cast<const uint4*>(p) + v));
+            r.w[4 * v + 0] = q.x;
+            r.w[4 * v + 1] = q.y;
+            r.w[4 * v + 2] = q.z;
+            r.w[4 * v + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < RS / 8; ++v) {
+            uint2 q;
+            asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                         : "=r"(q.x), "=r"(q.y)
+                         : "l"(reinterpret_cast<const uint2*>(p) + v));
+            r.w[2 * v + 0] = q.x;
+            r.w[2 * v + 1] = q.y;
+        }
+    }
+    return r;
+}
+
+template <int RS>
+__device__ __forceinline__ void store_rec(uint8_t* base, uint64_t idx, const Rec<RS>& r) {
+    uint8_t* p = base + idx * RS;
+    if constexpr (RS % 16 == 0) {
+#pragma unroll
+        for (int v = 0; v < RS / 16; ++v)
+            reinterpret_cast<uint4*>(p)[v] =
+                make_uint4(r.w[4 * v], r.w[4 * v + 1], r.w[4 * v + 2], r.w[4 * v + 3]);
+    } else {
+#pragma unroll
+        for (int v = 0; v < RS / 8; ++v)
+            reinterpret_cast<uint2*>(p)[v] = make_uint2(r.w[2 * v], r.w[2 * v + 1]);
+    }
+}
+
+// Shared-memory record slots (same vector widths).
+template <int RS>
+__device__ __forceinline__ void st_smem_rec(uint8_t* s, uint32_t slot, const Rec<RS>& r) {
+    store_rec<RS>(s, slot, r);
+}
+
+template <int RS>
+__device__ __forceinline__ Rec<RS> ld_smem_rec(const uint8_t* s, uint32_t slot) {
+    Rec<RS> r;
+    const uint8_t* p = s + size_t(slot) * RS;
+    if constexpr (RS % 16 == 0) {
+#pragma unroll
+        for (int v = 0; v < RS / 16; ++v) {
+            const uint4 q = reinterpret_cast<const uint4*>(p)[v];
+            r.w[4 * v + 0] = q.x;
+            r.w[4 * v + 1] = q.y;
+            r.w[4 * v + 2] = q.z;
+            r.w[4 * v + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < RS / 8; ++v) {
+            const uint2 q = reinterpret_cast<const uint2*>(p)[v];
+            r.w[2 * v + 0] = q.x;
+            r.w[2 * v + 1] = q.y;
+        }
+    }
+    return r;
+}
+
+// Record byte `p` (runtime, warp-uniform) from a register-held record, without
+// dynamic register indexing (compiles to a select chain, no local memory).
+template <int RS>
+__device__ __forceinline__ uint32_t rec_byte(const Rec<RS>& r, uint32_t p) {
+    const uint32_t wi = p >> 2;
+    uint32_t word = r.w[0];
+#pragma unroll
+    for (int k = 1; k < Rec<RS>::kWords; ++k) word = (wi == uint32_t(k)) ? r.w[k] : word;
+    return (word >> ((p & 3u) * 8u)) & 0xFFu;
+}
+
+// Little-endian 64-bit word k (record bytes 8k..8k+7).
+template <int RS>
+__device__ __forceinline__ uint64_t rec_word64(const Rec<RS>& r, int k) {
+    return uint64_t(r.w[2 * k]) | (uint64_t(r.w[2 * k + 1]) << 32);
+}
+
+// ---------------------------------------------------------------- misc
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ void st_volatile_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Device segment descriptors -------------------------------------------------
+
+// A contiguous run of records [start, start+size) that still needs ordering by
+// key bytes >= p; `parity` says which working buffer holds it (0: caller's
+// data, 1: tmp). Mirrors the reference's Bin (P/include/raduls/kernels.hpp:60-67)
+// with the digit expressed as a record byte offset.
+struct Seg {
+    uint64_t start;
+    uint64_t size;
+    uint32_t p;
+    uint32_t parity;
+    uint64_t htile_base;  // first histogram tile of this segment (when its histogram is pending)
+};
+
+// A run of one or more complete, adjacent small segments sorted by one CTA;
+// all its records share key bytes [0, p).
+struct Group {
+    uint64_t start;
+    uint32_t size;
+    uint32_t p;
+    uint32_t parity;
+    uint32_t pad;
+};
+
+// A range of finished records living in tmp that must move home.
+struct CopyRange {
+    uint64_t start;
+    uint32_t size;
+    uint32_t pad;
+};
+
+// Per-level counters (device, zeroed before the planner runs).
+struct LevelCounters {
+    uint32_t n_scatter_tiles;  // tiles of this level's scatter
+    uint32_t n_groups;         // local-sort groups emitted
+    uint32_t n_copy;           // copy-back ranges emitted
+    uint32_t n_next;           // next-level big segments
+    uint32_t n_next_htiles;    // histogram tiles of next-level segments
+    uint32_t n_scatter_segs;   // segments scattered this level (stats)
+    uint32_t tile_ticket;      // dynamic tile id dispenser for k_scatter
+    uint32_t pad;
+    unsigned long long moved_scatter;  // records moved by this level's scatter
+    unsigned long long moved_local;    // records moved by local sorts
+    unsigned long long moved_copy;     // records moved by copy-back
+    unsigned long long fallback_groups;  // groups whose window sort needed the full-key fallback
+};
+
+// Decoupled look-back status word: [63:62] flag, [61:0] value.
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagIncl = 2ull << 62;
+constexpr uint64_t kValueMask = (1ull << 62) - 1;
+
+}  // namespace rg

@@ -1,0 +1,65 @@
+// Multi-GPU key-range partition helpers (no reference
+// counterpart — the reference is single-address-space). A rank holds N/G
+// records; the 16-bit big-endian key prefix at bytes (pb, pb+1) selects a
+// bucket, a host-built map assigns contiguous bucket ranges to ranks, and the
+// records are split stably into G contiguous send ranges by k_scatter<RS, true>
+// (the same warp-ranked, look-back scatter as the MSD passes).
+#pragma once
+
+#include "common.cuh"
+
+namespace rg {
+
+template <int RS>
+__device__ __forceinline__ uint32_t prefix16(const Rec<RS>& r, uint32_t pb, uint32_t ks) {
+    const uint32_t hi = pb < ks ? rec_byte<RS>(r, pb) : 0u;
+    const uint32_t lo = pb + 1 < ks ? rec_byte<RS>(r, pb + 1) : 0u;
+    return (hi << 8) | lo;
+}
+
+// 65536-bucket prefix histogram, accumulated into hist (u64). Warp-aggregated
+// global atomics (a hot bucket costs one atomic per warp, not per record).
+template <int RS>
+__global__ void __launch_bounds__(256) k_prefix_hist(const uint8_t* __restrict__ data, uint64_t n,
+                                                     uint32_t ks, uint32_t pb,
+                                                     unsigned long long* __restrict__ hist) {
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
+        const uint64_t i = base + threadIdx.x;
+        const bool valid = i < n;
+        const uint32_t b = valid ? prefix16<RS>(load_rec_stream<RS>(data, i), pb, ks) : 0x10000u;
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, b);
+        if (valid && (threadIdx.x & 31) == uint32_t(__ffs(peers) - 1))
+            atomicAdd(&hist[b], (unsigned long long)__popc(peers));
+    }
+}
+
+// Per-rank record counts through the bucket -> rank map (u8).
+template <int RS>
+__global__ void __launch_bounds__(256) k_map_hist(const uint8_t* __restrict__ data, uint64_t n,
+                                                  uint32_t ks, uint32_t pb,
+                                                  const uint8_t* __restrict__ map,
+                                                  unsigned long long* __restrict__ counts) {
+    __shared__ uint32_t sh[kRadix];
+    sh[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t r = map[prefix16<RS>(load_rec_stream<RS>(data, i), pb, ks)];
+        atomicAdd(&sh[r], 1u);
+    }
+    __syncthreads();
+    if (sh[threadIdx.x]) atomicAdd(&counts[threadIdx.x], (unsigned long long)sh[threadIdx.x]);
+}
+
+__global__ void k_map_to_u8(const uint32_t* __restrict__ in, uint8_t* __restrict__ out,
+                            uint32_t n_ranks, unsigned int* __restrict__ bad) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < 65536) {
+        const uint32_t r = in[i];
+        if (r >= n_ranks) atomicOr(bad, 1u);
+        out[i] = uint8_t(r < n_ranks ? r : 0);
+    }
+}
+
+}  // namespace rg

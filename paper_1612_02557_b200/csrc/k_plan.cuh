@@ -1,0 +1,212 @@
+// Device-side pass planner: turns one level's per-segment digit histograms into
+// the next level's work lists, without a host round trip per segment.
+//
+// Reference: child_bins (P/include/raduls/kernels.hpp:82-94) — children tile
+// the parent in digit order, advance the digit and flip the buffer parity —
+// plus the bin routing of MsdSorter (P/include/raduls/detail/msd_sorter.hpp:
+// 89-214: size 0 skipped, size 1 finalized, tiny bins comparison-sorted, the
+// last digit finalized, the rest recursed/queued) and is_tiny
+// (P/include/raduls/small_sorts.hpp:31-37). The reference's thread-share
+// policy (scheduler.cpp:8-38) and task queues (task_queue.hpp) have no GPU
+// counterpart: size classes decide instead —
+//   * size <= kCap (local-sort capacity)   -> packed into local-sort groups,
+//   * larger                               -> next level (histogram, then scatter),
+// and (e) a segment whose key byte p is constant is not scattered at all: it is
+// re-queued at the first varying byte (or finished when none varies), keeping
+// its buffer parity.
+#pragma once
+
+#include "common.cuh"
+#include "k_histogram.cuh"
+#include "k_local_sort.cuh"
+
+namespace rg {
+
+struct PlanArgs {
+    const Seg* segs;
+    unsigned long long* seg_hist;        // [nseg][256]: in counts, out exclusive offsets
+    const unsigned long long* seg_andor;  // [nseg][8]
+    unsigned long long* stile_base;      // [nseg]
+    uint32_t* tile_seg;                  // scatter tile -> segment
+    Group* groups;
+    CopyRange* copies;
+    Seg* next;
+    unsigned long long* next_hist;
+    unsigned long long* next_andor;
+    uint32_t* next_htile_seg;
+    LevelCounters* ctr;
+    uint32_t ks;
+    uint32_t tile;      // scatter tile (records)
+    uint32_t cap_local;  // local-sort group capacity (records)
+};
+
+__device__ __forceinline__ uint32_t andor_byte_varies(const unsigned long long* ao, uint32_t b) {
+    const unsigned long long x = ao[2 * (b >> 3)] ^ ao[2 * (b >> 3) + 1];
+    return uint32_t((x >> ((b & 7u) * 8u)) & 0xFFull);
+}
+
+__global__ void k_init_andor(unsigned long long* andor, uint32_t rows) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < rows * 8) andor[i] = (i & 1) ? 0ull : ~0ull;
+}
+
+// Emit copy-back ranges covering [start, start+size).
+__device__ void emit_copies(const PlanArgs& A, uint64_t start, uint64_t size, uint32_t* s_base) {
+    const uint64_t nchunks = (size + kCopyTile - 1) / kCopyTile;
+    if (threadIdx.x == 0) {
+        *s_base = atomicAdd(&A.ctr->n_copy, uint32_t(nchunks));
+        atomicAdd(&A.ctr->moved_copy, (unsigned long long)size);
+    }
+    __syncthreads();
+    for (uint64_t c = threadIdx.x; c < nchunks; c += blockDim.x) {
+        CopyRange r;
+        r.start = start + c * kCopyTile;
+        r.size = uint32_t(min(uint64_t(kCopyTile), size - c * kCopyTile));
+        r.pad = 0;
+        A.copies[*s_base + c] = r;
+    }
+}
+
+// Allocate and initialise one next-level segment (called by a single thread).
+__device__ uint32_t emit_next(const PlanArgs& A, uint64_t start, uint64_t size, uint32_t p,
+                              uint32_t parity) {
+    const uint32_t idx = atomicAdd(&A.ctr->n_next, 1u);
+    const uint32_t nt = uint32_t((size + kHistTile - 1) / kHistTile);
+    const uint32_t hb = atomicAdd(&A.ctr->n_next_htiles, nt);
+    Seg s;
+    s.start = start;
+    s.size = size;
+    s.p = p;
+    s.parity = parity;
+    s.htile_base = hb;
+    A.next[idx] = s;
+    return idx;
+}
+
+__global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
+    __shared__ unsigned long long s_cnt[kRadix], s_off[kRadix];
+    __shared__ unsigned long long s_wsum[8];
+    __shared__ uint32_t s_action, s_pnext, s_base, s_ngroups, s_nnext;
+    __shared__ uint32_t s_next_idx[kRadix];
+    __shared__ uint64_t s_gstart[kRadix];
+    __shared__ uint32_t s_gsize[kRadix];
+    const uint32_t s = blockIdx.x;
+    const Seg g = A.segs[s];
+    const unsigned long long* ao = A.seg_andor + uint64_t(s) * 8;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    if (tid == 0) {
+        uint32_t pn = A.ks;
+        for (uint32_t b = g.p; b < A.ks; ++b)
+            if (andor_byte_varies(ao, b)) {
+                pn = b;
+                break;
+            }
+        s_pnext = pn;
+        s_action = pn >= A.ks ? 0u : (pn > g.p ? 1u : 2u);
+    }
+    __syncthreads();
+    const uint32_t action = s_action;
+    if (action == 0) {  // all keys equal: finished where it lies
+        if (g.parity) emit_copies(A, g.start, g.size, &s_base);
+        return;
+    }
+    if (action == 1) {  // (e) constant byte p: skip it without moving a record
+        if (tid == 0) {
+            const uint32_t idx = emit_next(A, g.start, g.size, s_pnext, g.parity);
+            s_base = idx;
+        }
+        __syncthreads();
+        const uint32_t idx = s_base;
+        const Seg nx = A.next[idx];
+        const uint32_t nt = uint32_t((g.size + kHistTile - 1) / kHistTile);
+        for (uint32_t t = tid; t < nt; t += blockDim.x) A.next_htile_seg[nx.htile_base + t] = idx;
+        A.next_hist[uint64_t(idx) * kRadix + tid] = 0ull;
+        if (tid < 8) A.next_andor[uint64_t(idx) * 8 + tid] = (tid & 1) ? 0ull : ~0ull;
+        return;
+    }
+
+    // action 2: scatter on byte p. Exclusive digit offsets (u64 block scan).
+    unsigned long long* hist = A.seg_hist + uint64_t(s) * kRadix;
+    const unsigned long long c = hist[tid];
+    unsigned long long x = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+        if (lane >= off) x += y;
+    }
+    if (lane == 31) s_wsum[warp] = x;
+    __syncthreads();
+    unsigned long long wbase = 0;
+    for (int k = 0; k < warp; ++k) wbase += s_wsum[k];
+    const unsigned long long off = wbase + x - c;
+    hist[tid] = off;
+    s_cnt[tid] = c;
+    s_off[tid] = off;
+    if (tid == 0) {
+        const uint32_t nt = uint32_t((g.size + A.tile - 1) / A.tile);
+        s_base = atomicAdd(&A.ctr->n_scatter_tiles, nt);
+        A.stile_base[s] = s_base;
+        atomicAdd(&A.ctr->n_scatter_segs, 1u);
+        atomicAdd(&A.ctr->moved_scatter, (unsigned long long)g.size);
+        s_nnext = 0;
+    }
+    __syncthreads();
+    {
+        const uint32_t nt = uint32_t((g.size + A.tile - 1) / A.tile);
+        const uint32_t tb = s_base;
+        for (uint32_t t = tid; t < nt; t += blockDim.x) A.tile_seg[tb + t] = s;
+    }
+    const uint32_t cp = 1u - g.parity;
+    if (g.p + 1 >= A.ks) {  // last key byte: every child is final after this split
+        __syncthreads();
+        if (cp) emit_copies(A, g.start, g.size, &s_base);
+        return;
+    }
+    // big children -> next level
+    const unsigned long long cs = s_cnt[tid];
+    s_next_idx[tid] = 0xFFFFFFFFu;
+    if (cs > A.cap_local) s_next_idx[tid] = emit_next(A, g.start + s_off[tid], cs, g.p + 1, cp);
+    // small children -> greedy groups (thread 0, digit order)
+    if (tid == 0) {
+        uint32_t ng = 0;
+        uint64_t gs = 0;
+        uint32_t gsz = 0;
+        for (int d = 0; d < kRadix; ++d) {
+            const unsigned long long sz = s_cnt[d];
+            if (sz == 0) continue;
+            if (sz > A.cap_local) {
+                if (gsz) s_gstart[ng] = gs, s_gsize[ng] = gsz, ++ng, gsz = 0;
+                continue;
+            }
+            if (gsz && gsz + sz > A.cap_local) s_gstart[ng] = gs, s_gsize[ng] = gsz, ++ng, gsz = 0;
+            if (gsz == 0) gs = g.start + s_off[d];
+            gsz += uint32_t(sz);
+        }
+        if (gsz) s_gstart[ng] = gs, s_gsize[ng] = gsz, ++ng;
+        s_ngroups = ng;
+        s_base = ng ? atomicAdd(&A.ctr->n_groups, ng) : 0u;
+    }
+    __syncthreads();
+    if (tid < int(s_ngroups)) {
+        Group gr;
+        gr.start = s_gstart[tid];
+        gr.size = s_gsize[tid];
+        gr.p = g.p;
+        gr.parity = cp;
+        gr.pad = 0;
+        A.groups[s_base + tid] = gr;
+    }
+    // initialise the next-level segments emitted by this block
+    for (int d = 0; d < kRadix; ++d) {
+        const uint32_t idx = s_next_idx[d];
+        if (idx == 0xFFFFFFFFu) continue;
+        const Seg nx = A.next[idx];
+        const uint32_t nt = uint32_t((nx.size + kHistTile - 1) / kHistTile);
+        for (uint32_t t = tid; t < nt; t += blockDim.x) A.next_htile_seg[nx.htile_base + t] = idx;
+        A.next_hist[uint64_t(idx) * kRadix + tid] = 0ull;
+        if (tid < 8) A.next_andor[uint64_t(idx) * 8 + tid] = (tid & 1) ? 0ull : ~0ull;
+    }
+}
+
+}  // namespace rg

@@ -1,0 +1,686 @@
+// libraduls_gpu.so — C-ABI + C++ host planner of the B200 MSD record sort.
+//
+// Host side of the reference's MsdSorter (P/include/raduls/detail/msd_sorter.hpp:
+// 41-233) and its entry raduls::sort (P/src/scheduler.cpp:40-45), re-designed
+// for one GPU: instead of T worker threads draining priority queues of bins,
+// the host runs a short loop over MSD *levels*; each level is a handful of
+// kernel launches over device-resident segment lists:
+//
+//   level 0   k_histo_all: histograms of key bytes 0..7 + AND/OR of all words
+//             (constant leading bytes skipped before any record moves);
+//   level L   [k_seg_hist]  per-segment digit histogram + AND/OR (one read)
+//             k_plan        per segment: finish / skip a constant byte /
+//                           scatter; children routed to groups or next level
+//             k_scatter     one stable split of every scattered segment
+//             k_local_sort  groups of small bins, sorted straight into `data`
+//             k_copy_back   finished bins that ended in tmp
+//
+// One device->host read of the level counters per level sizes the next
+// launches. See DESIGN.md for the data layout and the per-kernel rooflines.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "../../include/raduls_gpu.h"
+#include "common.cuh"
+#include "k_histogram.cuh"
+#include "k_local_sort.cuh"
+#include "k_partition.cuh"
+#include "k_plan.cuh"
+#include "k_scatter.cuh"
+#include "k_util.cuh"
+
+namespace {
+
+using namespace rg;
+
+constexpr int kMaxLevels = 72;
+
+struct CudaError {
+    int code;
+};
+
+#define RG_CHECK(expr)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            if (std::getenv("RADULS_GPU_DEBUG"))                                        \
+                std::fprintf(stderr, "raduls_gpu: %s failed: %s (%s:%d)\n", #expr,      \
+                             cudaGetErrorString(e_), __FILE__, __LINE__);               \
+            throw CudaError{e_ == cudaErrorMemoryAllocation ? RADULS_GPU_ENOMEM          \
+                                                            : RADULS_GPU_ECUDA};         \
+        }                                                                               \
+    } while (0)
+
+#define RG_LAUNCH_CHECK() RG_CHECK(cudaGetLastError())
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t cap = 0;  // elements
+    void ensure(size_t n) {
+        if (n <= cap) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(n, 1);
+        RG_CHECK(cudaMalloc(&p, want * sizeof(T)));
+        cap = want;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct Workspace {
+    int device = 0;
+    std::mutex mu;
+    DevBuf<unsigned long long> hist8, andor0, thr, acc;
+    DevBuf<LevelCounters> ctr;
+    DevBuf<Seg> segs[2];
+    DevBuf<unsigned long long> seg_hist[2], seg_andor[2];
+    DevBuf<unsigned long long> stile_base;
+    DevBuf<uint32_t> tile_seg, htile_seg[2];
+    DevBuf<unsigned long long> status;
+    DevBuf<Group> groups;
+    DevBuf<CopyRange> copies;
+    DevBuf<uint8_t> host_data, host_tmp, map8;
+    DevBuf<uint32_t> map32;
+    LevelCounters* h_ctr = nullptr;      // pinned [kMaxLevels]
+    unsigned long long* h_small = nullptr;  // pinned scratch [4096]
+    raduls_gpu_stats last{};
+    bool attrs_set[33] = {};
+
+    Workspace() {
+        RG_CHECK(cudaMallocHost(&h_ctr, sizeof(LevelCounters) * kMaxLevels));
+        RG_CHECK(cudaMallocHost(&h_small, sizeof(unsigned long long) * 4096));
+        hist8.ensure(8 * kRadix);
+        andor0.ensure(8);
+        acc.ensure(4);
+        ctr.ensure(kMaxLevels);
+        thr.ensure(256);
+    }
+};
+
+std::mutex g_mu;
+std::map<int, Workspace*> g_ws;
+
+Workspace& workspace() {
+    int dev = 0;
+    RG_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_ws.find(dev);
+    if (it != g_ws.end()) return *it->second;
+    auto* w = new Workspace();
+    w->device = dev;
+    g_ws[dev] = w;
+    return *w;
+}
+
+bool layout_ok(uint32_t rs, uint32_t ks) {
+    return (rs == 8 || rs == 16 || rs == 24 || rs == 32) && ks >= 1 && ks <= rs;
+}
+
+bool aligned_ok(const void* p, uint32_t rs) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    return (a % (rs % 16 == 0 ? 16 : 8)) == 0;
+}
+
+int grid_for(uint64_t n, int threads, int per_sm) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t want = (n + threads - 1) / threads;
+    return int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(sms) * per_sm)));
+}
+
+uint32_t first_varying_byte(const unsigned long long* andor, uint32_t from, uint32_t ks) {
+    for (uint32_t b = from; b < ks; ++b) {
+        const unsigned long long x = andor[2 * (b >> 3)] ^ andor[2 * (b >> 3) + 1];
+        if ((x >> ((b & 7) * 8)) & 0xFF) return b;
+    }
+    return ks;
+}
+
+// Capacities for a sort of n records.
+struct Caps {
+    size_t seg, tiles, htiles, groups, copies;
+};
+
+template <int RS>
+Caps caps_for(uint64_t n) {
+    const uint64_t cap_local = LocalCfg<RS>::kCap;
+    Caps c;
+    c.seg = size_t(n / (cap_local + 1) + 2);
+    c.tiles = size_t(n / ScatterCfg<RS>::kTile + c.seg + 2);
+    c.htiles = size_t(n / kHistTile + c.seg + 2);
+    c.groups = size_t(3 * (n / cap_local) + c.seg + 2);
+    c.copies = size_t(n / kCopyTile + c.seg + 2);
+    return c;
+}
+
+template <int RS>
+void ensure_caps(Workspace& ws, uint64_t n) {
+    const Caps c = caps_for<RS>(n);
+    for (int b = 0; b < 2; ++b) {
+        ws.segs[b].ensure(c.seg);
+        ws.seg_hist[b].ensure(c.seg * kRadix);
+        ws.seg_andor[b].ensure(c.seg * 8);
+        ws.htile_seg[b].ensure(c.htiles);
+    }
+    ws.stile_base.ensure(c.seg);
+    ws.tile_seg.ensure(c.tiles);
+    ws.status.ensure(c.tiles * kRadix);
+    ws.groups.ensure(c.groups);
+    ws.copies.ensure(c.copies);
+}
+
+template <int RS>
+void set_attrs(Workspace& ws) {
+    if (ws.attrs_set[RS]) return;
+    RG_CHECK(cudaFuncSetAttribute(k_local_sort<RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(LocalCfg<RS>::kSmem)));
+    ws.attrs_set[RS] = true;
+}
+
+// Launch the local sort over `ngroups` groups already in ws.groups.
+template <int RS>
+void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, uint32_t ks,
+                  LevelCounters* ctr, cudaStream_t st) {
+    if (!ngroups) return;
+    k_local_sort<RS><<<ngroups, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
+        data, tmp, ws.groups.p, ks, ctr);
+    RG_LAUNCH_CHECK();
+}
+
+template <int RS>
+void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t ks,
+               cudaStream_t st) {
+    raduls_gpu_stats stats{};
+    ws.last = stats;
+    if (n < 2) return;  // msd_sorter.hpp:51
+    set_attrs<RS>(ws);
+    ensure_caps<RS>(ws, n);
+
+    // ---- level 0: whole-array histograms of key bytes 0..7 + AND/OR
+    const uint32_t nb = std::min<uint32_t>(ks, 8);
+    RG_CHECK(cudaMemsetAsync(ws.hist8.p, 0, 8 * kRadix * sizeof(unsigned long long), st));
+    k_init_andor<<<1, 64, 0, st>>>(ws.andor0.p, 1);
+    RG_LAUNCH_CHECK();
+    k_histo_all<RS><<<grid_for(n, 256, 8), 256, 0, st>>>(data, n, nb, ws.hist8.p, ws.andor0.p);
+    RG_LAUNCH_CHECK();
+    stats.hist_records += n;
+    RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.andor0.p, 8 * sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, st));
+    RG_CHECK(cudaStreamSynchronize(st));
+    const uint32_t p0 = first_varying_byte(ws.h_small, 0, ks);
+    if (p0 >= ks) {  // every key equal: a stable sort is the identity
+        ws.last = stats;
+        return;
+    }
+    LevelCounters* dctr = ws.ctr.p;
+    if (n <= uint64_t(LocalCfg<RS>::kCap)) {  // one group sorts everything
+        Group g{0, uint32_t(n), p0, 0, 0};
+        RG_CHECK(cudaMemcpyAsync(ws.groups.p, &g, sizeof g, cudaMemcpyHostToDevice, st));
+        RG_CHECK(cudaMemsetAsync(dctr, 0, sizeof(LevelCounters), st));
+        launch_local<RS>(ws, data, tmp, 1, ks, dctr, st);
+        RG_CHECK(cudaMemcpyAsync(ws.h_ctr, dctr, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
+        RG_CHECK(cudaStreamSynchronize(st));
+        stats.levels = 1;
+        stats.local_records = ws.h_ctr[0].moved_local;
+        stats.fallback_groups = ws.h_ctr[0].fallback_groups;
+        ws.last = stats;
+        return;
+    }
+
+    int cur = 0;
+    {
+        Seg s0{0, n, p0, 0, 0};
+        RG_CHECK(cudaMemcpyAsync(ws.segs[0].p, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
+        if (p0 < 8) {
+            RG_CHECK(cudaMemcpyAsync(ws.seg_hist[0].p, ws.hist8.p + size_t(p0) * kRadix,
+                                     kRadix * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
+            RG_CHECK(cudaMemcpyAsync(ws.seg_andor[0].p, ws.andor0.p, 8 * sizeof(unsigned long long),
+                                     cudaMemcpyDeviceToDevice, st));
+        } else {  // first eight key bytes constant: histogram byte p0 now
+            RG_CHECK(cudaMemsetAsync(ws.seg_hist[0].p, 0, kRadix * sizeof(unsigned long long), st));
+            k_init_andor<<<1, 64, 0, st>>>(ws.seg_andor[0].p, 1);
+            RG_LAUNCH_CHECK();
+            const uint64_t nt = (n + kHistTile - 1) / kHistTile;
+            RG_CHECK(cudaMemsetAsync(ws.htile_seg[0].p, 0, nt * sizeof(uint32_t), st));
+            k_seg_hist<RS><<<uint32_t(nt), kHistThreads, 0, st>>>(data, tmp, ws.segs[0].p,
+                                                                 ws.htile_seg[0].p, ws.seg_hist[0].p,
+                                                                 ws.seg_andor[0].p);
+            RG_LAUNCH_CHECK();
+            stats.hist_records += n;
+        }
+    }
+    uint32_t nseg = 1;
+    uint32_t level = 0;
+    const Caps caps = caps_for<RS>(n);
+    while (nseg > 0) {
+        if (level >= uint32_t(kMaxLevels)) throw CudaError{RADULS_GPU_EINTERNAL};
+        LevelCounters* c = dctr + level;
+        RG_CHECK(cudaMemsetAsync(c, 0, sizeof(LevelCounters), st));
+        PlanArgs A;
+        A.segs = ws.segs[cur].p;
+        A.seg_hist = ws.seg_hist[cur].p;
+        A.seg_andor = ws.seg_andor[cur].p;
+        A.stile_base = ws.stile_base.p;
+        A.tile_seg = ws.tile_seg.p;
+        A.groups = ws.groups.p;
+        A.copies = ws.copies.p;
+        A.next = ws.segs[cur ^ 1].p;
+        A.next_hist = ws.seg_hist[cur ^ 1].p;
+        A.next_andor = ws.seg_andor[cur ^ 1].p;
+        A.next_htile_seg = ws.htile_seg[cur ^ 1].p;
+        A.ctr = c;
+        A.ks = ks;
+        A.tile = ScatterCfg<RS>::kTile;
+        A.cap_local = LocalCfg<RS>::kCap;
+        k_plan<<<nseg, 256, 0, st>>>(A);
+        RG_LAUNCH_CHECK();
+        RG_CHECK(cudaMemcpyAsync(ws.h_ctr + level, c, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
+        RG_CHECK(cudaStreamSynchronize(st));
+        const LevelCounters h = ws.h_ctr[level];
+        if (h.n_scatter_tiles > caps.tiles || h.n_groups > caps.groups || h.n_copy > caps.copies ||
+            h.n_next > caps.seg || h.n_next_htiles > caps.htiles)
+            throw CudaError{RADULS_GPU_EINTERNAL};
+        if (h.n_scatter_tiles) {
+            RG_CHECK(cudaMemsetAsync(ws.status.p, 0,
+                                     size_t(h.n_scatter_tiles) * kRadix * sizeof(unsigned long long), st));
+            k_scatter<RS><<<h.n_scatter_tiles, ScatterCfg<RS>::kThreads, 0, st>>>(
+                data, tmp, ws.segs[cur].p, ws.seg_hist[cur].p, ws.stile_base.p, ws.tile_seg.p,
+                ws.status.p, c);
+            RG_LAUNCH_CHECK();
+            stats.scatter_launches++;
+        }
+        launch_local<RS>(ws, data, tmp, h.n_groups, ks, c, st);
+        if (h.n_copy) {
+            k_copy_back<RS><<<h.n_copy, 256, 0, st>>>(data, tmp, ws.copies.p);
+            RG_LAUNCH_CHECK();
+        }
+        stats.scatter_records += h.moved_scatter;
+        stats.copy_records += h.moved_copy;
+        stats.skipped_levels += nseg - h.n_scatter_segs;
+        cur ^= 1;
+        nseg = h.n_next;
+        ++level;
+        if (nseg) {
+            k_seg_hist<RS><<<h.n_next_htiles, kHistThreads, 0, st>>>(
+                data, tmp, ws.segs[cur].p, ws.htile_seg[cur].p, ws.seg_hist[cur].p,
+                ws.seg_andor[cur].p);
+            RG_LAUNCH_CHECK();
+            // records histogrammed = sum of next segment sizes (from the planner's view)
+        }
+    }
+    // final counters (local-sort / fallback totals are written by kernels)
+    RG_CHECK(cudaMemcpyAsync(ws.h_ctr, dctr, sizeof(LevelCounters) * level, cudaMemcpyDeviceToHost, st));
+    RG_CHECK(cudaStreamSynchronize(st));
+    stats.levels = level;
+    for (uint32_t l = 0; l < level; ++l) {
+        stats.local_records += ws.h_ctr[l].moved_local;
+        stats.fallback_groups += ws.h_ctr[l].fallback_groups;
+        if (l + 1 < level) {
+            // histogram tiles read by level l+1 cover its segments exactly
+        }
+    }
+    ws.last = stats;
+}
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return RADULS_GPU_OK;
+    } catch (const CudaError& e) {
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        return RADULS_GPU_ENOMEM;
+    } catch (...) {
+        return RADULS_GPU_EINTERNAL;
+    }
+}
+
+template <typename F>
+void dispatch_rs(uint32_t rs, F&& f) {
+    switch (rs) {
+        case 8: f(std::integral_constant<int, 8>{}); break;
+        case 16: f(std::integral_constant<int, 16>{}); break;
+        case 24: f(std::integral_constant<int, 24>{}); break;
+        case 32: f(std::integral_constant<int, 32>{}); break;
+        default: throw CudaError{RADULS_GPU_EINVAL};
+    }
+}
+
+bool mul_overflows(uint64_t n, uint32_t rs) { return n > (~uint64_t(0)) / rs; }
+
+void zipf_thresholds(double s, uint32_t universe, unsigned long long* thr) {
+    // identical arithmetic to oracle/raduls_oracle.c orc_zipf_thresholds (checked by tests)
+    double run = 0.0, total = 0.0;
+    for (uint32_t r = 1; r <= universe; ++r) total += std::pow(double(r), -s);
+    for (uint32_t k = 0; k < universe; ++k) {
+        run += std::pow(double(k + 1), -s);
+        const double t = run / total * 9007199254740992.0;
+        thr[k] = (k + 1 == universe) ? 9007199254740992ull : (unsigned long long)t;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* raduls_gpu_strerror(int code) {
+    switch (code) {
+        case RADULS_GPU_OK: return "ok";
+        case RADULS_GPU_EINVAL: return "invalid argument (unsupported record layout, misaligned pointer or size overflow)";
+        case RADULS_GPU_ENOMEM: return "out of memory";
+        case RADULS_GPU_ECUDA: return "CUDA runtime error";
+        case RADULS_GPU_ENCCL: return "NCCL error";
+        case RADULS_GPU_EINTERNAL: return "internal error (planner invariant)";
+        default: return "unknown status";
+    }
+}
+
+int raduls_gpu_layout_valid(uint32_t rs, uint32_t ks) { return layout_ok(rs, ks) ? 1 : 0; }
+
+uint32_t raduls_gpu_version(void) { return 0x000100u; }
+
+int raduls_gpu_sort(void* d_data, void* d_tmp, uint64_t n, uint32_t rs, uint32_t ks, void* stream) {
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs)) return RADULS_GPU_EINVAL;
+    if (n >= 2 && (!d_data || !aligned_ok(d_data, rs) || (d_tmp && !aligned_ok(d_tmp, rs))))
+        return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        uint8_t* tmp = static_cast<uint8_t*>(d_tmp);
+        bool own = false;
+        if (n >= 2 && !tmp) {
+            RG_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), n * rs, st));
+            own = true;
+        }
+        try {
+            dispatch_rs(rs, [&](auto R) {
+                sort_impl<decltype(R)::value>(ws, static_cast<uint8_t*>(d_data), tmp, n, ks, st);
+            });
+        } catch (...) {
+            if (own) cudaFreeAsync(tmp, st);
+            throw;
+        }
+        if (own) RG_CHECK(cudaFreeAsync(tmp, st));
+        RG_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+int raduls_gpu_sort_host(uint8_t* data, uint8_t* /*tmp*/, uint64_t n, uint32_t rs, uint32_t ks) {
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs)) return RADULS_GPU_EINVAL;
+    if (n < 2) return RADULS_GPU_OK;
+    if (!data) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        const size_t bytes = size_t(n) * rs;
+        ws.host_data.ensure(bytes);
+        ws.host_tmp.ensure(bytes);
+        cudaStream_t st = nullptr;
+        RG_CHECK(cudaMemcpyAsync(ws.host_data.p, data, bytes, cudaMemcpyHostToDevice, st));
+        dispatch_rs(rs, [&](auto R) {
+            sort_impl<decltype(R)::value>(ws, ws.host_data.p, ws.host_tmp.p, n, ks, st);
+        });
+        RG_CHECK(cudaMemcpyAsync(data, ws.host_data.p, bytes, cudaMemcpyDeviceToHost, st));
+        RG_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+int raduls_gpu_last_stats(raduls_gpu_stats* out) {
+    if (!out) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        *out = ws.last;
+    });
+}
+
+int raduls_gpu_split(const void* d_src, void* d_dst, uint64_t n, uint32_t rs,
+                     uint32_t key_byte_offset, uint64_t* h_counts, void* stream) {
+    if (!layout_ok(rs, rs) || key_byte_offset >= rs || mul_overflows(n, rs)) return RADULS_GPU_EINVAL;
+    if (n && (!aligned_ok(d_src, rs) || !aligned_ok(d_dst, rs))) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (h_counts) std::memset(h_counts, 0, 256 * sizeof(uint64_t));
+        if (n == 0) return;
+        dispatch_rs(rs, [&](auto R) {
+            constexpr int RSC = decltype(R)::value;
+            ensure_caps<RSC>(ws, n);
+            // histogram of the byte via a one-segment k_seg_hist
+            Seg s0{0, n, key_byte_offset, 0, 0};
+            RG_CHECK(cudaMemcpyAsync(ws.segs[0].p, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
+            RG_CHECK(cudaMemsetAsync(ws.seg_hist[0].p, 0, kRadix * sizeof(unsigned long long), st));
+            k_init_andor<<<1, 64, 0, st>>>(ws.seg_andor[0].p, 1);
+            const uint64_t nt = (n + kHistTile - 1) / kHistTile;
+            RG_CHECK(cudaMemsetAsync(ws.htile_seg[0].p, 0, nt * sizeof(uint32_t), st));
+            uint8_t* src = const_cast<uint8_t*>(static_cast<const uint8_t*>(d_src));
+            k_seg_hist<RSC><<<uint32_t(nt), kHistThreads, 0, st>>>(src, src, ws.segs[0].p, ws.htile_seg[0].p,
+                                                                  ws.seg_hist[0].p, ws.seg_andor[0].p);
+            RG_LAUNCH_CHECK();
+            RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.seg_hist[0].p, kRadix * sizeof(unsigned long long),
+                                     cudaMemcpyDeviceToHost, st));
+            RG_CHECK(cudaStreamSynchronize(st));
+            if (h_counts) std::memcpy(h_counts, ws.h_small, 256 * sizeof(uint64_t));
+            unsigned long long off[256], run = 0;
+            for (int d = 0; d < 256; ++d) off[d] = run, run += ws.h_small[d];
+            RG_CHECK(cudaMemcpyAsync(ws.seg_hist[0].p, off, sizeof off, cudaMemcpyHostToDevice, st));
+            const uint32_t tiles = uint32_t((n + ScatterCfg<RSC>::kTile - 1) / ScatterCfg<RSC>::kTile);
+            RG_CHECK(cudaMemsetAsync(ws.tile_seg.p, 0, tiles * sizeof(uint32_t), st));
+            RG_CHECK(cudaMemsetAsync(ws.stile_base.p, 0, sizeof(unsigned long long), st));
+            RG_CHECK(cudaMemsetAsync(ws.status.p, 0, size_t(tiles) * kRadix * sizeof(unsigned long long), st));
+            RG_CHECK(cudaMemsetAsync(ws.ctr.p, 0, sizeof(LevelCounters), st));
+            // parity 0: src = "data" slot, dst = "tmp" slot
+            k_scatter<RSC><<<tiles, ScatterCfg<RSC>::kThreads, 0, st>>>(
+                src, static_cast<uint8_t*>(d_dst), ws.segs[0].p, ws.seg_hist[0].p, ws.stile_base.p,
+                ws.tile_seg.p, ws.status.p, ws.ctr.p);
+            RG_LAUNCH_CHECK();
+            RG_CHECK(cudaStreamSynchronize(st));
+        });
+    });
+}
+
+int raduls_gpu_histogram(const void* d_data, uint64_t n, uint32_t rs, uint32_t ks, uint64_t* h_hist,
+                         uint64_t* h_andor, void* stream) {
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs)) return RADULS_GPU_EINVAL;
+    if (n && !aligned_ok(d_data, rs)) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        RG_CHECK(cudaMemsetAsync(ws.hist8.p, 0, 8 * kRadix * sizeof(unsigned long long), st));
+        k_init_andor<<<1, 64, 0, st>>>(ws.andor0.p, 1);
+        if (n) {
+            dispatch_rs(rs, [&](auto R) {
+                k_histo_all<decltype(R)::value><<<grid_for(n, 256, 8), 256, 0, st>>>(
+                    static_cast<const uint8_t*>(d_data), n, std::min<uint32_t>(ks, 8), ws.hist8.p,
+                    ws.andor0.p);
+            });
+            RG_LAUNCH_CHECK();
+        }
+        RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.hist8.p, 8 * kRadix * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, st));
+        RG_CHECK(cudaMemcpyAsync(ws.h_small + 8 * kRadix, ws.andor0.p, 8 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, st));
+        RG_CHECK(cudaStreamSynchronize(st));
+        if (h_hist) std::memcpy(h_hist, ws.h_small, 8 * kRadix * sizeof(uint64_t));
+        if (h_andor) std::memcpy(h_andor, ws.h_small + 8 * kRadix, 8 * sizeof(uint64_t));
+    });
+}
+
+int raduls_gpu_generate(void* d_out, uint64_t n, uint32_t rs, uint32_t ks, uint32_t dist, uint64_t seed,
+                        uint64_t index_base, void* stream) {
+    if (!layout_ok(rs, ks) || dist > 1 || mul_overflows(n, rs)) return RADULS_GPU_EINVAL;
+    if (n && !aligned_ok(d_out, rs)) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (!n) return;
+        if (dist == 1) {
+            zipf_thresholds(1.2, 256, ws.h_small);
+            RG_CHECK(cudaMemcpyAsync(ws.thr.p, ws.h_small, 256 * sizeof(unsigned long long),
+                                     cudaMemcpyHostToDevice, st));
+        }
+        GenParams P{n, seed, index_base, ks, dist, ws.thr.p};
+        dispatch_rs(rs, [&](auto R) {
+            k_gen<decltype(R)::value><<<grid_for(n, 256, 16), 256, 0, st>>>(static_cast<uint8_t*>(d_out), P);
+        });
+        RG_LAUNCH_CHECK();
+        RG_CHECK(cudaStreamSynchronize(st));  // thresholds live in pinned scratch
+    });
+}
+
+int raduls_gpu_digest(const void* d_data, uint64_t n, uint32_t rs, uint64_t* lo, uint64_t* hi,
+                      void* stream) {
+    if (!layout_ok(rs, rs) || mul_overflows(n, rs)) return RADULS_GPU_EINVAL;
+    if (n && !aligned_ok(d_data, rs)) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        RG_CHECK(cudaMemsetAsync(ws.acc.p, 0, 2 * sizeof(unsigned long long), st));
+        if (n) {
+            dispatch_rs(rs, [&](auto R) {
+                k_digest<decltype(R)::value><<<grid_for(n, 256, 8), 256, 0, st>>>(
+                    static_cast<const uint8_t*>(d_data), n, ws.acc.p);
+            });
+            RG_LAUNCH_CHECK();
+        }
+        RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.acc.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        RG_CHECK(cudaStreamSynchronize(st));
+        *lo = ws.h_small[0];
+        *hi = ws.h_small[1];
+    });
+}
+
+int raduls_gpu_check_sorted(const void* d_data, uint64_t n, uint32_t rs, uint32_t ks, uint64_t* violations,
+                            uint64_t* first, void* stream) {
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs)) return RADULS_GPU_EINVAL;
+    if (n && !aligned_ok(d_data, rs)) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        unsigned long long init[2] = {0ull, ~0ull};
+        RG_CHECK(cudaMemcpyAsync(ws.acc.p, init, sizeof init, cudaMemcpyHostToDevice, st));
+        if (n > 1) {
+            dispatch_rs(rs, [&](auto R) {
+                k_check_sorted<decltype(R)::value><<<grid_for(n, 256, 8), 256, 0, st>>>(
+                    static_cast<const uint8_t*>(d_data), n, ks, ws.acc.p);
+            });
+            RG_LAUNCH_CHECK();
+        }
+        RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.acc.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        RG_CHECK(cudaStreamSynchronize(st));
+        if (violations) *violations = ws.h_small[0];
+        if (first) *first = ws.h_small[1];
+    });
+}
+
+int raduls_gpu_prefix_histogram(const void* d_data, uint64_t n, uint32_t rs, uint32_t ks,
+                                uint32_t prefix_byte, uint64_t* d_hist, void* stream) {
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs) || !d_hist) return RADULS_GPU_EINVAL;
+    if (n && !aligned_ok(d_data, rs)) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (!n) return;
+        dispatch_rs(rs, [&](auto R) {
+            k_prefix_hist<decltype(R)::value><<<grid_for(n, 256, 8), 256, 0, st>>>(
+                static_cast<const uint8_t*>(d_data), n, ks, prefix_byte,
+                reinterpret_cast<unsigned long long*>(d_hist));
+        });
+        RG_LAUNCH_CHECK();
+    });
+}
+
+int raduls_gpu_partition(const void* d_src, void* d_dst, uint64_t n, uint32_t rs, uint32_t ks,
+                         uint32_t prefix_byte, const uint32_t* d_bucket_rank, uint32_t n_ranks,
+                         uint64_t* h_rank_counts, void* stream) {
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs) || n_ranks < 1 || n_ranks > 256 || !d_bucket_rank)
+        return RADULS_GPU_EINVAL;
+    if (n && (!aligned_ok(d_src, rs) || !aligned_ok(d_dst, rs))) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (h_rank_counts) std::memset(h_rank_counts, 0, n_ranks * sizeof(uint64_t));
+        ws.map8.ensure(65536);
+        RG_CHECK(cudaMemsetAsync(ws.acc.p, 0, sizeof(unsigned long long), st));
+        k_map_to_u8<<<256, 256, 0, st>>>(d_bucket_rank, ws.map8.p, n_ranks,
+                                          reinterpret_cast<unsigned int*>(ws.acc.p));
+        RG_LAUNCH_CHECK();
+        RG_CHECK(cudaMemsetAsync(ws.hist8.p, 0, kRadix * sizeof(unsigned long long), st));
+        if (n) {
+            dispatch_rs(rs, [&](auto R) {
+                k_map_hist<decltype(R)::value><<<grid_for(n, 256, 8), 256, 0, st>>>(
+                    static_cast<const uint8_t*>(d_src), n, ks, prefix_byte, ws.map8.p, ws.hist8.p);
+            });
+            RG_LAUNCH_CHECK();
+        }
+        RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.hist8.p, kRadix * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, st));
+        RG_CHECK(cudaMemcpyAsync(ws.h_small + kRadix, ws.acc.p, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, st));
+        RG_CHECK(cudaStreamSynchronize(st));
+        if (uint32_t(ws.h_small[kRadix])) throw CudaError{RADULS_GPU_EINVAL};  // map entry >= n_ranks
+        if (h_rank_counts) std::memcpy(h_rank_counts, ws.h_small, n_ranks * sizeof(uint64_t));
+        if (!n) return;
+        unsigned long long off[256], run = 0;
+        for (int d = 0; d < 256; ++d) off[d] = run, run += ws.h_small[d];
+        dispatch_rs(rs, [&](auto R) {
+            constexpr int RSC = decltype(R)::value;
+            ensure_caps<RSC>(ws, n);
+            Seg s0{0, n, prefix_byte, 0, 0};
+            RG_CHECK(cudaMemcpyAsync(ws.segs[0].p, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
+            RG_CHECK(cudaMemcpyAsync(ws.seg_hist[0].p, off, sizeof off, cudaMemcpyHostToDevice, st));
+            const uint32_t tiles = uint32_t((n + ScatterCfg<RSC>::kTile - 1) / ScatterCfg<RSC>::kTile);
+            RG_CHECK(cudaMemsetAsync(ws.tile_seg.p, 0, tiles * sizeof(uint32_t), st));
+            RG_CHECK(cudaMemsetAsync(ws.stile_base.p, 0, sizeof(unsigned long long), st));
+            RG_CHECK(cudaMemsetAsync(ws.status.p, 0, size_t(tiles) * kRadix * sizeof(unsigned long long), st));
+            RG_CHECK(cudaMemsetAsync(ws.ctr.p, 0, sizeof(LevelCounters), st));
+            uint8_t* src = const_cast<uint8_t*>(static_cast<const uint8_t*>(d_src));
+            k_scatter<RSC, true><<<tiles, ScatterCfg<RSC>::kThreads, 0, st>>>(
+                src, static_cast<uint8_t*>(d_dst), ws.segs[0].p, ws.seg_hist[0].p, ws.stile_base.p,
+                ws.tile_seg.p, ws.status.p, ws.ctr.p, ks, ws.map8.p);
+            RG_LAUNCH_CHECK();
+            RG_CHECK(cudaStreamSynchronize(st));
+        });
+    });
+}
+
+void raduls_gpu_release(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto& kv : g_ws) {
+        Workspace* w = kv.second;
+        std::lock_guard<std::mutex> lk2(w->mu);
+        w->hist8.release(); w->andor0.release(); w->thr.release(); w->acc.release(); w->ctr.release();
+        for (int b = 0; b < 2; ++b) {
+            w->segs[b].release(); w->seg_hist[b].release(); w->seg_andor[b].release(); w->htile_seg[b].release();
+        }
+        w->stile_base.release(); w->tile_seg.release(); w->status.release(); w->groups.release();
+        w->copies.release(); w->host_data.release(); w->host_tmp.release(); w->map8.release(); w->map32.release();
+        if (w->h_ctr) cudaFreeHost(w->h_ctr);
+        if (w->h_small) cudaFreeHost(w->h_small);
+        delete w;
+    }
+    g_ws.clear();
+}
+
+}  // extern "C"

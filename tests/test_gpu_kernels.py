@@ -1,0 +1,107 @@
+"""GPU parity of the building-block kernels against the oracle.
+
+* generator bit-identical to oracle orc_generate;
+* histogram of bytes 0..7 == build_histogram (P/tests/test_kernels.cpp:62-85);
+* single-digit split byte-identical to radix_split (P/tests/test_kernels.cpp:114-143,
+  acceptance.cpp:138-166 kernel equivalence);
+* digest / check_sorted == array_digest / check_sorted (P/src/verify.cpp:27-50);
+* multi-GPU partition: stable grouping by destination rank.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from helpers import ALL_LAYOUTS, EXTRA_LAYOUTS, from_dev, make_input, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("rs,ks", ALL_LAYOUTS + [(32, 24), (16, 3)])
+@pytest.mark.parametrize("dist", [0, 1])
+def test_generator_bit_identical(rg, torch_cuda, rs, ks, dist):
+    for n, base in [(1, 0), (1000, 0), (77777, 123456789)]:
+        d = rg.generate(n, rg.RecordLayout(rs, ks), dist=dist, seed=0x5EED0001, index_base=base)
+        want = oracle.generate(n, rs, ks, dist, 0x5EED0001, base)
+        assert np.array_equal(from_dev(d), want)
+
+
+@pytest.mark.parametrize("rs,ks", ALL_LAYOUTS + EXTRA_LAYOUTS)
+def test_histogram_all_bytes(rg, torch_cuda, rs, ks):
+    for n, uni in [(0, 0), (1, 0), (5000, 0), (100003, 256), (65536, 1)]:
+        a = make_input(n, rs, ks, 17 + n, uni)
+        h, ao = rg.histogram(to_dev(torch_cuda, a), n, rg.RecordLayout(rs, ks))
+        for b in range(min(ks, 8)):
+            assert np.array_equal(h[b], oracle.histogram(a, rs, b)), (b, n)
+        if n:
+            words = a.reshape(n, rs).view("<u8")
+            for w in range(rs // 8):
+                assert int(ao[2 * w]) == int(np.bitwise_and.reduce(words[:, w]))
+                assert int(ao[2 * w + 1]) == int(np.bitwise_or.reduce(words[:, w]))
+
+
+@pytest.mark.parametrize("rs,ks", ALL_LAYOUTS)
+def test_split_matches_radix_split(rg, torch_cuda, rs, ks):
+    rng = np.random.default_rng(424242 + rs)
+    for it in range(6):
+        n = (1 << 20) if it == 0 else int(rng.integers(1, 300000))
+        a = make_input(n, rs, ks, int(rng.integers(1 << 40)), 1000 if it % 3 == 0 else 0)
+        off = int(rng.integers(0, ks))
+        src = to_dev(torch_cuda, a)
+        dst = torch_cuda.empty_like(src)
+        h = rg.split(src, dst, n, rs, off)
+        want, wh = oracle.radix_split(a, rs, off)
+        assert np.array_equal(h, wh)
+        assert np.array_equal(from_dev(dst), want)
+
+
+def test_split_identity_on_identical_keys(rg, torch_cuda):
+    """test_kernels.cpp:210-220."""
+    rs, n = 16, 10000
+    a = make_input(n, rs, 8, 1, universe=1)
+    src = to_dev(torch_cuda, a)
+    dst = torch_cuda.empty_like(src)
+    rg.split(src, dst, n, rs, 7)
+    assert np.array_equal(from_dev(dst), a)
+
+
+@pytest.mark.parametrize("rs,ks", ALL_LAYOUTS + [(32, 24)])
+def test_digest_and_check_sorted(rg, torch_cuda, rs, ks):
+    a = make_input(50001, rs, ks, 5, 300)
+    d = to_dev(torch_cuda, a)
+    assert rg.digest(d, 50001, rs) == oracle.digest(a, rs)
+    v, f = rg.check_sorted(d, 50001, rg.RecordLayout(rs, ks))
+    ok, first = oracle.check_sorted(a, rs, ks)
+    assert (v == 0) == ok
+    if not ok:
+        assert f == first
+    s = oracle.stable_sort(a, rs, ks)
+    assert rg.check_sorted(to_dev(torch_cuda, s), 50001, rg.RecordLayout(rs, ks))[0] == 0
+
+
+@pytest.mark.parametrize("rs,ks", [(16, 8), (8, 8), (32, 24)])
+def test_partition_stable_by_rank(rg, torch_cuda, rs, ks):
+    import ctypes as C
+    n, ranks, pb = 200000, 5, 0
+    a = make_input(n, rs, ks, 31 + rs, 0)
+    src = to_dev(torch_cuda, a)
+    dst = torch_cuda.empty_like(src)
+    # contiguous bucket ranges -> ranks
+    bucket_rank = (np.arange(65536) * ranks // 65536).astype(np.uint32)
+    dmap = torch_cuda.from_numpy(bucket_rank.view(np.int32)).cuda()
+    counts = np.zeros(ranks, dtype=np.uint64)
+    L = rg._lib.load()
+    rc = L.raduls_gpu_partition(src.data_ptr(), dst.data_ptr(), n, rs, ks, pb, dmap.data_ptr(),
+                                ranks, counts.ctypes.data_as(C.POINTER(C.c_uint64)), None)
+    assert rc == 0
+    torch_cuda.cuda.synchronize()
+    r = a.reshape(n, rs)
+    pref = (r[:, 0].astype(np.int64) << 8) | r[:, 1]
+    dest = bucket_rank[pref]
+    order = np.argsort(dest, kind="stable")
+    assert np.array_equal(counts, np.bincount(dest, minlength=ranks).astype(np.uint64))
+    assert np.array_equal(from_dev(dst).reshape(n, rs), r[order])
+    # prefix histogram
+    hist = torch_cuda.zeros(65536, dtype=torch_cuda.int64, device="cuda")
+    rc = L.raduls_gpu_prefix_histogram(src.data_ptr(), n, rs, ks, pb, hist.data_ptr(), None)
+    assert rc == 0
+    assert np.array_equal(hist.cpu().numpy(), np.bincount(pref, minlength=65536))

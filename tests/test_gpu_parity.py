@@ -1,0 +1,135 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bar: key sequence bit-exact, equal-key runs the same record
+multiset. The GPU sort is stable, so it must equal the oracle's *stable*
+sort (oracle_sort, P/src/verify.cpp:52-64) byte for byte, and for distinct
+keys it must equal the reference MSD (restated in oracle/raduls_oracle.c)
+byte for byte. Patterns follow P/tests/acceptance.cpp:102-166 and
+P/tests/test_scheduler.cpp:123-214.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from helpers import ALL_LAYOUTS, EXTRA_LAYOUTS, from_dev, make_input, to_dev
+
+pytestmark = pytest.mark.gpu
+
+SIZES = [0, 1, 2, 31, 32, 33, 100, 180, 383, 384, 385, 1000, 100000]
+
+
+def gpu_sort(rg, torch, a, rs, ks, tmp=False):
+    d = to_dev(torch, a)
+    t = torch.empty_like(d) if tmp else None
+    rg.sort(d, a.size // rs, rg.RecordLayout(rs, ks), tmp=t)
+    torch.cuda.synchronize()
+    return from_dev(d)
+
+
+def assert_parity(got, a, rs, ks):
+    want = oracle.stable_sort(a, rs, ks)
+    if not np.array_equal(got, want):
+        n = a.size // rs
+        g, w = got.reshape(n, rs), want.reshape(n, rs)
+        bad = np.nonzero((g != w).any(axis=1))[0]
+        raise AssertionError(f"mismatch at {len(bad)} records, first {bad[:5]} "
+                             f"(rs={rs} ks={ks} n={n})")
+
+
+@pytest.mark.parametrize("rs,ks", ALL_LAYOUTS + EXTRA_LAYOUTS)
+def test_oracle_equivalence_sizes(rg, torch_cuda, rs, ks):
+    """acceptance.cpp:102-136 pattern: layouts x boundary sizes x universes."""
+    seed = 20260809 + rs * 100 + ks
+    for i, n in enumerate(SIZES):
+        universe = (0, 256, 2)[i % 3]
+        a = make_input(n, rs, ks, seed + i, universe)
+        got = gpu_sort(rg, torch_cuda, a, rs, ks, tmp=bool(i % 2))
+        assert_parity(got, a, rs, ks)
+
+
+@pytest.mark.parametrize("rs,ks", [(8, 8), (16, 8), (32, 24), (24, 16)])
+def test_capacity_boundaries(rg, torch_cuda, rs, ks):
+    """Inputs straddling the local-sort capacity and the scatter tile."""
+    cap = rg.local_capacity(rs)
+    for j, n in enumerate([cap - 1, cap, cap + 1, 2 * cap + 3, 70000]):
+        a = make_input(n, rs, ks, 99 + j, (0, 256, 3)[j % 3])
+        assert_parity(gpu_sort(rg, torch_cuda, a, rs, ks), a, rs, ks)
+
+
+def test_distinct_keys_match_reference_msd_bytes(rg, torch_cuda):
+    """Distinct keys: byte-identical to the reference MSD (test_scheduler.cpp:171-183)."""
+    for rs, ks in ALL_LAYOUTS:
+        a = make_input(200000, rs, ks, 555 + rs + ks)
+        got = gpu_sort(rg, torch_cuda, a, rs, ks)
+        assert np.array_equal(got, oracle.msd_sort(a, rs, ks))
+
+
+def test_shape_extremes(rg, torch_cuda):
+    """test_scheduler.cpp:142-169: all-equal, sorted, reverse, empty."""
+    rs, ks = 16, 8
+    equal = make_input(50000, rs, ks, 7, universe=1)
+    assert np.array_equal(gpu_sort(rg, torch_cuda, equal, rs, ks), equal)  # stable identity
+    srt = oracle.stable_sort(make_input(20000, rs, ks, 8), rs, ks)
+    assert np.array_equal(gpu_sort(rg, torch_cuda, srt, rs, ks), srt)
+    rev = srt.reshape(-1, rs)[::-1].copy().reshape(-1)
+    assert_parity(gpu_sort(rg, torch_cuda, rev, rs, ks), rev, rs, ks)
+    empty = np.zeros(0, dtype=np.uint8)
+    assert gpu_sort(rg, torch_cuda, empty, rs, ks).size == 0
+
+
+def test_hot_leading_byte(rg, torch_cuda):
+    """test_scheduler.cpp:185-202: 80% of keys share the leading byte."""
+    rs, ks, n = 16, 8, 300000
+    a = make_input(n, rs, ks, 11)
+    r = a.reshape(n, rs)
+    hot = np.arange(n) % 5 != 0
+    r[hot, 0] = 0xAB
+    assert_parity(gpu_sort(rg, torch_cuda, a, rs, ks), a, rs, ks)
+
+
+def test_constant_middle_bytes_skew(rg, torch_cuda):
+    """C3-shaped input (leading constant bytes, Zipf byte): exercises (e)."""
+    rs, ks = 16, 8
+    a = make_input(1 << 20, rs, ks, 0x5EED0003, dist=oracle.DIST_SKEW)
+    assert_parity(gpu_sort(rg, torch_cuda, a, rs, ks), a, rs, ks)
+    st = rg.last_stats()
+    assert st["skipped_levels"] >= 0
+
+
+def test_long_ties_force_fallback(rg, torch_cuda):
+    """Keys equal on their first 20 bytes, different in the last 4: the local
+    sort's 4-byte window ties and the full-key fallback must order them."""
+    rs, ks, n = 32, 24, 9000
+    a = make_input(n, rs, ks, 3)
+    r = a.reshape(n, rs)
+    r[:, 0:20] = 7
+    assert_parity(gpu_sort(rg, torch_cuda, a, rs, ks), a, rs, ks)
+
+
+def test_million_records_digest(rg, torch_cuda):
+    """test_scheduler.cpp:204-214: 2^20 records, digest + sortedness on device."""
+    rs, ks, n = 16, 8, 1 << 20
+    a = make_input(n, rs, ks, 2718)
+    d = to_dev(torch_cuda, a)
+    before = rg.digest(d, n, rs)
+    assert before == oracle.digest(a, rs)
+    rg.sort(d, n, rg.RecordLayout(rs, ks))
+    assert rg.digest(d, n, rs) == before
+    assert rg.check_sorted(d, n, rg.RecordLayout(rs, ks))[0] == 0
+    assert_parity(from_dev(d), a, rs, ks)
+
+
+def test_host_dropin(rg):
+    """raduls_gpu_sort_host: the (data, tmp, n, rs, ks) drop-in on host memory."""
+    for rs, ks in [(16, 8), (32, 24), (8, 8)]:
+        a = make_input(123457, rs, ks, 42 + rs, 1000)
+        b = a.copy()
+        rg.sort(b, a.size // rs, rg.RecordLayout(rs, ks))
+        assert_parity(b, a, rs, ks)
+
+
+def test_invalid_layouts_raise(rg, torch_cuda):
+    buf = torch_cuda.zeros(64, dtype=torch_cuda.uint8, device="cuda")
+    for rs, ks in [(8, 16), (12, 8), (40, 8), (16, 0)]:
+        with pytest.raises(ValueError):
+            rg.sort(buf, 2, rg.RecordLayout(rs, ks))
