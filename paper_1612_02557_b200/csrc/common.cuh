@@ -60,7 +60,7 @@ __device__ __forceinline__ Rec<RS> load_rec_stream(const uint8_t* base, uint64_t
 #pragma unroll
         for (int v = 0; v < RS / 16; ++v) {
             uint4 q;
-            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+            asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                          : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w)
                          : "l"(reinterpret_cast<const uint4*>(p) + v));
             r.w[4 * v + 0] = q.x;
@@ -72,7 +72,7 @@ __device__ __forceinline__ Rec<RS> load_rec_stream(const uint8_t* base, uint64_t
 #pragma unroll
         for (int v = 0; v < RS / 8; ++v) {
             uint2 q;
-            asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+            asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
                          : "=r"(q.x), "=r"(q.y)
                          : "l"(reinterpret_cast<const uint2*>(p) + v));
             r.w[2 * v + 0] = q.x;
@@ -162,6 +162,80 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
     unsigned long long v;
     asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+
+// ---------------------------------------------------------------- TMA / mbarrier
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// Orders this thread's earlier generic-proxy shared-memory accesses (made
+// visible to it by a preceding __syncthreads) before its next async-proxy
+// (TMA) write into the same buffer.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+// 1-D TMA bulk copy global -> shared (16-B aligned addresses, size % 16 == 0),
+// completion signalled as transaction bytes on `bar`.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(a), "r"(phase)
+            : "memory");
+    } while (!ok);
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Named barrier over the first `nthreads` threads (consumer warps only).
+__device__ __forceinline__ void bar_sync_named(uint32_t id, uint32_t nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Warp multisplit peer mask for an 8-bit digit: lanes of this warp holding the
+// same digit (valid lanes only). Eight ballots instead of MATCH.ANY, whose
+// result latency dominated the first profile (ncu: short_sb stalls on the
+// BREV consuming it, profiles/r1_local_sort_match.txt).
+__device__ __forceinline__ uint32_t match_digit8(uint32_t d, bool valid) {
+    uint32_t m = __ballot_sync(0xFFFFFFFFu, valid);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const bool bit = (d >> b) & 1u;
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, bit);
+        m &= bit ? bal : ~bal;
+    }
+    return m;
 }
 
 // Device segment descriptors -------------------------------------------------

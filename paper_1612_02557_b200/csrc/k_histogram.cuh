@@ -50,35 +50,43 @@ __global__ void __launch_bounds__(256) k_histo_all(const uint8_t* __restrict__ d
 #pragma unroll
     for (int w = 0; w < KW; ++w) a[w] = ~0ull, o[w] = 0ull;
 
-    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-    for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x; base < n; base += stride) {
-        const uint64_t i = base + threadIdx.x;
-        const bool valid = i < n;
-        Rec<RS> r;
-        if (valid) {
-            r = load_rec_stream<RS>(data, i);
-        } else {
+    constexpr int U = 4;  // records in flight per thread
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * U;
+    for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x * U; base < n; base += stride) {
+        Rec<RS> r[U];
 #pragma unroll
-            for (int k = 0; k < Rec<RS>::kWords; ++k) r.w[k] = 0;
-        }
-        const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
-        const uint32_t lo = r.w[0], hi = r.w[1];
-        const uint32_t al = __reduce_and_sync(0xFFFFFFFFu, valid ? lo : ~0u);
-        const uint32_t ol = __reduce_or_sync(0xFFFFFFFFu, valid ? lo : 0u);
-        const uint32_t ah = __reduce_and_sync(0xFFFFFFFFu, valid ? hi : ~0u);
-        const uint32_t oh = __reduce_or_sync(0xFFFFFFFFu, valid ? hi : 0u);
-        for (uint32_t b = 0; b < nb; ++b) {  // nb is uniform
-            const uint32_t word = b < 4 ? lo : hi;
-            const uint32_t sh_ = (b & 3u) * 8u;
-            warp_hist_add(sh[b], (word >> sh_) & 0xFFu, valid, b < 4 ? al : ah, b < 4 ? ol : oh,
-                          sh_, nvalid);
-        }
-        if (valid) {
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + uint64_t(u) * blockDim.x + threadIdx.x;
+            if (i < n) {
+                r[u] = load_rec_stream<RS>(data, i);
+            } else {
 #pragma unroll
-            for (int w = 0; w < KW; ++w) {
-                const uint64_t v = rec_word64<RS>(r, w);
-                a[w] &= v;
-                o[w] |= v;
+                for (int k = 0; k < Rec<RS>::kWords; ++k) r[u].w[k] = 0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + uint64_t(u) * blockDim.x + threadIdx.x;
+            const bool valid = i < n;
+            const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
+            const uint32_t lo = r[u].w[0], hi = r[u].w[1];
+            const uint32_t al = __reduce_and_sync(0xFFFFFFFFu, valid ? lo : ~0u);
+            const uint32_t ol = __reduce_or_sync(0xFFFFFFFFu, valid ? lo : 0u);
+            const uint32_t ah = __reduce_and_sync(0xFFFFFFFFu, valid ? hi : ~0u);
+            const uint32_t oh = __reduce_or_sync(0xFFFFFFFFu, valid ? hi : 0u);
+            for (uint32_t b = 0; b < nb; ++b) {  // nb is uniform
+                const uint32_t word = b < 4 ? lo : hi;
+                const uint32_t sh_ = (b & 3u) * 8u;
+                warp_hist_add(sh[b], (word >> sh_) & 0xFFu, valid, b < 4 ? al : ah,
+                              b < 4 ? ol : oh, sh_, nvalid);
+            }
+            if (valid) {
+#pragma unroll
+                for (int w = 0; w < KW; ++w) {
+                    const uint64_t v = rec_word64<RS>(r[u], w);
+                    a[w] &= v;
+                    o[w] |= v;
+                }
             }
         }
     }

@@ -7,26 +7,29 @@
 // (msd_sorter.hpp:76-80).
 //
 // B200 design: one 1024-thread CTA sorts a *group* — one or more adjacent
-// complete segments (bins) of at most kCap records in total, all sharing key
-// bytes [0, p). Sorting the group by key bytes [p, ks) equals sorting each bin
-// on its own, because the bins are contiguous and already in key order.
-//   1. coalesced load of the group; AND/OR of the key words over the group
-//      gives the non-constant key bytes L = l0 < l1 < ... in [p, ks);
-//   2. the first <= 4 of them are packed big-endian into a 32-bit window per
-//      record, kept in shared memory;
-//   3. stable LSD passes (warp multisplit with __match_any_sync, per-warp
-//      counters, digit-major/warp-minor offsets) over the window bytes sort a
-//      16-bit permutation in shared memory;
-//   4. if more than four key bytes vary, adjacent records that tie on the window
-//      are compared on the remaining bytes; any inversion sends the group through
-//      a full stable LSD over every byte of L (rare on real keys, always correct);
-//   5. records are gathered in sorted order (the group was just read, so this hits
-//      L2), held in registers until the whole group is read, then written with
-//      coalesced vector stores straight into the caller's buffer — no separate
-//      copy-back pass, and safe when source and destination are the same buffer.
-// The whole sort is stable (stable splits + stable local sort), so its output
-// equals a stable sort by key; with distinct keys it is byte-identical to the
-// reference's (unstable) MSD output.
+// complete segments (bins) of at most kCap records, all sharing key bytes
+// [0, p). Sorting the group by key bytes [p, ks) equals sorting each bin on its
+// own, because the bins are contiguous and already in key order.
+//   1. every record of the group is loaded once (coalesced) and stays in
+//      registers until the end, so the sort is safe in place (source ==
+//      destination buffer);
+//   2. AND/OR of the key words over the group gives the varying key bytes
+//      L = l0 < l1 < ... in [p, ks); the first <= 4 are packed big-endian into
+//      a 32-bit window w per record (shared memory);
+//   3. fast path — one counting pass: bucket = the top B varying bits of w
+//      (B ~ log2 n, so buckets hold ~1 record), shared-memory histogram, scan,
+//      scatter of record ids into bucket order; then every record ranks itself
+//      inside its bucket by (w, remaining key bytes, input index). That is a
+//      comparison sort of ~1-2 records per bucket — the GPU counterpart of the
+//      reference's radix split followed by insertion sort of tiny bins;
+//   4. robust path, when a bucket would hold more than kMaxBucket records
+//      (duplicate-heavy or adversarial keys): stable LSD passes over the
+//      window bytes (ballot multisplit ranking), then over the bytes beyond
+//      the window if adjacent records still tie;
+//   5. each thread stores its own records at their final positions.
+// Every path orders equal keys by input index, so the whole MSD sort is
+// stable: its output equals a stable sort by key, and for distinct keys it is
+// byte-identical to the reference's (unstable) MSD output.
 #pragma once
 
 #include "common.cuh"
@@ -39,18 +42,48 @@ struct LocalCfg {
     static constexpr int kWarps = kThreads / 32;
     static constexpr int kIpt = RS == 8 ? 20 : RS == 16 ? 10 : RS == 24 ? 7 : 5;
     static constexpr int kCap = kThreads * kIpt;  // records per group (C_local)
-    static constexpr size_t kSmem = size_t(kCap) * (4 + 2 + 2) + size_t(kWarps) * kRadix * 4 + 2048;
+    static constexpr int kBucketBits = RS == 8 ? 14 : RS == 16 ? 14 : 13;
+    static constexpr int kCntBytes =
+        (1 << kBucketBits) * 2 > kWarps * kRadix * 4 ? (1 << kBucketBits) * 2 : kWarps * kRadix * 4;
+    static constexpr size_t kSmem = size_t(kCap) * (4 + 2 + 2) + size_t(kCntBytes);
 };
 
-struct LocalShared {
-    uint32_t* win;    // [cap]
-    uint16_t* pa;     // [cap]
-    uint16_t* pb;     // [cap]
-    uint32_t* wcnt;   // [warps][256]
-};
+constexpr uint32_t kMaxBucket = 48;
+
+// Block-wide exclusive scan of one u32 per thread (blockDim 1024).
+__device__ __forceinline__ uint32_t block_scan_excl_1024(uint32_t v, uint32_t* s_w,
+                                                         uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+        if (lane >= off) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = s_w[lane];
+        uint32_t z = w;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, z, off);
+            if (lane >= off) z += y;
+        }
+        s_w[32 + lane] = z - w;
+        if (lane == 31) s_w[64] = z;
+    }
+    __syncthreads();
+    const uint32_t r = s_w[32 + warp] + x - v;
+    *total = s_w[64];
+    __syncthreads();
+    return r;
+}
 
 // One stable LSD pass: pout <- pin ordered by digit(pin[pos]). Positions are
-// split into 32 contiguous warp chunks (multiples of 32) processed in order.
+// split into 32 contiguous warp chunks (multiples of 32) processed in order;
+// ranking by ballot multisplit with warp-private counters (digit-major,
+// warp-minor offsets keep it stable).
 template <int IPT, bool kIdentity, typename DigitFn>
 __device__ __forceinline__ void lsd_pass(uint32_t n, const uint16_t* pin, uint16_t* pout,
                                          uint32_t* wcnt, uint32_t* s_tot, DigitFn digit_of) {
@@ -71,17 +104,13 @@ __device__ __forceinline__ void lsd_pass(uint32_t n, const uint16_t* pin, uint16
             const uint32_t pos = warp * chunk + s * 32 + lane;
             const bool valid = pos < n;
             const uint32_t e = valid ? (kIdentity ? pos : uint32_t(pin[pos])) : 0u;
-            const uint32_t d = valid ? digit_of(e) : 0x100u;
-            const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
-            const int leader = __ffs(peers) - 1;
-            uint32_t old = 0;
-            if (lane == leader && valid) {
-                old = my[d];
-                my[d] = old + __popc(peers);
-            }
-            old = __shfl_sync(0xFFFFFFFFu, old, leader);
+            const uint32_t d = valid ? digit_of(e) : 0u;
+            const uint32_t peers = match_digit8(d, valid);
+            const uint32_t before = valid ? my[d] : 0u;
             __syncwarp();
-            if (valid) pk[s] = d | ((old + __popc(peers & lt)) << 8);
+            if (valid && uint32_t(lane) == 31u - __clz(peers)) my[d] = before + __popc(peers);
+            __syncwarp();
+            if (valid) pk[s] = d | ((before + __popc(peers & lt)) << 8);
         }
     }
     __syncthreads();
@@ -91,16 +120,14 @@ __device__ __forceinline__ void lsd_pass(uint32_t n, const uint16_t* pin, uint16
         uint32_t part = 0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) part += wcnt[(q * 8 + w) * kRadix + d];
-        // exclusive scan across the 4 quarter-threads of this digit (consecutive lanes)
         uint32_t x = part;
         uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, 1, 4);
         if (q >= 1) x += y;
         y = __shfl_up_sync(0xFFFFFFFFu, x, 2, 4);
         if (q >= 2) x += y;
         const uint32_t qexcl = x - part;
-        if (q == 3) s_tot[d] = x;  // digit total
+        if (q == 3) s_tot[d] = x;
         __syncthreads();
-        // warp 0: exclusive scan of the 256 digit totals (8 per lane)
         if (warp == 0) {
             uint32_t v[8], sum = 0;
 #pragma unroll
@@ -141,10 +168,23 @@ __device__ __forceinline__ void lsd_pass(uint32_t n, const uint16_t* pin, uint16
     __syncthreads();
 }
 
-// Key byte `b` of record `e` of the group, read from global memory (fallback path).
+// Key byte `b` of group record `e`, read from global memory (L2-resident: the
+// group was just loaded).
 template <int RS>
 __device__ __forceinline__ uint32_t gbyte(const uint8_t* src, uint32_t e, uint32_t b) {
     return src[size_t(e) * RS + b];
+}
+
+// -1/0/+1: compare records a, b of the group on the varying key bytes beyond
+// the window (L[4..nL)).
+template <int RS>
+__device__ __forceinline__ int cmp_beyond(const uint8_t* src, uint32_t a, uint32_t b,
+                                          const uint32_t* L, uint32_t nL) {
+    for (uint32_t q = 4; q < nL; ++q) {
+        const uint32_t x = gbyte<RS>(src, a, L[q]), y = gbyte<RS>(src, b, L[q]);
+        if (x != y) return x < y ? -1 : 1;
+    }
+    return 0;
 }
 
 template <int RS>
@@ -156,15 +196,16 @@ __global__ void __launch_bounds__(1024, 1) k_local_sort(uint8_t* __restrict__ da
     using C = LocalCfg<RS>;
     constexpr int T = C::kThreads, IPT = C::kIpt;
     constexpr int KW = RS / 8;
-    extern __shared__ __align__(16) uint8_t smem[];
-    uint32_t* win = reinterpret_cast<uint32_t*>(smem);
-    uint16_t* pa = reinterpret_cast<uint16_t*>(win + C::kCap);
-    uint16_t* pb = pa + C::kCap;
-    uint32_t* wcnt = reinterpret_cast<uint32_t*>(pb + C::kCap);
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint32_t* win = reinterpret_cast<uint32_t*>(smem);              // [cap]
+    uint16_t* slot = reinterpret_cast<uint16_t*>(win + C::kCap);    // [cap]  (LSD: pa)
+    uint16_t* fpos = slot + C::kCap;                                // [cap]  (LSD: pb)
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(fpos + C::kCap);    // packed u16 pairs / LSD wcnt
     __shared__ uint32_t s_tot[512];
     __shared__ unsigned long long s_and[32][KW], s_or[32][KW];
     __shared__ uint32_t s_L[32];
-    __shared__ uint32_t s_nL, s_flag;
+    __shared__ uint32_t s_nL, s_flag, s_maxb, s_hb;
+    __shared__ uint32_t s_scan[65];
 
     const Group g = groups[blockIdx.x];
     const uint32_t n = g.size;
@@ -177,149 +218,252 @@ __global__ void __launch_bounds__(1024, 1) k_local_sort(uint8_t* __restrict__ da
         return;
     }
 
-    // 1. load keys, AND/OR reduce
-    uint64_t a[KW], o[KW];
-#pragma unroll
-    for (int w = 0; w < KW; ++w) a[w] = ~0ull, o[w] = 0ull;
+    // 1. load the group into registers; AND/OR of every record word
+    Rec<RS> r[IPT];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
-        const uint32_t i = uint32_t(j) * T + threadIdx.x;
-        if (i < n) {
-            const Rec<RS> r = load_rec<RS>(src, i);
+        const uint32_t e = uint32_t(j) * T + threadIdx.x;
+        if (e < n) r[j] = load_rec_stream<RS>(src, e);
+    }
+    {
+        uint64_t a[KW], o[KW];
 #pragma unroll
-            for (int w = 0; w < KW; ++w) {
-                const uint64_t v = rec_word64<RS>(r, w);
-                a[w] &= v;
-                o[w] |= v;
+        for (int w = 0; w < KW; ++w) a[w] = ~0ull, o[w] = 0ull;
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            if (uint32_t(j) * T + threadIdx.x < n) {
+#pragma unroll
+                for (int w = 0; w < KW; ++w) {
+                    const uint64_t v = rec_word64<RS>(r[j], w);
+                    a[w] &= v;
+                    o[w] |= v;
+                }
             }
         }
-    }
-#pragma unroll
-    for (int w = 0; w < KW; ++w) {
-        for (int off = 16; off; off >>= 1) {
-            a[w] &= __shfl_xor_sync(0xFFFFFFFFu, a[w], off);
-            o[w] |= __shfl_xor_sync(0xFFFFFFFFu, o[w], off);
-        }
-        if (lane == 0) s_and[warp][w] = a[w], s_or[warp][w] = o[w];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint64_t diff[KW];
 #pragma unroll
         for (int w = 0; w < KW; ++w) {
-            uint64_t ra = ~0ull, ro = 0ull;
-            for (int q = 0; q < 32; ++q) ra &= s_and[q][w], ro |= s_or[q][w];
-            diff[w] = ra ^ ro;
+            for (int off = 16; off; off >>= 1) {
+                a[w] &= __shfl_xor_sync(0xFFFFFFFFu, a[w], off);
+                o[w] |= __shfl_xor_sync(0xFFFFFFFFu, o[w], off);
+            }
+            if (lane == 0) s_and[warp][w] = a[w], s_or[warp][w] = o[w];
         }
-        uint32_t nL = 0;
-        for (uint32_t b = g.p; b < ks; ++b) {
-            uint64_t dw = diff[0];
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // warp 0: varying key bytes in [p, ks)
+        uint32_t diffb = 0;  // lane b: byte b varies
+        {
+            const uint32_t b = lane;
+            if (b >= g.p && b < ks && b < uint32_t(RS)) {
+                unsigned long long ra = ~0ull, ro = 0ull;
+                for (int q = 0; q < 32; ++q) {
+                    unsigned long long xa = s_and[q][0], xo = s_or[q][0];
 #pragma unroll
-            for (int w = 1; w < KW; ++w) dw = (b >> 3) == uint32_t(w) ? diff[w] : dw;
-            if ((dw >> ((b & 7) * 8)) & 0xFF) s_L[nL++] = b;
+                    for (int w = 1; w < KW; ++w)
+                        if ((b >> 3) == uint32_t(w)) xa = s_and[q][w], xo = s_or[q][w];
+                    ra &= xa;
+                    ro |= xo;
+                }
+                diffb = uint32_t(((ra ^ ro) >> ((b & 7) * 8)) & 0xFF);
+            }
         }
-        s_nL = nL;
-        s_flag = 0;
+        const uint32_t vm = __ballot_sync(0xFFFFFFFFu, diffb != 0);
+        if (diffb) s_L[__popc(vm & lanemask_lt())] = lane;
+        const uint32_t first = vm ? uint32_t(__ffs(vm) - 1) : 0u;
+        const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, diffb, first);
+        if (lane == 0) {
+            s_hb = x0 ? 24u + (31u - __clz(x0)) : 31u;
+            s_nL = __popc(vm);
+            s_flag = 0;
+            s_maxb = 0;
+        }
     }
     __syncthreads();
     const uint32_t nL = s_nL;
+    if (nL == 0) {  // every key equal: stable order is the input order
+        if (g.parity) {
+#pragma unroll
+            for (int j = 0; j < IPT; ++j) {
+                const uint32_t e = uint32_t(j) * T + threadIdx.x;
+                if (e < n) store_rec<RS>(dst, e, r[j]);
+            }
+        }
+        return;
+    }
     const uint32_t nwin = nL < 4 ? nL : 4;
 
-    uint16_t* sorted = pa;  // identity when nL == 0
-    if (nL > 0) {
-        // 2. windows: bytes L[0..nwin) packed big-endian into the top of a u32
+    // 2. 32-bit windows
+    {
         const uint32_t L0 = s_L[0], L1 = s_L[nwin > 1 ? 1 : 0], L2 = s_L[nwin > 2 ? 2 : 0],
                        L3 = s_L[nwin > 3 ? 3 : 0];
 #pragma unroll
         for (int j = 0; j < IPT; ++j) {
-            const uint32_t i = uint32_t(j) * T + threadIdx.x;
-            if (i < n) {
-                const Rec<RS> r = load_rec<RS>(src, i);  // L1/L2 hit: just loaded
-                uint32_t wv = rec_byte<RS>(r, L0) << 24;
-                if (nwin > 1) wv |= rec_byte<RS>(r, L1) << 16;
-                if (nwin > 2) wv |= rec_byte<RS>(r, L2) << 8;
-                if (nwin > 3) wv |= rec_byte<RS>(r, L3);
-                win[i] = wv;
+            const uint32_t e = uint32_t(j) * T + threadIdx.x;
+            if (e < n) {
+                uint32_t wv = rec_byte<RS>(r[j], L0) << 24;
+                if (nwin > 1) wv |= rec_byte<RS>(r[j], L1) << 16;
+                if (nwin > 2) wv |= rec_byte<RS>(r[j], L2) << 8;
+                if (nwin > 3) wv |= rec_byte<RS>(r[j], L3);
+                win[e] = wv;
+            }
+        }
+    }
+    // bucket geometry: the top B bits below the window's highest varying bit
+    // (byte L0 varies, so that bit is in [24, 31]).
+    uint32_t B = 32u - __clz(n - 1);  // ceil(log2 n)
+    B = B < 1 ? 1 : (B > uint32_t(C::kBucketBits) ? uint32_t(C::kBucketBits) : B);
+    const uint32_t hb = s_hb;  // window bit of the highest varying key bit (byte L0)
+    const uint32_t shift = hb + 1u - B;  // >= 24+1-14 > 0
+    const uint32_t bmask = (1u << B) - 1u;
+    const uint32_t nbk = 1u << B;
+    const bool beyond = nL > 4;
+
+    // 3a. bucket histogram (packed u16 pairs)
+    for (uint32_t i = threadIdx.x; i < nbk / 2; i += T) cnt[i] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        const uint32_t e = uint32_t(j) * T + threadIdx.x;
+        if (e < n) {
+            const uint32_t b = (win[e] >> shift) & bmask;
+            atomicAdd(&cnt[b >> 1], 1u << ((b & 1) * 16));
+        }
+    }
+    __syncthreads();
+    // 3b. exclusive scan over nbk buckets; each thread owns a contiguous run
+    {
+        const uint32_t per = nbk > uint32_t(T) ? nbk / T : 1u;  // buckets per thread (even or 1)
+        const uint32_t b0 = threadIdx.x * per;
+        uint32_t sum = 0, mx = 0;
+        if (b0 < nbk) {
+            for (uint32_t b = b0; b < b0 + per; ++b) {
+                const uint32_t c = (cnt[b >> 1] >> ((b & 1) * 16)) & 0xFFFFu;
+                sum += c;
+                mx = c > mx ? c : mx;
+            }
+        }
+        uint32_t total;
+        uint32_t run = block_scan_excl_1024(sum, s_scan, &total);
+        // max bucket
+        for (int off = 16; off; off >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, off));
+        if (lane == 0 && mx) atomicMax(&s_maxb, mx);
+        if (b0 < nbk) {
+            for (uint32_t b = b0; b < b0 + per; b += (per >= 2 ? 2 : 1)) {
+                if (per >= 2) {
+                    const uint32_t w = cnt[b >> 1];
+                    const uint32_t c0 = w & 0xFFFFu, c1 = w >> 16;
+                    cnt[b >> 1] = run | ((run + c0) << 16);
+                    run += c0 + c1;
+                } else {
+                    // per == 1 (nbk <= 1024): owner of the even bucket rewrites the pair
+                    const uint32_t w = cnt[b >> 1];
+                    if ((b & 1) == 0) {
+                        const uint32_t c0 = w & 0xFFFFu;
+                        cnt[b >> 1] = run | ((run + c0) << 16);
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const bool fast = s_maxb <= kMaxBucket;
+
+    if (fast) {
+        // 3c. scatter record ids into bucket order (cursor = packed start)
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            const uint32_t e = uint32_t(j) * T + threadIdx.x;
+            if (e < n) {
+                const uint32_t b = (win[e] >> shift) & bmask;
+                const uint32_t old = atomicAdd(&cnt[b >> 1], 1u << ((b & 1) * 16));
+                slot[(old >> ((b & 1) * 16)) & 0xFFFFu] = uint16_t(e);
             }
         }
         __syncthreads();
-        // 3. LSD over the window bytes, least significant first
-        uint16_t *pin = pa, *pout = pb;
+        // 3d. rank inside the bucket: cnt now holds bucket ends
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            const uint32_t e = uint32_t(j) * T + threadIdx.x;
+            if (e < n) {
+                const uint32_t w = win[e];
+                const uint32_t b = (w >> shift) & bmask;
+                const uint32_t en = (cnt[b >> 1] >> ((b & 1) * 16)) & 0xFFFFu;
+                const uint32_t st =
+                    b ? (cnt[(b - 1) >> 1] >> (((b - 1) & 1) * 16)) & 0xFFFFu : 0u;
+                uint32_t rank = 0;
+                for (uint32_t q = st; q < en; ++q) {
+                    const uint32_t e2 = slot[q];
+                    const uint32_t w2 = win[e2];
+                    bool less = w2 < w;
+                    if (w2 == w && e2 != e) {
+                        int c = beyond ? cmp_beyond<RS>(src, e2, e, s_L, nL) : 0;
+                        less = c < 0 || (c == 0 && e2 < e);
+                    }
+                    rank += less;
+                }
+                fpos[e] = uint16_t(st + rank);
+            }
+        }
+        __syncthreads();
+    } else {
+        // 4. robust stable LSD over the window bytes, then beyond if needed
+        if (threadIdx.x == 0) atomicAdd(&ctr->fallback_groups, 1ull);
+        uint16_t *pin = slot, *pout = fpos;
         bool first = true;
         for (int q = int(nwin) - 1; q >= 0; --q) {
-            const uint32_t shift = 24u - 8u * uint32_t(q);
-            auto dig = [&](uint32_t e) { return (win[e] >> shift) & 0xFFu; };
+            const uint32_t sh = 24u - 8u * uint32_t(q);
+            auto dig = [&](uint32_t e) { return (win[e] >> sh) & 0xFFu; };
             if (first)
-                lsd_pass<IPT, true>(n, pin, pout, wcnt, s_tot, dig);
+                lsd_pass<IPT, true>(n, pin, pout, cnt, s_tot, dig);
             else
-                lsd_pass<IPT, false>(n, pin, pout, wcnt, s_tot, dig);
+                lsd_pass<IPT, false>(n, pin, pout, cnt, s_tot, dig);
             first = false;
             uint16_t* t = pin;
             pin = pout;
             pout = t;
         }
-        sorted = pin;
-        // 4. ties beyond the window
-        if (nL > 4) {
+        if (beyond) {
             for (uint32_t pos = threadIdx.x + 1; pos < n; pos += T) {
-                const uint32_t ea = sorted[pos - 1], eb = sorted[pos];
-                if (win[ea] == win[eb]) {
-                    for (uint32_t q = 4; q < nL; ++q) {
-                        const uint32_t ba = gbyte<RS>(src, ea, s_L[q]);
-                        const uint32_t bb = gbyte<RS>(src, eb, s_L[q]);
-                        if (ba != bb) {
-                            if (bb < ba) s_flag = 1;
-                            break;
-                        }
-                    }
-                }
+                const uint32_t ea = pin[pos - 1], eb = pin[pos];
+                if (win[ea] == win[eb] && cmp_beyond<RS>(src, ea, eb, s_L, nL) > 0) s_flag = 1;
             }
             __syncthreads();
             if (s_flag) {  // full stable LSD over every varying byte
-                if (threadIdx.x == 0) atomicAdd(&ctr->fallback_groups, 1ull);
-                pin = pa;
-                pout = pb;
                 first = true;
                 for (int q = int(nL) - 1; q >= 0; --q) {
                     const uint32_t b = s_L[q];
                     if (q >= 4) {
                         auto dig = [&](uint32_t e) { return gbyte<RS>(src, e, b); };
                         if (first)
-                            lsd_pass<IPT, true>(n, pin, pout, wcnt, s_tot, dig);
+                            lsd_pass<IPT, true>(n, pin, pout, cnt, s_tot, dig);
                         else
-                            lsd_pass<IPT, false>(n, pin, pout, wcnt, s_tot, dig);
+                            lsd_pass<IPT, false>(n, pin, pout, cnt, s_tot, dig);
                     } else {
-                        const uint32_t shift = 24u - 8u * uint32_t(q);
-                        auto dig = [&](uint32_t e) { return (win[e] >> shift) & 0xFFu; };
+                        const uint32_t sh = 24u - 8u * uint32_t(q);
+                        auto dig = [&](uint32_t e) { return (win[e] >> sh) & 0xFFu; };
                         if (first)
-                            lsd_pass<IPT, true>(n, pin, pout, wcnt, s_tot, dig);
+                            lsd_pass<IPT, true>(n, pin, pout, cnt, s_tot, dig);
                         else
-                            lsd_pass<IPT, false>(n, pin, pout, wcnt, s_tot, dig);
+                            lsd_pass<IPT, false>(n, pin, pout, cnt, s_tot, dig);
                     }
                     first = false;
                     uint16_t* t = pin;
                     pin = pout;
                     pout = t;
                 }
-                sorted = pin;
             }
         }
-    } else if (!g.parity) {
-        return;  // every key equal and already home: stable order == input order
+        // inverse permutation into pout (e -> final position)
+        for (uint32_t pos = threadIdx.x; pos < n; pos += T) pout[pin[pos]] = uint16_t(pos);
+        __syncthreads();
+        fpos = pout;
     }
 
-    // 5. gather in sorted order (all reads before any write), coalesced stores
-    Rec<RS> out[IPT];
+    // 5. every record to its final position (all reads of src are done)
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
-        const uint32_t pos = uint32_t(j) * T + threadIdx.x;
-        if (pos < n) out[j] = load_rec<RS>(src, nL > 0 ? uint32_t(sorted[pos]) : pos);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-        const uint32_t pos = uint32_t(j) * T + threadIdx.x;
-        if (pos < n) store_rec<RS>(dst, pos, out[j]);
+        const uint32_t e = uint32_t(j) * T + threadIdx.x;
+        if (e < n) store_rec<RS>(dst, fpos[e], r[j]);
     }
     if (threadIdx.x == 0) atomicAdd(&ctr->moved_local, (unsigned long long)n);
 }

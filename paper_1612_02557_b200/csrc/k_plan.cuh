@@ -67,9 +67,10 @@ __device__ void emit_copies(const PlanArgs& A, uint64_t start, uint64_t size, ui
     }
 }
 
-// Allocate and initialise one next-level segment (called by a single thread).
+// Allocate one next-level segment (called by a single thread); *htile_base
+// receives its first histogram tile.
 __device__ uint32_t emit_next(const PlanArgs& A, uint64_t start, uint64_t size, uint32_t p,
-                              uint32_t parity) {
+                              uint32_t parity, uint32_t* htile_base) {
     const uint32_t idx = atomicAdd(&A.ctr->n_next, 1u);
     const uint32_t nt = uint32_t((size + kHistTile - 1) / kHistTile);
     const uint32_t hb = atomicAdd(&A.ctr->n_next_htiles, nt);
@@ -80,14 +81,15 @@ __device__ uint32_t emit_next(const PlanArgs& A, uint64_t start, uint64_t size, 
     s.parity = parity;
     s.htile_base = hb;
     A.next[idx] = s;
+    *htile_base = hb;
     return idx;
 }
 
 __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
     __shared__ unsigned long long s_cnt[kRadix], s_off[kRadix];
     __shared__ unsigned long long s_wsum[8];
-    __shared__ uint32_t s_action, s_pnext, s_base, s_ngroups, s_nnext;
-    __shared__ uint32_t s_next_idx[kRadix];
+    __shared__ uint32_t s_action, s_pnext, s_base, s_ngroups, s_hb0;
+    __shared__ uint32_t s_next_idx[kRadix], s_next_hb[kRadix];
     __shared__ uint64_t s_gstart[kRadix];
     __shared__ uint32_t s_gsize[kRadix];
     const uint32_t s = blockIdx.x;
@@ -112,15 +114,11 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
         return;
     }
     if (action == 1) {  // (e) constant byte p: skip it without moving a record
-        if (tid == 0) {
-            const uint32_t idx = emit_next(A, g.start, g.size, s_pnext, g.parity);
-            s_base = idx;
-        }
+        if (tid == 0) s_base = emit_next(A, g.start, g.size, s_pnext, g.parity, &s_hb0);
         __syncthreads();
         const uint32_t idx = s_base;
-        const Seg nx = A.next[idx];
         const uint32_t nt = uint32_t((g.size + kHistTile - 1) / kHistTile);
-        for (uint32_t t = tid; t < nt; t += blockDim.x) A.next_htile_seg[nx.htile_base + t] = idx;
+        for (uint32_t t = tid; t < nt; t += blockDim.x) A.next_htile_seg[s_hb0 + t] = idx;
         A.next_hist[uint64_t(idx) * kRadix + tid] = 0ull;
         if (tid < 8) A.next_andor[uint64_t(idx) * 8 + tid] = (tid & 1) ? 0ull : ~0ull;
         return;
@@ -149,7 +147,6 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
         A.stile_base[s] = s_base;
         atomicAdd(&A.ctr->n_scatter_segs, 1u);
         atomicAdd(&A.ctr->moved_scatter, (unsigned long long)g.size);
-        s_nnext = 0;
     }
     __syncthreads();
     {
@@ -166,7 +163,8 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
     // big children -> next level
     const unsigned long long cs = s_cnt[tid];
     s_next_idx[tid] = 0xFFFFFFFFu;
-    if (cs > A.cap_local) s_next_idx[tid] = emit_next(A, g.start + s_off[tid], cs, g.p + 1, cp);
+    if (cs > A.cap_local)
+        s_next_idx[tid] = emit_next(A, g.start + s_off[tid], cs, g.p + 1, cp, &s_next_hb[tid]);
     // small children -> greedy groups (thread 0, digit order)
     if (tid == 0) {
         uint32_t ng = 0;
@@ -201,9 +199,9 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
     for (int d = 0; d < kRadix; ++d) {
         const uint32_t idx = s_next_idx[d];
         if (idx == 0xFFFFFFFFu) continue;
-        const Seg nx = A.next[idx];
-        const uint32_t nt = uint32_t((nx.size + kHistTile - 1) / kHistTile);
-        for (uint32_t t = tid; t < nt; t += blockDim.x) A.next_htile_seg[nx.htile_base + t] = idx;
+        const uint32_t nt = uint32_t((s_cnt[d] + kHistTile - 1) / kHistTile);
+        const uint32_t hb = s_next_hb[d];
+        for (uint32_t t = tid; t < nt; t += blockDim.x) A.next_htile_seg[hb + t] = idx;
         A.next_hist[uint64_t(idx) * kRadix + tid] = 0ull;
         if (tid < 8) A.next_andor[uint64_t(idx) * 8 + tid] = (tid & 1) ? 0ull : ~0ull;
     }

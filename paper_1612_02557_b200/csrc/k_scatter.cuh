@@ -36,10 +36,12 @@ struct ScatterCfg {
     static constexpr int kItems = RS == 8 ? 16 : RS == 16 ? 8 : RS == 24 ? 5 : 4;
     static constexpr int kTile = kThreads * kItems;
     static constexpr int kWarps = kThreads / 32;
+    static constexpr int kBufBytes = ((kTile * RS + 16 + 127) / 128) * 128;  // + alignment slack
+    static constexpr size_t kSmem = size_t(2) * kBufBytes + size_t(kTile) * 3;  // 2 buffers + map + digit
 };
 
-// Block-wide exclusive scan of one u32 per thread over the first 256 threads
-// (blockDim >= 256). Returns the exclusive prefix; *total gets the sum.
+// Exclusive scan of one u32 per thread over the 256 consumer threads (named
+// barrier 1; every consumer thread must call it). Returns the exclusive prefix; *total gets the sum.
 __device__ __forceinline__ uint32_t scan256_exclusive(uint32_t v, uint32_t* s_warp,
                                                       uint32_t* total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -50,7 +52,7 @@ __device__ __forceinline__ uint32_t scan256_exclusive(uint32_t v, uint32_t* s_wa
         if (lane >= off) x += y;
     }
     if (threadIdx.x < 256 && lane == 31) s_warp[warp] = x;
-    __syncthreads();
+    bar_sync_named(1, 256);
     uint32_t wsum = 0, tot = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -58,146 +60,226 @@ __device__ __forceinline__ uint32_t scan256_exclusive(uint32_t v, uint32_t* s_wa
         wsum += (k < warp) ? c : 0u;
         tot += c;
     }
-    __syncthreads();
+    bar_sync_named(1, 256);
     *total = tot;
     return wsum + x - v;
 }
 
-// Digit of a record: key byte p (MSD split), or — kMap — the destination rank
-// of its 16-bit key prefix at bytes (p, p+1) through a 65536-entry map (the
-// multi-GPU key-range partition).
+// Digit of a staged record: key byte p (MSD split), or — kMap — the
+// destination rank of its 16-bit key prefix at bytes (p, p+1) through a
+// 65536-entry map (the multi-GPU key-range partition).
 template <int RS, bool kMap>
-__device__ __forceinline__ uint32_t scatter_digit(const Rec<RS>& r, uint32_t p, uint32_t ks,
-                                                  const uint8_t* __restrict__ map) {
+__device__ __forceinline__ uint32_t scatter_digit_smem(const uint8_t* rec, uint32_t p, uint32_t ks,
+                                                       const uint8_t* __restrict__ map) {
     if constexpr (kMap) {
-        const uint32_t hi = p < ks ? rec_byte<RS>(r, p) : 0u;
-        const uint32_t lo = p + 1 < ks ? rec_byte<RS>(r, p + 1) : 0u;
+        const uint32_t hi = p < ks ? rec[p] : 0u;
+        const uint32_t lo = p + 1 < ks ? rec[p + 1] : 0u;
         return __ldg(map + ((hi << 8) | lo));
     } else {
-        return rec_byte<RS>(r, p);
+        return rec[p];
     }
 }
 
+// Per-tile facts resolved by the issuing thread when the tile is claimed.
+struct TileInfo {
+    uint32_t tile;    // ticket (status row); >= n_tiles: none
+    uint32_t seg;
+    uint32_t tn;      // records in the tile
+    uint32_t p;
+    uint32_t parity;
+    uint32_t head;    // byte offset of the tile inside its smem buffer (0 or 8)
+    uint64_t k;       // tile index inside the segment
+    uint64_t gstart;  // first record of the tile (global record index)
+    uint64_t seg_start;
+};
+
+// Warp-specialised, persistent: warp 8 is the producer (claims tile tickets,
+// resolves their segment, TMA-loads the tile into one of two shared-memory
+// buffers), warps 0-7 consume (rank, look-back, write). full/empty mbarriers
+// hand buffers back and forth, so the next tile streams in from HBM while the
+// current one is ranked and written.
 template <int RS, bool kMap = false>
-__global__ void __launch_bounds__(ScatterCfg<RS>::kThreads) k_scatter(
+__global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
     uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Seg* __restrict__ segs,
     const unsigned long long* __restrict__ seg_off,  // [nseg][256] exclusive digit offsets
     const unsigned long long* __restrict__ stile_base, const uint32_t* __restrict__ tile_seg,
     unsigned long long* __restrict__ status,  // [ntiles][256], zeroed
-    LevelCounters* __restrict__ ctr, uint32_t ks = 0, const uint8_t* __restrict__ map = nullptr) {
+    LevelCounters* __restrict__ ctr, uint32_t n_tiles, uint32_t ks = 0,
+    const uint8_t* __restrict__ map = nullptr) {
     using C = ScatterCfg<RS>;
     constexpr int T = C::kThreads, IT = C::kItems, W = C::kWarps;
-    __shared__ __align__(16) uint8_t s_recs[C::kTile * RS];
-    __shared__ uint8_t s_dig[C::kTile];
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t* buf0 = smem;
+    uint16_t* s_map = reinterpret_cast<uint16_t*>(smem + 2 * C::kBufBytes);
+    uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_map + C::kTile);
     __shared__ uint32_t s_wcnt[W][kRadix];
     __shared__ uint32_t s_lstart[kRadix];
     __shared__ long long s_gdelta[kRadix];
     __shared__ uint32_t s_scan[8];
-    __shared__ uint32_t s_tile;
+    __shared__ __align__(8) unsigned long long s_full[2], s_empty[2];
+    __shared__ TileInfo s_info[2];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_ticket, 1u);
-    for (int i = threadIdx.x; i < W * kRadix; i += T) (&s_wcnt[0][0])[i] = 0;
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    const uint32_t s = tile_seg[tile];
-    const Seg g = segs[s];
-    const uint64_t k = uint64_t(tile) - stile_base[s];
-    const uint64_t t0 = k * C::kTile;
-    const uint32_t tn = uint32_t(min(uint64_t(C::kTile), g.size - t0));
-    const uint8_t* src = (g.parity ? tmp : data) + (g.start + t0) * RS;
-    uint8_t* dst = (g.parity ? data : tmp);
-    const uint32_t p = g.p;
-
-    // 1-2: load + warp multisplit rank
-    Rec<RS> r[IT];
-    uint32_t pk[IT];  // digit (9 bits, 0x100 = invalid) | (rank within warp) << 9
-    const uint32_t lt = lanemask_lt();
-#pragma unroll
-    for (int j = 0; j < IT; ++j) {
-        const uint32_t i = uint32_t(warp * IT + j) * 32u + lane;
-        const bool valid = i < tn;
-        if (valid) {
-            r[j] = load_rec_stream<RS>(src, i);
-        } else {
-#pragma unroll
-            for (int q = 0; q < Rec<RS>::kWords; ++q) r[j].w[q] = 0;
-        }
-        const uint32_t d = valid ? scatter_digit<RS, kMap>(r[j], p, ks, map) : 0x100u;
-        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
-        const int leader = __ffs(peers) - 1;
-        uint32_t old = 0;
-        if (lane == leader && valid) {
-            old = s_wcnt[warp][d];
-            s_wcnt[warp][d] = old + __popc(peers);
-        }
-        old = __shfl_sync(0xFFFFFFFFu, old, leader);
-        __syncwarp();
-        pk[j] = d | ((old + __popc(peers & lt)) << 9);
+    if (threadIdx.x == 0) {
+        mbar_init(&s_full[0], 1);
+        mbar_init(&s_full[1], 1);
+        mbar_init(&s_empty[0], 1);
+        mbar_init(&s_empty[1], 1);
+        fence_mbar_init();
     }
     __syncthreads();
 
-    // 3: per-digit tile totals, warp-exclusive offsets, tile-local starts
-    uint32_t tcount = 0;
-    if (threadIdx.x < kRadix) {
-        const int d = threadIdx.x;
-#pragma unroll
-        for (int w = 0; w < W; ++w) {
-            const uint32_t c = s_wcnt[w][d];
-            s_wcnt[w][d] = tcount;
-            tcount += c;
-        }
-    }
-    // 4a: publish aggregate (or inclusive, for a segment's first tile) early
-    unsigned long long* my_status = status + uint64_t(tile) * kRadix;
-    if (threadIdx.x < kRadix)
-        st_volatile_u64(my_status + threadIdx.x, (k == 0 ? kFlagIncl : kFlagAgg) | tcount);
-    uint32_t total;
-    const uint32_t lstart = scan256_exclusive(threadIdx.x < kRadix ? tcount : 0u, s_scan, &total);
-    if (threadIdx.x < kRadix) s_lstart[threadIdx.x] = lstart;
-    __syncthreads();
-
-    // 5a: stage records in digit order
-#pragma unroll
-    for (int j = 0; j < IT; ++j) {
-        const uint32_t d = pk[j] & 0x1FFu;
-        if (d < 256u) {
-            const uint32_t slot = s_lstart[d] + s_wcnt[warp][d] + (pk[j] >> 9);
-            st_smem_rec<RS>(s_recs, slot, r[j]);
-            s_dig[slot] = uint8_t(d);
-        }
-    }
-
-    // 4b: look-back within the segment (one thread per digit)
-    if (threadIdx.x < kRadix) {
-        const int d = threadIdx.x;
-        uint64_t excl = 0;
-        if (k > 0) {
-            int64_t t = int64_t(tile) - 1;
-            while (true) {
-                const uint64_t v = ld_volatile_u64(status + uint64_t(t) * kRadix + d);
-                const uint64_t flag = v & ~kValueMask;
-                if (flag == 0) continue;  // predecessor not published yet
-                excl += v & kValueMask;
-                if (flag == kFlagIncl) break;
-                --t;
+    if (warp == W) {  // ------------------------------------------------ producer
+        if (lane != 0) return;
+        for (uint32_t it = 0;; ++it) {
+            const int b = it & 1;
+            if (it >= 2) mbar_wait(&s_empty[b], ((it >> 1) - 1) & 1u);
+            TileInfo ti;
+            ti.tile = atomicAdd(&ctr->tile_ticket, 1u);
+            uint32_t body = 0;
+            if (ti.tile < n_tiles) {
+                ti.seg = tile_seg[ti.tile];
+                const Seg g = segs[ti.seg];
+                ti.k = uint64_t(ti.tile) - stile_base[ti.seg];
+                ti.seg_start = g.start;
+                ti.gstart = g.start + ti.k * C::kTile;
+                ti.tn = uint32_t(min(uint64_t(C::kTile), g.size - ti.k * C::kTile));
+                ti.p = g.p;
+                ti.parity = g.parity;
+                const uint8_t* gsrc = (g.parity ? tmp : data) + ti.gstart * RS;
+                const uint32_t bytes = ti.tn * RS;
+                const uint32_t head = uint32_t(reinterpret_cast<uintptr_t>(gsrc) & 15u);  // 0 or 8
+                const uint32_t hb = head ? min(8u, bytes) : 0u;
+                body = (bytes - hb) & ~15u;
+                const uint32_t tail = bytes - hb - body;  // 0 or 8
+                ti.head = head;
+                uint8_t* sb = buf0 + b * C::kBufBytes + head;
+                if (hb) *reinterpret_cast<uint2*>(sb) = *reinterpret_cast<const uint2*>(gsrc);
+                if (tail)
+                    *reinterpret_cast<uint2*>(sb + hb + body) =
+                        *reinterpret_cast<const uint2*>(gsrc + hb + body);
+                fence_proxy_async_smem();
+                s_info[b] = ti;
+                mbar_arrive_expect_tx(&s_full[b], body);
+                if (body) tma_load_1d(sb + hb, gsrc + hb, body, &s_full[b]);
+            } else {
+                s_info[b] = ti;
+                mbar_arrive_expect_tx(&s_full[b], 0);
+                return;
             }
-            st_volatile_u64(my_status + d, kFlagIncl | (excl + tcount));
         }
-        s_gdelta[d] = (long long)(g.start + seg_off[uint64_t(s) * kRadix + d] + excl) -
-                      (long long)s_lstart[d];
     }
-    __syncthreads();
 
-    // 5b: coalesced write-out of the staged tile
+    // ------------------------------------------------------------ consumers
+    const uint32_t lt = lanemask_lt();
+    for (uint32_t it = 0;; ++it) {
+        const int b = it & 1;
+        // own warp's counter row (only this warp touches it while ranking)
 #pragma unroll
-    for (int j = 0; j < IT; ++j) {
-        const uint32_t slot = uint32_t(j) * T + threadIdx.x;
-        if (slot < tn) {
-            const Rec<RS> v = ld_smem_rec<RS>(s_recs, slot);
-            const uint32_t d = s_dig[slot];
-            store_rec<RS>(dst, uint64_t(s_gdelta[d] + (long long)slot), v);
+        for (int q = 0; q < kRadix / 32; ++q) s_wcnt[warp][q * 32 + lane] = 0;
+        mbar_wait(&s_full[b], (it >> 1) & 1u);
+        const TileInfo ti = s_info[b];
+        if (ti.tile >= n_tiles) break;
+        const unsigned long long my_off =
+            threadIdx.x < kRadix ? seg_off[uint64_t(ti.seg) * kRadix + threadIdx.x] : 0ull;
+        const uint8_t* tile = buf0 + b * C::kBufBytes + ti.head;
+        const uint32_t tn = ti.tn, p = ti.p;
+        __syncwarp();
+
+        // 1: warp multisplit rank (ballot peers, warp-private counters)
+        uint32_t pk[IT];  // digit | rank << 9 ; 0x100 = invalid
+#pragma unroll
+        for (int j = 0; j < IT; ++j) {
+            const uint32_t i = uint32_t(warp * IT + j) * 32u + lane;
+            const bool valid = i < tn;
+            const uint32_t d =
+                valid ? scatter_digit_smem<RS, kMap>(tile + size_t(i) * RS, p, ks, map) : 0u;
+            const uint32_t peers = match_digit8(d, valid);
+            const uint32_t before = valid ? s_wcnt[warp][d] : 0u;
+            __syncwarp();
+            if (valid && uint32_t(lane) == 31u - __clz(peers)) s_wcnt[warp][d] = before + __popc(peers);
+            __syncwarp();
+            pk[j] = valid ? (d | ((before + __popc(peers & lt)) << 9)) : 0x100u;
         }
+        bar_sync_named(1, T);
+
+        // 2: per-digit tile totals, warp-exclusive offsets, early aggregate
+        uint32_t tcount = 0;
+        {
+            const int d = threadIdx.x;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const uint32_t c = s_wcnt[w][d];
+                s_wcnt[w][d] = tcount;
+                tcount += c;
+            }
+            st_volatile_u64(status + uint64_t(ti.tile) * kRadix + d,
+                            (ti.k == 0 ? kFlagIncl : kFlagAgg) | tcount);
+        }
+        uint32_t total;
+        const uint32_t lstart = scan256_exclusive(tcount, s_scan, &total);
+        s_lstart[threadIdx.x] = lstart;
+        bar_sync_named(1, T);
+
+        // 3: slot map (digit order) in shared memory
+#pragma unroll
+        for (int j = 0; j < IT; ++j) {
+            const uint32_t d = pk[j] & 0x1FFu;
+            if (d < 256u) {
+                const uint32_t slot = s_lstart[d] + s_wcnt[warp][d] + (pk[j] >> 9);
+                s_map[slot] = uint16_t(uint32_t(warp * IT + j) * 32u + lane);
+                s_dig[slot] = uint8_t(d);
+            }
+        }
+
+        // 4: decoupled look-back within the segment (one thread per digit),
+        // kLook predecessor words per round.
+        {
+            constexpr int kLook = 4;
+            const int d = threadIdx.x;
+            uint64_t excl = 0;
+            if (ti.k > 0) {
+                const int64_t first = int64_t(ti.tile) - int64_t(ti.k);
+                int64_t t = int64_t(ti.tile) - 1;
+                while (true) {
+                    unsigned long long v[kLook];
+#pragma unroll
+                    for (int q = 0; q < kLook; ++q)
+                        v[q] = (t - q >= first) ? ld_volatile_u64(status + uint64_t(t - q) * kRadix + d)
+                                                : 0ull;
+                    bool done = false;
+                    int used = 0;
+#pragma unroll
+                    for (int q = 0; q < kLook; ++q) {
+                        if (done || used != q || t - q < first) continue;
+                        const uint64_t flag = v[q] & ~kValueMask;
+                        if (flag == 0) continue;
+                        excl += v[q] & kValueMask;
+                        ++used;
+                        if (flag == kFlagIncl) done = true;
+                    }
+                    if (done) break;
+                    t -= used;
+                }
+                st_volatile_u64(status + uint64_t(ti.tile) * kRadix + d, kFlagIncl | (excl + tcount));
+            }
+            s_gdelta[d] = (long long)(ti.seg_start + my_off + excl) - (long long)s_lstart[d];
+        }
+        bar_sync_named(1, T);
+
+        // 5: write-out in digit order: consecutive slots of a digit go to
+        // consecutive destinations (coalesced vector stores)
+        uint8_t* dst = ti.parity ? data : tmp;
+#pragma unroll 4
+        for (int j = 0; j < IT; ++j) {
+            const uint32_t slot = uint32_t(j) * T + threadIdx.x;
+            if (slot < tn) {
+                const Rec<RS> v = ld_smem_rec<RS>(tile, s_map[slot]);
+                store_rec<RS>(dst, uint64_t(s_gdelta[s_dig[slot]] + (long long)slot), v);
+            }
+        }
+        bar_sync_named(1, T);  // buffer b, map and counters free for reuse
+        if (threadIdx.x == 0) mbar_arrive(&s_empty[b]);
     }
 }
 

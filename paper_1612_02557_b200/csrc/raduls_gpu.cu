@@ -188,7 +188,26 @@ void set_attrs(Workspace& ws) {
     if (ws.attrs_set[RS]) return;
     RG_CHECK(cudaFuncSetAttribute(k_local_sort<RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(LocalCfg<RS>::kSmem)));
+    RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(ScatterCfg<RS>::kSmem)));
+    RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(ScatterCfg<RS>::kSmem)));
     ws.attrs_set[RS] = true;
+}
+
+// Persistent scatter launch: at most two CTAs per SM, never more CTAs than tiles.
+template <int RS, bool kMap>
+void launch_scatter(uint8_t* data, uint8_t* tmp, const Seg* segs, const unsigned long long* seg_off,
+                    const unsigned long long* stile_base, const uint32_t* tile_seg,
+                    unsigned long long* status, LevelCounters* ctr, uint32_t n_tiles, uint32_t ks,
+                    const uint8_t* map, cudaStream_t st) {
+    int dev = 0, sms = 148;
+    RG_CHECK(cudaGetDevice(&dev));
+    RG_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const uint32_t grid = std::min<uint32_t>(n_tiles, uint32_t(sms) * 2);
+    k_scatter<RS, kMap><<<grid, ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>::kSmem, st>>>(
+        data, tmp, segs, seg_off, stile_base, tile_seg, status, ctr, n_tiles, ks, map);
+    RG_LAUNCH_CHECK();
 }
 
 // Launch the local sort over `ngroups` groups already in ws.groups.
@@ -297,10 +316,8 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         if (h.n_scatter_tiles) {
             RG_CHECK(cudaMemsetAsync(ws.status.p, 0,
                                      size_t(h.n_scatter_tiles) * kRadix * sizeof(unsigned long long), st));
-            k_scatter<RS><<<h.n_scatter_tiles, ScatterCfg<RS>::kThreads, 0, st>>>(
-                data, tmp, ws.segs[cur].p, ws.seg_hist[cur].p, ws.stile_base.p, ws.tile_seg.p,
-                ws.status.p, c);
-            RG_LAUNCH_CHECK();
+            launch_scatter<RS, false>(data, tmp, ws.segs[cur].p, ws.seg_hist[cur].p, ws.stile_base.p,
+                                      ws.tile_seg.p, ws.status.p, c, h.n_scatter_tiles, ks, nullptr, st);
             stats.scatter_launches++;
         }
         launch_local<RS>(ws, data, tmp, h.n_groups, ks, c, st);
@@ -487,10 +504,10 @@ int raduls_gpu_split(const void* d_src, void* d_dst, uint64_t n, uint32_t rs,
             RG_CHECK(cudaMemsetAsync(ws.status.p, 0, size_t(tiles) * kRadix * sizeof(unsigned long long), st));
             RG_CHECK(cudaMemsetAsync(ws.ctr.p, 0, sizeof(LevelCounters), st));
             // parity 0: src = "data" slot, dst = "tmp" slot
-            k_scatter<RSC><<<tiles, ScatterCfg<RSC>::kThreads, 0, st>>>(
-                src, static_cast<uint8_t*>(d_dst), ws.segs[0].p, ws.seg_hist[0].p, ws.stile_base.p,
-                ws.tile_seg.p, ws.status.p, ws.ctr.p);
-            RG_LAUNCH_CHECK();
+            set_attrs<RSC>(ws);
+            launch_scatter<RSC, false>(src, static_cast<uint8_t*>(d_dst), ws.segs[0].p, ws.seg_hist[0].p,
+                                       ws.stile_base.p, ws.tile_seg.p, ws.status.p, ws.ctr.p, tiles, 0,
+                                       nullptr, st);
             RG_CHECK(cudaStreamSynchronize(st));
         });
     });
@@ -656,10 +673,10 @@ int raduls_gpu_partition(const void* d_src, void* d_dst, uint64_t n, uint32_t rs
             RG_CHECK(cudaMemsetAsync(ws.status.p, 0, size_t(tiles) * kRadix * sizeof(unsigned long long), st));
             RG_CHECK(cudaMemsetAsync(ws.ctr.p, 0, sizeof(LevelCounters), st));
             uint8_t* src = const_cast<uint8_t*>(static_cast<const uint8_t*>(d_src));
-            k_scatter<RSC, true><<<tiles, ScatterCfg<RSC>::kThreads, 0, st>>>(
-                src, static_cast<uint8_t*>(d_dst), ws.segs[0].p, ws.seg_hist[0].p, ws.stile_base.p,
-                ws.tile_seg.p, ws.status.p, ws.ctr.p, ks, ws.map8.p);
-            RG_LAUNCH_CHECK();
+            set_attrs<RSC>(ws);
+            launch_scatter<RSC, true>(src, static_cast<uint8_t*>(d_dst), ws.segs[0].p, ws.seg_hist[0].p,
+                                      ws.stile_base.p, ws.tile_seg.p, ws.status.p, ws.ctr.p, tiles, ks,
+                                      ws.map8.p, st);
             RG_CHECK(cudaStreamSynchronize(st));
         });
     });
