@@ -249,8 +249,11 @@ struct Seg {
     uint64_t size;
     uint32_t p;
     uint32_t parity;
-    uint64_t htile_base;  // first histogram tile of this segment (when its histogram is pending)
+    uint32_t tile_base;  // first tile (histogram + scatter partition) of this segment
+    uint32_t action;     // set by the planner: kActScatter when this level splits it
 };
+
+constexpr uint32_t kActScatter = 2;
 
 // A run of one or more complete, adjacent small segments sorted by one CTA;
 // all its records share key bytes [0, p).
@@ -271,18 +274,17 @@ struct CopyRange {
 
 // Per-level counters (device, zeroed before the planner runs).
 struct LevelCounters {
-    uint32_t n_scatter_tiles;  // tiles of this level's scatter
     uint32_t n_groups;         // local-sort groups emitted
     uint32_t n_copy;           // copy-back ranges emitted
-    uint32_t n_next;           // next-level big segments
-    uint32_t n_next_htiles;    // histogram tiles of next-level segments
-    uint32_t n_scatter_segs;   // segments scattered this level (stats)
-    uint32_t tile_ticket;      // dynamic tile id dispenser for k_scatter
-    uint32_t pad;
-    unsigned long long moved_scatter;  // records moved by this level's scatter
-    unsigned long long moved_local;    // records moved by local sorts
-    unsigned long long moved_copy;     // records moved by copy-back
-    unsigned long long fallback_groups;  // groups whose window sort needed the full-key fallback
+    uint32_t n_next;           // next-level segments
+    uint32_t n_next_tiles;     // tiles of next-level segments
+    uint32_t n_scatter_segs;   // segments scattered this level
+    uint32_t scan_ticket;      // dynamic chunk id dispenser for k_tile_scan
+    unsigned long long moved_scatter;    // records moved by this level's scatter
+    unsigned long long moved_local;      // records moved by local sorts
+    unsigned long long moved_copy;       // records moved by copy-back
+    unsigned long long fallback_groups;  // local-sort groups that needed the LSD fallback
+    unsigned long long hist_records;     // records read by this level's tile histogram
 };
 
 // Decoupled look-back status word: [63:62] flag, [61:0] value.

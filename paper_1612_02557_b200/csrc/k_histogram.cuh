@@ -1,18 +1,20 @@
 // (a) Digit histogramming in shared memory with warp-aggregated atomics, and
 // (e) constant-digit detection.
 //
-// Reference: build_histogram (P/include/raduls/kernels.hpp:71-77) and the count
-// loop of buffered_radix_split (kernels.hpp:212-218). The reference counts one
-// digit per split; here one read of the whole array counts the first eight key
-// bytes at once and reduces the bitwise AND / OR of every key word, so a key
-// byte is constant over the array iff its AND byte equals its OR byte — the
-// reference has no counterpart for that skip.
+// Reference: build_histogram (P/include/raduls/kernels.hpp:71-77) and the
+// count loop of buffered_radix_split (kernels.hpp:212-218), which counts one
+// digit per chunk into chunk_hist[c] so that compute_offsets (:198-209) can
+// give every (chunk, digit) a disjoint destination range. Here a "chunk" is a
+// scatter tile: k_tile_hist writes the 256 digit counts of every tile (the
+// reference's chunk_hist) plus the AND/OR of every record word over the
+// segment — a key byte is constant over a segment iff its AND byte equals its
+// OR byte, which lets the planner skip it (no reference counterpart).
 //
-// Warp aggregation: each warp first reduces AND/OR of its 32 records' key word
-// with REDUX (__reduce_and_sync/__reduce_or_sync). For a byte that is constant
-// across the warp one lane adds the warp's count to the shared bin instead of
-// 32 lanes colliding on the same shared-memory address (C3's three all-zero
-// leading bytes would otherwise serialise every atomic 32 ways).
+// Warp aggregation: each warp reduces AND/OR of the 32-bit word holding the
+// digit with REDUX (__reduce_and_sync/__reduce_or_sync); for a digit that is
+// constant across the warp one lane adds the warp's count instead of 32 lanes
+// colliding on one shared-memory counter (C3's skewed byte and constant
+// bytes would otherwise serialise the atomics 32 ways).
 #pragma once
 
 #include "common.cuh"
@@ -31,133 +33,101 @@ __device__ __forceinline__ void warp_hist_add(uint32_t* h, uint32_t b, bool vali
     }
 }
 
-// Whole-array histograms of record bytes 0..nb-1 (nb = min(ks, 8)) plus the
-// AND/OR of every 64-bit record word. hist: [8][256] u64, andor: [2*4] u64
-// (and[w] at 2w, or[w] at 2w+1). Both must be initialised by the caller
-// (hist 0, and ~0, or 0).
+// AND/OR of every 64-bit record word over a sample of the array (stride
+// sampling): the first key byte that varies in the sample varies globally, so
+// it is the level-0 digit unless a more significant byte varies only outside
+// the sample (then the host re-histograms; the result is never wrong).
 template <int RS>
-__global__ void __launch_bounds__(256) k_histo_all(const uint8_t* __restrict__ data, uint64_t n,
-                                                   uint32_t nb,
-                                                   unsigned long long* __restrict__ hist,
-                                                   unsigned long long* __restrict__ andor) {
+__global__ void __launch_bounds__(256) k_sample_andor(const uint8_t* __restrict__ data, uint64_t n,
+                                                      uint64_t stride, uint32_t samples,
+                                                      unsigned long long* __restrict__ andor) {
     constexpr int KW = RS / 8;
-    __shared__ uint32_t sh[8][kRadix];
-    __shared__ unsigned long long s_and[8][KW], s_or[8][KW];
-    for (int i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) (&sh[0][0])[i] = 0;
-    __syncthreads();
-
     uint64_t a[KW], o[KW];
 #pragma unroll
     for (int w = 0; w < KW; ++w) a[w] = ~0ull, o[w] = 0ull;
-
-    constexpr int U = 4;  // records in flight per thread
-    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * U;
-    for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x * U; base < n; base += stride) {
-        Rec<RS> r[U];
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < samples; s += gridDim.x * blockDim.x) {
+        const uint64_t i = min(n - 1, uint64_t(s) * stride);
+        const Rec<RS> r = load_rec<RS>(data, i);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint64_t i = base + uint64_t(u) * blockDim.x + threadIdx.x;
-            if (i < n) {
-                r[u] = load_rec_stream<RS>(data, i);
-            } else {
-#pragma unroll
-                for (int k = 0; k < Rec<RS>::kWords; ++k) r[u].w[k] = 0;
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint64_t i = base + uint64_t(u) * blockDim.x + threadIdx.x;
-            const bool valid = i < n;
-            const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
-            const uint32_t lo = r[u].w[0], hi = r[u].w[1];
-            const uint32_t al = __reduce_and_sync(0xFFFFFFFFu, valid ? lo : ~0u);
-            const uint32_t ol = __reduce_or_sync(0xFFFFFFFFu, valid ? lo : 0u);
-            const uint32_t ah = __reduce_and_sync(0xFFFFFFFFu, valid ? hi : ~0u);
-            const uint32_t oh = __reduce_or_sync(0xFFFFFFFFu, valid ? hi : 0u);
-            for (uint32_t b = 0; b < nb; ++b) {  // nb is uniform
-                const uint32_t word = b < 4 ? lo : hi;
-                const uint32_t sh_ = (b & 3u) * 8u;
-                warp_hist_add(sh[b], (word >> sh_) & 0xFFu, valid, b < 4 ? al : ah,
-                              b < 4 ? ol : oh, sh_, nvalid);
-            }
-            if (valid) {
-#pragma unroll
-                for (int w = 0; w < KW; ++w) {
-                    const uint64_t v = rec_word64<RS>(r[u], w);
-                    a[w] &= v;
-                    o[w] |= v;
-                }
-            }
+        for (int w = 0; w < KW; ++w) {
+            const uint64_t v = rec_word64<RS>(r, w);
+            a[w] &= v;
+            o[w] |= v;
         }
     }
-    // block reduce AND/OR
-    const int warp = threadIdx.x >> 5;
 #pragma unroll
     for (int w = 0; w < KW; ++w) {
         for (int off = 16; off; off >>= 1) {
             a[w] &= __shfl_xor_sync(0xFFFFFFFFu, a[w], off);
             o[w] |= __shfl_xor_sync(0xFFFFFFFFu, o[w], off);
         }
-        if (lane_id() == 0) s_and[warp][w] = a[w], s_or[warp][w] = o[w];
-    }
-    __syncthreads();
-    if (threadIdx.x < KW) {
-        unsigned long long ra = ~0ull, ro = 0ull;
-        for (int k = 0; k < int(blockDim.x >> 5); ++k) ra &= s_and[k][threadIdx.x], ro |= s_or[k][threadIdx.x];
-        atomicAnd(&andor[2 * threadIdx.x], ra);
-        atomicOr(&andor[2 * threadIdx.x + 1], ro);
-    }
-    for (uint32_t i = threadIdx.x; i < nb * kRadix; i += blockDim.x) {
-        const uint32_t c = (&sh[0][0])[i];
-        if (c) atomicAdd(&hist[i], (unsigned long long)c);
+        if (lane_id() == 0) {
+            atomicAnd(&andor[2 * w], a[w]);
+            atomicOr(&andor[2 * w + 1], o[w]);
+        }
     }
 }
 
-// Per-segment histogram of record byte segs[s].p, plus the AND/OR of every
-// record word over the segment. One CTA per histogram tile of kHistTile
-// records; tile -> segment through htile_seg. seg_hist: [nseg][256] u64,
-// seg_andor: [nseg][8] u64 (and at 2w, or at 2w+1); both pre-initialised.
-constexpr int kHistThreads = 256;
-constexpr int kHistItems = 16;
-constexpr int kHistTile = kHistThreads * kHistItems;
-
-template <int RS>
-__global__ void __launch_bounds__(kHistThreads) k_seg_hist(
-    const uint8_t* __restrict__ data, const uint8_t* __restrict__ tmp, const Seg* __restrict__ segs,
-    const uint32_t* __restrict__ htile_seg, unsigned long long* __restrict__ seg_hist,
-    unsigned long long* __restrict__ seg_andor) {
+// Per-tile digit counts of byte segs[s].p for every tile of every segment of
+// the level, plus AND/OR of every record word per segment. One CTA per tile
+// (the scatter's tile partition: kTile records, tile -> segment through
+// tile_seg, tile index inside the segment = tile - segs[s].tile_base).
+// tile_cnt: [ntiles][256] u16. seg_andor: [nseg][8] u64 (and at 2w, or at
+// 2w+1), pre-initialised.
+// kMap: the digit is the destination rank of the record's 16-bit key prefix
+// at bytes (p, p+1) through a 65536-entry map (multi-GPU partition).
+template <int RS, int kTile, bool kMap = false>
+__global__ void __launch_bounds__(256) k_tile_hist(const uint8_t* __restrict__ data,
+                                                   const uint8_t* __restrict__ tmp,
+                                                   const Seg* __restrict__ segs,
+                                                   const uint32_t* __restrict__ tile_seg,
+                                                   uint16_t* __restrict__ tile_cnt,
+                                                   unsigned long long* __restrict__ seg_andor,
+                                                   LevelCounters* __restrict__ ctr, uint32_t ks = 0,
+                                                   const uint8_t* __restrict__ map = nullptr) {
     constexpr int KW = RS / 8;
+    constexpr int IT = kTile / 256;
     __shared__ uint32_t sh[kRadix];
-    __shared__ unsigned long long s_and[kHistThreads / 32][KW], s_or[kHistThreads / 32][KW];
+    __shared__ unsigned long long s_and[8][KW], s_or[8][KW];
     sh[threadIdx.x] = 0;
-    const uint32_t s = htile_seg[blockIdx.x];
+    const uint32_t tile = blockIdx.x;
+    const uint32_t s = tile_seg[tile];
     const Seg g = segs[s];
-    const uint64_t k = uint64_t(blockIdx.x) - g.htile_base;
-    const uint8_t* src = (g.parity ? tmp : data) + g.start * RS;
-    const uint64_t t0 = k * kHistTile;
-    const uint64_t tn = min(uint64_t(kHistTile), g.size - t0);
+    const uint64_t k = uint64_t(tile) - g.tile_base;
+    const uint8_t* src = (g.parity ? tmp : data) + (g.start + k * kTile) * RS;
+    const uint32_t tn = uint32_t(min(uint64_t(kTile), g.size - k * kTile));
     const uint32_t p = g.p;
+    Rec<RS> r[IT];
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {  // all loads in flight
+        const uint32_t i = uint32_t(j) * 256u + threadIdx.x;
+        if (i < tn) {
+            r[j] = load_rec_stream<RS>(src, i);
+        } else {
+#pragma unroll
+            for (int q = 0; q < Rec<RS>::kWords; ++q) r[j].w[q] = 0;
+        }
+    }
     __syncthreads();
-
     uint64_t a[KW], o[KW];
 #pragma unroll
     for (int w = 0; w < KW; ++w) a[w] = ~0ull, o[w] = 0ull;
-#pragma unroll 4
-    for (int j = 0; j < kHistItems; ++j) {
-        const uint64_t i = uint64_t(j) * kHistThreads + threadIdx.x;
-        const bool valid = i < tn;
-        Rec<RS> r;
-        if (valid) {
-            r = load_rec_stream<RS>(src, t0 + i);
-        } else {
 #pragma unroll
-            for (int q = 0; q < Rec<RS>::kWords; ++q) r.w[q] = 0;
+    for (int j = 0; j < IT; ++j) {
+        const uint32_t i = uint32_t(j) * 256u + threadIdx.x;
+        const bool valid = i < tn;
+        if constexpr (kMap) {
+            if (valid) {
+                const uint32_t hi = p < ks ? rec_byte<RS>(r[j], p) : 0u;
+                const uint32_t lo = p + 1 < ks ? rec_byte<RS>(r[j], p + 1) : 0u;
+                atomicAdd(&sh[__ldg(map + ((hi << 8) | lo))], 1u);
+            }
+            continue;
         }
         const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
-        // word holding byte p (select chain, p uniform)
-        uint32_t word = r.w[0];
+        uint32_t word = r[j].w[0];
 #pragma unroll
-        for (int q = 1; q < Rec<RS>::kWords; ++q) word = (p >> 2) == uint32_t(q) ? r.w[q] : word;
+        for (int q = 1; q < Rec<RS>::kWords; ++q) word = (p >> 2) == uint32_t(q) ? r[j].w[q] : word;
         const uint32_t wa = __reduce_and_sync(0xFFFFFFFFu, valid ? word : ~0u);
         const uint32_t wo = __reduce_or_sync(0xFFFFFFFFu, valid ? word : 0u);
         const uint32_t shf = (p & 3u) * 8u;
@@ -165,30 +135,32 @@ __global__ void __launch_bounds__(kHistThreads) k_seg_hist(
         if (valid) {
 #pragma unroll
             for (int w = 0; w < KW; ++w) {
-                const uint64_t v = rec_word64<RS>(r, w);
+                const uint64_t v = rec_word64<RS>(r[j], w);
                 a[w] &= v;
                 o[w] |= v;
             }
         }
     }
     const int warp = threadIdx.x >> 5;
+    if constexpr (!kMap) {
 #pragma unroll
-    for (int w = 0; w < KW; ++w) {
-        for (int off = 16; off; off >>= 1) {
-            a[w] &= __shfl_xor_sync(0xFFFFFFFFu, a[w], off);
-            o[w] |= __shfl_xor_sync(0xFFFFFFFFu, o[w], off);
+        for (int w = 0; w < KW; ++w) {
+            for (int off = 16; off; off >>= 1) {
+                a[w] &= __shfl_xor_sync(0xFFFFFFFFu, a[w], off);
+                o[w] |= __shfl_xor_sync(0xFFFFFFFFu, o[w], off);
+            }
+            if (lane_id() == 0) s_and[warp][w] = a[w], s_or[warp][w] = o[w];
         }
-        if (lane_id() == 0) s_and[warp][w] = a[w], s_or[warp][w] = o[w];
     }
     __syncthreads();
-    if (threadIdx.x < KW) {
+    if (!kMap && threadIdx.x < KW) {
         unsigned long long ra = ~0ull, ro = 0ull;
-        for (int q = 0; q < kHistThreads / 32; ++q) ra &= s_and[q][threadIdx.x], ro |= s_or[q][threadIdx.x];
+        for (int q = 0; q < 8; ++q) ra &= s_and[q][threadIdx.x], ro |= s_or[q][threadIdx.x];
         atomicAnd(&seg_andor[uint64_t(s) * 8 + 2 * threadIdx.x], ra);
         atomicOr(&seg_andor[uint64_t(s) * 8 + 2 * threadIdx.x + 1], ro);
     }
-    const uint32_t c = sh[threadIdx.x];
-    if (c) atomicAdd(&seg_hist[uint64_t(s) * kRadix + threadIdx.x], (unsigned long long)c);
+    if (threadIdx.x == 0) atomicAdd(&ctr->hist_records, (unsigned long long)tn);
+    tile_cnt[uint64_t(tile) * kRadix + threadIdx.x] = uint16_t(sh[threadIdx.x]);
 }
 
 }  // namespace rg

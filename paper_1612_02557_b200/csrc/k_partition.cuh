@@ -2,8 +2,8 @@
 // counterpart — the reference is single-address-space). A rank holds N/G
 // records; the 16-bit big-endian key prefix at bytes (pb, pb+1) selects a
 // bucket, a host-built map assigns contiguous bucket ranges to ranks, and the
-// records are split stably into G contiguous send ranges by k_scatter<RS, true>
-// (the same warp-ranked, look-back scatter as the MSD passes).
+// records are split stably into G contiguous send ranges by k_tile_hist /
+// k_tile_scan / k_scatter with kMap = true (the same passes as an MSD level).
 #pragma once
 
 #include "common.cuh"
@@ -32,24 +32,6 @@ __global__ void __launch_bounds__(256) k_prefix_hist(const uint8_t* __restrict__
         if (valid && (threadIdx.x & 31) == uint32_t(__ffs(peers) - 1))
             atomicAdd(&hist[b], (unsigned long long)__popc(peers));
     }
-}
-
-// Per-rank record counts through the bucket -> rank map (u8).
-template <int RS>
-__global__ void __launch_bounds__(256) k_map_hist(const uint8_t* __restrict__ data, uint64_t n,
-                                                  uint32_t ks, uint32_t pb,
-                                                  const uint8_t* __restrict__ map,
-                                                  unsigned long long* __restrict__ counts) {
-    __shared__ uint32_t sh[kRadix];
-    sh[threadIdx.x] = 0;
-    __syncthreads();
-    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-        const uint32_t r = map[prefix16<RS>(load_rec_stream<RS>(data, i), pb, ks)];
-        atomicAdd(&sh[r], 1u);
-    }
-    __syncthreads();
-    if (sh[threadIdx.x]) atomicAdd(&counts[threadIdx.x], (unsigned long long)sh[threadIdx.x]);
 }
 
 __global__ void k_map_to_u8(const uint32_t* __restrict__ in, uint8_t* __restrict__ out,

@@ -1,4 +1,4 @@
-// Device-side pass planner: turns one level's per-segment digit histograms into
+// Device-side pass planner: turns one level's per-segment digit totals into
 // the next level's work lists, without a host round trip per segment.
 //
 // Reference: child_bins (P/include/raduls/kernels.hpp:82-94) — children tile
@@ -17,26 +17,22 @@
 #pragma once
 
 #include "common.cuh"
-#include "k_histogram.cuh"
 #include "k_local_sort.cuh"
 
 namespace rg {
 
 struct PlanArgs {
-    const Seg* segs;
-    unsigned long long* seg_hist;        // [nseg][256]: in counts, out exclusive offsets
+    Seg* segs;                           // this level; action written here
+    unsigned long long* seg_tot;         // [nseg][256]: in digit totals, out exclusive digit bases
     const unsigned long long* seg_andor;  // [nseg][8]
-    unsigned long long* stile_base;      // [nseg]
-    uint32_t* tile_seg;                  // scatter tile -> segment
     Group* groups;
     CopyRange* copies;
     Seg* next;
-    unsigned long long* next_hist;
     unsigned long long* next_andor;
-    uint32_t* next_htile_seg;
+    uint32_t* next_tile_seg;
     LevelCounters* ctr;
     uint32_t ks;
-    uint32_t tile;      // scatter tile (records)
+    uint32_t tile;       // tile partition (records)
     uint32_t cap_local;  // local-sort group capacity (records)
 };
 
@@ -50,7 +46,7 @@ __global__ void k_init_andor(unsigned long long* andor, uint32_t rows) {
     if (i < rows * 8) andor[i] = (i & 1) ? 0ull : ~0ull;
 }
 
-// Emit copy-back ranges covering [start, start+size).
+// Emit copy-back ranges covering [start, start+size) (whole block).
 __device__ void emit_copies(const PlanArgs& A, uint64_t start, uint64_t size, uint32_t* s_base) {
     const uint64_t nchunks = (size + kCopyTile - 1) / kCopyTile;
     if (threadIdx.x == 0) {
@@ -67,45 +63,52 @@ __device__ void emit_copies(const PlanArgs& A, uint64_t start, uint64_t size, ui
     }
 }
 
-// Allocate one next-level segment (called by a single thread); *htile_base
-// receives its first histogram tile.
+// Allocate one next-level segment and its tiles (single thread).
 __device__ uint32_t emit_next(const PlanArgs& A, uint64_t start, uint64_t size, uint32_t p,
-                              uint32_t parity, uint32_t* htile_base) {
+                              uint32_t parity, uint32_t* tile_base) {
     const uint32_t idx = atomicAdd(&A.ctr->n_next, 1u);
-    const uint32_t nt = uint32_t((size + kHistTile - 1) / kHistTile);
-    const uint32_t hb = atomicAdd(&A.ctr->n_next_htiles, nt);
+    const uint32_t nt = uint32_t((size + A.tile - 1) / A.tile);
+    const uint32_t tb = atomicAdd(&A.ctr->n_next_tiles, nt);
     Seg s;
     s.start = start;
     s.size = size;
     s.p = p;
     s.parity = parity;
-    s.htile_base = hb;
+    s.tile_base = tb;
+    s.action = 0;
     A.next[idx] = s;
-    *htile_base = hb;
+    *tile_base = tb;
     return idx;
+}
+
+// Block-cooperative initialisation of a next-level segment's tile map and AND/OR.
+__device__ __forceinline__ void init_next(const PlanArgs& A, uint32_t idx, uint32_t tb, uint64_t size) {
+    const uint32_t nt = uint32_t((size + A.tile - 1) / A.tile);
+    for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x) A.next_tile_seg[tb + t] = idx;
+    if (threadIdx.x < 8) A.next_andor[uint64_t(idx) * 8 + threadIdx.x] = (threadIdx.x & 1) ? 0ull : ~0ull;
 }
 
 __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
     __shared__ unsigned long long s_cnt[kRadix], s_off[kRadix];
     __shared__ unsigned long long s_wsum[8];
-    __shared__ uint32_t s_action, s_pnext, s_base, s_ngroups, s_hb0;
-    __shared__ uint32_t s_next_idx[kRadix], s_next_hb[kRadix];
+    __shared__ uint32_t s_action, s_pnext, s_base, s_ngroups, s_tb0;
+    __shared__ uint32_t s_next_idx[kRadix], s_next_tb[kRadix];
     __shared__ uint64_t s_gstart[kRadix];
     __shared__ uint32_t s_gsize[kRadix];
     const uint32_t s = blockIdx.x;
     const Seg g = A.segs[s];
-    const unsigned long long* ao = A.seg_andor + uint64_t(s) * 8;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    if (tid == 0) {
-        uint32_t pn = A.ks;
-        for (uint32_t b = g.p; b < A.ks; ++b)
-            if (andor_byte_varies(ao, b)) {
-                pn = b;
-                break;
-            }
-        s_pnext = pn;
-        s_action = pn >= A.ks ? 0u : (pn > g.p ? 1u : 2u);
+    if (tid < 32) {  // first varying key byte >= p (AND/OR of the segment)
+        const unsigned long long* ao = A.seg_andor + uint64_t(s) * 8;
+        const uint32_t b = g.p + lane;
+        const bool varies = b < A.ks && andor_byte_varies(ao, b);
+        const uint32_t m = __ballot_sync(0xFFFFFFFFu, varies);
+        if (lane == 0) {
+            const uint32_t pn = m ? g.p + __ffs(m) - 1 : A.ks;
+            s_pnext = pn;
+            s_action = pn >= A.ks ? 0u : (pn > g.p ? 1u : 2u);
+        }
     }
     __syncthreads();
     const uint32_t action = s_action;
@@ -114,19 +117,15 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
         return;
     }
     if (action == 1) {  // (e) constant byte p: skip it without moving a record
-        if (tid == 0) s_base = emit_next(A, g.start, g.size, s_pnext, g.parity, &s_hb0);
+        if (tid == 0) s_base = emit_next(A, g.start, g.size, s_pnext, g.parity, &s_tb0);
         __syncthreads();
-        const uint32_t idx = s_base;
-        const uint32_t nt = uint32_t((g.size + kHistTile - 1) / kHistTile);
-        for (uint32_t t = tid; t < nt; t += blockDim.x) A.next_htile_seg[s_hb0 + t] = idx;
-        A.next_hist[uint64_t(idx) * kRadix + tid] = 0ull;
-        if (tid < 8) A.next_andor[uint64_t(idx) * 8 + tid] = (tid & 1) ? 0ull : ~0ull;
+        init_next(A, s_base, s_tb0, g.size);
         return;
     }
 
-    // action 2: scatter on byte p. Exclusive digit offsets (u64 block scan).
-    unsigned long long* hist = A.seg_hist + uint64_t(s) * kRadix;
-    const unsigned long long c = hist[tid];
+    // action 2: scatter on byte p. Exclusive digit bases (u64 block scan).
+    unsigned long long* tot = A.seg_tot + uint64_t(s) * kRadix;
+    const unsigned long long c = tot[tid];
     unsigned long long x = c;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -138,25 +137,17 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
     unsigned long long wbase = 0;
     for (int k = 0; k < warp; ++k) wbase += s_wsum[k];
     const unsigned long long off = wbase + x - c;
-    hist[tid] = off;
+    tot[tid] = off;
     s_cnt[tid] = c;
     s_off[tid] = off;
     if (tid == 0) {
-        const uint32_t nt = uint32_t((g.size + A.tile - 1) / A.tile);
-        s_base = atomicAdd(&A.ctr->n_scatter_tiles, nt);
-        A.stile_base[s] = s_base;
+        A.segs[s].action = kActScatter;
         atomicAdd(&A.ctr->n_scatter_segs, 1u);
         atomicAdd(&A.ctr->moved_scatter, (unsigned long long)g.size);
     }
     __syncthreads();
-    {
-        const uint32_t nt = uint32_t((g.size + A.tile - 1) / A.tile);
-        const uint32_t tb = s_base;
-        for (uint32_t t = tid; t < nt; t += blockDim.x) A.tile_seg[tb + t] = s;
-    }
     const uint32_t cp = 1u - g.parity;
     if (g.p + 1 >= A.ks) {  // last key byte: every child is final after this split
-        __syncthreads();
         if (cp) emit_copies(A, g.start, g.size, &s_base);
         return;
     }
@@ -164,7 +155,7 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
     const unsigned long long cs = s_cnt[tid];
     s_next_idx[tid] = 0xFFFFFFFFu;
     if (cs > A.cap_local)
-        s_next_idx[tid] = emit_next(A, g.start + s_off[tid], cs, g.p + 1, cp, &s_next_hb[tid]);
+        s_next_idx[tid] = emit_next(A, g.start + s_off[tid], cs, g.p + 1, cp, &s_next_tb[tid]);
     // small children -> greedy groups (thread 0, digit order)
     if (tid == 0) {
         uint32_t ng = 0;
@@ -195,15 +186,9 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
         gr.pad = 0;
         A.groups[s_base + tid] = gr;
     }
-    // initialise the next-level segments emitted by this block
     for (int d = 0; d < kRadix; ++d) {
         const uint32_t idx = s_next_idx[d];
-        if (idx == 0xFFFFFFFFu) continue;
-        const uint32_t nt = uint32_t((s_cnt[d] + kHistTile - 1) / kHistTile);
-        const uint32_t hb = s_next_hb[d];
-        for (uint32_t t = tid; t < nt; t += blockDim.x) A.next_htile_seg[hb + t] = idx;
-        A.next_hist[uint64_t(idx) * kRadix + tid] = 0ull;
-        if (tid < 8) A.next_andor[uint64_t(idx) * 8 + tid] = (tid & 1) ? 0ull : ~0ull;
+        if (idx != 0xFFFFFFFFu) init_next(A, idx, s_next_tb[d], s_cnt[d]);
     }
 }
 

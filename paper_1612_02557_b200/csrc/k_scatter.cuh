@@ -1,29 +1,26 @@
-// (b) decoupled-lookback exclusive scan of bin offsets + (c) warp-ranked,
-// shared-memory-staged scatter with coalesced vector stores.
+// (c) Scatter pass: warp-ranked, shared-memory-staged, coalesced vector stores.
 //
-// Reference: buffered_radix_split (P/include/raduls/kernels.hpp:175-264) —
-// chunk histograms (:212-218), digit-major/chunk-minor offsets computed by one
-// thread behind a std::barrier (:198-209), then 256 per-thread write-combining
-// lanes flushed with SSE2 streaming stores (:221-245, :134-151). The result is
+// Reference: the scatter loop of buffered_radix_split
+// (P/include/raduls/kernels.hpp:221-245): records are copied into one of 256
+// per-thread write-combining lanes by digit and every full lane is flushed as
+// one contiguous block with SSE2 streaming stores (flush_block, :134-151), at
+// destinations fixed beforehand by compute_offsets (:198-209). The result is
 // the stable split of radix_split (kernels.hpp:157-167).
 //
-// B200 design (one CTA per tile of kTile records, tiles claimed through a
-// dynamic ticket so every predecessor of a tile is already running):
-//   1. coalesced vector loads of the tile (warp-striped: warp w owns a
-//      contiguous run of 32*ITEMS records, lane-interleaved);
-//   2. warp multisplit ranking with __match_any_sync: each lane learns how many
-//      earlier lanes of its warp (in input order) share its digit;
-//   3. per-warp counts -> per-digit tile counts and tile-local exclusive
-//      offsets (digit-major, warp-minor: keeps the split stable);
-//   4. decoupled look-back across the tiles of the same segment, one thread per
-//      digit, over 64-bit {flag, count} status words — the GPU replacement for
-//      the reference's barrier + compute_offsets;
-//   5. records are staged in shared memory in digit order, then each thread
-//      writes consecutive staged records to consecutive destinations, so a
-//      digit run becomes one contiguous span of 16-B (or 8-B) vector stores —
-//      the analogue of the reference's 256-B write-combining lanes.
-// Segment-aware: a launch scatters any number of segments (MSD bins); each tile
-// belongs to one segment and looks back only within it.
+// B200 design — persistent and warp-specialised:
+//   * warp 8 (producer) walks this CTA's tiles (static round-robin over the
+//     level's tile list), skips tiles of segments the planner did not split,
+//     and TMA-loads each tile (cp.async.bulk, mbarrier transaction count) into
+//     one of two shared-memory buffers;
+//   * warps 0-7 (consumers) rank the tile's records by digit with a ballot
+//     multisplit (stable: warp-striped input order, digit-major/warp-minor
+//     offsets), build a slot map in digit order, and write the records out in
+//     that order: consecutive slots of one digit go to consecutive destinations,
+//     so every digit run becomes one contiguous span of 16-B (8-B) vector
+//     stores — the GPU analogue of the 256-B write-combining lanes.
+// Destinations come from k_tile_scan (per-tile digit offsets inside the
+// segment, the decoupled-lookback scan) and k_plan (digit bases): no tile waits
+// on another, so prefetching the next tile cannot stall anyone.
 #pragma once
 
 #include "common.cuh"
@@ -93,19 +90,12 @@ struct TileInfo {
     uint64_t seg_start;
 };
 
-// Warp-specialised, persistent: warp 8 is the producer (claims tile tickets,
-// resolves their segment, TMA-loads the tile into one of two shared-memory
-// buffers), warps 0-7 consume (rank, look-back, write). full/empty mbarriers
-// hand buffers back and forth, so the next tile streams in from HBM while the
-// current one is ranked and written.
 template <int RS, bool kMap = false>
 __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
     uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Seg* __restrict__ segs,
-    const unsigned long long* __restrict__ seg_off,  // [nseg][256] exclusive digit offsets
-    const unsigned long long* __restrict__ stile_base, const uint32_t* __restrict__ tile_seg,
-    unsigned long long* __restrict__ status,  // [ntiles][256], zeroed
-    LevelCounters* __restrict__ ctr, uint32_t n_tiles, uint32_t ks = 0,
-    const uint8_t* __restrict__ map = nullptr) {
+    const unsigned long long* __restrict__ seg_base,  // [nseg][256] exclusive digit bases
+    const uint32_t* __restrict__ tile_seg, const uint32_t* __restrict__ tile_off,  // [ntiles][256]
+    uint32_t n_tiles, uint32_t ks = 0, const uint8_t* __restrict__ map = nullptr) {
     using C = ScatterCfg<RS>;
     constexpr int T = C::kThreads, IT = C::kItems, W = C::kWarps;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -131,42 +121,48 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
 
     if (warp == W) {  // ------------------------------------------------ producer
         if (lane != 0) return;
-        for (uint32_t it = 0;; ++it) {
+        uint32_t it = 0;
+        for (uint32_t tile = blockIdx.x;; tile += gridDim.x) {
+            Seg g;
+            uint32_t s = 0;
+            if (tile < n_tiles) {
+                s = tile_seg[tile];
+                g = segs[s];
+                if (g.action != kActScatter) continue;  // constant byte / finished: not split
+            }
             const int b = it & 1;
             if (it >= 2) mbar_wait(&s_empty[b], ((it >> 1) - 1) & 1u);
+            ++it;
             TileInfo ti;
-            ti.tile = atomicAdd(&ctr->tile_ticket, 1u);
-            uint32_t body = 0;
-            if (ti.tile < n_tiles) {
-                ti.seg = tile_seg[ti.tile];
-                const Seg g = segs[ti.seg];
-                ti.k = uint64_t(ti.tile) - stile_base[ti.seg];
-                ti.seg_start = g.start;
-                ti.gstart = g.start + ti.k * C::kTile;
-                ti.tn = uint32_t(min(uint64_t(C::kTile), g.size - ti.k * C::kTile));
-                ti.p = g.p;
-                ti.parity = g.parity;
-                const uint8_t* gsrc = (g.parity ? tmp : data) + ti.gstart * RS;
-                const uint32_t bytes = ti.tn * RS;
-                const uint32_t head = uint32_t(reinterpret_cast<uintptr_t>(gsrc) & 15u);  // 0 or 8
-                const uint32_t hb = head ? min(8u, bytes) : 0u;
-                body = (bytes - hb) & ~15u;
-                const uint32_t tail = bytes - hb - body;  // 0 or 8
-                ti.head = head;
-                uint8_t* sb = buf0 + b * C::kBufBytes + head;
-                if (hb) *reinterpret_cast<uint2*>(sb) = *reinterpret_cast<const uint2*>(gsrc);
-                if (tail)
-                    *reinterpret_cast<uint2*>(sb + hb + body) =
-                        *reinterpret_cast<const uint2*>(gsrc + hb + body);
-                fence_proxy_async_smem();
-                s_info[b] = ti;
-                mbar_arrive_expect_tx(&s_full[b], body);
-                if (body) tma_load_1d(sb + hb, gsrc + hb, body, &s_full[b]);
-            } else {
+            ti.tile = tile;
+            if (tile >= n_tiles) {
                 s_info[b] = ti;
                 mbar_arrive_expect_tx(&s_full[b], 0);
                 return;
             }
+            ti.seg = s;
+            ti.k = uint64_t(tile) - g.tile_base;
+            ti.seg_start = g.start;
+            ti.gstart = g.start + ti.k * C::kTile;
+            ti.tn = uint32_t(min(uint64_t(C::kTile), g.size - ti.k * C::kTile));
+            ti.p = g.p;
+            ti.parity = g.parity;
+            const uint8_t* gsrc = (g.parity ? tmp : data) + ti.gstart * RS;
+            const uint32_t bytes = ti.tn * RS;
+            const uint32_t head = uint32_t(reinterpret_cast<uintptr_t>(gsrc) & 15u);  // 0 or 8
+            const uint32_t hb = head ? min(8u, bytes) : 0u;
+            const uint32_t body = (bytes - hb) & ~15u;
+            const uint32_t tail = bytes - hb - body;  // 0 or 8
+            ti.head = head;
+            uint8_t* sb = buf0 + b * C::kBufBytes + head;
+            if (hb) *reinterpret_cast<uint2*>(sb) = *reinterpret_cast<const uint2*>(gsrc);
+            if (tail)
+                *reinterpret_cast<uint2*>(sb + hb + body) =
+                    *reinterpret_cast<const uint2*>(gsrc + hb + body);
+            fence_proxy_async_smem();
+            s_info[b] = ti;
+            mbar_arrive_expect_tx(&s_full[b], body);
+            if (body) tma_load_1d(sb + hb, gsrc + hb, body, &s_full[b]);
         }
     }
 
@@ -174,14 +170,15 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
     const uint32_t lt = lanemask_lt();
     for (uint32_t it = 0;; ++it) {
         const int b = it & 1;
-        // own warp's counter row (only this warp touches it while ranking)
 #pragma unroll
         for (int q = 0; q < kRadix / 32; ++q) s_wcnt[warp][q * 32 + lane] = 0;
         mbar_wait(&s_full[b], (it >> 1) & 1u);
         const TileInfo ti = s_info[b];
         if (ti.tile >= n_tiles) break;
-        const unsigned long long my_off =
-            threadIdx.x < kRadix ? seg_off[uint64_t(ti.seg) * kRadix + threadIdx.x] : 0ull;
+        // this thread's digit: base inside the segment + offset of the tile
+        const unsigned long long my_base =
+            seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x] +
+            tile_off[uint64_t(ti.tile) * kRadix + threadIdx.x];
         const uint8_t* tile = buf0 + b * C::kBufBytes + ti.head;
         const uint32_t tn = ti.tn, p = ti.p;
         __syncwarp();
@@ -203,7 +200,7 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
         }
         bar_sync_named(1, T);
 
-        // 2: per-digit tile totals, warp-exclusive offsets, early aggregate
+        // 2: per-digit tile totals, warp-exclusive offsets, tile-local starts
         uint32_t tcount = 0;
         {
             const int d = threadIdx.x;
@@ -213,12 +210,11 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
                 s_wcnt[w][d] = tcount;
                 tcount += c;
             }
-            st_volatile_u64(status + uint64_t(ti.tile) * kRadix + d,
-                            (ti.k == 0 ? kFlagIncl : kFlagAgg) | tcount);
         }
         uint32_t total;
         const uint32_t lstart = scan256_exclusive(tcount, s_scan, &total);
         s_lstart[threadIdx.x] = lstart;
+        s_gdelta[threadIdx.x] = (long long)(ti.seg_start + my_base) - (long long)lstart;
         bar_sync_named(1, T);
 
         // 3: slot map (digit order) in shared memory
@@ -231,43 +227,9 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
                 s_dig[slot] = uint8_t(d);
             }
         }
-
-        // 4: decoupled look-back within the segment (one thread per digit),
-        // kLook predecessor words per round.
-        {
-            constexpr int kLook = 4;
-            const int d = threadIdx.x;
-            uint64_t excl = 0;
-            if (ti.k > 0) {
-                const int64_t first = int64_t(ti.tile) - int64_t(ti.k);
-                int64_t t = int64_t(ti.tile) - 1;
-                while (true) {
-                    unsigned long long v[kLook];
-#pragma unroll
-                    for (int q = 0; q < kLook; ++q)
-                        v[q] = (t - q >= first) ? ld_volatile_u64(status + uint64_t(t - q) * kRadix + d)
-                                                : 0ull;
-                    bool done = false;
-                    int used = 0;
-#pragma unroll
-                    for (int q = 0; q < kLook; ++q) {
-                        if (done || used != q || t - q < first) continue;
-                        const uint64_t flag = v[q] & ~kValueMask;
-                        if (flag == 0) continue;
-                        excl += v[q] & kValueMask;
-                        ++used;
-                        if (flag == kFlagIncl) done = true;
-                    }
-                    if (done) break;
-                    t -= used;
-                }
-                st_volatile_u64(status + uint64_t(ti.tile) * kRadix + d, kFlagIncl | (excl + tcount));
-            }
-            s_gdelta[d] = (long long)(ti.seg_start + my_off + excl) - (long long)s_lstart[d];
-        }
         bar_sync_named(1, T);
 
-        // 5: write-out in digit order: consecutive slots of a digit go to
+        // 4: write-out in digit order: consecutive slots of a digit go to
         // consecutive destinations (coalesced vector stores)
         uint8_t* dst = ti.parity ? data : tmp;
 #pragma unroll 4

@@ -6,9 +6,9 @@
 // the host runs a short loop over MSD *levels*; each level is a handful of
 // kernel launches over device-resident segment lists:
 //
-//   level 0   k_histo_all: histograms of key bytes 0..7 + AND/OR of all words
-//             (constant leading bytes skipped before any record moves);
-//   level L   [k_seg_hist]  per-segment digit histogram + AND/OR (one read)
+//   level 0   k_sample_andor: first varying key byte of a strided sample
+//   level L   k_tile_hist   per-tile digit counts + per-segment AND/OR (one read)
+//             k_tile_scan   decoupled-lookback segmented scan -> per-tile offsets
 //             k_plan        per segment: finish / skip a constant byte /
 //                           scatter; children routed to groups or next level
 //             k_scatter     one stable split of every scattered segment
@@ -33,6 +33,7 @@
 #include "k_local_sort.cuh"
 #include "k_partition.cuh"
 #include "k_plan.cuh"
+#include "k_scan.cuh"
 #include "k_scatter.cuh"
 #include "k_util.cuh"
 
@@ -41,6 +42,8 @@ namespace {
 using namespace rg;
 
 constexpr int kMaxLevels = 72;
+// Per-call record limit: per-tile digit offsets are 32-bit (k_tile_scan).
+constexpr uint64_t kMaxRecords = 1ull << 32;
 
 struct CudaError {
     int code;
@@ -86,15 +89,15 @@ struct Workspace {
     DevBuf<unsigned long long> hist8, andor0, thr, acc;
     DevBuf<LevelCounters> ctr;
     DevBuf<Seg> segs[2];
-    DevBuf<unsigned long long> seg_hist[2], seg_andor[2];
-    DevBuf<unsigned long long> stile_base;
-    DevBuf<uint32_t> tile_seg, htile_seg[2];
+    DevBuf<unsigned long long> seg_tot[2], seg_andor[2];
+    DevBuf<uint32_t> tile_seg[2];
+    DevBuf<uint16_t> tile_cnt;
+    DevBuf<uint32_t> tile_off;
     DevBuf<unsigned long long> status;
     DevBuf<Group> groups;
     DevBuf<CopyRange> copies;
     DevBuf<uint8_t> host_data, host_tmp, map8;
-    DevBuf<uint32_t> map32;
-    LevelCounters* h_ctr = nullptr;      // pinned [kMaxLevels]
+    LevelCounters* h_ctr = nullptr;         // pinned [kMaxLevels]
     unsigned long long* h_small = nullptr;  // pinned scratch [4096]
     raduls_gpu_stats last{};
     bool attrs_set[33] = {};
@@ -152,7 +155,7 @@ uint32_t first_varying_byte(const unsigned long long* andor, uint32_t from, uint
 
 // Capacities for a sort of n records.
 struct Caps {
-    size_t seg, tiles, htiles, groups, copies;
+    size_t seg, tiles, groups, copies;
 };
 
 template <int RS>
@@ -161,7 +164,6 @@ Caps caps_for(uint64_t n) {
     Caps c;
     c.seg = size_t(n / (cap_local + 1) + 2);
     c.tiles = size_t(n / ScatterCfg<RS>::kTile + c.seg + 2);
-    c.htiles = size_t(n / kHistTile + c.seg + 2);
     c.groups = size_t(3 * (n / cap_local) + c.seg + 2);
     c.copies = size_t(n / kCopyTile + c.seg + 2);
     return c;
@@ -172,13 +174,13 @@ void ensure_caps(Workspace& ws, uint64_t n) {
     const Caps c = caps_for<RS>(n);
     for (int b = 0; b < 2; ++b) {
         ws.segs[b].ensure(c.seg);
-        ws.seg_hist[b].ensure(c.seg * kRadix);
+        ws.seg_tot[b].ensure(c.seg * kRadix);
         ws.seg_andor[b].ensure(c.seg * 8);
-        ws.htile_seg[b].ensure(c.htiles);
+        ws.tile_seg[b].ensure(c.tiles);
     }
-    ws.stile_base.ensure(c.seg);
-    ws.tile_seg.ensure(c.tiles);
-    ws.status.ensure(c.tiles * kRadix);
+    ws.tile_cnt.ensure(c.tiles * kRadix);
+    ws.tile_off.ensure(c.tiles * kRadix);
+    ws.status.ensure((c.tiles / kScanChunk + 1) * kRadix);
     ws.groups.ensure(c.groups);
     ws.copies.ensure(c.copies);
 }
@@ -195,18 +197,35 @@ void set_attrs(Workspace& ws) {
     ws.attrs_set[RS] = true;
 }
 
-// Persistent scatter launch: at most two CTAs per SM, never more CTAs than tiles.
-template <int RS, bool kMap>
-void launch_scatter(uint8_t* data, uint8_t* tmp, const Seg* segs, const unsigned long long* seg_off,
-                    const unsigned long long* stile_base, const uint32_t* tile_seg,
-                    unsigned long long* status, LevelCounters* ctr, uint32_t n_tiles, uint32_t ks,
-                    const uint8_t* map, cudaStream_t st) {
+int sm_count() {
     int dev = 0, sms = 148;
     RG_CHECK(cudaGetDevice(&dev));
     RG_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const uint32_t grid = std::min<uint32_t>(n_tiles, uint32_t(sms) * 2);
+    return sms;
+}
+
+// Tile histogram + segmented look-back scan of one level: per-tile digit
+// offsets (ws.tile_off), per-segment digit totals (ws.seg_tot[cur]).
+template <int RS, bool kMap = false>
+void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t ntiles, LevelCounters* c,
+                  cudaStream_t st, uint32_t ks = 0, const uint8_t* map = nullptr) {
+    constexpr int TILE = ScatterCfg<RS>::kTile;
+    k_tile_hist<RS, TILE, kMap><<<ntiles, 256, 0, st>>>(data, tmp, ws.segs[cur].p, ws.tile_seg[cur].p,
+                                                        ws.tile_cnt.p, ws.seg_andor[cur].p, c, ks, map);
+    RG_LAUNCH_CHECK();
+    const uint32_t nchunks = (ntiles + kScanChunk - 1) / kScanChunk;
+    RG_CHECK(cudaMemsetAsync(ws.status.p, 0, size_t(nchunks) * kRadix * sizeof(unsigned long long), st));
+    k_tile_scan<TILE><<<nchunks, 256, 0, st>>>(ws.segs[cur].p, ws.tile_seg[cur].p, ws.tile_cnt.p, ntiles,
+                                               ws.tile_off.p, ws.seg_tot[cur].p, ws.status.p, c);
+    RG_LAUNCH_CHECK();
+}
+
+template <int RS, bool kMap>
+void launch_scatter(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t ntiles, uint32_t ks,
+                    const uint8_t* map, cudaStream_t st) {
+    const uint32_t grid = std::min<uint32_t>(ntiles, uint32_t(sm_count()) * 2);
     k_scatter<RS, kMap><<<grid, ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>::kSmem, st>>>(
-        data, tmp, segs, seg_off, stile_base, tile_seg, status, ctr, n_tiles, ks, map);
+        data, tmp, ws.segs[cur].p, ws.seg_tot[cur].p, ws.tile_seg[cur].p, ws.tile_off.p, ntiles, ks, map);
     RG_LAUNCH_CHECK();
 }
 
@@ -223,31 +242,16 @@ void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, 
 template <int RS>
 void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t ks,
                cudaStream_t st) {
+    constexpr int TILE = ScatterCfg<RS>::kTile;
     raduls_gpu_stats stats{};
     ws.last = stats;
     if (n < 2) return;  // msd_sorter.hpp:51
     set_attrs<RS>(ws);
     ensure_caps<RS>(ws, n);
-
-    // ---- level 0: whole-array histograms of key bytes 0..7 + AND/OR
-    const uint32_t nb = std::min<uint32_t>(ks, 8);
-    RG_CHECK(cudaMemsetAsync(ws.hist8.p, 0, 8 * kRadix * sizeof(unsigned long long), st));
-    k_init_andor<<<1, 64, 0, st>>>(ws.andor0.p, 1);
-    RG_LAUNCH_CHECK();
-    k_histo_all<RS><<<grid_for(n, 256, 8), 256, 0, st>>>(data, n, nb, ws.hist8.p, ws.andor0.p);
-    RG_LAUNCH_CHECK();
-    stats.hist_records += n;
-    RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.andor0.p, 8 * sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, st));
-    RG_CHECK(cudaStreamSynchronize(st));
-    const uint32_t p0 = first_varying_byte(ws.h_small, 0, ks);
-    if (p0 >= ks) {  // every key equal: a stable sort is the identity
-        ws.last = stats;
-        return;
-    }
     LevelCounters* dctr = ws.ctr.p;
-    if (n <= uint64_t(LocalCfg<RS>::kCap)) {  // one group sorts everything
-        Group g{0, uint32_t(n), p0, 0, 0};
+
+    if (n <= uint64_t(LocalCfg<RS>::kCap)) {  // one group sorts everything, in place
+        Group g{0, uint32_t(n), 0, 0, 0};
         RG_CHECK(cudaMemcpyAsync(ws.groups.p, &g, sizeof g, cudaMemcpyHostToDevice, st));
         RG_CHECK(cudaMemsetAsync(dctr, 0, sizeof(LevelCounters), st));
         launch_local<RS>(ws, data, tmp, 1, ks, dctr, st);
@@ -260,64 +264,71 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         return;
     }
 
+    // ---- level 0: guess the first varying key byte from a strided sample,
+    // histogram the whole array on it, confirm with the global AND/OR.
+    k_init_andor<<<1, 64, 0, st>>>(ws.andor0.p, 1);
+    RG_LAUNCH_CHECK();
+    const uint32_t samples = uint32_t(std::min<uint64_t>(n, 65536));
+    k_sample_andor<RS><<<64, 256, 0, st>>>(data, n, std::max<uint64_t>(1, n / samples), samples, ws.andor0.p);
+    RG_LAUNCH_CHECK();
+    RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.andor0.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    RG_CHECK(cudaStreamSynchronize(st));
+    uint32_t p0 = first_varying_byte(ws.h_small, 0, ks);
+    if (p0 >= ks) p0 = 0;  // sample saw one key only: histogram byte 0 and let AND/OR decide
+    const uint32_t nt0 = uint32_t((n + TILE - 1) / TILE);
     int cur = 0;
     {
-        Seg s0{0, n, p0, 0, 0};
+        Seg s0{0, n, p0, 0, 0, 0};
         RG_CHECK(cudaMemcpyAsync(ws.segs[0].p, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
-        if (p0 < 8) {
-            RG_CHECK(cudaMemcpyAsync(ws.seg_hist[0].p, ws.hist8.p + size_t(p0) * kRadix,
-                                     kRadix * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));
-            RG_CHECK(cudaMemcpyAsync(ws.seg_andor[0].p, ws.andor0.p, 8 * sizeof(unsigned long long),
-                                     cudaMemcpyDeviceToDevice, st));
-        } else {  // first eight key bytes constant: histogram byte p0 now
-            RG_CHECK(cudaMemsetAsync(ws.seg_hist[0].p, 0, kRadix * sizeof(unsigned long long), st));
+        RG_CHECK(cudaMemsetAsync(ws.tile_seg[0].p, 0, nt0 * sizeof(uint32_t), st));
+        k_init_andor<<<1, 64, 0, st>>>(ws.seg_andor[0].p, 1);
+        RG_LAUNCH_CHECK();
+        RG_CHECK(cudaMemsetAsync(dctr, 0, sizeof(LevelCounters), st));
+        level_counts<RS>(ws, data, tmp, 0, nt0, dctr, st);
+        RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.seg_andor[0].p, 8 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, st));
+        RG_CHECK(cudaStreamSynchronize(st));
+        const uint32_t pg = first_varying_byte(ws.h_small, 0, ks);
+        if (pg >= ks) {  // every key equal: a stable sort is the identity
+            ws.last = stats;
+            return;
+        }
+        if (pg != p0) {  // a more significant byte varies outside the sample
+            s0.p = pg;
+            RG_CHECK(cudaMemcpyAsync(ws.segs[0].p, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
             k_init_andor<<<1, 64, 0, st>>>(ws.seg_andor[0].p, 1);
             RG_LAUNCH_CHECK();
-            const uint64_t nt = (n + kHistTile - 1) / kHistTile;
-            RG_CHECK(cudaMemsetAsync(ws.htile_seg[0].p, 0, nt * sizeof(uint32_t), st));
-            k_seg_hist<RS><<<uint32_t(nt), kHistThreads, 0, st>>>(data, tmp, ws.segs[0].p,
-                                                                 ws.htile_seg[0].p, ws.seg_hist[0].p,
-                                                                 ws.seg_andor[0].p);
-            RG_LAUNCH_CHECK();
-            stats.hist_records += n;
+            level_counts<RS>(ws, data, tmp, 0, nt0, dctr, st);
         }
     }
-    uint32_t nseg = 1;
-    uint32_t level = 0;
+    uint32_t nseg = 1, ntiles = nt0, level = 0;
     const Caps caps = caps_for<RS>(n);
-    while (nseg > 0) {
+    while (true) {
         if (level >= uint32_t(kMaxLevels)) throw CudaError{RADULS_GPU_EINTERNAL};
         LevelCounters* c = dctr + level;
-        RG_CHECK(cudaMemsetAsync(c, 0, sizeof(LevelCounters), st));
         PlanArgs A;
         A.segs = ws.segs[cur].p;
-        A.seg_hist = ws.seg_hist[cur].p;
+        A.seg_tot = ws.seg_tot[cur].p;
         A.seg_andor = ws.seg_andor[cur].p;
-        A.stile_base = ws.stile_base.p;
-        A.tile_seg = ws.tile_seg.p;
         A.groups = ws.groups.p;
         A.copies = ws.copies.p;
         A.next = ws.segs[cur ^ 1].p;
-        A.next_hist = ws.seg_hist[cur ^ 1].p;
         A.next_andor = ws.seg_andor[cur ^ 1].p;
-        A.next_htile_seg = ws.htile_seg[cur ^ 1].p;
+        A.next_tile_seg = ws.tile_seg[cur ^ 1].p;
         A.ctr = c;
         A.ks = ks;
-        A.tile = ScatterCfg<RS>::kTile;
+        A.tile = TILE;
         A.cap_local = LocalCfg<RS>::kCap;
         k_plan<<<nseg, 256, 0, st>>>(A);
         RG_LAUNCH_CHECK();
         RG_CHECK(cudaMemcpyAsync(ws.h_ctr + level, c, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
         RG_CHECK(cudaStreamSynchronize(st));
         const LevelCounters h = ws.h_ctr[level];
-        if (h.n_scatter_tiles > caps.tiles || h.n_groups > caps.groups || h.n_copy > caps.copies ||
-            h.n_next > caps.seg || h.n_next_htiles > caps.htiles)
+        if (h.n_groups > caps.groups || h.n_copy > caps.copies || h.n_next > caps.seg ||
+            h.n_next_tiles > caps.tiles)
             throw CudaError{RADULS_GPU_EINTERNAL};
-        if (h.n_scatter_tiles) {
-            RG_CHECK(cudaMemsetAsync(ws.status.p, 0,
-                                     size_t(h.n_scatter_tiles) * kRadix * sizeof(unsigned long long), st));
-            launch_scatter<RS, false>(data, tmp, ws.segs[cur].p, ws.seg_hist[cur].p, ws.stile_base.p,
-                                      ws.tile_seg.p, ws.status.p, c, h.n_scatter_tiles, ks, nullptr, st);
+        if (h.n_scatter_segs) {
+            launch_scatter<RS, false>(ws, data, tmp, cur, ntiles, ks, nullptr, st);
             stats.scatter_launches++;
         }
         launch_local<RS>(ws, data, tmp, h.n_groups, ks, c, st);
@@ -328,27 +339,21 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         stats.scatter_records += h.moved_scatter;
         stats.copy_records += h.moved_copy;
         stats.skipped_levels += nseg - h.n_scatter_segs;
+        ++level;
+        if (!h.n_next) break;
         cur ^= 1;
         nseg = h.n_next;
-        ++level;
-        if (nseg) {
-            k_seg_hist<RS><<<h.n_next_htiles, kHistThreads, 0, st>>>(
-                data, tmp, ws.segs[cur].p, ws.htile_seg[cur].p, ws.seg_hist[cur].p,
-                ws.seg_andor[cur].p);
-            RG_LAUNCH_CHECK();
-            // records histogrammed = sum of next segment sizes (from the planner's view)
-        }
+        ntiles = h.n_next_tiles;
+        RG_CHECK(cudaMemsetAsync(dctr + level, 0, sizeof(LevelCounters), st));
+        level_counts<RS>(ws, data, tmp, cur, ntiles, dctr + level, st);
     }
-    // final counters (local-sort / fallback totals are written by kernels)
     RG_CHECK(cudaMemcpyAsync(ws.h_ctr, dctr, sizeof(LevelCounters) * level, cudaMemcpyDeviceToHost, st));
     RG_CHECK(cudaStreamSynchronize(st));
     stats.levels = level;
     for (uint32_t l = 0; l < level; ++l) {
         stats.local_records += ws.h_ctr[l].moved_local;
         stats.fallback_groups += ws.h_ctr[l].fallback_groups;
-        if (l + 1 < level) {
-            // histogram tiles read by level l+1 cover its segments exactly
-        }
+        stats.hist_records += ws.h_ctr[l].hist_records;
     }
     ws.last = stats;
 }
@@ -412,7 +417,7 @@ int raduls_gpu_layout_valid(uint32_t rs, uint32_t ks) { return layout_ok(rs, ks)
 uint32_t raduls_gpu_version(void) { return 0x000100u; }
 
 int raduls_gpu_sort(void* d_data, void* d_tmp, uint64_t n, uint32_t rs, uint32_t ks, void* stream) {
-    if (!layout_ok(rs, ks) || mul_overflows(n, rs)) return RADULS_GPU_EINVAL;
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs) || n > kMaxRecords) return RADULS_GPU_EINVAL;
     if (n >= 2 && (!d_data || !aligned_ok(d_data, rs) || (d_tmp && !aligned_ok(d_tmp, rs))))
         return RADULS_GPU_EINVAL;
     return guarded([&] {
@@ -439,7 +444,7 @@ int raduls_gpu_sort(void* d_data, void* d_tmp, uint64_t n, uint32_t rs, uint32_t
 }
 
 int raduls_gpu_sort_host(uint8_t* data, uint8_t* /*tmp*/, uint64_t n, uint32_t rs, uint32_t ks) {
-    if (!layout_ok(rs, ks) || mul_overflows(n, rs)) return RADULS_GPU_EINVAL;
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs) || n > kMaxRecords) return RADULS_GPU_EINVAL;
     if (n < 2) return RADULS_GPU_OK;
     if (!data) return RADULS_GPU_EINVAL;
     return guarded([&] {
@@ -467,9 +472,56 @@ int raduls_gpu_last_stats(raduls_gpu_stats* out) {
     });
 }
 
+}  // extern "C"
+
+namespace {
+// One-segment helper: histogram + scan of the whole array on byte p (or the
+// mapped prefix), digit bases on the host; returns totals in h_tot[256].
+template <int RS, bool kMap>
+void single_segment_counts(Workspace& ws, uint8_t* src, uint64_t n, uint32_t p, uint32_t ks,
+                           const uint8_t* map, unsigned long long* h_tot, cudaStream_t st) {
+    constexpr int TILE = ScatterCfg<RS>::kTile;
+    ensure_caps<RS>(ws, n);
+    set_attrs<RS>(ws);
+    Seg s0{0, n, p, 0, 0, 0};
+    RG_CHECK(cudaMemcpyAsync(ws.segs[0].p, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
+    const uint32_t nt = uint32_t((n + TILE - 1) / TILE);
+    RG_CHECK(cudaMemsetAsync(ws.tile_seg[0].p, 0, nt * sizeof(uint32_t), st));
+    k_init_andor<<<1, 64, 0, st>>>(ws.seg_andor[0].p, 1);
+    RG_LAUNCH_CHECK();
+    RG_CHECK(cudaMemsetAsync(ws.ctr.p, 0, sizeof(LevelCounters), st));
+    level_counts<RS, kMap>(ws, src, src, 0, nt, ws.ctr.p, st, ks, map);
+    RG_CHECK(cudaMemcpyAsync(h_tot, ws.seg_tot[0].p, kRadix * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             st));
+    RG_CHECK(cudaStreamSynchronize(st));
+}
+
+// Scatter the single segment prepared by single_segment_counts from src into dst.
+template <int RS, bool kMap>
+void single_segment_scatter(Workspace& ws, uint8_t* src, uint8_t* dst, uint64_t n, uint32_t ks,
+                            const uint8_t* map, const unsigned long long* h_tot, cudaStream_t st) {
+    constexpr int TILE = ScatterCfg<RS>::kTile;
+    unsigned long long* off = ws.h_small + 1024;
+    unsigned long long run = 0;
+    for (int d = 0; d < 256; ++d) off[d] = run, run += h_tot[d];
+    RG_CHECK(cudaMemcpyAsync(ws.seg_tot[0].p, off, kRadix * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                             st));
+    const uint32_t act = kActScatter;
+    RG_CHECK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(ws.segs[0].p) + offsetof(Seg, action), &act,
+                             sizeof act, cudaMemcpyHostToDevice, st));
+    const uint32_t nt = uint32_t((n + TILE - 1) / TILE);
+    launch_scatter<RS, kMap>(ws, src, dst, 0, nt, ks, map, st);
+    RG_CHECK(cudaStreamSynchronize(st));
+}
+
+}  // namespace
+
+extern "C" {
+
 int raduls_gpu_split(const void* d_src, void* d_dst, uint64_t n, uint32_t rs,
                      uint32_t key_byte_offset, uint64_t* h_counts, void* stream) {
-    if (!layout_ok(rs, rs) || key_byte_offset >= rs || mul_overflows(n, rs)) return RADULS_GPU_EINVAL;
+    if (!layout_ok(rs, rs) || key_byte_offset >= rs || mul_overflows(n, rs) || n > kMaxRecords)
+        return RADULS_GPU_EINVAL;
     if (n && (!aligned_ok(d_src, rs) || !aligned_ok(d_dst, rs))) return RADULS_GPU_EINVAL;
     return guarded([&] {
         Workspace& ws = workspace();
@@ -479,65 +531,39 @@ int raduls_gpu_split(const void* d_src, void* d_dst, uint64_t n, uint32_t rs,
         if (n == 0) return;
         dispatch_rs(rs, [&](auto R) {
             constexpr int RSC = decltype(R)::value;
-            ensure_caps<RSC>(ws, n);
-            // histogram of the byte via a one-segment k_seg_hist
-            Seg s0{0, n, key_byte_offset, 0, 0};
-            RG_CHECK(cudaMemcpyAsync(ws.segs[0].p, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
-            RG_CHECK(cudaMemsetAsync(ws.seg_hist[0].p, 0, kRadix * sizeof(unsigned long long), st));
-            k_init_andor<<<1, 64, 0, st>>>(ws.seg_andor[0].p, 1);
-            const uint64_t nt = (n + kHistTile - 1) / kHistTile;
-            RG_CHECK(cudaMemsetAsync(ws.htile_seg[0].p, 0, nt * sizeof(uint32_t), st));
             uint8_t* src = const_cast<uint8_t*>(static_cast<const uint8_t*>(d_src));
-            k_seg_hist<RSC><<<uint32_t(nt), kHistThreads, 0, st>>>(src, src, ws.segs[0].p, ws.htile_seg[0].p,
-                                                                  ws.seg_hist[0].p, ws.seg_andor[0].p);
-            RG_LAUNCH_CHECK();
-            RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.seg_hist[0].p, kRadix * sizeof(unsigned long long),
-                                     cudaMemcpyDeviceToHost, st));
-            RG_CHECK(cudaStreamSynchronize(st));
-            if (h_counts) std::memcpy(h_counts, ws.h_small, 256 * sizeof(uint64_t));
-            unsigned long long off[256], run = 0;
-            for (int d = 0; d < 256; ++d) off[d] = run, run += ws.h_small[d];
-            RG_CHECK(cudaMemcpyAsync(ws.seg_hist[0].p, off, sizeof off, cudaMemcpyHostToDevice, st));
-            const uint32_t tiles = uint32_t((n + ScatterCfg<RSC>::kTile - 1) / ScatterCfg<RSC>::kTile);
-            RG_CHECK(cudaMemsetAsync(ws.tile_seg.p, 0, tiles * sizeof(uint32_t), st));
-            RG_CHECK(cudaMemsetAsync(ws.stile_base.p, 0, sizeof(unsigned long long), st));
-            RG_CHECK(cudaMemsetAsync(ws.status.p, 0, size_t(tiles) * kRadix * sizeof(unsigned long long), st));
-            RG_CHECK(cudaMemsetAsync(ws.ctr.p, 0, sizeof(LevelCounters), st));
-            // parity 0: src = "data" slot, dst = "tmp" slot
-            set_attrs<RSC>(ws);
-            launch_scatter<RSC, false>(src, static_cast<uint8_t*>(d_dst), ws.segs[0].p, ws.seg_hist[0].p,
-                                       ws.stile_base.p, ws.tile_seg.p, ws.status.p, ws.ctr.p, tiles, 0,
-                                       nullptr, st);
-            RG_CHECK(cudaStreamSynchronize(st));
+            unsigned long long* tot = ws.h_small;
+            single_segment_counts<RSC, false>(ws, src, n, key_byte_offset, rs, nullptr, tot, st);
+            if (h_counts) std::memcpy(h_counts, tot, 256 * sizeof(uint64_t));
+            single_segment_scatter<RSC, false>(ws, src, static_cast<uint8_t*>(d_dst), n, rs, nullptr, tot, st);
         });
     });
 }
 
 int raduls_gpu_histogram(const void* d_data, uint64_t n, uint32_t rs, uint32_t ks, uint64_t* h_hist,
                          uint64_t* h_andor, void* stream) {
-    if (!layout_ok(rs, ks) || mul_overflows(n, rs)) return RADULS_GPU_EINVAL;
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs) || n > kMaxRecords) return RADULS_GPU_EINVAL;
     if (n && !aligned_ok(d_data, rs)) return RADULS_GPU_EINVAL;
     return guarded([&] {
         Workspace& ws = workspace();
         std::lock_guard<std::mutex> lk(ws.mu);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
-        RG_CHECK(cudaMemsetAsync(ws.hist8.p, 0, 8 * kRadix * sizeof(unsigned long long), st));
-        k_init_andor<<<1, 64, 0, st>>>(ws.andor0.p, 1);
-        if (n) {
-            dispatch_rs(rs, [&](auto R) {
-                k_histo_all<decltype(R)::value><<<grid_for(n, 256, 8), 256, 0, st>>>(
-                    static_cast<const uint8_t*>(d_data), n, std::min<uint32_t>(ks, 8), ws.hist8.p,
-                    ws.andor0.p);
-            });
-            RG_LAUNCH_CHECK();
-        }
-        RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.hist8.p, 8 * kRadix * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, st));
-        RG_CHECK(cudaMemcpyAsync(ws.h_small + 8 * kRadix, ws.andor0.p, 8 * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, st));
-        RG_CHECK(cudaStreamSynchronize(st));
-        if (h_hist) std::memcpy(h_hist, ws.h_small, 8 * kRadix * sizeof(uint64_t));
-        if (h_andor) std::memcpy(h_andor, ws.h_small + 8 * kRadix, 8 * sizeof(uint64_t));
+        if (h_hist) std::memset(h_hist, 0, 8 * 256 * sizeof(uint64_t));
+        if (h_andor)
+            for (int w = 0; w < 8; ++w) h_andor[w] = (w & 1) ? 0ull : ~0ull;
+        if (!n) return;
+        dispatch_rs(rs, [&](auto R) {
+            constexpr int RSC = decltype(R)::value;
+            uint8_t* src = const_cast<uint8_t*>(static_cast<const uint8_t*>(d_data));
+            for (uint32_t b = 0; b < std::min<uint32_t>(ks, 8); ++b) {
+                single_segment_counts<RSC, false>(ws, src, n, b, ks, nullptr, ws.h_small, st);
+                if (h_hist) std::memcpy(h_hist + 256 * b, ws.h_small, 256 * sizeof(uint64_t));
+            }
+            RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.seg_andor[0].p, 8 * sizeof(unsigned long long),
+                                     cudaMemcpyDeviceToHost, st));
+            RG_CHECK(cudaStreamSynchronize(st));
+            if (h_andor) std::memcpy(h_andor, ws.h_small, 8 * sizeof(uint64_t));
+        });
     });
 }
 
@@ -630,7 +656,8 @@ int raduls_gpu_prefix_histogram(const void* d_data, uint64_t n, uint32_t rs, uin
 int raduls_gpu_partition(const void* d_src, void* d_dst, uint64_t n, uint32_t rs, uint32_t ks,
                          uint32_t prefix_byte, const uint32_t* d_bucket_rank, uint32_t n_ranks,
                          uint64_t* h_rank_counts, void* stream) {
-    if (!layout_ok(rs, ks) || mul_overflows(n, rs) || n_ranks < 1 || n_ranks > 256 || !d_bucket_rank)
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs) || n_ranks < 1 || n_ranks > 256 || !d_bucket_rank ||
+        n > kMaxRecords)
         return RADULS_GPU_EINVAL;
     if (n && (!aligned_ok(d_src, rs) || !aligned_ok(d_dst, rs))) return RADULS_GPU_EINVAL;
     return guarded([&] {
@@ -643,41 +670,18 @@ int raduls_gpu_partition(const void* d_src, void* d_dst, uint64_t n, uint32_t rs
         k_map_to_u8<<<256, 256, 0, st>>>(d_bucket_rank, ws.map8.p, n_ranks,
                                           reinterpret_cast<unsigned int*>(ws.acc.p));
         RG_LAUNCH_CHECK();
-        RG_CHECK(cudaMemsetAsync(ws.hist8.p, 0, kRadix * sizeof(unsigned long long), st));
-        if (n) {
-            dispatch_rs(rs, [&](auto R) {
-                k_map_hist<decltype(R)::value><<<grid_for(n, 256, 8), 256, 0, st>>>(
-                    static_cast<const uint8_t*>(d_src), n, ks, prefix_byte, ws.map8.p, ws.hist8.p);
-            });
-            RG_LAUNCH_CHECK();
-        }
-        RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.hist8.p, kRadix * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, st));
-        RG_CHECK(cudaMemcpyAsync(ws.h_small + kRadix, ws.acc.p, sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, st));
+        RG_CHECK(cudaMemcpyAsync(ws.h_small + 2048, ws.acc.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                 st));
         RG_CHECK(cudaStreamSynchronize(st));
-        if (uint32_t(ws.h_small[kRadix])) throw CudaError{RADULS_GPU_EINVAL};  // map entry >= n_ranks
-        if (h_rank_counts) std::memcpy(h_rank_counts, ws.h_small, n_ranks * sizeof(uint64_t));
+        if (uint32_t(ws.h_small[2048])) throw CudaError{RADULS_GPU_EINVAL};  // map entry >= n_ranks
         if (!n) return;
-        unsigned long long off[256], run = 0;
-        for (int d = 0; d < 256; ++d) off[d] = run, run += ws.h_small[d];
         dispatch_rs(rs, [&](auto R) {
             constexpr int RSC = decltype(R)::value;
-            ensure_caps<RSC>(ws, n);
-            Seg s0{0, n, prefix_byte, 0, 0};
-            RG_CHECK(cudaMemcpyAsync(ws.segs[0].p, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
-            RG_CHECK(cudaMemcpyAsync(ws.seg_hist[0].p, off, sizeof off, cudaMemcpyHostToDevice, st));
-            const uint32_t tiles = uint32_t((n + ScatterCfg<RSC>::kTile - 1) / ScatterCfg<RSC>::kTile);
-            RG_CHECK(cudaMemsetAsync(ws.tile_seg.p, 0, tiles * sizeof(uint32_t), st));
-            RG_CHECK(cudaMemsetAsync(ws.stile_base.p, 0, sizeof(unsigned long long), st));
-            RG_CHECK(cudaMemsetAsync(ws.status.p, 0, size_t(tiles) * kRadix * sizeof(unsigned long long), st));
-            RG_CHECK(cudaMemsetAsync(ws.ctr.p, 0, sizeof(LevelCounters), st));
             uint8_t* src = const_cast<uint8_t*>(static_cast<const uint8_t*>(d_src));
-            set_attrs<RSC>(ws);
-            launch_scatter<RSC, true>(src, static_cast<uint8_t*>(d_dst), ws.segs[0].p, ws.seg_hist[0].p,
-                                      ws.stile_base.p, ws.tile_seg.p, ws.status.p, ws.ctr.p, tiles, ks,
-                                      ws.map8.p, st);
-            RG_CHECK(cudaStreamSynchronize(st));
+            unsigned long long* tot = ws.h_small;
+            single_segment_counts<RSC, true>(ws, src, n, prefix_byte, ks, ws.map8.p, tot, st);
+            if (h_rank_counts) std::memcpy(h_rank_counts, tot, n_ranks * sizeof(uint64_t));
+            single_segment_scatter<RSC, true>(ws, src, static_cast<uint8_t*>(d_dst), n, ks, ws.map8.p, tot, st);
         });
     });
 }
@@ -689,10 +693,10 @@ void raduls_gpu_release(void) {
         std::lock_guard<std::mutex> lk2(w->mu);
         w->hist8.release(); w->andor0.release(); w->thr.release(); w->acc.release(); w->ctr.release();
         for (int b = 0; b < 2; ++b) {
-            w->segs[b].release(); w->seg_hist[b].release(); w->seg_andor[b].release(); w->htile_seg[b].release();
+            w->segs[b].release(); w->seg_tot[b].release(); w->seg_andor[b].release(); w->tile_seg[b].release();
         }
-        w->stile_base.release(); w->tile_seg.release(); w->status.release(); w->groups.release();
-        w->copies.release(); w->host_data.release(); w->host_tmp.release(); w->map8.release(); w->map32.release();
+        w->tile_cnt.release(); w->tile_off.release(); w->status.release(); w->groups.release();
+        w->copies.release(); w->host_data.release(); w->host_tmp.release(); w->map8.release();
         if (w->h_ctr) cudaFreeHost(w->h_ctr);
         if (w->h_small) cudaFreeHost(w->h_small);
         delete w;
