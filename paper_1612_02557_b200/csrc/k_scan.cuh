@@ -98,7 +98,11 @@ __global__ void __launch_bounds__(256) k_tile_scan(const Seg* __restrict__ segs,
     unsigned long long excl = 0;
     unsigned long long* my = status + uint64_t(c) * kRadix + d;
     if (first_head < kScanChunk) {
+        // the trailing run starts at a segment head inside this chunk: its
+        // prefix is complete, publish it at once
         st_volatile_u64(my, kFlagIncl | run);
+        // tiles before the head continue a segment begun in an earlier chunk
+        if (first_head > 0) excl = lookback_chunks(status, int64_t(c), d);
     } else {
         st_volatile_u64(my, kFlagAgg | run);
         excl = lookback_chunks(status, int64_t(c), d);
