@@ -127,15 +127,30 @@ __device__ __forceinline__ Rec<RS> ld_smem_rec(const uint8_t* s, uint32_t slot) 
     return r;
 }
 
-// Record byte `p` (runtime, warp-uniform) from a register-held record, without
-// dynamic register indexing (compiles to a select chain, no local memory).
+// 32-bit word `wi` (runtime, warp-uniform) of a register-held record via a
+// binary tree of selects on the bits of wi — written so that the compiler
+// cannot turn it back into a dynamically indexed (local-memory) array access.
+template <int LO, int N, int RS>
+__device__ __forceinline__ uint32_t rec_word_tree(const Rec<RS>& r, uint32_t wi) {
+    if constexpr (N == 1) {
+        return r.w[LO];
+    } else {
+        constexpr int H = N / 2;
+        const uint32_t a = rec_word_tree<LO, H, RS>(r, wi);
+        const uint32_t b = rec_word_tree<LO + H, N - H, RS>(r, wi);
+        return wi < uint32_t(LO + H) ? a : b;
+    }
+}
+
+template <int RS>
+__device__ __forceinline__ uint32_t rec_word32(const Rec<RS>& r, uint32_t wi) {
+    return rec_word_tree<0, Rec<RS>::kWords, RS>(r, wi);
+}
+
+// Record byte `p` (runtime, warp-uniform) from a register-held record.
 template <int RS>
 __device__ __forceinline__ uint32_t rec_byte(const Rec<RS>& r, uint32_t p) {
-    const uint32_t wi = p >> 2;
-    uint32_t word = r.w[0];
-#pragma unroll
-    for (int k = 1; k < Rec<RS>::kWords; ++k) word = (wi == uint32_t(k)) ? r.w[k] : word;
-    return (word >> ((p & 3u) * 8u)) & 0xFFu;
+    return (rec_word32<RS>(r, p >> 2) >> ((p & 3u) * 8u)) & 0xFFu;
 }
 
 // Little-endian 64-bit word k (record bytes 8k..8k+7).

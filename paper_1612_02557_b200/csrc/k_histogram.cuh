@@ -125,9 +125,7 @@ __global__ void __launch_bounds__(256) k_tile_hist(const uint8_t* __restrict__ d
             continue;
         }
         const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
-        uint32_t word = r[j].w[0];
-#pragma unroll
-        for (int q = 1; q < Rec<RS>::kWords; ++q) word = (p >> 2) == uint32_t(q) ? r[j].w[q] : word;
+        const uint32_t word = rec_word32<RS>(r[j], p >> 2);
         const uint32_t wa = __reduce_and_sync(0xFFFFFFFFu, valid ? word : ~0u);
         const uint32_t wo = __reduce_or_sync(0xFFFFFFFFu, valid ? word : 0u);
         const uint32_t shf = (p & 3u) * 8u;

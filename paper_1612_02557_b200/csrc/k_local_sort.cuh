@@ -187,12 +187,20 @@ __device__ __forceinline__ int cmp_beyond(const uint8_t* src, uint32_t a, uint32
     return 0;
 }
 
-template <int RS>
+// kFallback = false: the fast path; a group whose buckets overflow kMaxBucket
+// is appended to `spill` untouched (nothing written) and sorted later by the
+// kFallback = true instance (stable LSD only), launched once per sort on the
+// collected list. Keeping the LSD code out of the fast kernel keeps the
+// group's records in registers without spilling.
+template <int RS, bool kFallback>
 __global__ void __launch_bounds__(1024, 1) k_local_sort(uint8_t* __restrict__ data,
                                                         uint8_t* __restrict__ tmp,
                                                         const Group* __restrict__ groups,
                                                         uint32_t ks,
-                                                        LevelCounters* __restrict__ ctr) {
+                                                        LevelCounters* __restrict__ ctr,
+                                                        Group* __restrict__ spill,
+                                                        unsigned int* __restrict__ n_spill,
+                                                        uint32_t spill_cap) {
     using C = LocalCfg<RS>;
     constexpr int T = C::kThreads, IPT = C::kIpt;
     constexpr int KW = RS / 8;
@@ -366,7 +374,15 @@ __global__ void __launch_bounds__(1024, 1) k_local_sort(uint8_t* __restrict__ da
         }
     }
     __syncthreads();
-    const bool fast = s_maxb <= kMaxBucket;
+    const bool fast = !kFallback && s_maxb <= kMaxBucket;
+    if (!kFallback && !fast) {  // hand the untouched group to the LSD instance
+        if (threadIdx.x == 0) {
+            const uint32_t i = atomicAdd(n_spill, 1u);
+            if (i < spill_cap) spill[i] = g;
+            atomicAdd(&ctr->fallback_groups, 1ull);
+        }
+        return;
+    }
 
     if (fast) {
         // 3c. scatter record ids into bucket order (cursor = packed start)
@@ -380,34 +396,44 @@ __global__ void __launch_bounds__(1024, 1) k_local_sort(uint8_t* __restrict__ da
             }
         }
         __syncthreads();
-        // 3d. rank inside the bucket: cnt now holds bucket ends
-#pragma unroll
-        for (int j = 0; j < IPT; ++j) {
-            const uint32_t e = uint32_t(j) * T + threadIdx.x;
-            if (e < n) {
-                const uint32_t w = win[e];
-                const uint32_t b = (w >> shift) & bmask;
-                const uint32_t en = (cnt[b >> 1] >> ((b & 1) * 16)) & 0xFFFFu;
-                const uint32_t st =
-                    b ? (cnt[(b - 1) >> 1] >> (((b - 1) & 1) * 16)) & 0xFFFFu : 0u;
-                uint32_t rank = 0;
-                for (uint32_t q = st; q < en; ++q) {
-                    const uint32_t e2 = slot[q];
-                    const uint32_t w2 = win[e2];
-                    bool less = w2 < w;
-                    if (w2 == w && e2 != e) {
-                        int c = beyond ? cmp_beyond<RS>(src, e2, e, s_L, nL) : 0;
-                        less = c < 0 || (c == 0 && e2 < e);
+        // 3d. order inside each bucket: cnt now holds bucket ends. Thread t
+        // owns the contiguous bucket run [b0, b0+per): work ~ sum(size^2),
+        // no divergence on the largest bucket of a warp.
+        {
+            const uint32_t per = nbk > uint32_t(T) ? nbk / T : 1u;
+            const uint32_t b0 = threadIdx.x * per;
+            if (b0 < nbk) {
+                auto end_of = [&](uint32_t b) { return (cnt[b >> 1] >> ((b & 1) * 16)) & 0xFFFFu; };
+                uint32_t st = b0 ? end_of(b0 - 1) : 0u;
+                for (uint32_t b = b0; b < b0 + per; ++b) {
+                    const uint32_t en = end_of(b);
+                    if (en - st == 1) {
+                        fpos[slot[st]] = uint16_t(st);
+                    } else if (en > st) {
+                        for (uint32_t q = st; q < en; ++q) {
+                            const uint32_t e = slot[q];
+                            const uint32_t w = win[e];
+                            uint32_t rank = 0;
+                            for (uint32_t q2 = st; q2 < en; ++q2) {
+                                const uint32_t e2 = slot[q2];
+                                const uint32_t w2 = win[e2];
+                                bool less = w2 < w;
+                                if (w2 == w && e2 != e) {
+                                    const int c = beyond ? cmp_beyond<RS>(src, e2, e, s_L, nL) : 0;
+                                    less = c < 0 || (c == 0 && e2 < e);
+                                }
+                                rank += less;
+                            }
+                            fpos[e] = uint16_t(st + rank);
+                        }
                     }
-                    rank += less;
+                    st = en;
                 }
-                fpos[e] = uint16_t(st + rank);
             }
         }
         __syncthreads();
-    } else {
+    } else if constexpr (kFallback) {
         // 4. robust stable LSD over the window bytes, then beyond if needed
-        if (threadIdx.x == 0) atomicAdd(&ctr->fallback_groups, 1ull);
         uint16_t *pin = slot, *pout = fpos;
         bool first = true;
         for (int q = int(nwin) - 1; q >= 0; --q) {

@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
     __shared__ unsigned long long s_wsum[8];
     __shared__ uint32_t s_action, s_pnext, s_base, s_ngroups, s_tb0;
     __shared__ uint32_t s_next_idx[kRadix], s_next_tb[kRadix];
+    __shared__ uint32_t s_wbig[8], s_wtiles[8], s_nb_base, s_nt_base;
     __shared__ uint64_t s_gstart[kRadix];
     __shared__ uint32_t s_gsize[kRadix];
     const uint32_t s = blockIdx.x;
@@ -151,11 +152,50 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
         if (cp) emit_copies(A, g.start, g.size, &s_base);
         return;
     }
-    // big children -> next level
+    // big children -> next level: block-scan the flags and tile counts so the
+    // whole block allocates with two atomics
     const unsigned long long cs = s_cnt[tid];
-    s_next_idx[tid] = 0xFFFFFFFFu;
-    if (cs > A.cap_local)
-        s_next_idx[tid] = emit_next(A, g.start + s_off[tid], cs, g.p + 1, cp, &s_next_tb[tid]);
+    const bool big = cs > A.cap_local;
+    const uint32_t nt_child = big ? uint32_t((cs + A.tile - 1) / A.tile) : 0u;
+    {
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, big);
+        uint32_t t = nt_child;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane == 31) s_wbig[warp] = __popc(bal), s_wtiles[warp] = t;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t nb = 0, nt = 0;
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t a = s_wbig[k], b = s_wtiles[k];
+                s_wbig[k] = nb, s_wtiles[k] = nt;
+                nb += a, nt += b;
+            }
+            s_nb_base = nb ? atomicAdd(&A.ctr->n_next, nb) : 0u;
+            s_nt_base = nt ? atomicAdd(&A.ctr->n_next_tiles, nt) : 0u;
+        }
+        __syncthreads();
+        s_next_idx[tid] = 0xFFFFFFFFu;
+        if (big) {
+            const uint32_t idx = s_nb_base + s_wbig[warp] + __popc(bal & lanemask_lt());
+            const uint32_t tb = s_nt_base + s_wtiles[warp] + t - nt_child;
+            Seg nx;
+            nx.start = g.start + s_off[tid];
+            nx.size = cs;
+            nx.p = g.p + 1;
+            nx.parity = cp;
+            nx.tile_base = tb;
+            nx.action = 0;
+            A.next[idx] = nx;
+            for (int w = 0; w < 8; w += 2) A.next_andor[uint64_t(idx) * 8 + w] = ~0ull,
+                                             A.next_andor[uint64_t(idx) * 8 + w + 1] = 0ull;
+            s_next_idx[tid] = idx;
+            s_next_tb[tid] = tb;
+        }
+    }
     // small children -> greedy groups (thread 0, digit order)
     if (tid == 0) {
         uint32_t ng = 0;
@@ -186,9 +226,13 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
         gr.pad = 0;
         A.groups[s_base + tid] = gr;
     }
-    for (int d = 0; d < kRadix; ++d) {
+    // tile -> segment map of the big children: one warp per child
+    for (int d = warp; d < kRadix; d += 8) {
         const uint32_t idx = s_next_idx[d];
-        if (idx != 0xFFFFFFFFu) init_next(A, idx, s_next_tb[d], s_cnt[d]);
+        if (idx == 0xFFFFFFFFu) continue;
+        const uint32_t nt = uint32_t((s_cnt[d] + A.tile - 1) / A.tile);
+        const uint32_t tb = s_next_tb[d];
+        for (uint32_t t = lane; t < nt; t += 32) A.next_tile_seg[tb + t] = idx;
     }
 }
 

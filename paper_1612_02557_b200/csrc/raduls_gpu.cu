@@ -94,7 +94,8 @@ struct Workspace {
     DevBuf<uint16_t> tile_cnt;
     DevBuf<uint32_t> tile_off;
     DevBuf<unsigned long long> status;
-    DevBuf<Group> groups;
+    DevBuf<Group> groups, spill;
+    DevBuf<unsigned int> n_spill;
     DevBuf<CopyRange> copies;
     DevBuf<uint8_t> host_data, host_tmp, map8;
     LevelCounters* h_ctr = nullptr;         // pinned [kMaxLevels]
@@ -182,13 +183,17 @@ void ensure_caps(Workspace& ws, uint64_t n) {
     ws.tile_off.ensure(c.tiles * kRadix);
     ws.status.ensure((c.tiles / kScanChunk + 1) * kRadix);
     ws.groups.ensure(c.groups);
+    ws.spill.ensure(c.groups);
+    ws.n_spill.ensure(1);
     ws.copies.ensure(c.copies);
 }
 
 template <int RS>
 void set_attrs(Workspace& ws) {
     if (ws.attrs_set[RS]) return;
-    RG_CHECK(cudaFuncSetAttribute(k_local_sort<RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RG_CHECK(cudaFuncSetAttribute(k_local_sort<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(LocalCfg<RS>::kSmem)));
+    RG_CHECK(cudaFuncSetAttribute(k_local_sort<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(LocalCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(ScatterCfg<RS>::kSmem)));
@@ -234,9 +239,25 @@ template <int RS>
 void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, uint32_t ks,
                   LevelCounters* ctr, cudaStream_t st) {
     if (!ngroups) return;
-    k_local_sort<RS><<<ngroups, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
-        data, tmp, ws.groups.p, ks, ctr);
+    k_local_sort<RS, false><<<ngroups, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
+        data, tmp, ws.groups.p, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
     RG_LAUNCH_CHECK();
+}
+
+// Groups the fast local sort handed over (duplicate-heavy keys): stable LSD.
+// Reads the spill count (synchronises `st`).
+template <int RS>
+void finish_spilled(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ks, LevelCounters* ctr,
+                    cudaStream_t st) {
+    unsigned int n = 0;
+    RG_CHECK(cudaMemcpyAsync(&n, ws.n_spill.p, sizeof n, cudaMemcpyDeviceToHost, st));
+    RG_CHECK(cudaStreamSynchronize(st));
+    if (!n) return;
+    if (n > ws.spill.cap) throw CudaError{RADULS_GPU_EINTERNAL};
+    k_local_sort<RS, true><<<n, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
+        data, tmp, ws.spill.p, ks, ctr, nullptr, nullptr, 0);
+    RG_LAUNCH_CHECK();
+    RG_CHECK(cudaStreamSynchronize(st));
 }
 
 template <int RS>
@@ -249,12 +270,14 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
     set_attrs<RS>(ws);
     ensure_caps<RS>(ws, n);
     LevelCounters* dctr = ws.ctr.p;
+    RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, sizeof(unsigned int), st));
 
     if (n <= uint64_t(LocalCfg<RS>::kCap)) {  // one group sorts everything, in place
         Group g{0, uint32_t(n), 0, 0, 0};
         RG_CHECK(cudaMemcpyAsync(ws.groups.p, &g, sizeof g, cudaMemcpyHostToDevice, st));
         RG_CHECK(cudaMemsetAsync(dctr, 0, sizeof(LevelCounters), st));
         launch_local<RS>(ws, data, tmp, 1, ks, dctr, st);
+        finish_spilled<RS>(ws, data, tmp, ks, dctr, st);
         RG_CHECK(cudaMemcpyAsync(ws.h_ctr, dctr, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
         RG_CHECK(cudaStreamSynchronize(st));
         stats.levels = 1;
@@ -347,6 +370,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         RG_CHECK(cudaMemsetAsync(dctr + level, 0, sizeof(LevelCounters), st));
         level_counts<RS>(ws, data, tmp, cur, ntiles, dctr + level, st);
     }
+    finish_spilled<RS>(ws, data, tmp, ks, dctr, st);
     RG_CHECK(cudaMemcpyAsync(ws.h_ctr, dctr, sizeof(LevelCounters) * level, cudaMemcpyDeviceToHost, st));
     RG_CHECK(cudaStreamSynchronize(st));
     stats.levels = level;
@@ -695,7 +719,7 @@ void raduls_gpu_release(void) {
         for (int b = 0; b < 2; ++b) {
             w->segs[b].release(); w->seg_tot[b].release(); w->seg_andor[b].release(); w->tile_seg[b].release();
         }
-        w->tile_cnt.release(); w->tile_off.release(); w->status.release(); w->groups.release();
+        w->tile_cnt.release(); w->tile_off.release(); w->status.release(); w->groups.release(); w->spill.release(); w->n_spill.release();
         w->copies.release(); w->host_data.release(); w->host_tmp.release(); w->map8.release();
         if (w->h_ctr) cudaFreeHost(w->h_ctr);
         if (w->h_small) cudaFreeHost(w->h_small);
