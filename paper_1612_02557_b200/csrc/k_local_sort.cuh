@@ -16,8 +16,9 @@
 //   2. AND/OR of the key words over the group gives the varying key bytes
 //      L = l0 < l1 < ... in [p, ks); the first <= 4 are packed big-endian into
 //      a 32-bit window w per record (shared memory);
-//   3. fast path — one counting pass: bucket = the top B varying bits of w
-//      (B ~ log2 n, so buckets hold ~1 record), shared-memory histogram, scan,
+//   3. fast path — one counting pass: ~n buckets spread linearly over the
+//      group's window range [min w, max w] (so buckets hold ~1 record for
+//      uniformly distributed bytes), shared-memory histogram, scan,
 //      scatter of record ids into bucket order; then every record ranks itself
 //      inside its bucket by (w, remaining key bytes, input index). That is a
 //      comparison sort of ~1-2 records per bucket — the GPU counterpart of the
@@ -48,7 +49,7 @@ struct LocalCfg {
     static constexpr size_t kSmem = size_t(kCap) * (4 + 2 + 2) + size_t(kCntBytes);
 };
 
-constexpr uint32_t kMaxBucket = 48;
+constexpr uint32_t kMaxBucket = 32;
 
 // Block-wide exclusive scan of one u32 per thread (blockDim 1024).
 __device__ __forceinline__ uint32_t block_scan_excl_1024(uint32_t v, uint32_t* s_w,
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(1024, 1) k_local_sort(uint8_t* __restrict__ da
     __shared__ uint32_t s_tot[512];
     __shared__ unsigned long long s_and[32][KW], s_or[32][KW];
     __shared__ uint32_t s_L[32];
-    __shared__ uint32_t s_nL, s_flag, s_maxb, s_hb;
+    __shared__ uint32_t s_nL, s_flag, s_maxb, s_wmin, s_wmax;
     __shared__ uint32_t s_scan[65];
 
     const Group g = groups[blockIdx.x];
@@ -277,10 +278,9 @@ __global__ void __launch_bounds__(1024, 1) k_local_sort(uint8_t* __restrict__ da
         }
         const uint32_t vm = __ballot_sync(0xFFFFFFFFu, diffb != 0);
         if (diffb) s_L[__popc(vm & lanemask_lt())] = lane;
-        const uint32_t first = vm ? uint32_t(__ffs(vm) - 1) : 0u;
-        const uint32_t x0 = __shfl_sync(0xFFFFFFFFu, diffb, first);
         if (lane == 0) {
-            s_hb = x0 ? 24u + (31u - __clz(x0)) : 31u;
+            s_wmin = 0xFFFFFFFFu;
+            s_wmax = 0u;
             s_nL = __popc(vm);
             s_flag = 0;
             s_maxb = 0;
@@ -316,24 +316,49 @@ __global__ void __launch_bounds__(1024, 1) k_local_sort(uint8_t* __restrict__ da
             }
         }
     }
-    // bucket geometry: the top B bits below the window's highest varying bit
-    // (byte L0 varies, so that bit is in [24, 31]).
+    // bucket geometry: nbk ~ n buckets spread linearly over the window range
+    // [wmin, wmax] of the group (block min/max), so uniformly distributed key
+    // bytes give ~1 record per bucket whatever the group's digit span.
+    {
+        uint32_t mn = 0xFFFFFFFFu, mx = 0u;
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            const uint32_t e = uint32_t(j) * T + threadIdx.x;
+            if (e < n) {
+                const uint32_t w = win[e];
+                mn = min(mn, w);
+                mx = max(mx, w);
+            }
+        }
+        mn = __reduce_min_sync(0xFFFFFFFFu, mn);
+        mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+        if (lane == 0) {
+            atomicMin(&s_wmin, mn);
+            atomicMax(&s_wmax, mx);
+        }
+    }
     uint32_t B = 32u - __clz(n - 1);  // ceil(log2 n)
     B = B < 1 ? 1 : (B > uint32_t(C::kBucketBits) ? uint32_t(C::kBucketBits) : B);
-    const uint32_t hb = s_hb;  // window bit of the highest varying key bit (byte L0)
-    const uint32_t shift = hb + 1u - B;  // >= 24+1-14 > 0
-    const uint32_t bmask = (1u << B) - 1u;
     const uint32_t nbk = 1u << B;
     const bool beyond = nL > 4;
-
     // 3a. bucket histogram (packed u16 pairs)
     for (uint32_t i = threadIdx.x; i < nbk / 2; i += T) cnt[i] = 0;
     __syncthreads();
+    const uint32_t wmin = s_wmin;
+    const uint32_t range = s_wmax - wmin;
+    // bucket(w) = floor((w - wmin) * nbk / (range + 1)), monotone in w, < nbk
+    const bool exact = uint64_t(range) + 1 <= nbk;
+    const unsigned long long mul =
+        exact ? 0ull : (((unsigned long long)nbk << 32) / (uint64_t(range) + 1));
+    auto bucket_of = [&](uint32_t w) -> uint32_t {
+        const uint32_t d = w - wmin;
+        return exact ? d : uint32_t((uint64_t(d) * mul) >> 32);
+    };
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
         const uint32_t e = uint32_t(j) * T + threadIdx.x;
         if (e < n) {
-            const uint32_t b = (win[e] >> shift) & bmask;
+            const uint32_t b = bucket_of(win[e]);
             atomicAdd(&cnt[b >> 1], 1u << ((b & 1) * 16));
         }
     }
@@ -390,7 +415,7 @@ __global__ void __launch_bounds__(1024, 1) k_local_sort(uint8_t* __restrict__ da
         for (int j = 0; j < IPT; ++j) {
             const uint32_t e = uint32_t(j) * T + threadIdx.x;
             if (e < n) {
-                const uint32_t b = (win[e] >> shift) & bmask;
+                const uint32_t b = bucket_of(win[e]);
                 const uint32_t old = atomicAdd(&cnt[b >> 1], 1u << ((b & 1) * 16));
                 slot[(old >> ((b & 1) * 16)) & 0xFFFFu] = uint16_t(e);
             }

@@ -31,6 +31,7 @@
 #include "common.cuh"
 #include "k_histogram.cuh"
 #include "k_local_sort.cuh"
+#include "k_local_smem.cuh"
 #include "k_partition.cuh"
 #include "k_plan.cuh"
 #include "k_scan.cuh"
@@ -154,6 +155,14 @@ uint32_t first_varying_byte(const unsigned long long* andor, uint32_t from, uint
     return ks;
 }
 
+// Local-sort group capacity: the register variant for 8-B records (C2 needs
+// ~17 K-record groups), the shared-memory variant otherwise.
+template <int RS>
+constexpr uint32_t local_cap() {
+    if constexpr (RS == 8) return LocalCfg<RS>::kCap;
+    else return LocalSmemCfg<RS>::kCap;
+}
+
 // Capacities for a sort of n records.
 struct Caps {
     size_t seg, tiles, groups, copies;
@@ -161,7 +170,7 @@ struct Caps {
 
 template <int RS>
 Caps caps_for(uint64_t n) {
-    const uint64_t cap_local = LocalCfg<RS>::kCap;
+    const uint64_t cap_local = local_cap<RS>();
     Caps c;
     c.seg = size_t(n / (cap_local + 1) + 2);
     c.tiles = size_t(n / ScatterCfg<RS>::kTile + c.seg + 2);
@@ -191,10 +200,17 @@ void ensure_caps(Workspace& ws, uint64_t n) {
 template <int RS>
 void set_attrs(Workspace& ws) {
     if (ws.attrs_set[RS]) return;
-    RG_CHECK(cudaFuncSetAttribute(k_local_sort<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(LocalCfg<RS>::kSmem)));
-    RG_CHECK(cudaFuncSetAttribute(k_local_sort<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(LocalCfg<RS>::kSmem)));
+    if constexpr (RS == 8) {
+        RG_CHECK(cudaFuncSetAttribute(k_local_sort<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(LocalCfg<RS>::kSmem)));
+        RG_CHECK(cudaFuncSetAttribute(k_local_sort<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(LocalCfg<RS>::kSmem)));
+    } else {
+        RG_CHECK(cudaFuncSetAttribute(k_local_smem<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(LocalSmemCfg<RS>::kSmem)));
+        RG_CHECK(cudaFuncSetAttribute(k_local_smem<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(LocalSmemCfg<RS>::kSmem)));
+    }
     RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(ScatterCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -239,8 +255,12 @@ template <int RS>
 void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, uint32_t ks,
                   LevelCounters* ctr, cudaStream_t st) {
     if (!ngroups) return;
-    k_local_sort<RS, false><<<ngroups, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
-        data, tmp, ws.groups.p, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
+    if constexpr (RS == 8)
+        k_local_sort<RS, false><<<ngroups, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
+            data, tmp, ws.groups.p, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
+    else
+        k_local_smem<RS, false><<<ngroups, LocalSmemCfg<RS>::kThreads, LocalSmemCfg<RS>::kSmem, st>>>(
+            data, tmp, ws.groups.p, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
     RG_LAUNCH_CHECK();
 }
 
@@ -254,8 +274,12 @@ void finish_spilled(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ks, Lev
     RG_CHECK(cudaStreamSynchronize(st));
     if (!n) return;
     if (n > ws.spill.cap) throw CudaError{RADULS_GPU_EINTERNAL};
-    k_local_sort<RS, true><<<n, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
-        data, tmp, ws.spill.p, ks, ctr, nullptr, nullptr, 0);
+    if constexpr (RS == 8)
+        k_local_sort<RS, true><<<n, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
+            data, tmp, ws.spill.p, ks, ctr, nullptr, nullptr, 0);
+    else
+        k_local_smem<RS, true><<<n, LocalSmemCfg<RS>::kThreads, LocalSmemCfg<RS>::kSmem, st>>>(
+            data, tmp, ws.spill.p, ks, ctr, nullptr, nullptr, 0);
     RG_LAUNCH_CHECK();
     RG_CHECK(cudaStreamSynchronize(st));
 }
@@ -272,7 +296,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
     LevelCounters* dctr = ws.ctr.p;
     RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, sizeof(unsigned int), st));
 
-    if (n <= uint64_t(LocalCfg<RS>::kCap)) {  // one group sorts everything, in place
+    if (n <= uint64_t(local_cap<RS>())) {  // one group sorts everything, in place
         Group g{0, uint32_t(n), 0, 0, 0};
         RG_CHECK(cudaMemcpyAsync(ws.groups.p, &g, sizeof g, cudaMemcpyHostToDevice, st));
         RG_CHECK(cudaMemsetAsync(dctr, 0, sizeof(LevelCounters), st));
@@ -341,7 +365,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         A.ctr = c;
         A.ks = ks;
         A.tile = TILE;
-        A.cap_local = LocalCfg<RS>::kCap;
+        A.cap_local = local_cap<RS>();
         k_plan<<<nseg, 256, 0, st>>>(A);
         RG_LAUNCH_CHECK();
         RG_CHECK(cudaMemcpyAsync(ws.h_ctr + level, c, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));

@@ -237,9 +237,9 @@ def check_sorted(data, n: int, layout: RecordLayout, stream=None) -> tuple[int, 
     return v.value, f.value
 
 
-# Local-sort group capacity per record size (mirrors LocalCfg<RS>::kCap in
-# csrc/k_local_sort.cuh; used by tests to aim at boundaries).
-_LOCAL_CAP = {8: 1024 * 20, 16: 1024 * 10, 24: 1024 * 7, 32: 1024 * 5}
+# Local-sort group capacity per record size (mirrors local_cap<RS>() in
+# csrc/raduls_gpu.cu; used by tests to aim at boundaries).
+_LOCAL_CAP = {8: 1024 * 20, 16: 3584, 24: 2560, 32: 4608}
 
 
 def local_capacity(record_size: int) -> int:
