@@ -90,6 +90,19 @@ typedef struct {
 
 int raduls_gpu_last_stats(raduls_gpu_stats* out);
 
+/* Per-kernel device time of the most recent sort, when profiling is on
+ * (CUDA events recorded around every launch on the sort's stream; adds a few
+ * microseconds per launch). Classes: sample, tile_hist, tile_scan, plan,
+ * scatter, local_sort, copy_back. */
+typedef struct {
+    char name[16];
+    uint32_t launches;
+    double ms;
+} raduls_gpu_kernel_time;
+
+int raduls_gpu_set_profiling(int on);
+int raduls_gpu_last_kernel_times(raduls_gpu_kernel_time* out, int capacity, int* count);
+
 /*
  * Building blocks (tests, benchmarks and the multi-GPU driver). All device
  * pointers; asynchronous on `stream` unless noted.
@@ -112,6 +125,12 @@ int raduls_gpu_histogram(const void* d_data, uint64_t n_recs, uint32_t rec_size,
  * global index index_base + i. */
 int raduls_gpu_generate(void* d_out, uint64_t n_recs, uint32_t rec_size, uint32_t key_size,
                         uint32_t dist, uint64_t seed, uint64_t index_base, void* stream);
+
+/* AND / OR of every 64-bit record word over the array (h_andor: host [8] u64,
+ * and at 2w, or at 2w+1); a key byte is constant iff its AND and OR bytes
+ * agree. Synchronous. */
+int raduls_gpu_andor(const void* d_data, uint64_t n_recs, uint32_t rec_size, uint64_t* h_andor,
+                     void* stream);
 
 /* array_digest (reference verify.cpp:37-50). Synchronous. */
 int raduls_gpu_digest(const void* d_data, uint64_t n_recs, uint32_t rec_size, uint64_t* lo,

@@ -18,8 +18,10 @@ from .raduls import (  # noqa: F401
     digest,
     generate,
     histogram,
+    last_kernel_times,
     last_stats,
     local_capacity,
+    set_profiling,
     sort,
     sort_device,
     split,

@@ -31,6 +31,9 @@ EXPORTED = [
     "raduls_gpu_prefix_histogram",
     "raduls_gpu_partition",
     "raduls_gpu_release",
+    "raduls_gpu_set_profiling",
+    "raduls_gpu_last_kernel_times",
+    "raduls_gpu_andor",
 ]
 
 
@@ -48,6 +51,10 @@ class Stats(C.Structure):
 
     def as_dict(self) -> dict:
         return {f: int(getattr(self, f)) for f, _ in self._fields_}
+
+
+class KernelTime(C.Structure):
+    _fields_ = [("name", C.c_char * 16), ("launches", C.c_uint32), ("ms", C.c_double)]
 
 
 _lock = threading.Lock()
@@ -92,6 +99,10 @@ def load(build_if_missing: bool = False):
         L.raduls_gpu_prefix_histogram.argtypes = [_vp, _u64, _u32, _u32, _u32, _vp, _vp]
         L.raduls_gpu_partition.argtypes = [_vp, _vp, _u64, _u32, _u32, _u32, _vp, _u32, _u64p, _vp]
         L.raduls_gpu_release.restype = None
+        L.raduls_gpu_set_profiling.argtypes = [C.c_int]
+        L.raduls_gpu_andor.argtypes = [_vp, _u64, _u32, _u64p, _vp]
+        L.raduls_gpu_last_kernel_times.argtypes = [C.POINTER(KernelTime), C.c_int,
+                                                   C.POINTER(C.c_int)]
         _lib = L
         return L
 

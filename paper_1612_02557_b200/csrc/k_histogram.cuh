@@ -68,6 +68,37 @@ __global__ void __launch_bounds__(256) k_sample_andor(const uint8_t* __restrict_
     }
 }
 
+// AND/OR of every 64-bit record word over the whole array (grid-stride).
+template <int RS>
+__global__ void __launch_bounds__(256) k_andor(const uint8_t* __restrict__ data, uint64_t n,
+                                               unsigned long long* __restrict__ andor) {
+    constexpr int KW = RS / 8;
+    uint64_t a[KW], o[KW];
+#pragma unroll
+    for (int w = 0; w < KW; ++w) a[w] = ~0ull, o[w] = 0ull;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const Rec<RS> r = load_rec_stream<RS>(data, i);
+#pragma unroll
+        for (int w = 0; w < KW; ++w) {
+            const uint64_t v = rec_word64<RS>(r, w);
+            a[w] &= v;
+            o[w] |= v;
+        }
+    }
+#pragma unroll
+    for (int w = 0; w < KW; ++w) {
+        for (int off = 16; off; off >>= 1) {
+            a[w] &= __shfl_xor_sync(0xFFFFFFFFu, a[w], off);
+            o[w] |= __shfl_xor_sync(0xFFFFFFFFu, o[w], off);
+        }
+        if (lane_id() == 0) {
+            atomicAnd(&andor[2 * w], a[w]);
+            atomicOr(&andor[2 * w + 1], o[w]);
+        }
+    }
+}
+
 // Per-tile digit counts of byte segs[s].p for every tile of every segment of
 // the level, plus AND/OR of every record word per segment. One CTA per tile
 // (the scatter's tile partition: kTile records, tile -> segment through

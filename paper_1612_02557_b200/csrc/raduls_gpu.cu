@@ -84,8 +84,55 @@ struct DevBuf {
     }
 };
 
+// Optional per-kernel timing (raduls_gpu_set_profiling): CUDA events around
+// every launch of the sort, on the launching stream, collected at the end of
+// the sort (which synchronises anyway). Used by bench.py for the live
+// roofline of the dominant kernel.
+enum KClass { K_SAMPLE, K_HIST, K_SCAN, K_PLAN, K_SCATTER, K_LOCAL, K_COPY, K_INIT, K_NCLASS };
+static const char* kClassName[K_NCLASS] = {"sample", "tile_hist", "tile_scan", "plan",
+                                           "scatter", "local_sort", "copy_back", "init"};
+
+struct Prof {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> cls;  // per recorded pair
+    size_t used = 0;
+    double ms[K_NCLASS] = {};
+    uint32_t launches[K_NCLASS] = {};
+    void reset() {
+        used = 0;
+        cls.clear();
+        for (int i = 0; i < K_NCLASS; ++i) ms[i] = 0, launches[i] = 0;
+    }
+    int begin(int c, cudaStream_t st) {
+        if (!on) return -1;
+        while (ev.size() < 2 * (used + 1)) {
+            cudaEvent_t e;
+            RG_CHECK(cudaEventCreate(&e));
+            ev.push_back(e);
+        }
+        RG_CHECK(cudaEventRecord(ev[2 * used], st));
+        cls.push_back(c);
+        return int(used++);
+    }
+    void end(int i, cudaStream_t st) {
+        if (i >= 0) RG_CHECK(cudaEventRecord(ev[2 * i + 1], st));
+    }
+    void collect() {  // after the stream has been synchronised
+        for (size_t i = 0; i < used; ++i) {
+            float t = 0.f;
+            RG_CHECK(cudaEventElapsedTime(&t, ev[2 * i], ev[2 * i + 1]));
+            ms[cls[i]] += t;
+            launches[cls[i]]++;
+        }
+        used = 0;
+        cls.clear();
+    }
+};
+
 struct Workspace {
     int device = 0;
+    Prof prof;
     std::mutex mu;
     DevBuf<unsigned long long> hist8, andor0, thr, acc;
     DevBuf<LevelCounters> ctr;
@@ -231,23 +278,29 @@ template <int RS, bool kMap = false>
 void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t ntiles, LevelCounters* c,
                   cudaStream_t st, uint32_t ks = 0, const uint8_t* map = nullptr) {
     constexpr int TILE = ScatterCfg<RS>::kTile;
+    int pe = ws.prof.begin(K_HIST, st);
     k_tile_hist<RS, TILE, kMap><<<ntiles, 256, 0, st>>>(data, tmp, ws.segs[cur].p, ws.tile_seg[cur].p,
                                                         ws.tile_cnt.p, ws.seg_andor[cur].p, c, ks, map);
     RG_LAUNCH_CHECK();
+    ws.prof.end(pe, st);
     const uint32_t nchunks = (ntiles + kScanChunk - 1) / kScanChunk;
     RG_CHECK(cudaMemsetAsync(ws.status.p, 0, size_t(nchunks) * kRadix * sizeof(unsigned long long), st));
+    pe = ws.prof.begin(K_SCAN, st);
     k_tile_scan<TILE><<<nchunks, 256, 0, st>>>(ws.segs[cur].p, ws.tile_seg[cur].p, ws.tile_cnt.p, ntiles,
                                                ws.tile_off.p, ws.seg_tot[cur].p, ws.status.p, c);
     RG_LAUNCH_CHECK();
+    ws.prof.end(pe, st);
 }
 
 template <int RS, bool kMap>
 void launch_scatter(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t ntiles, uint32_t ks,
                     const uint8_t* map, cudaStream_t st) {
     const uint32_t grid = std::min<uint32_t>(ntiles, uint32_t(sm_count()) * 2);
+    const int pe = ws.prof.begin(K_SCATTER, st);
     k_scatter<RS, kMap><<<grid, ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>::kSmem, st>>>(
         data, tmp, ws.segs[cur].p, ws.seg_tot[cur].p, ws.tile_seg[cur].p, ws.tile_off.p, ntiles, ks, map);
     RG_LAUNCH_CHECK();
+    ws.prof.end(pe, st);
 }
 
 // Launch the local sort over `ngroups` groups already in ws.groups.
@@ -255,6 +308,7 @@ template <int RS>
 void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, uint32_t ks,
                   LevelCounters* ctr, cudaStream_t st) {
     if (!ngroups) return;
+    const int pe = ws.prof.begin(K_LOCAL, st);
     if constexpr (RS == 8)
         k_local_sort<RS, false><<<ngroups, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
             data, tmp, ws.groups.p, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
@@ -262,6 +316,7 @@ void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, 
         k_local_smem<RS, false><<<ngroups, LocalSmemCfg<RS>::kThreads, LocalSmemCfg<RS>::kSmem, st>>>(
             data, tmp, ws.groups.p, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
     RG_LAUNCH_CHECK();
+    ws.prof.end(pe, st);
 }
 
 // Groups the fast local sort handed over (duplicate-heavy keys): stable LSD.
@@ -274,6 +329,7 @@ void finish_spilled(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ks, Lev
     RG_CHECK(cudaStreamSynchronize(st));
     if (!n) return;
     if (n > ws.spill.cap) throw CudaError{RADULS_GPU_EINTERNAL};
+    const int pe = ws.prof.begin(K_LOCAL, st);
     if constexpr (RS == 8)
         k_local_sort<RS, true><<<n, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
             data, tmp, ws.spill.p, ks, ctr, nullptr, nullptr, 0);
@@ -281,6 +337,7 @@ void finish_spilled(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ks, Lev
         k_local_smem<RS, true><<<n, LocalSmemCfg<RS>::kThreads, LocalSmemCfg<RS>::kSmem, st>>>(
             data, tmp, ws.spill.p, ks, ctr, nullptr, nullptr, 0);
     RG_LAUNCH_CHECK();
+    ws.prof.end(pe, st);
     RG_CHECK(cudaStreamSynchronize(st));
 }
 
@@ -290,6 +347,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
     constexpr int TILE = ScatterCfg<RS>::kTile;
     raduls_gpu_stats stats{};
     ws.last = stats;
+    ws.prof.reset();
     if (n < 2) return;  // msd_sorter.hpp:51
     set_attrs<RS>(ws);
     ensure_caps<RS>(ws, n);
@@ -304,6 +362,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         finish_spilled<RS>(ws, data, tmp, ks, dctr, st);
         RG_CHECK(cudaMemcpyAsync(ws.h_ctr, dctr, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
         RG_CHECK(cudaStreamSynchronize(st));
+        ws.prof.collect();
         stats.levels = 1;
         stats.local_records = ws.h_ctr[0].moved_local;
         stats.fallback_groups = ws.h_ctr[0].fallback_groups;
@@ -313,11 +372,17 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
 
     // ---- level 0: guess the first varying key byte from a strided sample,
     // histogram the whole array on it, confirm with the global AND/OR.
-    k_init_andor<<<1, 64, 0, st>>>(ws.andor0.p, 1);
-    RG_LAUNCH_CHECK();
+    {
+        const int pi = ws.prof.begin(K_INIT, st);
+        k_init_andor<<<1, 64, 0, st>>>(ws.andor0.p, 1);
+        RG_LAUNCH_CHECK();
+        ws.prof.end(pi, st);
+    }
     const uint32_t samples = uint32_t(std::min<uint64_t>(n, 65536));
+    int pe = ws.prof.begin(K_SAMPLE, st);
     k_sample_andor<RS><<<64, 256, 0, st>>>(data, n, std::max<uint64_t>(1, n / samples), samples, ws.andor0.p);
     RG_LAUNCH_CHECK();
+    ws.prof.end(pe, st);
     RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.andor0.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     RG_CHECK(cudaStreamSynchronize(st));
     uint32_t p0 = first_varying_byte(ws.h_small, 0, ks);
@@ -328,8 +393,16 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         Seg s0{0, n, p0, 0, 0, 0};
         RG_CHECK(cudaMemcpyAsync(ws.segs[0].p, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
         RG_CHECK(cudaMemsetAsync(ws.tile_seg[0].p, 0, nt0 * sizeof(uint32_t), st));
-        k_init_andor<<<1, 64, 0, st>>>(ws.seg_andor[0].p, 1);
-        RG_LAUNCH_CHECK();
+        {
+            const int pi = ws.prof.begin(K_INIT, st);
+            {
+                const int pi = ws.prof.begin(K_INIT, st);
+                k_init_andor<<<1, 64, 0, st>>>(ws.seg_andor[0].p, 1);
+                RG_LAUNCH_CHECK();
+                ws.prof.end(pi, st);
+            }
+            ws.prof.end(pi, st);
+        }
         RG_CHECK(cudaMemsetAsync(dctr, 0, sizeof(LevelCounters), st));
         level_counts<RS>(ws, data, tmp, 0, nt0, dctr, st);
         RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.seg_andor[0].p, 8 * sizeof(unsigned long long),
@@ -337,14 +410,19 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         RG_CHECK(cudaStreamSynchronize(st));
         const uint32_t pg = first_varying_byte(ws.h_small, 0, ks);
         if (pg >= ks) {  // every key equal: a stable sort is the identity
+            ws.prof.collect();
             ws.last = stats;
             return;
         }
         if (pg != p0) {  // a more significant byte varies outside the sample
             s0.p = pg;
             RG_CHECK(cudaMemcpyAsync(ws.segs[0].p, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
-            k_init_andor<<<1, 64, 0, st>>>(ws.seg_andor[0].p, 1);
-            RG_LAUNCH_CHECK();
+            {
+                const int pi = ws.prof.begin(K_INIT, st);
+                k_init_andor<<<1, 64, 0, st>>>(ws.seg_andor[0].p, 1);
+                RG_LAUNCH_CHECK();
+                ws.prof.end(pi, st);
+            }
             level_counts<RS>(ws, data, tmp, 0, nt0, dctr, st);
         }
     }
@@ -366,8 +444,10 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         A.ks = ks;
         A.tile = TILE;
         A.cap_local = local_cap<RS>();
+        pe = ws.prof.begin(K_PLAN, st);
         k_plan<<<nseg, 256, 0, st>>>(A);
         RG_LAUNCH_CHECK();
+        ws.prof.end(pe, st);
         RG_CHECK(cudaMemcpyAsync(ws.h_ctr + level, c, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
         RG_CHECK(cudaStreamSynchronize(st));
         const LevelCounters h = ws.h_ctr[level];
@@ -380,8 +460,10 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         }
         launch_local<RS>(ws, data, tmp, h.n_groups, ks, c, st);
         if (h.n_copy) {
+            pe = ws.prof.begin(K_COPY, st);
             k_copy_back<RS><<<h.n_copy, 256, 0, st>>>(data, tmp, ws.copies.p);
             RG_LAUNCH_CHECK();
+            ws.prof.end(pe, st);
         }
         stats.scatter_records += h.moved_scatter;
         stats.copy_records += h.moved_copy;
@@ -397,6 +479,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
     finish_spilled<RS>(ws, data, tmp, ks, dctr, st);
     RG_CHECK(cudaMemcpyAsync(ws.h_ctr, dctr, sizeof(LevelCounters) * level, cudaMemcpyDeviceToHost, st));
     RG_CHECK(cudaStreamSynchronize(st));
+    ws.prof.collect();
     stats.levels = level;
     for (uint32_t l = 0; l < level; ++l) {
         stats.local_records += ws.h_ctr[l].moved_local;
@@ -731,6 +814,55 @@ int raduls_gpu_partition(const void* d_src, void* d_dst, uint64_t n, uint32_t rs
             if (h_rank_counts) std::memcpy(h_rank_counts, tot, n_ranks * sizeof(uint64_t));
             single_segment_scatter<RSC, true>(ws, src, static_cast<uint8_t*>(d_dst), n, ks, ws.map8.p, tot, st);
         });
+    });
+}
+
+int raduls_gpu_andor(const void* d_data, uint64_t n, uint32_t rs, uint64_t* h_andor, void* stream) {
+    if (!layout_ok(rs, rs) || mul_overflows(n, rs) || !h_andor) return RADULS_GPU_EINVAL;
+    if (n && !aligned_ok(d_data, rs)) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        k_init_andor<<<1, 64, 0, st>>>(ws.andor0.p, 1);
+        RG_LAUNCH_CHECK();
+        if (n) {
+            dispatch_rs(rs, [&](auto R) {
+                k_andor<decltype(R)::value><<<grid_for(n, 256, 8), 256, 0, st>>>(
+                    static_cast<const uint8_t*>(d_data), n, ws.andor0.p);
+            });
+            RG_LAUNCH_CHECK();
+        }
+        RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.andor0.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        RG_CHECK(cudaStreamSynchronize(st));
+        std::memcpy(h_andor, ws.h_small, 8 * sizeof(uint64_t));
+    });
+}
+
+int raduls_gpu_set_profiling(int on) {
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        ws.prof.on = on != 0;
+    });
+}
+
+int raduls_gpu_last_kernel_times(raduls_gpu_kernel_time* out, int capacity, int* count) {
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        int k = 0;
+        for (int c = 0; c < K_NCLASS; ++c) {
+            if (!ws.prof.launches[c]) continue;
+            if (out && k < capacity) {
+                std::memset(&out[k], 0, sizeof out[k]);
+                std::snprintf(out[k].name, sizeof out[k].name, "%s", kClassName[c]);
+                out[k].launches = ws.prof.launches[c];
+                out[k].ms = ws.prof.ms[c];
+            }
+            ++k;
+        }
+        if (count) *count = k;
     });
 }
 

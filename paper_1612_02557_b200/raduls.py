@@ -31,6 +31,7 @@ __all__ = [
     "RecordLayout", "SchedulerConfig", "TinyPolicy", "BigBinFraction", "ResourceError",
     "CudaError", "sort", "sort_device", "split", "histogram", "generate", "digest",
     "check_sorted", "last_stats", "DIST_UNIFORM", "DIST_SKEW", "local_capacity",
+    "set_profiling", "last_kernel_times",
 ]
 
 DIST_UNIFORM = 0
@@ -181,6 +182,21 @@ def last_stats() -> dict:
     s = _lib.Stats()
     _raise(_lib.load().raduls_gpu_last_stats(C.byref(s)), "raduls_gpu_last_stats")
     return s.as_dict()
+
+
+def set_profiling(on: bool) -> None:
+    """Per-kernel CUDA-event timing of subsequent sorts (raduls_gpu_set_profiling)."""
+    _raise(_lib.load().raduls_gpu_set_profiling(1 if on else 0), "raduls_gpu_set_profiling")
+
+
+def last_kernel_times() -> dict:
+    """{kernel class: (launches, ms)} of the most recent sort (profiling on)."""
+    buf = (_lib.KernelTime * 16)()
+    cnt = C.c_int(0)
+    _raise(_lib.load().raduls_gpu_last_kernel_times(buf, 16, C.byref(cnt)),
+           "raduls_gpu_last_kernel_times")
+    return {buf[i].name.decode(): (int(buf[i].launches), float(buf[i].ms))
+            for i in range(min(cnt.value, 16))}
 
 
 def split(src, dst, n: int, record_size: int, key_byte_offset: int, stream=None) -> np.ndarray:
