@@ -551,6 +551,7 @@ int raduls_gpu_sort(void* d_data, void* d_tmp, uint64_t n, uint32_t rs, uint32_t
     if (!layout_ok(rs, ks) || mul_overflows(n, rs) || n > kMaxRecords) return RADULS_GPU_EINVAL;
     if (n >= 2 && (!d_data || !aligned_ok(d_data, rs) || (d_tmp && !aligned_ok(d_tmp, rs))))
         return RADULS_GPU_EINVAL;
+    if (n < 2) return RADULS_GPU_OK;  // msd_sorter.hpp:51: nothing to do, nothing allocated
     return guarded([&] {
         Workspace& ws = workspace();
         std::lock_guard<std::mutex> lk(ws.mu);

@@ -1,0 +1,73 @@
+"""CPU: the C-ABI library loads and exports every entry point include/raduls_gpu.h
+declares; host-side argument validation works without a GPU (errors are
+reported before any device work, like the reference's std::invalid_argument,
+P/include/raduls/detail/dispatch.hpp:37-39)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1612_02557_b200 as rg
+from paper_1612_02557_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "raduls_gpu.h")
+
+
+def declared_functions():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(raduls_gpu_\w+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.load()
+    names = declared_functions()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(L, name), f"{name} missing from libraduls_gpu.so"
+    assert set(_lib.EXPORTED) <= set(names)
+
+
+def test_no_oracle_in_product():
+    """The product package never imports the oracle (test infrastructure)."""
+    pkg = os.path.join(ROOT, "paper_1612_02557_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f), errors="ignore").read()
+                assert "import oracle" not in src and "liboracle" not in src, f
+
+
+def test_layout_validation_matches_reference_table():
+    L = _lib.load()
+    # reference valid set (P/include/raduls/layout.hpp:22-27) plus widened key sizes
+    for rs, ks in [(8, 8), (16, 8), (16, 16), (24, 8), (24, 16), (32, 8), (32, 16), (32, 24),
+                   (16, 1), (32, 32)]:
+        assert L.raduls_gpu_layout_valid(rs, ks) == 1
+        assert rg.RecordLayout(rs, ks).valid()
+    for rs, ks in [(8, 16), (12, 8), (16, 12 + 8), (40, 8), (0, 8), (16, 0)]:
+        assert L.raduls_gpu_layout_valid(rs, ks) == 0
+
+
+def test_invalid_arguments_rejected_without_gpu():
+    L = _lib.load()
+    assert L.raduls_gpu_sort(None, None, 10, 12, 8, None) == _lib.EINVAL
+    assert L.raduls_gpu_sort(None, None, 10, 16, 17, None) == _lib.EINVAL
+    assert L.raduls_gpu_sort(None, None, 2**62, 16, 8, None) == _lib.EINVAL  # size overflow
+    assert L.raduls_gpu_sort(None, None, 10, 16, 8, None) == _lib.EINVAL      # null data
+    assert L.raduls_gpu_sort(8, None, 10, 16, 8, None) == _lib.EINVAL         # misaligned
+    assert L.raduls_gpu_sort_host(None, None, 10, 8, 8) == _lib.EINVAL
+    assert L.raduls_gpu_sort(None, None, 1, 16, 8, None) == _lib.OK           # n < 2: no-op
+    assert L.raduls_gpu_sort_host(None, None, 0, 16, 8) == _lib.OK
+    assert "invalid" in _lib.strerror(_lib.EINVAL)
+    with pytest.raises(ValueError, match="unsupported record layout"):
+        rg.sort(np.zeros(64, dtype=np.uint8), 2, rg.RecordLayout(8, 16))
+
+
+def test_version_and_stats_struct():
+    L = _lib.load()
+    assert L.raduls_gpu_version() >= 0x000100
+    assert C.sizeof(_lib.Stats) == 4 + 4 + 6 * 8
