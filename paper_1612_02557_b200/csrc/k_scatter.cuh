@@ -30,11 +30,12 @@ namespace rg {
 template <int RS>
 struct ScatterCfg {
     static constexpr int kThreads = 256;
-    static constexpr int kItems = RS == 8 ? 16 : RS == 16 ? 8 : RS == 24 ? 5 : 4;
+    static constexpr int kItems = RS == 8 ? 12 : RS == 16 ? 8 : RS == 24 ? 5 : 4;
     static constexpr int kTile = kThreads * kItems;
     static constexpr int kWarps = kThreads / 32;
+    static constexpr int kStages = 3;  // tile buffers in the TMA ring
     static constexpr int kBufBytes = ((kTile * RS + 16 + 127) / 128) * 128;  // + alignment slack
-    static constexpr size_t kSmem = size_t(2) * kBufBytes + size_t(kTile) * 3;  // 2 buffers + map + digit
+    static constexpr size_t kSmem = size_t(kStages) * kBufBytes + size_t(kTile) * 3;  // ring + map + digit
 };
 
 // Exclusive scan of one u32 per thread over the 256 consumer threads (named
@@ -100,21 +101,22 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
     constexpr int T = C::kThreads, IT = C::kItems, W = C::kWarps;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* buf0 = smem;
-    uint16_t* s_map = reinterpret_cast<uint16_t*>(smem + 2 * C::kBufBytes);
+    constexpr int S = C::kStages;
+    uint16_t* s_map = reinterpret_cast<uint16_t*>(smem + S * C::kBufBytes);
     uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_map + C::kTile);
-    __shared__ uint32_t s_wcnt[W][kRadix];
+    __shared__ uint16_t s_wcnt[W][kRadix];  // per-warp digit counts, then warp-exclusive offsets
     __shared__ uint32_t s_lstart[kRadix];
     __shared__ long long s_gdelta[kRadix];
     __shared__ uint32_t s_scan[8];
-    __shared__ __align__(8) unsigned long long s_full[2], s_empty[2];
-    __shared__ TileInfo s_info[2];
+    __shared__ __align__(8) unsigned long long s_full[C::kStages], s_empty[C::kStages];
+    __shared__ TileInfo s_info[C::kStages];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
-        mbar_init(&s_full[0], 1);
-        mbar_init(&s_full[1], 1);
-        mbar_init(&s_empty[0], 1);
-        mbar_init(&s_empty[1], 1);
+        for (int q = 0; q < S; ++q) {
+            mbar_init(&s_full[q], 1);
+            mbar_init(&s_empty[q], 1);
+        }
         fence_mbar_init();
     }
     __syncthreads();
@@ -130,8 +132,8 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
                 g = segs[s];
                 if (g.action != kActScatter) continue;  // constant byte / finished: not split
             }
-            const int b = it & 1;
-            if (it >= 2) mbar_wait(&s_empty[b], ((it >> 1) - 1) & 1u);
+            const int b = it % S;
+            if (it >= uint32_t(S)) mbar_wait(&s_empty[b], ((it / S) - 1) & 1u);
             ++it;
             TileInfo ti;
             ti.tile = tile;
@@ -169,10 +171,10 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
     // ------------------------------------------------------------ consumers
     const uint32_t lt = lanemask_lt();
     for (uint32_t it = 0;; ++it) {
-        const int b = it & 1;
+        const int b = it % S;
 #pragma unroll
         for (int q = 0; q < kRadix / 32; ++q) s_wcnt[warp][q * 32 + lane] = 0;
-        mbar_wait(&s_full[b], (it >> 1) & 1u);
+        mbar_wait(&s_full[b], (it / S) & 1u);
         const TileInfo ti = s_info[b];
         if (ti.tile >= n_tiles) break;
         // this thread's digit: base inside the segment + offset of the tile
@@ -194,7 +196,8 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
             const uint32_t peers = match_digit8(d, valid);
             const uint32_t before = valid ? s_wcnt[warp][d] : 0u;
             __syncwarp();
-            if (valid && uint32_t(lane) == 31u - __clz(peers)) s_wcnt[warp][d] = before + __popc(peers);
+            if (valid && uint32_t(lane) == 31u - __clz(peers))
+                s_wcnt[warp][d] = uint16_t(before + __popc(peers));
             __syncwarp();
             pk[j] = valid ? (d | ((before + __popc(peers & lt)) << 9)) : 0x100u;
         }
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
 #pragma unroll
             for (int w = 0; w < W; ++w) {
                 const uint32_t c = s_wcnt[w][d];
-                s_wcnt[w][d] = tcount;
+                s_wcnt[w][d] = uint16_t(tcount);
                 tcount += c;
             }
         }
