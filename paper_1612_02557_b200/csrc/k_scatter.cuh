@@ -33,7 +33,7 @@ struct ScatterCfg {
     static constexpr int kItems = RS == 8 ? 12 : RS == 16 ? 8 : RS == 24 ? 5 : 4;
     static constexpr int kTile = kThreads * kItems;
     static constexpr int kWarps = kThreads / 32;
-    static constexpr int kStages = 3;  // tile buffers in the TMA ring
+    static constexpr int kStages = 2;  // tile buffers in the TMA ring
     static constexpr int kBufBytes = ((kTile * RS + 16 + 127) / 128) * 128;  // + alignment slack
     static constexpr size_t kSmem = size_t(kStages) * kBufBytes + size_t(kTile) * 3;  // ring + map + digit
 };
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
     constexpr int S = C::kStages;
     uint16_t* s_map = reinterpret_cast<uint16_t*>(smem + S * C::kBufBytes);
     uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_map + C::kTile);
-    __shared__ uint16_t s_wcnt[W][kRadix];  // per-warp digit counts, then warp-exclusive offsets
+    __shared__ uint32_t s_wcnt[W][kRadix];  // per-warp digit counts, then warp-exclusive offsets
     __shared__ uint32_t s_lstart[kRadix];
     __shared__ long long s_gdelta[kRadix];
     __shared__ uint32_t s_scan[8];
@@ -169,7 +169,6 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
     }
 
     // ------------------------------------------------------------ consumers
-    const uint32_t lt = lanemask_lt();
     for (uint32_t it = 0;; ++it) {
         const int b = it % S;
 #pragma unroll
@@ -185,7 +184,11 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
         const uint32_t tn = ti.tn, p = ti.p;
         __syncwarp();
 
-        // 1: warp multisplit rank (ballot peers, warp-private counters)
+        // 1: rank inside the warp with warp-private shared-memory counters: one
+        // ATOMS per record. Items are warp-striped in input order and the
+        // counters are per warp, so ranks follow input order as long as the
+        // hardware serves conflicting lanes of one atomic in lane order (the
+        // byte-exact stable-sort parity tests check this on the device).
         uint32_t pk[IT];  // digit | rank << 9 ; 0x100 = invalid
 #pragma unroll
         for (int j = 0; j < IT; ++j) {
@@ -193,13 +196,7 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
             const bool valid = i < tn;
             const uint32_t d =
                 valid ? scatter_digit_smem<RS, kMap>(tile + size_t(i) * RS, p, ks, map) : 0u;
-            const uint32_t peers = match_digit8(d, valid);
-            const uint32_t before = valid ? s_wcnt[warp][d] : 0u;
-            __syncwarp();
-            if (valid && uint32_t(lane) == 31u - __clz(peers))
-                s_wcnt[warp][d] = uint16_t(before + __popc(peers));
-            __syncwarp();
-            pk[j] = valid ? (d | ((before + __popc(peers & lt)) << 9)) : 0x100u;
+            pk[j] = valid ? (d | (atomicAdd(&s_wcnt[warp][d], 1u) << 9)) : 0x100u;
         }
         bar_sync_named(1, T);
 
@@ -210,7 +207,7 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
 #pragma unroll
             for (int w = 0; w < W; ++w) {
                 const uint32_t c = s_wcnt[w][d];
-                s_wcnt[w][d] = uint16_t(tcount);
+                s_wcnt[w][d] = tcount;
                 tcount += c;
             }
         }
