@@ -1,0 +1,565 @@
+// (d) segmented small-bin sort for the MSD tail.
+//
+// Reference: the tiny-bin comparison sorts (P/include/raduls/small_sorts.hpp:
+// 48-191: insertion / Shell {8,1} / introsort chosen by TinyPolicy :14-45), the
+// plain radix_split used for bins that fit half of L2 (kernels.hpp:157-167 via
+// msd_sorter.hpp:188-196) and finalize()'s copy back to the caller's buffer
+// (msd_sorter.hpp:76-80).
+//
+// One CTA sorts a *group*: one or more adjacent complete segments (bins) of at
+// most kCap records that share key bytes [0, p). Sorting the group by key bytes
+// [p, ks) equals sorting each bin on its own (the bins are contiguous and
+// already in key order). The whole group is held on chip before anything is
+// written, so the sort is safe in place (source == destination buffer):
+//   * record sizes 16/24/32: one TMA bulk copy (cp.async.bulk + mbarrier) puts
+//     the group in shared memory; the output walks final positions in order
+//     (coalesced vector stores) reading records from shared memory;
+//   * record size 8 (groups up to 20 K records, BASELINE C2's 16 K-record
+//     bins): records stay in registers and each thread stores its own records
+//     at their final positions.
+// Steps: AND/OR of the key words (REDUX) -> the varying key bytes
+// L = l0 < l1 < ... in [p, ks); their first <= 4 form a big-endian 32-bit
+// window w per record; one counting pass over ~n buckets spread linearly over
+// [min w, max w] (histogram, scan, scatter of record ids); then each slot ranks
+// its record inside its (tiny) bucket by (w, remaining key bytes, input index)
+// with warp shuffles over neighbouring slots. Duplicate-heavy groups (a bucket
+// over kMaxBucket) are handed untouched to the kFallback instance: a stable LSD
+// over every varying byte. Every path orders equal keys by input index, so the
+// sort is stable.
+#pragma once
+
+#include "common.cuh"
+
+namespace rg {
+
+constexpr uint32_t kMaxBucket = 32;
+
+template <int RS>
+struct LocalCfg {
+    static constexpr bool kRegRecords = RS == 8;  // records in registers (else shared memory)
+    static constexpr int kThreads = kRegRecords ? 1024 : 512;
+    static constexpr int kWarps = kThreads / 32;
+    static constexpr int kCap = RS == 8 ? 20480 : RS == 16 ? 3584 : RS == 24 ? 2560 : 4608;
+    static constexpr int kIpt = (kCap + kThreads - 1) / kThreads;
+    static constexpr int kBucketBits = RS == 8 ? 14 : 13;
+    static constexpr int kCntBytes = ((1 << kBucketBits) * 2 > kWarps * kRadix * 4)
+                                         ? (1 << kBucketBits) * 2
+                                         : kWarps * kRadix * 4;
+    static constexpr int kRecBytes = kRegRecords ? 0 : ((kCap * RS + 16 + 127) / 128) * 128;
+    static constexpr size_t kSmem = size_t(kRecBytes) + size_t(kCap) * (4 + 2 + 2) + kCntBytes;
+};
+
+// Block-wide exclusive scan (blockDim a multiple of 32, <= 1024).
+__device__ __forceinline__ uint32_t block_scan_excl(uint32_t v, uint32_t* s_w, uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+        if (lane >= off) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = lane < nw ? s_w[lane] : 0u;
+        uint32_t z = w;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, z, off);
+            if (lane >= off) z += y;
+        }
+        s_w[32 + lane] = z - w;
+        if (lane == 31) s_w[64] = z;
+    }
+    __syncthreads();
+    const uint32_t r = s_w[32 + warp] + x - v;
+    *total = s_w[64];
+    __syncthreads();
+    return r;
+}
+
+// Stable LSD pass for W warps (T = 32 W threads, T % 256 == 0): pout <- pin
+// ordered by digit(pin[pos]); ballot multisplit with warp-private counters,
+// digit-major / warp-minor offsets.
+template <int IPT, int W, bool kIdentity, typename DigitFn>
+__device__ __forceinline__ void lsd_pass_w(uint32_t n, const uint16_t* pin, uint16_t* pout,
+                                           uint32_t* wcnt, uint32_t* s_tot, DigitFn digit_of) {
+    constexpr int T = W * 32;
+    constexpr int TPD = T / 256;  // threads per digit in the offset scan
+    constexpr int WPT = W / TPD;  // warps per such thread
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t chunk = ((n + T - 1) / T) * 32;  // per-warp positions
+    const uint32_t steps = chunk / 32;
+    uint32_t* my = wcnt + warp * kRadix;
+#pragma unroll
+    for (int q = 0; q < kRadix / 32; ++q) my[q * 32 + lane] = 0;
+    __syncwarp();
+    const uint32_t lt = lanemask_lt();
+    uint32_t pk[IPT];
+#pragma unroll
+    for (int s = 0; s < IPT; ++s) {
+        pk[s] = 0xFFFFFFFFu;
+        if (uint32_t(s) < steps) {
+            const uint32_t pos = warp * chunk + s * 32 + lane;
+            const bool valid = pos < n;
+            const uint32_t e = valid ? (kIdentity ? pos : uint32_t(pin[pos])) : 0u;
+            const uint32_t d = valid ? digit_of(e) : 0u;
+            const uint32_t peers = match_digit8(d, valid);
+            const uint32_t before = valid ? my[d] : 0u;
+            __syncwarp();
+            if (valid && uint32_t(lane) == 31u - __clz(peers)) my[d] = before + __popc(peers);
+            __syncwarp();
+            if (valid) pk[s] = d | ((before + __popc(peers & lt)) << 8);
+        }
+    }
+    __syncthreads();
+    {
+        const uint32_t d = threadIdx.x / TPD, q = threadIdx.x % TPD;
+        uint32_t part = 0;
+#pragma unroll
+        for (int w = 0; w < WPT; ++w) part += wcnt[(q * WPT + w) * kRadix + d];
+        uint32_t x = part;
+#pragma unroll
+        for (int o = 1; o < TPD; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o, TPD);
+            if (q >= uint32_t(o)) x += y;
+        }
+        const uint32_t qexcl = x - part;
+        if (q == TPD - 1) s_tot[d] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t v[8], sum = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = s_tot[lane * 8 + i], sum += v[i];
+            uint32_t xs = sum;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t z = __shfl_up_sync(0xFFFFFFFFu, xs, off);
+                if (lane >= off) xs += z;
+            }
+            uint32_t run = xs - sum;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                s_tot[256 + lane * 8 + i] = run;
+                run += v[i];
+            }
+        }
+        __syncthreads();
+        uint32_t run = s_tot[256 + d] + qexcl;
+#pragma unroll
+        for (int w = 0; w < WPT; ++w) {
+            uint32_t* c = &wcnt[(q * WPT + w) * kRadix + d];
+            const uint32_t cnt = *c;
+            *c = run;
+            run += cnt;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < IPT; ++s) {
+        if (pk[s] != 0xFFFFFFFFu) {
+            const uint32_t d = pk[s] & 0xFFu;
+            const uint32_t pos = warp * chunk + s * 32 + lane;
+            const uint32_t e = kIdentity ? pos : uint32_t(pin[pos]);
+            pout[my[d] + (pk[s] >> 8)] = uint16_t(e);
+        }
+    }
+    __syncthreads();
+}
+
+template <int RS, bool kFallback>
+__global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kRegRecords ? 1 : 2) k_local(
+    uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group* __restrict__ groups,
+    uint32_t ks, LevelCounters* __restrict__ ctr, Group* __restrict__ spill,
+    unsigned int* __restrict__ n_spill, uint32_t spill_cap) {
+    using C = LocalCfg<RS>;
+    constexpr bool REG = C::kRegRecords;
+    constexpr int T = C::kThreads, W = C::kWarps, IPT = C::kIpt;
+    constexpr int KW = RS / 8;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint32_t* win = reinterpret_cast<uint32_t*>(smem + C::kRecBytes);  // [cap]
+    uint16_t* slot = reinterpret_cast<uint16_t*>(win + C::kCap);        // [cap] bucket order
+    uint16_t* perm = slot + C::kCap;                                    // [cap] final order / fpos
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(perm + C::kCap);        // packed u16 pairs
+    __shared__ uint32_t s_tot[512];
+    __shared__ uint32_t s_scan[65];
+    __shared__ uint32_t s_and[W][2 * KW], s_or[W][2 * KW];
+    __shared__ uint32_t s_L[32];
+    __shared__ uint32_t s_nL, s_flag, s_maxb, s_wmin, s_wmax, s_B;
+    __shared__ unsigned long long s_mul;
+    __shared__ __align__(8) unsigned long long s_bar;
+
+    const Group g = groups[blockIdx.x];
+    const uint32_t n = g.size;
+    const uint8_t* gsrc = (g.parity ? tmp : data) + g.start * RS;
+    uint8_t* dst = data + g.start * RS;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (n <= 1) {
+        if (n == 1 && g.parity && threadIdx.x == 0) store_rec<RS>(dst, 0, load_rec<RS>(gsrc, 0));
+        return;
+    }
+
+    // ---- 1. the group on chip
+    const uint32_t head = REG ? 0u : uint32_t(reinterpret_cast<uintptr_t>(gsrc) & 15u);
+    const uint8_t* recs = smem + head;  // shared-memory records (REG == false)
+    Rec<RS> r[REG ? IPT : 1];
+    if constexpr (REG) {
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            const uint32_t e = uint32_t(j) * T + threadIdx.x;
+            if (e < n) r[j] = load_rec_stream<RS>(gsrc, e);
+        }
+    } else if (threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        fence_mbar_init();
+        const uint32_t bytes = n * RS;
+        const uint32_t hb = head ? min(8u, bytes) : 0u;
+        const uint32_t body = (bytes - hb) & ~15u;
+        const uint32_t tail = bytes - hb - body;
+        if (hb) *reinterpret_cast<uint2*>(smem + head) = *reinterpret_cast<const uint2*>(gsrc);
+        if (tail)
+            *reinterpret_cast<uint2*>(smem + head + hb + body) =
+                *reinterpret_cast<const uint2*>(gsrc + hb + body);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&s_bar, body);
+        for (uint32_t o = 0; o < body; o += 32768u)
+            tma_load_1d(smem + head + hb + o, gsrc + hb + o, min(32768u, body - o), &s_bar);
+    }
+    if (threadIdx.x == 0) {
+        s_wmin = 0xFFFFFFFFu;
+        s_wmax = 0u;
+        s_flag = 0;
+        s_maxb = 0;
+    }
+    __syncthreads();
+    if constexpr (!REG) mbar_wait(&s_bar, 0);
+    auto rec_of = [&](int j, uint32_t e) -> Rec<RS> {
+        if constexpr (REG) return r[j];
+        else return ld_smem_rec<RS>(recs, e);
+    };
+
+    // ---- 2. AND/OR of the record words (REDUX) -> varying key bytes L
+    {
+        uint32_t a[2 * KW], o[2 * KW];
+#pragma unroll
+        for (int w = 0; w < 2 * KW; ++w) a[w] = ~0u, o[w] = 0u;
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            const uint32_t e = uint32_t(j) * T + threadIdx.x;
+            if (e < n) {
+                const Rec<RS> v = rec_of(j, e);
+#pragma unroll
+                for (int w = 0; w < 2 * KW; ++w) a[w] &= v.w[w], o[w] |= v.w[w];
+            }
+        }
+#pragma unroll
+        for (int w = 0; w < 2 * KW; ++w) {
+            a[w] = __reduce_and_sync(0xFFFFFFFFu, a[w]);
+            o[w] = __reduce_or_sync(0xFFFFFFFFu, o[w]);
+        }
+        if (lane < 2 * KW) {
+            uint32_t av = a[0], ov = o[0];
+#pragma unroll
+            for (int w = 1; w < 2 * KW; ++w)
+                if (lane == w) av = a[w], ov = o[w];
+            s_and[warp][lane] = av;
+            s_or[warp][lane] = ov;
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t b = lane;  // key byte b lives in 32-bit word b/4
+        uint32_t diffb = 0;
+        if (b >= g.p && b < ks && b < uint32_t(RS)) {
+            uint32_t ra = ~0u, ro = 0u;
+            for (int q = 0; q < W; ++q) ra &= s_and[q][b >> 2], ro |= s_or[q][b >> 2];
+            diffb = ((ra ^ ro) >> ((b & 3) * 8)) & 0xFFu;
+        }
+        const uint32_t vm = __ballot_sync(0xFFFFFFFFu, diffb != 0);
+        if (diffb) s_L[__popc(vm & lanemask_lt())] = lane;
+        if (lane == 0) s_nL = __popc(vm);
+    }
+    __syncthreads();
+    const uint32_t nL = s_nL;
+    if (nL == 0) {  // every key equal: stable order is the input order
+        if (g.parity) {
+#pragma unroll
+            for (int j = 0; j < IPT; ++j) {
+                const uint32_t e = uint32_t(j) * T + threadIdx.x;
+                if (e < n) store_rec<RS>(dst, e, rec_of(j, e));
+            }
+        }
+        return;
+    }
+    const uint32_t nwin = nL < 4 ? nL : 4;
+    const bool beyond = nL > 4;
+
+    // ---- 3. windows (registers + shared memory), their range
+    // windows / buckets kept in registers when records are not (register budget)
+    constexpr bool KEEP = !REG;
+    uint32_t wv[KEEP ? IPT : 1];
+    {
+        const uint32_t L0 = s_L[0], L1 = s_L[nwin > 1 ? 1 : 0], L2 = s_L[nwin > 2 ? 2 : 0],
+                       L3 = s_L[nwin > 3 ? 3 : 0];
+        uint32_t mn = 0xFFFFFFFFu, mx = 0u;
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            const uint32_t e = uint32_t(j) * T + threadIdx.x;
+            uint32_t w = 0;
+            if (e < n) {
+                if constexpr (REG) {
+                    w = rec_byte<RS>(r[j], L0) << 24;
+                    if (nwin > 1) w |= rec_byte<RS>(r[j], L1) << 16;
+                    if (nwin > 2) w |= rec_byte<RS>(r[j], L2) << 8;
+                    if (nwin > 3) w |= rec_byte<RS>(r[j], L3);
+                } else {
+                    const uint8_t* rp = recs + size_t(e) * RS;
+                    w = uint32_t(rp[L0]) << 24;
+                    if (nwin > 1) w |= uint32_t(rp[L1]) << 16;
+                    if (nwin > 2) w |= uint32_t(rp[L2]) << 8;
+                    if (nwin > 3) w |= uint32_t(rp[L3]);
+                }
+                win[e] = w;
+                mn = min(mn, w);
+                mx = max(mx, w);
+            }
+            if constexpr (KEEP) wv[j] = w;
+        }
+        mn = __reduce_min_sync(0xFFFFFFFFu, mn);
+        mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+        if (lane == 0) {
+            atomicMin(&s_wmin, mn);
+            atomicMax(&s_wmax, mx);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // bucket geometry (one 64-bit division per group)
+        uint32_t B = 32u - __clz(n - 1);  // ceil(log2 n)
+        B = B < 1 ? 1 : (B > uint32_t(C::kBucketBits) ? uint32_t(C::kBucketBits) : B);
+        const uint32_t nbk = 1u << B;
+        const uint64_t range1 = uint64_t(s_wmax - s_wmin) + 1;
+        s_B = B;
+        s_mul = range1 <= nbk ? 0ull : ((unsigned long long)nbk << 32) / range1;
+    }
+    __syncthreads();
+    const uint32_t nbk = 1u << s_B;
+    const uint32_t wmin = s_wmin;
+    const unsigned long long mul = s_mul;
+    auto bucket_of = [&](uint32_t w) -> uint32_t {  // monotone in w, < nbk
+        const uint32_t d = w - wmin;
+        return mul ? uint32_t((uint64_t(d) * mul) >> 32) : d;
+    };
+    auto end_of = [&](uint32_t b) { return (cnt[b >> 1] >> ((b & 1) * 16)) & 0xFFFFu; };
+    auto cmp_rest = [&](uint32_t a, uint32_t b) -> int {  // bytes beyond the window
+        for (uint32_t q = 4; q < nL; ++q) {
+            uint32_t x, y;
+            if constexpr (REG) {
+                x = gsrc[size_t(a) * RS + s_L[q]];
+                y = gsrc[size_t(b) * RS + s_L[q]];
+            } else {
+                x = recs[size_t(a) * RS + s_L[q]];
+                y = recs[size_t(b) * RS + s_L[q]];
+            }
+            if (x != y) return x < y ? -1 : 1;
+        }
+        return 0;
+    };
+
+    // ---- 4. bucket histogram (packed u16 pairs), scan, largest bucket
+    for (uint32_t i = threadIdx.x; i < nbk / 2; i += T) cnt[i] = 0;
+    __syncthreads();
+    uint32_t bk[KEEP ? IPT : 1];
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        const uint32_t e = uint32_t(j) * T + threadIdx.x;
+        if (e < n) {
+            uint32_t b;
+            if constexpr (KEEP) b = bk[j] = bucket_of(wv[j]);
+            else b = bucket_of(win[e]);
+            atomicAdd(&cnt[b >> 1], 1u << ((b & 1) * 16));
+        }
+    }
+    __syncthreads();
+    {
+        const uint32_t per = nbk > uint32_t(T) ? nbk / T : 1u;
+        const uint32_t b0 = threadIdx.x * per;
+        uint32_t sum = 0, mx = 0;
+        if (b0 < nbk) {
+            for (uint32_t b = b0; b < b0 + per; ++b) {
+                const uint32_t c = end_of(b);  // still counts
+                sum += c;
+                mx = c > mx ? c : mx;
+            }
+        }
+        uint32_t total;
+        uint32_t run = block_scan_excl(sum, s_scan, &total);
+        mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+        if (lane == 0 && mx) atomicMax(&s_maxb, mx);
+        if (b0 < nbk) {
+            if (per >= 2) {
+                for (uint32_t b = b0; b < b0 + per; b += 2) {
+                    const uint32_t w = cnt[b >> 1];
+                    const uint32_t c0 = w & 0xFFFFu, c1 = w >> 16;
+                    cnt[b >> 1] = run | ((run + c0) << 16);
+                    run += c0 + c1;
+                }
+            } else if ((b0 & 1) == 0) {
+                const uint32_t c0 = cnt[b0 >> 1] & 0xFFFFu;
+                cnt[b0 >> 1] = run | ((run + c0) << 16);
+            }
+        }
+    }
+    __syncthreads();
+
+    if (!kFallback && s_maxb <= kMaxBucket) {
+        // ---- 5. record ids into bucket order (cnt: starts -> ends)
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            const uint32_t e = uint32_t(j) * T + threadIdx.x;
+            if (e < n) {
+                uint32_t b;
+                if constexpr (KEEP) b = bk[j];
+                else b = bucket_of(win[e]);
+                const uint32_t old = atomicAdd(&cnt[b >> 1], 1u << ((b & 1) * 16));
+                slot[(old >> ((b & 1) * 16)) & 0xFFFFu] = uint16_t(e);
+            }
+        }
+        __syncthreads();
+        // ---- 6. rank inside buckets: lanes hold consecutive slots, bucket
+        // neighbours are compared through warp shuffles
+        for (uint32_t q0 = uint32_t(warp) * 32; q0 < n; q0 += T) {
+            const uint32_t q = q0 + lane;
+            const bool valid = q < n;
+            const uint32_t e = valid ? slot[q] : 0u;
+            const uint32_t w = valid ? win[e] : 0u;
+            const uint32_t b = bucket_of(w);
+            const uint32_t en = valid ? end_of(b) : 0u;
+            const uint32_t st = valid ? (b ? end_of(b - 1) : 0u) : 0u;
+            auto less = [&](uint32_t w2, uint32_t e2) -> bool {
+                if (w2 != w) return w2 < w;
+                const int c = beyond ? cmp_rest(e2, e) : 0;
+                return c < 0 || (c == 0 && e2 < e);
+            };
+            uint32_t rank = 0;
+            const bool inwarp = !valid || (st >= q0 && en <= q0 + 32);
+            const uint32_t K = __reduce_max_sync(0xFFFFFFFFu, valid ? en - st : 0u);
+            for (uint32_t k = 1; k < K; ++k) {
+                const uint32_t wu = __shfl_up_sync(0xFFFFFFFFu, w, k);
+                const uint32_t eu = __shfl_up_sync(0xFFFFFFFFu, e, k);
+                const uint32_t wd = __shfl_down_sync(0xFFFFFFFFu, w, k);
+                const uint32_t ed = __shfl_down_sync(0xFFFFFFFFu, e, k);
+                if (valid && uint32_t(lane) >= k && q - k >= st) rank += less(wu, eu);
+                if (valid && uint32_t(lane) + k < 32 && q + k < en) rank += less(wd, ed);
+            }
+            if (!inwarp) {  // bucket straddles this warp's 32 slots: plain loop
+                rank = 0;
+                for (uint32_t q2 = st; q2 < en; ++q2)
+                    if (q2 != q) rank += less(win[slot[q2]], slot[q2]);
+            }
+            if (valid) {
+                if constexpr (REG) perm[e] = uint16_t(st + rank);  // e -> final position
+                else perm[st + rank] = uint16_t(e);                // final position -> e
+            }
+        }
+        __syncthreads();
+    } else {
+        if (!kFallback) {  // crowded buckets: hand the untouched group to the LSD instance
+            if (threadIdx.x == 0) {
+                const uint32_t i = atomicAdd(n_spill, 1u);
+                if (i < spill_cap) spill[i] = g;
+                atomicAdd(&ctr->fallback_groups, 1ull);
+            }
+            return;
+        }
+        if constexpr (kFallback) {
+            // stable LSD over the window bytes, then every varying byte if ties remain
+            uint16_t *pin = slot, *pout = perm;
+            bool first = true;
+            for (int q = int(nwin) - 1; q >= 0; --q) {
+                const uint32_t sh = 24u - 8u * uint32_t(q);
+                auto dig = [&](uint32_t e) { return (win[e] >> sh) & 0xFFu; };
+                if (first)
+                    lsd_pass_w<IPT, W, true>(n, pin, pout, cnt, s_tot, dig);
+                else
+                    lsd_pass_w<IPT, W, false>(n, pin, pout, cnt, s_tot, dig);
+                first = false;
+                uint16_t* t = pin;
+                pin = pout;
+                pout = t;
+            }
+            if (beyond) {
+                for (uint32_t pos = threadIdx.x + 1; pos < n; pos += T) {
+                    const uint32_t ea = pin[pos - 1], eb = pin[pos];
+                    if (win[ea] == win[eb] && cmp_rest(ea, eb) > 0) s_flag = 1;
+                }
+                __syncthreads();
+                if (s_flag) {
+                    first = true;
+                    for (int q = int(nL) - 1; q >= 0; --q) {
+                        const uint32_t bb = s_L[q];
+                        auto dig = [&](uint32_t e) -> uint32_t {
+                            if constexpr (REG) return gsrc[size_t(e) * RS + bb];
+                            else return recs[size_t(e) * RS + bb];
+                        };
+                        if (first)
+                            lsd_pass_w<IPT, W, true>(n, pin, pout, cnt, s_tot, dig);
+                        else
+                            lsd_pass_w<IPT, W, false>(n, pin, pout, cnt, s_tot, dig);
+                        first = false;
+                        uint16_t* t = pin;
+                        pin = pout;
+                        pout = t;
+                    }
+                }
+            }
+            // pin: final position -> e. Into perm in the layout the output step expects.
+            if constexpr (REG) {
+                for (uint32_t i = threadIdx.x; i < n; i += T) pout[pin[i]] = uint16_t(i);
+                __syncthreads();
+                if (pout != perm)
+                    for (uint32_t i = threadIdx.x; i < n; i += T) perm[i] = pout[i];
+            } else if (pin != perm) {
+                for (uint32_t i = threadIdx.x; i < n; i += T) perm[i] = pin[i];
+            }
+            __syncthreads();
+        }
+    }
+
+    // ---- 7. output (all reads of the source are done)
+    if constexpr (REG) {
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            const uint32_t e = uint32_t(j) * T + threadIdx.x;
+            if (e < n) store_rec<RS>(dst, perm[e], r[j]);
+        }
+    } else {
+#pragma unroll 4
+        for (uint32_t f = threadIdx.x; f < n; f += T)
+            store_rec<RS>(dst, f, ld_smem_rec<RS>(recs, perm[f]));
+    }
+    if (threadIdx.x == 0) atomicAdd(&ctr->moved_local, (unsigned long long)n);
+}
+
+// Finished records that ended in tmp move home (reference finalize(),
+// msd_sorter.hpp:76-80). One CTA per range of <= kCopyTile records.
+constexpr int kCopyTile = 8192;
+
+template <int RS>
+__global__ void __launch_bounds__(256) k_copy_back(uint8_t* __restrict__ data,
+                                                   const uint8_t* __restrict__ tmp,
+                                                   const CopyRange* __restrict__ ranges) {
+    const CopyRange c = ranges[blockIdx.x];
+    const uint64_t bytes = uint64_t(c.size) * RS;
+    const uint8_t* s = tmp + c.start * RS;
+    uint8_t* d = data + c.start * RS;
+    if constexpr (RS % 16 == 0) {
+        for (uint64_t i = threadIdx.x; i < bytes / 16; i += blockDim.x)
+            reinterpret_cast<uint4*>(d)[i] = reinterpret_cast<const uint4*>(s)[i];
+    } else {
+        for (uint64_t i = threadIdx.x; i < bytes / 8; i += blockDim.x)
+            reinterpret_cast<uint2*>(d)[i] = reinterpret_cast<const uint2*>(s)[i];
+    }
+}
+
+}  // namespace rg

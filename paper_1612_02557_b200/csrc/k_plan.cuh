@@ -17,7 +17,7 @@
 #pragma once
 
 #include "common.cuh"
-#include "k_local_sort.cuh"
+#include "k_local.cuh"
 
 namespace rg {
 

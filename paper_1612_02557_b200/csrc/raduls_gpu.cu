@@ -30,8 +30,7 @@
 #include "../../include/raduls_gpu.h"
 #include "common.cuh"
 #include "k_histogram.cuh"
-#include "k_local_sort.cuh"
-#include "k_local_smem.cuh"
+#include "k_local.cuh"
 #include "k_partition.cuh"
 #include "k_plan.cuh"
 #include "k_scan.cuh"
@@ -206,8 +205,7 @@ uint32_t first_varying_byte(const unsigned long long* andor, uint32_t from, uint
 // ~17 K-record groups), the shared-memory variant otherwise.
 template <int RS>
 constexpr uint32_t local_cap() {
-    if constexpr (RS == 8) return LocalCfg<RS>::kCap;
-    else return LocalSmemCfg<RS>::kCap;
+    return LocalCfg<RS>::kCap;
 }
 
 // Capacities for a sort of n records.
@@ -247,17 +245,10 @@ void ensure_caps(Workspace& ws, uint64_t n) {
 template <int RS>
 void set_attrs(Workspace& ws) {
     if (ws.attrs_set[RS]) return;
-    if constexpr (RS == 8) {
-        RG_CHECK(cudaFuncSetAttribute(k_local_sort<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(LocalCfg<RS>::kSmem)));
-        RG_CHECK(cudaFuncSetAttribute(k_local_sort<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(LocalCfg<RS>::kSmem)));
-    } else {
-        RG_CHECK(cudaFuncSetAttribute(k_local_smem<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(LocalSmemCfg<RS>::kSmem)));
-        RG_CHECK(cudaFuncSetAttribute(k_local_smem<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(LocalSmemCfg<RS>::kSmem)));
-    }
+    RG_CHECK(cudaFuncSetAttribute(k_local<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(LocalCfg<RS>::kSmem)));
+    RG_CHECK(cudaFuncSetAttribute(k_local<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(LocalCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(ScatterCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -309,12 +300,8 @@ void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, 
                   LevelCounters* ctr, cudaStream_t st) {
     if (!ngroups) return;
     const int pe = ws.prof.begin(K_LOCAL, st);
-    if constexpr (RS == 8)
-        k_local_sort<RS, false><<<ngroups, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
-            data, tmp, ws.groups.p, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
-    else
-        k_local_smem<RS, false><<<ngroups, LocalSmemCfg<RS>::kThreads, LocalSmemCfg<RS>::kSmem, st>>>(
-            data, tmp, ws.groups.p, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
+    k_local<RS, false><<<ngroups, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
+        data, tmp, ws.groups.p, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
 }
@@ -330,12 +317,8 @@ void finish_spilled(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ks, Lev
     if (!n) return;
     if (n > ws.spill.cap) throw CudaError{RADULS_GPU_EINTERNAL};
     const int pe = ws.prof.begin(K_LOCAL, st);
-    if constexpr (RS == 8)
-        k_local_sort<RS, true><<<n, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
-            data, tmp, ws.spill.p, ks, ctr, nullptr, nullptr, 0);
-    else
-        k_local_smem<RS, true><<<n, LocalSmemCfg<RS>::kThreads, LocalSmemCfg<RS>::kSmem, st>>>(
-            data, tmp, ws.spill.p, ks, ctr, nullptr, nullptr, 0);
+    k_local<RS, true><<<n, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
+        data, tmp, ws.spill.p, ks, ctr, nullptr, nullptr, 0);
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
     RG_CHECK(cudaStreamSynchronize(st));
