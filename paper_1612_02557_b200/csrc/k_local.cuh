@@ -426,33 +426,49 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kRegReco
             }
         }
         __syncthreads();
-        // ---- 6. rank inside buckets: lanes hold consecutive slots, bucket
-        // neighbours are compared through warp shuffles
+        // ---- 6. rank inside buckets. Lanes hold consecutive slots (bucket
+        // order), so a bucket's members are neighbouring lanes: compare
+        // (w, rest of key, input index) with same-bucket neighbours through
+        // shuffles until no lane has one left. Buckets that straddle the
+        // 32-slot window take a shared-memory loop.
         for (uint32_t q0 = uint32_t(warp) * 32; q0 < n; q0 += T) {
             const uint32_t q = q0 + lane;
             const bool valid = q < n;
-            const uint32_t e = valid ? slot[q] : 0u;
-            const uint32_t w = valid ? win[e] : 0u;
-            const uint32_t b = bucket_of(w);
-            const uint32_t en = valid ? end_of(b) : 0u;
-            const uint32_t st = valid ? (b ? end_of(b - 1) : 0u) : 0u;
+            const uint32_t e = valid ? slot[q] : 0xFFFFu;
+            const uint32_t w = valid ? win[e] : 0xFFFFFFFFu;
+            const uint32_t b = valid ? bucket_of(w) : 0xFFFFFFFFu;
             auto less = [&](uint32_t w2, uint32_t e2) -> bool {
                 if (w2 != w) return w2 < w;
                 const int c = beyond ? cmp_rest(e2, e) : 0;
                 return c < 0 || (c == 0 && e2 < e);
             };
-            uint32_t rank = 0;
-            const bool inwarp = !valid || (st >= q0 && en <= q0 + 32);
-            const uint32_t K = __reduce_max_sync(0xFFFFFFFFu, valid ? en - st : 0u);
-            for (uint32_t k = 1; k < K; ++k) {
+            uint32_t below = 0, rank = 0;
+            for (uint32_t k = 1; k < 32; ++k) {
                 const uint32_t wu = __shfl_up_sync(0xFFFFFFFFu, w, k);
                 const uint32_t eu = __shfl_up_sync(0xFFFFFFFFu, e, k);
+                const uint32_t bu = __shfl_up_sync(0xFFFFFFFFu, b, k);
                 const uint32_t wd = __shfl_down_sync(0xFFFFFFFFu, w, k);
                 const uint32_t ed = __shfl_down_sync(0xFFFFFFFFu, e, k);
-                if (valid && uint32_t(lane) >= k && q - k >= st) rank += less(wu, eu);
-                if (valid && uint32_t(lane) + k < 32 && q + k < en) rank += less(wd, ed);
+                const uint32_t bd = __shfl_down_sync(0xFFFFFFFFu, b, k);
+                const bool up = valid && uint32_t(lane) >= k && bu == b;
+                const bool dn = valid && uint32_t(lane) + k < 32 && bd == b;
+                if (up) {
+                    ++below;
+                    rank += less(wu, eu);
+                }
+                if (dn) rank += less(wd, ed);
+                if (!__any_sync(0xFFFFFFFFu, up || dn)) break;
             }
-            if (!inwarp) {  // bucket straddles this warp's 32 slots: plain loop
+            uint32_t st = q - below;
+            // straddling buckets: the first lane's bucket may begin before q0, the
+            // last lane's may end after q0 + 32
+            const uint32_t b_first = __shfl_sync(0xFFFFFFFFu, b, 0);
+            const uint32_t b_last = __shfl_sync(0xFFFFFFFFu, b, 31);
+            const bool straddle = valid && ((b == b_first && q0 > 0 && bucket_of(win[slot[q0 - 1]]) == b) ||
+                                            (b == b_last && q0 + 32 < n && bucket_of(win[slot[q0 + 32]]) == b));
+            if (straddle) {
+                const uint32_t en = end_of(b);
+                st = b ? end_of(b - 1) : 0u;
                 rank = 0;
                 for (uint32_t q2 = st; q2 < en; ++q2)
                     if (q2 != q) rank += less(win[slot[q2]], slot[q2]);
