@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kRegReco
     }
     __syncthreads();
     if (threadIdx.x == 0) {  // bucket geometry (one 64-bit division per group)
-        uint32_t B = 32u - __clz(n - 1);  // ceil(log2 n)
+        uint32_t B = 33u - __clz(n - 1);  // ceil(log2 n) + 1: ~0.5 records per bucket
         B = B < 1 ? 1 : (B > uint32_t(C::kBucketBits) ? uint32_t(C::kBucketBits) : B);
         const uint32_t nbk = 1u << B;
         const uint64_t range1 = uint64_t(s_wmax - s_wmin) + 1;
@@ -426,56 +426,69 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kRegReco
             }
         }
         __syncthreads();
-        // ---- 6. rank inside buckets. Lanes hold consecutive slots (bucket
-        // order), so a bucket's members are neighbouring lanes: compare
-        // (w, rest of key, input index) with same-bucket neighbours through
-        // shuffles until no lane has one left. Buckets that straddle the
-        // 32-slot window take a shared-memory loop.
-        for (uint32_t q0 = uint32_t(warp) * 32; q0 < n; q0 += T) {
-            const uint32_t q = q0 + lane;
-            const bool valid = q < n;
-            const uint32_t e = valid ? slot[q] : 0xFFFFu;
-            const uint32_t w = valid ? win[e] : 0xFFFFFFFFu;
-            const uint32_t b = valid ? bucket_of(w) : 0xFFFFFFFFu;
-            auto less = [&](uint32_t w2, uint32_t e2) -> bool {
-                if (w2 != w) return w2 < w;
-                const int c = beyond ? cmp_rest(e2, e) : 0;
-                return c < 0 || (c == 0 && e2 < e);
-            };
-            uint32_t below = 0, rank = 0;
-            for (uint32_t k = 1; k < 32; ++k) {
-                const uint32_t wu = __shfl_up_sync(0xFFFFFFFFu, w, k);
-                const uint32_t eu = __shfl_up_sync(0xFFFFFFFFu, e, k);
-                const uint32_t bu = __shfl_up_sync(0xFFFFFFFFu, b, k);
-                const uint32_t wd = __shfl_down_sync(0xFFFFFFFFu, w, k);
-                const uint32_t ed = __shfl_down_sync(0xFFFFFFFFu, e, k);
-                const uint32_t bd = __shfl_down_sync(0xFFFFFFFFu, b, k);
-                const bool up = valid && uint32_t(lane) >= k && bu == b;
-                const bool dn = valid && uint32_t(lane) + k < 32 && bd == b;
-                if (up) {
-                    ++below;
-                    rank += less(wu, eu);
+        // ---- 6. order inside buckets (~1 record each). Per record: size-1
+        // bucket -> its start; size-2 -> one comparison; larger buckets (a few
+        // percent) go to a compact list processed densely afterwards, so no
+        // warp iterates to its largest bucket.
+        auto less = [&](uint32_t w2, uint32_t e2, uint32_t w, uint32_t e) -> bool {
+            if (w2 != w) return w2 < w;
+            const int c = beyond ? cmp_rest(e2, e) : 0;
+            return c < 0 || (c == 0 && e2 < e);
+        };
+        auto place = [&](uint32_t e, uint32_t f) {
+            if constexpr (REG) perm[e] = uint16_t(f);  // e -> final position
+            else perm[f] = uint16_t(e);                // final position -> e
+        };
+        uint16_t* lst = reinterpret_cast<uint16_t*>(s_tot);  // up to 1024 deferred records
+        if (threadIdx.x == 0) s_flag = 0;  // list length
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            const uint32_t e = uint32_t(j) * T + threadIdx.x;
+            if (e < n) {
+                uint32_t bb;
+                if constexpr (KEEP) bb = bk[j];
+                else bb = bucket_of(win[e]);
+                const uint32_t en = end_of(bb);
+                const uint32_t st = bb ? end_of(bb - 1) : 0u;
+                if (en - st == 1) {
+                    place(e, st);
+                } else if (en - st == 2) {
+                    const uint32_t s0 = slot[st];
+                    const uint32_t e2 = s0 == e ? slot[st + 1] : s0;
+                    const uint32_t w = KEEP ? wv[KEEP ? j : 0] : win[e];
+                    place(e, st + (less(win[e2], e2, w, e) ? 1u : 0u));
+                } else {
+                    const uint32_t i = atomicAdd(&s_flag, 1u);
+                    if (i < 1024u) {
+                        lst[i] = uint16_t(e);
+                    } else {  // list full: rank inline
+                        const uint32_t w = win[e];
+                        uint32_t rank = 0;
+                        for (uint32_t q2 = st; q2 < en; ++q2) {
+                            const uint32_t e2 = slot[q2];
+                            if (e2 != e) rank += less(win[e2], e2, w, e);
+                        }
+                        place(e, st + rank);
+                    }
                 }
-                if (dn) rank += less(wd, ed);
-                if (!__any_sync(0xFFFFFFFFu, up || dn)) break;
             }
-            uint32_t st = q - below;
-            // straddling buckets: the first lane's bucket may begin before q0, the
-            // last lane's may end after q0 + 32
-            const uint32_t b_first = __shfl_sync(0xFFFFFFFFu, b, 0);
-            const uint32_t b_last = __shfl_sync(0xFFFFFFFFu, b, 31);
-            const bool straddle = valid && ((b == b_first && q0 > 0 && bucket_of(win[slot[q0 - 1]]) == b) ||
-                                            (b == b_last && q0 + 32 < n && bucket_of(win[slot[q0 + 32]]) == b));
-            if (straddle) {
-                const uint32_t en = end_of(b);
-                st = b ? end_of(b - 1) : 0u;
-                rank = 0;
-                for (uint32_t q2 = st; q2 < en; ++q2)
-                    if (q2 != q) rank += less(win[slot[q2]], slot[q2]);
-            }
-            if (valid) {
-                if constexpr (REG) perm[e] = uint16_t(st + rank);  // e -> final position
-                else perm[st + rank] = uint16_t(e);                // final position -> e
+        }
+        __syncthreads();
+        {
+            const uint32_t nl = min(s_flag, 1024u);
+            for (uint32_t i = threadIdx.x; i < nl; i += T) {
+                const uint32_t e = lst[i];
+                const uint32_t w = win[e];
+                const uint32_t bb = bucket_of(w);
+                const uint32_t en = end_of(bb);
+                const uint32_t st = bb ? end_of(bb - 1) : 0u;
+                uint32_t rank = 0;
+                for (uint32_t q2 = st; q2 < en; ++q2) {
+                    const uint32_t e2 = slot[q2];
+                    if (e2 != e) rank += less(win[e2], e2, w, e);
+                }
+                place(e, st + rank);
             }
         }
         __syncthreads();
