@@ -37,9 +37,13 @@ constexpr uint32_t kMaxBucket = 32;
 template <int RS>
 struct LocalCfg {
     static constexpr bool kRegRecords = RS == 8;  // records in registers (else shared memory)
-    static constexpr int kThreads = kRegRecords ? 1024 : 512;
+    // 16/24-B records: small CTAs, four per SM, so one group's HBM traffic and
+    // barriers overlap other groups' work; 32-B records keep 4608-record groups
+    // (BASELINE C4's ~4 K-record bins) at one CTA per SM.
+    static constexpr int kThreads = kRegRecords ? 1024 : (RS == 32 ? 512 : 256);
+    static constexpr int kMinBlocks = (RS == 16 || RS == 24) ? 4 : 1;
     static constexpr int kWarps = kThreads / 32;
-    static constexpr int kCap = RS == 8 ? 20480 : RS == 16 ? 3584 : RS == 24 ? 2560 : 4608;
+    static constexpr int kCap = RS == 8 ? 20480 : RS == 16 ? 1792 : RS == 24 ? 1280 : 4608;
     static constexpr int kIpt = (kCap + kThreads - 1) / kThreads;
     static constexpr int kBucketBits = RS == 8 ? 14 : 13;
     static constexpr int kCntBytes = ((1 << kBucketBits) * 2 > kWarps * kRadix * 4)
@@ -169,7 +173,7 @@ __device__ __forceinline__ void lsd_pass_w(uint32_t n, const uint16_t* pin, uint
 }
 
 template <int RS, bool kFallback>
-__global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kRegRecords ? 1 : 2) k_local(
+__global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBlocks) k_local(
     uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group* __restrict__ groups,
     uint32_t ks, LevelCounters* __restrict__ ctr, Group* __restrict__ spill,
     unsigned int* __restrict__ n_spill, uint32_t spill_cap) {
@@ -439,7 +443,7 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kRegReco
             if constexpr (REG) perm[e] = uint16_t(f);  // e -> final position
             else perm[f] = uint16_t(e);                // final position -> e
         };
-        uint16_t* lst = reinterpret_cast<uint16_t*>(s_tot);  // up to 1024 deferred records
+        uint16_t* lst = reinterpret_cast<uint16_t*>(s_tot);  // up to 1024 deferred records (s_tot: 512 u32)
         if (threadIdx.x == 0) s_flag = 0;  // list length
         __syncthreads();
 #pragma unroll
