@@ -46,9 +46,10 @@ struct LocalCfg {
     static constexpr int kCap = RS == 8 ? 20480 : RS == 16 ? 1792 : RS == 24 ? 1280 : 4608;
     static constexpr int kIpt = (kCap + kThreads - 1) / kThreads;
     static constexpr int kBucketBits = RS == 8 ? 14 : 13;
-    static constexpr int kCntBytes = ((1 << kBucketBits) * 2 > kWarps * kRadix * 4)
-                                         ? (1 << kBucketBits) * 2
-                                         : kWarps * kRadix * 4;
+    // packed u16 bucket counters, one pad word per 32 (conflict-free scan)
+    static constexpr int kCntWords = (1 << kBucketBits) / 2 + (1 << kBucketBits) / 64;
+    static constexpr int kCntBytes = (kCntWords * 4 > kWarps * kRadix * 4) ? kCntWords * 4
+                                                                             : kWarps * kRadix * 4;
     static constexpr int kRecBytes = kRegRecords ? 0 : ((kCap * RS + 16 + 127) / 128) * 128;
     static constexpr size_t kSmem = size_t(kRecBytes) + size_t(kCap) * (4 + 2 + 2) + kCntBytes;
 };
@@ -317,12 +318,12 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
                     if (nwin > 1) w |= rec_byte<RS>(r[j], L1) << 16;
                     if (nwin > 2) w |= rec_byte<RS>(r[j], L2) << 8;
                     if (nwin > 3) w |= rec_byte<RS>(r[j], L3);
-                } else {
-                    const uint8_t* rp = recs + size_t(e) * RS;
-                    w = uint32_t(rp[L0]) << 24;
-                    if (nwin > 1) w |= uint32_t(rp[L1]) << 16;
-                    if (nwin > 2) w |= uint32_t(rp[L2]) << 8;
-                    if (nwin > 3) w |= uint32_t(rp[L3]);
+                } else {  // whole-record vector load: lanes hit consecutive banks
+                    const Rec<RS> v = ld_smem_rec<RS>(recs, e);
+                    w = rec_byte<RS>(v, L0) << 24;
+                    if (nwin > 1) w |= rec_byte<RS>(v, L1) << 16;
+                    if (nwin > 2) w |= rec_byte<RS>(v, L2) << 8;
+                    if (nwin > 3) w |= rec_byte<RS>(v, L3);
                 }
                 win[e] = w;
                 mn = min(mn, w);
@@ -354,7 +355,9 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         const uint32_t d = w - wmin;
         return mul ? uint32_t((uint64_t(d) * mul) >> 32) : d;
     };
-    auto end_of = [&](uint32_t b) { return (cnt[b >> 1] >> ((b & 1) * 16)) & 0xFFFFu; };
+    // packed counter word of bucket b (u16 pairs, padded: +1 word per 32)
+    auto cw = [&](uint32_t b) -> uint32_t& { return cnt[(b >> 1) + (b >> 6)]; };
+    auto end_of = [&](uint32_t b) { return (cw(b) >> ((b & 1) * 16)) & 0xFFFFu; };
     auto cmp_rest = [&](uint32_t a, uint32_t b) -> int {  // bytes beyond the window
         for (uint32_t q = 4; q < nL; ++q) {
             uint32_t x, y;
@@ -371,7 +374,7 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
     };
 
     // ---- 4. bucket histogram (packed u16 pairs), scan, largest bucket
-    for (uint32_t i = threadIdx.x; i < nbk / 2; i += T) cnt[i] = 0;
+    for (uint32_t i = threadIdx.x; i < nbk / 2 + nbk / 64; i += T) cnt[i] = 0;
     __syncthreads();
     uint32_t bk[KEEP ? IPT : 1];
 #pragma unroll
@@ -381,7 +384,7 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
             uint32_t b;
             if constexpr (KEEP) b = bk[j] = bucket_of(wv[j]);
             else b = bucket_of(win[e]);
-            atomicAdd(&cnt[b >> 1], 1u << ((b & 1) * 16));
+            atomicAdd(&cw(b), 1u << ((b & 1) * 16));
         }
     }
     __syncthreads();
@@ -403,14 +406,14 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         if (b0 < nbk) {
             if (per >= 2) {
                 for (uint32_t b = b0; b < b0 + per; b += 2) {
-                    const uint32_t w = cnt[b >> 1];
+                    const uint32_t w = cw(b);
                     const uint32_t c0 = w & 0xFFFFu, c1 = w >> 16;
-                    cnt[b >> 1] = run | ((run + c0) << 16);
+                    cw(b) = run | ((run + c0) << 16);
                     run += c0 + c1;
                 }
             } else if ((b0 & 1) == 0) {
-                const uint32_t c0 = cnt[b0 >> 1] & 0xFFFFu;
-                cnt[b0 >> 1] = run | ((run + c0) << 16);
+                const uint32_t c0 = cw(b0) & 0xFFFFu;
+                cw(b0) = run | ((run + c0) << 16);
             }
         }
     }
@@ -425,7 +428,7 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
                 uint32_t b;
                 if constexpr (KEEP) b = bk[j];
                 else b = bucket_of(win[e]);
-                const uint32_t old = atomicAdd(&cnt[b >> 1], 1u << ((b & 1) * 16));
+                const uint32_t old = atomicAdd(&cw(b), 1u << ((b & 1) * 16));
                 slot[(old >> ((b & 1) * 16)) & 0xFFFFu] = uint16_t(e);
             }
         }
