@@ -8,8 +8,7 @@
 // the stable split of radix_split (kernels.hpp:157-167).
 //
 // B200 design — persistent and warp-specialised:
-//   * warp 8 (producer) walks this CTA's tiles (static round-robin over the
-//     level's tile list), skips tiles of segments the planner did not split,
+//   * warp 8 (producer) claims tiles in order through a global ticket, skips tiles of segments the planner did not split,
 //     and TMA-loads each tile (cp.async.bulk, mbarrier transaction count) into
 //     one of two shared-memory buffers;
 //   * warps 0-7 (consumers) rank the tile's records by digit with a ballot
@@ -96,7 +95,8 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
     uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Seg* __restrict__ segs,
     const unsigned long long* __restrict__ seg_base,  // [nseg][256] exclusive digit bases
     const uint32_t* __restrict__ tile_seg, const uint32_t* __restrict__ tile_off,  // [ntiles][256]
-    uint32_t n_tiles, uint32_t ks = 0, const uint8_t* __restrict__ map = nullptr) {
+    uint32_t n_tiles, unsigned int* __restrict__ ticket, uint32_t ks = 0,
+    const uint8_t* __restrict__ map = nullptr) {
     using C = ScatterCfg<RS>;
     constexpr int T = C::kThreads, IT = C::kItems, W = C::kWarps;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -123,8 +123,15 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
 
     if (warp == W) {  // ------------------------------------------------ producer
         if (lane != 0) return;
+        // Tiles are claimed in order through a global ticket, so all CTAs work
+        // on a narrow window of consecutive tiles: the bucket frontiers each
+        // tile writes stay few and L2-resident until neighbouring tiles
+        // complete their lines (a static round-robin lets 296 persistent CTAs
+        // drift thousands of tiles apart on 2^32-record inputs, and the
+        // half-written lines that get evicted cost read-modify-write traffic).
         uint32_t it = 0;
-        for (uint32_t tile = blockIdx.x;; tile += gridDim.x) {
+        while (true) {
+            const uint32_t tile = atomicAdd(ticket, 1u);
             Seg g;
             uint32_t s = 0;
             if (tile < n_tiles) {

@@ -288,11 +288,12 @@ void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t 
 
 template <int RS, bool kMap>
 void launch_scatter(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t ntiles, uint32_t ks,
-                    const uint8_t* map, cudaStream_t st) {
+                    const uint8_t* map, LevelCounters* c, cudaStream_t st) {
     const uint32_t grid = std::min<uint32_t>(ntiles, uint32_t(sm_count()) * 2);
     const int pe = ws.prof.begin(K_SCATTER, st);
     k_scatter<RS, kMap><<<grid, ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>::kSmem, st>>>(
-        data, tmp, ws.segs[cur].p, ws.seg_tot[cur].p, ws.tile_seg[cur].p, ws.tile_off.p, ntiles, ks, map);
+        data, tmp, ws.segs[cur].p, ws.seg_tot[cur].p, ws.tile_seg[cur].p, ws.tile_off.p, ntiles,
+        &c->scatter_ticket, ks, map);
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
 }
@@ -413,6 +414,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
                 RG_LAUNCH_CHECK();
                 ws.prof.end(pi, st);
             }
+            RG_CHECK(cudaMemsetAsync(dctr, 0, sizeof(LevelCounters), st));
             level_counts<RS>(ws, data, tmp, 0, nt0, dctr, st);
         }
     }
@@ -445,7 +447,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
             h.n_next_tiles > caps.tiles)
             throw CudaError{RADULS_GPU_EINTERNAL};
         if (h.n_scatter_segs) {
-            launch_scatter<RS, false>(ws, data, tmp, cur, ntiles, ks, nullptr, st);
+            launch_scatter<RS, false>(ws, data, tmp, cur, ntiles, ks, nullptr, c, st);
             stats.scatter_launches++;
         }
         launch_local<RS>(ws, data, tmp, h.n_groups, ks, c, st);
@@ -632,7 +634,7 @@ void single_segment_scatter(Workspace& ws, uint8_t* src, uint8_t* dst, uint64_t 
     RG_CHECK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(ws.segs[0].p) + offsetof(Seg, action), &act,
                              sizeof act, cudaMemcpyHostToDevice, st));
     const uint32_t nt = uint32_t((n + TILE - 1) / TILE);
-    launch_scatter<RS, kMap>(ws, src, dst, 0, nt, ks, map, st);
+    launch_scatter<RS, kMap>(ws, src, dst, 0, nt, ks, map, ws.ctr.p, st);
     RG_CHECK(cudaStreamSynchronize(st));
 }
 

@@ -133,3 +133,28 @@ def test_invalid_layouts_raise(rg, torch_cuda):
     for rs, ks in [(8, 16), (12, 8), (40, 8), (16, 0)]:
         with pytest.raises(ValueError):
             rg.sort(buf, 2, rg.RecordLayout(rs, ks))
+
+
+def test_varying_byte_missed_by_the_sample(rg, torch_cuda):
+    """Level 0 guesses the first varying key byte from a strided sample; a more
+    significant byte that varies only off the sample must still be honoured."""
+    rs, ks, n = 16, 8, 1 << 20
+    a = make_input(n, rs, ks, 12)
+    r = a.reshape(n, rs)
+    r[:, 0] = 0
+    r[7, 0] = 1       # off the stride-16 sample
+    r[1001, 0] = 2
+    assert_parity(gpu_sort(rg, torch_cuda, a, rs, ks), a, rs, ks)
+
+
+def test_pair_ties_beyond_the_window(rg, torch_cuda):
+    """Records whose first four varying key bytes tie in pairs (and in triples)
+    but differ further down the key: the local sort's window tie handling."""
+    rs, ks = 32, 24
+    for n, rep in [(1500, 2), (1500, 3), (4000, 2)]:
+        a = make_input(n, rs, ks, 77 + rep)
+        r = a.reshape(n, rs)
+        r[:, 0:16] = 0
+        base = np.arange(n) // rep       # groups of `rep` records share bytes 16..19
+        r[:, 16:20] = (base.astype(">u4")).view(np.uint8).reshape(n, 4)
+        assert_parity(gpu_sort(rg, torch_cuda, a, rs, ks), a, rs, ks)
