@@ -40,10 +40,10 @@ struct LocalCfg {
     // 16/24-B records: small CTAs, four per SM, so one group's HBM traffic and
     // barriers overlap other groups' work; 32-B records keep 4608-record groups
     // (BASELINE C4's ~4 K-record bins) at one CTA per SM.
-    static constexpr int kThreads = kRegRecords ? 1024 : (RS == 32 ? 512 : 256);
-    static constexpr int kMinBlocks = (RS == 16 || RS == 24) ? 4 : 1;
+    static constexpr int kThreads = kRegRecords ? 1024 : 512;
+    static constexpr int kMinBlocks = (RS == 16 || RS == 24) ? 2 : 1;
     static constexpr int kWarps = kThreads / 32;
-    static constexpr int kCap = RS == 8 ? 20480 : RS == 16 ? 1792 : RS == 24 ? 1280 : 4608;
+    static constexpr int kCap = RS == 8 ? 20480 : RS == 16 ? 3584 : RS == 24 ? 2560 : 4608;
     static constexpr int kIpt = (kCap + kThreads - 1) / kThreads;
     static constexpr int kBucketBits = RS == 8 ? 14 : 13;
     // packed u16 bucket counters, one pad word per 32 (conflict-free scan)
@@ -615,9 +615,9 @@ namespace rg {
 // instance. No bucket scan, no divergent loops.
 template <int RS>
 struct LsdCfg {
-    static constexpr int kThreads = RS == 32 ? 512 : 256;
+    static constexpr int kThreads = 512;
     static constexpr int kWarps = kThreads / 32;
-    static constexpr int kMinBlocks = RS == 32 ? 1 : 4;
+    static constexpr int kMinBlocks = RS == 32 ? 1 : 2;
     static constexpr int kCap = LocalCfg<RS>::kCap;
     static constexpr int kIpt = (kCap + kThreads - 1) / kThreads;
     static constexpr int kChunk = kIpt * 32;  // positions per warp

@@ -304,10 +304,14 @@ void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, 
                   LevelCounters* ctr, cudaStream_t st) {
     if (!ngroups) return;
     const int pe = ws.prof.begin(K_LOCAL, st);
-    if constexpr (RS == 8)
+    static const bool use_lsd = [] {
+        const char* v = std::getenv("RADULS_GPU_LOCAL");
+        return !(v && std::strcmp(v, "bucket") == 0);
+    }();
+    if (RS == 8 || !use_lsd)
         k_local<RS, false><<<ngroups, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
             data, tmp, ws.groups.p, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
-    else
+    else if constexpr (RS != 8)
         k_local_lsd<RS><<<ngroups, LsdCfg<RS>::kThreads, LsdCfg<RS>::kSmem, st>>>(
             data, tmp, ws.groups.p, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
     RG_LAUNCH_CHECK();

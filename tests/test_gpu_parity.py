@@ -155,6 +155,10 @@ def test_pair_ties_beyond_the_window(rg, torch_cuda):
         a = make_input(n, rs, ks, 77 + rep)
         r = a.reshape(n, rs)
         r[:, 0:16] = 0
-        base = np.arange(n) // rep       # groups of `rep` records share bytes 16..19
-        r[:, 16:20] = (base.astype(">u4")).view(np.uint8).reshape(n, 4)
+        # groups of `rep` records share bytes 16..19 (a bijective scramble of the
+        # group id, so all four bytes vary); bytes 20..23 stay random
+        base = (np.arange(n, dtype=np.uint64) // rep * np.uint64(2654435761)) % np.uint64(2**32)
+        r[:, 16:20] = base.astype(">u4").view(np.uint8).reshape(n, 4)
+        rng = np.random.default_rng(rep)
+        r[:] = r[rng.permutation(n)]
         assert_parity(gpu_sort(rg, torch_cuda, a, rs, ks), a, rs, ks)
