@@ -304,9 +304,11 @@ void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, 
                   LevelCounters* ctr, cudaStream_t st) {
     if (!ngroups) return;
     const int pe = ws.prof.begin(K_LOCAL, st);
+    // bucket variant by default (fewer shared-memory wavefronts per record);
+    // RADULS_GPU_LOCAL=lsd selects the window-LSD variant (A/B experiments)
     static const bool use_lsd = [] {
         const char* v = std::getenv("RADULS_GPU_LOCAL");
-        return !(v && std::strcmp(v, "bucket") == 0);
+        return v && std::strcmp(v, "lsd") == 0;
     }();
     if (RS == 8 || !use_lsd)
         k_local<RS, false><<<ngroups, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
