@@ -7,6 +7,8 @@ keys it must equal the reference MSD (restated in oracle/raduls_oracle.c)
 byte for byte. Patterns follow P/tests/acceptance.cpp:102-166 and
 P/tests/test_scheduler.cpp:123-214.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -162,3 +164,48 @@ def test_pair_ties_beyond_the_window(rg, torch_cuda):
         rng = np.random.default_rng(rep)
         r[:] = r[rng.permutation(n)]
         assert_parity(gpu_sort(rg, torch_cuda, a, rs, ks), a, rs, ks)
+
+
+def test_cpp_dropin_shim(rg):
+    """include/raduls_gpu.hpp from C++: raduls::gpu::sort with the reference's
+    signature, invalid layouts -> std::invalid_argument (tests/cpp/dropin_main.cpp)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "dropin_main")
+    if not os.path.exists(exe):
+        import __graft_entry__
+        __graft_entry__.build_cpp_dropin()
+    for args in (["100000", "16", "8"], ["54321", "32", "24"], ["300000", "8", "8"]):
+        r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=120)
+        assert r.returncode == 0 and r.stdout.startswith("OK"), r.stdout + r.stderr
+
+
+CONFIG_GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                             "reference_configs.json")
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_full_size_configs_match_reference_hash(rg, torch_cuda, name):
+    """BASELINE configs C1-C4 at full size, generated on the device, against the
+    sha256 of the reference's canonical output (tests/golden/make_golden.py
+    --configs, reference raduls::sort with T=8; C4 through the exact (32,16)
+    proxy). The GPU sort is stable and payload word 0 is the record index, so
+    its output is already canonical."""
+    import hashlib
+    import json
+    gold = json.load(open(CONFIG_GOLDEN))[name]
+    n, rs, ks, dist, seed = gold["n"], gold["rs"], gold["ks"], gold["dist"], gold["seed"]
+    lay = rg.RecordLayout(rs, ks)
+    d = rg.generate(n, lay, dist=dist, seed=seed)
+    assert list(rg.digest(d, n, rs)) == gold["digest"]
+    rg.sort(d, n, lay)
+    torch_cuda.cuda.synchronize()
+    assert rg.check_sorted(d, n, lay)[0] == 0
+    assert list(rg.digest(d, n, rs)) == gold["digest"]
+    h = hashlib.sha256()
+    step = 1 << 30
+    for o in range(0, n * rs, step):
+        h.update(memoryview(d[o:o + step].cpu().numpy()))
+    del d
+    torch_cuda.cuda.empty_cache()
+    assert h.hexdigest() == gold["canonical_sha"]
