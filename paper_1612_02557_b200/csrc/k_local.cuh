@@ -43,9 +43,9 @@ struct LocalCfg {
     static constexpr int kThreads = kRegRecords ? 1024 : 512;
     static constexpr int kMinBlocks = (RS == 16 || RS == 24) ? 2 : 1;
     static constexpr int kWarps = kThreads / 32;
-    static constexpr int kCap = RS == 8 ? 20480 : RS == 16 ? 3584 : RS == 24 ? 2560 : 4608;
+    static constexpr int kCap = RS == 8 ? 18432 : RS == 16 ? 3584 : RS == 24 ? 2560 : 4608;
     static constexpr int kIpt = (kCap + kThreads - 1) / kThreads;
-    static constexpr int kBucketBits = RS == 8 ? 14 : 13;
+    static constexpr int kBucketBits = RS == 8 ? 15 : 13;
     // packed u16 bucket counters, one pad word per 32 (conflict-free scan)
     static constexpr int kCntWords = (1 << kBucketBits) / 2 + (1 << kBucketBits) / 64;
     static constexpr int kCntBytes = (kCntWords * 4 > kWarps * kRadix * 4) ? kCntWords * 4
@@ -460,11 +460,14 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
                 const uint32_t st = bb ? end_of(bb - 1) : 0u;
                 if (en - st == 1) {
                     place(e, st);
-                } else if (en - st == 2) {
-                    const uint32_t s0 = slot[st];
-                    const uint32_t e2 = s0 == e ? slot[st + 1] : s0;
+                } else if (en - st <= 3) {  // two or three records: compare with the others
                     const uint32_t w = KEEP ? wv[KEEP ? j : 0] : win[e];
-                    place(e, st + (less(win[e2], e2, w, e) ? 1u : 0u));
+                    uint32_t rank = 0;
+                    for (uint32_t q2 = st; q2 < en; ++q2) {
+                        const uint32_t e2 = slot[q2];
+                        if (e2 != e) rank += less(win[e2], e2, w, e);
+                    }
+                    place(e, st + rank);
                 } else {
                     const uint32_t i = atomicAdd(&s_flag, 1u);
                     if (i < 1024u) {

@@ -255,7 +255,7 @@ def check_sorted(data, n: int, layout: RecordLayout, stream=None) -> tuple[int, 
 
 # Local-sort group capacity per record size (mirrors local_cap<RS>() in
 # csrc/raduls_gpu.cu; used by tests to aim at boundaries).
-_LOCAL_CAP = {8: 1024 * 20, 16: 3584, 24: 2560, 32: 4608}
+_LOCAL_CAP = {8: 18432, 16: 3584, 24: 2560, 32: 4608}
 
 
 def local_capacity(record_size: int) -> int:
