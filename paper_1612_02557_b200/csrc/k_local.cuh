@@ -567,10 +567,25 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
 
     // ---- 7. output (all reads of the source are done)
     if constexpr (REG) {
+        // stage through shared memory (the window array, free now) in chunks of
+        // final positions, so the global stores are coalesced instead of one
+        // scattered 8-B store per lane
+        constexpr uint32_t CC = uint32_t(C::kCap) * 4u / RS;  // records per chunk
+        uint8_t* stage = reinterpret_cast<uint8_t*>(win);
+        for (uint32_t c0 = 0; c0 < n; c0 += CC) {
 #pragma unroll
-        for (int j = 0; j < IPT; ++j) {
-            const uint32_t e = uint32_t(j) * T + threadIdx.x;
-            if (e < n) store_rec<RS>(dst, perm[e], r[j]);
+            for (int j = 0; j < IPT; ++j) {
+                const uint32_t e = uint32_t(j) * T + threadIdx.x;
+                if (e < n) {
+                    const uint32_t f = perm[e];
+                    if (f >= c0 && f < c0 + CC) st_smem_rec<RS>(stage, f - c0, r[j]);
+                }
+            }
+            __syncthreads();
+            const uint32_t cn = min(CC, n - c0);
+            for (uint32_t i = threadIdx.x; i < cn; i += T)
+                store_rec<RS>(dst, c0 + i, ld_smem_rec<RS>(stage, i));
+            __syncthreads();
         }
     } else {
 #pragma unroll 4
