@@ -153,6 +153,41 @@ __device__ __forceinline__ uint32_t rec_byte(const Rec<RS>& r, uint32_t p) {
     return (rec_word32<RS>(r, p >> 2) >> ((p & 3u) * 8u)) & 0xFFu;
 }
 
+// Big-endian window of up to four record bytes L0 < L1 < L2 < L3 that all lie
+// in the 32-bit words q, q+1 (always true for 8-B records with q = 0): one
+// byte permute instead of four byte extractions. `sel`/`mask` come from
+// make_window_sel; the selector picks (L0, L1, L2, L3) into bytes (3, 2, 1, 0).
+template <bool B>
+struct BoolC {
+    static constexpr bool value = B;
+};
+
+struct WindowSel {
+    uint32_t q, sel, mask;
+    bool fast;
+};
+__device__ __forceinline__ WindowSel make_window_sel(const uint32_t* L, uint32_t nwin,
+                                                     uint32_t rs_words, bool force_q0) {
+    WindowSel s;
+    s.q = force_q0 ? 0u : (L[0] >> 2);
+    if (s.q + 1 >= rs_words && rs_words >= 2) s.q = rs_words - 2;
+    s.sel = 0;
+    s.fast = true;
+    for (uint32_t k = 0; k < nwin; ++k) {
+        const uint32_t rel = L[k] - 4 * s.q;
+        if (rel >= 8) s.fast = false;
+        s.sel |= (rel & 7u) << (4 * (3 - k));
+    }
+    s.mask = nwin >= 4 ? 0xFFFFFFFFu : (0xFFFFFFFFu << (8 * (4 - nwin)));
+    return s;
+}
+template <int RS>
+__device__ __forceinline__ uint32_t rec_window(const Rec<RS>& r, const WindowSel& s) {
+    if constexpr (RS == 8) return __byte_perm(r.w[0], r.w[1], s.sel) & s.mask;
+    else
+        return __byte_perm(rec_word32<RS>(r, s.q), rec_word32<RS>(r, s.q + 1), s.sel) & s.mask;
+}
+
 // Little-endian 64-bit word k (record bytes 8k..8k+7).
 template <int RS>
 __device__ __forceinline__ uint64_t rec_word64(const Rec<RS>& r, int k) {

@@ -46,8 +46,8 @@ struct LocalCfg {
     static constexpr int kCap = RS == 8 ? 18432 : RS == 16 ? 3584 : RS == 24 ? 2560 : 4608;
     static constexpr int kIpt = (kCap + kThreads - 1) / kThreads;
     static constexpr int kBucketBits = RS == 8 ? 15 : 13;
-    // packed u16 bucket counters, one pad word per 32 (conflict-free scan)
-    static constexpr int kCntWords = (1 << kBucketBits) / 2 + (1 << kBucketBits) / 64;
+    // packed u16 bucket counters, four pad words per 64 buckets (conflict-free LDS.128 scan)
+    static constexpr int kCntWords = (1 << kBucketBits) / 2 + (1 << kBucketBits) / 16;
     static constexpr int kCntBytes = (kCntWords * 4 > kWarps * kRadix * 4) ? kCntWords * 4
                                                                              : kWarps * kRadix * 4;
     static constexpr int kRecBytes = kRegRecords ? 0 : ((kCap * RS + 16 + 127) / 128) * 128;
@@ -210,10 +210,11 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
     const uint8_t* recs = smem + head;  // shared-memory records (REG == false)
     Rec<RS> r[REG ? IPT : 1];
     if constexpr (REG) {
+        const uint8_t* tsrc = gsrc + size_t(threadIdx.x) * RS;  // constant offsets per j
 #pragma unroll
         for (int j = 0; j < IPT; ++j) {
             const uint32_t e = uint32_t(j) * T + threadIdx.x;
-            if (e < n) r[j] = load_rec_stream<RS>(gsrc, e);
+            if (e < n) r[j] = load_rec_stream<RS>(tsrc, uint64_t(j) * T);
         }
     } else if (threadIdx.x == 0) {
         mbar_init(&s_bar, 1);
@@ -307,30 +308,33 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
     {
         const uint32_t L0 = s_L[0], L1 = s_L[nwin > 1 ? 1 : 0], L2 = s_L[nwin > 2 ? 2 : 0],
                        L3 = s_L[nwin > 3 ? 3 : 0];
+        const WindowSel ws = make_window_sel(s_L, nwin, RS / 4, RS == 8);
         uint32_t mn = 0xFFFFFFFFu, mx = 0u;
+        auto windows = [&](auto fastc) {
 #pragma unroll
-        for (int j = 0; j < IPT; ++j) {
-            const uint32_t e = uint32_t(j) * T + threadIdx.x;
-            uint32_t w = 0;
-            if (e < n) {
-                if constexpr (REG) {
-                    w = rec_byte<RS>(r[j], L0) << 24;
-                    if (nwin > 1) w |= rec_byte<RS>(r[j], L1) << 16;
-                    if (nwin > 2) w |= rec_byte<RS>(r[j], L2) << 8;
-                    if (nwin > 3) w |= rec_byte<RS>(r[j], L3);
-                } else {  // whole-record vector load: lanes hit consecutive banks
-                    const Rec<RS> v = ld_smem_rec<RS>(recs, e);
-                    w = rec_byte<RS>(v, L0) << 24;
-                    if (nwin > 1) w |= rec_byte<RS>(v, L1) << 16;
-                    if (nwin > 2) w |= rec_byte<RS>(v, L2) << 8;
-                    if (nwin > 3) w |= rec_byte<RS>(v, L3);
+            for (int j = 0; j < IPT; ++j) {
+                const uint32_t e = uint32_t(j) * T + threadIdx.x;
+                uint32_t w = 0;
+                if (e < n) {
+                    // whole-record vector load from shared memory: lanes hit consecutive banks
+                    const Rec<RS> v = rec_of(j, e);
+                    if constexpr (decltype(fastc)::value) {
+                        w = rec_window<RS>(v, ws);
+                    } else {
+                        w = rec_byte<RS>(v, L0) << 24;
+                        if (nwin > 1) w |= rec_byte<RS>(v, L1) << 16;
+                        if (nwin > 2) w |= rec_byte<RS>(v, L2) << 8;
+                        if (nwin > 3) w |= rec_byte<RS>(v, L3);
+                    }
+                    win[e] = w;
+                    mn = min(mn, w);
+                    mx = max(mx, w);
                 }
-                win[e] = w;
-                mn = min(mn, w);
-                mx = max(mx, w);
+                if constexpr (KEEP) wv[j] = w;
             }
-            if constexpr (KEEP) wv[j] = w;
-        }
+        };
+        if (RS == 8 || ws.fast) windows(BoolC<true>{});
+        else windows(BoolC<RS == 8>{});
         mn = __reduce_min_sync(0xFFFFFFFFu, mn);
         mx = __reduce_max_sync(0xFFFFFFFFu, mx);
         if (lane == 0) {
@@ -355,8 +359,8 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         const uint32_t d = w - wmin;
         return mul ? uint32_t((uint64_t(d) * mul) >> 32) : d;
     };
-    // packed counter word of bucket b (u16 pairs, padded: +1 word per 32)
-    auto cw = [&](uint32_t b) -> uint32_t& { return cnt[(b >> 1) + (b >> 6)]; };
+    // packed counter word of bucket b (u16 pairs, padded: +4 words per 64 buckets)
+    auto cw = [&](uint32_t b) -> uint32_t& { return cnt[(b >> 1) + ((b >> 6) << 2)]; };
     auto end_of = [&](uint32_t b) { return (cw(b) >> ((b & 1) * 16)) & 0xFFFFu; };
     auto cmp_rest = [&](uint32_t a, uint32_t b) -> int {  // bytes beyond the window
         for (uint32_t q = 4; q < nL; ++q) {
@@ -374,7 +378,8 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
     };
 
     // ---- 4. bucket histogram (packed u16 pairs), scan, largest bucket
-    for (uint32_t i = threadIdx.x; i < nbk / 2 + nbk / 64; i += T) cnt[i] = 0;
+    for (uint32_t i = threadIdx.x; i < (nbk / 2 + nbk / 16 + 3) / 4; i += T)
+        reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     uint32_t bk[KEEP ? IPT : 1];
 #pragma unroll
@@ -392,7 +397,21 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         const uint32_t per = nbk > uint32_t(T) ? nbk / T : 1u;
         const uint32_t b0 = threadIdx.x * per;
         uint32_t sum = 0, mx = 0;
-        if (b0 < nbk) {
+        // per >= 8: the thread's per/2 counter words are contiguous and 16-B
+        // aligned; the pad words make the LDS.128 of 8 threads conflict-free.
+        // Packed u16 pairs are summed as u32 (each half stays < 65536).
+        uint4* pv = reinterpret_cast<uint4*>(&cw(b0));
+        const uint32_t nv = per / 8;
+        if (per >= 8) {
+            uint32_t S = 0, M = 0;
+            for (uint32_t v = 0; v < nv; ++v) {
+                const uint4 q = pv[v];
+                S += q.x + q.y + q.z + q.w;
+                M = __vmaxu2(M, __vmaxu2(__vmaxu2(q.x, q.y), __vmaxu2(q.z, q.w)));
+            }
+            sum = (S & 0xFFFFu) + (S >> 16);
+            mx = max(M & 0xFFFFu, M >> 16);
+        } else if (b0 < nbk) {
             for (uint32_t b = b0; b < b0 + per; ++b) {
                 const uint32_t c = end_of(b);  // still counts
                 sum += c;
@@ -403,7 +422,22 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         uint32_t run = block_scan_excl(sum, s_scan, &total);
         mx = __reduce_max_sync(0xFFFFFFFFu, mx);
         if (lane == 0 && mx) atomicMax(&s_maxb, mx);
-        if (b0 < nbk) {
+        // counts -> (start of even bucket | start of odd bucket << 16)
+        auto starts = [&](uint32_t w) {
+            const uint32_t o = run * 0x10001u + (w << 16);
+            run += (w * 0x10001u) >> 16;
+            return o;
+        };
+        if (per >= 8) {
+            for (uint32_t v = 0; v < nv; ++v) {
+                uint4 q = pv[v];
+                q.x = starts(q.x);
+                q.y = starts(q.y);
+                q.z = starts(q.z);
+                q.w = starts(q.w);
+                pv[v] = q;
+            }
+        } else if (b0 < nbk) {
             if (per >= 2) {
                 for (uint32_t b = b0; b < b0 + per; b += 2) {
                     const uint32_t w = cw(b);
@@ -446,41 +480,48 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
             if constexpr (REG) perm[e] = uint16_t(f);  // e -> final position
             else perm[f] = uint16_t(e);                // final position -> e
         };
+        auto rank_slow = [&](uint32_t e, uint32_t w, uint32_t st, uint32_t en) {
+            uint32_t rank = 0;
+            for (uint32_t q2 = st; q2 < en; ++q2) {
+                const uint32_t e2 = slot[q2];
+                if (e2 != e) rank += less(win[e2], e2, w, e);
+            }
+            return rank;
+        };
         uint16_t* lst = reinterpret_cast<uint16_t*>(s_tot);  // up to 1024 deferred records (s_tot: 512 u32)
         if (threadIdx.x == 0) s_flag = 0;  // list length
         __syncthreads();
+        // Buckets of <= 3 records (nearly all): branch-free, so the unrolled
+        // loop overlaps the shared-memory loads of all the thread's records; the
+        // bucket's slots are read clamped (a slot equal to e counts nothing).
+        // Equal windows with key bytes beyond them take the full comparison.
 #pragma unroll
         for (int j = 0; j < IPT; ++j) {
             const uint32_t e = uint32_t(j) * T + threadIdx.x;
             if (e < n) {
-                uint32_t bb;
-                if constexpr (KEEP) bb = bk[j];
-                else bb = bucket_of(win[e]);
+                uint32_t w, bb;
+                if constexpr (KEEP) w = wv[j], bb = bk[j];
+                else w = win[e], bb = bucket_of(w);
                 const uint32_t en = end_of(bb);
                 const uint32_t st = bb ? end_of(bb - 1) : 0u;
-                if (en - st == 1) {
-                    place(e, st);
-                } else if (en - st <= 3) {  // two or three records: compare with the others
-                    const uint32_t w = KEEP ? wv[KEEP ? j : 0] : win[e];
+                const uint32_t sz = en - st;
+                if (sz <= 3) {
+                    const uint32_t last = en - 1;
+                    const uint32_t e1 = slot[st], e2 = slot[min(st + 1, last)],
+                                   e3 = slot[min(st + 2, last)];
+                    const uint32_t w1 = win[e1], w2 = win[e2], w3 = win[e3];
+                    const bool u1 = e1 != e, u2 = e2 != e && e2 != e1, u3 = e3 != e && e3 != e2;
                     uint32_t rank = 0;
-                    for (uint32_t q2 = st; q2 < en; ++q2) {
-                        const uint32_t e2 = slot[q2];
-                        if (e2 != e) rank += less(win[e2], e2, w, e);
-                    }
+                    rank += u1 && (w1 < w || (w1 == w && e1 < e));
+                    rank += u2 && (w2 < w || (w2 == w && e2 < e));
+                    rank += u3 && (w3 < w || (w3 == w && e3 < e));
+                    const bool tie = (u1 && w1 == w) || (u2 && w2 == w) || (u3 && w3 == w);
+                    if (beyond && tie) rank = rank_slow(e, w, st, en);
                     place(e, st + rank);
                 } else {
                     const uint32_t i = atomicAdd(&s_flag, 1u);
-                    if (i < 1024u) {
-                        lst[i] = uint16_t(e);
-                    } else {  // list full: rank inline
-                        const uint32_t w = win[e];
-                        uint32_t rank = 0;
-                        for (uint32_t q2 = st; q2 < en; ++q2) {
-                            const uint32_t e2 = slot[q2];
-                            if (e2 != e) rank += less(win[e2], e2, w, e);
-                        }
-                        place(e, st + rank);
-                    }
+                    if (i < 1024u) lst[i] = uint16_t(e);
+                    else place(e, st + rank_slow(e, w, st, en));  // list full: rank inline
                 }
             }
         }
@@ -493,12 +534,7 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
                 const uint32_t bb = bucket_of(w);
                 const uint32_t en = end_of(bb);
                 const uint32_t st = bb ? end_of(bb - 1) : 0u;
-                uint32_t rank = 0;
-                for (uint32_t q2 = st; q2 < en; ++q2) {
-                    const uint32_t e2 = slot[q2];
-                    if (e2 != e) rank += less(win[e2], e2, w, e);
-                }
-                place(e, st + rank);
+                place(e, st + rank_slow(e, w, st, en));
             }
         }
         __syncthreads();
