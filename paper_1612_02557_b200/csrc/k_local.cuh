@@ -183,16 +183,17 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
     constexpr int T = C::kThreads, W = C::kWarps, IPT = C::kIpt;
     constexpr int KW = RS / 8;
     extern __shared__ __align__(128) uint8_t smem[];
-    uint32_t* win = reinterpret_cast<uint32_t*>(smem + C::kRecBytes);  // [cap]
+    // [perm][win][slot][cnt]: win..cnt is one span, the 8-B output's staging area
+    uint16_t* perm = reinterpret_cast<uint16_t*>(smem + C::kRecBytes);  // [cap] final order / fpos
+    uint32_t* win = reinterpret_cast<uint32_t*>(perm + C::kCap);        // [cap]
     uint16_t* slot = reinterpret_cast<uint16_t*>(win + C::kCap);        // [cap] bucket order
-    uint16_t* perm = slot + C::kCap;                                    // [cap] final order / fpos
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(perm + C::kCap);        // packed u16 pairs
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(slot + C::kCap);        // packed u16 pairs
     __shared__ uint32_t s_tot[512];
     __shared__ uint32_t s_scan[65];
     __shared__ uint32_t s_and[W][2 * KW], s_or[W][2 * KW];
     __shared__ uint32_t s_L[32];
     __shared__ uint32_t s_nL, s_flag, s_maxb, s_wmin, s_wmax, s_B;
-    __shared__ unsigned long long s_mul;
+    __shared__ uint32_t s_mul;
     __shared__ __align__(8) unsigned long long s_bar;
 
     const Group g = groups[blockIdx.x];
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         const uint8_t* tsrc = gsrc + size_t(threadIdx.x) * RS;  // constant offsets per j
 #pragma unroll
         for (int j = 0; j < IPT; ++j) {
+            if (uint32_t(j) * T >= n) break;  // block-uniform
             const uint32_t e = uint32_t(j) * T + threadIdx.x;
             if (e < n) r[j] = load_rec_stream<RS>(tsrc, uint64_t(j) * T);
         }
@@ -252,6 +254,7 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         for (int w = 0; w < 2 * KW; ++w) a[w] = ~0u, o[w] = 0u;
 #pragma unroll
         for (int j = 0; j < IPT; ++j) {
+            if (uint32_t(j) * T >= n) break;  // block-uniform
             const uint32_t e = uint32_t(j) * T + threadIdx.x;
             if (e < n) {
                 const Rec<RS> v = rec_of(j, e);
@@ -292,6 +295,7 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         if (g.parity) {
 #pragma unroll
             for (int j = 0; j < IPT; ++j) {
+                if (uint32_t(j) * T >= n) break;  // block-uniform
                 const uint32_t e = uint32_t(j) * T + threadIdx.x;
                 if (e < n) store_rec<RS>(dst, e, rec_of(j, e));
             }
@@ -313,6 +317,7 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         auto windows = [&](auto fastc) {
 #pragma unroll
             for (int j = 0; j < IPT; ++j) {
+                if (uint32_t(j) * T >= n) break;  // block-uniform
                 const uint32_t e = uint32_t(j) * T + threadIdx.x;
                 uint32_t w = 0;
                 if (e < n) {
@@ -349,19 +354,22 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         const uint32_t nbk = 1u << B;
         const uint64_t range1 = uint64_t(s_wmax - s_wmin) + 1;
         s_B = B;
-        s_mul = range1 <= nbk ? 0ull : ((unsigned long long)nbk << 32) / range1;
+        // range1 > nbk: the multiplier fits 32 bits, bucket = umulhi(w - wmin, mul)
+        s_mul = range1 <= nbk ? 0u : uint32_t(((unsigned long long)nbk << 32) / range1);
     }
     __syncthreads();
     const uint32_t nbk = 1u << s_B;
     const uint32_t wmin = s_wmin;
-    const unsigned long long mul = s_mul;
+    const uint32_t mul = s_mul;
     auto bucket_of = [&](uint32_t w) -> uint32_t {  // monotone in w, < nbk
         const uint32_t d = w - wmin;
-        return mul ? uint32_t((uint64_t(d) * mul) >> 32) : d;
+        return mul ? __umulhi(d, mul) : d;
     };
     // packed counter word of bucket b (u16 pairs, padded: +4 words per 64 buckets)
     auto cw = [&](uint32_t b) -> uint32_t& { return cnt[(b >> 1) + ((b >> 6) << 2)]; };
-    auto end_of = [&](uint32_t b) { return (cw(b) >> ((b & 1) * 16)) & 0xFFFFu; };
+    // the same counter as a u16 (little-endian halves: even bucket low)
+    const uint16_t* cnt16 = reinterpret_cast<const uint16_t*>(cnt);
+    auto end_of = [&](uint32_t b) -> uint32_t { return cnt16[b + ((b >> 6) << 3)]; };
     auto cmp_rest = [&](uint32_t a, uint32_t b) -> int {  // bytes beyond the window
         for (uint32_t q = 4; q < nL; ++q) {
             uint32_t x, y;
@@ -384,6 +392,7 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
     uint32_t bk[KEEP ? IPT : 1];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
+        if (uint32_t(j) * T >= n) break;  // block-uniform
         const uint32_t e = uint32_t(j) * T + threadIdx.x;
         if (e < n) {
             uint32_t b;
@@ -457,6 +466,7 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         // ---- 5. record ids into bucket order (cnt: starts -> ends)
 #pragma unroll
         for (int j = 0; j < IPT; ++j) {
+            if (uint32_t(j) * T >= n) break;  // block-uniform
             const uint32_t e = uint32_t(j) * T + threadIdx.x;
             if (e < n) {
                 uint32_t b;
@@ -497,6 +507,7 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         // Equal windows with key bytes beyond them take the full comparison.
 #pragma unroll
         for (int j = 0; j < IPT; ++j) {
+            if (uint32_t(j) * T >= n) break;  // block-uniform
             const uint32_t e = uint32_t(j) * T + threadIdx.x;
             if (e < n) {
                 uint32_t w, bb;
@@ -511,10 +522,12 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
                                    e3 = slot[min(st + 2, last)];
                     const uint32_t w1 = win[e1], w2 = win[e2], w3 = win[e3];
                     const bool u1 = e1 != e, u2 = e2 != e && e2 != e1, u3 = e3 != e && e3 != e2;
+                    // (window, index) order as one 64-bit compare
+                    const uint64_t k = (uint64_t(w) << 32) | e;
                     uint32_t rank = 0;
-                    rank += u1 && (w1 < w || (w1 == w && e1 < e));
-                    rank += u2 && (w2 < w || (w2 == w && e2 < e));
-                    rank += u3 && (w3 < w || (w3 == w && e3 < e));
+                    rank += u1 && ((uint64_t(w1) << 32) | e1) < k;
+                    rank += u2 && ((uint64_t(w2) << 32) | e2) < k;
+                    rank += u3 && ((uint64_t(w3) << 32) | e3) < k;
                     const bool tie = (u1 && w1 == w) || (u2 && w2 == w) || (u3 && w3 == w);
                     if (beyond && tie) rank = rank_slow(e, w, st, en);
                     place(e, st + rank);
@@ -603,25 +616,27 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
 
     // ---- 7. output (all reads of the source are done)
     if constexpr (REG) {
-        // stage through shared memory (the window array, free now) in chunks of
-        // final positions, so the global stores are coalesced instead of one
-        // scattered 8-B store per lane
-        constexpr uint32_t CC = uint32_t(C::kCap) * 4u / RS;  // records per chunk
+        // stage through shared memory (win..cnt, free now) so the global stores
+        // are coalesced instead of one scattered 8-B store per lane; chunks of
+        // final positions when the group outgrows the span
+        constexpr uint32_t CC = uint32_t(size_t(C::kCap) * 6 + C::kCntBytes) / RS;
         uint8_t* stage = reinterpret_cast<uint8_t*>(win);
         for (uint32_t c0 = 0; c0 < n; c0 += CC) {
 #pragma unroll
             for (int j = 0; j < IPT; ++j) {
+                if (uint32_t(j) * T >= n) break;  // block-uniform
                 const uint32_t e = uint32_t(j) * T + threadIdx.x;
                 if (e < n) {
                     const uint32_t f = perm[e];
-                    if (f >= c0 && f < c0 + CC) st_smem_rec<RS>(stage, f - c0, r[j]);
+                    if (CC >= uint32_t(C::kCap) || (f >= c0 && f < c0 + CC))
+                        st_smem_rec<RS>(stage, f - c0, r[j]);
                 }
             }
             __syncthreads();
             const uint32_t cn = min(CC, n - c0);
             for (uint32_t i = threadIdx.x; i < cn; i += T)
                 store_rec<RS>(dst, c0 + i, ld_smem_rec<RS>(stage, i));
-            __syncthreads();
+            if (c0 + CC < n) __syncthreads();
         }
     } else {
 #pragma unroll 4
