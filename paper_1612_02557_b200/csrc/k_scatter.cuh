@@ -34,7 +34,7 @@ struct ScatterCfg {
     static constexpr int kWarps = kThreads / 32;
     static constexpr int kStages = 2;  // tile buffers in the TMA ring
     static constexpr int kBufBytes = ((kTile * RS + 16 + 127) / 128) * 128;  // + alignment slack
-    static constexpr size_t kSmem = size_t(kStages) * kBufBytes + size_t(kTile) * 3;  // ring + map + digit
+    static constexpr size_t kSmem = size_t(kStages) * kBufBytes + size_t(kTile) * 4;  // ring + slot map
 };
 
 // Exclusive scan of one u32 per thread over the 256 consumer threads (named
@@ -102,11 +102,11 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* buf0 = smem;
     constexpr int S = C::kStages;
-    uint16_t* s_map = reinterpret_cast<uint16_t*>(smem + S * C::kBufBytes);
-    uint8_t* s_dig = reinterpret_cast<uint8_t*>(s_map + C::kTile);
-    __shared__ uint32_t s_wcnt[W][kRadix];  // per-warp digit counts, then warp-exclusive offsets
-    __shared__ uint32_t s_lstart[kRadix];
-    __shared__ long long s_gdelta[kRadix];
+    // slot map: record index | digit << 16, in digit order
+    uint32_t* s_map = reinterpret_cast<uint32_t*>(smem + S * C::kBufBytes);
+    __shared__ uint32_t s_wcnt[W][kRadix];  // per-warp digit counts, then tile-local slot starts
+    // destination of slot 0 of each digit, relative to the segment start (segments hold < 2^32 records)
+    __shared__ uint32_t s_gdelta[kRadix];
     __shared__ uint32_t s_scan[8];
     __shared__ __align__(8) unsigned long long s_full[C::kStages], s_empty[C::kStages];
     __shared__ TileInfo s_info[C::kStages];
@@ -208,20 +208,27 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
         bar_sync_named(1, T);
 
         // 2: per-digit tile totals, warp-exclusive offsets, tile-local starts
-        uint32_t tcount = 0;
+        uint32_t tcount = 0, wc[W];
         {
             const int d = threadIdx.x;
 #pragma unroll
             for (int w = 0; w < W; ++w) {
-                const uint32_t c = s_wcnt[w][d];
-                s_wcnt[w][d] = tcount;
-                tcount += c;
+                wc[w] = s_wcnt[w][d];
+                tcount += wc[w];
             }
         }
         uint32_t total;
         const uint32_t lstart = scan256_exclusive(tcount, s_scan, &total);
-        s_lstart[threadIdx.x] = lstart;
-        s_gdelta[threadIdx.x] = (long long)(ti.seg_start + my_base) - (long long)lstart;
+        {  // warp w's first slot of digit d
+            const int d = threadIdx.x;
+            uint32_t run = lstart;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                s_wcnt[w][d] = run;
+                run += wc[w];
+            }
+        }
+        s_gdelta[threadIdx.x] = uint32_t(my_base) - lstart;
         bar_sync_named(1, T);
 
         // 3: slot map (digit order) in shared memory
@@ -229,22 +236,22 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
         for (int j = 0; j < IT; ++j) {
             const uint32_t d = pk[j] & 0x1FFu;
             if (d < 256u) {
-                const uint32_t slot = s_lstart[d] + s_wcnt[warp][d] + (pk[j] >> 9);
-                s_map[slot] = uint16_t(uint32_t(warp * IT + j) * 32u + lane);
-                s_dig[slot] = uint8_t(d);
+                const uint32_t slot = s_wcnt[warp][d] + (pk[j] >> 9);
+                s_map[slot] = (uint32_t(warp * IT + j) * 32u + lane) | (d << 16);
             }
         }
         bar_sync_named(1, T);
 
         // 4: write-out in digit order: consecutive slots of a digit go to
         // consecutive destinations (coalesced vector stores)
-        uint8_t* dst = ti.parity ? data : tmp;
+        uint8_t* dst = (ti.parity ? data : tmp) + ti.seg_start * RS;
 #pragma unroll 4
         for (int j = 0; j < IT; ++j) {
             const uint32_t slot = uint32_t(j) * T + threadIdx.x;
             if (slot < tn) {
-                const Rec<RS> v = ld_smem_rec<RS>(tile, s_map[slot]);
-                store_rec<RS>(dst, uint64_t(s_gdelta[s_dig[slot]] + (long long)slot), v);
+                const uint32_t m = s_map[slot];
+                const Rec<RS> v = ld_smem_rec<RS>(tile, m & 0xFFFFu);
+                store_rec<RS>(dst, uint32_t(s_gdelta[m >> 16] + slot), v);
             }
         }
         bar_sync_named(1, T);  // buffer b, map and counters free for reuse
