@@ -76,6 +76,20 @@ int raduls_gpu_sort(void* d_data, void* d_tmp, uint64_t n_recs, uint32_t rec_siz
 int raduls_gpu_sort_host(uint8_t* data, uint8_t* tmp, uint64_t n_recs, uint32_t rec_size,
                          uint32_t key_size);
 
+/*
+ * LSD baseline (replaces raduls::lsd_sort; P/include/raduls/lsd.hpp:16-22,
+ * P/src/lsd.cpp:12-35): key_size stable byte splits, least significant first,
+ * ping-ponging between d_data and d_tmp (NULL: library-allocated), result in
+ * d_data. Bytes that are constant over the input are skipped. Stable, so the
+ * output equals raduls_gpu_sort's byte for byte. Blocking like raduls_gpu_sort.
+ */
+int raduls_gpu_lsd_sort(void* d_data, void* d_tmp, uint64_t n_recs, uint32_t rec_size,
+                        uint32_t key_size, void* stream);
+/* Host-memory LSD drop-in (raduls::lsd_sort(data, n, layout, cfg)): H2D ->
+ * raduls_gpu_lsd_sort -> D2H, like raduls_gpu_sort_host. */
+int raduls_gpu_lsd_sort_host(uint8_t* data, uint8_t* tmp, uint64_t n_recs, uint32_t rec_size,
+                             uint32_t key_size);
+
 /* Accounting of the most recent sort on the calling thread's device. */
 typedef struct {
     uint32_t levels;            /* planner levels executed */

@@ -7,6 +7,8 @@
 //   raduls::sort(uint8_t*, size_t, const RecordLayout&, const SchedulerConfig&)
 //                                      /root/reference/proj/include/raduls/scheduler.hpp:60-61
 //   raduls::resource_error             /root/reference/proj/include/raduls/errors.hpp:12-22
+//   struct raduls::LsdConfig, raduls::lsd_sort(uint8_t*, size_t, const RecordLayout&, const LsdConfig&)
+//                                      /root/reference/proj/include/raduls/lsd.hpp:12-22
 // inside namespace raduls::gpu, so a caller switches implementations by
 // changing the namespace (e.g. the reference bench's run_algo, bench.cpp:30-47,
 // gains an "raduls_gpu" case calling raduls::gpu::sort). Error mapping:
@@ -69,6 +71,24 @@ inline void sort(uint8_t* data, size_t n, const RecordLayout& layout,
                                     " key_size=" + std::to_string(layout.key_size));
     throw_on_error(raduls_gpu_sort_host(data, nullptr, n, layout.record_size, layout.key_size),
                    "raduls_gpu_sort_host");
+}
+
+// LSD baseline (lsd.hpp:12-22). The lane size must be a positive multiple of 64
+// as in the reference (lsd.cpp:13-14); it and `threads` steer the CPU scatter only.
+struct LsdConfig {
+    size_t buffer_bytes_per_digit = 64;
+    unsigned threads = 1;
+};
+
+inline void lsd_sort(uint8_t* data, size_t n, const RecordLayout& layout, const LsdConfig& cfg = {}) {
+    if (cfg.buffer_bytes_per_digit == 0 || cfg.buffer_bytes_per_digit % 64 != 0)
+        throw std::invalid_argument("LSD buffer size must be a positive multiple of 64 bytes");
+    if (!layout.valid())
+        throw std::invalid_argument("unsupported record layout: record_size=" +
+                                    std::to_string(layout.record_size) +
+                                    " key_size=" + std::to_string(layout.key_size));
+    throw_on_error(raduls_gpu_lsd_sort_host(data, nullptr, n, layout.record_size, layout.key_size),
+                   "raduls_gpu_lsd_sort_host");
 }
 
 // Device-resident variant: d_data/d_tmp are device pointers (d_tmp may be null).

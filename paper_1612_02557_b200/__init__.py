@@ -10,6 +10,7 @@ from .raduls import (  # noqa: F401
     DIST_UNIFORM,
     BigBinFraction,
     CudaError,
+    LsdConfig,
     RecordLayout,
     ResourceError,
     SchedulerConfig,
@@ -21,6 +22,7 @@ from .raduls import (  # noqa: F401
     last_kernel_times,
     last_stats,
     local_capacity,
+    lsd_sort,
     set_profiling,
     sort,
     sort_device,

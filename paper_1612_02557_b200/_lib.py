@@ -22,6 +22,8 @@ EXPORTED = [
     "raduls_gpu_version",
     "raduls_gpu_sort",
     "raduls_gpu_sort_host",
+    "raduls_gpu_lsd_sort",
+    "raduls_gpu_lsd_sort_host",
     "raduls_gpu_last_stats",
     "raduls_gpu_split",
     "raduls_gpu_histogram",
@@ -90,6 +92,8 @@ def load(build_if_missing: bool = False):
         L.raduls_gpu_version.restype = _u32
         L.raduls_gpu_sort.argtypes = [_vp, _vp, _u64, _u32, _u32, _vp]
         L.raduls_gpu_sort_host.argtypes = [_vp, _vp, _u64, _u32, _u32]
+        L.raduls_gpu_lsd_sort.argtypes = [_vp, _vp, _u64, _u32, _u32, _vp]
+        L.raduls_gpu_lsd_sort_host.argtypes = [_vp, _vp, _u64, _u32, _u32]
         L.raduls_gpu_last_stats.argtypes = [C.POINTER(Stats)]
         L.raduls_gpu_split.argtypes = [_vp, _vp, _u64, _u32, _u32, _u64p, _vp]
         L.raduls_gpu_histogram.argtypes = [_vp, _u64, _u32, _u32, _u64p, _u64p, _vp]

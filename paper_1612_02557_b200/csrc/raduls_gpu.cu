@@ -644,9 +644,81 @@ void single_segment_scatter(Workspace& ws, uint8_t* src, uint8_t* dst, uint64_t 
     RG_CHECK(cudaStreamSynchronize(st));
 }
 
+// LSD baseline (reference lsd_sort, P/src/lsd.cpp:12-35): ks stable splits
+// from the least to the most significant key byte, ping-ponging between data
+// and tmp; a byte whose split would not move anything (one digit holds every
+// record) is skipped. Same stable result as the MSD sort.
+template <int RS>
+void lsd_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t ks, cudaStream_t st) {
+    uint8_t* src = data;
+    uint8_t* dst = tmp;
+    for (uint32_t pass = 0; pass < ks; ++pass) {
+        const uint32_t byte = ks - 1 - pass;
+        unsigned long long* tot = ws.h_small;
+        single_segment_counts<RS, false>(ws, src, n, byte, ks, nullptr, tot, st);
+        bool moves = true;
+        for (int d = 0; d < 256; ++d)
+            if (tot[d] == n) moves = false;
+        if (!moves) continue;
+        single_segment_scatter<RS, false>(ws, src, dst, n, ks, nullptr, tot, st);
+        std::swap(src, dst);
+    }
+    if (src != data) RG_CHECK(cudaMemcpyAsync(data, src, n * RS, cudaMemcpyDeviceToDevice, st));
+}
+
+
 }  // namespace
 
 extern "C" {
+
+int raduls_gpu_lsd_sort(void* d_data, void* d_tmp, uint64_t n, uint32_t rs, uint32_t ks, void* stream) {
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs) || n > kMaxRecords) return RADULS_GPU_EINVAL;
+    if (n >= 2 && (!d_data || !aligned_ok(d_data, rs) || (d_tmp && !aligned_ok(d_tmp, rs))))
+        return RADULS_GPU_EINVAL;
+    if (n < 2) return RADULS_GPU_OK;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        uint8_t* tmp = static_cast<uint8_t*>(d_tmp);
+        bool own = false;
+        if (!tmp) {
+            RG_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), n * rs, st));
+            own = true;
+        }
+        try {
+            dispatch_rs(rs, [&](auto R) {
+                lsd_impl<decltype(R)::value>(ws, static_cast<uint8_t*>(d_data), tmp, n, ks, st);
+            });
+        } catch (...) {
+            if (own) cudaFreeAsync(tmp, st);
+            throw;
+        }
+        if (own) RG_CHECK(cudaFreeAsync(tmp, st));
+        RG_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+int raduls_gpu_lsd_sort_host(uint8_t* data, uint8_t* /*tmp*/, uint64_t n, uint32_t rs, uint32_t ks) {
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs) || n > kMaxRecords) return RADULS_GPU_EINVAL;
+    if (n < 2) return RADULS_GPU_OK;
+    if (!data) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        const size_t bytes = size_t(n) * rs;
+        ws.host_data.ensure(bytes);
+        ws.host_tmp.ensure(bytes);
+        cudaStream_t st = nullptr;
+        RG_CHECK(cudaMemcpyAsync(ws.host_data.p, data, bytes, cudaMemcpyHostToDevice, st));
+        dispatch_rs(rs, [&](auto R) {
+            lsd_impl<decltype(R)::value>(ws, ws.host_data.p, ws.host_tmp.p, n, ks, st);
+        });
+        RG_CHECK(cudaMemcpyAsync(data, ws.host_data.p, bytes, cudaMemcpyDeviceToHost, st));
+        RG_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
 
 int raduls_gpu_split(const void* d_src, void* d_dst, uint64_t n, uint32_t rs,
                      uint32_t key_byte_offset, uint64_t* h_counts, void* stream) {

@@ -13,6 +13,8 @@ Reference names kept (P = /root/reference/proj):
   ``data`` may be a CUDA ``torch.uint8`` tensor (sorted in place on the
   device) or host memory (numpy array / bytearray / ``RecordArray``; sorted in
   place through H2D -> device sort -> D2H).
+* ``LsdConfig`` / ``lsd_sort(data, n, layout, cfg)`` — the reference's LSD
+  baseline, P/include/raduls/lsd.hpp:12-22 (stable; equals ``sort``'s output).
 * errors: ``ValueError`` for unsupported layouts (the reference's
   ``std::invalid_argument``, dispatch.hpp:37-39), ``ResourceError`` (a
   ``MemoryError``; the reference's ``raduls::resource_error``,
@@ -31,7 +33,7 @@ __all__ = [
     "RecordLayout", "SchedulerConfig", "TinyPolicy", "BigBinFraction", "ResourceError",
     "CudaError", "sort", "sort_device", "split", "histogram", "generate", "digest",
     "check_sorted", "last_stats", "DIST_UNIFORM", "DIST_SKEW", "local_capacity",
-    "set_profiling", "last_kernel_times",
+    "set_profiling", "last_kernel_times", "LsdConfig", "lsd_sort",
 ]
 
 DIST_UNIFORM = 0
@@ -87,6 +89,15 @@ class SchedulerConfig:
     first_chunk_divisor: int = 64
     buffer_bytes: int = 256
     tiny: TinyPolicy = field(default_factory=TinyPolicy)
+
+
+@dataclass
+class LsdConfig:
+    """P/include/raduls/lsd.hpp:12-15. ``buffer_bytes_per_digit`` (write-
+    combining lane size) must be a positive multiple of 64 as in the reference
+    (lsd.cpp:13-14); like ``threads`` it steers the CPU scatter only."""
+    buffer_bytes_per_digit: int = 64
+    threads: int = 1
 
 
 def _raise(rc: int, what: str) -> None:
@@ -260,3 +271,51 @@ _LOCAL_CAP = {8: 18432, 16: 3584, 24: 2560, 32: 4608}
 
 def local_capacity(record_size: int) -> int:
     return _LOCAL_CAP[record_size]
+
+
+def _host_records(data, n, rs):
+    if isinstance(data, (bytearray, memoryview)):
+        arr = np.frombuffer(data, dtype=np.uint8)
+    else:
+        arr = data
+    if not isinstance(arr, np.ndarray) or arr.dtype != np.uint8 or not arr.flags["C_CONTIGUOUS"]:
+        raise TypeError("host data must be a C-contiguous uint8 buffer")
+    if n is None:
+        n = arr.size // rs
+    if arr.size < n * rs:
+        raise ValueError("data holds fewer than n records")
+    if not arr.flags["WRITEABLE"]:
+        raise ValueError("host data is read-only")
+    return arr, n
+
+
+def lsd_sort(data, n: int | None = None, layout: RecordLayout = RecordLayout(),
+             cfg: LsdConfig | None = None, *, tmp=None, stream=None) -> None:
+    """Stable LSD radix sort (``raduls::lsd_sort``, P/src/lsd.cpp:12-35) on the
+    device: one stable byte split per key byte, least significant first
+    (raduls_gpu_lsd_sort / raduls_gpu_lsd_sort_host). Same arguments and
+    errors as ``sort``."""
+    cfg = cfg or LsdConfig()
+    if cfg.buffer_bytes_per_digit <= 0 or cfg.buffer_bytes_per_digit % 64:
+        raise ValueError("LSD buffer size must be a positive multiple of 64 bytes")
+    if not layout.valid():
+        raise _layout_error(layout)
+    rs = layout.record_size
+    if hasattr(data, "layout") and hasattr(data, "buf") and n is None:  # RecordArray
+        return lsd_sort(data.buf, data.n, data.layout, cfg, tmp=tmp, stream=stream)
+    if _is_cuda_tensor(data):
+        if n is None:
+            n = data.numel() // rs
+        if data.numel() < n * rs:
+            raise ValueError("data holds fewer than n records")
+        if tmp is not None and tmp.numel() < n * rs:
+            raise ValueError("tmp holds fewer than n records")
+        tptr = tmp.data_ptr() if tmp is not None else None
+        rc = _lib.load().raduls_gpu_lsd_sort(data.data_ptr(), tptr, n, rs, layout.key_size,
+                                             _stream_ptr(stream))
+        _raise(rc, "raduls_gpu_lsd_sort")
+        return None
+    arr, n = _host_records(data, n, rs)
+    rc = _lib.load().raduls_gpu_lsd_sort_host(arr.ctypes.data, None, n, rs, layout.key_size)
+    _raise(rc, "raduls_gpu_lsd_sort_host")
+    return None

@@ -2,7 +2,9 @@
 // reference's own callers (P/src/bench.cpp:30-47 run_algo; P/tests/
 // test_scheduler.cpp:16-22 sort_copy): generate records, raduls::gpu::sort,
 // verify sortedness + multiset with the library's own checkers.
-// Usage: dropin_main <n> <record_size> <key_size>   (exit 0 = OK)
+// Usage: dropin_main <n> <record_size> <key_size> [lsd]   (exit 0 = OK)
+// With "lsd": raduls::gpu::lsd_sort (P/include/raduls/lsd.hpp:16-22) instead,
+// after checking that bad lane sizes throw (test_lsd.cpp:69-77).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -15,6 +17,7 @@
 int main(int argc, char** argv) {
     const size_t n = argc > 1 ? std::strtoull(argv[1], nullptr, 10) : 100000;
     const uint32_t rs = argc > 2 ? std::atoi(argv[2]) : 16, ks = argc > 3 ? std::atoi(argv[3]) : 8;
+    const bool lsd = argc > 4 && std::strcmp(argv[4], "lsd") == 0;
     raduls::gpu::RecordLayout layout{rs, ks};
     std::vector<uint8_t> data(n * rs);
     std::mt19937_64 eng(42);
@@ -26,8 +29,21 @@ int main(int argc, char** argv) {
         return 1;
     } catch (const std::invalid_argument&) {
     }
+    if (lsd) {
+        for (size_t lane : {size_t(63), size_t(0)}) {
+            try {
+                raduls::gpu::lsd_sort(data.data(), n, layout, raduls::gpu::LsdConfig{lane, 1});
+                std::puts("FAIL: bad LSD lane size accepted");
+                return 1;
+            } catch (const std::invalid_argument&) {
+            }
+        }
+    }
     std::vector<uint8_t> before = data;
-    raduls::gpu::sort(data.data(), n, layout);
+    if (lsd)
+        raduls::gpu::lsd_sort(data.data(), n, layout, raduls::gpu::LsdConfig{256, 4});
+    else
+        raduls::gpu::sort(data.data(), n, layout);
     for (size_t i = 0; i + 1 < n; ++i)
         if (std::memcmp(&data[i * rs], &data[(i + 1) * rs], ks) > 0) {
             std::printf("FAIL: inversion at %zu\n", i);

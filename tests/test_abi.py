@@ -71,3 +71,19 @@ def test_version_and_stats_struct():
     L = _lib.load()
     assert L.raduls_gpu_version() >= 0x000100
     assert C.sizeof(_lib.Stats) == 4 + 4 + 6 * 8
+
+
+def test_lsd_rejects_bad_config_and_layouts_without_gpu():
+    """test_lsd.cpp:69-77: lane sizes 63 and 0, layout (8, 16) -> invalid_argument."""
+    L = _lib.load()
+    buf = np.zeros(64, dtype=np.uint8)
+    for lane in (63, 0):
+        with pytest.raises(ValueError, match="multiple of 64"):
+            rg.lsd_sort(buf, 2, rg.RecordLayout(16, 8), rg.LsdConfig(lane, 1))
+    with pytest.raises(ValueError, match="unsupported record layout"):
+        rg.lsd_sort(buf, 2, rg.RecordLayout(8, 16), rg.LsdConfig(64, 1))
+    assert L.raduls_gpu_lsd_sort(None, None, 10, 12, 8, None) == _lib.EINVAL
+    assert L.raduls_gpu_lsd_sort(8, None, 10, 16, 8, None) == _lib.EINVAL       # misaligned
+    assert L.raduls_gpu_lsd_sort(None, None, 1, 16, 8, None) == _lib.OK         # n < 2
+    assert L.raduls_gpu_lsd_sort_host(None, None, 10, 16, 8) == _lib.EINVAL
+    assert L.raduls_gpu_lsd_sort_host(None, None, 1, 16, 8) == _lib.OK
