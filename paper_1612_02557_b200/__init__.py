@@ -29,4 +29,6 @@ from .raduls import (  # noqa: F401
     split,
 )
 
+from .records import FormatError, IoError, RecordArray, load_file, save_file  # noqa: F401,E402
+
 __version__ = "0.1.0"

@@ -24,7 +24,9 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/raduls_gpu.h"
@@ -129,6 +131,146 @@ struct Prof {
     }
 };
 
+// Host <-> device streaming for the host drop-ins.
+// Pinned (page-locked or registered) caller buffers go straight to the DMA
+// engine. Pageable ones -- the reference's callers pass plain heap memory --
+// would cap cudaMemcpy at ~11 GB/s H2D / ~21 GB/s D2H on the B200 box, so they
+// stream in chunks through a ring of pinned staging buffers: a small thread
+// pool copies chunk i between the caller's memory and a staging buffer while
+// the copy engine moves chunk i-1 (measurements in DESIGN.md).
+class CopyPool {
+  public:
+    explicit CopyPool(unsigned n) {
+        for (unsigned i = 0; i < n; ++i) th_.emplace_back([this, i] { run(i); });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    // memcpy split over the pool (the calling thread waits)
+    void copy(uint8_t* dst, const uint8_t* src, size_t len) {
+        if (len < (size_t(1) << 20) || th_.empty()) {
+            std::memcpy(dst, src, len);
+            return;
+        }
+        std::unique_lock<std::mutex> lk(m_);
+        dst_ = dst;
+        src_ = src;
+        len_ = len;
+        remaining_ = unsigned(th_.size());
+        ++gen_;
+        cv_.notify_all();
+        done_.wait(lk, [&] { return remaining_ == 0; });
+    }
+
+  private:
+    void run(unsigned id) {
+        uint64_t seen = 0;
+        for (;;) {
+            std::unique_lock<std::mutex> lk(m_);
+            cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+            uint8_t* d = dst_;
+            const uint8_t* s = src_;
+            const size_t len = len_, nt = th_.size();
+            lk.unlock();
+            size_t per = (len + nt - 1) / nt;
+            per = (per + 4095) & ~size_t(4095);
+            const size_t a = size_t(id) * per;
+            if (a < len) std::memcpy(d + a, s + a, std::min(per, len - a));
+            lk.lock();
+            if (--remaining_ == 0) done_.notify_all();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    uint8_t* dst_ = nullptr;
+    const uint8_t* src_ = nullptr;
+    size_t len_ = 0;
+    unsigned remaining_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+struct HostStager {
+    static constexpr size_t kChunk = size_t(32) << 20;
+    static constexpr int kRing = 3;
+    uint8_t* stage[kRing] = {};
+    cudaEvent_t ev[kRing] = {};
+    CopyPool pool;
+
+    static unsigned pool_threads() {
+        const unsigned hw = std::thread::hardware_concurrency();
+        return std::max(1u, std::min(8u, hw ? hw : 1u));
+    }
+    HostStager() : pool(pool_threads()) {
+        for (int i = 0; i < kRing; ++i) {
+            RG_CHECK(cudaMallocHost(&stage[i], kChunk));
+            RG_CHECK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+        }
+    }
+    ~HostStager() {
+        for (int i = 0; i < kRing; ++i) {
+            if (stage[i]) cudaFreeHost(stage[i]);
+            if (ev[i]) cudaEventDestroy(ev[i]);
+        }
+    }
+    static bool pinned(const void* p) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return a.type == cudaMemoryTypeHost;
+    }
+    void h2d(uint8_t* dev, const uint8_t* host, size_t bytes, cudaStream_t st) {
+        if (pinned(host)) {
+            RG_CHECK(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, st));
+            return;
+        }
+        const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+        for (size_t c = 0; c < nchunks; ++c) {
+            const int b = int(c % kRing);
+            const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+            if (c >= size_t(kRing)) RG_CHECK(cudaEventSynchronize(ev[b]));  // chunk c-kRing copied
+            pool.copy(stage[b], host + off, len);
+            RG_CHECK(cudaMemcpyAsync(dev + off, stage[b], len, cudaMemcpyHostToDevice, st));
+            RG_CHECK(cudaEventRecord(ev[b], st));
+        }
+    }
+    void d2h(uint8_t* host, const uint8_t* dev, size_t bytes, cudaStream_t st) {
+        if (pinned(host)) {
+            RG_CHECK(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, st));
+            RG_CHECK(cudaStreamSynchronize(st));
+            return;
+        }
+        const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+        // issue chunk c, then drain chunk c - (kRing - 1): kRing - 1 DMAs in flight
+        for (size_t c = 0; c < nchunks + kRing - 1; ++c) {
+            if (c < nchunks) {
+                const int b = int(c % kRing);
+                const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+                RG_CHECK(cudaMemcpyAsync(stage[b], dev + off, len, cudaMemcpyDeviceToHost, st));
+                RG_CHECK(cudaEventRecord(ev[b], st));
+            }
+            if (c >= size_t(kRing - 1)) {
+                const size_t j = c - (kRing - 1);
+                if (j >= nchunks) continue;
+                const int b = int(j % kRing);
+                const size_t off = j * kChunk, len = std::min(kChunk, bytes - off);
+                RG_CHECK(cudaEventSynchronize(ev[b]));
+                pool.copy(host + off, stage[b], len);
+            }
+        }
+    }
+};
+
 struct Workspace {
     int device = 0;
     Prof prof;
@@ -145,6 +287,11 @@ struct Workspace {
     DevBuf<unsigned int> n_spill;
     DevBuf<CopyRange> copies;
     DevBuf<uint8_t> host_data, host_tmp, map8;
+    HostStager* stager = nullptr;  // host drop-ins, created on first use
+    HostStager& host_stager() {
+        if (!stager) stager = new HostStager();
+        return *stager;
+    }
     LevelCounters* h_ctr = nullptr;         // pinned [kMaxLevels]
     unsigned long long* h_small = nullptr;  // pinned scratch [4096]
     raduls_gpu_stats last{};
@@ -584,11 +731,12 @@ int raduls_gpu_sort_host(uint8_t* data, uint8_t* /*tmp*/, uint64_t n, uint32_t r
         ws.host_data.ensure(bytes);
         ws.host_tmp.ensure(bytes);
         cudaStream_t st = nullptr;
-        RG_CHECK(cudaMemcpyAsync(ws.host_data.p, data, bytes, cudaMemcpyHostToDevice, st));
+        HostStager& hs = ws.host_stager();
+        hs.h2d(ws.host_data.p, data, bytes, st);
         dispatch_rs(rs, [&](auto R) {
             sort_impl<decltype(R)::value>(ws, ws.host_data.p, ws.host_tmp.p, n, ks, st);
         });
-        RG_CHECK(cudaMemcpyAsync(data, ws.host_data.p, bytes, cudaMemcpyDeviceToHost, st));
+        hs.d2h(data, ws.host_data.p, bytes, st);
         RG_CHECK(cudaStreamSynchronize(st));
     });
 }
@@ -710,11 +858,12 @@ int raduls_gpu_lsd_sort_host(uint8_t* data, uint8_t* /*tmp*/, uint64_t n, uint32
         ws.host_data.ensure(bytes);
         ws.host_tmp.ensure(bytes);
         cudaStream_t st = nullptr;
-        RG_CHECK(cudaMemcpyAsync(ws.host_data.p, data, bytes, cudaMemcpyHostToDevice, st));
+        HostStager& hs = ws.host_stager();
+        hs.h2d(ws.host_data.p, data, bytes, st);
         dispatch_rs(rs, [&](auto R) {
             lsd_impl<decltype(R)::value>(ws, ws.host_data.p, ws.host_tmp.p, n, ks, st);
         });
-        RG_CHECK(cudaMemcpyAsync(data, ws.host_data.p, bytes, cudaMemcpyDeviceToHost, st));
+        hs.d2h(data, ws.host_data.p, bytes, st);
         RG_CHECK(cudaStreamSynchronize(st));
     });
 }
@@ -948,6 +1097,7 @@ void raduls_gpu_release(void) {
         }
         w->tile_cnt.release(); w->tile_off.release(); w->status.release(); w->groups.release(); w->spill.release(); w->n_spill.release();
         w->copies.release(); w->host_data.release(); w->host_tmp.release(); w->map8.release();
+        delete w->stager;
         if (w->h_ctr) cudaFreeHost(w->h_ctr);
         if (w->h_small) cudaFreeHost(w->h_small);
         delete w;

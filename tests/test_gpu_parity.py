@@ -209,3 +209,26 @@ def test_full_size_configs_match_reference_hash(rg, torch_cuda, name):
     del d
     torch_cuda.cuda.empty_cache()
     assert h.hexdigest() == gold["canonical_sha"]
+
+
+def test_host_dropin_streams_pageable_and_pinned(rg, torch_cuda):
+    """raduls_gpu_sort_host on more than the pinned staging ring (5 x 32 MiB
+    chunks): pageable buffers stream through staging, pinned ones go direct;
+    an odd byte offset exercises 'any alignment' (scheduler.hpp:56-59)."""
+    rs, ks, n = 16, 8, 10_000_000
+    d = rg.generate(n, rg.RecordLayout(rs, ks), seed=0x5EED0001)
+    a = d.cpu().numpy()
+    want_sorted = d.clone()
+    rg.sort(want_sorted, n, rg.RecordLayout(rs, ks))
+    want = want_sorted.cpu().numpy()
+    page = np.empty(a.size + 3, dtype=np.uint8)[3:]
+    page[:] = a
+    rg.sort(page, n, rg.RecordLayout(rs, ks))
+    assert np.array_equal(page, want)
+    pin = torch_cuda.empty(a.size, dtype=torch_cuda.uint8, pin_memory=True).numpy()
+    pin[:] = a
+    rg.sort(pin, n, rg.RecordLayout(rs, ks))
+    assert np.array_equal(pin, want)
+    page[:] = a
+    rg.lsd_sort(page, n, rg.RecordLayout(rs, ks))
+    assert np.array_equal(page, want)
