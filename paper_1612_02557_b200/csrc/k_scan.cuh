@@ -20,7 +20,7 @@
 
 namespace rg {
 
-constexpr int kScanChunk = 16;
+constexpr int kScanChunk = 64;
 
 // Look-back over earlier chunks' status words for digit d, starting at chunk
 // c-1, until an inclusive prefix; returns the exclusive prefix.
@@ -77,22 +77,18 @@ __global__ void __launch_bounds__(256) k_tile_scan(const Seg* __restrict__ segs,
     }
     __syncthreads();
     const int d = threadIdx.x;
-    uint32_t cnt[kScanChunk];
-    unsigned long long loc[kScanChunk];
+    const uint16_t* cnt = tile_cnt + uint64_t(t0) * kRadix + d;
+    // pass 1: the chunk's trailing segmented sum (independent loads, unrolled)
     unsigned long long run = 0;
     int first_head = kScanChunk;
-#pragma unroll
+#pragma unroll 16
     for (int q = 0; q < kScanChunk; ++q) {
-        cnt[q] = 0;
-        loc[q] = 0;
         if (uint32_t(q) < tn) {
             if (s_head[q]) {
                 run = 0;
                 if (first_head == kScanChunk) first_head = q;
             }
-            cnt[q] = tile_cnt[uint64_t(t0 + q) * kRadix + d];
-            loc[q] = run;
-            run += cnt[q];
+            run += cnt[uint64_t(q) * kRadix];
         }
     }
     unsigned long long excl = 0;
@@ -108,12 +104,16 @@ __global__ void __launch_bounds__(256) k_tile_scan(const Seg* __restrict__ segs,
         excl = lookback_chunks(status, int64_t(c), d);
         st_volatile_u64(my, kFlagIncl | (excl + run));
     }
-#pragma unroll
+    // pass 2: per-tile exclusive offsets (the counts again, now cache-hot)
+    unsigned long long loc = excl;
+#pragma unroll 16
     for (int q = 0; q < kScanChunk; ++q) {
         if (uint32_t(q) < tn) {
-            const unsigned long long off = loc[q] + (q < first_head ? excl : 0ull);
-            tile_off[uint64_t(t0 + q) * kRadix + d] = uint32_t(off);
-            if (s_last[q]) seg_tot[uint64_t(s_seg[q]) * kRadix + d] = off + cnt[q];
+            if (s_head[q]) loc = 0;
+            const uint32_t k = cnt[uint64_t(q) * kRadix];
+            tile_off[uint64_t(t0 + q) * kRadix + d] = uint32_t(loc);
+            if (s_last[q]) seg_tot[uint64_t(s_seg[q]) * kRadix + d] = loc + k;
+            loc += k;
         }
     }
 }
