@@ -175,6 +175,22 @@ int raduls_gpu_partition(const void* d_src, void* d_dst, uint64_t n_recs, uint32
                          uint32_t key_size, uint32_t prefix_byte, const uint32_t* d_bucket_rank,
                          uint32_t n_ranks, uint64_t* h_rank_counts, void* stream);
 
+/*
+ * Multi-GPU sort in one call: G devices, one host thread
+ * per device. Device g holds n_in[g] records at d_in[g] (left unchanged). On
+ * return d_out[g] (capacity out_capacity_recs records) holds n_out[g] records:
+ * the g-th contiguous key range, sorted; the concatenation over g is the
+ * stable sort of the inputs concatenated in device order. Plan: the first
+ * key byte varying over all devices, 16-bit prefix histograms, contiguous
+ * count-balanced bucket ranges (a bucket is never split); stable device
+ * partition; peer copies over NVLink (cudaMemcpyPeerAsync); local sort.
+ * EINVAL (nothing written) when a device would receive more than
+ * out_capacity_recs records. A device may be listed more than once.
+ */
+int raduls_gpu_sort_multi(int n_dev, const int* devices, void* const* d_in, const uint64_t* n_in,
+                          void* const* d_out, uint64_t* n_out, uint64_t out_capacity_recs,
+                          uint32_t rec_size, uint32_t key_size);
+
 /* Release the cached per-device workspace (optional). */
 void raduls_gpu_release(void);
 

@@ -36,6 +36,7 @@ EXPORTED = [
     "raduls_gpu_set_profiling",
     "raduls_gpu_last_kernel_times",
     "raduls_gpu_andor",
+    "raduls_gpu_sort_multi",
 ]
 
 
@@ -105,6 +106,8 @@ def load(build_if_missing: bool = False):
         L.raduls_gpu_release.restype = None
         L.raduls_gpu_set_profiling.argtypes = [C.c_int]
         L.raduls_gpu_andor.argtypes = [_vp, _u64, _u32, _u64p, _vp]
+        L.raduls_gpu_sort_multi.argtypes = [C.c_int, C.POINTER(C.c_int), C.POINTER(_vp), _u64p,
+                                            C.POINTER(_vp), _u64p, _u64, _u32, _u32]
         L.raduls_gpu_last_kernel_times.argtypes = [C.POINTER(KernelTime), C.c_int,
                                                    C.POINTER(C.c_int)]
         _lib = L

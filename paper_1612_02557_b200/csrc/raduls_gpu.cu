@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -815,6 +816,53 @@ void lsd_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t k
 }
 
 
+// ---- multi-GPU key-range partition, host side of
+// raduls_gpu_sort_multi: the same plan as paper_1612_02557_b200/distributed.py
+// (first globally varying byte, 16-bit prefix histograms, contiguous
+// count-balanced bucket ranges), with the metadata combined in host memory and
+// the records exchanged by peer copies over NVLink.
+constexpr uint32_t kPrefixBuckets = 65536;
+
+uint32_t first_varying_byte_multi(const std::vector<std::array<uint64_t, 8>>& ao, uint32_t ks) {
+    uint64_t a[4] = {~0ull, ~0ull, ~0ull, ~0ull}, o[4] = {0, 0, 0, 0};
+    for (const auto& x : ao)
+        for (int w = 0; w < 4; ++w) a[w] &= x[2 * w], o[w] |= x[2 * w + 1];
+    for (uint32_t b = 0; b < ks; ++b)
+        if (((a[b >> 3] ^ o[b >> 3]) >> ((b & 7) * 8)) & 0xFF) return b;
+    return ks;
+}
+
+// bucket b -> the device whose ideal share [r N/G, (r+1) N/G) holds the
+// bucket's midpoint (monotone: each device gets a contiguous key range; a
+// bucket is never split, so equal keys stay together)
+std::vector<uint32_t> balanced_bucket_map_multi(const std::vector<uint64_t>& hist, uint32_t g) {
+    std::vector<uint32_t> map(kPrefixBuckets, 0);
+    double total = 0;
+    for (uint64_t h : hist) total += double(h);
+    if (total == 0) return map;
+    double before = 0;
+    for (uint32_t b = 0; b < kPrefixBuckets; ++b) {
+        const double h = double(hist[b]);
+        const double mid = before + h / 2.0;
+        int64_t r = int64_t(std::floor(mid * g / total));
+        map[b] = uint32_t(std::min<int64_t>(std::max<int64_t>(r, 0), g - 1));
+        before += h;
+    }
+    return map;
+}
+
+// run f(i) for i in [0, n) on n host threads; returns the first nonzero status
+template <typename F>
+int run_per_device(int n, F&& f) {
+    std::vector<int> rc(n, RADULS_GPU_OK);
+    std::vector<std::thread> th;
+    for (int i = 0; i < n; ++i) th.emplace_back([&, i] { rc[i] = f(i); });
+    for (auto& t : th) t.join();
+    for (int i = 0; i < n; ++i)
+        if (rc[i] != RADULS_GPU_OK) return rc[i];
+    return RADULS_GPU_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1103,6 +1151,150 @@ void raduls_gpu_release(void) {
         delete w;
     }
     g_ws.clear();
+}
+
+int raduls_gpu_sort_multi(int n_dev, const int* devices, void* const* d_in, const uint64_t* n_in,
+                          void* const* d_out, uint64_t* n_out, uint64_t out_capacity_recs,
+                          uint32_t rs, uint32_t ks) {
+    if (!layout_ok(rs, ks) || n_dev < 1 || n_dev > 256 || !devices || !d_in || !n_in || !d_out || !n_out)
+        return RADULS_GPU_EINVAL;
+    uint64_t total = 0;
+    for (int g = 0; g < n_dev; ++g) {
+        if (mul_overflows(n_in[g], rs) || n_in[g] > kMaxRecords) return RADULS_GPU_EINVAL;
+        if (n_in[g] && (!d_in[g] || !aligned_ok(d_in[g], rs))) return RADULS_GPU_EINVAL;
+        if (!d_out[g] || !aligned_ok(d_out[g], rs)) return RADULS_GPU_EINVAL;
+        total += n_in[g];
+    }
+    if (mul_overflows(out_capacity_recs, rs)) return RADULS_GPU_EINVAL;
+    const uint32_t G = uint32_t(n_dev);
+    // 1. the first key byte that varies over all devices' records
+    std::vector<std::array<uint64_t, 8>> ao(G);
+    int rc = run_per_device(n_dev, [&](int g) {
+        if (cudaSetDevice(devices[g]) != cudaSuccess) return int(RADULS_GPU_ECUDA);
+        uint64_t* h = ao[g].data();
+        for (int w = 0; w < 8; ++w) h[w] = (w & 1) ? 0ull : ~0ull;
+        return n_in[g] ? raduls_gpu_andor(d_in[g], n_in[g], rs, h, nullptr) : int(RADULS_GPU_OK);
+    });
+    if (rc) return rc;
+    uint32_t p0 = first_varying_byte_multi(ao, ks);
+    if (p0 >= ks) p0 = 0;  // every key equal: any contiguous map is correct
+    // 2. 16-bit prefix histograms at (p0, p0 + 1)
+    std::vector<std::vector<uint64_t>> hist(G, std::vector<uint64_t>(kPrefixBuckets, 0));
+    rc = run_per_device(n_dev, [&](int g) {
+        return guarded([&] {
+            RG_CHECK(cudaSetDevice(devices[g]));
+            if (!n_in[g]) return;
+            uint64_t* d_hist = nullptr;
+            RG_CHECK(cudaMalloc(&d_hist, kPrefixBuckets * sizeof(uint64_t)));
+            int r = RADULS_GPU_OK;
+            if (cudaMemset(d_hist, 0, kPrefixBuckets * sizeof(uint64_t)) != cudaSuccess) r = RADULS_GPU_ECUDA;
+            if (!r) r = raduls_gpu_prefix_histogram(d_in[g], n_in[g], rs, ks, p0, d_hist, nullptr);
+            if (!r && cudaMemcpy(hist[g].data(), d_hist, kPrefixBuckets * sizeof(uint64_t),
+                                 cudaMemcpyDeviceToHost) != cudaSuccess)
+                r = RADULS_GPU_ECUDA;
+            cudaFree(d_hist);
+            if (r) throw CudaError{r};
+        });
+    });
+    if (rc) return rc;
+    // 3. contiguous count-balanced bucket ranges; who sends what to whom
+    std::vector<uint64_t> global(kPrefixBuckets, 0);
+    for (uint32_t g = 0; g < G; ++g)
+        for (uint32_t b = 0; b < kPrefixBuckets; ++b) global[b] += hist[g][b];
+    const std::vector<uint32_t> map = balanced_bucket_map_multi(global, G);
+    std::vector<std::vector<uint64_t>> cnt(G, std::vector<uint64_t>(G, 0));  // [src][dst]
+    for (uint32_t g = 0; g < G; ++g)
+        for (uint32_t b = 0; b < kPrefixBuckets; ++b) cnt[g][map[b]] += hist[g][b];
+    std::vector<uint64_t> recv(G, 0);
+    for (uint32_t g = 0; g < G; ++g)
+        for (uint32_t r = 0; r < G; ++r) recv[r] += cnt[g][r];
+    for (uint32_t r = 0; r < G; ++r)
+        if (recv[r] > out_capacity_recs || recv[r] > kMaxRecords) return RADULS_GPU_EINVAL;  // nothing written yet
+    // 4. stable partition of each device's records into destination ranges
+    std::vector<uint8_t*> part(G, nullptr);
+    auto free_parts = [&] {
+        for (uint32_t g = 0; g < G; ++g)
+            if (part[g]) {
+                cudaSetDevice(devices[g]);
+                cudaFree(part[g]);
+            }
+    };
+    rc = run_per_device(n_dev, [&](int g) {
+        return guarded([&] {
+            RG_CHECK(cudaSetDevice(devices[g]));
+            const uint64_t bytes = std::max<uint64_t>(std::max(n_in[g], recv[g]) * rs, rs);
+            RG_CHECK(cudaMalloc(&part[g], bytes));
+            if (!n_in[g]) return;
+            uint32_t* d_map = nullptr;
+            RG_CHECK(cudaMalloc(&d_map, kPrefixBuckets * sizeof(uint32_t)));
+            int r = cudaMemcpy(d_map, map.data(), kPrefixBuckets * sizeof(uint32_t), cudaMemcpyHostToDevice) ==
+                            cudaSuccess
+                        ? int(RADULS_GPU_OK)
+                        : int(RADULS_GPU_ECUDA);
+            std::vector<uint64_t> got(G, 0);
+            if (!r) r = raduls_gpu_partition(d_in[g], part[g], n_in[g], rs, ks, p0, d_map, G, got.data(), nullptr);
+            cudaFree(d_map);
+            if (r) throw CudaError{r};
+            for (uint32_t q = 0; q < G; ++q)
+                if (got[q] != cnt[g][q]) throw CudaError{RADULS_GPU_EINTERNAL};
+        });
+    });
+    if (rc) {
+        free_parts();
+        return rc;
+    }
+    // 5. exchange: device g's range for r lands in d_out[r] after the ranges of
+    // devices < g (peer copies over NVLink on the source device's copy engine)
+    rc = guarded([&] {
+        for (uint32_t g = 0; g < G; ++g)
+            for (uint32_t r = 0; r < G; ++r) {
+                if (devices[g] == devices[r]) continue;
+                int ok = 0;
+                cudaDeviceCanAccessPeer(&ok, devices[g], devices[r]);
+                if (ok) {
+                    RG_CHECK(cudaSetDevice(devices[g]));
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(devices[r], 0);
+                    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) throw CudaError{RADULS_GPU_ECUDA};
+                    cudaGetLastError();
+                }
+            }
+        std::vector<cudaStream_t> st(G);
+        for (uint32_t g = 0; g < G; ++g) {
+            RG_CHECK(cudaSetDevice(devices[g]));
+            RG_CHECK(cudaStreamCreateWithFlags(&st[g], cudaStreamNonBlocking));
+        }
+        std::vector<uint64_t> at(G, 0);  // next free record of d_out[r]
+        for (uint32_t g = 0; g < G; ++g) {
+            uint64_t send = 0;
+            RG_CHECK(cudaSetDevice(devices[g]));
+            for (uint32_t r = 0; r < G; ++r) {
+                const uint64_t k = cnt[g][r];
+                if (k)
+                    RG_CHECK(cudaMemcpyPeerAsync(static_cast<uint8_t*>(d_out[r]) + at[r] * rs, devices[r],
+                                                 part[g] + send * rs, devices[g], k * rs, st[g]));
+                send += k;
+                at[r] += k;
+            }
+        }
+        for (uint32_t g = 0; g < G; ++g) {
+            RG_CHECK(cudaSetDevice(devices[g]));
+            RG_CHECK(cudaStreamSynchronize(st[g]));
+            RG_CHECK(cudaStreamDestroy(st[g]));
+        }
+    });
+    if (rc) {
+        free_parts();
+        return rc;
+    }
+    // 6. each device sorts its key range (the partition buffer is its scratch)
+    rc = run_per_device(n_dev, [&](int g) {
+        if (cudaSetDevice(devices[g]) != cudaSuccess) return int(RADULS_GPU_ECUDA);
+        n_out[g] = recv[g];
+        return raduls_gpu_sort(d_out[g], part[g], recv[g], rs, ks, nullptr);
+    });
+    free_parts();
+    (void)total;
+    return rc;
 }
 
 }  // extern "C"

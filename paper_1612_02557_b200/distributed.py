@@ -192,3 +192,31 @@ def sort_distributed(data, n: int, layout: RecordLayout, ops=None, group=None,
         timings.update(plan_partition_s=t1 - t0, exchange_s=t2 - t1, local_sort_s=t3 - t2,
                        sent_bytes=int((plan.send_counts.sum() - plan.send_counts[dist.get_rank(group)]) * rs))
     return recv, n_out
+
+
+# ---------------------------------------------------------------- one process, G devices
+
+def sort_multi(inputs, layout: RecordLayout, capacity: int | None = None):
+    """raduls_gpu_sort_multi: ``inputs`` is a list of CUDA uint8 tensors (one
+    per device; a device may appear more than once), each holding whole
+    records. Returns ``(outputs, counts)``: outputs[g] is a tensor on
+    inputs[g]'s device whose first counts[g] records are the g-th contiguous
+    key range, sorted (concatenated over g: the stable sort of the inputs in
+    list order). ``capacity`` (records per output) defaults to the total."""
+    import torch
+    G = len(inputs)
+    rs = layout.record_size
+    n_in = np.array([t.numel() // rs for t in inputs], dtype=np.uint64)
+    cap = int(n_in.sum()) if capacity is None else int(capacity)
+    outs = [torch.empty(max(cap, 1) * rs, dtype=torch.uint8, device=t.device) for t in inputs]
+    devs = (C.c_int * G)(*[t.device.index for t in inputs])
+    din = (C.c_void_p * G)(*[t.data_ptr() for t in inputs])
+    dout = (C.c_void_p * G)(*[t.data_ptr() for t in outs])
+    n_out = np.zeros(G, dtype=np.uint64)
+    for t in inputs:
+        torch.cuda.synchronize(t.device)
+    rc = _lib.load().raduls_gpu_sort_multi(G, devs, din, n_in.ctypes.data_as(_lib._u64p), dout,
+                                           n_out.ctypes.data_as(_lib._u64p), cap, rs,
+                                           layout.key_size)
+    _raise(rc, "raduls_gpu_sort_multi")
+    return outs, [int(x) for x in n_out]

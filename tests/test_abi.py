@@ -87,3 +87,15 @@ def test_lsd_rejects_bad_config_and_layouts_without_gpu():
     assert L.raduls_gpu_lsd_sort(None, None, 1, 16, 8, None) == _lib.OK         # n < 2
     assert L.raduls_gpu_lsd_sort_host(None, None, 10, 16, 8) == _lib.EINVAL
     assert L.raduls_gpu_lsd_sort_host(None, None, 1, 16, 8) == _lib.OK
+
+
+def test_sort_multi_rejects_bad_arguments_without_gpu():
+    L = _lib.load()
+    dev = (C.c_int * 1)(0)
+    ptrs = (C.c_void_p * 1)(None)
+    n = np.zeros(1, dtype=np.uint64)
+    nout = np.zeros(1, dtype=np.uint64)
+    args = (dev, ptrs, n.ctypes.data_as(_lib._u64p), ptrs, nout.ctypes.data_as(_lib._u64p), 10)
+    assert L.raduls_gpu_sort_multi(0, *args, 16, 8) == _lib.EINVAL      # no devices
+    assert L.raduls_gpu_sort_multi(1, *args, 12, 8) == _lib.EINVAL      # layout
+    assert L.raduls_gpu_sort_multi(1, *args, 16, 8) == _lib.EINVAL      # null output
