@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <condition_variable>
 #include <mutex>
 #include <thread>
@@ -673,6 +674,65 @@ void zipf_thresholds(double s, uint32_t universe, unsigned long long* thr) {
     }
 }
 
+// ---- multi-GPU key-range partition (SURVEY.md §8(e)), host side of
+// raduls_gpu_sort_multi: the same plan as paper_1612_02557_b200/distributed.py
+// (first globally varying byte, 16-bit prefix histograms, contiguous
+// count-balanced bucket ranges), with the metadata combined in host memory and
+// the records exchanged by peer copies over NVLink.
+constexpr uint32_t kPrefixBuckets = 65536;
+
+uint32_t first_varying_byte_multi(const std::vector<std::array<uint64_t, 8>>& ao, uint32_t ks) {
+    uint64_t a[4] = {~0ull, ~0ull, ~0ull, ~0ull}, o[4] = {0, 0, 0, 0};
+    for (const auto& x : ao)
+        for (int w = 0; w < 4; ++w) a[w] &= x[2 * w], o[w] |= x[2 * w + 1];
+    for (uint32_t b = 0; b < ks; ++b)
+        if (((a[b >> 3] ^ o[b >> 3]) >> ((b & 7) * 8)) & 0xFF) return b;
+    return ks;
+}
+
+// bucket b -> the device whose ideal share [r N/G, (r+1) N/G) holds the
+// bucket's midpoint (monotone: each device gets a contiguous key range; a
+// bucket is never split, so equal keys stay together)
+std::vector<uint32_t> balanced_bucket_map_multi(const std::vector<uint64_t>& hist, uint32_t g) {
+    std::vector<uint32_t> map(kPrefixBuckets, 0);
+    double total = 0;
+    for (uint64_t h : hist) total += double(h);
+    if (total == 0) return map;
+    double before = 0;
+    for (uint32_t b = 0; b < kPrefixBuckets; ++b) {
+        const double h = double(hist[b]);
+        const double mid = before + h / 2.0;
+        int64_t r = int64_t(std::floor(mid * g / total));
+        map[b] = uint32_t(std::min<int64_t>(std::max<int64_t>(r, 0), g - 1));
+        before += h;
+    }
+    return map;
+}
+
+// run f(i) for i in [0, n) on n host threads; returns the first nonzero status
+template <typename F>
+int run_per_device(int n, F&& f) {
+    std::vector<int> rc(n, RADULS_GPU_OK);
+    std::vector<std::thread> th;
+    for (int i = 0; i < n; ++i) th.emplace_back([&, i] { rc[i] = f(i); });
+    for (auto& t : th) t.join();
+    for (int i = 0; i < n; ++i)
+        if (rc[i] != RADULS_GPU_OK) return rc[i];
+    return RADULS_GPU_OK;
+}
+
+// Device memory a host sort may use: free memory plus the cached host-path
+// buffers (reused), or RADULS_GPU_DEVICE_BUDGET bytes when set (tests force
+// the out-of-core path with it).
+uint64_t device_budget() {
+    if (const char* v = std::getenv("RADULS_GPU_DEVICE_BUDGET")) return std::strtoull(v, nullptr, 10);
+    size_t free_b = 0, total_b = 0;
+    RG_CHECK(cudaMemGetInfo(&free_b, &total_b));
+    Workspace& ws = workspace();
+    std::lock_guard<std::mutex> lk(ws.mu);
+    return uint64_t(free_b) + ws.host_data.cap + ws.host_tmp.cap;
+}
+
 }  // namespace
 
 extern "C" {
@@ -721,14 +781,137 @@ int raduls_gpu_sort(void* d_data, void* d_tmp, uint64_t n, uint32_t rs, uint32_t
     });
 }
 
-int raduls_gpu_sort_host(uint8_t* data, uint8_t* /*tmp*/, uint64_t n, uint32_t rs, uint32_t ks) {
-    if (!layout_ok(rs, ks) || mul_overflows(n, rs) || n > kMaxRecords) return RADULS_GPU_EINVAL;
+// Host sort larger than the device budget: the
+// multi-GPU plan applied to parts of one array. (1) a streamed pass over
+// chunks: AND/OR and the 16-bit prefix histogram at the first chunk's guess of
+// the first varying key byte (a second histogram pass only if the guess was
+// wrong); (2) contiguous bucket ranges packed greedily into parts that fit the
+// device; (3) a streamed stable partition of every chunk into the host scratch
+// `tmp` at each part's running offset; (4) each part to the device, sorted,
+// back to its final place in `data`. PCIe traffic: 3 reads + 2 writes of the
+// array (4 + 2 when the guess misses).
+static int sort_host_out_of_core(uint8_t* data, uint8_t* htmp, uint64_t n, uint32_t rs, uint32_t ks,
+                                 uint64_t budget) {
+    return guarded([&] {
+        {  // the in-core host path's cached device buffers are not needed
+            Workspace& ws = workspace();
+            std::lock_guard<std::mutex> lk(ws.mu);
+            ws.host_data.release();
+            ws.host_tmp.release();
+        }
+        const uint64_t reserve = std::min<uint64_t>(budget / 4, uint64_t(1) << 30);
+        uint64_t P = (budget - reserve) / (2 * rs + rs / 8 + 1);  // records per part (+ tmp + workspace)
+        P = std::min<uint64_t>(P, kMaxRecords);
+        if (P < (uint64_t(1) << 16)) throw CudaError{RADULS_GPU_ENOMEM};
+        std::unique_ptr<uint8_t[]> own_tmp;
+        if (!htmp) {
+            own_tmp.reset(new uint8_t[n * rs]);
+            htmp = own_tmp.get();
+        }
+        uint8_t *A = nullptr, *B = nullptr;
+        unsigned long long* d_hist = nullptr;
+        uint32_t* d_map = nullptr;
+        struct Free {
+            uint8_t **a, **b;
+            unsigned long long** h;
+            uint32_t** m;
+            ~Free() {
+                cudaFree(*a);
+                cudaFree(*b);
+                cudaFree(*h);
+                cudaFree(*m);
+            }
+        } fr{&A, &B, &d_hist, &d_map};
+        RG_CHECK(cudaMalloc(&A, P * rs));
+        RG_CHECK(cudaMalloc(&B, P * rs));
+        RG_CHECK(cudaMalloc(&d_hist, kPrefixBuckets * sizeof(unsigned long long)));
+        RG_CHECK(cudaMalloc(&d_map, kPrefixBuckets * sizeof(uint32_t)));
+        HostStager hs;
+        cudaStream_t st = nullptr;
+        auto check = [](int r) {
+            if (r) throw CudaError{r};
+        };
+        // (1) AND/OR + prefix histogram at the guessed byte
+        uint64_t all[8];
+        for (int w = 0; w < 8; ++w) all[w] = (w & 1) ? 0ull : ~0ull;
+        uint32_t guess = 0;
+        auto hist_pass = [&](uint32_t p, bool andor) {
+            RG_CHECK(cudaMemset(d_hist, 0, kPrefixBuckets * sizeof(unsigned long long)));
+            for (uint64_t off = 0; off < n; off += P) {
+                const uint64_t c = std::min(P, n - off);
+                hs.h2d(A, data + off * rs, c * rs, st);
+                if (andor) {
+                    uint64_t h[8];
+                    check(raduls_gpu_andor(A, c, rs, h, st));
+                    for (int w = 0; w < 8; ++w) all[w] = (w & 1) ? (all[w] | h[w]) : (all[w] & h[w]);
+                    if (off == 0) {
+                        std::vector<std::array<uint64_t, 8>> one(1);
+                        std::memcpy(one[0].data(), h, sizeof h);
+                        p = guess = std::min(first_varying_byte_multi(one, ks), ks - 1);
+                    }
+                }
+                check(raduls_gpu_prefix_histogram(A, c, rs, ks, p, reinterpret_cast<uint64_t*>(d_hist), st));
+            }
+        };
+        hist_pass(0, true);
+        std::vector<std::array<uint64_t, 8>> tot(1);
+        std::memcpy(tot[0].data(), all, sizeof all);
+        const uint32_t p0 = first_varying_byte_multi(tot, ks);
+        if (p0 >= ks) return;  // every key equal: the stable order is the input order
+        if (p0 != guess) hist_pass(p0, false);
+        std::vector<uint64_t> hist(kPrefixBuckets);
+        RG_CHECK(cudaMemcpy(hist.data(), d_hist, kPrefixBuckets * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        // (2) parts: contiguous bucket ranges of <= P records
+        std::vector<uint32_t> map(kPrefixBuckets);
+        std::vector<uint64_t> psz(1, 0);
+        for (uint32_t b = 0; b < kPrefixBuckets; ++b) {
+            if (hist[b] > P) throw CudaError{RADULS_GPU_ENOMEM};  // one 16-bit prefix outgrows the device
+            if (psz.back() + hist[b] > P) psz.push_back(0);
+            map[b] = uint32_t(psz.size() - 1);
+            psz.back() += hist[b];
+        }
+        const uint32_t K = uint32_t(psz.size());
+        if (K > 256) throw CudaError{RADULS_GPU_ENOMEM};
+        std::vector<uint64_t> poff(K, 0), written(K, 0);
+        for (uint32_t k = 1; k < K; ++k) poff[k] = poff[k - 1] + psz[k - 1];
+        RG_CHECK(cudaMemcpy(d_map, map.data(), kPrefixBuckets * sizeof(uint32_t), cudaMemcpyHostToDevice));
+        // (3) stable partition of every chunk into the parts' host ranges
+        std::vector<uint64_t> cnt(K);
+        for (uint64_t off = 0; off < n; off += P) {
+            const uint64_t c = std::min(P, n - off);
+            hs.h2d(A, data + off * rs, c * rs, st);
+            check(raduls_gpu_partition(A, B, c, rs, ks, p0, d_map, K, cnt.data(), st));
+            uint64_t run = 0;
+            for (uint32_t k = 0; k < K; ++k) {
+                if (cnt[k]) hs.d2h(htmp + (poff[k] + written[k]) * rs, B + run * rs, cnt[k] * rs, st);
+                written[k] += cnt[k];
+                run += cnt[k];
+            }
+        }
+        // (4) every part: to the device, sorted, to its place in data
+        for (uint32_t k = 0; k < K; ++k) {
+            if (!psz[k]) continue;
+            hs.h2d(A, htmp + poff[k] * rs, psz[k] * rs, st);
+            check(raduls_gpu_sort(A, B, psz[k], rs, ks, st));
+            hs.d2h(data + poff[k] * rs, A, psz[k] * rs, st);
+        }
+        RG_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+int raduls_gpu_sort_host(uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t rs, uint32_t ks) {
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs) || mul_overflows(2 * n, rs)) return RADULS_GPU_EINVAL;
     if (n < 2) return RADULS_GPU_OK;
     if (!data) return RADULS_GPU_EINVAL;
+    uint64_t budget = 0;
+    const int rc = guarded([&] { budget = device_budget(); });
+    if (rc) return rc;
+    const uint64_t bytes = n * rs;
+    if (n > kMaxRecords || 2 * bytes + bytes / 8 + (uint64_t(1) << 30) > budget)
+        return sort_host_out_of_core(data, tmp, n, rs, ks, budget);
     return guarded([&] {
         Workspace& ws = workspace();
         std::lock_guard<std::mutex> lk(ws.mu);
-        const size_t bytes = size_t(n) * rs;
         ws.host_data.ensure(bytes);
         ws.host_tmp.ensure(bytes);
         cudaStream_t st = nullptr;
@@ -815,53 +998,6 @@ void lsd_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t k
     if (src != data) RG_CHECK(cudaMemcpyAsync(data, src, n * RS, cudaMemcpyDeviceToDevice, st));
 }
 
-
-// ---- multi-GPU key-range partition (SURVEY.md §8(e)), host side of
-// raduls_gpu_sort_multi: the same plan as paper_1612_02557_b200/distributed.py
-// (first globally varying byte, 16-bit prefix histograms, contiguous
-// count-balanced bucket ranges), with the metadata combined in host memory and
-// the records exchanged by peer copies over NVLink.
-constexpr uint32_t kPrefixBuckets = 65536;
-
-uint32_t first_varying_byte_multi(const std::vector<std::array<uint64_t, 8>>& ao, uint32_t ks) {
-    uint64_t a[4] = {~0ull, ~0ull, ~0ull, ~0ull}, o[4] = {0, 0, 0, 0};
-    for (const auto& x : ao)
-        for (int w = 0; w < 4; ++w) a[w] &= x[2 * w], o[w] |= x[2 * w + 1];
-    for (uint32_t b = 0; b < ks; ++b)
-        if (((a[b >> 3] ^ o[b >> 3]) >> ((b & 7) * 8)) & 0xFF) return b;
-    return ks;
-}
-
-// bucket b -> the device whose ideal share [r N/G, (r+1) N/G) holds the
-// bucket's midpoint (monotone: each device gets a contiguous key range; a
-// bucket is never split, so equal keys stay together)
-std::vector<uint32_t> balanced_bucket_map_multi(const std::vector<uint64_t>& hist, uint32_t g) {
-    std::vector<uint32_t> map(kPrefixBuckets, 0);
-    double total = 0;
-    for (uint64_t h : hist) total += double(h);
-    if (total == 0) return map;
-    double before = 0;
-    for (uint32_t b = 0; b < kPrefixBuckets; ++b) {
-        const double h = double(hist[b]);
-        const double mid = before + h / 2.0;
-        int64_t r = int64_t(std::floor(mid * g / total));
-        map[b] = uint32_t(std::min<int64_t>(std::max<int64_t>(r, 0), g - 1));
-        before += h;
-    }
-    return map;
-}
-
-// run f(i) for i in [0, n) on n host threads; returns the first nonzero status
-template <typename F>
-int run_per_device(int n, F&& f) {
-    std::vector<int> rc(n, RADULS_GPU_OK);
-    std::vector<std::thread> th;
-    for (int i = 0; i < n; ++i) th.emplace_back([&, i] { rc[i] = f(i); });
-    for (auto& t : th) t.join();
-    for (int i = 0; i < n; ++i)
-        if (rc[i] != RADULS_GPU_OK) return rc[i];
-    return RADULS_GPU_OK;
-}
 
 }  // namespace
 

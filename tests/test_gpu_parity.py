@@ -266,3 +266,34 @@ def test_c5_full_size_matches_reference_group_hashes(rg, torch_cuda):
     assert off == n
     del d
     torch_cuda.cuda.empty_cache()
+
+
+def test_host_sort_out_of_core(rg, torch_cuda, monkeypatch):
+    """raduls_gpu_sort_host beyond the device budget:
+    RADULS_GPU_DEVICE_BUDGET forces the out-of-core plan (streamed AND/OR +
+    16-bit prefix histogram, greedy contiguous parts, streamed stable
+    partition into host scratch, per-part device sort) on inputs several times
+    the budget; the result must equal the in-core sort byte for byte."""
+    for rs, ks, dist, n in [(16, 8, oracle.DIST_UNIFORM, 6_000_000), (16, 8, oracle.DIST_SKEW, 3_000_000),
+                            (32, 24, oracle.DIST_UNIFORM, 2_000_000), (8, 8, oracle.DIST_UNIFORM, 5_000_000)]:
+        lay = rg.RecordLayout(rs, ks)
+        d = rg.generate(n, lay, dist=dist, seed=0x5EED0000 + rs + dist)
+        a = d.cpu().numpy()
+        rg.sort(d, n, lay)
+        want = d.cpu().numpy()
+        monkeypatch.setenv("RADULS_GPU_DEVICE_BUDGET", str(96 << 20))
+        b = a.copy()
+        rg.sort(b, n, lay)
+        assert np.array_equal(b, want), (rs, ks, dist)
+        # caller-provided host scratch (the drop-in's tmp argument)
+        c = a.copy()
+        tmp = np.empty_like(a)
+        rc = rg._lib.load().raduls_gpu_sort_host(c.ctypes.data, tmp.ctypes.data, n, rs, ks)
+        assert rc == 0 and np.array_equal(c, want)
+        monkeypatch.delenv("RADULS_GPU_DEVICE_BUDGET")
+    # all keys equal: nothing moves
+    monkeypatch.setenv("RADULS_GPU_DEVICE_BUDGET", str(96 << 20))
+    e = make_input(3_000_000, 16, 8, 1, universe=1)
+    f = e.copy()
+    rg.sort(f, 3_000_000, rg.RecordLayout(16, 8))
+    assert np.array_equal(f, e)
