@@ -107,8 +107,18 @@ __global__ void __launch_bounds__(256) k_andor(const uint8_t* __restrict__ data,
 // 2w+1), pre-initialised.
 // kMap: the digit is the destination rank of the record's 16-bit key prefix
 // at bytes (p, p+1) through a 65536-entry map (multi-GPU partition).
+// Threads of a histogram CTA: ~8 records in flight per thread whatever the
+// scatter tile size (a multiple of 32, <= 1024, >= 256 for the digit counts).
+template <int RS, int kTile>
+struct HistCfg {
+    static constexpr int kIt = RS == 8 ? 16 : 8;
+    static constexpr int kThreads = ((kTile + kIt - 1) / kIt + 31) / 32 * 32 < 256
+                                        ? 256
+                                        : ((kTile + kIt - 1) / kIt + 31) / 32 * 32;
+};
+
 template <int RS, int kTile, bool kMap = false>
-__global__ void __launch_bounds__(256) k_tile_hist(const uint8_t* __restrict__ data,
+__global__ void __launch_bounds__(HistCfg<RS, kTile>::kThreads) k_tile_hist(const uint8_t* __restrict__ data,
                                                    const uint8_t* __restrict__ tmp,
                                                    const Seg* __restrict__ segs,
                                                    const uint32_t* __restrict__ tile_seg,
@@ -117,10 +127,11 @@ __global__ void __launch_bounds__(256) k_tile_hist(const uint8_t* __restrict__ d
                                                    LevelCounters* __restrict__ ctr, uint32_t ks = 0,
                                                    const uint8_t* __restrict__ map = nullptr) {
     constexpr int KW = RS / 8;
-    constexpr int IT = kTile / 256;
+    constexpr int HT = HistCfg<RS, kTile>::kThreads, HW = HT / 32;
+    constexpr int IT = (kTile + HT - 1) / HT;
     __shared__ uint32_t sh[kRadix];
-    __shared__ unsigned long long s_and[8][KW], s_or[8][KW];
-    sh[threadIdx.x] = 0;
+    __shared__ unsigned long long s_and[HW][KW], s_or[HW][KW];
+    if (threadIdx.x < kRadix) sh[threadIdx.x] = 0;
     const uint32_t tile = blockIdx.x;
     const uint32_t s = tile_seg[tile];
     const Seg g = segs[s];
@@ -131,7 +142,7 @@ __global__ void __launch_bounds__(256) k_tile_hist(const uint8_t* __restrict__ d
     Rec<RS> r[IT];
 #pragma unroll
     for (int j = 0; j < IT; ++j) {  // all loads in flight
-        const uint32_t i = uint32_t(j) * 256u + threadIdx.x;
+        const uint32_t i = uint32_t(j) * HT + threadIdx.x;
         if (i < tn) {
             r[j] = load_rec_stream<RS>(src, i);
         } else {
@@ -145,7 +156,7 @@ __global__ void __launch_bounds__(256) k_tile_hist(const uint8_t* __restrict__ d
     for (int w = 0; w < KW; ++w) a[w] = ~0ull, o[w] = 0ull;
 #pragma unroll
     for (int j = 0; j < IT; ++j) {
-        const uint32_t i = uint32_t(j) * 256u + threadIdx.x;
+        const uint32_t i = uint32_t(j) * HT + threadIdx.x;
         const bool valid = i < tn;
         if constexpr (kMap) {
             if (valid) {
@@ -184,12 +195,12 @@ __global__ void __launch_bounds__(256) k_tile_hist(const uint8_t* __restrict__ d
     __syncthreads();
     if (!kMap && threadIdx.x < KW) {
         unsigned long long ra = ~0ull, ro = 0ull;
-        for (int q = 0; q < 8; ++q) ra &= s_and[q][threadIdx.x], ro |= s_or[q][threadIdx.x];
+        for (int q = 0; q < HW; ++q) ra &= s_and[q][threadIdx.x], ro |= s_or[q][threadIdx.x];
         atomicAnd(&seg_andor[uint64_t(s) * 8 + 2 * threadIdx.x], ra);
         atomicOr(&seg_andor[uint64_t(s) * 8 + 2 * threadIdx.x + 1], ro);
     }
     if (threadIdx.x == 0) atomicAdd(&ctr->hist_records, (unsigned long long)tn);
-    tile_cnt[uint64_t(tile) * kRadix + threadIdx.x] = uint16_t(sh[threadIdx.x]);
+    if (threadIdx.x < kRadix) tile_cnt[uint64_t(tile) * kRadix + threadIdx.x] = uint16_t(sh[threadIdx.x]);
 }
 
 }  // namespace rg

@@ -422,7 +422,7 @@ void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t 
                   cudaStream_t st, uint32_t ks = 0, const uint8_t* map = nullptr) {
     constexpr int TILE = ScatterCfg<RS>::kTile;
     int pe = ws.prof.begin(K_HIST, st);
-    k_tile_hist<RS, TILE, kMap><<<ntiles, 256, 0, st>>>(data, tmp, ws.segs[cur].p, ws.tile_seg[cur].p,
+    k_tile_hist<RS, TILE, kMap><<<ntiles, HistCfg<RS, TILE>::kThreads, 0, st>>>(data, tmp, ws.segs[cur].p, ws.tile_seg[cur].p,
                                                         ws.tile_cnt.p, ws.seg_andor[cur].p, c, ks, map);
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
