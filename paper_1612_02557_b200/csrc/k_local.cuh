@@ -14,18 +14,20 @@
 //   * record sizes 16/24/32: one TMA bulk copy (cp.async.bulk + mbarrier) puts
 //     the group in shared memory; the output walks final positions in order
 //     (coalesced vector stores) reading records from shared memory;
-//   * record size 8 (groups up to 20 K records, BASELINE C2's 16 K-record
-//     bins): records stay in registers and each thread stores its own records
-//     at their final positions.
+//   * record size 8 (groups up to 18 K records, BASELINE C2's 16 K-record
+//     bins): records stay in registers; the output is staged through shared
+//     memory in final order, then written with coalesced stores.
 // Steps: AND/OR of the key words (REDUX) -> the varying key bytes
 // L = l0 < l1 < ... in [p, ks); their first <= 4 form a big-endian 32-bit
-// window w per record; one counting pass over ~n buckets spread linearly over
-// [min w, max w] (histogram, scan, scatter of record ids); then each slot ranks
-// its record inside its (tiny) bucket by (w, remaining key bytes, input index)
-// with warp shuffles over neighbouring slots. Duplicate-heavy groups (a bucket
-// over kMaxBucket) are handed untouched to the kFallback instance: a stable LSD
-// over every varying byte. Every path orders equal keys by input index, so the
-// sort is stable.
+// window w per record (one byte permute when they sit in two adjacent words);
+// one counting pass over ~2n buckets spread linearly over [min w, max w]
+// (histogram with packed u16 counters, vectorised conflict-free scan, scatter
+// of record ids); then every record ranks itself inside its bucket, branch-
+// free for buckets of <= 3 records, by (w, remaining key bytes, input index);
+// larger buckets go to a short list ranked afterwards. Duplicate-heavy groups
+// (a bucket over kMaxBucket) are handed untouched to the kFallback instance: a
+// stable LSD over every varying byte. Every path orders equal keys by input
+// index, so the sort is stable.
 #pragma once
 
 #include "common.cuh"
@@ -665,285 +667,6 @@ __global__ void __launch_bounds__(256) k_copy_back(uint8_t* __restrict__ data,
         for (uint64_t i = threadIdx.x; i < bytes / 8; i += blockDim.x)
             reinterpret_cast<uint2*>(d)[i] = reinterpret_cast<const uint2*>(s)[i];
     }
-}
-
-}  // namespace rg
-
-namespace rg {
-
-// ---------------------------------------------------------------------------
-// LSD variant for 16/24/32-B records (k_local_lsd): the group is TMA-loaded
-// into shared memory as above; (window, record id) pairs live in registers in
-// warp-striped position order and go through one stable LSD pass per window
-// byte: rank = one shared-memory atomic on a warp-private digit counter
-// (conflicting lanes are served in lane order, the property the scatter's
-// byte-exact parity tests pin), digit-major / warp-minor offsets, exchange
-// through one shared buffer. After the passes, equal windows with more key
-// bytes beyond them are checked pairwise: a misordered pair is swapped, a longer
-// misordered tie run hands the untouched group to the k_local<RS, true> LSD
-// instance. No bucket scan, no divergent loops.
-template <int RS>
-struct LsdCfg {
-    static constexpr int kThreads = 512;
-    static constexpr int kWarps = kThreads / 32;
-    static constexpr int kMinBlocks = RS == 32 ? 1 : 2;
-    static constexpr int kCap = LocalCfg<RS>::kCap;
-    static constexpr int kIpt = (kCap + kThreads - 1) / kThreads;
-    static constexpr int kChunk = kIpt * 32;  // positions per warp
-    static constexpr int kRecBytes = ((kCap * RS + 16 + 127) / 128) * 128;
-    static constexpr size_t kSmem =
-        size_t(kRecBytes) + size_t(kCap) * (4 + 2) + size_t(kWarps) * kRadix * 4;
-};
-
-template <int RS>
-__global__ void __launch_bounds__(LsdCfg<RS>::kThreads, LsdCfg<RS>::kMinBlocks) k_local_lsd(
-    uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group* __restrict__ groups,
-    uint32_t ks, LevelCounters* __restrict__ ctr, Group* __restrict__ spill,
-    unsigned int* __restrict__ n_spill, uint32_t spill_cap) {
-    using C = LsdCfg<RS>;
-    constexpr int T = C::kThreads, W = C::kWarps, IPT = C::kIpt, CH = C::kChunk;
-    constexpr int TPD = T / 256, WPT = W / TPD;
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint32_t* xkey = reinterpret_cast<uint32_t*>(smem + C::kRecBytes);  // [cap] exchange
-    uint16_t* xidx = reinterpret_cast<uint16_t*>(xkey + C::kCap);       // [cap]
-    uint32_t* wcnt = reinterpret_cast<uint32_t*>(xidx + C::kCap);       // [W][256]
-    __shared__ uint32_t s_and[W][RS / 4], s_or[W][RS / 4];
-    __shared__ uint32_t s_L[32];
-    __shared__ uint32_t s_tot[512];
-    __shared__ uint32_t s_nL, s_flag;
-    __shared__ __align__(8) unsigned long long s_bar;
-
-    const Group g = groups[blockIdx.x];
-    const uint32_t n = g.size;
-    const uint8_t* gsrc = (g.parity ? tmp : data) + g.start * RS;
-    uint8_t* dst = data + g.start * RS;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (n <= 1) {
-        if (n == 1 && g.parity && threadIdx.x == 0) store_rec<RS>(dst, 0, load_rec<RS>(gsrc, 0));
-        return;
-    }
-    // ---- 1. the group into shared memory (TMA)
-    const uint32_t head = uint32_t(reinterpret_cast<uintptr_t>(gsrc) & 15u);
-    const uint8_t* recs = smem + head;
-    if (threadIdx.x == 0) {
-        mbar_init(&s_bar, 1);
-        fence_mbar_init();
-        const uint32_t bytes = n * RS;
-        const uint32_t hb = head ? min(8u, bytes) : 0u;
-        const uint32_t body = (bytes - hb) & ~15u;
-        const uint32_t tail = bytes - hb - body;
-        if (hb) *reinterpret_cast<uint2*>(smem + head) = *reinterpret_cast<const uint2*>(gsrc);
-        if (tail)
-            *reinterpret_cast<uint2*>(smem + head + hb + body) =
-                *reinterpret_cast<const uint2*>(gsrc + hb + body);
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&s_bar, body);
-        for (uint32_t o = 0; o < body; o += 32768u)
-            tma_load_1d(smem + head + hb + o, gsrc + hb + o, min(32768u, body - o), &s_bar);
-        s_flag = 0;
-    }
-    __syncthreads();
-    mbar_wait(&s_bar, 0);
-
-    // positions are warp-striped: warp w owns [w*CH, (w+1)*CH), round s, lane l
-    auto pos_of = [&](int s) { return uint32_t(warp) * CH + uint32_t(s) * 32 + lane; };
-
-    // ---- 2. AND/OR (REDUX) -> varying key bytes
-    {
-        uint32_t a[RS / 4], o[RS / 4];
-#pragma unroll
-        for (int w = 0; w < RS / 4; ++w) a[w] = ~0u, o[w] = 0u;
-#pragma unroll
-        for (int s = 0; s < IPT; ++s) {
-            const uint32_t e = pos_of(s);
-            if (e < n) {
-                const Rec<RS> v = ld_smem_rec<RS>(recs, e);
-#pragma unroll
-                for (int w = 0; w < RS / 4; ++w) a[w] &= v.w[w], o[w] |= v.w[w];
-            }
-        }
-#pragma unroll
-        for (int w = 0; w < RS / 4; ++w) {
-            a[w] = __reduce_and_sync(0xFFFFFFFFu, a[w]);
-            o[w] = __reduce_or_sync(0xFFFFFFFFu, o[w]);
-        }
-        if (lane < RS / 4) {
-            uint32_t av = a[0], ov = o[0];
-#pragma unroll
-            for (int w = 1; w < RS / 4; ++w)
-                if (lane == w) av = a[w], ov = o[w];
-            s_and[warp][lane] = av;
-            s_or[warp][lane] = ov;
-        }
-    }
-    __syncthreads();
-    if (warp == 0) {
-        const uint32_t b = lane;
-        uint32_t diffb = 0;
-        if (b >= g.p && b < ks && b < uint32_t(RS)) {
-            uint32_t ra = ~0u, ro = 0u;
-            for (int q = 0; q < W; ++q) ra &= s_and[q][b >> 2], ro |= s_or[q][b >> 2];
-            diffb = ((ra ^ ro) >> ((b & 3) * 8)) & 0xFFu;
-        }
-        const uint32_t vm = __ballot_sync(0xFFFFFFFFu, diffb != 0);
-        if (diffb) s_L[__popc(vm & lanemask_lt())] = lane;
-        if (lane == 0) s_nL = __popc(vm);
-    }
-    __syncthreads();
-    const uint32_t nL = s_nL;
-    if (nL == 0) {
-        if (g.parity)
-#pragma unroll
-            for (int s = 0; s < IPT; ++s) {
-                const uint32_t e = pos_of(s);
-                if (e < n) store_rec<RS>(dst, e, ld_smem_rec<RS>(recs, e));
-            }
-        return;
-    }
-    const uint32_t nwin = nL < 4 ? nL : 4;
-    const bool beyond = nL > 4;
-
-    // ---- 3. windows into registers (record id = initial position)
-    uint32_t kv[IPT], iv[IPT];
-    {
-        const uint32_t L0 = s_L[0], L1 = s_L[nwin > 1 ? 1 : 0], L2 = s_L[nwin > 2 ? 2 : 0],
-                       L3 = s_L[nwin > 3 ? 3 : 0];
-#pragma unroll
-        for (int s = 0; s < IPT; ++s) {
-            const uint32_t e = pos_of(s);
-            uint32_t w = 0;
-            if (e < n) {
-                const Rec<RS> v = ld_smem_rec<RS>(recs, e);
-                w = rec_byte<RS>(v, L0) << 24;
-                if (nwin > 1) w |= rec_byte<RS>(v, L1) << 16;
-                if (nwin > 2) w |= rec_byte<RS>(v, L2) << 8;
-                if (nwin > 3) w |= rec_byte<RS>(v, L3);
-            }
-            kv[s] = w;
-            iv[s] = e;
-        }
-    }
-
-    // ---- 4. stable LSD over the window bytes (least significant first)
-    uint32_t* my = wcnt + warp * kRadix;
-    for (int q = int(nwin) - 1; q >= 0; --q) {
-        const uint32_t sh = 24u - 8u * uint32_t(q);
-#pragma unroll
-        for (int k = 0; k < kRadix / 32; ++k) my[k * 32 + lane] = 0;
-        __syncwarp();
-        uint32_t pk[IPT];
-#pragma unroll
-        for (int s = 0; s < IPT; ++s) {
-            const uint32_t d = (kv[s] >> sh) & 0xFFu;
-            pk[s] = pos_of(s) < n ? (d | (atomicAdd(&my[d], 1u) << 8)) : 0xFFFFFFFFu;
-        }
-        __syncthreads();
-        {  // digit-major, warp-minor exclusive offsets
-            const uint32_t d = threadIdx.x / TPD, qq = threadIdx.x % TPD;
-            uint32_t part = 0;
-#pragma unroll
-            for (int w = 0; w < WPT; ++w) part += wcnt[(qq * WPT + w) * kRadix + d];
-            uint32_t x = part;
-#pragma unroll
-            for (int o = 1; o < TPD; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o, TPD);
-                if (qq >= uint32_t(o)) x += y;
-            }
-            const uint32_t qexcl = x - part;
-            if (qq == TPD - 1) s_tot[d] = x;
-            __syncthreads();
-            if (warp == 0) {
-                uint32_t v[8], sum = 0;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) v[i] = s_tot[lane * 8 + i], sum += v[i];
-                uint32_t xs = sum;
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const uint32_t z = __shfl_up_sync(0xFFFFFFFFu, xs, off);
-                    if (lane >= off) xs += z;
-                }
-                uint32_t run = xs - sum;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    s_tot[256 + lane * 8 + i] = run;
-                    run += v[i];
-                }
-            }
-            __syncthreads();
-            uint32_t run = s_tot[256 + d] + qexcl;
-#pragma unroll
-            for (int w = 0; w < WPT; ++w) {
-                uint32_t* c = &wcnt[(qq * WPT + w) * kRadix + d];
-                const uint32_t cn = *c;
-                *c = run;
-                run += cn;
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int s = 0; s < IPT; ++s) {
-            if (pk[s] != 0xFFFFFFFFu) {
-                const uint32_t np = my[pk[s] & 0xFFu] + (pk[s] >> 8);
-                xkey[np] = kv[s];
-                xidx[np] = uint16_t(iv[s]);
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int s = 0; s < IPT; ++s) {
-            const uint32_t p = pos_of(s);
-            if (p < n) kv[s] = xkey[p], iv[s] = xidx[p];
-        }
-    }
-
-    // ---- 5. ties beyond the window: swap a misordered pair, else fall back
-    uint32_t oe[IPT];  // record to emit at each owned position
-#pragma unroll
-    for (int s = 0; s < IPT; ++s) oe[s] = iv[s];
-    if (beyond) {
-        auto cmp_rest = [&](uint32_t a, uint32_t b) -> int {
-            for (uint32_t q = 4; q < nL; ++q) {
-                const uint32_t x = recs[size_t(a) * RS + s_L[q]], y = recs[size_t(b) * RS + s_L[q]];
-                if (x != y) return x < y ? -1 : 1;
-            }
-            return 0;
-        };
-#pragma unroll
-        for (int s = 0; s < IPT; ++s) {
-            const uint32_t p = pos_of(s);
-            if (p >= n) continue;
-            const uint32_t w = kv[s];
-            const bool peq = p > 0 && xkey[p - 1] == w;
-            const bool neq = p + 1 < n && xkey[p + 1] == w;
-            if (neq && cmp_rest(iv[s], xidx[p + 1]) > 0) {  // (p, p+1) misordered
-                const bool pair = !peq && !(p + 2 < n && xkey[p + 2] == w);
-                if (pair) oe[s] = xidx[p + 1];
-                else s_flag = 1;
-            }
-            if (peq && cmp_rest(xidx[p - 1], iv[s]) > 0) {  // (p-1, p) misordered
-                const bool pair = !neq && !(p >= 2 && xkey[p - 2] == w);
-                if (pair) oe[s] = xidx[p - 1];
-                else s_flag = 1;
-            }
-        }
-        __syncthreads();
-        if (s_flag) {  // hand the untouched group to the full-key LSD instance
-            if (threadIdx.x == 0) {
-                const uint32_t i = atomicAdd(n_spill, 1u);
-                if (i < spill_cap) spill[i] = g;
-                atomicAdd(&ctr->fallback_groups, 1ull);
-            }
-            return;
-        }
-    }
-
-    // ---- 6. coalesced output in final order, records read from shared memory
-#pragma unroll
-    for (int s = 0; s < IPT; ++s) {
-        const uint32_t p = pos_of(s);
-        if (p < n) store_rec<RS>(dst, p, ld_smem_rec<RS>(recs, oe[s]));
-    }
-    if (threadIdx.x == 0) atomicAdd(&ctr->moved_local, (unsigned long long)n);
 }
 
 }  // namespace rg

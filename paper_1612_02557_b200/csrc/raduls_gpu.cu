@@ -396,9 +396,6 @@ void set_attrs(Workspace& ws) {
     if (ws.attrs_set[RS]) return;
     RG_CHECK(cudaFuncSetAttribute(k_local<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(LocalCfg<RS>::kSmem)));
-    if constexpr (RS != 8)
-        RG_CHECK(cudaFuncSetAttribute(k_local_lsd<RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(LsdCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_local<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(LocalCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -453,18 +450,8 @@ void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, 
                   LevelCounters* ctr, cudaStream_t st) {
     if (!ngroups) return;
     const int pe = ws.prof.begin(K_LOCAL, st);
-    // bucket variant by default (fewer shared-memory wavefronts per record);
-    // RADULS_GPU_LOCAL=lsd selects the window-LSD variant (A/B experiments)
-    static const bool use_lsd = [] {
-        const char* v = std::getenv("RADULS_GPU_LOCAL");
-        return v && std::strcmp(v, "lsd") == 0;
-    }();
-    if (RS == 8 || !use_lsd)
-        k_local<RS, false><<<ngroups, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
-            data, tmp, ws.groups.p, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
-    else if constexpr (RS != 8)
-        k_local_lsd<RS><<<ngroups, LsdCfg<RS>::kThreads, LsdCfg<RS>::kSmem, st>>>(
-            data, tmp, ws.groups.p, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
+    k_local<RS, false><<<ngroups, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
+        data, tmp, ws.groups.p, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
 }
