@@ -273,6 +273,15 @@ def local_capacity(record_size: int) -> int:
     return _LOCAL_CAP[record_size]
 
 
+# Scatter / histogram tile per record size (mirrors ScatterCfg<RS>::kTile in
+# csrc/k_scatter.cuh; tests aim at its boundaries).
+_SCATTER_TILE = {8: 4096, 16: 2560, 24: 1792, 32: 1536}
+
+
+def scatter_tile(record_size: int) -> int:
+    return _SCATTER_TILE[record_size]
+
+
 def _host_records(data, n, rs):
     if isinstance(data, (bytearray, memoryview)):
         arr = np.frombuffer(data, dtype=np.uint8)

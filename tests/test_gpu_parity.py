@@ -297,3 +297,21 @@ def test_host_sort_out_of_core(rg, torch_cuda, monkeypatch):
     f = e.copy()
     rg.sort(f, 3_000_000, rg.RecordLayout(16, 8))
     assert np.array_equal(f, e)
+
+
+@pytest.mark.parametrize("rs,ks", [(8, 8), (16, 8), (24, 16), (32, 24)])
+def test_scatter_tile_boundaries(rg, torch_cuda, rs, ks):
+    """Sizes straddling multiples of the scatter tile above the local-sort
+    capacity (so a scatter level runs), and the single-segment split."""
+    tile, cap = rg.raduls.scatter_tile(rs), rg.local_capacity(rs)
+    k0 = cap // tile + 1
+    for j, n in enumerate([k0 * tile - 1, k0 * tile, k0 * tile + 1, (k0 + 3) * tile + 7]):
+        a = make_input(n, rs, ks, 4242 + j, (0, 300, 2, 0)[j])
+        assert_parity(gpu_sort(rg, torch_cuda, a, rs, ks), a, rs, ks)
+        d = to_dev(torch_cuda, a)
+        out = torch_cuda.empty_like(d)
+        counts = rg.split(d, out, n, rs, 0)
+        torch_cuda.cuda.synchronize()
+        want = a.reshape(n, rs)[np.argsort(a.reshape(n, rs)[:, 0], kind="stable")].reshape(-1)
+        assert np.array_equal(from_dev(out), want)
+        assert list(counts) == list(np.bincount(a.reshape(n, rs)[:, 0], minlength=256))
