@@ -57,6 +57,7 @@ struct LocalCfg {
 };
 
 // Block-wide exclusive scan (blockDim a multiple of 32, <= 1024).
+template <bool kTrailingSync = true>
 __device__ __forceinline__ uint32_t block_scan_excl(uint32_t v, uint32_t* s_w, uint32_t* total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
@@ -82,7 +83,7 @@ __device__ __forceinline__ uint32_t block_scan_excl(uint32_t v, uint32_t* s_w, u
     __syncthreads();
     const uint32_t r = s_w[32 + warp] + x - v;
     *total = s_w[64];
-    __syncthreads();
+    if (kTrailingSync) __syncthreads();  // s_w may be reused
     return r;
 }
 
@@ -193,8 +194,8 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
     __shared__ uint32_t s_tot[512];
     __shared__ uint32_t s_scan[65];
     __shared__ uint32_t s_and[W][2 * KW], s_or[W][2 * KW];
-    __shared__ uint32_t s_L[32];
-    __shared__ uint32_t s_nL, s_flag, s_maxb, s_wmin, s_wmax, s_B;
+    __shared__ uint32_t s_Lw[W][32];  // per-warp copy of the varying key bytes
+    __shared__ uint32_t s_flag, s_maxb, s_wmin, s_wmax, s_B;
     __shared__ uint32_t s_mul;
     __shared__ __align__(8) unsigned long long s_bar;
 
@@ -242,6 +243,9 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         s_flag = 0;
         s_maxb = 0;
     }
+    // bucket counters zeroed now (first used by the histogram, several barriers on)
+    for (uint32_t i = threadIdx.x; i < uint32_t(C::kCntWords + 3) / 4; i += T)
+        reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     if constexpr (!REG) mbar_wait(&s_bar, 0);
     auto rec_of = [&](int j, uint32_t e) -> Rec<RS> {
@@ -279,7 +283,10 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         }
     }
     __syncthreads();
-    if (warp == 0) {
+    // every warp derives the varying bytes itself (no second block barrier)
+    uint32_t* s_L = s_Lw[warp];
+    uint32_t nL;
+    {
         const uint32_t b = lane;  // key byte b lives in 32-bit word b/4
         uint32_t diffb = 0;
         if (b >= g.p && b < ks && b < uint32_t(RS)) {
@@ -289,10 +296,9 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         }
         const uint32_t vm = __ballot_sync(0xFFFFFFFFu, diffb != 0);
         if (diffb) s_L[__popc(vm & lanemask_lt())] = lane;
-        if (lane == 0) s_nL = __popc(vm);
+        nL = __popc(vm);
+        __syncwarp();
     }
-    __syncthreads();
-    const uint32_t nL = s_nL;
     if (nL == 0) {  // every key equal: stable order is the input order
         if (g.parity) {
 #pragma unroll
@@ -387,10 +393,7 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         return 0;
     };
 
-    // ---- 4. bucket histogram (packed u16 pairs), scan, largest bucket
-    for (uint32_t i = threadIdx.x; i < (nbk / 2 + nbk / 16 + 3) / 4; i += T)
-        reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
+    // ---- 4. bucket histogram (packed u16 pairs, zeroed at the start), scan, largest bucket
     uint32_t bk[KEEP ? IPT : 1];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
@@ -430,7 +433,7 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
             }
         }
         uint32_t total;
-        uint32_t run = block_scan_excl(sum, s_scan, &total);
+        uint32_t run = block_scan_excl<false>(sum, s_scan, &total);
         mx = __reduce_max_sync(0xFFFFFFFFu, mx);
         if (lane == 0 && mx) atomicMax(&s_maxb, mx);
         // counts -> (start of even bucket | start of odd bucket << 16)
@@ -501,8 +504,7 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
             return rank;
         };
         uint16_t* lst = reinterpret_cast<uint16_t*>(s_tot);  // up to 1024 deferred records (s_tot: 512 u32)
-        if (threadIdx.x == 0) s_flag = 0;  // list length
-        __syncthreads();
+        // s_flag (the list length) is still 0 from the start
         // Buckets of <= 3 records (nearly all): branch-free, so the unrolled
         // loop overlaps the shared-memory loads of all the thread's records; the
         // bucket's slots are read clamped (a slot equal to e counts nothing).
