@@ -176,9 +176,10 @@ __device__ __forceinline__ void lsd_pass_w(uint32_t n, const uint16_t* pin, uint
     __syncthreads();
 }
 
+// One group, by the whole CTA (called per group by the persistent k_local).
 template <int RS, bool kFallback>
-__global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBlocks) k_local(
-    uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group* __restrict__ groups,
+__device__ __forceinline__ void local_group(
+    uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group g,
     uint32_t ks, LevelCounters* __restrict__ ctr, Group* __restrict__ spill,
     unsigned int* __restrict__ n_spill, uint32_t spill_cap) {
     using C = LocalCfg<RS>;
@@ -199,7 +200,6 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
     __shared__ uint32_t s_mul;
     __shared__ __align__(8) unsigned long long s_bar;
 
-    const Group g = groups[blockIdx.x];
     const uint32_t n = g.size;
     const uint8_t* gsrc = (g.parity ? tmp : data) + g.start * RS;
     uint8_t* dst = data + g.start * RS;
@@ -648,6 +648,53 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
             store_rec<RS>(dst, f, ld_smem_rec<RS>(recs, perm[f]));
     }
     if (threadIdx.x == 0) atomicAdd(&ctr->moved_local, (unsigned long long)n);
+}
+
+// Pull a group's bytes toward L2 (cp.async.bulk.prefetch.L2): issued one group
+// ahead, so the next group's TMA copy / loads are served from L2 while this
+// group is being sorted.
+template <int RS>
+__device__ __forceinline__ void prefetch_group_l2(const uint8_t* data, const uint8_t* tmp, const Group& g) {
+    const uintptr_t src = reinterpret_cast<uintptr_t>((g.parity ? tmp : data) + g.start * RS);
+    uintptr_t a = (src + 15) & ~uintptr_t(15);
+    const uintptr_t e = (src + uintptr_t(g.size) * RS) & ~uintptr_t(15);
+    for (; a < e; a += 32768) {
+        const uint32_t sz = uint32_t(min(uintptr_t(32768), e - a));
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(sz) : "memory");
+    }
+}
+
+// Local sort launch. One CTA per SM (8- and 32-B records): persistent, CTAs
+// claim groups through a ticket one group ahead and prefetch the next group
+// into L2 while sorting the current one (its HBM latency otherwise stalls the
+// SM at every group start). Two CTAs per SM: one group per CTA.
+template <int RS, bool kFallback>
+__global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBlocks) k_local(
+    uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group* __restrict__ groups,
+    uint32_t n_groups, unsigned int* __restrict__ ticket, uint32_t ks,
+    LevelCounters* __restrict__ ctr, Group* __restrict__ spill, unsigned int* __restrict__ n_spill,
+    uint32_t spill_cap) {
+    if constexpr (LocalCfg<RS>::kMinBlocks > 1) {
+        // two CTAs per SM already overlap one group's load with the other's
+        // sort; the hardware block scheduler refills freed slots (measured:
+        // faster than a persistent loop here)
+        local_group<RS, kFallback>(data, tmp, groups[blockIdx.x], ks, ctr, spill, n_spill, spill_cap);
+        return;
+    }
+    __shared__ uint32_t s_next[2];
+    if (threadIdx.x == 0) s_next[1] = atomicAdd(ticket, 1u);
+    __syncthreads();
+    uint32_t cur = s_next[1];
+    for (uint32_t it = 0; cur < n_groups; ++it) {
+        if (threadIdx.x == 0) {
+            const uint32_t nxt = atomicAdd(ticket, 1u);
+            s_next[it & 1] = nxt;
+            if (nxt < n_groups) prefetch_group_l2<RS>(data, tmp, groups[nxt]);
+        }
+        local_group<RS, kFallback>(data, tmp, groups[cur], ks, ctr, spill, n_spill, spill_cap);
+        __syncthreads();  // shared memory free for the next group; s_next visible
+        cur = s_next[it & 1];
+    }
 }
 
 // Finished records that ended in tmp move home (reference finalize(),
