@@ -678,6 +678,10 @@ __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBloc
         // two CTAs per SM already overlap one group's load with the other's
         // sort; the hardware block scheduler refills freed slots (measured:
         // faster than a persistent loop here)
+        // the group one resident wave later starts from L2
+        constexpr uint32_t kAhead = 2 * 148;
+        if (threadIdx.x == 0 && blockIdx.x + kAhead < n_groups)
+            prefetch_group_l2<RS>(data, tmp, groups[blockIdx.x + kAhead]);
         local_group<RS, kFallback>(data, tmp, groups[blockIdx.x], ks, ctr, spill, n_spill, spill_cap);
         return;
     }
