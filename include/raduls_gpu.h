@@ -176,14 +176,39 @@ int raduls_gpu_partition(const void* d_src, void* d_dst, uint64_t n_recs, uint32
                          uint32_t n_ranks, uint64_t* h_rank_counts, void* stream);
 
 /*
+ * The partition fused with the exchange: like
+ * raduls_gpu_partition, but destination rank r's records are stored by the
+ * partition kernel itself, in stable order, to the byte address h_dst[r] —
+ * typically a peer GPU's receive buffer reached over NVLink (peer access
+ * enabled, or a raduls_gpu_ipc_open mapping), at this source's offset there.
+ * h_dst[r] must be 16-B aligned (8-B for record sizes 8 and 24). Synchronous.
+ */
+int raduls_gpu_partition_to(const void* d_src, uint64_t n_recs, uint32_t rec_size, uint32_t key_size,
+                            uint32_t prefix_byte, const uint32_t* d_bucket_rank, uint32_t n_ranks,
+                            const uint64_t* h_dst, uint64_t* h_rank_counts, void* stream);
+
+/*
+ * CUDA IPC for the multi-process exchange: raduls_gpu_ipc_alloc allocates
+ * device memory and returns its 64-byte IPC handle; a peer process maps it
+ * with raduls_gpu_ipc_open (lazy peer access) and unmaps with
+ * raduls_gpu_ipc_close; raduls_gpu_free releases the allocation.
+ */
+int raduls_gpu_ipc_alloc(uint64_t bytes, void** d_ptr, uint8_t* handle);
+int raduls_gpu_ipc_open(const uint8_t* handle, void** d_ptr);
+int raduls_gpu_ipc_close(void* d_ptr);
+int raduls_gpu_free(void* d_ptr);
+
+/*
  * Multi-GPU sort in one call: G devices, one host thread
  * per device. Device g holds n_in[g] records at d_in[g] (left unchanged). On
  * return d_out[g] (capacity out_capacity_recs records) holds n_out[g] records:
  * the g-th contiguous key range, sorted; the concatenation over g is the
  * stable sort of the inputs concatenated in device order. Plan: the first
  * key byte varying over all devices, 16-bit prefix histograms, contiguous
- * count-balanced bucket ranges (a bucket is never split); stable device
- * partition; peer copies over NVLink (cudaMemcpyPeerAsync); local sort.
+ * count-balanced bucket ranges (a bucket is never split); the stable device
+ * partition stores each destination's records straight into that device's
+ * d_out over NVLink (raduls_gpu_partition_to; peer copies when P2P is
+ * unavailable); local sort.
  * EINVAL (nothing written) when a device would receive more than
  * out_capacity_recs records. A device may be listed more than once.
  */

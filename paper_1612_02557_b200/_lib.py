@@ -37,6 +37,11 @@ EXPORTED = [
     "raduls_gpu_last_kernel_times",
     "raduls_gpu_andor",
     "raduls_gpu_sort_multi",
+    "raduls_gpu_partition_to",
+    "raduls_gpu_ipc_alloc",
+    "raduls_gpu_ipc_open",
+    "raduls_gpu_ipc_close",
+    "raduls_gpu_free",
 ]
 
 
@@ -106,6 +111,11 @@ def load(build_if_missing: bool = False):
         L.raduls_gpu_release.restype = None
         L.raduls_gpu_set_profiling.argtypes = [C.c_int]
         L.raduls_gpu_andor.argtypes = [_vp, _u64, _u32, _u64p, _vp]
+        L.raduls_gpu_partition_to.argtypes = [_vp, _u64, _u32, _u32, _u32, _vp, _u32, _u64p, _u64p, _vp]
+        L.raduls_gpu_ipc_alloc.argtypes = [_u64, C.POINTER(_vp), C.c_char_p]
+        L.raduls_gpu_ipc_open.argtypes = [C.c_char_p, C.POINTER(_vp)]
+        L.raduls_gpu_ipc_close.argtypes = [_vp]
+        L.raduls_gpu_free.argtypes = [_vp]
         L.raduls_gpu_sort_multi.argtypes = [C.c_int, C.POINTER(C.c_int), C.POINTER(_vp), _u64p,
                                             C.POINTER(_vp), _u64p, _u64, _u32, _u32]
         L.raduls_gpu_last_kernel_times.argtypes = [C.POINTER(KernelTime), C.c_int,

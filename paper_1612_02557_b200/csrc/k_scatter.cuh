@@ -90,13 +90,19 @@ struct TileInfo {
     uint64_t seg_start;
 };
 
-template <int RS, bool kMap = false>
+// kPeer (the multi-GPU partition): digit d is a destination
+// rank and its records are stored straight to dig_dst[d] — a peer GPU's
+// receive buffer over NVLink (P2P or CUDA-IPC mapped), at this source's offset
+// there — so the all-to-all is carried out by the partition's own coalesced
+// stores, tile by tile, instead of a separate collective.
+template <int RS, bool kMap = false, bool kPeer = false>
 __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
     uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Seg* __restrict__ segs,
     const unsigned long long* __restrict__ seg_base,  // [nseg][256] exclusive digit bases
     const uint32_t* __restrict__ tile_seg, const uint32_t* __restrict__ tile_off,  // [ntiles][256]
     uint32_t n_tiles, unsigned int* __restrict__ ticket, uint32_t ks = 0,
-    const uint8_t* __restrict__ map = nullptr) {
+    const uint8_t* __restrict__ map = nullptr,
+    const unsigned long long* __restrict__ dig_dst = nullptr) {
     using C = ScatterCfg<RS>;
     constexpr int T = C::kThreads, IT = C::kItems, W = C::kWarps;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -107,6 +113,7 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
     __shared__ uint32_t s_wcnt[W][kRadix];  // per-warp digit counts, then tile-local slot starts
     // destination of slot 0 of each digit, relative to the segment start (segments hold < 2^32 records)
     __shared__ uint32_t s_gdelta[kRadix];
+    __shared__ unsigned long long s_pdst[kPeer ? kRadix : 1];  // digit's destination - its base
     __shared__ uint32_t s_scan[8];
     __shared__ __align__(8) unsigned long long s_full[C::kStages], s_empty[C::kStages];
     __shared__ TileInfo s_info[C::kStages];
@@ -229,6 +236,9 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
             }
         }
         s_gdelta[threadIdx.x] = uint32_t(my_base) - lstart;
+        if constexpr (kPeer)
+            s_pdst[threadIdx.x] = dig_dst[threadIdx.x] -
+                                  (ti.seg_start + seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x]) * RS;
         bar_sync_named(1, T);
 
         // 3: slot map (digit order) in shared memory
@@ -251,7 +261,10 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
             if (slot < tn) {
                 const uint32_t m = s_map[slot];
                 const Rec<RS> v = ld_smem_rec<RS>(tile, m & 0xFFFFu);
-                store_rec<RS>(dst, uint32_t(s_gdelta[m >> 16] + slot), v);
+                if constexpr (kPeer)
+                    store_rec<RS>(reinterpret_cast<uint8_t*>(s_pdst[m >> 16] + ti.seg_start * RS), uint32_t(s_gdelta[m >> 16] + slot), v);
+                else
+                    store_rec<RS>(dst, uint32_t(s_gdelta[m >> 16] + slot), v);
             }
         }
         bar_sync_named(1, T);  // buffer b, map and counters free for reuse

@@ -289,6 +289,7 @@ struct Workspace {
     DevBuf<unsigned int> n_spill, local_ticket;
     DevBuf<CopyRange> copies;
     DevBuf<uint8_t> host_data, host_tmp, map8;
+    DevBuf<unsigned long long> dig_dst;  // per-destination byte addresses (raduls_gpu_partition_to)
     HostStager* stager = nullptr;  // host drop-ins, created on first use
     HostStager& host_stager() {
         if (!stager) stager = new HostStager();
@@ -403,6 +404,8 @@ void set_attrs(Workspace& ws) {
                                   int(ScatterCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(ScatterCfg<RS>::kSmem)));
+    RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(ScatterCfg<RS>::kSmem)));
     ws.attrs_set[RS] = true;
 }
 
@@ -433,14 +436,15 @@ void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t 
     ws.prof.end(pe, st);
 }
 
-template <int RS, bool kMap>
+template <int RS, bool kMap, bool kPeer = false>
 void launch_scatter(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t ntiles, uint32_t ks,
-                    const uint8_t* map, LevelCounters* c, cudaStream_t st) {
+                    const uint8_t* map, LevelCounters* c, cudaStream_t st,
+                    const unsigned long long* dig_dst = nullptr) {
     const uint32_t grid = std::min<uint32_t>(ntiles, uint32_t(sm_count()) * 2);
     const int pe = ws.prof.begin(K_SCATTER, st);
-    k_scatter<RS, kMap><<<grid, ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>::kSmem, st>>>(
+    k_scatter<RS, kMap, kPeer><<<grid, ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>::kSmem, st>>>(
         data, tmp, ws.segs[cur].p, ws.seg_tot[cur].p, ws.tile_seg[cur].p, ws.tile_off.p, ntiles,
-        &c->scatter_ticket, ks, map);
+        &c->scatter_ticket, ks, map, dig_dst);
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
 }
@@ -955,9 +959,10 @@ void single_segment_counts(Workspace& ws, uint8_t* src, uint64_t n, uint32_t p, 
 }
 
 // Scatter the single segment prepared by single_segment_counts from src into dst.
-template <int RS, bool kMap>
+template <int RS, bool kMap, bool kPeer = false>
 void single_segment_scatter(Workspace& ws, uint8_t* src, uint8_t* dst, uint64_t n, uint32_t ks,
-                            const uint8_t* map, const unsigned long long* h_tot, cudaStream_t st) {
+                            const uint8_t* map, const unsigned long long* h_tot, cudaStream_t st,
+                            const unsigned long long* dig_dst = nullptr) {
     constexpr int TILE = ScatterCfg<RS>::kTile;
     unsigned long long* off = ws.h_small + 1024;
     unsigned long long run = 0;
@@ -968,7 +973,7 @@ void single_segment_scatter(Workspace& ws, uint8_t* src, uint8_t* dst, uint64_t 
     RG_CHECK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(ws.segs[0].p) + offsetof(Seg, action), &act,
                              sizeof act, cudaMemcpyHostToDevice, st));
     const uint32_t nt = uint32_t((n + TILE - 1) / TILE);
-    launch_scatter<RS, kMap>(ws, src, dst, 0, nt, ks, map, ws.ctr.p, st);
+    launch_scatter<RS, kMap, kPeer>(ws, src, dst, 0, nt, ks, map, ws.ctr.p, st, dig_dst);
     RG_CHECK(cudaStreamSynchronize(st));
 }
 
@@ -1217,6 +1222,78 @@ int raduls_gpu_partition(const void* d_src, void* d_dst, uint64_t n, uint32_t rs
     });
 }
 
+int raduls_gpu_partition_to(const void* d_src, uint64_t n, uint32_t rs, uint32_t ks, uint32_t prefix_byte,
+                            const uint32_t* d_bucket_rank, uint32_t n_ranks, const uint64_t* h_dst,
+                            uint64_t* h_rank_counts, void* stream) {
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs) || n_ranks < 1 || n_ranks > 256 || !d_bucket_rank ||
+        !h_dst || n > kMaxRecords)
+        return RADULS_GPU_EINVAL;
+    if (n && !aligned_ok(d_src, rs)) return RADULS_GPU_EINVAL;
+    for (uint32_t r = 0; r < n_ranks; ++r)
+        if (h_dst[r] % (rs % 16 == 0 ? 16 : 8)) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (h_rank_counts) std::memset(h_rank_counts, 0, n_ranks * sizeof(uint64_t));
+        ws.map8.ensure(65536);
+        ws.dig_dst.ensure(kRadix);
+        RG_CHECK(cudaMemsetAsync(ws.acc.p, 0, sizeof(unsigned long long), st));
+        k_map_to_u8<<<256, 256, 0, st>>>(d_bucket_rank, ws.map8.p, n_ranks,
+                                          reinterpret_cast<unsigned int*>(ws.acc.p));
+        RG_LAUNCH_CHECK();
+        unsigned long long* hd = ws.h_small + 3072;  // pinned staging for the destinations
+        for (uint32_t r = 0; r < kRadix; ++r) hd[r] = r < n_ranks ? h_dst[r] : 0ull;
+        RG_CHECK(cudaMemcpyAsync(ws.dig_dst.p, hd, kRadix * sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+        RG_CHECK(cudaMemcpyAsync(ws.h_small + 2048, ws.acc.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                 st));
+        RG_CHECK(cudaStreamSynchronize(st));
+        if (uint32_t(ws.h_small[2048])) throw CudaError{RADULS_GPU_EINVAL};  // map entry >= n_ranks
+        if (!n) return;
+        dispatch_rs(rs, [&](auto R) {
+            constexpr int RSC = decltype(R)::value;
+            uint8_t* src = const_cast<uint8_t*>(static_cast<const uint8_t*>(d_src));
+            unsigned long long* tot = ws.h_small;
+            single_segment_counts<RSC, true>(ws, src, n, prefix_byte, ks, ws.map8.p, tot, st);
+            if (h_rank_counts) std::memcpy(h_rank_counts, tot, n_ranks * sizeof(uint64_t));
+            single_segment_scatter<RSC, true, true>(ws, src, nullptr, n, ks, ws.map8.p, tot, st, ws.dig_dst.p);
+        });
+    });
+}
+
+int raduls_gpu_ipc_alloc(uint64_t bytes, void** d_ptr, uint8_t* handle) {
+    if (!d_ptr || !handle) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        void* p = nullptr;
+        RG_CHECK(cudaMalloc(&p, std::max<uint64_t>(bytes, 256)));
+        cudaIpcMemHandle_t h;
+        const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            throw CudaError{RADULS_GPU_ECUDA};
+        }
+        std::memcpy(handle, &h, sizeof h);
+        *d_ptr = p;
+    });
+}
+
+int raduls_gpu_ipc_open(const uint8_t* handle, void** d_ptr) {
+    if (!d_ptr || !handle) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof h);
+        RG_CHECK(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+int raduls_gpu_ipc_close(void* d_ptr) {
+    return guarded([&] { RG_CHECK(cudaIpcCloseMemHandle(d_ptr)); });
+}
+
+int raduls_gpu_free(void* d_ptr) {
+    return guarded([&] { RG_CHECK(cudaFree(d_ptr)); });
+}
+
 int raduls_gpu_andor(const void* d_data, uint64_t n, uint32_t rs, uint64_t* h_andor, void* stream) {
     if (!layout_ok(rs, rs) || mul_overflows(n, rs) || !h_andor) return RADULS_GPU_EINVAL;
     if (n && !aligned_ok(d_data, rs)) return RADULS_GPU_EINVAL;
@@ -1276,7 +1353,7 @@ void raduls_gpu_release(void) {
             w->segs[b].release(); w->seg_tot[b].release(); w->seg_andor[b].release(); w->tile_seg[b].release();
         }
         w->tile_cnt.release(); w->tile_off.release(); w->status.release(); w->groups.release(); w->spill.release(); w->n_spill.release(); w->local_ticket.release();
-        w->copies.release(); w->host_data.release(); w->host_tmp.release(); w->map8.release();
+        w->copies.release(); w->host_data.release(); w->host_tmp.release(); w->map8.release(); w->dig_dst.release();
         delete w->stager;
         if (w->h_ctr) cudaFreeHost(w->h_ctr);
         if (w->h_small) cudaFreeHost(w->h_small);
@@ -1342,7 +1419,30 @@ int raduls_gpu_sort_multi(int n_dev, const int* devices, void* const* d_in, cons
         for (uint32_t r = 0; r < G; ++r) recv[r] += cnt[g][r];
     for (uint32_t r = 0; r < G; ++r)
         if (recv[r] > out_capacity_recs || recv[r] > kMaxRecords) return RADULS_GPU_EINVAL;  // nothing written yet
-    // 4. stable partition of each device's records into destination ranges
+    // 4. peer access between every pair of distinct devices (NVLink P2P)
+    bool p2p = true;
+    rc = guarded([&] {
+        for (uint32_t g = 0; g < G; ++g)
+            for (uint32_t r = 0; r < G; ++r) {
+                if (devices[g] == devices[r]) continue;
+                int ok = 0;
+                RG_CHECK(cudaDeviceCanAccessPeer(&ok, devices[g], devices[r]));
+                if (!ok) {
+                    p2p = false;
+                    continue;
+                }
+                RG_CHECK(cudaSetDevice(devices[g]));
+                const cudaError_t e = cudaDeviceEnablePeerAccess(devices[r], 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) throw CudaError{RADULS_GPU_ECUDA};
+                cudaGetLastError();
+            }
+    });
+    if (rc) return rc;
+    // destination of source g's range for device r: after the ranges of sources < g
+    std::vector<std::vector<uint64_t>> at(G, std::vector<uint64_t>(G, 0));
+    for (uint32_t r = 0; r < G; ++r)
+        for (uint32_t g = 1; g < G; ++g) at[g][r] = at[g - 1][r] + cnt[g - 1][r];
+    // scratch per device (the partition output when P2P is missing; the local sort's tmp)
     std::vector<uint8_t*> part(G, nullptr);
     auto free_parts = [&] {
         for (uint32_t g = 0; g < G; ++g)
@@ -1351,6 +1451,10 @@ int raduls_gpu_sort_multi(int n_dev, const int* devices, void* const* d_in, cons
                 cudaFree(part[g]);
             }
     };
+    // 5. the exchange. With P2P: ONE kernel per source device — the stable
+    // partition stores every destination's records straight into that device's
+    // d_out over NVLink (k_scatter<kPeer>). Without: partition locally, then
+    // peer copies.
     rc = run_per_device(n_dev, [&](int g) {
         return guarded([&] {
             RG_CHECK(cudaSetDevice(devices[g]));
@@ -1363,57 +1467,48 @@ int raduls_gpu_sort_multi(int n_dev, const int* devices, void* const* d_in, cons
                             cudaSuccess
                         ? int(RADULS_GPU_OK)
                         : int(RADULS_GPU_ECUDA);
-            std::vector<uint64_t> got(G, 0);
-            if (!r) r = raduls_gpu_partition(d_in[g], part[g], n_in[g], rs, ks, p0, d_map, G, got.data(), nullptr);
+            std::vector<uint64_t> got(G, 0), dst(G, 0);
+            for (uint32_t q = 0; q < G; ++q)
+                dst[q] = reinterpret_cast<uint64_t>(static_cast<uint8_t*>(d_out[q]) + at[g][q] * rs);
+            if (!r) {
+                if (p2p)
+                    r = raduls_gpu_partition_to(d_in[g], n_in[g], rs, ks, p0, d_map, G, dst.data(), got.data(),
+                                                nullptr);
+                else
+                    r = raduls_gpu_partition(d_in[g], part[g], n_in[g], rs, ks, p0, d_map, G, got.data(), nullptr);
+            }
             cudaFree(d_map);
             if (r) throw CudaError{r};
             for (uint32_t q = 0; q < G; ++q)
                 if (got[q] != cnt[g][q]) throw CudaError{RADULS_GPU_EINTERNAL};
+            RG_CHECK(cudaDeviceSynchronize());  // peer stores complete before the sort reads them
         });
     });
-    if (rc) {
-        free_parts();
-        return rc;
-    }
-    // 5. exchange: device g's range for r lands in d_out[r] after the ranges of
-    // devices < g (peer copies over NVLink on the source device's copy engine)
-    rc = guarded([&] {
-        for (uint32_t g = 0; g < G; ++g)
-            for (uint32_t r = 0; r < G; ++r) {
-                if (devices[g] == devices[r]) continue;
-                int ok = 0;
-                cudaDeviceCanAccessPeer(&ok, devices[g], devices[r]);
-                if (ok) {
-                    RG_CHECK(cudaSetDevice(devices[g]));
-                    const cudaError_t e = cudaDeviceEnablePeerAccess(devices[r], 0);
-                    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) throw CudaError{RADULS_GPU_ECUDA};
-                    cudaGetLastError();
+    if (!rc && !p2p) {
+        rc = guarded([&] {
+            std::vector<cudaStream_t> st(G);
+            for (uint32_t g = 0; g < G; ++g) {
+                RG_CHECK(cudaSetDevice(devices[g]));
+                RG_CHECK(cudaStreamCreateWithFlags(&st[g], cudaStreamNonBlocking));
+            }
+            for (uint32_t g = 0; g < G; ++g) {
+                uint64_t send = 0;
+                RG_CHECK(cudaSetDevice(devices[g]));
+                for (uint32_t r = 0; r < G; ++r) {
+                    const uint64_t k = cnt[g][r];
+                    if (k)
+                        RG_CHECK(cudaMemcpyPeerAsync(static_cast<uint8_t*>(d_out[r]) + at[g][r] * rs, devices[r],
+                                                     part[g] + send * rs, devices[g], k * rs, st[g]));
+                    send += k;
                 }
             }
-        std::vector<cudaStream_t> st(G);
-        for (uint32_t g = 0; g < G; ++g) {
-            RG_CHECK(cudaSetDevice(devices[g]));
-            RG_CHECK(cudaStreamCreateWithFlags(&st[g], cudaStreamNonBlocking));
-        }
-        std::vector<uint64_t> at(G, 0);  // next free record of d_out[r]
-        for (uint32_t g = 0; g < G; ++g) {
-            uint64_t send = 0;
-            RG_CHECK(cudaSetDevice(devices[g]));
-            for (uint32_t r = 0; r < G; ++r) {
-                const uint64_t k = cnt[g][r];
-                if (k)
-                    RG_CHECK(cudaMemcpyPeerAsync(static_cast<uint8_t*>(d_out[r]) + at[r] * rs, devices[r],
-                                                 part[g] + send * rs, devices[g], k * rs, st[g]));
-                send += k;
-                at[r] += k;
+            for (uint32_t g = 0; g < G; ++g) {
+                RG_CHECK(cudaSetDevice(devices[g]));
+                RG_CHECK(cudaStreamSynchronize(st[g]));
+                RG_CHECK(cudaStreamDestroy(st[g]));
             }
-        }
-        for (uint32_t g = 0; g < G; ++g) {
-            RG_CHECK(cudaSetDevice(devices[g]));
-            RG_CHECK(cudaStreamSynchronize(st[g]));
-            RG_CHECK(cudaStreamDestroy(st[g]));
-        }
-    });
+        });
+    }
     if (rc) {
         free_parts();
         return rc;

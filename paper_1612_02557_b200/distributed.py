@@ -15,7 +15,10 @@ the sort shards with ONE exchange step:
  4. stable local partition into per-destination send ranges on the device
     (raduls_gpu_partition: the same tile histogram / look-back scan / scatter
     kernels as an MSD level);
- 5. one all-to-all of the records (NCCL over NVLink on GPUs);
+ 5. the exchange: by default the partition kernel itself stores every
+    destination's records into that rank's receive window over NVLink (CUDA
+    IPC mappings; raduls_gpu_partition_to), so partition and all-to-all are
+    one kernel; or a local partition plus one NCCL all-to-all;
  6. each rank sorts what it received (raduls_gpu_sort).
 
 Rank r ends up holding the r-th contiguous key range, sorted; the concatenation
@@ -72,6 +75,7 @@ class ExchangePlan:
     bucket_rank: np.ndarray      # [65536] u32
     send_counts: np.ndarray      # [world] records this rank sends to each rank
     recv_counts: np.ndarray      # [world] records this rank receives from each rank
+    matrix: np.ndarray = None    # [world, world] records source -> destination
 
 
 # ---------------------------------------------------------------- per-rank compute
@@ -117,6 +121,18 @@ class DeviceOps:
                "raduls_gpu_partition")
         return out, counts
 
+    def partition_to(self, data, n: int, layout: RecordLayout, p0: int, bucket_rank: np.ndarray,
+                     world: int, dst: np.ndarray) -> np.ndarray:
+        """Partition fused with the exchange: rank r's records go to address dst[r]."""
+        dmap = self.torch.from_numpy(bucket_rank.astype(np.int32)).to(self.device)
+        counts = np.zeros(world, dtype=np.uint64)
+        _raise(self.L.raduls_gpu_partition_to(data.data_ptr(), n, layout.record_size, layout.key_size,
+                                              p0, dmap.data_ptr(), world,
+                                              dst.ctypes.data_as(_lib._u64p),
+                                              counts.ctypes.data_as(_lib._u64p), self.stream()),
+               "raduls_gpu_partition_to")
+        return counts
+
     def sort(self, data, n: int, layout: RecordLayout, tmp=None) -> None:
         _raise(self.L.raduls_gpu_sort(data.data_ptr(), tmp.data_ptr() if tmp is not None else None,
                                       n, layout.record_size, layout.key_size, self.stream()),
@@ -130,7 +146,8 @@ def plan_exchange(ops, data, n: int, layout: RecordLayout, group=None) -> Exchan
     import torch.distributed as dist
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    dev = data.device
+    # metadata collectives on the data's device under NCCL, on the host otherwise (gloo)
+    dev = data.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
     # 1. global constant-prefix detection
     ao = torch.from_numpy(ops.andor(data, n, layout).view(np.int64)).to(dev)
     all_ao = [torch.empty_like(ao) for _ in range(world)]
@@ -140,7 +157,7 @@ def plan_exchange(ops, data, n: int, layout: RecordLayout, group=None) -> Exchan
     if p0 >= layout.key_size:
         p0 = 0  # every key equal: any contiguous map is correct
     # 2. 16-bit prefix histograms, all-gathered
-    h = ops.prefix_hist(data, n, layout, p0)
+    h = ops.prefix_hist(data, n, layout, p0).to(dev)
     all_h = [torch.empty_like(h) for _ in range(world)]
     dist.all_gather(all_h, h, group=group)
     hist = np.stack([t.cpu().numpy() for t in all_h]).astype(np.uint64)  # [world, 65536]
@@ -151,24 +168,138 @@ def plan_exchange(ops, data, n: int, layout: RecordLayout, group=None) -> Exchan
     for r in range(world):
         src_dst[r] = np.bincount(bucket_rank, weights=hist[r].astype(np.float64),
                                  minlength=world).astype(np.uint64)
-    return ExchangePlan(p0, bucket_rank, src_dst[rank].copy(), src_dst[:, rank].copy())
+    return ExchangePlan(p0, bucket_rank, src_dst[rank].copy(), src_dst[:, rank].copy(), src_dst)
+
+
+class _CudaBytes:
+    """Zero-copy view of library-owned device memory for torch.as_tensor."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+class PeerWindows:
+    """One receive window per rank in device memory, mapped by every other
+    rank through CUDA IPC (one process per GPU on one node: NVLink P2P).
+    ``ptrs[r]`` is rank r's window as seen from this process."""
+
+    def __init__(self, nbytes: int, group=None):
+        import torch.distributed as dist
+        L = _lib.load()
+        self.nbytes = nbytes
+        self.rank = dist.get_rank(group)
+        own = C.c_void_p()
+        handle = C.create_string_buffer(64)
+        _raise(L.raduls_gpu_ipc_alloc(nbytes, C.byref(own), handle), "raduls_gpu_ipc_alloc")
+        self.own = own.value
+        handles = [None] * dist.get_world_size(group)
+        dist.all_gather_object(handles, handle.raw, group=group)
+        self.ptrs = []
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                self.ptrs.append(self.own)
+                continue
+            p = C.c_void_p()
+            _raise(L.raduls_gpu_ipc_open(h, C.byref(p)), "raduls_gpu_ipc_open")
+            self.ptrs.append(p.value)
+
+    def close(self) -> None:
+        L = _lib.load()
+        for r, p in enumerate(self.ptrs):
+            if r != self.rank:
+                L.raduls_gpu_ipc_close(p)
+        L.raduls_gpu_free(self.own)
+        self.ptrs = []
+
+
+_windows: dict = {}
+
+
+def _peer_windows(nbytes: int, group, device):
+    """Cached windows of at least nbytes; every rank asks for the same size
+    (it comes from the exchanged histograms), so re-creation is collective.
+    Returns None on every rank when any rank could not set its window up
+    (the caller then exchanges through NCCL)."""
+    import torch
+    import torch.distributed as dist
+    key = id(group)
+    w = _windows.get(key)
+    if w is not None and w.nbytes >= nbytes:
+        return w
+    if w is not None:
+        w.close()
+        _windows.pop(key, None)
+    ok = 1
+    try:
+        w = PeerWindows(nbytes, group)
+    except Exception:  # noqa: BLE001 - IPC unavailable: agree on the NCCL path below
+        ok, w = 0, None
+    dev = device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    if int(flag.item()) == 0:
+        if w is not None:
+            w.close()
+        return None
+    _windows[key] = w
+    return w
+
+
+def release_peer_windows() -> None:
+    for w in _windows.values():
+        w.close()
+    _windows.clear()
 
 
 def sort_distributed(data, n: int, layout: RecordLayout, ops=None, group=None,
-                     timings: dict | None = None):
+                     timings: dict | None = None, exchange: str | None = None):
     """Sort `n` local records (uint8 tensor on this rank's device) across the
     process group. Returns (out tensor, n_out): this rank's contiguous key
-    range, sorted."""
+    range, sorted.
+
+    exchange="p2p" (default with DeviceOps on CUDA): the partition kernel
+    stores every destination's records straight into that rank's receive
+    window over NVLink (CUDA IPC; raduls_gpu_partition_to) — the partition and
+    the all-to-all are one kernel. The returned tensor then aliases this
+    rank's cached window and stays valid until the next call on the group.
+    exchange="nccl": local partition, then one NCCL all_to_all_single."""
     import time
 
     import torch
     import torch.distributed as dist
     if ops is None:
         ops = DeviceOps(data.device)
+    if exchange is None:
+        exchange = "p2p" if isinstance(ops, DeviceOps) else "nccl"
     world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
     rs = layout.record_size
     t0 = time.perf_counter()
     plan = plan_exchange(ops, data, n, layout, group)
+    win = None
+    if exchange == "p2p":
+        win = _peer_windows(max(int(plan.matrix.sum(axis=0).max()), 1) * rs, group, data.device)
+    if win is not None:
+        matrix = plan.matrix
+        n_out = int(plan.recv_counts.sum())
+        dst = np.array([win.ptrs[r] + int(matrix[:rank, r].sum()) * rs for r in range(world)],
+                       dtype=np.uint64)
+        torch.cuda.synchronize(data.device)
+        dist.barrier(group=group)  # every window free (previous results consumed)
+        counts = ops.partition_to(data, n, layout, plan.p0, plan.bucket_rank, world, dst)
+        if not np.array_equal(counts, plan.send_counts):
+            raise RuntimeError("partition counts disagree with the exchanged histograms")
+        dist.barrier(group=group)  # every rank's stores into every window are complete
+        t2 = time.perf_counter()
+        recv = torch.as_tensor(_CudaBytes(win.own, max(n_out, 1) * rs), device=data.device)
+        tmp = ops.empty(max(n_out, 1) * rs)
+        ops.sort(recv, n_out, layout, tmp)
+        t3 = time.perf_counter()
+        if timings is not None:
+            timings.update(plan_partition_exchange_s=t2 - t0, local_sort_s=t3 - t2,
+                           sent_bytes=int((plan.send_counts.sum() - plan.send_counts[rank]) * rs))
+        return recv, n_out
     # 4. local stable partition into send ranges
     send, counts = ops.partition(data, n, layout, plan.p0, plan.bucket_rank, world)
     if not np.array_equal(counts, plan.send_counts):

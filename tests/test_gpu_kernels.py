@@ -105,3 +105,37 @@ def test_partition_stable_by_rank(rg, torch_cuda, rs, ks):
     rc = L.raduls_gpu_prefix_histogram(src.data_ptr(), n, rs, ks, pb, hist.data_ptr(), None)
     assert rc == 0
     assert np.array_equal(hist.cpu().numpy(), np.bincount(pref, minlength=65536))
+
+
+@pytest.mark.parametrize("rs,ks", [(16, 8), (8, 8), (24, 16), (32, 24)])
+def test_partition_to_equals_partition(rg, torch_cuda, rs, ks):
+    """raduls_gpu_partition_to (the partition fused with the exchange) writes
+    each rank's stable range to its own destination buffer: identical to the
+    ordinary partition output cut at the rank counts."""
+    import ctypes as C
+    from paper_1612_02557_b200 import _lib
+    from helpers import make_input, to_dev, from_dev
+    L = _lib.load()
+    n, ranks = 100_003, 3
+    a = make_input(n, rs, ks, 31 + rs, universe=(0 if rs != 8 else 5000))
+    d = to_dev(torch_cuda, a)
+    bmap = (np.arange(65536, dtype=np.uint32) * ranks // 65536).astype(np.uint32)
+    dmap = torch_cuda.from_numpy(bmap.view(np.int32)).cuda()
+    ref = torch_cuda.empty_like(d)
+    counts = np.zeros(ranks, dtype=np.uint64)
+    assert L.raduls_gpu_partition(d.data_ptr(), ref.data_ptr(), n, rs, ks, 0, dmap.data_ptr(), ranks,
+                                  counts.ctypes.data_as(_lib._u64p), None) == 0
+    outs = [torch_cuda.empty(int(c) * rs + 64, dtype=torch_cuda.uint8, device="cuda") for c in counts]
+    dst = np.array([o.data_ptr() for o in outs], dtype=np.uint64)
+    got = np.zeros(ranks, dtype=np.uint64)
+    assert L.raduls_gpu_partition_to(d.data_ptr(), n, rs, ks, 0, dmap.data_ptr(), ranks,
+                                     dst.ctypes.data_as(_lib._u64p), got.ctypes.data_as(_lib._u64p),
+                                     None) == 0
+    torch_cuda.cuda.synchronize()
+    assert list(got) == list(counts)
+    r = from_dev(ref)
+    off = 0
+    for o, c in zip(outs, counts):
+        c = int(c)
+        assert np.array_equal(from_dev(o)[:c * rs], r[off * rs:(off + c) * rs])
+        off += c
