@@ -252,6 +252,14 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
         : "memory");
 }
 
+// Asynchronous global -> shared copy of 8 bytes (LDGSTS, no register round
+// trip); cp_async_wait_all() completes this thread's outstanding copies.
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
     const uint32_t a = smem_u32(bar);
     uint32_t ok = 0;

@@ -177,11 +177,13 @@ __device__ __forceinline__ void lsd_pass_w(uint32_t n, const uint16_t* pin, uint
 }
 
 // One group, by the whole CTA (called per group by the persistent k_local).
-template <int RS, bool kFallback>
+// `mid` is called by every thread once the bucket geometry is known (the
+// persistent launch uses it to prefetch the next group off the critical path).
+template <int RS, bool kFallback, typename Mid>
 __device__ __forceinline__ void local_group(
     uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group g,
     uint32_t ks, LevelCounters* __restrict__ ctr, Group* __restrict__ spill,
-    unsigned int* __restrict__ n_spill, uint32_t spill_cap) {
+    unsigned int* __restrict__ n_spill, uint32_t spill_cap, Mid&& mid) {
     using C = LocalCfg<RS>;
     constexpr bool REG = C::kRegRecords;
     constexpr int T = C::kThreads, W = C::kWarps, IPT = C::kIpt;
@@ -393,6 +395,7 @@ __device__ __forceinline__ void local_group(
         return 0;
     };
 
+    mid();
     // ---- 4. bucket histogram (packed u16 pairs, zeroed at the start), scan, largest bucket
     uint32_t bk[KEEP ? IPT : 1];
 #pragma unroll
@@ -664,40 +667,53 @@ __device__ __forceinline__ void prefetch_group_l2(const uint8_t* data, const uin
     }
 }
 
-// Local sort launch. One CTA per SM (8- and 32-B records): persistent, CTAs
-// claim groups through a ticket one group ahead and prefetch the next group
-// into L2 while sorting the current one (its HBM latency otherwise stalls the
-// SM at every group start). Two CTAs per SM: one group per CTA.
+// Local sort launch. One CTA per SM (8- and 32-B records): persistent, one
+// resident CTA per SM, groups assigned round-robin (no atomics). The next group's descriptor is
+// copied into shared memory with cp.async while the current group is sorted,
+// and once its bucket geometry is known thread 0 prefetches the next group's
+// records into L2 (cp.async.bulk.prefetch.L2), so a group's start no longer
+// waits on a dependent descriptor load and a cold HBM read.
 template <int RS, bool kFallback>
 __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBlocks) k_local(
     uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group* __restrict__ groups,
-    uint32_t n_groups, unsigned int* __restrict__ ticket, uint32_t ks,
-    LevelCounters* __restrict__ ctr, Group* __restrict__ spill, unsigned int* __restrict__ n_spill,
-    uint32_t spill_cap) {
+    uint32_t n_groups, uint32_t ks, LevelCounters* __restrict__ ctr, Group* __restrict__ spill,
+    unsigned int* __restrict__ n_spill, uint32_t spill_cap) {
     if constexpr (LocalCfg<RS>::kMinBlocks > 1) {
-        // two CTAs per SM already overlap one group's load with the other's
-        // sort; the hardware block scheduler refills freed slots (measured:
-        // faster than a persistent loop here)
-        // the group one resident wave later starts from L2
+        // two CTAs per SM already overlap one group's start with the other's
+        // sort: one group per CTA (measured 4% faster than this loop), the
+        // group one resident wave later prefetched into L2
         constexpr uint32_t kAhead = 2 * 148;
         if (threadIdx.x == 0 && blockIdx.x + kAhead < n_groups)
             prefetch_group_l2<RS>(data, tmp, groups[blockIdx.x + kAhead]);
-        local_group<RS, kFallback>(data, tmp, groups[blockIdx.x], ks, ctr, spill, n_spill, spill_cap);
+        local_group<RS, kFallback>(data, tmp, groups[blockIdx.x], ks, ctr, spill, n_spill, spill_cap,
+                                   [] {});
         return;
     }
-    __shared__ uint32_t s_next[2];
-    if (threadIdx.x == 0) s_next[1] = atomicAdd(ticket, 1u);
+    __shared__ __align__(16) Group s_g[2];
+    uint32_t i = blockIdx.x;
+    if (i >= n_groups) return;
+    if (threadIdx.x == 0) s_g[0] = groups[i];
     __syncthreads();
-    uint32_t cur = s_next[1];
-    for (uint32_t it = 0; cur < n_groups; ++it) {
-        if (threadIdx.x == 0) {
-            const uint32_t nxt = atomicAdd(ticket, 1u);
-            s_next[it & 1] = nxt;
-            if (nxt < n_groups) prefetch_group_l2<RS>(data, tmp, groups[nxt]);
+    for (int buf = 0; i < n_groups; buf ^= 1) {
+        const uint32_t nx = i + gridDim.x;
+        const bool more = nx < n_groups;
+        if (threadIdx.x == 0 && more) {
+            static_assert(sizeof(Group) % 8 == 0, "Group copied in 8-B pieces");
+            for (int q = 0; q < int(sizeof(Group) / 8); ++q)
+                cp_async8(reinterpret_cast<uint8_t*>(&s_g[buf ^ 1]) + 8 * q,
+                          reinterpret_cast<const uint8_t*>(&groups[nx]) + 8 * q);
         }
-        local_group<RS, kFallback>(data, tmp, groups[cur], ks, ctr, spill, n_spill, spill_cap);
-        __syncthreads();  // shared memory free for the next group; s_next visible
-        cur = s_next[it & 1];
+        const Group g = s_g[buf];
+        auto mid = [&] {
+            if (threadIdx.x == 0 && more) {
+                cp_async_wait_all();
+                prefetch_group_l2<RS>(data, tmp, s_g[buf ^ 1]);
+            }
+        };
+        local_group<RS, kFallback>(data, tmp, g, ks, ctr, spill, n_spill, spill_cap, mid);
+        if (threadIdx.x == 0 && more) cp_async_wait_all();
+        __syncthreads();  // shared memory free for the next group; its descriptor visible
+        i = nx;
     }
 }
 

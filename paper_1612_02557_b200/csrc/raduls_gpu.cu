@@ -286,7 +286,7 @@ struct Workspace {
     DevBuf<uint32_t> tile_off;
     DevBuf<unsigned long long> status;
     DevBuf<Group> groups, spill;
-    DevBuf<unsigned int> n_spill, local_ticket;
+    DevBuf<unsigned int> n_spill;
     DevBuf<CopyRange> copies;
     DevBuf<uint8_t> host_data, host_tmp, map8;
     DevBuf<unsigned long long> dig_dst;  // per-destination byte addresses (raduls_gpu_partition_to)
@@ -307,7 +307,6 @@ struct Workspace {
         andor0.ensure(8);
         acc.ensure(4);
         ctr.ensure(kMaxLevels);
-        local_ticket.ensure(1);
         thr.ensure(256);
     }
 };
@@ -455,14 +454,11 @@ void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, 
                   LevelCounters* ctr, cudaStream_t st) {
     if (!ngroups) return;
     const int pe = ws.prof.begin(K_LOCAL, st);
-    RG_CHECK(cudaMemsetAsync(ws.local_ticket.p, 0, sizeof(unsigned int), st));
-    // one CTA per SM (8/32-B records): persistent, prefetching one group
-    // ahead; two per SM: one CTA per group
+    // one CTA per SM: persistent, groups round-robin; two per SM: a CTA per group
     const uint32_t grid = LocalCfg<RS>::kMinBlocks == 1 ? std::min<uint32_t>(ngroups, uint32_t(sm_count()))
                                                        : ngroups;
     k_local<RS, false><<<grid, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
-        data, tmp, ws.groups.p, ngroups, ws.local_ticket.p, ks, ctr, ws.spill.p, ws.n_spill.p,
-        uint32_t(ws.spill.cap));
+        data, tmp, ws.groups.p, ngroups, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
 }
@@ -478,10 +474,9 @@ void finish_spilled(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ks, Lev
     if (!n) return;
     if (n > ws.spill.cap) throw CudaError{RADULS_GPU_EINTERNAL};
     const int pe = ws.prof.begin(K_LOCAL, st);
-    RG_CHECK(cudaMemsetAsync(ws.local_ticket.p, 0, sizeof(unsigned int), st));
     const uint32_t grid = LocalCfg<RS>::kMinBlocks == 1 ? std::min<uint32_t>(n, uint32_t(sm_count())) : n;
     k_local<RS, true><<<grid, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
-        data, tmp, ws.spill.p, n, ws.local_ticket.p, ks, ctr, nullptr, nullptr, 0);
+        data, tmp, ws.spill.p, n, ks, ctr, nullptr, nullptr, 0);
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
     RG_CHECK(cudaStreamSynchronize(st));
@@ -1352,7 +1347,7 @@ void raduls_gpu_release(void) {
         for (int b = 0; b < 2; ++b) {
             w->segs[b].release(); w->seg_tot[b].release(); w->seg_andor[b].release(); w->tile_seg[b].release();
         }
-        w->tile_cnt.release(); w->tile_off.release(); w->status.release(); w->groups.release(); w->spill.release(); w->n_spill.release(); w->local_ticket.release();
+        w->tile_cnt.release(); w->tile_off.release(); w->status.release(); w->groups.release(); w->spill.release(); w->n_spill.release();
         w->copies.release(); w->host_data.release(); w->host_tmp.release(); w->map8.release(); w->dig_dst.release();
         delete w->stager;
         if (w->h_ctr) cudaFreeHost(w->h_ctr);
