@@ -339,7 +339,7 @@ struct LevelCounters {
     uint32_t n_scatter_segs;   // segments scattered this level
     uint32_t scan_ticket;      // dynamic chunk id dispenser for k_tile_scan
     uint32_t scatter_ticket;   // in-order tile dispenser for k_scatter
-    uint32_t pad0;
+    uint32_t hist_ticket;      // in-order tile dispenser for k_tile_hist
     unsigned long long moved_scatter;    // records moved by this level's scatter
     unsigned long long moved_local;      // records moved by local sorts
     unsigned long long moved_copy;       // records moved by copy-back

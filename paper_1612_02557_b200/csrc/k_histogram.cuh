@@ -18,6 +18,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "k_scatter.cuh"
 
 namespace rg {
 
@@ -100,17 +101,175 @@ __global__ void __launch_bounds__(256) k_andor(const uint8_t* __restrict__ data,
 }
 
 // Per-tile digit counts of byte segs[s].p for every tile of every segment of
-// the level, plus AND/OR of every record word per segment. One CTA per tile
-// (the scatter's tile partition: kTile records, tile -> segment through
-// tile_seg, tile index inside the segment = tile - segs[s].tile_base).
-// tile_cnt: [ntiles][256] u16. seg_andor: [nseg][8] u64 (and at 2w, or at
-// 2w+1), pre-initialised.
+// the level, plus AND/OR of every record word per segment, over the scatter's
+// tile partition (kTile records, tile -> segment through tile_seg, tile index
+// inside the segment = tile - segs[s].tile_base). tile_cnt: [ntiles][256]
+// u16. seg_andor: [nseg][8] u64 (and at 2w, or at 2w+1), pre-initialised.
 // kMap: the digit is the destination rank of the record's 16-bit key prefix
 // at bytes (p, p+1) through a 65536-entry map (multi-GPU partition).
-// Threads of a histogram CTA: ~8 records in flight per thread whatever the
-// scatter tile size (a multiple of 32, <= 1024, >= 256 for the digit counts).
-template <int RS, int kTile>
+//
+// Persistent and warp-specialised like k_scatter: a producer warp claims
+// tiles in order through a ticket and TMA-loads them (cp.async.bulk +
+// mbarrier) into a 2-stage shared-memory ring, so every SM always has tile
+// loads in flight; 8 consumer warps histogram a tile from shared memory
+// (warp-aggregated atomics into per-stage counts) while the next one lands.
+template <int RS>
 struct HistCfg {
+    static constexpr int kThreads = 256;  // consumers
+    static constexpr int kWarps = kThreads / 32;
+    static constexpr int kTile = ScatterCfg<RS>::kTile;
+    static constexpr int kItems = kTile / kThreads;
+    static constexpr int kStages = 2;
+    static constexpr int kBufBytes = ScatterCfg<RS>::kBufBytes;
+    static constexpr size_t kSmem = size_t(kStages) * kBufBytes;
+    static_assert(kTile % kThreads == 0, "tile of whole consumer rounds");
+};
+
+struct HistTile {
+    uint32_t tile;  // >= n_tiles: none
+    uint32_t seg, tn, p, head;
+};
+
+template <int RS, bool kMap = false>
+__global__ void __launch_bounds__(HistCfg<RS>::kThreads + 32, 2) k_tile_hist(
+    const uint8_t* __restrict__ data, const uint8_t* __restrict__ tmp, const Seg* __restrict__ segs,
+    const uint32_t* __restrict__ tile_seg, uint16_t* __restrict__ tile_cnt,
+    unsigned long long* __restrict__ seg_andor, LevelCounters* __restrict__ ctr, uint32_t n_tiles,
+    uint32_t ks = 0, const uint8_t* __restrict__ map = nullptr) {
+    using C = HistCfg<RS>;
+    constexpr int T = C::kThreads, W = C::kWarps, IT = C::kItems, S = C::kStages, KW = RS / 8;
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint32_t s_h[S][kRadix];
+    __shared__ unsigned long long s_and[S][W][KW], s_or[S][W][KW];
+    __shared__ __align__(8) unsigned long long s_full[S], s_empty[S];
+    __shared__ HistTile s_info[S];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x < kRadix)
+        for (int q = 0; q < S; ++q) s_h[q][threadIdx.x] = 0;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < S; ++q) {
+            mbar_init(&s_full[q], 1);
+            mbar_init(&s_empty[q], 1);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == W) {  // ------------------------------------------------ producer
+        if (lane != 0) return;
+        for (uint32_t it = 0;; ++it) {
+            const uint32_t tile = atomicAdd(&ctr->hist_ticket, 1u);
+            const int b = it % S;
+            if (it >= uint32_t(S)) mbar_wait(&s_empty[b], ((it / S) - 1) & 1u);
+            HistTile ti;
+            ti.tile = tile;
+            if (tile >= n_tiles) {
+                s_info[b] = ti;
+                mbar_arrive_expect_tx(&s_full[b], 0);
+                return;
+            }
+            const uint32_t s = tile_seg[tile];
+            const Seg g = segs[s];
+            const uint64_t k = uint64_t(tile) - g.tile_base;
+            const uint8_t* gsrc = (g.parity ? tmp : data) + (g.start + k * C::kTile) * RS;
+            ti.seg = s;
+            ti.tn = uint32_t(min(uint64_t(C::kTile), g.size - k * C::kTile));
+            ti.p = g.p;
+            const uint32_t bytes = ti.tn * RS;
+            const uint32_t head = uint32_t(reinterpret_cast<uintptr_t>(gsrc) & 15u);  // 0 or 8
+            const uint32_t hb = head ? min(8u, bytes) : 0u;
+            const uint32_t body = (bytes - hb) & ~15u;
+            const uint32_t tail = bytes - hb - body;
+            ti.head = head;
+            uint8_t* sb = smem + b * C::kBufBytes + head;
+            if (hb) *reinterpret_cast<uint2*>(sb) = *reinterpret_cast<const uint2*>(gsrc);
+            if (tail)
+                *reinterpret_cast<uint2*>(sb + hb + body) = *reinterpret_cast<const uint2*>(gsrc + hb + body);
+            fence_proxy_async_smem();
+            s_info[b] = ti;
+            mbar_arrive_expect_tx(&s_full[b], body);
+            if (body) tma_load_1d(sb + hb, gsrc + hb, body, &s_full[b]);
+        }
+    }
+
+    // ------------------------------------------------------------ consumers
+    unsigned long long recs = 0;
+    for (uint32_t it = 0;; ++it) {
+        const int b = it % S;
+        mbar_wait(&s_full[b], (it / S) & 1u);
+        const HistTile ti = s_info[b];
+        if (ti.tile >= n_tiles) break;
+        const uint8_t* tile = smem + b * C::kBufBytes + ti.head;
+        const uint32_t tn = ti.tn, p = ti.p;
+        uint32_t* hb = s_h[b];
+        uint64_t a[KW], o[KW];
+#pragma unroll
+        for (int w = 0; w < KW; ++w) a[w] = ~0ull, o[w] = 0ull;
+#pragma unroll
+        for (int j = 0; j < IT; ++j) {
+            const uint32_t i = uint32_t(warp * IT + j) * 32u + lane;  // warp-striped
+            const bool valid = i < tn;
+            Rec<RS> r;
+            if (valid) r = ld_smem_rec<RS>(tile, i);
+            else
+#pragma unroll
+                for (int q = 0; q < Rec<RS>::kWords; ++q) r.w[q] = 0;
+            if constexpr (kMap) {
+                if (valid) {
+                    const uint32_t hi = p < ks ? rec_byte<RS>(r, p) : 0u;
+                    const uint32_t lo = p + 1 < ks ? rec_byte<RS>(r, p + 1) : 0u;
+                    atomicAdd(&hb[__ldg(map + ((hi << 8) | lo))], 1u);
+                }
+                continue;
+            }
+            const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
+            const uint32_t word = rec_word32<RS>(r, p >> 2);
+            const uint32_t wa = __reduce_and_sync(0xFFFFFFFFu, valid ? word : ~0u);
+            const uint32_t wo = __reduce_or_sync(0xFFFFFFFFu, valid ? word : 0u);
+            const uint32_t shf = (p & 3u) * 8u;
+            warp_hist_add(hb, (word >> shf) & 0xFFu, valid, wa, wo, shf, nvalid);
+            if (valid) {
+#pragma unroll
+                for (int w = 0; w < KW; ++w) {
+                    const uint64_t v = rec_word64<RS>(r, w);
+                    a[w] &= v;
+                    o[w] |= v;
+                }
+            }
+        }
+        if constexpr (!kMap) {
+#pragma unroll
+            for (int w = 0; w < KW; ++w) {
+                for (int off = 16; off; off >>= 1) {
+                    a[w] &= __shfl_xor_sync(0xFFFFFFFFu, a[w], off);
+                    o[w] |= __shfl_xor_sync(0xFFFFFFFFu, o[w], off);
+                }
+                if (lane == 0) s_and[b][warp][w] = a[w], s_or[b][warp][w] = o[w];
+            }
+        }
+        bar_sync_named(1, T);  // the tile is read: the buffer goes back to the producer
+        if (threadIdx.x == 0) mbar_arrive(&s_empty[b]);
+        if (!kMap && threadIdx.x < KW) {
+            unsigned long long ra = ~0ull, ro = 0ull;
+            for (int q = 0; q < W; ++q) ra &= s_and[b][q][threadIdx.x], ro |= s_or[b][q][threadIdx.x];
+            atomicAnd(&seg_andor[uint64_t(ti.seg) * 8 + 2 * threadIdx.x], ra);
+            atomicOr(&seg_andor[uint64_t(ti.seg) * 8 + 2 * threadIdx.x + 1], ro);
+        }
+        // each thread drains (and clears) its own digit; stage b is reused two
+        // tiles on, after another consumer barrier
+        tile_cnt[uint64_t(ti.tile) * kRadix + threadIdx.x] = uint16_t(hb[threadIdx.x]);
+        hb[threadIdx.x] = 0;
+        recs += tn;
+    }
+    if (threadIdx.x == 0 && recs) atomicAdd(&ctr->hist_records, recs);
+}
+
+// 8-B records: one CTA per tile, all loads in flight in registers (measured
+// 5.2 TB/s at C2 against 4.4 for the TMA-fed kernel, whose 8 consumer warps
+// cannot keep up with 16 records each). Threads of a CTA: ~8 records in
+// flight per thread (16 at 8 B), a multiple of 32, >= 256 for the digit counts.
+template <int RS, int kTile>
+struct HistRegCfg {
     static constexpr int kIt = RS == 8 ? 16 : 8;
     static constexpr int kThreads = ((kTile + kIt - 1) / kIt + 31) / 32 * 32 < 256
                                         ? 256
@@ -120,7 +279,7 @@ struct HistCfg {
 constexpr uint32_t kHistAhead = 592;  // ~ resident histogram CTAs (4 per SM x 148)
 
 template <int RS, int kTile, bool kMap = false>
-__global__ void __launch_bounds__(HistCfg<RS, kTile>::kThreads) k_tile_hist(const uint8_t* __restrict__ data,
+__global__ void __launch_bounds__(HistRegCfg<RS, kTile>::kThreads) k_tile_hist_reg(const uint8_t* __restrict__ data,
                                                    const uint8_t* __restrict__ tmp,
                                                    const Seg* __restrict__ segs,
                                                    const uint32_t* __restrict__ tile_seg,
@@ -129,7 +288,7 @@ __global__ void __launch_bounds__(HistCfg<RS, kTile>::kThreads) k_tile_hist(cons
                                                    LevelCounters* __restrict__ ctr, uint32_t ks = 0,
                                                    const uint8_t* __restrict__ map = nullptr) {
     constexpr int KW = RS / 8;
-    constexpr int HT = HistCfg<RS, kTile>::kThreads, HW = HT / 32;
+    constexpr int HT = HistRegCfg<RS, kTile>::kThreads, HW = HT / 32;
     constexpr int IT = (kTile + HT - 1) / HT;
     __shared__ uint32_t sh[kRadix];
     __shared__ unsigned long long s_and[HW][KW], s_or[HW][KW];

@@ -399,6 +399,10 @@ void set_attrs(Workspace& ws) {
                                   int(LocalCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_local<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(LocalCfg<RS>::kSmem)));
+    RG_CHECK(cudaFuncSetAttribute(k_tile_hist<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(HistCfg<RS>::kSmem)));
+    RG_CHECK(cudaFuncSetAttribute(k_tile_hist<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(HistCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(ScatterCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -422,8 +426,15 @@ void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t 
                   cudaStream_t st, uint32_t ks = 0, const uint8_t* map = nullptr) {
     constexpr int TILE = ScatterCfg<RS>::kTile;
     int pe = ws.prof.begin(K_HIST, st);
-    k_tile_hist<RS, TILE, kMap><<<ntiles, HistCfg<RS, TILE>::kThreads, 0, st>>>(data, tmp, ws.segs[cur].p, ws.tile_seg[cur].p,
-                                                        ws.tile_cnt.p, ws.seg_andor[cur].p, c, ks, map);
+    if constexpr (RS == 8) {  // one CTA per tile (see k_tile_hist_reg)
+        k_tile_hist_reg<RS, TILE, kMap><<<ntiles, HistRegCfg<RS, TILE>::kThreads, 0, st>>>(
+            data, tmp, ws.segs[cur].p, ws.tile_seg[cur].p, ws.tile_cnt.p, ws.seg_andor[cur].p, c, ks, map);
+    } else {  // persistent, TMA-fed
+        const uint32_t hgrid = std::min<uint32_t>(ntiles, uint32_t(sm_count()) * 2);
+        k_tile_hist<RS, kMap><<<hgrid, HistCfg<RS>::kThreads + 32, HistCfg<RS>::kSmem, st>>>(
+            data, tmp, ws.segs[cur].p, ws.tile_seg[cur].p, ws.tile_cnt.p, ws.seg_andor[cur].p, c, ntiles, ks,
+            map);
+    }
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
     const uint32_t nchunks = (ntiles + kScanChunk - 1) / kScanChunk;
