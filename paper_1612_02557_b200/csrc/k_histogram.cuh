@@ -108,9 +108,9 @@ __global__ void __launch_bounds__(256) k_andor(const uint8_t* __restrict__ data,
 // kMap: the digit is the destination rank of the record's 16-bit key prefix
 // at bytes (p, p+1) through a 65536-entry map (multi-GPU partition).
 //
-// Persistent and warp-specialised like k_scatter: a producer warp claims
-// tiles in order through a ticket and TMA-loads them (cp.async.bulk +
-// mbarrier) into a 2-stage shared-memory ring, so every SM always has tile
+// Persistent and warp-specialised like k_scatter: a producer warp takes tiles
+// round-robin and TMA-loads them (cp.async.bulk + mbarrier) into a 2-stage
+// shared-memory ring, so every SM always has tile
 // loads in flight; 8 consumer warps histogram a tile from shared memory
 // (warp-aggregated atomics into per-stage counts) while the next one lands.
 template <int RS>
@@ -157,9 +157,15 @@ __global__ void __launch_bounds__(HistCfg<RS>::kThreads + 32, 2) k_tile_hist(
 
     if (warp == W) {  // ------------------------------------------------ producer
         if (lane != 0) return;
+        // tiles round-robin (a histogram has no write locality to keep), the
+        // next tile's metadata loaded while this one's buffer frees up
+        uint32_t tile = blockIdx.x;
+        uint32_t s = tile < n_tiles ? tile_seg[tile] : 0u;
+        Seg g = tile < n_tiles ? segs[s] : Seg{};
         for (uint32_t it = 0;; ++it) {
-            const uint32_t tile = atomicAdd(&ctr->hist_ticket, 1u);
             const int b = it % S;
+            const uint32_t tnext = tile + gridDim.x;
+            const uint32_t snext = tnext < n_tiles ? tile_seg[tnext] : 0u;
             if (it >= uint32_t(S)) mbar_wait(&s_empty[b], ((it / S) - 1) & 1u);
             HistTile ti;
             ti.tile = tile;
@@ -168,8 +174,6 @@ __global__ void __launch_bounds__(HistCfg<RS>::kThreads + 32, 2) k_tile_hist(
                 mbar_arrive_expect_tx(&s_full[b], 0);
                 return;
             }
-            const uint32_t s = tile_seg[tile];
-            const Seg g = segs[s];
             const uint64_t k = uint64_t(tile) - g.tile_base;
             const uint8_t* gsrc = (g.parity ? tmp : data) + (g.start + k * C::kTile) * RS;
             ti.seg = s;
@@ -189,6 +193,10 @@ __global__ void __launch_bounds__(HistCfg<RS>::kThreads + 32, 2) k_tile_hist(
             s_info[b] = ti;
             mbar_arrive_expect_tx(&s_full[b], body);
             if (body) tma_load_1d(sb + hb, gsrc + hb, body, &s_full[b]);
+            const Seg gnext = tnext < n_tiles ? segs[snext] : g;
+            tile = tnext;
+            s = snext;
+            g = gnext;
         }
     }
 
