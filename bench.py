@@ -24,6 +24,7 @@ box's host cores.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -66,7 +67,7 @@ def load_peaks() -> tuple[float, str]:
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -92,7 +93,10 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
-    def stop(self) -> dict | None:
+    def stop(self, window: tuple[float, float] | None = None) -> dict | None:
+        """Summarise the samples taken inside `window` (time.time() bounds of
+        the timed region; the sampler is started earlier so nvidia-smi's
+        start-up does not eat the region). All samples if none fall inside."""
         if not self.proc:
             return None
         self.proc.terminate()
@@ -102,24 +106,25 @@ class ClockSampler:
             self.proc.kill()
         if self.t:
             self.t.join(timeout=2)
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
+            if len(parts) < 9:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(parts[1]), float(parts[2]), parts[5:9]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
+        inside = [r for r in rows if window and window[0] <= r[0] <= window[1]]
+        sel = inside or rows
+        if not sel:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = {nm for r in sel for nm, v in zip(names, r[3]) if v.lower() == "active"}
+        return {"sm_mhz": statistics.median(r[1] for r in sel), "sm_max_mhz": max(r[2] for r in sel),
+                "reasons": sorted(reasons), "samples": len(sel),
+                "in_timed_region": bool(inside)}
 
 
 # ------------------------------------------------------------------ CPU baseline / reference arm
@@ -267,6 +272,8 @@ def main():
         barrier()
         return e0.elapsed_time(e1), out, n_out
 
+    clocks = ClockSampler(local_rank)
+    clocks.start()  # before the warm-up: nvidia-smi's start-up stays outside the timed region
     for _ in range(args.warmup):
         _, out, n_out = one_step(False)
         del out
@@ -274,12 +281,11 @@ def main():
     if world == 1:
         rg.generate(n_local, lay, dist=dist_kind, seed=seed, index_base=base, out=data)
         digest_in = rg.digest(data, n_local, rs)
-    clocks = ClockSampler(local_rank)
     rg.set_profiling(True)
     kt_sum: dict[str, list] = {}
     stats_sum: dict[str, int] = {}
     step_ms = []
-    clocks.start()
+    t_region0 = time.time()
     wall0 = time.perf_counter()
     for _ in range(args.steps):
         ms, out, n_out = one_step(True)
@@ -292,7 +298,7 @@ def main():
             for k, v in rg.last_stats().items():
                 stats_sum[k] = stats_sum.get(k, 0) + v
     wall = time.perf_counter() - wall0
-    clk = clocks.stop()
+    clk = clocks.stop((t_region0, time.time()))
     rg.set_profiling(False)
     # verify the last step (untimed)
     viol, _ = rg.check_sorted(out, n_out, lay)
