@@ -53,6 +53,9 @@ struct CudaError {
     int code;
 };
 
+// A failed call is also recorded as the runtime's last error; clear it so a
+// recoverable failure (an allocation) does not resurface at the next launch
+// check of a later call. Sticky errors persist regardless.
 #define RG_CHECK(expr)                                                                  \
     do {                                                                                \
         cudaError_t e_ = (expr);                                                        \
@@ -60,6 +63,7 @@ struct CudaError {
             if (std::getenv("RADULS_GPU_DEBUG"))                                        \
                 std::fprintf(stderr, "raduls_gpu: %s failed: %s (%s:%d)\n", #expr,      \
                              cudaGetErrorString(e_), __FILE__, __LINE__);               \
+            cudaGetLastError();                                                         \
             throw CudaError{e_ == cudaErrorMemoryAllocation ? RADULS_GPU_ENOMEM          \
                                                             : RADULS_GPU_ECUDA};         \
         }                                                                               \
@@ -644,6 +648,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
 
 template <typename F>
 int guarded(F&& f) {
+    cudaGetLastError();  // a stale non-sticky error (e.g. a caller's failed allocation) is not ours
     try {
         f();
         return RADULS_GPU_OK;

@@ -315,3 +315,30 @@ def test_scatter_tile_boundaries(rg, torch_cuda, rs, ks):
         want = a.reshape(n, rs)[np.argsort(a.reshape(n, rs)[:, 0], kind="stable")].reshape(-1)
         assert np.array_equal(from_dev(out), want)
         assert list(counts) == list(np.bincount(a.reshape(n, rs)[:, 0], minlength=256))
+
+
+def test_scratch_allocation_failure_leaves_input_untouched(rg, torch_cuda):
+    """The reference's resource_error contract (P/include/raduls/record_array.hpp:
+    21-28, scheduler.hpp:56-59): when the scratch array cannot be allocated the
+    call fails with ResourceError and the records are untouched. Here the
+    records take more than half of the free device memory, so the library's
+    own d_tmp allocation (cudaMallocAsync, d_tmp = NULL) cannot succeed."""
+    free, _ = torch_cuda.cuda.mem_get_info()
+    rs, ks = 32, 8  # 32-B records: 60% of the device within the 2^32-record limit
+    n = min(int(free * 0.6) // rs, 1 << 32)
+    if n * rs * 2 <= free:  # pragma: no cover - a device this roomy cannot exercise it
+        pytest.skip("not enough memory pressure")
+    lay = rg.RecordLayout(rs, ks)
+    d = rg.generate(n, lay, seed=7)
+    before = rg.digest(d, n, rs)
+    probe = d[:1 << 20].clone()
+    with pytest.raises(rg.ResourceError):
+        rg.sort(d, n, lay)
+    torch_cuda.cuda.synchronize()
+    assert rg.digest(d, n, rs) == before
+    assert torch_cuda.equal(d[:1 << 20], probe)
+    del d, probe
+    torch_cuda.cuda.empty_cache()
+    # the library still works afterwards
+    a = make_input(100000, rs, ks, 3)
+    assert_parity(gpu_sort(rg, torch_cuda, a, rs, ks), a, rs, ks)
