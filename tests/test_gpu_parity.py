@@ -342,3 +342,48 @@ def test_scratch_allocation_failure_leaves_input_untouched(rg, torch_cuda):
     # the library still works afterwards
     a = make_input(100000, rs, ks, 3)
     assert_parity(gpu_sort(rg, torch_cuda, a, rs, ks), a, rs, ks)
+
+
+def test_concurrent_callers_on_one_device(rg, torch_cuda):
+    """Concurrent calls on disjoint arrays are safe (no global
+    state in the reference, scheduler.hpp:56-61). ctypes drops the GIL, so the
+    threads enter the library together and serialise on the device workspace."""
+    import threading
+    cases = [(16, 8, 150_000, 1), (32, 24, 60_000, 2), (8, 8, 200_000, 3), (24, 16, 90_000, 4),
+             (16, 16, 5_000, 5), (16, 8, 400_000, 6)]
+    inputs = [make_input(n, rs, ks, seed, universe=(0, 500)[seed % 2]) for rs, ks, n, seed in cases]
+    devs = [to_dev(torch_cuda, a) for a in inputs]
+    errors = []
+
+    def work(i):
+        try:
+            rs, ks, n, _ = cases[i]
+            for _ in range(3):  # repeated sorts of a sorted array stay put
+                rg.sort(devs[i], n, rg.RecordLayout(rs, ks))
+            torch_cuda.cuda.synchronize()
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(cases))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    for (rs, ks, n, _), a, d in zip(cases, inputs, devs):
+        assert_parity(from_dev(d), a, rs, ks)
+
+
+def test_sort_on_a_caller_stream(rg, torch_cuda):
+    """raduls_gpu_sort on the caller's stream is ordered after the caller's
+    earlier work on that stream (the input is produced there)."""
+    rs, ks, n = 16, 8, 300_000
+    a = make_input(n, rs, ks, 9)
+    s = torch_cuda.cuda.Stream()
+    host = torch_cuda.from_numpy(a).pin_memory()
+    with torch_cuda.cuda.stream(s):
+        d = torch_cuda.empty(n * rs, dtype=torch_cuda.uint8, device="cuda")
+        d.copy_(host, non_blocking=True)  # produced on s
+        rg.sort(d, n, rg.RecordLayout(rs, ks), stream=s)
+    s.synchronize()
+    assert_parity(from_dev(d), a, rs, ks)
