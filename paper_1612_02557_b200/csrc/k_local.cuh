@@ -255,21 +255,42 @@ __device__ __forceinline__ void local_group(
         else return ld_smem_rec<RS>(recs, e);
     };
 
-    // ---- 2. AND/OR of the record words (REDUX) -> varying key bytes L
+    // ---- 2. AND/OR of the record words (REDUX) -> varying key bytes L.
+    // Shared-memory records: the same pass computes the window of the default
+    // varying bytes p..p+3 (what random keys have), kept if L confirms it, so
+    // the records are read once instead of twice.
+    constexpr bool KEEP = !REG;
+    uint32_t wv[KEEP ? IPT : 1];
+    uint32_t smn = 0xFFFFFFFFu, smx = 0u;
+    uint32_t Ldef[4] = {g.p, g.p + 1, g.p + 2, g.p + 3};
+    const WindowSel wsd = make_window_sel(Ldef, 4, RS / 4, false);
+    // (16/24-B records; measured a loss at 32 B, whose kernel is register-bound)
+    const bool spec = KEEP && RS <= 24 && g.p + 4 <= ks && g.p + 4 <= uint32_t(RS) && wsd.fast;
     {
         uint32_t a[2 * KW], o[2 * KW];
 #pragma unroll
         for (int w = 0; w < 2 * KW; ++w) a[w] = ~0u, o[w] = 0u;
+        auto andor = [&](auto specc) {
 #pragma unroll
-        for (int j = 0; j < IPT; ++j) {
-            if (uint32_t(j) * T >= n) break;  // block-uniform
-            const uint32_t e = uint32_t(j) * T + threadIdx.x;
-            if (e < n) {
-                const Rec<RS> v = rec_of(j, e);
+            for (int j = 0; j < IPT; ++j) {
+                if (uint32_t(j) * T >= n) break;  // block-uniform
+                const uint32_t e = uint32_t(j) * T + threadIdx.x;
+                if (e < n) {
+                    const Rec<RS> v = rec_of(j, e);
 #pragma unroll
-                for (int w = 0; w < 2 * KW; ++w) a[w] &= v.w[w], o[w] |= v.w[w];
+                    for (int w = 0; w < 2 * KW; ++w) a[w] &= v.w[w], o[w] |= v.w[w];
+                    if constexpr (decltype(specc)::value) {
+                        const uint32_t w = rec_window<RS>(v, wsd);
+                        wv[KEEP ? j : 0] = w;
+                        win[e] = w;
+                        smn = min(smn, w);
+                        smx = max(smx, w);
+                    }
+                }
             }
-        }
+        };
+        if (spec) andor(BoolC<KEEP>{});
+        else andor(BoolC<false>{});
 #pragma unroll
         for (int w = 0; w < 2 * KW; ++w) {
             a[w] = __reduce_and_sync(0xFFFFFFFFu, a[w]);
@@ -314,12 +335,19 @@ __device__ __forceinline__ void local_group(
     }
     const uint32_t nwin = nL < 4 ? nL : 4;
     const bool beyond = nL > 4;
+    const bool spec_ok = spec && nwin == 4 && s_L[0] == g.p && s_L[1] == g.p + 1 && s_L[2] == g.p + 2 &&
+                         s_L[3] == g.p + 3;  // warp-uniform and equal in every warp
 
     // ---- 3. windows (registers + shared memory), their range
     // windows / buckets kept in registers when records are not (register budget)
-    constexpr bool KEEP = !REG;
-    uint32_t wv[KEEP ? IPT : 1];
-    {
+    if (spec_ok) {  // computed by the AND/OR pass
+        smn = __reduce_min_sync(0xFFFFFFFFu, smn);
+        smx = __reduce_max_sync(0xFFFFFFFFu, smx);
+        if (lane == 0) {
+            atomicMin(&s_wmin, smn);
+            atomicMax(&s_wmax, smx);
+        }
+    } else {
         const uint32_t L0 = s_L[0], L1 = s_L[nwin > 1 ? 1 : 0], L2 = s_L[nwin > 2 ? 2 : 0],
                        L3 = s_L[nwin > 3 ? 3 : 0];
         const WindowSel ws = make_window_sel(s_L, nwin, RS / 4, RS == 8);
