@@ -425,16 +425,23 @@ __device__ __forceinline__ void local_group(
 
     mid();
     // ---- 4. bucket histogram (packed u16 pairs, zeroed at the start), scan, largest bucket
+    // KEEP: per record (padded u16 counter index | bucket << 16), the address
+    // math done once for the histogram, the id scatter and the rank
+    auto i16_of = [](uint32_t b) { return b + ((b >> 6) << 3); };
     uint32_t bk[KEEP ? IPT : 1];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
         if (uint32_t(j) * T >= n) break;  // block-uniform
         const uint32_t e = uint32_t(j) * T + threadIdx.x;
         if (e < n) {
-            uint32_t b;
-            if constexpr (KEEP) b = bk[j] = bucket_of(wv[j]);
-            else b = bucket_of(win[e]);
-            atomicAdd(&cw(b), 1u << ((b & 1) * 16));
+            if constexpr (KEEP) {
+                const uint32_t b = bucket_of(wv[j]), i = i16_of(b);
+                bk[j] = i | (b << 16);
+                atomicAdd(&cnt[i >> 1], 1u << ((i & 1) * 16));
+            } else {
+                const uint32_t b = bucket_of(win[e]);
+                atomicAdd(&cw(b), 1u << ((b & 1) * 16));
+            }
         }
     }
     __syncthreads();
@@ -505,11 +512,11 @@ __device__ __forceinline__ void local_group(
             if (uint32_t(j) * T >= n) break;  // block-uniform
             const uint32_t e = uint32_t(j) * T + threadIdx.x;
             if (e < n) {
-                uint32_t b;
-                if constexpr (KEEP) b = bk[j];
-                else b = bucket_of(win[e]);
-                const uint32_t old = atomicAdd(&cw(b), 1u << ((b & 1) * 16));
-                slot[(old >> ((b & 1) * 16)) & 0xFFFFu] = uint16_t(e);
+                uint32_t i;  // the bucket's u16 counter index
+                if constexpr (KEEP) i = bk[j] & 0xFFFFu;
+                else i = i16_of(bucket_of(win[e]));
+                const uint32_t old = atomicAdd(&cnt[i >> 1], 1u << ((i & 1) * 16));
+                slot[(old >> ((i & 1) * 16)) & 0xFFFFu] = uint16_t(e);
             }
         }
         __syncthreads();
@@ -545,11 +552,19 @@ __device__ __forceinline__ void local_group(
             if (uint32_t(j) * T >= n) break;  // block-uniform
             const uint32_t e = uint32_t(j) * T + threadIdx.x;
             if (e < n) {
-                uint32_t w, bb;
-                if constexpr (KEEP) w = wv[j], bb = bk[j];
-                else w = win[e], bb = bucket_of(w);
-                const uint32_t en = end_of(bb);
-                const uint32_t st = bb ? end_of(bb - 1) : 0u;
+                uint32_t w, bb, en, st;
+                if constexpr (KEEP) {
+                    w = wv[j];
+                    bb = bk[j] >> 16;
+                    const uint32_t i = bk[j] & 0xFFFFu;  // bucket bb - 1 sits 1 (9 across a pad) below
+                    en = cnt16[i];
+                    st = bb ? cnt16[i - ((bb & 63) ? 1u : 9u)] : 0u;
+                } else {
+                    w = win[e];
+                    bb = bucket_of(w);
+                    en = end_of(bb);
+                    st = bb ? end_of(bb - 1) : 0u;
+                }
                 const uint32_t sz = en - st;
                 if (sz <= 3) {
                     const uint32_t last = en - 1;
