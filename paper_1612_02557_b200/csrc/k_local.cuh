@@ -568,9 +568,17 @@ __device__ __forceinline__ void local_group(
                 const uint32_t sz = en - st;
                 if (sz <= 3) {
                     const uint32_t last = en - 1;
-                    const uint32_t e1 = slot[st], e2 = slot[min(st + 1, last)],
-                                   e3 = slot[min(st + 2, last)];
-                    const uint32_t w1 = win[e1], w2 = win[e2], w3 = win[e3];
+                    // a bucket of one (most records) needs no neighbour: its
+                    // lanes skip the loads (no shared-memory requests issued)
+                    uint32_t e1 = e, e2 = e, e3 = e, w1 = w, w2 = w, w3 = w;
+                    if (sz > 1) {
+                        e1 = slot[st];
+                        e2 = slot[min(st + 1, last)];
+                        e3 = slot[min(st + 2, last)];
+                        w1 = win[e1];
+                        w2 = win[e2];
+                        w3 = win[e3];
+                    }
                     const bool u1 = e1 != e, u2 = e2 != e && e2 != e1, u3 = e3 != e && e3 != e2;
                     // (window, index) order as one 64-bit compare
                     const uint64_t k = (uint64_t(w) << 32) | e;
