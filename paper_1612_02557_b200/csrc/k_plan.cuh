@@ -88,6 +88,40 @@ __device__ __forceinline__ void init_next(const PlanArgs& A, uint32_t idx, uint3
     if (threadIdx.x < 8) A.next_andor[uint64_t(idx) * 8 + threadIdx.x] = (threadIdx.x & 1) ? 0ull : ~0ull;
 }
 
+// Level 0 without host round trips. k_set_seg0: the whole array as one
+// segment at the first key byte that varies in the strided sample (0 if none).
+__global__ void k_set_seg0(const unsigned long long* __restrict__ andor, uint32_t ks, uint64_t n,
+                           Seg* __restrict__ seg) {
+    const uint32_t b = threadIdx.x;  // one warp
+    const bool varies = b < ks && andor_byte_varies(andor, b);
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, varies);
+    if (b == 0) {
+        Seg s0;
+        s0.start = 0;
+        s0.size = n;
+        s0.p = m ? __ffs(m) - 1 : 0u;
+        s0.parity = 0;
+        s0.tile_base = 0;
+        s0.action = 0;
+        *seg = s0;
+    }
+}
+
+// After the level-0 histogram: a more significant byte than the sample's
+// guess varies (it varies only off the sample) -> flag = 0x100 | that byte;
+// the host then redoes level 0 on it. Never the other way round: a byte that
+// varies in the sample varies in the array.
+__global__ void k_check_seg0(const unsigned long long* __restrict__ andor, const Seg* __restrict__ seg,
+                             uint32_t ks, unsigned long long* __restrict__ flag) {
+    const uint32_t b = threadIdx.x;
+    const bool varies = b < ks && andor_byte_varies(andor, b);
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, varies);
+    if (b == 0) {
+        const uint32_t pg = m ? __ffs(m) - 1 : ks;
+        *flag = (pg < ks && pg != seg->p) ? (0x100ull | pg) : 0ull;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
     __shared__ unsigned long long s_cnt[kRadix], s_off[kRadix];
     __shared__ unsigned long long s_wsum[8];

@@ -347,14 +347,6 @@ int grid_for(uint64_t n, int threads, int per_sm) {
     return int(std::max<uint64_t>(1, std::min<uint64_t>(want, uint64_t(sms) * per_sm)));
 }
 
-uint32_t first_varying_byte(const unsigned long long* andor, uint32_t from, uint32_t ks) {
-    for (uint32_t b = from; b < ks; ++b) {
-        const unsigned long long x = andor[2 * (b >> 3)] ^ andor[2 * (b >> 3) + 1];
-        if ((x >> ((b & 7) * 8)) & 0xFF) return b;
-    }
-    return ks;
-}
-
 // Local-sort group capacity: the register variant for 8-B records (C2 needs
 // ~17 K-record groups), the shared-memory variant otherwise.
 template <int RS>
@@ -479,13 +471,10 @@ void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, 
 }
 
 // Groups the fast local sort handed over (duplicate-heavy keys): stable LSD.
-// Reads the spill count (synchronises `st`).
+// `n` = the spill count, read back with the level counters.
 template <int RS>
 void finish_spilled(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ks, LevelCounters* ctr,
-                    cudaStream_t st) {
-    unsigned int n = 0;
-    RG_CHECK(cudaMemcpyAsync(&n, ws.n_spill.p, sizeof n, cudaMemcpyDeviceToHost, st));
-    RG_CHECK(cudaStreamSynchronize(st));
+                    cudaStream_t st, unsigned int n) {
     if (!n) return;
     if (n > ws.spill.cap) throw CudaError{RADULS_GPU_EINTERNAL};
     const int pe = ws.prof.begin(K_LOCAL, st);
@@ -494,6 +483,22 @@ void finish_spilled(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ks, Lev
         data, tmp, ws.spill.p, n, ks, ctr, nullptr, nullptr, 0);
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
+    RG_CHECK(cudaStreamSynchronize(st));
+}
+
+// The counters of `levels` levels and the spill count in one readback; the
+// spilled groups (rare) get the LSD fallback and the counters are re-read.
+template <int RS>
+void read_counters_and_finish(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ks, LevelCounters* dctr,
+                              uint32_t levels, cudaStream_t st) {
+    unsigned int* hn = reinterpret_cast<unsigned int*>(ws.h_small + 4001);
+    RG_CHECK(cudaMemcpyAsync(ws.h_ctr, dctr, sizeof(LevelCounters) * levels, cudaMemcpyDeviceToHost, st));
+    RG_CHECK(cudaMemcpyAsync(hn, ws.n_spill.p, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    RG_CHECK(cudaStreamSynchronize(st));
+    const unsigned int n = *hn;
+    if (!n) return;
+    finish_spilled<RS>(ws, data, tmp, ks, dctr, st, n);
+    RG_CHECK(cudaMemcpyAsync(ws.h_ctr, dctr, sizeof(LevelCounters) * levels, cudaMemcpyDeviceToHost, st));
     RG_CHECK(cudaStreamSynchronize(st));
 }
 
@@ -515,9 +520,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         RG_CHECK(cudaMemcpyAsync(ws.groups.p, &g, sizeof g, cudaMemcpyHostToDevice, st));
         RG_CHECK(cudaMemsetAsync(dctr, 0, sizeof(LevelCounters), st));
         launch_local<RS>(ws, data, tmp, 1, ks, dctr, st);
-        finish_spilled<RS>(ws, data, tmp, ks, dctr, st);
-        RG_CHECK(cudaMemcpyAsync(ws.h_ctr, dctr, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
-        RG_CHECK(cudaStreamSynchronize(st));
+        read_counters_and_finish<RS>(ws, data, tmp, ks, dctr, 1, st);
         ws.prof.collect();
         stats.levels = 1;
         stats.local_records = ws.h_ctr[0].moved_local;
@@ -539,50 +542,26 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
     k_sample_andor<RS><<<64, 256, 0, st>>>(data, n, std::max<uint64_t>(1, n / samples), samples, ws.andor0.p);
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
-    RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.andor0.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    RG_CHECK(cudaStreamSynchronize(st));
-    uint32_t p0 = first_varying_byte(ws.h_small, 0, ks);
-    if (p0 >= ks) p0 = 0;  // sample saw one key only: histogram byte 0 and let AND/OR decide
+    // no host round trip: the guess goes straight into the level-0 segment,
+    // and a check after the histogram flags (rarely) a more significant
+    // varying byte; the flag is read with the level-0 plan's counters
+    k_set_seg0<<<1, 32, 0, st>>>(ws.andor0.p, ks, n, ws.segs[0].p);
+    RG_LAUNCH_CHECK();
     const uint32_t nt0 = uint32_t((n + TILE - 1) / TILE);
     int cur = 0;
-    {
-        Seg s0{0, n, p0, 0, 0, 0};
-        RG_CHECK(cudaMemcpyAsync(ws.segs[0].p, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
+    unsigned long long* d_flag = ws.acc.p + 3;
+    auto level0_counts = [&] {
         RG_CHECK(cudaMemsetAsync(ws.tile_seg[0].p, 0, nt0 * sizeof(uint32_t), st));
-        {
-            const int pi = ws.prof.begin(K_INIT, st);
-            {
-                const int pi = ws.prof.begin(K_INIT, st);
-                k_init_andor<<<1, 64, 0, st>>>(ws.seg_andor[0].p, 1);
-                RG_LAUNCH_CHECK();
-                ws.prof.end(pi, st);
-            }
-            ws.prof.end(pi, st);
-        }
+        const int pi = ws.prof.begin(K_INIT, st);
+        k_init_andor<<<1, 64, 0, st>>>(ws.seg_andor[0].p, 1);
+        RG_LAUNCH_CHECK();
+        ws.prof.end(pi, st);
         RG_CHECK(cudaMemsetAsync(dctr, 0, sizeof(LevelCounters), st));
         level_counts<RS>(ws, data, tmp, 0, nt0, dctr, st);
-        RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.seg_andor[0].p, 8 * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, st));
-        RG_CHECK(cudaStreamSynchronize(st));
-        const uint32_t pg = first_varying_byte(ws.h_small, 0, ks);
-        if (pg >= ks) {  // every key equal: a stable sort is the identity
-            ws.prof.collect();
-            ws.last = stats;
-            return;
-        }
-        if (pg != p0) {  // a more significant byte varies outside the sample
-            s0.p = pg;
-            RG_CHECK(cudaMemcpyAsync(ws.segs[0].p, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
-            {
-                const int pi = ws.prof.begin(K_INIT, st);
-                k_init_andor<<<1, 64, 0, st>>>(ws.seg_andor[0].p, 1);
-                RG_LAUNCH_CHECK();
-                ws.prof.end(pi, st);
-            }
-            RG_CHECK(cudaMemsetAsync(dctr, 0, sizeof(LevelCounters), st));
-            level_counts<RS>(ws, data, tmp, 0, nt0, dctr, st);
-        }
-    }
+        k_check_seg0<<<1, 32, 0, st>>>(ws.seg_andor[0].p, ws.segs[0].p, ks, d_flag);
+        RG_LAUNCH_CHECK();
+    };
+    level0_counts();
     uint32_t nseg = 1, ntiles = nt0, level = 0;
     const Caps caps = caps_for<RS>(n);
     while (true) {
@@ -606,7 +585,15 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         RG_LAUNCH_CHECK();
         ws.prof.end(pe, st);
         RG_CHECK(cudaMemcpyAsync(ws.h_ctr + level, c, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
+        if (level == 0)
+            RG_CHECK(cudaMemcpyAsync(ws.h_small + 4000, d_flag, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         RG_CHECK(cudaStreamSynchronize(st));
+        if (level == 0 && ws.h_small[4000]) {  // a more significant byte varies off the sample: redo level 0 on it
+            Seg s0{0, n, uint32_t(ws.h_small[4000] & 0xFF), 0, 0, 0};
+            RG_CHECK(cudaMemcpyAsync(ws.segs[0].p, &s0, sizeof s0, cudaMemcpyHostToDevice, st));
+            level0_counts();
+            continue;
+        }
         const LevelCounters h = ws.h_ctr[level];
         if (h.n_groups > caps.groups || h.n_copy > caps.copies || h.n_next > caps.seg ||
             h.n_next_tiles > caps.tiles)
@@ -633,9 +620,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         RG_CHECK(cudaMemsetAsync(dctr + level, 0, sizeof(LevelCounters), st));
         level_counts<RS>(ws, data, tmp, cur, ntiles, dctr + level, st);
     }
-    finish_spilled<RS>(ws, data, tmp, ks, dctr, st);
-    RG_CHECK(cudaMemcpyAsync(ws.h_ctr, dctr, sizeof(LevelCounters) * level, cudaMemcpyDeviceToHost, st));
-    RG_CHECK(cudaStreamSynchronize(st));
+    read_counters_and_finish<RS>(ws, data, tmp, ks, dctr, level, st);
     ws.prof.collect();
     stats.levels = level;
     for (uint32_t l = 0; l < level; ++l) {
