@@ -29,7 +29,7 @@ namespace rg {
 template <int RS>
 struct ScatterCfg {
     static constexpr int kThreads = 256;
-    static constexpr int kItems = RS == 8 ? 16 : RS == 16 ? 11 : RS == 24 ? 7 : 6;
+    static constexpr int kItems = RS == 8 ? 20 : RS == 16 ? 11 : RS == 24 ? 7 : 6;
     static constexpr int kTile = kThreads * kItems;
     static constexpr int kWarps = kThreads / 32;
     static constexpr int kStages = 2;  // tile buffers in the TMA ring

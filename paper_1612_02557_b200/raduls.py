@@ -275,7 +275,7 @@ def local_capacity(record_size: int) -> int:
 
 # Scatter / histogram tile per record size (mirrors ScatterCfg<RS>::kTile in
 # csrc/k_scatter.cuh; tests aim at its boundaries).
-_SCATTER_TILE = {8: 4096, 16: 2816, 24: 1792, 32: 1536}
+_SCATTER_TILE = {8: 5120, 16: 2816, 24: 1792, 32: 1536}
 
 
 def scatter_tile(record_size: int) -> int:
