@@ -129,7 +129,8 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
     __shared__ uint32_t s_next_idx[kRadix], s_next_tb[kRadix];
     __shared__ uint32_t s_wbig[8], s_wtiles[8], s_nb_base, s_nt_base;
     __shared__ uint64_t s_gstart[kRadix];
-    __shared__ uint32_t s_gsize[kRadix];
+    __shared__ uint32_t s_gsize[kRadix], s_P[kRadix + 1], s_nbig[kRadix], s_open[kRadix], s_end[kRadix];
+    __shared__ uint32_t s_wsz[8];
     const uint32_t s = blockIdx.x;
     const Seg g = A.segs[s];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -230,25 +231,67 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
             s_next_tb[tid] = tb;
         }
     }
-    // small children -> greedy groups (thread 0, digit order)
-    if (tid == 0) {
-        uint32_t ng = 0;
-        uint64_t gs = 0;
-        uint32_t gsz = 0;
-        for (int d = 0; d < kRadix; ++d) {
-            const unsigned long long sz = s_cnt[d];
-            if (sz == 0) continue;
-            if (sz > A.cap_local) {
-                if (gsz) s_gstart[ng] = gs, s_gsize[ng] = gsz, ++ng, gsz = 0;
-                continue;
-            }
-            if (gsz && gsz + sz > A.cap_local) s_gstart[ng] = gs, s_gsize[ng] = gsz, ++ng, gsz = 0;
-            if (gsz == 0) gs = g.start + s_off[d];
-            gsz += uint32_t(sz);
+    // small children -> greedy groups in digit order (a child joins the open
+    // group while the group stays <= cap; a big child closes it). With the
+    // exclusive prefix P of the small sizes, a group opened at digit d ends at
+    // the first d' > d that is big or has P[d' + 1] - P[d] > cap: every digit
+    // finds its own end by binary search (P is monotone), a suffix minimum
+    // gives the next open digit, and thread 0 walks the ~n/cap-long chain.
+    {
+        const uint32_t cap = uint32_t(A.cap_local);
+        const unsigned long long c = s_cnt[tid];
+        const bool big = c > cap;
+        const uint32_t sz = big ? 0u : uint32_t(c);
+        // exclusive prefix of the small sizes (block scan over 256 digits)
+        uint32_t x = sz;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o) x += y;
         }
-        if (gsz) s_gstart[ng] = gs, s_gsize[ng] = gsz, ++ng;
-        s_ngroups = ng;
-        s_base = ng ? atomicAdd(&A.ctr->n_groups, ng) : 0u;
+        if (lane == 31) s_wsz[warp] = x;
+        __syncthreads();
+        uint32_t wb = 0;
+        for (int k = 0; k < warp; ++k) wb += s_wsz[k];
+        s_P[tid] = wb + x - sz;
+        if (tid == kRadix - 1) s_P[kRadix] = wb + x;
+        // next big digit after d, next open (small, non-empty) digit >= d: suffix minima
+        s_nbig[tid] = big ? tid : kRadix;
+        s_open[tid] = sz ? tid : kRadix;
+        __syncthreads();
+        for (int o = 1; o < kRadix; o <<= 1) {
+            const uint32_t nb = tid + o < kRadix ? s_nbig[tid + o] : kRadix;
+            const uint32_t op = tid + o < kRadix ? s_open[tid + o] : kRadix;
+            __syncthreads();
+            s_nbig[tid] = min(s_nbig[tid], nb);
+            s_open[tid] = min(s_open[tid], op);
+            __syncthreads();
+        }
+        // end of a group opened here: first d' in (d, next big) with P[d'+1] > P[d] + cap
+        if (sz) {
+            const uint32_t lim = tid + 1 < kRadix ? s_nbig[tid + 1] : kRadix;  // first big after d
+            const uint32_t bound = s_P[tid] + cap;
+            uint32_t lo = tid + 1, hi = lim;  // answer in [lo, hi]; hi = lim: no overflow before it
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (s_P[mid + 1] > bound) hi = mid;
+                else lo = mid + 1;
+            }
+            s_end[tid] = lo;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t ng = 0;
+            for (uint32_t d0 = s_open[0]; d0 < uint32_t(kRadix);) {
+                const uint32_t e = s_end[d0];
+                s_gstart[ng] = g.start + s_off[d0];
+                s_gsize[ng] = s_P[e] - s_P[d0];
+                ++ng;
+                d0 = e < uint32_t(kRadix) ? s_open[e] : uint32_t(kRadix);
+            }
+            s_ngroups = ng;
+            s_base = ng ? atomicAdd(&A.ctr->n_groups, ng) : 0u;
+        }
     }
     __syncthreads();
     if (tid < int(s_ngroups)) {
