@@ -426,8 +426,8 @@ void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t 
         k_tile_hist_reg<RS, TILE, kMap><<<ntiles, HistRegCfg<RS, TILE>::kThreads, 0, st>>>(
             data, tmp, ws.segs[cur].p, ws.tile_seg[cur].p, ws.tile_cnt.p, ws.seg_andor[cur].p, c, ks, map);
     } else {  // persistent, TMA-fed
-        const uint32_t hgrid = std::min<uint32_t>(ntiles, uint32_t(sm_count()) * 2);
-        k_tile_hist<RS, kMap><<<hgrid, HistCfg<RS>::kThreads + 32, HistCfg<RS>::kSmem, st>>>(
+        const uint32_t hgrid = std::min<uint32_t>(ntiles, uint32_t(sm_count()) * HistCfg<RS>::kCtas);
+        k_tile_hist<RS, kMap><<<hgrid, HistCfg<RS>::kThreads + 64, HistCfg<RS>::kSmem, st>>>(
             data, tmp, ws.segs[cur].p, ws.tile_seg[cur].p, ws.tile_cnt.p, ws.seg_andor[cur].p, c, ntiles, ks,
             map);
     }
