@@ -26,13 +26,20 @@
 
 namespace rg {
 
+#ifndef RG_SC_STAGES
+#define RG_SC_STAGES 2
+#endif
+#ifndef RG_SC_CTAS
+#define RG_SC_CTAS 2
+#endif
 template <int RS>
 struct ScatterCfg {
     static constexpr int kThreads = 256;
     static constexpr int kItems = RS == 8 ? 20 : RS == 16 ? 11 : RS == 24 ? 7 : 6;
     static constexpr int kTile = kThreads * kItems;
     static constexpr int kWarps = kThreads / 32;
-    static constexpr int kStages = 2;  // tile buffers in the TMA ring
+    static constexpr int kStages = RG_SC_STAGES;  // tile buffers in the TMA ring
+    static constexpr int kCtas = RG_SC_CTAS;      // resident per SM (grid = kCtas x SMs)
     static constexpr int kBufBytes = ((kTile * RS + 16 + 127) / 128) * 128;  // + alignment slack
     static constexpr size_t kSmem = size_t(kStages) * kBufBytes + size_t(kTile) * 4;  // ring + slot map
 };
@@ -96,7 +103,7 @@ struct TileInfo {
 // there — so the all-to-all is carried out by the partition's own coalesced
 // stores, tile by tile, instead of a separate collective.
 template <int RS, bool kMap = false, bool kPeer = false>
-__global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, 2) k_scatter(
+__global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>::kCtas) k_scatter(
     uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Seg* __restrict__ segs,
     const unsigned long long* __restrict__ seg_base,  // [nseg][256] exclusive digit bases
     const uint32_t* __restrict__ tile_seg, const uint32_t* __restrict__ tile_off,  // [ntiles][256]
