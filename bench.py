@@ -177,12 +177,14 @@ def run_cpu_reference(cfg_name: str, n_sample: int, steps: int, warmup: int) -> 
 
 def algorithmic_bytes(stats: dict, rs: int) -> dict:
     """SURVEY.md §8(d): 2*rs per record per executed pass (read + write);
-    histogram-only reads are overhead (1*rs)."""
+    histogram-only reads are overhead (1*rs per record read whole, 1 byte per
+    record read from the digit array, which the scatter before wrote)."""
+    nd = stats.get("hist_digit_records", 0)
     return {
         "scatter": 2 * rs * stats["scatter_records"],
         "local_sort": 2 * rs * stats["local_records"],
         "copy_back": 2 * rs * stats["copy_records"],
-        "tile_hist": rs * stats["hist_records"],
+        "tile_hist": rs * stats["hist_records"] + nd,
     }
 
 

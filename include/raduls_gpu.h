@@ -100,6 +100,8 @@ typedef struct {
     uint64_t copy_records;      /* records moved by copy-back */
     uint64_t fallback_groups;   /* local-sort groups that needed the full-key fallback */
     uint64_t skipped_levels;    /* segment-levels skipped as constant digits (e) */
+    uint64_t hist_digit_records; /* records histogrammed from the digit array (1 byte each; the
+                                    scatter before wrote that byte) instead of from the records */
 } raduls_gpu_stats;
 
 int raduls_gpu_last_stats(raduls_gpu_stats* out);

@@ -55,6 +55,7 @@ class Stats(C.Structure):
         ("copy_records", C.c_uint64),
         ("fallback_groups", C.c_uint64),
         ("skipped_levels", C.c_uint64),
+        ("hist_digit_records", C.c_uint64),
     ]
 
     def as_dict(self) -> dict:

@@ -345,6 +345,9 @@ struct LevelCounters {
     unsigned long long moved_copy;       // records moved by copy-back
     unsigned long long fallback_groups;  // local-sort groups that needed the LSD fallback
     unsigned long long hist_records;     // records read by this level's tile histogram
+    unsigned long long hist_digit_records;  // records histogrammed from the digit array (1 byte each)
+    uint32_t n_skip;                     // segments re-queued at a later byte without a split
+    uint32_t pad;
 };
 
 // Decoupled look-back status word: [63:62] flag, [61:0] value.

@@ -34,6 +34,7 @@ struct PlanArgs {
     uint32_t ks;
     uint32_t tile;       // tile partition (records)
     uint32_t cap_local;  // local-sort group capacity (records)
+    uint32_t side;       // this level was histogrammed from the digit array (no AND/OR)
 };
 
 __device__ __forceinline__ uint32_t andor_byte_varies(const unsigned long long* ao, uint32_t b) {
@@ -135,7 +136,16 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
     const Seg g = A.segs[s];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    if (tid < 32) {  // first varying key byte >= p (AND/OR of the segment)
+    if (A.side) {
+        // byte p histogrammed from the digit array: it varies iff more than one
+        // digit is populated; if it does not, the segment is re-queued at p + 1
+        // (whose first varying byte the next level's record histogram finds)
+        const uint32_t nz = __syncthreads_count(A.seg_tot[uint64_t(s) * kRadix + tid] != 0ull);
+        if (tid == 0) {
+            s_pnext = g.p + 1;
+            s_action = nz > 1 ? 2u : (g.p + 1 >= A.ks ? 0u : 1u);
+        }
+    } else if (tid < 32) {  // first varying key byte >= p (AND/OR of the segment)
         const unsigned long long* ao = A.seg_andor + uint64_t(s) * 8;
         const uint32_t b = g.p + lane;
         const bool varies = b < A.ks && andor_byte_varies(ao, b);
@@ -153,7 +163,10 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
         return;
     }
     if (action == 1) {  // (e) constant byte p: skip it without moving a record
-        if (tid == 0) s_base = emit_next(A, g.start, g.size, s_pnext, g.parity, &s_tb0);
+        if (tid == 0) {
+            s_base = emit_next(A, g.start, g.size, s_pnext, g.parity, &s_tb0);
+            atomicAdd(&A.ctr->n_skip, 1u);
+        }
         __syncthreads();
         init_next(A, s_base, s_tb0, g.size);
         return;

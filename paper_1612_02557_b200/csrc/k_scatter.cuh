@@ -95,6 +95,7 @@ struct TileInfo {
     uint64_t k;       // tile index inside the segment
     uint64_t gstart;  // first record of the tile (global record index)
     uint64_t seg_start;
+    uint64_t seg_size;
 };
 
 // kPeer (the multi-GPU partition): digit d is a destination
@@ -109,7 +110,8 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
     const uint32_t* __restrict__ tile_seg, const uint32_t* __restrict__ tile_off,  // [ntiles][256]
     uint32_t n_tiles, unsigned int* __restrict__ ticket, uint32_t ks = 0,
     const uint8_t* __restrict__ map = nullptr,
-    const unsigned long long* __restrict__ dig_dst = nullptr) {
+    const unsigned long long* __restrict__ dig_dst = nullptr, uint8_t* __restrict__ nd = nullptr,
+    uint32_t cap_local = 0) {
     using C = ScatterCfg<RS>;
     constexpr int T = C::kThreads, IT = C::kItems, W = C::kWarps;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -122,6 +124,7 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
     __shared__ uint32_t s_gdelta[kRadix];
     __shared__ unsigned long long s_pdst[kPeer ? kRadix : 1];  // digit's destination - its base
     __shared__ uint32_t s_scan[8];
+    __shared__ uint32_t s_big[kRadix];  // nd: 1 << 24 for digits whose child is split next level
     __shared__ __align__(8) unsigned long long s_full[C::kStages], s_empty[C::kStages];
     __shared__ TileInfo s_info[C::kStages];
 
@@ -166,6 +169,7 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
             ti.seg = s;
             ti.k = uint64_t(tile) - g.tile_base;
             ti.seg_start = g.start;
+            ti.seg_size = g.size;
             ti.gstart = g.start + ti.k * C::kTile;
             ti.tn = uint32_t(min(uint64_t(C::kTile), g.size - ti.k * C::kTile));
             ti.p = g.p;
@@ -243,6 +247,12 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
             }
         }
         s_gdelta[threadIdx.x] = uint32_t(my_base) - lstart;
+        if (nd) {  // children the next level splits: their records' next key byte goes to nd
+            const uint64_t sb = seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x];
+            const uint64_t se = threadIdx.x + 1 < kRadix ? seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x + 1]
+                                                         : ti.seg_size;
+            s_big[threadIdx.x] = (se - sb > cap_local) ? (1u << 24) : 0u;
+        }
         if constexpr (kPeer)
             s_pdst[threadIdx.x] = dig_dst[threadIdx.x] -
                                   (ti.seg_start + seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x]) * RS;
@@ -254,7 +264,7 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
             const uint32_t d = pk[j] & 0x1FFu;
             if (d < 256u) {
                 const uint32_t slot = s_wcnt[warp][d] + (pk[j] >> 9);
-                s_map[slot] = (uint32_t(warp * IT + j) * 32u + lane) | (d << 16);
+                s_map[slot] = (uint32_t(warp * IT + j) * 32u + lane) | (d << 16) | (nd ? s_big[d] : 0u);
             }
         }
         bar_sync_named(1, T);
@@ -268,10 +278,14 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
             if (slot < tn) {
                 const uint32_t m = s_map[slot];
                 const Rec<RS> v = ld_smem_rec<RS>(tile, m & 0xFFFFu);
-                if constexpr (kPeer)
-                    store_rec<RS>(reinterpret_cast<uint8_t*>(s_pdst[m >> 16] + ti.seg_start * RS), uint32_t(s_gdelta[m >> 16] + slot), v);
-                else
-                    store_rec<RS>(dst, uint32_t(s_gdelta[m >> 16] + slot), v);
+                const uint32_t d = (m >> 16) & 0xFFu;
+                if constexpr (kPeer) {
+                    store_rec<RS>(reinterpret_cast<uint8_t*>(s_pdst[d] + ti.seg_start * RS), uint32_t(s_gdelta[d] + slot), v);
+                } else {
+                    const uint32_t di = s_gdelta[d] + slot;
+                    store_rec<RS>(dst, di, v);
+                    if (m >> 24) nd[ti.seg_start + di] = uint8_t(rec_byte<RS>(v, p + 1));
+                }
             }
         }
         bar_sync_named(1, T);  // buffer b, map and counters free for reuse

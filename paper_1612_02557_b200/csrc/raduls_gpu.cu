@@ -23,6 +23,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -294,6 +295,7 @@ struct Workspace {
     DevBuf<CopyRange> copies;
     DevBuf<uint8_t> host_data, host_tmp, map8;
     DevBuf<unsigned long long> dig_dst;  // per-destination byte addresses (raduls_gpu_partition_to)
+    DevBuf<uint8_t> nd;                  // digit array: next key byte per record position (sort_impl)
     HostStager* stager = nullptr;  // host drop-ins, created on first use
     HostStager& host_stager() {
         if (!stager) stager = new HostStager();
@@ -417,12 +419,18 @@ int sm_count() {
 
 // Tile histogram + segmented look-back scan of one level: per-tile digit
 // offsets (ws.tile_off), per-segment digit totals (ws.seg_tot[cur]).
+// side: byte p of every record of the level is in ws.nd (written by the
+// previous level's scatter), so the histogram reads one byte per record.
 template <int RS, bool kMap = false>
 void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t ntiles, LevelCounters* c,
-                  cudaStream_t st, uint32_t ks = 0, const uint8_t* map = nullptr) {
+                  cudaStream_t st, uint32_t ks = 0, const uint8_t* map = nullptr, bool side = false) {
     constexpr int TILE = ScatterCfg<RS>::kTile;
     int pe = ws.prof.begin(K_HIST, st);
-    if constexpr (RS == 8) {  // one CTA per tile (see k_tile_hist_reg)
+    if (side) {
+        const uint32_t grid = std::min<uint32_t>((ntiles + kNdWarps - 1) / kNdWarps, uint32_t(sm_count()) * 4);
+        k_tile_hist_nd<TILE><<<grid, kNdWarps * 32, 0, st>>>(ws.nd.p, ws.segs[cur].p, ws.tile_seg[cur].p,
+                                                             ws.tile_cnt.p, c, ntiles);
+    } else if constexpr (RS == 8) {  // one CTA per tile (see k_tile_hist_reg)
         k_tile_hist_reg<RS, TILE, kMap><<<ntiles, HistRegCfg<RS, TILE>::kThreads, 0, st>>>(
             data, tmp, ws.segs[cur].p, ws.tile_seg[cur].p, ws.tile_cnt.p, ws.seg_andor[cur].p, c, ks, map);
     } else {  // persistent, TMA-fed
@@ -445,12 +453,12 @@ void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t 
 template <int RS, bool kMap, bool kPeer = false>
 void launch_scatter(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t ntiles, uint32_t ks,
                     const uint8_t* map, LevelCounters* c, cudaStream_t st,
-                    const unsigned long long* dig_dst = nullptr) {
+                    const unsigned long long* dig_dst = nullptr, uint8_t* nd = nullptr) {
     const uint32_t grid = std::min<uint32_t>(ntiles, uint32_t(sm_count()) * 2);
     const int pe = ws.prof.begin(K_SCATTER, st);
     k_scatter<RS, kMap, kPeer><<<grid, ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>::kSmem, st>>>(
         data, tmp, ws.segs[cur].p, ws.seg_tot[cur].p, ws.tile_seg[cur].p, ws.tile_off.p, ntiles,
-        &c->scatter_ticket, ks, map, dig_dst);
+        &c->scatter_ticket, ks, map, dig_dst, nd, local_cap<RS>());
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
 }
@@ -500,6 +508,22 @@ void read_counters_and_finish(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32
     finish_spilled<RS>(ws, data, tmp, ks, dctr, st, n);
     RG_CHECK(cudaMemcpyAsync(ws.h_ctr, dctr, sizeof(LevelCounters) * levels, cudaMemcpyDeviceToHost, st));
     RG_CHECK(cudaStreamSynchronize(st));
+}
+
+// The digit array for a sort of n records (grown on demand, +16 B for the
+// histogram's vector over-read). false if it cannot be allocated or
+// RADULS_GPU_NO_DIGIT_ARRAY is set.
+bool digit_array(Workspace& ws, uint64_t n) {
+    if (std::getenv("RADULS_GPU_NO_DIGIT_ARRAY")) return false;
+    if (ws.nd.cap >= n + 16) return true;
+    ws.nd.release();
+    if (cudaMalloc(&ws.nd.p, n + 16) != cudaSuccess) {
+        cudaGetLastError();  // not sticky: clear it
+        ws.nd.p = nullptr;
+        return false;
+    }
+    ws.nd.cap = n + 16;
+    return true;
 }
 
 template <int RS>
@@ -564,6 +588,11 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
     level0_counts();
     uint32_t nseg = 1, ntiles = nt0, level = 0;
     const Caps caps = caps_for<RS>(n);
+    bool side = false;  // this level's histogram came from the digit array
+    // Digit array: the scatter writes the next key byte of every record whose
+    // child is split again, so the next histogram reads 1 byte, not rs. Best
+    // effort: without the n extra bytes every level reads whole records.
+    const bool nd_ok = digit_array(ws, n);
     while (true) {
         if (level >= uint32_t(kMaxLevels)) throw CudaError{RADULS_GPU_EINTERNAL};
         LevelCounters* c = dctr + level;
@@ -580,6 +609,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         A.ks = ks;
         A.tile = TILE;
         A.cap_local = local_cap<RS>();
+        A.side = side ? 1u : 0u;
         pe = ws.prof.begin(K_PLAN, st);
         k_plan<<<nseg, 256, 0, st>>>(A);
         RG_LAUNCH_CHECK();
@@ -598,8 +628,13 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         if (h.n_groups > caps.groups || h.n_copy > caps.copies || h.n_next > caps.seg ||
             h.n_next_tiles > caps.tiles)
             throw CudaError{RADULS_GPU_EINTERNAL};
+        // the next level reads its digits from nd iff every one of its
+        // segments comes out of this level's scatter (none re-queued at a
+        // later byte without a split)
+        const bool side_next = nd_ok && h.n_next && !h.n_skip;
         if (h.n_scatter_segs) {
-            launch_scatter<RS, false>(ws, data, tmp, cur, ntiles, ks, nullptr, c, st);
+            launch_scatter<RS, false>(ws, data, tmp, cur, ntiles, ks, nullptr, c, st, nullptr,
+                                      side_next ? ws.nd.p : nullptr);
             stats.scatter_launches++;
         }
         launch_local<RS>(ws, data, tmp, h.n_groups, ks, c, st);
@@ -618,7 +653,8 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         nseg = h.n_next;
         ntiles = h.n_next_tiles;
         RG_CHECK(cudaMemsetAsync(dctr + level, 0, sizeof(LevelCounters), st));
-        level_counts<RS>(ws, data, tmp, cur, ntiles, dctr + level, st);
+        side = side_next;
+        level_counts<RS>(ws, data, tmp, cur, ntiles, dctr + level, st, ks, nullptr, side);
     }
     read_counters_and_finish<RS>(ws, data, tmp, ks, dctr, level, st);
     ws.prof.collect();
@@ -627,6 +663,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         stats.local_records += ws.h_ctr[l].moved_local;
         stats.fallback_groups += ws.h_ctr[l].fallback_groups;
         stats.hist_records += ws.h_ctr[l].hist_records;
+        stats.hist_digit_records += ws.h_ctr[l].hist_digit_records;
     }
     ws.last = stats;
 }
