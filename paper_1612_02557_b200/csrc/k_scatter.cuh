@@ -17,6 +17,9 @@
 //     that order: consecutive slots of one digit go to consecutive destinations,
 //     so every digit run becomes one contiguous span of 16-B (8-B) vector
 //     stores — the GPU analogue of the 256-B write-combining lanes.
+// With `nd` (the digit array), records whose child is split again next level
+// also store their next key byte at their destination index, so that level's
+// histogram reads 1 byte per record instead of the record (k_tile_hist_nd).
 // Destinations come from k_tile_scan (per-tile digit offsets inside the
 // segment, the decoupled-lookback scan) and k_plan (digit bases): no tile waits
 // on another, so prefetching the next tile cannot stall anyone.
@@ -124,7 +127,6 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
     __shared__ uint32_t s_gdelta[kRadix];
     __shared__ unsigned long long s_pdst[kPeer ? kRadix : 1];  // digit's destination - its base
     __shared__ uint32_t s_scan[8];
-    __shared__ uint32_t s_big[kRadix];  // nd: 1 << 24 for digits whose child is split next level
     __shared__ __align__(8) unsigned long long s_full[C::kStages], s_empty[C::kStages];
     __shared__ TileInfo s_info[C::kStages];
 
@@ -202,9 +204,14 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
         const TileInfo ti = s_info[b];
         if (ti.tile >= n_tiles) break;
         // this thread's digit: base inside the segment + offset of the tile
-        const unsigned long long my_base =
-            seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x] +
-            tile_off[uint64_t(ti.tile) * kRadix + threadIdx.x];
+        const unsigned long long my_sb = seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x];
+        const unsigned long long my_base = my_sb + tile_off[uint64_t(ti.tile) * kRadix + threadIdx.x];
+        uint32_t big = 0;
+        if (nd) {
+            const uint64_t se = threadIdx.x + 1 < kRadix ? seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x + 1]
+                                                         : ti.seg_size;
+            big = se - my_sb > cap_local ? (1u << 24) : 0u;
+        }
         const uint8_t* tile = buf0 + b * C::kBufBytes + ti.head;
         const uint32_t tn = ti.tn, p = ti.p;
         __syncwarp();
@@ -237,22 +244,17 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
         }
         uint32_t total;
         const uint32_t lstart = scan256_exclusive(tcount, s_scan, &total);
-        {  // warp w's first slot of digit d
+        {  // warp w's first slot of digit d; bit 24: the digit's child is split
+           // next level, so its records' next key byte goes to nd
             const int d = threadIdx.x;
             uint32_t run = lstart;
 #pragma unroll
             for (int w = 0; w < W; ++w) {
-                s_wcnt[w][d] = run;
+                s_wcnt[w][d] = run | big;
                 run += wc[w];
             }
         }
         s_gdelta[threadIdx.x] = uint32_t(my_base) - lstart;
-        if (nd) {  // children the next level splits: their records' next key byte goes to nd
-            const uint64_t sb = seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x];
-            const uint64_t se = threadIdx.x + 1 < kRadix ? seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x + 1]
-                                                         : ti.seg_size;
-            s_big[threadIdx.x] = (se - sb > cap_local) ? (1u << 24) : 0u;
-        }
         if constexpr (kPeer)
             s_pdst[threadIdx.x] = dig_dst[threadIdx.x] -
                                   (ti.seg_start + seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x]) * RS;
@@ -263,8 +265,8 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
         for (int j = 0; j < IT; ++j) {
             const uint32_t d = pk[j] & 0x1FFu;
             if (d < 256u) {
-                const uint32_t slot = s_wcnt[warp][d] + (pk[j] >> 9);
-                s_map[slot] = (uint32_t(warp * IT + j) * 32u + lane) | (d << 16) | (nd ? s_big[d] : 0u);
+                const uint32_t sw = s_wcnt[warp][d] + (pk[j] >> 9);
+                s_map[sw & 0xFFFFFFu] = (uint32_t(warp * IT + j) * 32u + lane) | (d << 16) | (sw & (1u << 24));
             }
         }
         bar_sync_named(1, T);
