@@ -198,8 +198,7 @@ __device__ __forceinline__ void local_group(
     __shared__ uint32_t s_scan[65];
     __shared__ uint32_t s_and[W][2 * KW], s_or[W][2 * KW];
     __shared__ uint32_t s_Lw[W][32];  // per-warp copy of the varying key bytes
-    __shared__ uint32_t s_flag, s_maxb, s_wmin, s_wmax, s_B;
-    __shared__ uint32_t s_mul;
+    __shared__ uint32_t s_flag, s_maxb, s_wmin, s_wmax;
     __shared__ __align__(8) unsigned long long s_bar;
 
     const uint32_t n = g.size;
@@ -386,19 +385,17 @@ __device__ __forceinline__ void local_group(
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {  // bucket geometry (one 64-bit division per group)
-        uint32_t B = 33u - __clz(n - 1);  // ceil(log2 n) + 1: ~0.5 records per bucket
-        B = B < 1 ? 1 : (B > uint32_t(C::kBucketBits) ? uint32_t(C::kBucketBits) : B);
-        const uint32_t nbk = 1u << B;
-        const uint64_t range1 = uint64_t(s_wmax - s_wmin) + 1;
-        s_B = B;
-        // range1 > nbk: the multiplier fits 32 bits, bucket = umulhi(w - wmin, mul)
-        s_mul = range1 <= nbk ? 0u : uint32_t(((unsigned long long)nbk << 32) / range1);
-    }
-    __syncthreads();
-    const uint32_t nbk = 1u << s_B;
+    // bucket geometry, computed by every thread (no serial step, no barrier):
+    // 2^B buckets spread linearly over [wmin, wmax] by bucket = umulhi(w - wmin,
+    // mul). Any mul keeps buckets monotone in w; mul <= nbk 2^32 / range
+    // (rounded down with a 1e-6 margin over the float error) keeps them < nbk.
+    uint32_t B = 33u - __clz(n - 1);  // ceil(log2 n) + 1: ~0.5 records per bucket
+    B = B < 1 ? 1 : (B > uint32_t(C::kBucketBits) ? uint32_t(C::kBucketBits) : B);
+    const uint32_t nbk = 1u << B;
     const uint32_t wmin = s_wmin;
-    const uint32_t mul = s_mul;
+    const uint32_t rm1 = s_wmax - wmin;  // range - 1
+    const uint32_t mul =
+        rm1 < nbk ? 0u : uint32_t(__fdiv_rz(float(nbk) * 4294967296.0f, float(rm1) + 1.0f) * 0.999999f);
     auto bucket_of = [&](uint32_t w) -> uint32_t {  // monotone in w, < nbk
         const uint32_t d = w - wmin;
         return mul ? __umulhi(d, mul) : d;

@@ -29,6 +29,9 @@
 
 namespace rg {
 
+#ifndef RG_SC_NDSMEM
+#define RG_SC_NDSMEM 1
+#endif
 #ifndef RG_SC_STAGES
 #define RG_SC_STAGES 2
 #endif
@@ -45,6 +48,14 @@ struct ScatterCfg {
     static constexpr int kCtas = RG_SC_CTAS;      // resident per SM (grid = kCtas x SMs)
     static constexpr int kBufBytes = ((kTile * RS + 16 + 127) / 128) * 128;  // + alignment slack
     static constexpr size_t kSmem = size_t(kStages) * kBufBytes + size_t(kTile) * 4;  // ring + slot map
+    // plain split (no map): + the tile's digit bytes per stage, u16 slot map
+    static constexpr int kNdBytes = ((kTile + 32 + 15) / 16) * 16;
+    // (32-B records only: their record byte reads are 8-way bank-conflicted;
+    // measured a loss at 8/16/24 B, where the u16 map's digit re-extraction
+    // and the second bulk copy cost more than the 2-4-way conflicts saved)
+    static constexpr bool kNdSmem = RG_SC_NDSMEM && RS == 32;
+    static constexpr size_t kSmemPlain = kNdSmem ? size_t(kStages) * (kBufBytes + kNdBytes) + size_t(kTile) * 2
+                                                 : kSmem;
 };
 
 // Exclusive scan of one u32 per thread over the 256 consumer threads (named
@@ -99,6 +110,8 @@ struct TileInfo {
     uint64_t gstart;  // first record of the tile (global record index)
     uint64_t seg_start;
     uint64_t seg_size;
+    uint32_t ndh;  // offset of the tile's first digit byte in its stage's digit buffer (nd_in)
+    uint32_t pad;
 };
 
 // kPeer (the multi-GPU partition): digit d is a destination
@@ -114,14 +127,22 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
     uint32_t n_tiles, unsigned int* __restrict__ ticket, uint32_t ks = 0,
     const uint8_t* __restrict__ map = nullptr,
     const unsigned long long* __restrict__ dig_dst = nullptr, uint8_t* __restrict__ nd = nullptr,
-    uint32_t cap_local = 0) {
+    uint32_t cap_local = 0, const uint8_t* __restrict__ nd_in = nullptr) {
     using C = ScatterCfg<RS>;
     constexpr int T = C::kThreads, IT = C::kItems, W = C::kWarps;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* buf0 = smem;
     constexpr int S = C::kStages;
-    // slot map: record index | digit << 16, in digit order
+    // Plain split: the digits can come TMA-loaded from nd_in (this level's
+    // digit array) into a per-stage byte buffer — conflict-free byte reads
+    // instead of 4-way bank-conflicted reads of the records — and the slot
+    // map is u16 (record index | nd flag << 15; step 4 re-reads the digit from
+    // the record it loads anyway).
+    constexpr bool kU16 = !kMap && C::kNdSmem;
+    uint8_t* snd = smem + S * C::kBufBytes;  // [S][kNdBytes] (kU16)
+    // slot map: record index | digit << 16 | nd flag << 24, in digit order (u32), or (kU16) u16
     uint32_t* s_map = reinterpret_cast<uint32_t*>(smem + S * C::kBufBytes);
+    uint16_t* s_map16 = reinterpret_cast<uint16_t*>(smem + S * (C::kBufBytes + C::kNdBytes));
     __shared__ uint32_t s_wcnt[W][kRadix];  // per-warp digit counts, then tile-local slot starts
     // destination of slot 0 of each digit, relative to the segment start (segments hold < 2^32 records)
     __shared__ uint32_t s_gdelta[kRadix];
@@ -188,10 +209,18 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
             if (tail)
                 *reinterpret_cast<uint2*>(sb + hb + body) =
                     *reinterpret_cast<const uint2*>(gsrc + hb + body);
+            uint32_t ndb = 0;
+            uint64_t nda = 0;
+            if (kU16 && nd_in) {  // the tile's digit bytes, 16-B aligned around [gstart, gstart + tn)
+                nda = ti.gstart & ~uint64_t(15);
+                ndb = uint32_t(((ti.gstart + ti.tn + 15) & ~uint64_t(15)) - nda);
+                ti.ndh = uint32_t(ti.gstart - nda);
+            }
             fence_proxy_async_smem();
             s_info[b] = ti;
-            mbar_arrive_expect_tx(&s_full[b], body);
+            mbar_arrive_expect_tx(&s_full[b], body + ndb);
             if (body) tma_load_1d(sb + hb, gsrc + hb, body, &s_full[b]);
+            if (ndb) tma_load_1d(snd + b * C::kNdBytes, nd_in + nda, ndb, &s_full[b]);
         }
     }
 
@@ -222,12 +251,14 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
         // hardware serves conflicting lanes of one atomic in lane order (the
         // byte-exact stable-sort parity tests check this on the device).
         uint32_t pk[IT];  // digit | rank << 9 ; 0x100 = invalid
+        const uint8_t* sdig = snd + b * C::kNdBytes + ti.ndh;
+        const bool dig_nd = kU16 && nd_in != nullptr;
 #pragma unroll
         for (int j = 0; j < IT; ++j) {
             const uint32_t i = uint32_t(warp * IT + j) * 32u + lane;
             const bool valid = i < tn;
-            const uint32_t d =
-                valid ? scatter_digit_smem<RS, kMap>(tile + size_t(i) * RS, p, ks, map) : 0u;
+            uint32_t d = 0;
+            if (valid) d = dig_nd ? uint32_t(sdig[i]) : scatter_digit_smem<RS, kMap>(tile + size_t(i) * RS, p, ks, map);
             pk[j] = valid ? (d | (atomicAdd(&s_wcnt[warp][d], 1u) << 9)) : 0x100u;
         }
         bar_sync_named(1, T);
@@ -266,7 +297,9 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
             const uint32_t d = pk[j] & 0x1FFu;
             if (d < 256u) {
                 const uint32_t sw = s_wcnt[warp][d] + (pk[j] >> 9);
-                s_map[sw & 0xFFFFFFu] = (uint32_t(warp * IT + j) * 32u + lane) | (d << 16) | (sw & (1u << 24));
+                const uint32_t idx = uint32_t(warp * IT + j) * 32u + lane;
+                if constexpr (kU16) s_map16[sw & 0xFFFFFFu] = uint16_t(idx | ((sw >> 9) & 0x8000u));
+                else s_map[sw & 0xFFFFFFu] = idx | (d << 16) | (sw & (1u << 24));
             }
         }
         bar_sync_named(1, T);
@@ -278,9 +311,18 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
         for (int j = 0; j < IT; ++j) {
             const uint32_t slot = uint32_t(j) * T + threadIdx.x;
             if (slot < tn) {
-                const uint32_t m = s_map[slot];
-                const Rec<RS> v = ld_smem_rec<RS>(tile, m & 0xFFFFu);
-                const uint32_t d = (m >> 16) & 0xFFu;
+                uint32_t m, d;
+                Rec<RS> v;
+                if constexpr (kU16) {
+                    const uint32_t m16 = s_map16[slot];
+                    v = ld_smem_rec<RS>(tile, m16 & 0x7FFFu);
+                    d = rec_byte<RS>(v, p);
+                    m = m16 << 9;  // nd flag -> bit 24
+                } else {
+                    m = s_map[slot];
+                    v = ld_smem_rec<RS>(tile, m & 0xFFFFu);
+                    d = (m >> 16) & 0xFFu;
+                }
                 if constexpr (kPeer) {
                     store_rec<RS>(reinterpret_cast<uint8_t*>(s_pdst[d] + ti.seg_start * RS), uint32_t(s_gdelta[d] + slot), v);
                 } else {

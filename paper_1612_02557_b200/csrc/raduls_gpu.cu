@@ -402,7 +402,7 @@ void set_attrs(Workspace& ws) {
     RG_CHECK(cudaFuncSetAttribute(k_tile_hist<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(HistCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(ScatterCfg<RS>::kSmem)));
+                                  int(ScatterCfg<RS>::kSmemPlain)));
     RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(ScatterCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -419,16 +419,17 @@ int sm_count() {
 
 // Tile histogram + segmented look-back scan of one level: per-tile digit
 // offsets (ws.tile_off), per-segment digit totals (ws.seg_tot[cur]).
-// side: byte p of every record of the level is in ws.nd (written by the
-// previous level's scatter), so the histogram reads one byte per record.
+// nd_in: byte p of every record of the level, by record position (written
+// by the previous level's scatter), so the histogram reads one byte per record.
 template <int RS, bool kMap = false>
 void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t ntiles, LevelCounters* c,
-                  cudaStream_t st, uint32_t ks = 0, const uint8_t* map = nullptr, bool side = false) {
+                  cudaStream_t st, uint32_t ks = 0, const uint8_t* map = nullptr,
+                  const uint8_t* nd_in = nullptr) {
     constexpr int TILE = ScatterCfg<RS>::kTile;
     int pe = ws.prof.begin(K_HIST, st);
-    if (side) {
+    if (nd_in) {
         const uint32_t grid = std::min<uint32_t>((ntiles + kNdWarps - 1) / kNdWarps, uint32_t(sm_count()) * 4);
-        k_tile_hist_nd<TILE><<<grid, kNdWarps * 32, 0, st>>>(ws.nd.p, ws.segs[cur].p, ws.tile_seg[cur].p,
+        k_tile_hist_nd<TILE><<<grid, kNdWarps * 32, 0, st>>>(nd_in, ws.segs[cur].p, ws.tile_seg[cur].p,
                                                              ws.tile_cnt.p, c, ntiles);
     } else if constexpr (RS == 8) {  // one CTA per tile (see k_tile_hist_reg)
         k_tile_hist_reg<RS, TILE, kMap><<<ntiles, HistRegCfg<RS, TILE>::kThreads, 0, st>>>(
@@ -453,12 +454,14 @@ void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t 
 template <int RS, bool kMap, bool kPeer = false>
 void launch_scatter(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t ntiles, uint32_t ks,
                     const uint8_t* map, LevelCounters* c, cudaStream_t st,
-                    const unsigned long long* dig_dst = nullptr, uint8_t* nd = nullptr) {
+                    const unsigned long long* dig_dst = nullptr, uint8_t* nd = nullptr,
+                    const uint8_t* nd_in = nullptr) {
     const uint32_t grid = std::min<uint32_t>(ntiles, uint32_t(sm_count()) * 2);
     const int pe = ws.prof.begin(K_SCATTER, st);
-    k_scatter<RS, kMap, kPeer><<<grid, ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>::kSmem, st>>>(
+    const size_t smem = (kMap || kPeer) ? ScatterCfg<RS>::kSmem : ScatterCfg<RS>::kSmemPlain;
+    k_scatter<RS, kMap, kPeer><<<grid, ScatterCfg<RS>::kThreads + 32, smem, st>>>(
         data, tmp, ws.segs[cur].p, ws.seg_tot[cur].p, ws.tile_seg[cur].p, ws.tile_off.p, ntiles,
-        &c->scatter_ticket, ks, map, dig_dst, nd, local_cap<RS>());
+        &c->scatter_ticket, ks, map, dig_dst, nd, local_cap<RS>(), nd_in);
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
 }
@@ -510,20 +513,23 @@ void read_counters_and_finish(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32
     RG_CHECK(cudaStreamSynchronize(st));
 }
 
-// The digit array for a sort of n records (grown on demand, +16 B for the
-// histogram's vector over-read). false if it cannot be allocated or
+// The digit arrays of a sort of n records, `stride` bytes apart: one, or two
+// when the scatter also reads its digits from them (it then writes the next
+// level's into the other); grown on demand, +16 B for the 16-B aligned
+// vector / TMA over-reads. 0 if they cannot be allocated or
 // RADULS_GPU_NO_DIGIT_ARRAY is set.
-bool digit_array(Workspace& ws, uint64_t n) {
-    if (std::getenv("RADULS_GPU_NO_DIGIT_ARRAY")) return false;
-    if (ws.nd.cap >= n + 16) return true;
+size_t digit_arrays(Workspace& ws, uint64_t n, int halves) {
+    if (std::getenv("RADULS_GPU_NO_DIGIT_ARRAY")) return 0;
+    const size_t stride = (size_t(n) + 16 + 255) & ~size_t(255);
+    if (ws.nd.cap >= halves * stride) return stride;
     ws.nd.release();
-    if (cudaMalloc(&ws.nd.p, n + 16) != cudaSuccess) {
+    if (cudaMalloc(&ws.nd.p, halves * stride) != cudaSuccess) {
         cudaGetLastError();  // not sticky: clear it
         ws.nd.p = nullptr;
-        return false;
+        return 0;
     }
-    ws.nd.cap = n + 16;
-    return true;
+    ws.nd.cap = halves * stride;
+    return stride;
 }
 
 template <int RS>
@@ -588,11 +594,14 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
     level0_counts();
     uint32_t nseg = 1, ntiles = nt0, level = 0;
     const Caps caps = caps_for<RS>(n);
-    bool side = false;  // this level's histogram came from the digit array
-    // Digit array: the scatter writes the next key byte of every record whose
-    // child is split again, so the next histogram reads 1 byte, not rs. Best
-    // effort: without the n extra bytes every level reads whole records.
-    const bool nd_ok = digit_array(ws, n);
+    // Digit arrays: the scatter writes the next key byte of every record whose
+    // child is split again, so the next level's histogram reads 1 byte, not
+    // rs, and its scatter takes its digits from there too. Best effort:
+    // without the 2n extra bytes every level reads whole records.
+    constexpr int nd_halves = ScatterCfg<RS>::kNdSmem ? 2 : 1;
+    const size_t nd_stride = digit_arrays(ws, n, nd_halves);
+    const uint8_t* nd_in = nullptr;  // this level's digits (null: read from the records)
+    int nd_half = 0;
     while (true) {
         if (level >= uint32_t(kMaxLevels)) throw CudaError{RADULS_GPU_EINTERNAL};
         LevelCounters* c = dctr + level;
@@ -609,7 +618,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         A.ks = ks;
         A.tile = TILE;
         A.cap_local = local_cap<RS>();
-        A.side = side ? 1u : 0u;
+        A.side = nd_in ? 1u : 0u;
         pe = ws.prof.begin(K_PLAN, st);
         k_plan<<<nseg, 256, 0, st>>>(A);
         RG_LAUNCH_CHECK();
@@ -631,10 +640,11 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         // the next level reads its digits from nd iff every one of its
         // segments comes out of this level's scatter (none re-queued at a
         // later byte without a split)
-        const bool side_next = nd_ok && h.n_next && !h.n_skip;
+        uint8_t* nd_out =
+            (nd_stride && h.n_next && !h.n_skip) ? ws.nd.p + (nd_halves == 2 ? nd_half : 0) * nd_stride : nullptr;
         if (h.n_scatter_segs) {
-            launch_scatter<RS, false>(ws, data, tmp, cur, ntiles, ks, nullptr, c, st, nullptr,
-                                      side_next ? ws.nd.p : nullptr);
+            launch_scatter<RS, false>(ws, data, tmp, cur, ntiles, ks, nullptr, c, st, nullptr, nd_out,
+                                      nd_halves == 2 ? nd_in : nullptr);
             stats.scatter_launches++;
         }
         launch_local<RS>(ws, data, tmp, h.n_groups, ks, c, st);
@@ -653,8 +663,9 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         nseg = h.n_next;
         ntiles = h.n_next_tiles;
         RG_CHECK(cudaMemsetAsync(dctr + level, 0, sizeof(LevelCounters), st));
-        side = side_next;
-        level_counts<RS>(ws, data, tmp, cur, ntiles, dctr + level, st, ks, nullptr, side);
+        nd_in = nd_out;
+        nd_half ^= 1;
+        level_counts<RS>(ws, data, tmp, cur, ntiles, dctr + level, st, ks, nullptr, nd_in);
     }
     read_counters_and_finish<RS>(ws, data, tmp, ks, dctr, level, st);
     ws.prof.collect();
