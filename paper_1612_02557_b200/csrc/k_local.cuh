@@ -56,7 +56,8 @@ struct LocalCfg {
     static constexpr size_t kSmem = size_t(kRecBytes) + size_t(kCap) * (4 + 2 + 2) + kCntBytes;
 };
 
-// Block-wide exclusive scan (blockDim a multiple of 32, <= 1024).
+// Block-wide exclusive scan (blockDim a multiple of 32, <= 1024): one
+// barrier; every warp then adds up the totals of the warps before it itself.
 template <bool kTrailingSync = true>
 __device__ __forceinline__ uint32_t block_scan_excl(uint32_t v, uint32_t* s_w, uint32_t* total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -69,22 +70,12 @@ __device__ __forceinline__ uint32_t block_scan_excl(uint32_t v, uint32_t* s_w, u
     }
     if (lane == 31) s_w[warp] = x;
     __syncthreads();
-    if (warp == 0) {
-        const uint32_t w = lane < nw ? s_w[lane] : 0u;
-        uint32_t z = w;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, z, off);
-            if (lane >= off) z += y;
-        }
-        s_w[32 + lane] = z - w;
-        if (lane == 31) s_w[64] = z;
-    }
-    __syncthreads();
-    const uint32_t r = s_w[32 + warp] + x - v;
-    *total = s_w[64];
+    // lane q holds warp q's total; the warp's base is the sum over q < warp
+    const uint32_t t = lane < nw ? s_w[lane] : 0u;
+    const uint32_t base = __reduce_add_sync(0xFFFFFFFFu, lane < warp ? t : 0u);
+    *total = __reduce_add_sync(0xFFFFFFFFu, t);
     if (kTrailingSync) __syncthreads();  // s_w may be reused
-    return r;
+    return base + x - v;
 }
 
 // Stable LSD pass for W warps (T = 32 W threads, T % 256 == 0): pout <- pin
@@ -198,7 +189,7 @@ __device__ __forceinline__ void local_group(
     __shared__ uint32_t s_scan[65];
     __shared__ uint32_t s_and[W][2 * KW], s_or[W][2 * KW];
     __shared__ uint32_t s_Lw[W][32];  // per-warp copy of the varying key bytes
-    __shared__ uint32_t s_flag, s_maxb, s_wmin, s_wmax;
+    __shared__ uint32_t s_flag, s_maxb, s_wmin, s_wmax, s_wmin2, s_wmax2;
     __shared__ __align__(8) unsigned long long s_bar;
 
     const uint32_t n = g.size;
@@ -241,6 +232,8 @@ __device__ __forceinline__ void local_group(
     if (threadIdx.x == 0) {
         s_wmin = 0xFFFFFFFFu;
         s_wmax = 0u;
+        s_wmin2 = 0xFFFFFFFFu;
+        s_wmax2 = 0u;
         s_flag = 0;
         s_maxb = 0;
     }
@@ -303,6 +296,14 @@ __device__ __forceinline__ void local_group(
             s_and[warp][lane] = av;
             s_or[warp][lane] = ov;
         }
+        if (spec) {  // the default windows' range, complete at the barrier below
+            smn = __reduce_min_sync(0xFFFFFFFFu, smn);
+            smx = __reduce_max_sync(0xFFFFFFFFu, smx);
+            if (lane == 0) {
+                atomicMin(&s_wmin, smn);
+                atomicMax(&s_wmax, smx);
+            }
+        }
     }
     __syncthreads();
     // every warp derives the varying bytes itself (no second block barrier)
@@ -339,14 +340,8 @@ __device__ __forceinline__ void local_group(
 
     // ---- 3. windows (registers + shared memory), their range
     // windows / buckets kept in registers when records are not (register budget)
-    if (spec_ok) {  // computed by the AND/OR pass
-        smn = __reduce_min_sync(0xFFFFFFFFu, smn);
-        smx = __reduce_max_sync(0xFFFFFFFFu, smx);
-        if (lane == 0) {
-            atomicMin(&s_wmin, smn);
-            atomicMax(&s_wmax, smx);
-        }
-    } else {
+    // spec_ok: windows and range came with the AND/OR pass (no barrier here)
+    if (!spec_ok) {
         const uint32_t L0 = s_L[0], L1 = s_L[nwin > 1 ? 1 : 0], L2 = s_L[nwin > 2 ? 2 : 0],
                        L3 = s_L[nwin > 3 ? 3 : 0];
         const WindowSel ws = make_window_sel(s_L, nwin, RS / 4, RS == 8);
@@ -380,11 +375,11 @@ __device__ __forceinline__ void local_group(
         mn = __reduce_min_sync(0xFFFFFFFFu, mn);
         mx = __reduce_max_sync(0xFFFFFFFFu, mx);
         if (lane == 0) {
-            atomicMin(&s_wmin, mn);
-            atomicMax(&s_wmax, mx);
+            atomicMin(&s_wmin2, mn);
+            atomicMax(&s_wmax2, mx);
         }
+        __syncthreads();
     }
-    __syncthreads();
     // bucket geometry, computed by every thread (no serial step, no barrier):
     // 2^B buckets spread linearly over [wmin, wmax] by bucket = umulhi(w - wmin,
     // mul). Any mul keeps buckets monotone in w; mul <= nbk 2^32 / range
@@ -392,8 +387,8 @@ __device__ __forceinline__ void local_group(
     uint32_t B = 33u - __clz(n - 1);  // ceil(log2 n) + 1: ~0.5 records per bucket
     B = B < 1 ? 1 : (B > uint32_t(C::kBucketBits) ? uint32_t(C::kBucketBits) : B);
     const uint32_t nbk = 1u << B;
-    const uint32_t wmin = s_wmin;
-    const uint32_t rm1 = s_wmax - wmin;  // range - 1
+    const uint32_t wmin = spec_ok ? s_wmin : s_wmin2;
+    const uint32_t rm1 = (spec_ok ? s_wmax : s_wmax2) - wmin;  // range - 1
     const uint32_t mul =
         rm1 < nbk ? 0u : uint32_t(__fdiv_rz(float(nbk) * 4294967296.0f, float(rm1) + 1.0f) * 0.999999f);
     auto bucket_of = [&](uint32_t w) -> uint32_t {  // monotone in w, < nbk
