@@ -190,6 +190,7 @@ __device__ __forceinline__ void local_group(
     __shared__ uint32_t s_and[W][2 * KW], s_or[W][2 * KW];
     __shared__ uint32_t s_Lw[W][32];  // per-warp copy of the varying key bytes
     __shared__ uint32_t s_flag, s_maxb, s_wmin, s_wmax, s_wmin2, s_wmax2;
+    __shared__ uint32_t s_wq[W];  // per-warp deferred-record list lengths
     __shared__ __align__(8) unsigned long long s_bar;
 
     const uint32_t n = g.size;
@@ -235,6 +236,7 @@ __device__ __forceinline__ void local_group(
         s_wmin2 = 0xFFFFFFFFu;
         s_wmax2 = 0u;
         s_flag = 0;
+        for (int q = 0; q < W; ++q) s_wq[q] = 0;
         s_maxb = 0;
     }
     // bucket counters zeroed now (first used by the histogram, several barriers on)
@@ -310,13 +312,17 @@ __device__ __forceinline__ void local_group(
     uint32_t* s_L = s_Lw[warp];
     uint32_t nL;
     {
+        // lane q < W holds warp q's partials; REDUX combines them per word
         const uint32_t b = lane;  // key byte b lives in 32-bit word b/4
-        uint32_t diffb = 0;
-        if (b >= g.p && b < ks && b < uint32_t(RS)) {
-            uint32_t ra = ~0u, ro = 0u;
-            for (int q = 0; q < W; ++q) ra &= s_and[q][b >> 2], ro |= s_or[q][b >> 2];
-            diffb = ((ra ^ ro) >> ((b & 3) * 8)) & 0xFFu;
+        uint32_t dsel = 0;
+#pragma unroll
+        for (int w = 0; w < 2 * KW; ++w) {
+            const uint32_t ra = __reduce_and_sync(0xFFFFFFFFu, lane < W ? s_and[lane][w] : ~0u);
+            const uint32_t ro = __reduce_or_sync(0xFFFFFFFFu, lane < W ? s_or[lane][w] : 0u);
+            if ((b >> 2) == uint32_t(w)) dsel = ra ^ ro;
         }
+        uint32_t diffb = 0;
+        if (b >= g.p && b < ks && b < uint32_t(RS)) diffb = (dsel >> ((b & 3) * 8)) & 0xFFu;
         const uint32_t vm = __ballot_sync(0xFFFFFFFFu, diffb != 0);
         if (diffb) s_L[__popc(vm & lanemask_lt())] = lane;
         nL = __popc(vm);
@@ -533,8 +539,11 @@ __device__ __forceinline__ void local_group(
             }
             return rank;
         };
-        uint16_t* lst = reinterpret_cast<uint16_t*>(s_tot);  // up to 1024 deferred records (s_tot: 512 u32)
-        // s_flag (the list length) is still 0 from the start
+        // records of buckets over 3 go to a per-warp list (s_tot: 1024 u16 split
+        // over the warps), ranked densely by the same warp after its loop — no
+        // block barrier between the two; s_wq (the lengths) are 0 from the start
+        constexpr uint32_t kWq = 1024 / W;
+        uint16_t* lst = reinterpret_cast<uint16_t*>(s_tot) + warp * kWq;
         // Buckets of <= 3 records (nearly all): branch-free, so the unrolled
         // loop overlaps the shared-memory loads of all the thread's records; the
         // bucket's slots are read clamped (a slot equal to e counts nothing).
@@ -582,16 +591,16 @@ __device__ __forceinline__ void local_group(
                     if (beyond && tie) rank = rank_slow(e, w, st, en);
                     place(e, st + rank);
                 } else {
-                    const uint32_t i = atomicAdd(&s_flag, 1u);
-                    if (i < 1024u) lst[i] = uint16_t(e);
+                    const uint32_t i = atomicAdd(&s_wq[warp], 1u);
+                    if (i < kWq) lst[i] = uint16_t(e);
                     else place(e, st + rank_slow(e, w, st, en));  // list full: rank inline
                 }
             }
         }
-        __syncthreads();
+        __syncwarp();
         {
-            const uint32_t nl = min(s_flag, 1024u);
-            for (uint32_t i = threadIdx.x; i < nl; i += T) {
+            const uint32_t nl = min(s_wq[warp], kWq);
+            for (uint32_t i = lane; i < nl; i += 32) {
                 const uint32_t e = lst[i];
                 const uint32_t w = win[e];
                 const uint32_t bb = bucket_of(w);
