@@ -218,7 +218,9 @@ int raduls_gpu_sort_multi(int n_dev, const int* devices, void* const* d_in, cons
                           void* const* d_out, uint64_t* n_out, uint64_t out_capacity_recs,
                           uint32_t rec_size, uint32_t key_size);
 
-/* Release the cached per-device workspace (optional). */
+/* Release the cached per-device workspace (optional): level metadata (~0.7 B
+ * per record) and the digit array(s) (1 B per record, 2 B at rec_size 32)
+ * that a sort grows on demand and keeps for the next call. */
 void raduls_gpu_release(void);
 
 #ifdef __cplusplus

@@ -1398,6 +1398,7 @@ void raduls_gpu_release(void) {
         }
         w->tile_cnt.release(); w->tile_off.release(); w->status.release(); w->groups.release(); w->spill.release(); w->n_spill.release();
         w->copies.release(); w->host_data.release(); w->host_tmp.release(); w->map8.release(); w->dig_dst.release();
+        w->nd.release();
         delete w->stager;
         if (w->h_ctr) cudaFreeHost(w->h_ctr);
         if (w->h_small) cudaFreeHost(w->h_small);
