@@ -190,6 +190,33 @@ int raduls_gpu_partition_to(const void* d_src, uint64_t n_recs, uint32_t rec_siz
                             const uint64_t* h_dst, uint64_t* h_rank_counts, void* stream);
 
 /*
+ * The same partition in two phases, so that a multi-GPU plan can exchange the
+ * exact per-destination counts before any record moves (the bucket map can
+ * then come from a sample):
+ *   raduls_gpu_partition_plan: per-destination record counts (h_rank_counts,
+ *     n_ranks entries) of the stable partition by d_bucket_rank[16-bit prefix
+ *     at prefix_byte], and the AND/OR of every record word (h_andor, 8 u64:
+ *     and at 2w, or at 2w+1), in one read of d_src; the per-tile offsets stay
+ *     in the calling thread's device workspace;
+ *   raduls_gpu_partition_store: the stores of that plan (same d_src, n, layout),
+ *     rank r's records to the byte address h_dst[r] (as raduls_gpu_partition_to).
+ * Any other call of this library on the device in between invalidates the
+ * plan (store then returns RADULS_GPU_EINVAL). Synchronous.
+ * raduls_gpu_sample_andor / raduls_gpu_sample_prefix_histogram: AND/OR (to
+ * the host) and the 16-bit prefix histogram (accumulated into d_hist, 65536
+ * u64) of a strided sample of `samples` records — inputs for the bucket map.
+ */
+int raduls_gpu_partition_plan(const void* d_src, uint64_t n_recs, uint32_t rec_size, uint32_t key_size,
+                              uint32_t prefix_byte, const uint32_t* d_bucket_rank, uint32_t n_ranks,
+                              uint64_t* h_rank_counts, uint64_t* h_andor, void* stream);
+int raduls_gpu_partition_store(const void* d_src, uint64_t n_recs, uint32_t rec_size, uint32_t key_size,
+                               const uint64_t* h_dst, void* stream);
+int raduls_gpu_sample_andor(const void* d_data, uint64_t n_recs, uint32_t rec_size, uint32_t samples,
+                            uint64_t* h_andor, void* stream);
+int raduls_gpu_sample_prefix_histogram(const void* d_data, uint64_t n_recs, uint32_t rec_size, uint32_t key_size,
+                                       uint32_t prefix_byte, uint32_t samples, uint64_t* d_hist, void* stream);
+
+/*
  * CUDA IPC for the multi-process exchange: raduls_gpu_ipc_alloc allocates
  * device memory and returns its 64-byte IPC handle; a peer process maps it
  * with raduls_gpu_ipc_open (lazy peer access) and unmaps with

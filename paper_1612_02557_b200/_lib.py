@@ -38,6 +38,10 @@ EXPORTED = [
     "raduls_gpu_andor",
     "raduls_gpu_sort_multi",
     "raduls_gpu_partition_to",
+    "raduls_gpu_partition_plan",
+    "raduls_gpu_partition_store",
+    "raduls_gpu_sample_andor",
+    "raduls_gpu_sample_prefix_histogram",
     "raduls_gpu_ipc_alloc",
     "raduls_gpu_ipc_open",
     "raduls_gpu_ipc_close",
@@ -113,6 +117,10 @@ def load(build_if_missing: bool = False):
         L.raduls_gpu_set_profiling.argtypes = [C.c_int]
         L.raduls_gpu_andor.argtypes = [_vp, _u64, _u32, _u64p, _vp]
         L.raduls_gpu_partition_to.argtypes = [_vp, _u64, _u32, _u32, _u32, _vp, _u32, _u64p, _u64p, _vp]
+        L.raduls_gpu_partition_plan.argtypes = [_vp, _u64, _u32, _u32, _u32, _vp, _u32, _u64p, _u64p, _vp]
+        L.raduls_gpu_partition_store.argtypes = [_vp, _u64, _u32, _u32, _u64p, _vp]
+        L.raduls_gpu_sample_andor.argtypes = [_vp, _u64, _u32, _u32, _u64p, _vp]
+        L.raduls_gpu_sample_prefix_histogram.argtypes = [_vp, _u64, _u32, _u32, _u32, _u32, _vp, _vp]
         L.raduls_gpu_ipc_alloc.argtypes = [_u64, C.POINTER(_vp), C.c_char_p]
         L.raduls_gpu_ipc_open.argtypes = [C.c_char_p, C.POINTER(_vp)]
         L.raduls_gpu_ipc_close.argtypes = [_vp]

@@ -106,7 +106,8 @@ __global__ void __launch_bounds__(256) k_andor(const uint8_t* __restrict__ data,
 // inside the segment = tile - segs[s].tile_base). tile_cnt: [ntiles][256]
 // u16. seg_andor: [nseg][8] u64 (and at 2w, or at 2w+1), pre-initialised.
 // kMap: the digit is the destination rank of the record's 16-bit key prefix
-// at bytes (p, p+1) through a 65536-entry map (multi-GPU partition).
+// at bytes (p, p+1) through a 65536-entry map (multi-GPU partition); the
+// AND/OR is computed there too (the multi-GPU plan verifies its prefix byte).
 //
 // Persistent and warp-specialised like k_scatter: a producer warp takes tiles
 // round-robin and TMA-loads them (cp.async.bulk + mbarrier) into a 2-stage
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(HistCfg<RS>::kThreads + 64, HistCfg<RS>::kCtas
             o.z = (y.x & 0xFFFFu) | (y.y << 16);
             o.w = (y.z & 0xFFFFu) | (y.w << 16);
             *reinterpret_cast<uint4*>(tile_cnt + uint64_t(ti.tile) * kRadix + lane * 8) = o;
-            if (!kMap && lane < KW) {
+            if (lane < KW) {  // (kMap too: the multi-GPU plan checks its prefix byte with it)
                 unsigned long long ra = ~0ull, ro = 0ull;
                 for (int q = 0; q < W; ++q) ra &= s_and[b][q][lane], ro |= s_or[b][q][lane];
                 atomicAnd(&seg_andor[uint64_t(ti.seg) * 8 + 2 * lane], ra);
@@ -279,14 +280,14 @@ __global__ void __launch_bounds__(HistCfg<RS>::kThreads + 64, HistCfg<RS>::kCtas
                     const uint32_t lo = p + 1 < ks ? rec_byte<RS>(r, p + 1) : 0u;
                     atomicAdd(&hb[__ldg(map + ((hi << 8) | lo))], 1u);
                 }
-                continue;
+            } else {
+                const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
+                const uint32_t word = rec_word32<RS>(r, p >> 2);
+                const uint32_t wa = __reduce_and_sync(0xFFFFFFFFu, valid ? word : ~0u);
+                const uint32_t wo = __reduce_or_sync(0xFFFFFFFFu, valid ? word : 0u);
+                const uint32_t shf = (p & 3u) * 8u;
+                warp_hist_add(hb, (word >> shf) & 0xFFu, valid, wa, wo, shf, nvalid);
             }
-            const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
-            const uint32_t word = rec_word32<RS>(r, p >> 2);
-            const uint32_t wa = __reduce_and_sync(0xFFFFFFFFu, valid ? word : ~0u);
-            const uint32_t wo = __reduce_or_sync(0xFFFFFFFFu, valid ? word : 0u);
-            const uint32_t shf = (p & 3u) * 8u;
-            warp_hist_add(hb, (word >> shf) & 0xFFu, valid, wa, wo, shf, nvalid);
             if (valid) {
 #pragma unroll
                 for (int w = 0; w < KW; ++w) {
@@ -296,15 +297,13 @@ __global__ void __launch_bounds__(HistCfg<RS>::kThreads + 64, HistCfg<RS>::kCtas
                 }
             }
         }
-        if constexpr (!kMap) {
 #pragma unroll
-            for (int w = 0; w < KW; ++w) {
-                for (int off = 16; off; off >>= 1) {
-                    a[w] &= __shfl_xor_sync(0xFFFFFFFFu, a[w], off);
-                    o[w] |= __shfl_xor_sync(0xFFFFFFFFu, o[w], off);
-                }
-                if (lane == 0) s_and[b][warp][w] = a[w], s_or[b][warp][w] = o[w];
+        for (int w = 0; w < KW; ++w) {
+            for (int off = 16; off; off >>= 1) {
+                a[w] &= __shfl_xor_sync(0xFFFFFFFFu, a[w], off);
+                o[w] |= __shfl_xor_sync(0xFFFFFFFFu, o[w], off);
             }
+            if (lane == 0) s_and[b][warp][w] = a[w], s_or[b][warp][w] = o[w];
         }
         __syncwarp();  // the warp's counts and partials before its arrival
         if (lane == 0) mbar_arrive(&s_done[b]);
@@ -383,14 +382,14 @@ __global__ void __launch_bounds__(HistRegCfg<RS, kTile>::kThreads) k_tile_hist_r
                 const uint32_t lo = p + 1 < ks ? rec_byte<RS>(r[j], p + 1) : 0u;
                 atomicAdd(&sh[__ldg(map + ((hi << 8) | lo))], 1u);
             }
-            continue;
+        } else {
+            const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
+            const uint32_t word = rec_word32<RS>(r[j], p >> 2);
+            const uint32_t wa = __reduce_and_sync(0xFFFFFFFFu, valid ? word : ~0u);
+            const uint32_t wo = __reduce_or_sync(0xFFFFFFFFu, valid ? word : 0u);
+            const uint32_t shf = (p & 3u) * 8u;
+            warp_hist_add(sh, (word >> shf) & 0xFFu, valid, wa, wo, shf, nvalid);
         }
-        const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
-        const uint32_t word = rec_word32<RS>(r[j], p >> 2);
-        const uint32_t wa = __reduce_and_sync(0xFFFFFFFFu, valid ? word : ~0u);
-        const uint32_t wo = __reduce_or_sync(0xFFFFFFFFu, valid ? word : 0u);
-        const uint32_t shf = (p & 3u) * 8u;
-        warp_hist_add(sh, (word >> shf) & 0xFFu, valid, wa, wo, shf, nvalid);
         if (valid) {
 #pragma unroll
             for (int w = 0; w < KW; ++w) {
@@ -401,18 +400,16 @@ __global__ void __launch_bounds__(HistRegCfg<RS, kTile>::kThreads) k_tile_hist_r
         }
     }
     const int warp = threadIdx.x >> 5;
-    if constexpr (!kMap) {
 #pragma unroll
-        for (int w = 0; w < KW; ++w) {
-            for (int off = 16; off; off >>= 1) {
-                a[w] &= __shfl_xor_sync(0xFFFFFFFFu, a[w], off);
-                o[w] |= __shfl_xor_sync(0xFFFFFFFFu, o[w], off);
-            }
-            if (lane_id() == 0) s_and[warp][w] = a[w], s_or[warp][w] = o[w];
+    for (int w = 0; w < KW; ++w) {
+        for (int off = 16; off; off >>= 1) {
+            a[w] &= __shfl_xor_sync(0xFFFFFFFFu, a[w], off);
+            o[w] |= __shfl_xor_sync(0xFFFFFFFFu, o[w], off);
         }
+        if (lane_id() == 0) s_and[warp][w] = a[w], s_or[warp][w] = o[w];
     }
     __syncthreads();
-    if (!kMap && threadIdx.x < KW) {
+    if (threadIdx.x < KW) {
         unsigned long long ra = ~0ull, ro = 0ull;
         for (int q = 0; q < HW; ++q) ra &= s_and[q][threadIdx.x], ro |= s_or[q][threadIdx.x];
         atomicAnd(&seg_andor[uint64_t(s) * 8 + 2 * threadIdx.x], ra);

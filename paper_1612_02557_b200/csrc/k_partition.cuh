@@ -34,6 +34,25 @@ __global__ void __launch_bounds__(256) k_prefix_hist(const uint8_t* __restrict__
     }
 }
 
+// k_prefix_hist over a strided sample of `samples` records (record
+// min(n - 1, s * stride)): the multi-GPU plan's bucket map only needs to be
+// balanced, not exact (the exact per-rank counts come from the partition's
+// own tile histogram).
+template <int RS>
+__global__ void __launch_bounds__(256) k_sample_prefix_hist(const uint8_t* __restrict__ data, uint64_t n,
+                                                            uint64_t stride, uint32_t samples, uint32_t ks,
+                                                            uint32_t pb, unsigned long long* __restrict__ hist) {
+    for (uint32_t base = blockIdx.x * blockDim.x; base < samples; base += gridDim.x * blockDim.x) {
+        const uint32_t s = base + threadIdx.x;
+        const bool valid = s < samples;
+        const uint32_t b = valid ? prefix16<RS>(load_rec<RS>(data, min(n - 1, uint64_t(s) * stride)), pb, ks)
+                                 : 0x10000u;
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, b);
+        if (valid && (threadIdx.x & 31) == uint32_t(__ffs(peers) - 1))
+            atomicAdd(&hist[b], (unsigned long long)__popc(peers));
+    }
+}
+
 __global__ void k_map_to_u8(const uint32_t* __restrict__ in, uint8_t* __restrict__ out,
                             uint32_t n_ranks, unsigned int* __restrict__ bad) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;

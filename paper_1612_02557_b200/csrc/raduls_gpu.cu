@@ -305,6 +305,14 @@ struct Workspace {
     unsigned long long* h_small = nullptr;  // pinned scratch [4096]
     raduls_gpu_stats last{};
     bool attrs_set[33] = {};
+    // raduls_gpu_partition_plan -> raduls_gpu_partition_store hand-over
+    struct PartPlan {
+        bool pending = false;
+        const void* src = nullptr;
+        uint64_t n = 0;
+        uint32_t rs = 0, ks = 0;
+        unsigned long long tot[256] = {};
+    } part;
 
     Workspace() {
         RG_CHECK(cudaMallocHost(&h_ctr, sizeof(LevelCounters) * kMaxLevels));
@@ -539,6 +547,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
     raduls_gpu_stats stats{};
     ws.last = stats;
     ws.prof.reset();
+    ws.part.pending = false;
     if (n < 2) return;  // msd_sorter.hpp:51
     set_attrs<RS>(ws);
     ensure_caps<RS>(ws, n);
@@ -987,6 +996,7 @@ template <int RS, bool kMap>
 void single_segment_counts(Workspace& ws, uint8_t* src, uint64_t n, uint32_t p, uint32_t ks,
                            const uint8_t* map, unsigned long long* h_tot, cudaStream_t st) {
     constexpr int TILE = ScatterCfg<RS>::kTile;
+    ws.part.pending = false;
     ensure_caps<RS>(ws, n);
     set_attrs<RS>(ws);
     Seg s0{0, n, p, 0, 0, 0};
@@ -1302,6 +1312,119 @@ int raduls_gpu_partition_to(const void* d_src, uint64_t n, uint32_t rs, uint32_t
             if (h_rank_counts) std::memcpy(h_rank_counts, tot, n_ranks * sizeof(uint64_t));
             single_segment_scatter<RSC, true, true>(ws, src, nullptr, n, ks, ws.map8.p, tot, st, ws.dig_dst.p);
         });
+    });
+}
+
+// Load the bucket -> rank map (u8) and check it; false when an entry is >= n_ranks.
+static bool load_rank_map(Workspace& ws, const uint32_t* d_bucket_rank, uint32_t n_ranks, cudaStream_t st) {
+    ws.map8.ensure(65536);
+    RG_CHECK(cudaMemsetAsync(ws.acc.p, 0, sizeof(unsigned long long), st));
+    k_map_to_u8<<<256, 256, 0, st>>>(d_bucket_rank, ws.map8.p, n_ranks, reinterpret_cast<unsigned int*>(ws.acc.p));
+    RG_LAUNCH_CHECK();
+    RG_CHECK(cudaMemcpyAsync(ws.h_small + 2048, ws.acc.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    RG_CHECK(cudaStreamSynchronize(st));
+    return uint32_t(ws.h_small[2048]) == 0;
+}
+
+int raduls_gpu_partition_plan(const void* d_src, uint64_t n, uint32_t rs, uint32_t ks, uint32_t prefix_byte,
+                              const uint32_t* d_bucket_rank, uint32_t n_ranks, uint64_t* h_rank_counts,
+                              uint64_t* h_andor, void* stream) {
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs) || n_ranks < 1 || n_ranks > 256 || !d_bucket_rank ||
+        !h_rank_counts || !h_andor || n > kMaxRecords)
+        return RADULS_GPU_EINVAL;
+    if (n && !aligned_ok(d_src, rs)) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        ws.part.pending = false;
+        std::memset(h_rank_counts, 0, n_ranks * sizeof(uint64_t));
+        for (int w = 0; w < 8; ++w) h_andor[w] = (w & 1) ? 0ull : ~0ull;
+        if (!load_rank_map(ws, d_bucket_rank, n_ranks, st)) throw CudaError{RADULS_GPU_EINVAL};
+        if (!n) return;
+        dispatch_rs(rs, [&](auto R) {
+            constexpr int RSC = decltype(R)::value;
+            uint8_t* src = const_cast<uint8_t*>(static_cast<const uint8_t*>(d_src));
+            single_segment_counts<RSC, true>(ws, src, n, prefix_byte, ks, ws.map8.p, ws.part.tot, st);
+        });
+        RG_CHECK(cudaMemcpyAsync(ws.h_small + 2048, ws.seg_andor[0].p, 8 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, st));
+        RG_CHECK(cudaStreamSynchronize(st));
+        std::memcpy(h_andor, ws.h_small + 2048, 8 * sizeof(uint64_t));
+        std::memcpy(h_rank_counts, ws.part.tot, n_ranks * sizeof(uint64_t));
+        ws.part.pending = true;
+        ws.part.src = d_src;
+        ws.part.n = n;
+        ws.part.rs = rs;
+        ws.part.ks = ks;
+    });
+}
+
+int raduls_gpu_partition_store(const void* d_src, uint64_t n, uint32_t rs, uint32_t ks, const uint64_t* h_dst,
+                               void* stream) {
+    if (!layout_ok(rs, ks) || !h_dst) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (!n) return;
+        if (!ws.part.pending || ws.part.src != d_src || ws.part.n != n || ws.part.rs != rs || ws.part.ks != ks)
+            throw CudaError{RADULS_GPU_EINVAL};  // no matching plan on this device
+        ws.part.pending = false;
+        ws.dig_dst.ensure(kRadix);
+        unsigned long long* hd = ws.h_small + 3072;  // pinned staging for the destinations
+        for (uint32_t r = 0; r < kRadix; ++r) {
+            hd[r] = ws.part.tot[r] ? h_dst[r] : 0ull;  // ranks without records: never dereferenced
+            if (hd[r] % (rs % 16 == 0 ? 16 : 8)) throw CudaError{RADULS_GPU_EINVAL};
+        }
+        RG_CHECK(cudaMemcpyAsync(ws.dig_dst.p, hd, kRadix * sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+        dispatch_rs(rs, [&](auto R) {
+            constexpr int RSC = decltype(R)::value;
+            uint8_t* src = const_cast<uint8_t*>(static_cast<const uint8_t*>(d_src));
+            single_segment_scatter<RSC, true, true>(ws, src, nullptr, n, ks, ws.map8.p, ws.part.tot, st,
+                                                    ws.dig_dst.p);
+        });
+    });
+}
+
+int raduls_gpu_sample_andor(const void* d_data, uint64_t n, uint32_t rs, uint32_t samples, uint64_t* h_andor,
+                            void* stream) {
+    if (!layout_ok(rs, rs) || mul_overflows(n, rs) || !h_andor) return RADULS_GPU_EINVAL;
+    if (n && !aligned_ok(d_data, rs)) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        k_init_andor<<<1, 64, 0, st>>>(ws.andor0.p, 1);
+        RG_LAUNCH_CHECK();
+        const uint32_t sm = uint32_t(std::min<uint64_t>(n, std::max<uint32_t>(samples, 1)));
+        if (n) {
+            dispatch_rs(rs, [&](auto R) {
+                k_sample_andor<decltype(R)::value><<<64, 256, 0, st>>>(
+                    static_cast<const uint8_t*>(d_data), n, std::max<uint64_t>(1, n / sm), sm, ws.andor0.p);
+            });
+            RG_LAUNCH_CHECK();
+        }
+        RG_CHECK(cudaMemcpyAsync(ws.h_small, ws.andor0.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        RG_CHECK(cudaStreamSynchronize(st));
+        std::memcpy(h_andor, ws.h_small, 8 * sizeof(uint64_t));
+    });
+}
+
+int raduls_gpu_sample_prefix_histogram(const void* d_data, uint64_t n, uint32_t rs, uint32_t ks,
+                                       uint32_t prefix_byte, uint32_t samples, uint64_t* d_hist, void* stream) {
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs) || !d_hist) return RADULS_GPU_EINVAL;
+    if (n && !aligned_ok(d_data, rs)) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (!n || !samples) return;
+        const uint32_t sm = uint32_t(std::min<uint64_t>(n, samples));
+        dispatch_rs(rs, [&](auto R) {
+            k_sample_prefix_hist<decltype(R)::value><<<grid_for(sm, 256, 4), 256, 0, st>>>(
+                static_cast<const uint8_t*>(d_data), n, std::max<uint64_t>(1, n / sm), sm, ks, prefix_byte,
+                reinterpret_cast<unsigned long long*>(d_hist));
+        });
+        RG_LAUNCH_CHECK();
     });
 }
 

@@ -5,21 +5,30 @@ std::thread workers); MSD bins are independent once the top-prefix partition
 is fixed (children tile the parent, P/include/raduls/kernels.hpp:82-94), so
 the sort shards with ONE exchange step:
 
- 1. AND/OR of the local key words on the device, all-gathered -> the global
-    first varying key byte p0 (constant leading bytes — C3's three zero bytes
-    — are skipped, (e));
- 2. 65 536-bucket histogram of the 16-bit prefix at key bytes (p0, p0+1) on
-    the device, all-gathered: every rank learns the global counts;
+ 1. AND/OR of the local key words, all-gathered -> the global first varying
+    key byte p0 (constant leading bytes — C3's three zero bytes — are
+    skipped, (e));
+ 2. 65 536-bucket histogram of the 16-bit prefix at key bytes (p0, p0+1),
+    all-gathered: every rank learns the global distribution;
  3. bucket -> rank map: contiguous bucket ranges balanced by record count
     (a bucket is never split, so equal keys stay on one rank);
  4. stable local partition into per-destination send ranges on the device
-    (raduls_gpu_partition: the same tile histogram / look-back scan / scatter
-    kernels as an MSD level);
+    (the same tile histogram / look-back scan / scatter kernels as an MSD
+    level);
  5. the exchange: by default the partition kernel itself stores every
     destination's records into that rank's receive window over NVLink (CUDA
-    IPC mappings; raduls_gpu_partition_to), so partition and all-to-all are
-    one kernel; or a local partition plus one NCCL all-to-all;
+    IPC mappings), so partition and all-to-all are one kernel; or a local
+    partition plus one NCCL all-to-all;
  6. each rank sorts what it received (raduls_gpu_sort).
+
+On the default (NVLink window) path, steps 1-2 read strided samples only
+(plan_exchange_sampled): the map only has to be balanced. The exact
+per-destination counts (for the window offsets) and the exact AND/OR (to
+confirm p0) come from the partition's own tile histogram
+(raduls_gpu_partition_plan) and are all-gathered before the stores
+(raduls_gpu_partition_store), so the data is read twice before the local
+sort (histogram + stores) instead of four times. A byte that varies only off
+the sample makes every rank re-plan exactly (plan_exchange).
 
 Rank r ends up holding the r-th contiguous key range, sorted; the concatenation
 over ranks is the sorted whole. The collective plumbing is torch.distributed;
@@ -133,6 +142,40 @@ class DeviceOps:
                "raduls_gpu_partition_to")
         return counts
 
+    def sample_andor(self, data, n: int, layout: RecordLayout, samples: int) -> np.ndarray:
+        out = np.zeros(8, dtype=np.uint64)
+        _raise(self.L.raduls_gpu_sample_andor(data.data_ptr(), n, layout.record_size, samples,
+                                              out.ctypes.data_as(_lib._u64p), self.stream()),
+               "raduls_gpu_sample_andor")
+        return out
+
+    def sample_prefix_hist(self, data, n: int, layout: RecordLayout, p0: int, samples: int):
+        h = self.torch.zeros(NBUCKETS, dtype=self.torch.int64, device=self.device)
+        _raise(self.L.raduls_gpu_sample_prefix_histogram(data.data_ptr(), n, layout.record_size,
+                                                         layout.key_size, p0, samples, h.data_ptr(),
+                                                         self.stream()),
+               "raduls_gpu_sample_prefix_histogram")
+        return h
+
+    def partition_plan(self, data, n: int, layout: RecordLayout, p0: int, bucket_rank: np.ndarray,
+                       world: int):
+        """Exact per-destination counts and the AND/OR of every record word
+        (one read); the stores follow in partition_store."""
+        dmap = self.torch.from_numpy(bucket_rank.astype(np.int32)).to(self.device)
+        counts = np.zeros(world, dtype=np.uint64)
+        andor = np.zeros(8, dtype=np.uint64)
+        _raise(self.L.raduls_gpu_partition_plan(data.data_ptr(), n, layout.record_size, layout.key_size,
+                                                p0, dmap.data_ptr(), world,
+                                                counts.ctypes.data_as(_lib._u64p),
+                                                andor.ctypes.data_as(_lib._u64p), self.stream()),
+               "raduls_gpu_partition_plan")
+        return counts, andor
+
+    def partition_store(self, data, n: int, layout: RecordLayout, dst: np.ndarray) -> None:
+        _raise(self.L.raduls_gpu_partition_store(data.data_ptr(), n, layout.record_size, layout.key_size,
+                                                 dst.ctypes.data_as(_lib._u64p), self.stream()),
+               "raduls_gpu_partition_store")
+
     def sort(self, data, n: int, layout: RecordLayout, tmp=None) -> None:
         _raise(self.L.raduls_gpu_sort(data.data_ptr(), tmp.data_ptr() if tmp is not None else None,
                                       n, layout.record_size, layout.key_size, self.stream()),
@@ -169,6 +212,60 @@ def plan_exchange(ops, data, n: int, layout: RecordLayout, group=None) -> Exchan
         src_dst[r] = np.bincount(bucket_rank, weights=hist[r].astype(np.float64),
                                  minlength=world).astype(np.uint64)
     return ExchangePlan(p0, bucket_rank, src_dst[rank].copy(), src_dst[:, rank].copy(), src_dst)
+
+
+SAMPLE_ANDOR = 1 << 16
+SAMPLE_HIST = 1 << 20
+
+
+def plan_exchange_sampled(ops, data, n: int, layout: RecordLayout, group=None):
+    """The exchange plan without a full read of the data before the
+    partition: the prefix byte and the bucket map come from strided samples
+    (the map only has to be balanced), and the exact send/receive counts plus
+    the exact AND/OR come from the partition's own tile histogram
+    (ops.partition_plan), all-gathered. Returns (plan, ok): ok is False on
+    every rank when the exact AND/OR shows a more significant varying byte
+    than the sample's (a byte that varies only off-sample); the caller then
+    plans exactly (plan_exchange)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    ks = layout.key_size
+    dev = data.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    # 1. sampled AND/OR -> the guessed first varying key byte
+    ao = torch.from_numpy(ops.sample_andor(data, n, layout, SAMPLE_ANDOR).view(np.int64)).to(dev)
+    all_ao = [torch.empty_like(ao) for _ in range(world)]
+    dist.all_gather(all_ao, ao, group=group)
+    p0 = first_varying_byte(np.stack([t.cpu().numpy().view(np.uint64) for t in all_ao]), ks)
+    if p0 >= ks:
+        p0 = 0
+    # 2. sampled 16-bit prefix histograms, each weighted by its rank's record count
+    h = ops.sample_prefix_hist(data, n, layout, p0, SAMPLE_HIST).to(dev)
+    all_h = [torch.empty_like(h) for _ in range(world)]
+    dist.all_gather(all_h, h, group=group)
+    nn = torch.tensor([n], dtype=torch.int64, device=dev)
+    all_n = [torch.empty_like(nn) for _ in range(world)]
+    dist.all_gather(all_n, nn, group=group)
+    weights = np.zeros(NBUCKETS, dtype=np.float64)
+    for t, tn in zip(all_h, all_n):
+        hr = t.cpu().numpy().astype(np.float64)
+        s_r = hr.sum()
+        if s_r > 0:
+            weights += hr * (float(tn.item()) / s_r)
+    bucket_rank = balanced_bucket_map(weights, world)
+    # 3. exact counts and AND/OR from the partition's histogram, all-gathered
+    counts, andor = ops.partition_plan(data, n, layout, p0, bucket_rank, world)
+    row = torch.from_numpy(np.concatenate([counts, andor]).view(np.int64)).to(dev)
+    rows = [torch.empty_like(row) for _ in range(world)]
+    dist.all_gather(rows, row, group=group)
+    m = np.stack([t.cpu().numpy().view(np.uint64) for t in rows])  # [world, world + 8]
+    src_dst = m[:, :world].copy()
+    p_exact = first_varying_byte(m[:, world:], ks)
+    if p_exact >= ks:
+        p_exact = 0
+    plan = ExchangePlan(p0, bucket_rank, src_dst[rank].copy(), src_dst[:, rank].copy(), src_dst)
+    return plan, p_exact == p0
 
 
 class _CudaBytes:
@@ -276,7 +373,13 @@ def sort_distributed(data, n: int, layout: RecordLayout, ops=None, group=None,
     rank = dist.get_rank(group)
     rs = layout.record_size
     t0 = time.perf_counter()
-    plan = plan_exchange(ops, data, n, layout, group)
+    planned = False  # the partition's counts pass already ran (ops.partition_plan)
+    if exchange == "p2p":
+        plan, planned = plan_exchange_sampled(ops, data, n, layout, group)
+        if not planned:  # a key byte varies only off the sample: plan exactly
+            plan = plan_exchange(ops, data, n, layout, group)
+    else:
+        plan = plan_exchange(ops, data, n, layout, group)
     win = None
     if exchange == "p2p":
         win = _peer_windows(max(int(plan.matrix.sum(axis=0).max()), 1) * rs, group, data.device)
@@ -287,9 +390,12 @@ def sort_distributed(data, n: int, layout: RecordLayout, ops=None, group=None,
                        dtype=np.uint64)
         torch.cuda.synchronize(data.device)
         dist.barrier(group=group)  # every window free (previous results consumed)
-        counts = ops.partition_to(data, n, layout, plan.p0, plan.bucket_rank, world, dst)
-        if not np.array_equal(counts, plan.send_counts):
-            raise RuntimeError("partition counts disagree with the exchanged histograms")
+        if planned:
+            ops.partition_store(data, n, layout, dst)
+        else:
+            counts = ops.partition_to(data, n, layout, plan.p0, plan.bucket_rank, world, dst)
+            if not np.array_equal(counts, plan.send_counts):
+                raise RuntimeError("partition counts disagree with the exchanged histograms")
         dist.barrier(group=group)  # every rank's stores into every window are complete
         t2 = time.perf_counter()
         recv = torch.as_tensor(_CudaBytes(win.own, max(n_out, 1) * rs), device=data.device)

@@ -99,3 +99,23 @@ def test_sort_multi_rejects_bad_arguments_without_gpu():
     assert L.raduls_gpu_sort_multi(0, *args, 16, 8) == _lib.EINVAL      # no devices
     assert L.raduls_gpu_sort_multi(1, *args, 12, 8) == _lib.EINVAL      # layout
     assert L.raduls_gpu_sort_multi(1, *args, 16, 8) == _lib.EINVAL      # null output
+
+
+def test_partition_phases_and_samples_reject_bad_arguments_without_gpu():
+    """raduls_gpu_partition_plan / _store and the sample entry points validate
+    before touching a device (include/raduls_gpu.h)."""
+    L = _lib.load()
+    cnt = np.zeros(2, dtype=np.uint64)
+    ao = np.zeros(8, dtype=np.uint64)
+    cp, ap = cnt.ctypes.data_as(_lib._u64p), ao.ctypes.data_as(_lib._u64p)
+    assert L.raduls_gpu_partition_plan(None, 10, 12, 8, 0, 16, 2, cp, ap, None) == _lib.EINVAL  # layout
+    assert L.raduls_gpu_partition_plan(None, 10, 16, 8, 0, None, 2, cp, ap, None) == _lib.EINVAL  # no map
+    assert L.raduls_gpu_partition_plan(None, 10, 16, 8, 0, 16, 0, cp, ap, None) == _lib.EINVAL  # 0 ranks
+    assert L.raduls_gpu_partition_plan(None, 10, 16, 8, 0, 16, 2, None, ap, None) == _lib.EINVAL
+    assert L.raduls_gpu_partition_plan(8, 10, 16, 8, 0, 16, 2, cp, ap, None) == _lib.EINVAL  # misaligned
+    assert L.raduls_gpu_partition_store(None, 10, 12, 8, cp, None) == _lib.EINVAL
+    assert L.raduls_gpu_partition_store(None, 10, 16, 8, None, None) == _lib.EINVAL
+    assert L.raduls_gpu_sample_andor(None, 10, 12, 64, ap, None) == _lib.EINVAL
+    assert L.raduls_gpu_sample_andor(None, 10, 16, 64, None, None) == _lib.EINVAL
+    assert L.raduls_gpu_sample_prefix_histogram(None, 10, 16, 17, 0, 64, 16, None) == _lib.EINVAL
+    assert L.raduls_gpu_sample_prefix_histogram(8, 10, 16, 8, 0, 64, 16, None) == _lib.EINVAL

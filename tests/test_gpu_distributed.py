@@ -23,7 +23,7 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, cfg, outdir):
+def _worker(rank, world, port, cfg, outdir, poke=False):
     import torch
     import torch.distributed as dist
 
@@ -40,6 +40,11 @@ def _worker(rank, world, port, cfg, outdir):
         n_local = n_total - base
     for step in range(2):  # the second step reuses the cached windows
         data = rg.generate(n_local, lay, dist=dist_kind, seed=seed, index_base=base)
+        if poke and rank == world - 1:
+            # key byte 0 varies in one record only, past the strided AND/OR
+            # sample: the sampled plan's prefix byte is wrong, the exact
+            # AND/OR from the partition's histogram catches it (exact re-plan)
+            data[(n_local - 1) * rs] = 1
         np.save(os.path.join(outdir, f"in{rank}.npy"), data.cpu().numpy())
         out, n_out = sort_distributed(data, n_local, lay, exchange="p2p")
         torch.cuda.synchronize()
@@ -68,4 +73,21 @@ def test_distributed_p2p_exchange_matches_oracle(torch_cuda, tmp_path, world, cf
     for step in range(2):
         got = np.concatenate([np.load(tmp_path / f"out{r}_{step}.npy") for r in range(world)])
         assert got.size == n_total * rs
+        assert np.array_equal(got, want), f"step {step}"
+
+
+def test_distributed_p2p_sample_misses_a_varying_byte(torch_cuda, tmp_path):
+    import torch.multiprocessing as mp
+
+    import oracle
+    world, cfg = 2, (250_000, 16, 8, 1, 0x5EED0003)  # bytes 0-2 constant except the poked record
+    port = _free_port()
+    mp.start_processes(_worker, args=(world, port, cfg, str(tmp_path), True), nprocs=world,
+                       join=True, start_method="spawn")
+    n_total, rs, ks, _, _ = cfg
+    inputs = np.concatenate([np.load(tmp_path / f"in{r}.npy") for r in range(world)])
+    assert inputs.reshape(-1, rs)[:, 0].max() == 1
+    want = oracle.stable_sort(inputs, rs, ks)
+    for step in range(2):
+        got = np.concatenate([np.load(tmp_path / f"out{r}_{step}.npy") for r in range(world)])
         assert np.array_equal(got, want), f"step {step}"

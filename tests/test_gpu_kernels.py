@@ -139,3 +139,73 @@ def test_partition_to_equals_partition(rg, torch_cuda, rs, ks):
         c = int(c)
         assert np.array_equal(from_dev(o)[:c * rs], r[off * rs:(off + c) * rs])
         off += c
+
+
+@pytest.mark.parametrize("rs,ks", [(16, 8), (8, 8), (24, 16), (32, 24)])
+def test_partition_plan_store_equals_partition(rg, torch_cuda, rs, ks):
+    """raduls_gpu_partition_plan + raduls_gpu_partition_store (the two-phase
+    fused partition of the sampled multi-GPU plan): same counts and same
+    per-rank ranges as the ordinary partition; the plan's AND/OR is the
+    array's; any other call in between invalidates the plan."""
+    from paper_1612_02557_b200 import _lib
+    from helpers import make_input, to_dev, from_dev
+    L = _lib.load()
+    n, ranks = 100_003, 3
+    a = make_input(n, rs, ks, 41 + rs, universe=(0 if rs != 8 else 5000))
+    d = to_dev(torch_cuda, a)
+    bmap = (np.arange(65536, dtype=np.uint32) * ranks // 65536).astype(np.uint32)
+    dmap = torch_cuda.from_numpy(bmap.view(np.int32)).cuda()
+    ref = torch_cuda.empty_like(d)
+    counts = np.zeros(ranks, dtype=np.uint64)
+    assert L.raduls_gpu_partition(d.data_ptr(), ref.data_ptr(), n, rs, ks, 0, dmap.data_ptr(), ranks,
+                                  counts.ctypes.data_as(_lib._u64p), None) == 0
+    got = np.zeros(ranks, dtype=np.uint64)
+    ao = np.zeros(8, dtype=np.uint64)
+    assert L.raduls_gpu_partition_plan(d.data_ptr(), n, rs, ks, 0, dmap.data_ptr(), ranks,
+                                       got.ctypes.data_as(_lib._u64p), ao.ctypes.data_as(_lib._u64p),
+                                       None) == 0
+    assert list(got) == list(counts)
+    w = a.reshape(n, rs).view("<u8")
+    for k in range(rs // 8):
+        assert ao[2 * k] == np.bitwise_and.reduce(w[:, k]) and ao[2 * k + 1] == np.bitwise_or.reduce(w[:, k])
+    outs = [torch_cuda.empty(int(c) * rs + 64, dtype=torch_cuda.uint8, device="cuda") for c in counts]
+    dst = np.array([o.data_ptr() for o in outs], dtype=np.uint64)
+    assert L.raduls_gpu_partition_store(d.data_ptr(), n, rs, ks, dst.ctypes.data_as(_lib._u64p), None) == 0
+    torch_cuda.cuda.synchronize()
+    r = from_dev(ref)
+    off = 0
+    for o, c in zip(outs, counts):
+        c = int(c)
+        assert np.array_equal(from_dev(o)[:c * rs], r[off * rs:(off + c) * rs])
+        off += c
+    # a second store of the same plan, or one after another call, is refused
+    assert L.raduls_gpu_partition_store(d.data_ptr(), n, rs, ks, dst.ctypes.data_as(_lib._u64p), None) == _lib.EINVAL
+    assert L.raduls_gpu_partition_plan(d.data_ptr(), n, rs, ks, 0, dmap.data_ptr(), ranks,
+                                       got.ctypes.data_as(_lib._u64p), ao.ctypes.data_as(_lib._u64p),
+                                       None) == 0
+    tmp = to_dev(torch_cuda, a)
+    rg.sort(tmp, n, rg.RecordLayout(rs, ks))
+    assert L.raduls_gpu_partition_store(d.data_ptr(), n, rs, ks, dst.ctypes.data_as(_lib._u64p), None) == _lib.EINVAL
+
+
+@pytest.mark.parametrize("rs,ks", [(16, 8), (8, 8), (32, 24)])
+def test_sampled_andor_and_prefix_histogram(rg, torch_cuda, rs, ks):
+    from paper_1612_02557_b200 import _lib
+    from helpers import make_input, to_dev
+    L = _lib.load()
+    n, samples = 300_001, 4096
+    a = make_input(n, rs, ks, 51 + rs)
+    d = to_dev(torch_cuda, a)
+    stride = max(1, n // samples)
+    idx = np.minimum(n - 1, np.arange(samples, dtype=np.int64) * stride)
+    recs = a.reshape(n, rs)[idx]
+    ao = np.zeros(8, dtype=np.uint64)
+    assert L.raduls_gpu_sample_andor(d.data_ptr(), n, rs, samples, ao.ctypes.data_as(_lib._u64p), None) == 0
+    w = recs.view("<u8")
+    for k in range(rs // 8):
+        assert ao[2 * k] == np.bitwise_and.reduce(w[:, k]) and ao[2 * k + 1] == np.bitwise_or.reduce(w[:, k])
+    pb = 1
+    hist = torch_cuda.zeros(65536, dtype=torch_cuda.int64, device="cuda")
+    assert L.raduls_gpu_sample_prefix_histogram(d.data_ptr(), n, rs, ks, pb, samples, hist.data_ptr(), None) == 0
+    pref = (recs[:, pb].astype(np.int64) << 8) | recs[:, pb + 1].astype(np.int64)
+    assert np.array_equal(hist.cpu().numpy(), np.bincount(pref, minlength=65536))
