@@ -42,6 +42,20 @@ __device__ __forceinline__ uint32_t andor_byte_varies(const unsigned long long* 
     return uint32_t((x >> ((b & 7u) * 8u)) & 0xFFull);
 }
 
+// A batch of a level's segments (src, contiguous, with contiguous tiles from
+// tb0 on) as a level of its own: segments renumbered from 0, tile bases from
+// 0, and the tile -> segment map rebuilt. One block per segment.
+__global__ void k_rebase_segs(const Seg* __restrict__ src, uint32_t tb0, Seg* __restrict__ dst,
+                              uint32_t* __restrict__ tile_seg, uint32_t tile) {
+    const uint32_t i = blockIdx.x;
+    Seg g = src[i];
+    g.tile_base -= tb0;
+    g.action = 0;
+    if (threadIdx.x == 0) dst[i] = g;
+    const uint32_t nt = uint32_t((g.size + tile - 1) / tile);
+    for (uint32_t t = threadIdx.x; t < nt; t += blockDim.x) tile_seg[g.tile_base + t] = i;
+}
+
 __global__ void k_init_andor(unsigned long long* andor, uint32_t rows) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < rows * 8) andor[i] = (i & 1) ? 0ull : ~0ull;

@@ -24,7 +24,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <condition_variable>
@@ -47,6 +49,9 @@ namespace {
 using namespace rg;
 
 constexpr int kMaxLevels = 72;
+// Key-range batches of a progressive sort (the host drop-in's overlapped
+// device->host copy): the last batch's copy is the part left unoverlapped.
+constexpr uint32_t kProgressiveBatches = 16;
 // Per-call record limit: per-tile digit offsets are 32-bit (k_tile_scan).
 constexpr uint64_t kMaxRecords = 1ull << 32;
 
@@ -216,13 +221,19 @@ struct HostStager {
         const unsigned hw = std::thread::hardware_concurrency();
         return std::max(1u, std::min(8u, hw ? hw : 1u));
     }
+    cudaStream_t copy = nullptr;  // device->host copies of finished key ranges (progressive sort)
+    cudaEvent_t done = nullptr;
     HostStager() : pool(pool_threads()) {
         for (int i = 0; i < kRing; ++i) {
             RG_CHECK(cudaMallocHost(&stage[i], kChunk));
             RG_CHECK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
         }
+        RG_CHECK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+        RG_CHECK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
     }
     ~HostStager() {
+        if (copy) cudaStreamDestroy(copy);
+        if (done) cudaEventDestroy(done);
         for (int i = 0; i < kRing; ++i) {
             if (stage[i]) cudaFreeHost(stage[i]);
             if (ev[i]) cudaEventDestroy(ev[i]);
@@ -296,6 +307,7 @@ struct Workspace {
     DevBuf<uint8_t> host_data, host_tmp, map8;
     DevBuf<unsigned long long> dig_dst;  // per-destination byte addresses (raduls_gpu_partition_to)
     DevBuf<uint8_t> nd;                  // digit array: next key byte per record position (sort_impl)
+    DevBuf<Seg> bsegs;                   // level-1 segments of a progressive sort
     HostStager* stager = nullptr;  // host drop-ins, created on first use
     HostStager& host_stager() {
         if (!stager) stager = new HostStager();
@@ -394,7 +406,7 @@ void ensure_caps(Workspace& ws, uint64_t n) {
     ws.status.ensure((c.tiles / kScanChunk + 1) * kRadix);
     ws.groups.ensure(c.groups);
     ws.spill.ensure(c.groups);
-    ws.n_spill.ensure(1);
+    ws.n_spill.ensure(2);  // (read back as one 8-B word)
     ws.copies.ensure(c.copies);
 }
 
@@ -505,19 +517,35 @@ void finish_spilled(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ks, Lev
     RG_CHECK(cudaStreamSynchronize(st));
 }
 
+// Device -> pinned-host copy of a few words by a kernel (stores from the SMs
+// over PCIe) instead of a DMA: the level loop's counter read-backs must not
+// queue behind the multi-GB device->host copies the progressive host sort
+// keeps on the copy engine. (Pinned host memory is device-accessible under UVA.)
+__global__ void k_publish(unsigned long long* __restrict__ dst, const unsigned long long* __restrict__ src,
+                          uint32_t words) {
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+}
+static_assert(sizeof(LevelCounters) % 8 == 0, "LevelCounters published as u64 words");
+
+void publish(void* h_dst, const void* d_src, size_t bytes, cudaStream_t st) {
+    k_publish<<<1, 64, 0, st>>>(static_cast<unsigned long long*>(h_dst),
+                                static_cast<const unsigned long long*>(d_src), uint32_t((bytes + 7) / 8));
+    RG_LAUNCH_CHECK();
+}
+
 // The counters of `levels` levels and the spill count in one readback; the
 // spilled groups (rare) get the LSD fallback and the counters are re-read.
 template <int RS>
 void read_counters_and_finish(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ks, LevelCounters* dctr,
                               uint32_t levels, cudaStream_t st) {
     unsigned int* hn = reinterpret_cast<unsigned int*>(ws.h_small + 4001);
-    RG_CHECK(cudaMemcpyAsync(ws.h_ctr, dctr, sizeof(LevelCounters) * levels, cudaMemcpyDeviceToHost, st));
-    RG_CHECK(cudaMemcpyAsync(hn, ws.n_spill.p, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    publish(ws.h_ctr, dctr, sizeof(LevelCounters) * levels, st);
+    publish(hn, ws.n_spill.p, 8, st);  // (n_spill is the low half of an 8-B allocation)
     RG_CHECK(cudaStreamSynchronize(st));
     const unsigned int n = *hn;
     if (!n) return;
     finish_spilled<RS>(ws, data, tmp, ks, dctr, st, n);
-    RG_CHECK(cudaMemcpyAsync(ws.h_ctr, dctr, sizeof(LevelCounters) * levels, cudaMemcpyDeviceToHost, st));
+    publish(ws.h_ctr, dctr, sizeof(LevelCounters) * levels, st);
     RG_CHECK(cudaStreamSynchronize(st));
 }
 
@@ -540,9 +568,14 @@ size_t digit_arrays(Workspace& ws, uint64_t n, int halves) {
     return stride;
 }
 
+// on_final (optional): called with record ranges [begin, end) whose content
+// in `data` is final once the work enqueued on `st` so far completes, in key
+// order, covering [0, n) — the host drop-in overlaps their device->host copy
+// with the rest of the sort. Without it (or when the level-0 split does not
+// qualify) the sort runs level by level over all segments.
 template <int RS>
 void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t ks,
-               cudaStream_t st) {
+               cudaStream_t st, const std::function<void(uint64_t, uint64_t)>* on_final = nullptr) {
     constexpr int TILE = ScatterCfg<RS>::kTile;
     raduls_gpu_stats stats{};
     ws.last = stats;
@@ -601,7 +634,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         RG_LAUNCH_CHECK();
     };
     level0_counts();
-    uint32_t nseg = 1, ntiles = nt0, level = 0;
+    uint32_t nseg = 1, ntiles = nt0;
     const Caps caps = caps_for<RS>(n);
     // Digit arrays: the scatter writes the next key byte of every record whose
     // child is split again, so the next level's histogram reads 1 byte, not
@@ -611,6 +644,12 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
     const size_t nd_stride = digit_arrays(ws, n, nd_halves);
     const uint8_t* nd_in = nullptr;  // this level's digits (null: read from the records)
     int nd_half = 0;
+    // The level loop from `level` on (its counters at dctr + level); returns the
+    // level count reached. stop_after_first: return after this level's
+    // launches with cur / nseg / ntiles / nd_in describing the next level,
+    // before its histogram.
+    uint32_t last_skip = 0;  // n_skip of the last level run
+    auto run_levels = [&](uint32_t level, bool stop_after_first) -> uint32_t {
     while (true) {
         if (level >= uint32_t(kMaxLevels)) throw CudaError{RADULS_GPU_EINTERNAL};
         LevelCounters* c = dctr + level;
@@ -632,9 +671,8 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         k_plan<<<nseg, 256, 0, st>>>(A);
         RG_LAUNCH_CHECK();
         ws.prof.end(pe, st);
-        RG_CHECK(cudaMemcpyAsync(ws.h_ctr + level, c, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
-        if (level == 0)
-            RG_CHECK(cudaMemcpyAsync(ws.h_small + 4000, d_flag, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        publish(ws.h_ctr + level, c, sizeof(LevelCounters), st);
+        if (level == 0) publish(ws.h_small + 4000, d_flag, sizeof(unsigned long long), st);
         RG_CHECK(cudaStreamSynchronize(st));
         if (level == 0 && ws.h_small[4000]) {  // a more significant byte varies off the sample: redo level 0 on it
             Seg s0{0, n, uint32_t(ws.h_small[4000] & 0xFF), 0, 0, 0};
@@ -667,24 +705,96 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         stats.copy_records += h.moved_copy;
         stats.skipped_levels += nseg - h.n_scatter_segs;
         ++level;
+        last_skip = h.n_skip;
         if (!h.n_next) break;
         cur ^= 1;
         nseg = h.n_next;
         ntiles = h.n_next_tiles;
-        RG_CHECK(cudaMemsetAsync(dctr + level, 0, sizeof(LevelCounters), st));
         nd_in = nd_out;
         nd_half ^= 1;
+        if (stop_after_first) break;
+        RG_CHECK(cudaMemsetAsync(dctr + level, 0, sizeof(LevelCounters), st));
         level_counts<RS>(ws, data, tmp, cur, ntiles, dctr + level, st, ks, nullptr, nd_in);
     }
+    return level;
+    };
+    // per-level accounting known only once the level's local sorts ran
+    auto add_level_stats = [&](uint32_t l0, uint32_t l1) {
+        for (uint32_t l = l0; l < l1; ++l) {
+            stats.local_records += ws.h_ctr[l].moved_local;
+            stats.fallback_groups += ws.h_ctr[l].fallback_groups;
+            stats.hist_records += ws.h_ctr[l].hist_records;
+            stats.hist_digit_records += ws.h_ctr[l].hist_digit_records;
+        }
+    };
+    const uint64_t prog_min = [] {
+        const char* e = std::getenv("RADULS_GPU_PROGRESSIVE_BYTES");
+        return e ? std::strtoull(e, nullptr, 10) : (uint64_t(256) << 20);
+    }();
+    if (on_final && n * RS >= prog_min) {
+        // Progressive: level 0 over the whole array, then its children (one
+        // parent: in digit order = key order, tiles in the same order) in
+        // batches of contiguous key ranges, each sorted to the end before the
+        // next starts, so each range is final — and handed to on_final —
+        // while later ranges are still being sorted.
+        uint32_t levels = run_levels(0, true);
+        const bool split = levels == 1 && nseg >= 2 && !last_skip && ws.h_ctr[0].n_scatter_segs == 1;
+        read_counters_and_finish<RS>(ws, data, tmp, ks, dctr, 1, st);
+        add_level_stats(0, 1);
+        RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, sizeof(unsigned int), st));
+        if (!split) {  // nothing to batch (level 0 finished it, or skipped a constant byte)
+            if (nseg && levels == 1 && ws.h_ctr[0].n_next) {
+                RG_CHECK(cudaMemsetAsync(dctr + 1, 0, sizeof(LevelCounters), st));
+                level_counts<RS>(ws, data, tmp, cur, ntiles, dctr + 1, st, ks, nullptr, nd_in);
+                levels = run_levels(1, false);
+                read_counters_and_finish<RS>(ws, data, tmp, ks, dctr, levels, st);
+                add_level_stats(1, levels);
+            }
+            (*on_final)(0, n);
+        } else {
+            std::vector<Seg> hs(nseg);
+            RG_CHECK(cudaMemcpyAsync(hs.data(), ws.segs[cur].p, nseg * sizeof(Seg), cudaMemcpyDeviceToHost, st));
+            ws.bsegs.ensure(nseg);
+            RG_CHECK(cudaMemcpyAsync(ws.bsegs.p, ws.segs[cur].p, nseg * sizeof(Seg), cudaMemcpyDeviceToDevice, st));
+            RG_CHECK(cudaStreamSynchronize(st));
+            const int cur1 = cur;
+            const uint32_t nseg1 = nseg, ntiles1 = ntiles;
+            const uint8_t* nd_in1 = nd_in;
+            const int nd_half1 = nd_half;
+            const uint32_t K = std::min<uint32_t>(nseg1, kProgressiveBatches);
+            for (uint32_t b = 0; b < K; ++b) {
+                const uint32_t s0 = uint32_t(uint64_t(b) * nseg1 / K), s1 = uint32_t(uint64_t(b + 1) * nseg1 / K);
+                const uint32_t tb0 = hs[s0].tile_base, tb1 = b + 1 < K ? hs[s1].tile_base : ntiles1;
+                const uint64_t p0 = b ? hs[s0].start : 0, p1 = b + 1 < K ? hs[s1].start : n;
+                cur = cur1;
+                nseg = s1 - s0;
+                ntiles = tb1 - tb0;
+                nd_in = nd_in1;
+                nd_half = nd_half1;
+                k_rebase_segs<<<nseg, 256, 0, st>>>(ws.bsegs.p + s0, tb0, ws.segs[cur].p, ws.tile_seg[cur].p, TILE);
+                RG_LAUNCH_CHECK();
+                k_init_andor<<<(nseg * 8 + 255) / 256, 256, 0, st>>>(ws.seg_andor[cur].p, nseg);
+                RG_LAUNCH_CHECK();
+                RG_CHECK(cudaMemsetAsync(dctr + 1, 0, sizeof(LevelCounters), st));
+                level_counts<RS>(ws, data, tmp, cur, ntiles, dctr + 1, st, ks, nullptr, nd_in);
+                const uint32_t lv = run_levels(1, false);
+                levels = std::max(levels, lv);
+                read_counters_and_finish<RS>(ws, data, tmp, ks, dctr, lv, st);
+                add_level_stats(1, lv);
+                RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, sizeof(unsigned int), st));
+                (*on_final)(p0, p1);
+            }
+        }
+        ws.prof.collect();
+        stats.levels = levels;
+        ws.last = stats;
+        return;
+    }
+    const uint32_t level = run_levels(0, false);
     read_counters_and_finish<RS>(ws, data, tmp, ks, dctr, level, st);
     ws.prof.collect();
     stats.levels = level;
-    for (uint32_t l = 0; l < level; ++l) {
-        stats.local_records += ws.h_ctr[l].moved_local;
-        stats.fallback_groups += ws.h_ctr[l].fallback_groups;
-        stats.hist_records += ws.h_ctr[l].hist_records;
-        stats.hist_digit_records += ws.h_ctr[l].hist_digit_records;
-    }
+    add_level_stats(0, level);
     ws.last = stats;
 }
 
@@ -969,12 +1079,39 @@ int raduls_gpu_sort_host(uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t rs, u
         ws.host_tmp.ensure(bytes);
         cudaStream_t st = nullptr;
         HostStager& hs = ws.host_stager();
+        const bool timing = std::getenv("RADULS_GPU_HOST_TIMING") != nullptr;
+        auto now = [] { return std::chrono::steady_clock::now(); };
+        const auto t0 = now();
         hs.h2d(ws.host_data.p, data, bytes, st);
+        if (timing) RG_CHECK(cudaStreamSynchronize(st));
+        const auto t1 = now();
+        // pinned buffers: each key range is copied back as soon as it is final
+        // (progressive sort), overlapping the copy with the rest of the sort
+        const bool pinned = HostStager::pinned(data);
+        uint64_t covered = 0;
+        std::function<void(uint64_t, uint64_t)> fin = [&](uint64_t a, uint64_t b) {
+            RG_CHECK(cudaEventRecord(hs.done, st));
+            RG_CHECK(cudaStreamWaitEvent(hs.copy, hs.done, 0));
+            RG_CHECK(cudaMemcpyAsync(data + a * rs, ws.host_data.p + a * rs, (b - a) * rs, cudaMemcpyDeviceToHost,
+                                     hs.copy));
+            covered += b - a;
+        };
         dispatch_rs(rs, [&](auto R) {
-            sort_impl<decltype(R)::value>(ws, ws.host_data.p, ws.host_tmp.p, n, ks, st);
+            sort_impl<decltype(R)::value>(ws, ws.host_data.p, ws.host_tmp.p, n, ks, st, pinned ? &fin : nullptr);
         });
-        hs.d2h(data, ws.host_data.p, bytes, st);
+        const auto t2 = now();
+        if (covered) {  // the sort handed over its ranges (all of them)
+            RG_CHECK(cudaStreamSynchronize(hs.copy));
+            if (covered != n) throw CudaError{RADULS_GPU_EINTERNAL};
+        } else {  // not a progressive sort (small, or pageable buffer): copy back now
+            hs.d2h(data, ws.host_data.p, bytes, st);
+        }
         RG_CHECK(cudaStreamSynchronize(st));
+        if (timing) {
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            std::fprintf(stderr, "raduls_gpu_sort_host: h2d %.1f ms, sort %.1f ms, d2h tail %.1f ms%s\n",
+                         ms(t0, t1), ms(t1, t2), ms(t2, now()), covered ? " (progressive)" : "");
+        }
     });
 }
 
@@ -1521,7 +1658,7 @@ void raduls_gpu_release(void) {
         }
         w->tile_cnt.release(); w->tile_off.release(); w->status.release(); w->groups.release(); w->spill.release(); w->n_spill.release();
         w->copies.release(); w->host_data.release(); w->host_tmp.release(); w->map8.release(); w->dig_dst.release();
-        w->nd.release();
+        w->nd.release(); w->bsegs.release();
         delete w->stager;
         if (w->h_ctr) cudaFreeHost(w->h_ctr);
         if (w->h_small) cudaFreeHost(w->h_small);
