@@ -35,6 +35,12 @@ namespace rg {
 #ifndef RG_SC_STAGES
 #define RG_SC_STAGES 2
 #endif
+#ifndef RG_SC_EARLY8
+#define RG_SC_EARLY8 1
+#endif
+#ifndef RG_SC_EARLY16
+#define RG_SC_EARLY16 0
+#endif
 #ifndef RG_SC_CTAS
 #define RG_SC_CTAS 2
 #endif
@@ -232,14 +238,29 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
         mbar_wait(&s_full[b], (it / S) & 1u);
         const TileInfo ti = s_info[b];
         if (ti.tile >= n_tiles) break;
-        // this thread's digit: base inside the segment + offset of the tile
+        // this thread's digit: base inside the segment + offset of the tile.
+        // kEarly 1 (8-B records): issued now, consumed after the ranking, the
+        // tile offset by cp.async into s_gdelta (free since the last tile's
+        // write-out) so ptxas cannot sink the load past the named barriers.
+        // Measured in one process, interleaved (scripts/ab_interleave.py):
+        // C2 scatter -3%; at 16 B the same change costs +3-7% (C5 77.9 vs
+        // 75.1 ms), so kEarly 0 loads and resolves them here.
+        constexpr int kEarly = RS == 8 ? RG_SC_EARLY8 : RG_SC_EARLY16;
         const unsigned long long my_sb = seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x];
-        const unsigned long long my_base = my_sb + tile_off[uint64_t(ti.tile) * kRadix + threadIdx.x];
-        uint32_t big = 0;
-        if (nd) {
-            const uint64_t se = threadIdx.x + 1 < kRadix ? seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x + 1]
-                                                         : ti.seg_size;
-            big = se - my_sb > cap_local ? (1u << 24) : 0u;
+        uint32_t my_toff = 0, big = 0;
+        uint64_t my_se = 0;
+        if constexpr (kEarly == 1) {
+            cp_async4(&s_gdelta[threadIdx.x], tile_off + uint64_t(ti.tile) * kRadix + threadIdx.x);
+            if (nd)
+                my_se = threadIdx.x + 1 < kRadix ? seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x + 1]
+                                                 : ti.seg_size;
+        } else {
+            my_toff = tile_off[uint64_t(ti.tile) * kRadix + threadIdx.x];
+            if (nd) {
+                const uint64_t se = threadIdx.x + 1 < kRadix ? seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x + 1]
+                                                             : ti.seg_size;
+                big = se - my_sb > cap_local ? (1u << 24) : 0u;
+            }
         }
         const uint8_t* tile = buf0 + b * C::kBufBytes + ti.head;
         const uint32_t tn = ti.tn, p = ti.p;
@@ -264,6 +285,7 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
         bar_sync_named(1, T);
 
         // 2: per-digit tile totals, warp-exclusive offsets, tile-local starts
+        if constexpr (kEarly != 0) big = (nd && my_se - my_sb > cap_local) ? (1u << 24) : 0u;
         uint32_t tcount = 0, wc[W];
         {
             const int d = threadIdx.x;
@@ -285,7 +307,11 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
                 run += wc[w];
             }
         }
-        s_gdelta[threadIdx.x] = uint32_t(my_base) - lstart;
+        if constexpr (kEarly == 1) {
+            cp_async_wait_all();  // this thread's own element
+            my_toff = s_gdelta[threadIdx.x];
+        }
+        s_gdelta[threadIdx.x] = uint32_t(my_sb) + my_toff - lstart;
         if constexpr (kPeer)
             s_pdst[threadIdx.x] = dig_dst[threadIdx.x] -
                                   (ti.seg_start + seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x]) * RS;
