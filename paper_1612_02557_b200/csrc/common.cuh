@@ -162,6 +162,11 @@ struct BoolC {
     static constexpr bool value = B;
 };
 
+template <int V>
+struct IntC {
+    static constexpr int value = V;
+};
+
 struct WindowSel {
     uint32_t q, sel, mask;
     bool fast;
@@ -251,6 +256,59 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+
+// The same with an L2 eviction-priority hint (kHint 0: none; 1: evict_first,
+// for streams read once, so they leave L2 before the scatter's half-written
+// destination lines).
+template <int kHint>
+__device__ __forceinline__ void tma_load_1d_h(void* dst, const void* src, uint32_t bytes,
+                                              unsigned long long* bar) {
+    if constexpr (kHint == 0) {
+        tma_load_1d(dst, src, bytes, bar);
+    } else {
+        uint64_t pol;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                smem_u32(dst)),
+            "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+            : "memory");
+    }
+}
+
+#ifndef RG_HINT_SC
+#define RG_HINT_SC 0
+#endif
+#ifndef RG_HINT_HIST
+#define RG_HINT_HIST 1
+#endif
+#ifndef RG_HINT_SCST
+#define RG_HINT_SCST 2
+#endif
+
+// Record store with an L2 eviction-priority hint (1: evict_first, 2: evict_last).
+template <int RS, int kHint>
+__device__ __forceinline__ void store_rec_h(uint8_t* base, uint64_t idx, const Rec<RS>& r) {
+    if constexpr (kHint == 0 || RS % 16 != 0) {
+        store_rec<RS>(base, idx, r);
+    } else {
+        uint64_t pol;
+        if constexpr (kHint == 1)
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        else
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        uint8_t* p = base + idx * RS;
+#pragma unroll
+        for (int v = 0; v < RS / 16; ++v)
+            asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p + 16 * v),
+                         "r"(r.w[4 * v]), "r"(r.w[4 * v + 1]), "r"(r.w[4 * v + 2]), "r"(r.w[4 * v + 3]),
+                         "l"(pol)
+                         : "memory");
+    }
+}
+#ifndef RG_HINT_LOCAL
+#define RG_HINT_LOCAL 0
+#endif
 
 // Asynchronous global -> shared copy of 8 bytes (LDGSTS, no register round
 // trip); cp_async_wait_all() completes this thread's outstanding copies.

@@ -36,6 +36,10 @@ namespace rg {
 
 constexpr uint32_t kMaxBucket = 32;
 
+#ifndef RG_LOC_KEYW
+#define RG_LOC_KEYW 1
+#endif
+
 template <int RS>
 struct LocalCfg {
     static constexpr bool kRegRecords = RS == 8;  // records in registers (else shared memory)
@@ -228,7 +232,7 @@ __device__ __forceinline__ void local_group(
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(&s_bar, body);
         for (uint32_t o = 0; o < body; o += 32768u)
-            tma_load_1d(smem + head + hb + o, gsrc + hb + o, min(32768u, body - o), &s_bar);
+            tma_load_1d_h<RG_HINT_LOCAL>(smem + head + hb + o, gsrc + hb + o, min(32768u, body - o), &s_bar);
     }
     if (threadIdx.x == 0) {
         s_wmin = 0xFFFFFFFFu;
@@ -260,11 +264,15 @@ __device__ __forceinline__ void local_group(
     const WindowSel wsd = make_window_sel(Ldef, 4, RS / 4, false);
     // (16/24-B records; measured a loss at 32 B, whose kernel is register-bound)
     const bool spec = KEEP && RS <= 24 && g.p + 4 <= ks && g.p + 4 <= uint32_t(RS) && wsd.fast;
+    // only the words holding key bytes (payload words cannot vary the
+    // order): the first half when ks <= rs / 2, e.g. BASELINE C1/C3/C5
+    const uint32_t nk = (RG_LOC_KEYW && RS >= 16 && ks <= uint32_t(4 * KW)) ? uint32_t(KW) : uint32_t(2 * KW);
     {
         uint32_t a[2 * KW], o[2 * KW];
 #pragma unroll
         for (int w = 0; w < 2 * KW; ++w) a[w] = ~0u, o[w] = 0u;
-        auto andor = [&](auto specc) {
+        auto andor = [&](auto specc, auto nkc) {
+            constexpr int NK = decltype(nkc)::value;
 #pragma unroll
             for (int j = 0; j < IPT; ++j) {
                 if (uint32_t(j) * T >= n) break;  // block-uniform
@@ -272,7 +280,7 @@ __device__ __forceinline__ void local_group(
                 if (e < n) {
                     const Rec<RS> v = rec_of(j, e);
 #pragma unroll
-                    for (int w = 0; w < 2 * KW; ++w) a[w] &= v.w[w], o[w] |= v.w[w];
+                    for (int w = 0; w < NK; ++w) a[w] &= v.w[w], o[w] |= v.w[w];
                     if constexpr (decltype(specc)::value) {
                         const uint32_t w = rec_window<RS>(v, wsd);
                         wv[KEEP ? j : 0] = w;
@@ -283,12 +291,19 @@ __device__ __forceinline__ void local_group(
                 }
             }
         };
-        if (spec) andor(BoolC<KEEP>{});
-        else andor(BoolC<false>{});
+        if (nk == uint32_t(KW)) {
+            if (spec) andor(BoolC<KEEP>{}, IntC<KW>{});
+            else andor(BoolC<false>{}, IntC<KW>{});
+        } else {
+            if (spec) andor(BoolC<KEEP>{}, IntC<2 * KW>{});
+            else andor(BoolC<false>{}, IntC<2 * KW>{});
+        }
 #pragma unroll
         for (int w = 0; w < 2 * KW; ++w) {
-            a[w] = __reduce_and_sync(0xFFFFFFFFu, a[w]);
-            o[w] = __reduce_or_sync(0xFFFFFFFFu, o[w]);
+            if (uint32_t(w) < nk) {  // (the rest stay ~0 / 0: constant)
+                a[w] = __reduce_and_sync(0xFFFFFFFFu, a[w]);
+                o[w] = __reduce_or_sync(0xFFFFFFFFu, o[w]);
+            }
         }
         if (lane < 2 * KW) {
             uint32_t av = a[0], ov = o[0];
@@ -317,9 +332,11 @@ __device__ __forceinline__ void local_group(
         uint32_t dsel = 0;
 #pragma unroll
         for (int w = 0; w < 2 * KW; ++w) {
-            const uint32_t ra = __reduce_and_sync(0xFFFFFFFFu, lane < W ? s_and[lane][w] : ~0u);
-            const uint32_t ro = __reduce_or_sync(0xFFFFFFFFu, lane < W ? s_or[lane][w] : 0u);
-            if ((b >> 2) == uint32_t(w)) dsel = ra ^ ro;
+            if (uint32_t(w) < nk) {
+                const uint32_t ra = __reduce_and_sync(0xFFFFFFFFu, lane < W ? s_and[lane][w] : ~0u);
+                const uint32_t ro = __reduce_or_sync(0xFFFFFFFFu, lane < W ? s_or[lane][w] : 0u);
+                if ((b >> 2) == uint32_t(w)) dsel = ra ^ ro;
+            }
         }
         uint32_t diffb = 0;
         if (b >= g.p && b < ks && b < uint32_t(RS)) diffb = (dsel >> ((b & 3) * 8)) & 0xFFu;

@@ -35,6 +35,9 @@ namespace rg {
 #ifndef RG_SC_STAGES
 #define RG_SC_STAGES 2
 #endif
+#ifndef RG_HINT_NDST
+#define RG_HINT_NDST 0
+#endif
 #ifndef RG_SC_EARLY8
 #define RG_SC_EARLY8 1
 #endif
@@ -225,7 +228,7 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
             fence_proxy_async_smem();
             s_info[b] = ti;
             mbar_arrive_expect_tx(&s_full[b], body + ndb);
-            if (body) tma_load_1d(sb + hb, gsrc + hb, body, &s_full[b]);
+            if (body) tma_load_1d_h<RG_HINT_SC>(sb + hb, gsrc + hb, body, &s_full[b]);
             if (ndb) tma_load_1d(snd + b * C::kNdBytes, nd_in + nda, ndb, &s_full[b]);
         }
     }
@@ -353,8 +356,18 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
                     store_rec<RS>(reinterpret_cast<uint8_t*>(s_pdst[d] + ti.seg_start * RS), uint32_t(s_gdelta[d] + slot), v);
                 } else {
                     const uint32_t di = s_gdelta[d] + slot;
-                    store_rec<RS>(dst, di, v);
-                    if (m >> 24) nd[ti.seg_start + di] = uint8_t(rec_byte<RS>(v, p + 1));
+                    store_rec_h<RS, RG_HINT_SCST>(dst, di, v);
+                    if (m >> 24) {
+                        if constexpr (RG_HINT_NDST == 0) {
+                            nd[ti.seg_start + di] = uint8_t(rec_byte<RS>(v, p + 1));
+                        } else {
+                            uint64_t pol;
+                            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+                            asm volatile("st.global.L2::cache_hint.u8 [%0], %1, %2;" ::"l"(nd + ti.seg_start + di),
+                                         "r"(rec_byte<RS>(v, p + 1)), "l"(pol)
+                                         : "memory");
+                        }
+                    }
                 }
             }
         }

@@ -421,6 +421,8 @@ void set_attrs(Workspace& ws) {
                                   int(HistCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_tile_hist<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(HistCfg<RS>::kSmem)));
+    RG_CHECK(cudaFuncSetAttribute(k_tile_hist<RS, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(HistCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(ScatterCfg<RS>::kSmemPlain)));
     RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -441,7 +443,7 @@ int sm_count() {
 // offsets (ws.tile_off), per-segment digit totals (ws.seg_tot[cur]).
 // nd_in: byte p of every record of the level, by record position (written
 // by the previous level's scatter), so the histogram reads one byte per record.
-template <int RS, bool kMap = false>
+template <int RS, bool kMap = false, bool kKey1 = false>
 void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t ntiles, LevelCounters* c,
                   cudaStream_t st, uint32_t ks = 0, const uint8_t* map = nullptr,
                   const uint8_t* nd_in = nullptr) {
@@ -456,7 +458,7 @@ void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t 
             data, tmp, ws.segs[cur].p, ws.tile_seg[cur].p, ws.tile_cnt.p, ws.seg_andor[cur].p, c, ks, map);
     } else {  // persistent, TMA-fed
         const uint32_t hgrid = std::min<uint32_t>(ntiles, uint32_t(sm_count()) * HistCfg<RS>::kCtas);
-        k_tile_hist<RS, kMap><<<hgrid, HistCfg<RS>::kThreads + 64, HistCfg<RS>::kSmem, st>>>(
+        k_tile_hist<RS, kMap, kKey1><<<hgrid, HistCfg<RS>::kThreads + 64, HistCfg<RS>::kSmem, st>>>(
             data, tmp, ws.segs[cur].p, ws.tile_seg[cur].p, ws.tile_cnt.p, ws.seg_andor[cur].p, c, ntiles, ks,
             map);
     }
@@ -629,7 +631,8 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         RG_LAUNCH_CHECK();
         ws.prof.end(pi, st);
         RG_CHECK(cudaMemsetAsync(dctr, 0, sizeof(LevelCounters), st));
-        level_counts<RS>(ws, data, tmp, 0, nt0, dctr, st);
+        if (ks <= 8) level_counts<RS, false, true>(ws, data, tmp, 0, nt0, dctr, st);
+        else level_counts<RS>(ws, data, tmp, 0, nt0, dctr, st);
         k_check_seg0<<<1, 32, 0, st>>>(ws.seg_andor[0].p, ws.segs[0].p, ks, d_flag);
         RG_LAUNCH_CHECK();
     };
@@ -714,7 +717,8 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         nd_half ^= 1;
         if (stop_after_first) break;
         RG_CHECK(cudaMemsetAsync(dctr + level, 0, sizeof(LevelCounters), st));
-        level_counts<RS>(ws, data, tmp, cur, ntiles, dctr + level, st, ks, nullptr, nd_in);
+        if (ks <= 8) level_counts<RS, false, true>(ws, data, tmp, cur, ntiles, dctr + level, st, ks, nullptr, nd_in);
+        else level_counts<RS>(ws, data, tmp, cur, ntiles, dctr + level, st, ks, nullptr, nd_in);
     }
     return level;
     };
@@ -745,7 +749,8 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         if (!split) {  // nothing to batch (level 0 finished it, or skipped a constant byte)
             if (nseg && levels == 1 && ws.h_ctr[0].n_next) {
                 RG_CHECK(cudaMemsetAsync(dctr + 1, 0, sizeof(LevelCounters), st));
-                level_counts<RS>(ws, data, tmp, cur, ntiles, dctr + 1, st, ks, nullptr, nd_in);
+                if (ks <= 8) level_counts<RS, false, true>(ws, data, tmp, cur, ntiles, dctr + 1, st, ks, nullptr, nd_in);
+                else level_counts<RS>(ws, data, tmp, cur, ntiles, dctr + 1, st, ks, nullptr, nd_in);
                 levels = run_levels(1, false);
                 read_counters_and_finish<RS>(ws, data, tmp, ks, dctr, levels, st);
                 add_level_stats(1, levels);
@@ -776,7 +781,8 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
                 k_init_andor<<<(nseg * 8 + 255) / 256, 256, 0, st>>>(ws.seg_andor[cur].p, nseg);
                 RG_LAUNCH_CHECK();
                 RG_CHECK(cudaMemsetAsync(dctr + 1, 0, sizeof(LevelCounters), st));
-                level_counts<RS>(ws, data, tmp, cur, ntiles, dctr + 1, st, ks, nullptr, nd_in);
+                if (ks <= 8) level_counts<RS, false, true>(ws, data, tmp, cur, ntiles, dctr + 1, st, ks, nullptr, nd_in);
+                else level_counts<RS>(ws, data, tmp, cur, ntiles, dctr + 1, st, ks, nullptr, nd_in);
                 const uint32_t lv = run_levels(1, false);
                 levels = std::max(levels, lv);
                 read_counters_and_finish<RS>(ws, data, tmp, ks, dctr, lv, st);
