@@ -18,7 +18,7 @@ for r in rows:
         continue
     if hdr and len(r) == len(hdr):
         d = dict(zip(hdr, r))
-        k.setdefault((int(d["ID"]), d["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "")), {})[
+        k.setdefault((int(d["ID"]), d["Kernel Name"].replace("<unnamed>::", "").split("(")[0].split("<")[0].replace("void ", "").split("::")[-1]), {})[
             d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
 items = list(k.items())
 start = max(i for i, ((_, n), _) in enumerate(items) if n == "k_sample_andor")

@@ -1,0 +1,27 @@
+"""Selected metrics of a one-kernel ncu --set full report as JSON:
+python scripts/ncu_metrics.py report.ncu-rep "source description" > out.json"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
+        "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__inst_executed.sum",
+        "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__inst_executed.avg.per_cycle_active"]
+out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True,
+                     text=True, check=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+hdr, units, vals = rows[0], rows[1], rows[2]
+ix = {h: i for i, h in enumerate(hdr)}
+res = {k: vals[ix[k]] for k in KEYS if k in ix}
+res["units"] = {k: units[ix[k]] for k in KEYS if k in ix}
+res["kernel"] = vals[ix["Kernel Name"]]
+res["source"] = sys.argv[2] if len(sys.argv) > 2 else sys.argv[1]
+print(json.dumps(res, indent=1))
