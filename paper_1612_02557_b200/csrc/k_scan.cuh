@@ -20,13 +20,19 @@
 
 namespace rg {
 
-constexpr int kScanChunk = 64;
+#ifndef RG_SCAN_CHUNK
+#define RG_SCAN_CHUNK 64
+#endif
+#ifndef RG_SCAN_LOOK
+#define RG_SCAN_LOOK 4
+#endif
+constexpr int kScanChunk = RG_SCAN_CHUNK;
 
 // Look-back over earlier chunks' status words for digit d, starting at chunk
 // c-1, until an inclusive prefix; returns the exclusive prefix.
 __device__ __forceinline__ unsigned long long lookback_chunks(const unsigned long long* status,
                                                               int64_t c, int d) {
-    constexpr int kLook = 4;
+    constexpr int kLook = RG_SCAN_LOOK;
     unsigned long long excl = 0;
     int64_t t = c - 1;
     while (true) {
