@@ -430,6 +430,9 @@ __global__ void __launch_bounds__(HistRegCfg<RS, kTile>::kThreads) k_tile_hist_r
 // the tile's bytes, counts flushed as u16 like k_tile_hist. No AND/OR: the
 // planner reads constancy of byte p off the digit totals (one non-zero digit).
 constexpr int kNdWarps = 8;
+#ifndef RG_ND_CH
+#define RG_ND_CH 6
+#endif
 
 template <int kTile>
 __global__ void __launch_bounds__(kNdWarps * 32, 4) k_tile_hist_nd(
@@ -446,7 +449,7 @@ __global__ void __launch_bounds__(kNdWarps * 32, 4) k_tile_hist_nd(
     unsigned long long recs = 0;
     Seg g = tile < n_tiles ? segs[tile_seg[tile]] : Seg{};
     constexpr int kIt = (kTile + 15) / 512 + 1;  // 16-B vectors per lane covering a tile (any alignment)
-    constexpr int kCh = 6;
+    constexpr int kCh = RG_ND_CH;
     while (tile < n_tiles) {
         const uint32_t tnext = tile + nwarps;
         const Seg gnext = tnext < n_tiles ? segs[tile_seg[tnext]] : g;  // next tile's metadata in flight

@@ -43,6 +43,10 @@ constexpr uint32_t kMaxBucket = 32;
 #endif
 template <int RS>
 constexpr int kLocOutUnroll = RG_LOC_OUTU ? RG_LOC_OUTU : (RS == 32 ? 2 : 8);
+#ifndef RG_LOC_OUT8U
+#define RG_LOC_OUT8U 0
+#endif
+constexpr int kLocOut8Unroll = RG_LOC_OUT8U;  // 8-B staged output loop
 #ifndef RG_LOC_KEYW
 #define RG_LOC_KEYW 1
 #endif
@@ -717,6 +721,9 @@ __device__ __forceinline__ void local_group(
             }
             __syncthreads();
             const uint32_t cn = min(CC, n - c0);
+#if RG_LOC_OUT8U
+#pragma unroll kLocOut8Unroll
+#endif
             for (uint32_t i = threadIdx.x; i < cn; i += T)
                 store_rec<RS>(dst, c0 + i, ld_smem_rec<RS>(stage, i));
             if (c0 + CC < n) __syncthreads();
