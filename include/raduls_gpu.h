@@ -119,6 +119,14 @@ typedef struct {
 int raduls_gpu_set_profiling(int on);
 int raduls_gpu_last_kernel_times(raduls_gpu_kernel_time* out, int capacity, int* count);
 
+/* How the scatter ranks records inside a warp on the current device (decided
+ * on first use): 0 = one shared-memory atomic per record, used only after a
+ * device self-test (k_rank_selftest) confirmed that the conflicting lanes of
+ * one atomic are served in lane order; 1 = ballot ranking (stable by
+ * construction; also forced by RADULS_GPU_STABLE_RANK=ballot). Either way the
+ * sort is stable. The LSD baseline and raduls_gpu_split always use 1. */
+int raduls_gpu_rank_mode(int* mode);
+
 /*
  * Building blocks (tests, benchmarks and the multi-GPU driver). All device
  * pointers; asynchronous on `stream` unless noted.

@@ -3,9 +3,14 @@
 //
 // Mirrors, name for name:
 //   struct raduls::RecordLayout        /root/reference/proj/include/raduls/layout.hpp:16-28
+//   struct raduls::TinyPolicy          /root/reference/proj/include/raduls/small_sorts.hpp:14-25
 //   struct raduls::SchedulerConfig     /root/reference/proj/include/raduls/scheduler.hpp:23-32
 //   raduls::sort(uint8_t*, size_t, const RecordLayout&, const SchedulerConfig&)
 //                                      /root/reference/proj/include/raduls/scheduler.hpp:60-61
+//   raduls::sort(RecordArray&, const SchedulerConfig&)
+//                                      /root/reference/proj/include/raduls/scheduler.hpp:63-65
+//   class raduls::RecordArray, allocate_record_bytes
+//                                      /root/reference/proj/include/raduls/record_array.hpp:15-61
 //   raduls::resource_error             /root/reference/proj/include/raduls/errors.hpp:12-22
 //   struct raduls::LsdConfig, raduls::lsd_sort(uint8_t*, size_t, const RecordLayout&, const LsdConfig&)
 //                                      /root/reference/proj/include/raduls/lsd.hpp:12-22
@@ -16,8 +21,12 @@
 // RADULS_GPU_ENOMEM -> resource_error, anything else -> std::runtime_error.
 #pragma once
 
+#include <algorithm>
 #include <cstddef>
 #include <cstdint>
+#include <cstring>
+#include <memory>
+#include <new>
 #include <stdexcept>
 #include <string>
 
@@ -37,6 +46,22 @@ struct BigBinFraction {
     uint32_t den = 3;
 };
 
+// The reference's tiny-bin policy (which comparison sort finishes a bin).
+// Accepted and ignored like the scheduler knobs: the GPU's small-bin sort is
+// stable and its output does not depend on it.
+struct TinyPolicy {
+    size_t tiny_threshold = 384;
+    size_t insertion_threshold = 32;
+    size_t narrowing_factor_limit = 16;
+    size_t narrowed_tiny_threshold = 32;
+    size_t intro_vs_shell_override = 0;  // 0: derive from the key size
+
+    size_t intro_vs_shell_threshold(size_t key_size) const {
+        if (intro_vs_shell_override) return intro_vs_shell_override;
+        return std::clamp<size_t>(100 + 5 * key_size, 100, 180);
+    }
+};
+
 // Accepted for signature compatibility. The reference's knobs steer CPU thread
 // scheduling and never change the sorted content (test_scheduler.cpp:171-177);
 // the GPU planner ignores them.
@@ -48,10 +73,58 @@ struct SchedulerConfig {
     unsigned chunk_multiplier = 8;
     unsigned first_chunk_divisor = 64;
     size_t buffer_bytes = 256;
+    TinyPolicy tiny{};
 };
 
 struct resource_error : std::runtime_error {
     using std::runtime_error::runtime_error;
+};
+
+// 64-B aligned owning record storage (record_array.hpp:15-61): same
+// allocation contract -- resource_error instead of std::bad_alloc.
+struct AlignedFree {
+    void operator()(uint8_t* p) const { ::operator delete[](p, std::align_val_t{64}); }
+};
+
+using AlignedBytes = std::unique_ptr<uint8_t[], AlignedFree>;
+
+inline AlignedBytes allocate_record_bytes(size_t bytes) {
+    try {
+        return AlignedBytes(new (std::align_val_t{64}) uint8_t[bytes ? bytes : 1]);
+    } catch (const std::bad_alloc&) {
+        throw resource_error("cannot allocate " + std::to_string(bytes) + " bytes of record storage");
+    }
+}
+
+class RecordArray {
+  public:
+    RecordArray() = default;
+    RecordArray(const RecordLayout& layout, size_t n)
+        : layout_(layout), n_(n), buf_(allocate_record_bytes(n * layout.record_size)) {}
+    RecordArray(RecordArray&&) noexcept = default;
+    RecordArray& operator=(RecordArray&&) noexcept = default;
+    RecordArray(const RecordArray&) = delete;
+    RecordArray& operator=(const RecordArray&) = delete;
+
+    uint8_t* data() { return buf_.get(); }
+    const uint8_t* data() const { return buf_.get(); }
+    uint8_t* record(size_t i) { return buf_.get() + i * layout_.record_size; }
+    const uint8_t* record(size_t i) const { return buf_.get() + i * layout_.record_size; }
+    size_t size() const { return n_; }
+    size_t byte_size() const { return n_ * layout_.record_size; }
+    const RecordLayout& layout() const { return layout_; }
+    bool empty() const { return n_ == 0; }
+
+    RecordArray clone() const {
+        RecordArray c(layout_, n_);
+        if (byte_size()) std::memcpy(c.data(), data(), byte_size());
+        return c;
+    }
+
+  private:
+    RecordLayout layout_{};
+    size_t n_ = 0;
+    AlignedBytes buf_{};
 };
 
 inline void throw_on_error(int rc, const char* what) {
@@ -71,6 +144,10 @@ inline void sort(uint8_t* data, size_t n, const RecordLayout& layout,
                                     " key_size=" + std::to_string(layout.key_size));
     throw_on_error(raduls_gpu_sort_host(data, nullptr, n, layout.record_size, layout.key_size),
                    "raduls_gpu_sort_host");
+}
+
+inline void sort(RecordArray& array, const SchedulerConfig& cfg = {}) {
+    sort(array.data(), array.size(), array.layout(), cfg);
 }
 
 // LSD baseline (lsd.hpp:12-22). The lane size must be a positive multiple of 64

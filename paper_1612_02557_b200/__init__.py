@@ -22,6 +22,7 @@ from .raduls import (  # noqa: F401
     last_kernel_times,
     last_stats,
     local_capacity,
+    rank_mode,
     lsd_sort,
     set_profiling,
     sort,

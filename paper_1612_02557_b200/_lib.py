@@ -46,6 +46,7 @@ EXPORTED = [
     "raduls_gpu_ipc_open",
     "raduls_gpu_ipc_close",
     "raduls_gpu_free",
+    "raduls_gpu_rank_mode",
 ]
 
 
@@ -125,6 +126,7 @@ def load(build_if_missing: bool = False):
         L.raduls_gpu_ipc_open.argtypes = [C.c_char_p, C.POINTER(_vp)]
         L.raduls_gpu_ipc_close.argtypes = [_vp]
         L.raduls_gpu_free.argtypes = [_vp]
+        L.raduls_gpu_rank_mode.argtypes = [C.POINTER(C.c_int)]
         L.raduls_gpu_sort_multi.argtypes = [C.c_int, C.POINTER(C.c_int), C.POINTER(_vp), _u64p,
                                             C.POINTER(_vp), _u64p, _u64, _u32, _u32]
         L.raduls_gpu_last_kernel_times.argtypes = [C.POINTER(KernelTime), C.c_int,

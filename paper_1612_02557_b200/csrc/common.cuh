@@ -357,6 +357,73 @@ __device__ __forceinline__ uint32_t match_digit8(uint32_t d, bool valid) {
     return m;
 }
 
+// Stable in-warp rank of digit d: the number of this warp's earlier items
+// (earlier calls, then lower lanes of this call) holding d. `cnt` is the
+// warp's private 256-entry counter table. Every lane of the warp calls it.
+//   kMode 0: one shared-memory atomic per item. Ranks follow lane order only
+//            if the hardware serves the conflicting lanes of one atomic in
+//            lane order, which PTX does not promise: the library runs it only
+//            after k_rank_selftest has checked that behaviour on the device
+//            (else it uses kMode 1). Measured C5 scatter 73.6 ms vs 94.7 ms
+//            with kMode 1 and 110.2 ms with kMode 2 (same box, interleaved);
+//   kMode 1: peers from eight ballots (match_digit8), rank = counter +
+//            popc(peers & lanemask_lt), the highest peer lane advances the
+//            counter (stable by construction);
+//   kMode 2: the same with MATCH.ANY for the peer mask.
+template <int kMode>
+__device__ __forceinline__ uint32_t warp_rank(uint32_t* cnt, uint32_t d, bool valid) {
+    if constexpr (kMode == 0) {
+        return valid ? atomicAdd(&cnt[d], 1u) : 0u;
+    } else {
+        uint32_t peers;
+        if constexpr (kMode == 1) {
+            peers = match_digit8(d, valid);
+        } else {
+            peers = __match_any_sync(0xFFFFFFFFu, valid ? d : 0x100u);
+            if (!valid) peers = 0;
+        }
+        const uint32_t before = valid ? cnt[d] : 0u;
+        __syncwarp();
+        if (valid && lane_id() == 31u - __clz(peers)) cnt[d] = before + __popc(peers);
+        __syncwarp();
+        return before + __popc(peers & lanemask_lt());
+    }
+}
+
+// Device check of what kMode 0 relies on (run once per device before the first
+// sort): every warp ranks pseudo-random digit streams -- all lanes equal, 2-64
+// distinct values, alternating patterns -- with kMode 0 and kMode 1 on two
+// private counter tables; any rank that differs sets *bad.
+__global__ void __launch_bounds__(256) k_rank_selftest(uint32_t rounds, unsigned int* __restrict__ bad) {
+    __shared__ uint32_t t0[8][256], t1[8][256];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    for (uint32_t q = lane; q < 256; q += 32) t0[warp][q] = t1[warp][q] = 0;
+    __syncwarp();
+    uint32_t diff = 0;
+    for (uint32_t it = 0; it < rounds; ++it) {
+        uint32_t h = (it * 0x9E3779B9u) ^ (blockIdx.x * 0x85EBCA6Bu) ^ (warp * 0xC2B2AE35u) ^ (lane * 0x27D4EB2Fu);
+        h ^= h >> 15;
+        h *= 0x2C1B3C6Du;
+        h ^= h >> 12;
+        const uint32_t kind = it % 8;
+        uint32_t d;
+        if (kind == 0) d = it & 0xFFu;                        // all lanes one digit
+        else if (kind == 1) d = (lane & 1u) ? 7u : 200u;      // alternating
+        else if (kind == 2) d = lane < 16 ? 3u : 250u;        // halves
+        else d = (h >> 8) % (2u << kind) * 37u & 0xFFu;       // 4..256 distinct values
+        const bool valid = kind != 7 || (h & 7u) != 0;        // some lanes idle
+        const uint32_t r0 = warp_rank<0>(&t0[warp][0], d, valid);
+        const uint32_t r1 = warp_rank<1>(&t1[warp][0], d, valid);
+        diff |= valid && r0 != r1;
+        if ((it & 255u) == 255u) {  // keep the counters small
+            __syncwarp();
+            for (uint32_t q = lane; q < 256; q += 32) t0[warp][q] = t1[warp][q] = 0;
+            __syncwarp();
+        }
+    }
+    if (__any_sync(0xFFFFFFFFu, diff) && lane == 0) atomicOr(bad, 1u);
+}
+
 // Device segment descriptors -------------------------------------------------
 
 // A contiguous run of records [start, start+size) that still needs ordering by

@@ -12,7 +12,9 @@
 //     and TMA-loads each tile (cp.async.bulk, mbarrier transaction count) into
 //     one of two shared-memory buffers;
 //   * warps 0-7 (consumers) rank the tile's records by digit with a ballot
-//     multisplit (stable: warp-striped input order, digit-major/warp-minor
+//     multisplit (warp_rank: peers of a digit from eight ballots, rank =
+//     warp-private counter + popc(peers & lanemask_lt) -- stable by
+//     construction: warp-striped input order, digit-major/warp-minor
 //     offsets), build a slot map in digit order, and write the records out in
 //     that order: consecutive slots of one digit go to consecutive destinations,
 //     so every digit run becomes one contiguous span of 16-B (8-B) vector
@@ -133,7 +135,8 @@ struct TileInfo {
 // receive buffer over NVLink (P2P or CUDA-IPC mapped), at this source's offset
 // there — so the all-to-all is carried out by the partition's own coalesced
 // stores, tile by tile, instead of a separate collective.
-template <int RS, bool kMap = false, bool kPeer = false>
+// kRank: warp_rank mode (0: atomic ranks, device-checked; 1: ballot ranks).
+template <int RS, bool kMap = false, bool kPeer = false, int kRank = 0>
 __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>::kCtas) k_scatter(
     uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Seg* __restrict__ segs,
     const unsigned long long* __restrict__ seg_base,  // [nseg][256] exclusive digit bases
@@ -274,11 +277,10 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
         const uint32_t tn = ti.tn, p = ti.p;
         __syncwarp();
 
-        // 1: rank inside the warp with warp-private shared-memory counters: one
-        // ATOMS per record. Items are warp-striped in input order and the
-        // counters are per warp, so ranks follow input order as long as the
-        // hardware serves conflicting lanes of one atomic in lane order (the
-        // byte-exact stable-sort parity tests check this on the device).
+        // 1: stable rank inside the warp (warp_rank, common.cuh): items are
+        // warp-striped in input order and the counters are per warp, so ranks
+        // follow input order by construction (lane order inside one call from
+        // popc(peers & lanemask_lt), not from the order atomics are served).
         uint32_t pk[IT];  // digit | rank << 9 ; 0x100 = invalid
         const uint8_t* sdig = snd + b * C::kNdBytes + ti.ndh;
         const bool dig_nd = kU16 && nd_in != nullptr;
@@ -288,7 +290,8 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
             const bool valid = i < tn;
             uint32_t d = 0;
             if (valid) d = dig_nd ? uint32_t(sdig[i]) : scatter_digit_smem<RS, kMap>(tile + size_t(i) * RS, p, ks, map);
-            pk[j] = valid ? (d | (atomicAdd(&s_wcnt[warp][d], 1u) << 9)) : 0x100u;
+            const uint32_t rk = warp_rank<kRank>(&s_wcnt[warp][0], d, valid);  // every lane calls it
+            pk[j] = valid ? (d | (rk << 9)) : 0x100u;
         }
         bar_sync_named(1, T);
 

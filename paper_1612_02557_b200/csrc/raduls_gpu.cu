@@ -256,7 +256,10 @@ struct HostStager {
         for (size_t c = 0; c < nchunks; ++c) {
             const int b = int(c % kRing);
             const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
-            if (c >= size_t(kRing)) RG_CHECK(cudaEventSynchronize(ev[b]));  // chunk c-kRing copied
+            // the staging buffer's last DMA -- from this call or an earlier
+            // h2d/d2h, which may still be in flight -- must be done before the
+            // host overwrites it (an event never recorded returns at once)
+            RG_CHECK(cudaEventSynchronize(ev[b]));
             pool.copy(stage[b], host + off, len);
             RG_CHECK(cudaMemcpyAsync(dev + off, stage[b], len, cudaMemcpyHostToDevice, st));
             RG_CHECK(cudaEventRecord(ev[b], st));
@@ -317,6 +320,7 @@ struct Workspace {
     unsigned long long* h_small = nullptr;  // pinned scratch [4096]
     raduls_gpu_stats last{};
     bool attrs_set[33] = {};
+    int rank_mode = -1;  // scatter ranking: -1 unchecked, 0 atomic (device-checked), 1 ballot
     // raduls_gpu_partition_plan -> raduls_gpu_partition_store hand-over
     struct PartPlan {
         bool pending = false;
@@ -423,12 +427,14 @@ void set_attrs(Workspace& ws) {
                                   int(HistCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_tile_hist<RS, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(HistCfg<RS>::kSmem)));
-    RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(ScatterCfg<RS>::kSmemPlain)));
-    RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(ScatterCfg<RS>::kSmem)));
-    RG_CHECK(cudaFuncSetAttribute(k_scatter<RS, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(ScatterCfg<RS>::kSmem)));
+    for (int r = 0; r < 2; ++r) {
+        RG_CHECK(cudaFuncSetAttribute(r ? k_scatter<RS, false, false, 1> : k_scatter<RS, false, false, 0>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(ScatterCfg<RS>::kSmemPlain)));
+        RG_CHECK(cudaFuncSetAttribute(r ? k_scatter<RS, true, false, 1> : k_scatter<RS, true, false, 0>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(ScatterCfg<RS>::kSmem)));
+        RG_CHECK(cudaFuncSetAttribute(r ? k_scatter<RS, true, true, 1> : k_scatter<RS, true, true, 0>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(ScatterCfg<RS>::kSmem)));
+    }
     ws.attrs_set[RS] = true;
 }
 
@@ -473,17 +479,46 @@ void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t 
     ws.prof.end(pe, st);
 }
 
+// Whether the scatter may rank with shared-memory atomics (warp_rank<0>):
+// decided once per device by k_rank_selftest, overridable with
+// RADULS_GPU_STABLE_RANK=ballot (always warp_rank<1>) for tests and A/B.
+bool atomic_rank_ok(Workspace& ws) {
+    if (ws.rank_mode < 0) {
+        const char* e = std::getenv("RADULS_GPU_STABLE_RANK");
+        if (e && std::strcmp(e, "ballot") == 0) {
+            ws.rank_mode = 1;
+        } else {
+            unsigned int* d_bad = reinterpret_cast<unsigned int*>(ws.acc.p + 2);
+            RG_CHECK(cudaMemset(d_bad, 0, sizeof(unsigned int)));
+            k_rank_selftest<<<2 * sm_count(), 256>>>(4096, d_bad);
+            RG_LAUNCH_CHECK();
+            unsigned int bad = 1;
+            RG_CHECK(cudaMemcpy(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost));
+            ws.rank_mode = bad ? 1 : 0;
+        }
+    }
+    return ws.rank_mode == 0;
+}
+
+// stable_ballot: rank with ballots regardless of the device check (the LSD
+// baseline and the single-split API, whose contract is stability itself).
 template <int RS, bool kMap, bool kPeer = false>
 void launch_scatter(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t ntiles, uint32_t ks,
                     const uint8_t* map, LevelCounters* c, cudaStream_t st,
                     const unsigned long long* dig_dst = nullptr, uint8_t* nd = nullptr,
-                    const uint8_t* nd_in = nullptr) {
+                    const uint8_t* nd_in = nullptr, bool stable_ballot = false) {
     const uint32_t grid = std::min<uint32_t>(ntiles, uint32_t(sm_count()) * 2);
-    const int pe = ws.prof.begin(K_SCATTER, st);
     const size_t smem = (kMap || kPeer) ? ScatterCfg<RS>::kSmem : ScatterCfg<RS>::kSmemPlain;
-    k_scatter<RS, kMap, kPeer><<<grid, ScatterCfg<RS>::kThreads + 32, smem, st>>>(
-        data, tmp, ws.segs[cur].p, ws.seg_tot[cur].p, ws.tile_seg[cur].p, ws.tile_off.p, ntiles,
-        &c->scatter_ticket, ks, map, dig_dst, nd, local_cap<RS>(), nd_in);
+    const bool atomic = !stable_ballot && atomic_rank_ok(ws);
+    const int pe = ws.prof.begin(K_SCATTER, st);
+    if (atomic)
+        k_scatter<RS, kMap, kPeer, 0><<<grid, ScatterCfg<RS>::kThreads + 32, smem, st>>>(
+            data, tmp, ws.segs[cur].p, ws.seg_tot[cur].p, ws.tile_seg[cur].p, ws.tile_off.p, ntiles,
+            &c->scatter_ticket, ks, map, dig_dst, nd, local_cap<RS>(), nd_in);
+    else
+        k_scatter<RS, kMap, kPeer, 1><<<grid, ScatterCfg<RS>::kThreads + 32, smem, st>>>(
+            data, tmp, ws.segs[cur].p, ws.seg_tot[cur].p, ws.tile_seg[cur].p, ws.tile_off.p, ntiles,
+            &c->scatter_ticket, ks, map, dig_dst, nd, local_cap<RS>(), nd_in);
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
 }
@@ -1052,11 +1087,16 @@ static int sort_host_out_of_core(uint8_t* data, uint8_t* htmp, uint64_t n, uint3
             check(raduls_gpu_partition(A, B, c, rs, ks, p0, d_map, K, cnt.data(), st));
             uint64_t run = 0;
             for (uint32_t k = 0; k < K; ++k) {
+                // a part never outgrows the size its histogram promised
+                // (a mismatch would overlap the next part in htmp)
+                if (written[k] + cnt[k] > psz[k]) throw CudaError{RADULS_GPU_EINTERNAL};
                 if (cnt[k]) hs.d2h(htmp + (poff[k] + written[k]) * rs, B + run * rs, cnt[k] * rs, st);
                 written[k] += cnt[k];
                 run += cnt[k];
             }
         }
+        for (uint32_t k = 0; k < K; ++k)
+            if (written[k] != psz[k]) throw CudaError{RADULS_GPU_EINTERNAL};
         // (4) every part: to the device, sorted, to its place in data
         for (uint32_t k = 0; k < K; ++k) {
             if (!psz[k]) continue;
@@ -1159,7 +1199,7 @@ void single_segment_counts(Workspace& ws, uint8_t* src, uint64_t n, uint32_t p, 
 template <int RS, bool kMap, bool kPeer = false>
 void single_segment_scatter(Workspace& ws, uint8_t* src, uint8_t* dst, uint64_t n, uint32_t ks,
                             const uint8_t* map, const unsigned long long* h_tot, cudaStream_t st,
-                            const unsigned long long* dig_dst = nullptr) {
+                            const unsigned long long* dig_dst = nullptr, bool stable_ballot = false) {
     constexpr int TILE = ScatterCfg<RS>::kTile;
     unsigned long long* off = ws.h_small + 1024;
     unsigned long long run = 0;
@@ -1170,7 +1210,8 @@ void single_segment_scatter(Workspace& ws, uint8_t* src, uint8_t* dst, uint64_t 
     RG_CHECK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(ws.segs[0].p) + offsetof(Seg, action), &act,
                              sizeof act, cudaMemcpyHostToDevice, st));
     const uint32_t nt = uint32_t((n + TILE - 1) / TILE);
-    launch_scatter<RS, kMap, kPeer>(ws, src, dst, 0, nt, ks, map, ws.ctr.p, st, dig_dst);
+    launch_scatter<RS, kMap, kPeer>(ws, src, dst, 0, nt, ks, map, ws.ctr.p, st, dig_dst, nullptr, nullptr,
+                                    stable_ballot);
     RG_CHECK(cudaStreamSynchronize(st));
 }
 
@@ -1190,7 +1231,7 @@ void lsd_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t k
         for (int d = 0; d < 256; ++d)
             if (tot[d] == n) moves = false;
         if (!moves) continue;
-        single_segment_scatter<RS, false>(ws, src, dst, n, ks, nullptr, tot, st);
+        single_segment_scatter<RS, false>(ws, src, dst, n, ks, nullptr, tot, st, nullptr, true);
         std::swap(src, dst);
     }
     if (src != data) RG_CHECK(cudaMemcpyAsync(data, src, n * RS, cudaMemcpyDeviceToDevice, st));
@@ -1268,7 +1309,8 @@ int raduls_gpu_split(const void* d_src, void* d_dst, uint64_t n, uint32_t rs,
             unsigned long long* tot = ws.h_small;
             single_segment_counts<RSC, false>(ws, src, n, key_byte_offset, rs, nullptr, tot, st);
             if (h_counts) std::memcpy(h_counts, tot, 256 * sizeof(uint64_t));
-            single_segment_scatter<RSC, false>(ws, src, static_cast<uint8_t*>(d_dst), n, rs, nullptr, tot, st);
+            single_segment_scatter<RSC, false>(ws, src, static_cast<uint8_t*>(d_dst), n, rs, nullptr, tot, st,
+                                               nullptr, true);
         });
     });
 }
@@ -1631,6 +1673,15 @@ int raduls_gpu_set_profiling(int on) {
         Workspace& ws = workspace();
         std::lock_guard<std::mutex> lk(ws.mu);
         ws.prof.on = on != 0;
+    });
+}
+
+int raduls_gpu_rank_mode(int* mode) {
+    if (!mode) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        *mode = atomic_rank_ok(ws) ? 0 : 1;
     });
 }
 

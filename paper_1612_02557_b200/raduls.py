@@ -33,7 +33,7 @@ __all__ = [
     "RecordLayout", "SchedulerConfig", "TinyPolicy", "BigBinFraction", "ResourceError",
     "CudaError", "sort", "sort_device", "split", "histogram", "generate", "digest",
     "check_sorted", "last_stats", "DIST_UNIFORM", "DIST_SKEW", "local_capacity",
-    "set_profiling", "last_kernel_times", "LsdConfig", "lsd_sort",
+    "set_profiling", "last_kernel_times", "LsdConfig", "lsd_sort", "rank_mode",
 ]
 
 DIST_UNIFORM = 0
@@ -129,10 +129,25 @@ def _is_cuda_tensor(x) -> bool:
     return isinstance(x, torch.Tensor) and x.is_cuda
 
 
-def _stream_ptr(stream) -> int | None:
+def _check_device_tensor(data, tmp) -> None:
+    """uint8, contiguous, and tmp on data's device: n counts bytes / rs, and
+    the library reads the tensor's memory from data_ptr() on."""
+    torch = _torch()
+    for name, t in (("data", data), ("tmp", tmp)):
+        if t is None:
+            continue
+        if t.dtype != torch.uint8:
+            raise TypeError(f"{name} must be a torch.uint8 tensor (got {t.dtype})")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+    if tmp is not None and tmp.device != data.device:
+        raise ValueError("tmp must be on data's device")
+
+
+def _stream_ptr(stream, device=None) -> int | None:
     if stream is None:
         torch = _torch()
-        return torch.cuda.current_stream().cuda_stream
+        return torch.cuda.current_stream(device).cuda_stream
     return stream if isinstance(stream, int) else stream.cuda_stream
 
 
@@ -160,6 +175,7 @@ def sort(data, n: int | None = None, layout: RecordLayout = RecordLayout(),
     if hasattr(data, "layout") and hasattr(data, "buf") and n is None:  # RecordArray
         return sort(data.buf, data.n, data.layout, cfg, tmp=tmp, stream=stream)
     if _is_cuda_tensor(data):
+        _check_device_tensor(data, tmp)
         if n is None:
             n = data.numel() // rs
         if data.numel() < n * rs:
@@ -167,8 +183,10 @@ def sort(data, n: int | None = None, layout: RecordLayout = RecordLayout(),
         tptr = tmp.data_ptr() if tmp is not None else None
         if tmp is not None and tmp.numel() < n * rs:
             raise ValueError("tmp holds fewer than n records")
-        st = _stream_ptr(stream)
-        rc = _lib.load().raduls_gpu_sort(data.data_ptr(), tptr, n, rs, layout.key_size, st)
+        torch = _torch()
+        with torch.cuda.device(data.device):  # the library works on the current device
+            st = _stream_ptr(stream, data.device)
+            rc = _lib.load().raduls_gpu_sort(data.data_ptr(), tptr, n, rs, layout.key_size, st)
         _raise(rc, "raduls_gpu_sort")
         return None
     # host memory
@@ -193,6 +211,15 @@ def last_stats() -> dict:
     s = _lib.Stats()
     _raise(_lib.load().raduls_gpu_last_stats(C.byref(s)), "raduls_gpu_last_stats")
     return s.as_dict()
+
+
+def rank_mode() -> int:
+    """The scatter's in-warp ranking on this device (raduls_gpu_rank_mode):
+    0 = shared-memory atomics, used after the device self-test confirmed they
+    are served in lane order; 1 = ballot ranking. The sort is stable either way."""
+    m = C.c_int(-1)
+    _raise(_lib.load().raduls_gpu_rank_mode(C.byref(m)), "raduls_gpu_rank_mode")
+    return m.value
 
 
 def set_profiling(on: bool) -> None:
@@ -313,6 +340,7 @@ def lsd_sort(data, n: int | None = None, layout: RecordLayout = RecordLayout(),
     if hasattr(data, "layout") and hasattr(data, "buf") and n is None:  # RecordArray
         return lsd_sort(data.buf, data.n, data.layout, cfg, tmp=tmp, stream=stream)
     if _is_cuda_tensor(data):
+        _check_device_tensor(data, tmp)
         if n is None:
             n = data.numel() // rs
         if data.numel() < n * rs:
@@ -320,8 +348,10 @@ def lsd_sort(data, n: int | None = None, layout: RecordLayout = RecordLayout(),
         if tmp is not None and tmp.numel() < n * rs:
             raise ValueError("tmp holds fewer than n records")
         tptr = tmp.data_ptr() if tmp is not None else None
-        rc = _lib.load().raduls_gpu_lsd_sort(data.data_ptr(), tptr, n, rs, layout.key_size,
-                                             _stream_ptr(stream))
+        torch = _torch()
+        with torch.cuda.device(data.device):
+            rc = _lib.load().raduls_gpu_lsd_sort(data.data_ptr(), tptr, n, rs, layout.key_size,
+                                                 _stream_ptr(stream, data.device))
         _raise(rc, "raduls_gpu_lsd_sort")
         return None
     arr, n = _host_records(data, n, rs)

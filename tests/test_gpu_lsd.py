@@ -85,6 +85,6 @@ def test_lsd_cpp_shim(rg):
     if not os.path.exists(exe):
         import __graft_entry__
         __graft_entry__.build_cpp_dropin()
-    for args in (["100000", "16", "8", "lsd"], ["30000", "32", "24", "lsd"]):
+    for args in (["100000", "16", "8", "lsd4"], ["30000", "32", "24", "lsd1"]):
         r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=120)
         assert r.returncode == 0 and r.stdout.startswith("OK"), r.stdout + r.stderr

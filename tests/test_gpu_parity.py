@@ -95,7 +95,10 @@ def test_constant_middle_bytes_skew(rg, torch_cuda):
     a = make_input(1 << 20, rs, ks, 0x5EED0003, dist=oracle.DIST_SKEW)
     assert_parity(gpu_sort(rg, torch_cuda, a, rs, ks), a, rs, ks)
     st = rg.last_stats()
-    assert st["skipped_levels"] >= 0
+    # bytes 0-2 are constant: level 0 starts at byte 3 without moving a record
+    # (a sort that split them would scatter every record three extra times)
+    n = a.size // rs
+    assert st["hist_records"] == n and st["scatter_records"] < 3 * n, st
 
 
 def test_long_ties_force_fallback(rg, torch_cuda):
@@ -299,6 +302,23 @@ def test_host_sort_out_of_core(rg, torch_cuda, monkeypatch):
     assert np.array_equal(f, e)
 
 
+def test_host_sort_out_of_core_late_varying_top_byte(rg, torch_cuda, monkeypatch):
+    """Out-of-core host sort whose first chunk has a constant top key byte that
+    varies only in later chunks: the first pass guesses byte 1, the exact AND/OR
+    forces a second prefix-histogram pass on byte 0 (back-to-back staged copies
+    of a pageable buffer: a staging buffer must not be refilled while its last
+    DMA is still reading it)."""
+    rs, ks, n = 16, 8, 6_000_000
+    a = make_input(n, rs, ks, 0xACE)
+    r = a.reshape(n, rs)
+    r[: n // 2, 0] = 0x42  # first half (and so the first chunks): constant byte 0
+    want = oracle.stable_sort(a, rs, ks)
+    monkeypatch.setenv("RADULS_GPU_DEVICE_BUDGET", str(96 << 20))
+    b = a.copy()
+    rg.sort(b, n, rg.RecordLayout(rs, ks))
+    assert np.array_equal(b, want)
+
+
 @pytest.mark.parametrize("rs,ks", [(8, 8), (16, 8), (24, 16), (32, 24)])
 def test_scatter_tile_boundaries(rg, torch_cuda, rs, ks):
     """Sizes straddling multiples of the scatter tile above the local-sort
@@ -387,3 +407,49 @@ def test_sort_on_a_caller_stream(rg, torch_cuda):
         rg.sort(d, n, rg.RecordLayout(rs, ks), stream=s)
     s.synchronize()
     assert_parity(from_dev(d), a, rs, ks)
+
+
+def test_device_tensor_arguments_are_checked(rg, torch_cuda):
+    """Only contiguous uint8 tensors are sorted (n counts bytes / rs and the
+    library reads from data_ptr() on); anything else is rejected up front."""
+    torch = torch_cuda
+    lay = rg.RecordLayout(16, 8)
+    with pytest.raises(TypeError):
+        rg.sort(torch.zeros(64, dtype=torch.int32, device="cuda"), 4, lay)
+    with pytest.raises(ValueError):
+        rg.sort(torch.zeros(128, dtype=torch.uint8, device="cuda")[::2], 4, lay)
+    d = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    with pytest.raises(TypeError):
+        rg.sort(d, 4, lay, tmp=torch.zeros(16, dtype=torch.int32, device="cuda"))
+
+
+def test_scatter_rank_modes_are_both_stable(rg, torch_cuda, monkeypatch):
+    """The scatter ranks with shared-memory atomics only after the device
+    self-test (k_rank_selftest) confirmed lane-ordered service; the ballot
+    ranker (stable by construction) is what the library falls back to. Both
+    must give the stable sort byte for byte, on duplicate-heavy inputs where
+    an unstable rank would reorder equal keys."""
+    import subprocess
+    import sys
+    mode = rg.rank_mode()
+    assert mode in (0, 1)
+    cases = [(16, 8, 300_000, 7), (8, 8, 400_000, 3), (32, 24, 120_000, 50), (24, 16, 90_000, 2)]
+    for rs, ks, n, universe in cases:
+        a = make_input(n, rs, ks, 1234 + rs, universe)
+        assert_parity(gpu_sort(rg, torch_cuda, a, rs, ks), a, rs, ks)
+    # the ballot ranker, in a fresh process (the mode is chosen once per device)
+    code = (
+        "import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import numpy as np, torch, oracle, paper_1612_02557_b200 as rg\n"
+        "from helpers import make_input\n"
+        "assert rg.rank_mode() == 1\n"
+        "for rs, ks, n, u in %r:\n"
+        "    a = make_input(n, rs, ks, 1234 + rs, u)\n"
+        "    d = torch.from_numpy(a.copy()).cuda()\n"
+        "    rg.sort(d, n, rg.RecordLayout(rs, ks)); torch.cuda.synchronize()\n"
+        "    assert np.array_equal(d.cpu().numpy(), oracle.stable_sort(a, rs, ks)), (rs, ks)\n"
+        "print('OK')\n" % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                           os.path.dirname(os.path.abspath(__file__)), cases))
+    env = dict(os.environ, RADULS_GPU_STABLE_RANK="ballot")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
