@@ -219,6 +219,33 @@ int raduls_gpu_partition_plan(const void* d_src, uint64_t n_recs, uint32_t rec_s
                               uint64_t* h_rank_counts, uint64_t* h_andor, void* stream);
 int raduls_gpu_partition_store(const void* d_src, uint64_t n_recs, uint32_t rec_size, uint32_t key_size,
                                const uint64_t* h_dst, void* stream);
+
+/*
+ * Hot keys ("only a single-key bucket may be split"):
+ * a plan may give a hot 16-bit bucket its own digit and spread that digit's
+ * records over several destinations by count, provided the bucket holds one
+ * key only.
+ *   raduls_gpu_digit_andor: AND/OR of the key words (64-bit words holding key
+ *     bytes) of the records whose bucket maps to a digit d with h_hot[d] != 0
+ *     (at most 32 such digits); h_andor: host [n_digits][8] u64 (and at 2w,
+ *     or at 2w+1; ~0/0 for digits without records or not flagged). The digit
+ *     holds a single key iff and == or on every key byte. Synchronous;
+ *     cancels a pending raduls_gpu_partition_plan.
+ *   raduls_gpu_partition_store_pieces: the stores of the pending plan, with
+ *     each digit's run cut into pieces: n_pieces entries (h_piece_digit[i],
+ *     h_piece_count[i], h_piece_dst[i]) in increasing digit order; a digit's
+ *     pieces take its records in stable order, count by count, each to its
+ *     own byte address (16-B aligned; 8-B for record sizes 8 and 24). The
+ *     counts of every digit must add up to the plan's count for it.
+ *     Synchronous.
+ */
+int raduls_gpu_digit_andor(const void* d_src, uint64_t n_recs, uint32_t rec_size, uint32_t key_size,
+                           uint32_t prefix_byte, const uint32_t* d_bucket_digit, uint32_t n_digits,
+                           const uint8_t* h_hot, uint64_t* h_andor, void* stream);
+int raduls_gpu_partition_store_pieces(const void* d_src, uint64_t n_recs, uint32_t rec_size,
+                                      uint32_t key_size, uint32_t n_pieces, const uint32_t* h_piece_digit,
+                                      const uint64_t* h_piece_count, const uint64_t* h_piece_dst,
+                                      void* stream);
 int raduls_gpu_sample_andor(const void* d_data, uint64_t n_recs, uint32_t rec_size, uint32_t samples,
                             uint64_t* h_andor, void* stream);
 int raduls_gpu_sample_prefix_histogram(const void* d_data, uint64_t n_recs, uint32_t rec_size, uint32_t key_size,

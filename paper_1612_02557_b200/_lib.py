@@ -47,6 +47,8 @@ EXPORTED = [
     "raduls_gpu_ipc_close",
     "raduls_gpu_free",
     "raduls_gpu_rank_mode",
+    "raduls_gpu_digit_andor",
+    "raduls_gpu_partition_store_pieces",
 ]
 
 
@@ -127,6 +129,9 @@ def load(build_if_missing: bool = False):
         L.raduls_gpu_ipc_close.argtypes = [_vp]
         L.raduls_gpu_free.argtypes = [_vp]
         L.raduls_gpu_rank_mode.argtypes = [C.POINTER(C.c_int)]
+        L.raduls_gpu_digit_andor.argtypes = [_vp, _u64, _u32, _u32, _u32, _vp, _u32, _vp, _u64p, _vp]
+        L.raduls_gpu_partition_store_pieces.argtypes = [_vp, _u64, _u32, _u32, _u32, _vp, _u64p, _u64p,
+                                                        _vp]
         L.raduls_gpu_sort_multi.argtypes = [C.c_int, C.POINTER(C.c_int), C.POINTER(_vp), _u64p,
                                             C.POINTER(_vp), _u64p, _u64, _u32, _u32]
         L.raduls_gpu_last_kernel_times.argtypes = [C.POINTER(KernelTime), C.c_int,

@@ -130,11 +130,20 @@ struct TileInfo {
     uint32_t pad;
 };
 
-// kPeer (the multi-GPU partition): digit d is a destination
-// rank and its records are stored straight to dig_dst[d] — a peer GPU's
-// receive buffer over NVLink (P2P or CUDA-IPC mapped), at this source's offset
-// there — so the all-to-all is carried out by the partition's own coalesced
-// stores, tile by tile, instead of a separate collective.
+// kPeer (the multi-GPU partition): digit d's records are
+// stored straight to dig_dst[d] — a peer GPU's receive buffer over NVLink (P2P
+// or CUDA-IPC mapped), at this source's offset there — so the all-to-all is
+// carried out by the partition's own coalesced stores, tile by tile, instead
+// of a separate collective. A digit whose run is split across several
+// destinations (one hot key spread over ranks by count) has bit 63 set in
+// dig_dst[d] and its pieces at pieces[dig_dst[d] & 0x7FFFFFFF ...]: the
+// record at index i of the digit's run goes to the first piece with
+// i < end, at address adj + i * RS.
+struct Piece {
+    unsigned long long end;  // exclusive end index of the piece inside the digit's run
+    unsigned long long adj;  // destination address of the piece's first record - its start index * RS
+};
+
 // kRank: warp_rank mode (0: atomic ranks, device-checked; 1: ballot ranks).
 template <int RS, bool kMap = false, bool kPeer = false, int kRank = 0>
 __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>::kCtas) k_scatter(
@@ -144,7 +153,8 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
     uint32_t n_tiles, unsigned int* __restrict__ ticket, uint32_t ks = 0,
     const uint8_t* __restrict__ map = nullptr,
     const unsigned long long* __restrict__ dig_dst = nullptr, uint8_t* __restrict__ nd = nullptr,
-    uint32_t cap_local = 0, const uint8_t* __restrict__ nd_in = nullptr) {
+    uint32_t cap_local = 0, const uint8_t* __restrict__ nd_in = nullptr,
+    const Piece* __restrict__ pieces = nullptr) {
     using C = ScatterCfg<RS>;
     constexpr int T = C::kThreads, IT = C::kItems, W = C::kWarps;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -323,9 +333,12 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
             my_toff = s_gdelta[threadIdx.x];
         }
         s_gdelta[threadIdx.x] = uint32_t(my_sb) + my_toff - lstart;
-        if constexpr (kPeer)
-            s_pdst[threadIdx.x] = dig_dst[threadIdx.x] -
-                                  (ti.seg_start + seg_base[uint64_t(ti.seg) * kRadix + threadIdx.x]) * RS;
+        if constexpr (kPeer) {
+            const unsigned long long dd = dig_dst[threadIdx.x];
+            // split digit: flag | first piece << 32 | the digit's base in the segment
+            s_pdst[threadIdx.x] = (dd >> 63) ? ((dd & 0xFFFFFFFF00000000ull) | uint32_t(my_sb))
+                                             : dd - (ti.seg_start + my_sb) * RS;
+        }
         bar_sync_named(1, T);
 
         // 3: slot map (digit order) in shared memory
@@ -361,7 +374,16 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
                     d = (m >> 16) & 0xFFu;
                 }
                 if constexpr (kPeer) {
-                    store_rec<RS>(reinterpret_cast<uint8_t*>(s_pdst[d] + ti.seg_start * RS), uint32_t(s_gdelta[d] + slot), v);
+                    const unsigned long long pd = s_pdst[d];
+                    const uint32_t di = s_gdelta[d] + slot;
+                    if (!(pd >> 63)) {
+                        store_rec<RS>(reinterpret_cast<uint8_t*>(pd + ti.seg_start * RS), di, v);
+                    } else {  // a digit split over several destinations (rare)
+                        const uint32_t idx = di - uint32_t(pd);
+                        const Piece* pc = pieces + ((pd >> 32) & 0x7FFFFFFFu);
+                        while (idx >= pc->end) ++pc;
+                        store_rec<RS>(reinterpret_cast<uint8_t*>(pc->adj), idx, v);
+                    }
                 } else {
                     const uint32_t di = s_gdelta[d] + slot;
                     store_rec_h<RS, RG_HINT_SCST>(dst, di, v);

@@ -309,6 +309,8 @@ struct Workspace {
     DevBuf<CopyRange> copies;
     DevBuf<uint8_t> host_data, host_tmp, map8;
     DevBuf<unsigned long long> dig_dst;  // per-destination byte addresses (raduls_gpu_partition_to)
+    DevBuf<Piece> pieces;
+    DevBuf<unsigned long long> hot;       // raduls_gpu_digit_andor: slot flags + accumulators                // split digits' destination pieces (raduls_gpu_partition_store_pieces)
     DevBuf<uint8_t> nd;                  // digit array: next key byte per record position (sort_impl)
     DevBuf<Seg> bsegs;                   // level-1 segments of a progressive sort
     HostStager* stager = nullptr;  // host drop-ins, created on first use
@@ -506,7 +508,8 @@ template <int RS, bool kMap, bool kPeer = false>
 void launch_scatter(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t ntiles, uint32_t ks,
                     const uint8_t* map, LevelCounters* c, cudaStream_t st,
                     const unsigned long long* dig_dst = nullptr, uint8_t* nd = nullptr,
-                    const uint8_t* nd_in = nullptr, bool stable_ballot = false) {
+                    const uint8_t* nd_in = nullptr, bool stable_ballot = false,
+                    const Piece* pieces = nullptr) {
     const uint32_t grid = std::min<uint32_t>(ntiles, uint32_t(sm_count()) * 2);
     const size_t smem = (kMap || kPeer) ? ScatterCfg<RS>::kSmem : ScatterCfg<RS>::kSmemPlain;
     const bool atomic = !stable_ballot && atomic_rank_ok(ws);
@@ -514,11 +517,11 @@ void launch_scatter(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_
     if (atomic)
         k_scatter<RS, kMap, kPeer, 0><<<grid, ScatterCfg<RS>::kThreads + 32, smem, st>>>(
             data, tmp, ws.segs[cur].p, ws.seg_tot[cur].p, ws.tile_seg[cur].p, ws.tile_off.p, ntiles,
-            &c->scatter_ticket, ks, map, dig_dst, nd, local_cap<RS>(), nd_in);
+            &c->scatter_ticket, ks, map, dig_dst, nd, local_cap<RS>(), nd_in, pieces);
     else
         k_scatter<RS, kMap, kPeer, 1><<<grid, ScatterCfg<RS>::kThreads + 32, smem, st>>>(
             data, tmp, ws.segs[cur].p, ws.seg_tot[cur].p, ws.tile_seg[cur].p, ws.tile_off.p, ntiles,
-            &c->scatter_ticket, ks, map, dig_dst, nd, local_cap<RS>(), nd_in);
+            &c->scatter_ticket, ks, map, dig_dst, nd, local_cap<RS>(), nd_in, pieces);
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
 }
@@ -1199,7 +1202,8 @@ void single_segment_counts(Workspace& ws, uint8_t* src, uint64_t n, uint32_t p, 
 template <int RS, bool kMap, bool kPeer = false>
 void single_segment_scatter(Workspace& ws, uint8_t* src, uint8_t* dst, uint64_t n, uint32_t ks,
                             const uint8_t* map, const unsigned long long* h_tot, cudaStream_t st,
-                            const unsigned long long* dig_dst = nullptr, bool stable_ballot = false) {
+                            const unsigned long long* dig_dst = nullptr, bool stable_ballot = false,
+                            const Piece* pieces = nullptr) {
     constexpr int TILE = ScatterCfg<RS>::kTile;
     unsigned long long* off = ws.h_small + 1024;
     unsigned long long run = 0;
@@ -1211,7 +1215,7 @@ void single_segment_scatter(Workspace& ws, uint8_t* src, uint8_t* dst, uint64_t 
                              sizeof act, cudaMemcpyHostToDevice, st));
     const uint32_t nt = uint32_t((n + TILE - 1) / TILE);
     launch_scatter<RS, kMap, kPeer>(ws, src, dst, 0, nt, ks, map, ws.ctr.p, st, dig_dst, nullptr, nullptr,
-                                    stable_ballot);
+                                    stable_ballot, pieces);
     RG_CHECK(cudaStreamSynchronize(st));
 }
 
@@ -1572,6 +1576,116 @@ int raduls_gpu_partition_store(const void* d_src, uint64_t n, uint32_t rs, uint3
     });
 }
 
+int raduls_gpu_partition_store_pieces(const void* d_src, uint64_t n, uint32_t rs, uint32_t ks, uint32_t n_pieces,
+                                      const uint32_t* h_piece_digit, const uint64_t* h_piece_count,
+                                      const uint64_t* h_piece_dst, void* stream) {
+    if (!layout_ok(rs, ks) || (n_pieces && (!h_piece_digit || !h_piece_count || !h_piece_dst)))
+        return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (!n) return;
+        if (!ws.part.pending || ws.part.src != d_src || ws.part.n != n || ws.part.rs != rs || ws.part.ks != ks)
+            throw CudaError{RADULS_GPU_EINVAL};  // no matching plan on this device
+        // pieces in digit order; every digit's pieces add up to its planned count
+        const uint32_t align = rs % 16 == 0 ? 16 : 8;
+        std::vector<Piece> table;
+        unsigned long long* hd = ws.h_small + 3072;  // pinned staging for the destinations
+        for (uint32_t d = 0; d < kRadix; ++d) hd[d] = 0ull;
+        std::vector<uint64_t> sum(kRadix, 0);
+        uint32_t i = 0;
+        int last = -1;
+        while (i < n_pieces) {
+            const uint32_t d = h_piece_digit[i];
+            if (d >= kRadix || int(d) <= last) throw CudaError{RADULS_GPU_EINVAL};
+            last = int(d);
+            uint32_t j = i;
+            while (j < n_pieces && h_piece_digit[j] == d) ++j;
+            for (uint32_t k = i; k < j; ++k) {
+                if (h_piece_dst[k] % align) throw CudaError{RADULS_GPU_EINVAL};
+                sum[d] += h_piece_count[k];
+            }
+            if (j - i == 1) {
+                hd[d] = h_piece_dst[i];
+            } else {
+                hd[d] = (1ull << 63) | (uint64_t(table.size()) << 32);
+                uint64_t start = 0;
+                for (uint32_t k = i; k < j; ++k) {
+                    if (!h_piece_count[k]) continue;
+                    table.push_back(Piece{start + h_piece_count[k], h_piece_dst[k] - start * rs});
+                    start += h_piece_count[k];
+                }
+                if (table.empty() || (table.back().end != sum[d])) throw CudaError{RADULS_GPU_EINVAL};
+            }
+            i = j;
+        }
+        for (uint32_t d = 0; d < kRadix; ++d)
+            if (sum[d] != ws.part.tot[d]) throw CudaError{RADULS_GPU_EINVAL};  // pieces != the plan's counts
+        ws.part.pending = false;
+        ws.dig_dst.ensure(kRadix);
+        RG_CHECK(cudaMemcpyAsync(ws.dig_dst.p, hd, kRadix * sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+        if (!table.empty()) {
+            ws.pieces.ensure(table.size());
+            RG_CHECK(cudaMemcpyAsync(ws.pieces.p, table.data(), table.size() * sizeof(Piece), cudaMemcpyHostToDevice,
+                                     st));
+        }
+        dispatch_rs(rs, [&](auto R) {
+            constexpr int RSC = decltype(R)::value;
+            uint8_t* src = const_cast<uint8_t*>(static_cast<const uint8_t*>(d_src));
+            single_segment_scatter<RSC, true, true>(ws, src, nullptr, n, ks, ws.map8.p, ws.part.tot, st,
+                                                    ws.dig_dst.p, false, table.empty() ? nullptr : ws.pieces.p);
+        });
+    });
+}
+
+int raduls_gpu_digit_andor(const void* d_src, uint64_t n, uint32_t rs, uint32_t ks, uint32_t prefix_byte,
+                           const uint32_t* d_bucket_digit, uint32_t n_digits, const uint8_t* h_hot,
+                           uint64_t* h_andor, void* stream) {
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs) || n_digits < 1 || n_digits > 256 || !d_bucket_digit ||
+        !h_hot || !h_andor)
+        return RADULS_GPU_EINVAL;
+    if (n && !aligned_ok(d_src, rs)) return RADULS_GPU_EINVAL;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        for (uint32_t d = 0; d < n_digits; ++d)
+            for (int w = 0; w < 8; ++w) h_andor[8 * d + w] = (w & 1) ? 0ull : ~0ull;
+        // hot digits -> compact slots
+        uint8_t* hslot = reinterpret_cast<uint8_t*>(ws.h_small + 3584);  // pinned, 256 B
+        std::vector<uint32_t> slot_digit;
+        for (uint32_t d = 0; d < kRadix; ++d) {
+            hslot[d] = 0;
+            if (d < n_digits && h_hot[d]) {
+                if (slot_digit.size() >= size_t(kHotSlots)) throw CudaError{RADULS_GPU_EINVAL};
+                slot_digit.push_back(d);
+                hslot[d] = uint8_t(slot_digit.size());
+            }
+        }
+        ws.part.pending = false;  // the bucket map below replaces a pending plan's
+        if (!load_rank_map(ws, d_bucket_digit, n_digits, st)) throw CudaError{RADULS_GPU_EINVAL};
+        if (!n || slot_digit.empty()) return;
+        ws.hot.ensure(256 + kHotSlots * 8 * 8);
+        uint8_t* d_hot = reinterpret_cast<uint8_t*>(ws.hot.p);
+        unsigned long long* d_out = ws.hot.p + 32;
+        unsigned long long* init = ws.h_small + 2304;  // pinned [kHotSlots * 8]
+        for (int i = 0; i < kHotSlots * 8; ++i) init[i] = (i & 1) ? 0ull : ~0ull;
+        RG_CHECK(cudaMemcpyAsync(d_hot, hslot, 256, cudaMemcpyHostToDevice, st));
+        RG_CHECK(cudaMemcpyAsync(d_out, init, kHotSlots * 8 * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                                 st));
+        dispatch_rs(rs, [&](auto R) {
+            k_digit_andor<decltype(R)::value><<<grid_for(n, 256, 8), 256, 0, st>>>(
+                static_cast<const uint8_t*>(d_src), n, ks, prefix_byte, ws.map8.p, d_hot, d_out);
+        });
+        RG_LAUNCH_CHECK();
+        RG_CHECK(cudaMemcpyAsync(init, d_out, kHotSlots * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        RG_CHECK(cudaStreamSynchronize(st));
+        for (size_t k = 0; k < slot_digit.size(); ++k)
+            for (int w = 0; w < 8; ++w) h_andor[8 * slot_digit[k] + w] = init[8 * k + w];
+    });
+}
+
 int raduls_gpu_sample_andor(const void* d_data, uint64_t n, uint32_t rs, uint32_t samples, uint64_t* h_andor,
                             void* stream) {
     if (!layout_ok(rs, rs) || mul_overflows(n, rs) || !h_andor) return RADULS_GPU_EINVAL;
@@ -1714,7 +1828,7 @@ void raduls_gpu_release(void) {
             w->segs[b].release(); w->seg_tot[b].release(); w->seg_andor[b].release(); w->tile_seg[b].release();
         }
         w->tile_cnt.release(); w->tile_off.release(); w->status.release(); w->groups.release(); w->spill.release(); w->n_spill.release();
-        w->copies.release(); w->host_data.release(); w->host_tmp.release(); w->map8.release(); w->dig_dst.release();
+        w->copies.release(); w->host_data.release(); w->host_tmp.release(); w->map8.release(); w->dig_dst.release(); w->pieces.release(); w->hot.release();
         w->nd.release(); w->bsegs.release();
         delete w->stager;
         if (w->h_ctr) cudaFreeHost(w->h_ctr);

@@ -10,8 +10,13 @@ the sort shards with ONE exchange step:
     skipped, (e));
  2. 65 536-bucket histogram of the 16-bit prefix at key bytes (p0, p0+1),
     all-gathered: every rank learns the global distribution;
- 3. bucket -> rank map: contiguous bucket ranges balanced by record count
-    (a bucket is never split, so equal keys stay on one rank);
+ 3. bucket -> digit map (DigitPlan): contiguous bucket ranges balanced by
+    record count, one digit per rank range; a hot bucket (more than
+    1/(HOT_SHARE * world) of the records) gets a digit of its own, and when
+    its records provably share one key (raduls_gpu_digit_andor) that digit is
+    spread over consecutive ranks by count — SURVEY.md §8(e) step 4 "only a
+    single-key bucket may be split" — so one hot key cannot overload a rank;
+    equal keys keep their global (rank, position) order;
  4. stable local partition into per-destination send ranges on the device
     (the same tile histogram / look-back scan / scatter kernels as an MSD
     level);
@@ -78,13 +83,106 @@ def balanced_bucket_map(global_hist: np.ndarray, world: int) -> np.ndarray:
     return np.clip(r, 0, world - 1).astype(np.uint32)
 
 
+HOT_SHARE = 4  # a bucket with more than total / (HOT_SHARE * world) records is hot
+
+
+@dataclass
+class DigitPlan:
+    """The partition's digits: digit = bucket_digit[16-bit prefix at p0].
+    Digits are monotone in the bucket (key order); hot[d] marks a digit that
+    is exactly one hot bucket (a candidate for splitting by count)."""
+    p0: int
+    bucket_digit: np.ndarray   # [65536] u32
+    n_digits: int
+    hot: np.ndarray            # [n_digits] bool
+
+
+def make_digits(weights: np.ndarray, world: int, p0: int = 0, split_hot: bool = True) -> DigitPlan:
+    """Digits from global bucket weights (exact counts or sample estimates):
+    each rank's contiguous bucket range (balanced_bucket_map) is one digit,
+    except that every hot bucket is a digit of its own."""
+    w = np.asarray(weights, dtype=np.float64)
+    rank = balanced_bucket_map(w, world).astype(np.int64)
+    total = w.sum()
+    hot = (w > total / (HOT_SHARE * world)) if (split_hot and world > 1 and total > 0) \
+        else np.zeros(NBUCKETS, dtype=bool)
+    change = np.zeros(NBUCKETS, dtype=bool)
+    change[1:] = (rank[1:] != rank[:-1]) | hot[1:] | hot[:-1]
+    digit = np.cumsum(change).astype(np.uint32)
+    n_digits = int(digit[-1]) + 1
+    if n_digits > 256:  # too many ranks for separate hot digits: whole buckets only
+        return make_digits(weights, world, p0, split_hot=False)
+    dhot = np.zeros(n_digits, dtype=bool)
+    dhot[digit[hot]] = True
+    return DigitPlan(p0, digit, n_digits, dhot)
+
+
+def assign_pieces(M: np.ndarray, splittable: np.ndarray, world: int):
+    """Destination ranks of every digit's records, from the exact counts
+    M[source, digit]. Returns (pieces, S): pieces[s] is the list of
+    (digit, rank, count) for source s in digit order (a digit's pieces in
+    rank order), S[s, r] the records source s sends to rank r.
+
+    Global order = digit order, inside a digit source order then position (the
+    stable order of the concatenated inputs). A plain digit goes whole to the
+    rank holding its midpoint; a splittable digit (one key) is cut at the
+    ideal rank boundaries ceil(k N / world), clamped to the ranks of its
+    plain neighbours so the ranks stay monotone."""
+    M = np.asarray(M, dtype=np.int64)
+    G, D = M.shape
+    C = M.sum(axis=0)
+    N = int(C.sum())
+    P = np.concatenate([[0], np.cumsum(C)[:-1]]).astype(np.int64)
+    rank = np.zeros(D, dtype=np.int64)
+    if N:
+        rank = np.minimum((2 * P + C) * world // (2 * N), world - 1)
+    plain = ~np.asarray(splittable, dtype=bool)
+    S = np.zeros((G, world), dtype=np.int64)
+    pieces = [[] for _ in range(G)]
+    bound = [(k * N + world - 1) // world for k in range(world + 1)]  # first position of rank k
+    for d in range(D):
+        if C[d] == 0:
+            continue
+        if plain[d]:
+            for s in range(G):
+                if M[s, d]:
+                    pieces[s].append((d, int(rank[d]), int(M[s, d])))
+                    S[s, rank[d]] += M[s, d]
+            continue
+        prev = [int(rank[q]) for q in range(d - 1, -1, -1) if plain[q] and C[q]]
+        nxt = [int(rank[q]) for q in range(d + 1, D) if plain[q] and C[q]]
+        r_lo = prev[0] if prev else 0
+        r_hi = nxt[0] if nxt else world - 1
+        start = int(P[d])
+        for s in range(G):
+            a = start
+            b = a + int(M[s, d])
+            start = b
+            for k in range(r_lo, r_hi + 1):
+                lo = a if k == r_lo else max(a, bound[k])
+                hi = b if k == r_hi else min(b, bound[k + 1])
+                if hi > lo:
+                    pieces[s].append((d, k, hi - lo))
+                    S[s, k] += hi - lo
+    return pieces, S
+
+
 @dataclass
 class ExchangePlan:
-    p0: int
-    bucket_rank: np.ndarray      # [65536] u32
-    send_counts: np.ndarray      # [world] records this rank sends to each rank
-    recv_counts: np.ndarray      # [world] records this rank receives from each rank
-    matrix: np.ndarray = None    # [world, world] records source -> destination
+    digits: DigitPlan
+    M: np.ndarray                # [world, n_digits] records source -> digit
+    pieces: list                 # per source: [(digit, rank, count)] in digit order
+    matrix: np.ndarray           # [world, world] records source -> destination rank
+
+    @property
+    def p0(self) -> int:
+        return self.digits.p0
+
+    def send_counts(self, rank: int) -> np.ndarray:
+        return self.matrix[rank]
+
+    def recv_counts(self, rank: int) -> np.ndarray:
+        return self.matrix[:, rank]
 
 
 # ---------------------------------------------------------------- per-rank compute
@@ -176,6 +274,30 @@ class DeviceOps:
                                                  dst.ctypes.data_as(_lib._u64p), self.stream()),
                "raduls_gpu_partition_store")
 
+    def digit_andor(self, data, n: int, layout: RecordLayout, p0: int, bucket_digit: np.ndarray,
+                    hot: np.ndarray) -> np.ndarray:
+        """[n_digits, 8] AND/OR of the key words of each flagged digit's records."""
+        nd = len(hot)
+        dmap = self.torch.from_numpy(bucket_digit.astype(np.int32)).to(self.device)
+        flags = np.ascontiguousarray(hot.astype(np.uint8))
+        out = np.zeros((nd, 8), dtype=np.uint64)
+        _raise(self.L.raduls_gpu_digit_andor(data.data_ptr(), n, layout.record_size, layout.key_size, p0,
+                                             dmap.data_ptr(), nd, flags.ctypes.data,
+                                             out.ctypes.data_as(_lib._u64p), self.stream()),
+               "raduls_gpu_digit_andor")
+        return out
+
+    def partition_store_pieces(self, data, n: int, layout: RecordLayout, digit: np.ndarray,
+                               count: np.ndarray, dst: np.ndarray) -> None:
+        digit = np.ascontiguousarray(digit, dtype=np.uint32)
+        count = np.ascontiguousarray(count, dtype=np.uint64)
+        dst = np.ascontiguousarray(dst, dtype=np.uint64)
+        _raise(self.L.raduls_gpu_partition_store_pieces(data.data_ptr(), n, layout.record_size,
+                                                        layout.key_size, len(digit), digit.ctypes.data,
+                                                        count.ctypes.data_as(_lib._u64p),
+                                                        dst.ctypes.data_as(_lib._u64p), self.stream()),
+               "raduls_gpu_partition_store_pieces")
+
     def sort(self, data, n: int, layout: RecordLayout, tmp=None) -> None:
         _raise(self.L.raduls_gpu_sort(data.data_ptr(), tmp.data_ptr() if tmp is not None else None,
                                       n, layout.record_size, layout.key_size, self.stream()),
@@ -184,34 +306,70 @@ class DeviceOps:
 
 # ---------------------------------------------------------------- driver
 
-def plan_exchange(ops, data, n: int, layout: RecordLayout, group=None) -> ExchangePlan:
+def _coll_device(data, group):
+    """Metadata collectives run on the data's device under NCCL, on the host otherwise (gloo)."""
+    import torch
+    import torch.distributed as dist
+    return data.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+
+
+def _all_gather_np(arr: np.ndarray, dev, group) -> np.ndarray:
+    """All-gather of a fixed-size u64/i64 numpy row -> [world, ...] numpy."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    # metadata collectives on the data's device under NCCL, on the host otherwise (gloo)
-    dev = data.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    t = torch.from_numpy(np.ascontiguousarray(arr).view(np.int64)).to(dev)
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t, group=group)
+    return np.stack([o.cpu().numpy() for o in out]).view(arr.dtype)
+
+
+def _key_bytes_constant(andor: np.ndarray, ks: int) -> bool:
+    """andor: [8] u64 (and at 2w, or at 2w+1): every key byte constant?"""
+    for b in range(ks):
+        w = b >> 3
+        if ((int(andor[2 * w]) ^ int(andor[2 * w + 1])) >> ((b & 7) * 8)) & 0xFF:
+            return False
+    return True
+
+
+def _splittable(ops, data, n, layout, digits: DigitPlan, group) -> np.ndarray:
+    """Hot digits whose records (over every rank) share one key."""
+    split = np.zeros(digits.n_digits, dtype=bool)
+    if not digits.hot.any():
+        return split
+    ao = ops.digit_andor(data, n, layout, digits.p0, digits.bucket_digit, digits.hot)  # [D, 8]
+    allao = _all_gather_np(ao.astype(np.uint64), _coll_device(data, group), group)  # [world, D, 8]
+    a = np.bitwise_and.reduce(allao[:, :, 0::2], axis=0)
+    o = np.bitwise_or.reduce(allao[:, :, 1::2], axis=0)
+    comb = np.empty((digits.n_digits, 8), dtype=np.uint64)
+    comb[:, 0::2], comb[:, 1::2] = a, o
+    for d in np.nonzero(digits.hot)[0]:
+        split[d] = _key_bytes_constant(comb[d], layout.key_size)
+    return split
+
+
+def plan_exchange(ops, data, n: int, layout: RecordLayout, group=None) -> ExchangePlan:
+    """Exact plan: full AND/OR and full 16-bit prefix histograms, all-gathered;
+    per-source digit counts follow from the histograms."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    dev = _coll_device(data, group)
     # 1. global constant-prefix detection
-    ao = torch.from_numpy(ops.andor(data, n, layout).view(np.int64)).to(dev)
-    all_ao = [torch.empty_like(ao) for _ in range(world)]
-    dist.all_gather(all_ao, ao, group=group)
-    ao_np = np.stack([t.cpu().numpy().view(np.uint64) for t in all_ao])
-    p0 = first_varying_byte(ao_np, layout.key_size)
+    p0 = first_varying_byte(_all_gather_np(ops.andor(data, n, layout).astype(np.uint64), dev, group),
+                            layout.key_size)
     if p0 >= layout.key_size:
         p0 = 0  # every key equal: any contiguous map is correct
     # 2. 16-bit prefix histograms, all-gathered
-    h = ops.prefix_hist(data, n, layout, p0).to(dev)
-    all_h = [torch.empty_like(h) for _ in range(world)]
-    dist.all_gather(all_h, h, group=group)
-    hist = np.stack([t.cpu().numpy() for t in all_h]).astype(np.uint64)  # [world, 65536]
-    # 3. contiguous, count-balanced bucket ranges
-    bucket_rank = balanced_bucket_map(hist.sum(axis=0), world)
-    # per-(source rank, destination rank) counts follow from the histograms
-    src_dst = np.zeros((world, world), dtype=np.uint64)
-    for r in range(world):
-        src_dst[r] = np.bincount(bucket_rank, weights=hist[r].astype(np.float64),
-                                 minlength=world).astype(np.uint64)
-    return ExchangePlan(p0, bucket_rank, src_dst[rank].copy(), src_dst[:, rank].copy(), src_dst)
+    h = ops.prefix_hist(data, n, layout, p0).cpu().numpy().astype(np.int64)
+    hist = _all_gather_np(h, dev, group).astype(np.int64)  # [world, 65536]
+    # 3. digits, hot single-key digits, exact counts, pieces
+    digits = make_digits(hist.sum(axis=0), world, p0)
+    split = _splittable(ops, data, n, layout, digits, group)
+    M = np.stack([np.bincount(digits.bucket_digit, weights=hist[r].astype(np.float64),
+                              minlength=digits.n_digits) for r in range(world)]).astype(np.int64)
+    pieces, S = assign_pieces(M, split, world)
+    return ExchangePlan(digits, M, pieces, S)
 
 
 SAMPLE_ANDOR = 1 << 16
@@ -220,52 +378,43 @@ SAMPLE_HIST = 1 << 20
 
 def plan_exchange_sampled(ops, data, n: int, layout: RecordLayout, group=None):
     """The exchange plan without a full read of the data before the
-    partition: the prefix byte and the bucket map come from strided samples
-    (the map only has to be balanced), and the exact send/receive counts plus
+    partition: the prefix byte and the digit map come from strided samples
+    (the map only has to be balanced), and the exact per-digit counts plus
     the exact AND/OR come from the partition's own tile histogram
     (ops.partition_plan), all-gathered. Returns (plan, ok): ok is False on
     every rank when the exact AND/OR shows a more significant varying byte
     than the sample's (a byte that varies only off-sample); the caller then
-    plans exactly (plan_exchange)."""
-    import torch
+    plans exactly (plan_exchange). On success the device holds the armed
+    partition plan (partition_store_pieces follows)."""
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
     ks = layout.key_size
-    dev = data.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    dev = _coll_device(data, group)
     # 1. sampled AND/OR -> the guessed first varying key byte
-    ao = torch.from_numpy(ops.sample_andor(data, n, layout, SAMPLE_ANDOR).view(np.int64)).to(dev)
-    all_ao = [torch.empty_like(ao) for _ in range(world)]
-    dist.all_gather(all_ao, ao, group=group)
-    p0 = first_varying_byte(np.stack([t.cpu().numpy().view(np.uint64) for t in all_ao]), ks)
+    sao = ops.sample_andor(data, n, layout, SAMPLE_ANDOR).astype(np.uint64)
+    p0 = first_varying_byte(_all_gather_np(sao, dev, group), ks)
     if p0 >= ks:
         p0 = 0
     # 2. sampled 16-bit prefix histograms, each weighted by its rank's record count
-    h = ops.sample_prefix_hist(data, n, layout, p0, SAMPLE_HIST).to(dev)
-    all_h = [torch.empty_like(h) for _ in range(world)]
-    dist.all_gather(all_h, h, group=group)
-    nn = torch.tensor([n], dtype=torch.int64, device=dev)
-    all_n = [torch.empty_like(nn) for _ in range(world)]
-    dist.all_gather(all_n, nn, group=group)
+    h = ops.sample_prefix_hist(data, n, layout, p0, SAMPLE_HIST).cpu().numpy().astype(np.int64)
+    row = np.concatenate([h, [n]]).astype(np.int64)
+    rows = _all_gather_np(row, dev, group)
     weights = np.zeros(NBUCKETS, dtype=np.float64)
-    for t, tn in zip(all_h, all_n):
-        hr = t.cpu().numpy().astype(np.float64)
-        s_r = hr.sum()
-        if s_r > 0:
-            weights += hr * (float(tn.item()) / s_r)
-    bucket_rank = balanced_bucket_map(weights, world)
-    # 3. exact counts and AND/OR from the partition's histogram, all-gathered
-    counts, andor = ops.partition_plan(data, n, layout, p0, bucket_rank, world)
-    row = torch.from_numpy(np.concatenate([counts, andor]).view(np.int64)).to(dev)
-    rows = [torch.empty_like(row) for _ in range(world)]
-    dist.all_gather(rows, row, group=group)
-    m = np.stack([t.cpu().numpy().view(np.uint64) for t in rows])  # [world, world + 8]
-    src_dst = m[:, :world].copy()
-    p_exact = first_varying_byte(m[:, world:], ks)
+    for r in range(world):
+        hr = rows[r, :NBUCKETS].astype(np.float64)
+        if hr.sum() > 0:
+            weights += hr * (float(rows[r, NBUCKETS]) / hr.sum())
+    digits = make_digits(weights, world, p0)
+    split = _splittable(ops, data, n, layout, digits, group)
+    # 3. exact per-digit counts and AND/OR from the partition's histogram, all-gathered
+    counts, andor = ops.partition_plan(data, n, layout, p0, digits.bucket_digit, digits.n_digits)
+    m = _all_gather_np(np.concatenate([counts.astype(np.uint64), andor.astype(np.uint64)]), dev, group)
+    M = m[:, :digits.n_digits].astype(np.int64)
+    p_exact = first_varying_byte(m[:, digits.n_digits:], ks)
     if p_exact >= ks:
         p_exact = 0
-    plan = ExchangePlan(p0, bucket_rank, src_dst[rank].copy(), src_dst[:, rank].copy(), src_dst)
-    return plan, p_exact == p0
+    pieces, S = assign_pieces(M, split, world)
+    return ExchangePlan(digits, M, pieces, S), p_exact == p0
 
 
 class _CudaBytes:
@@ -349,6 +498,35 @@ def release_peer_windows() -> None:
     _windows.clear()
 
 
+def _piece_destinations(plan: ExchangePlan, rank: int, rs: int, bases) -> tuple:
+    """This source's pieces with their byte addresses in the receivers'
+    windows: receiver k holds its sources' records source-major, each
+    source's pieces in digit order."""
+    S = plan.matrix
+    run = {k: int(S[:rank, k].sum()) for k in range(S.shape[1])}
+    dg, ct, ds = [], [], []
+    for d, k, c in plan.pieces[rank]:
+        dg.append(d)
+        ct.append(c)
+        ds.append(bases[k] + run[k] * rs)
+        run[k] += c
+    return (np.array(dg, dtype=np.uint32), np.array(ct, dtype=np.uint64), np.array(ds, dtype=np.uint64))
+
+
+def _all_to_all(recv, send, out_splits, in_splits, group):
+    """dist.all_to_all_single; gloo cannot move CUDA tensors, so there the
+    exchange is staged through host memory (tests on one shared device)."""
+    import torch.distributed as dist
+    if dist.get_backend(group) != "nccl" and send.is_cuda:
+        r = recv.new_empty(recv.numel(), device="cpu")
+        dist.all_to_all_single(r, send.cpu(), output_split_sizes=out_splits,
+                               input_split_sizes=in_splits, group=group)
+        recv.copy_(r)
+        return
+    dist.all_to_all_single(recv, send, output_split_sizes=out_splits, input_split_sizes=in_splits,
+                           group=group)
+
+
 def sort_distributed(data, n: int, layout: RecordLayout, ops=None, group=None,
                      timings: dict | None = None, exchange: str | None = None):
     """Sort `n` local records (uint8 tensor on this rank's device) across the
@@ -357,10 +535,16 @@ def sort_distributed(data, n: int, layout: RecordLayout, ops=None, group=None,
 
     exchange="p2p" (default with DeviceOps on CUDA): the partition kernel
     stores every destination's records straight into that rank's receive
-    window over NVLink (CUDA IPC; raduls_gpu_partition_to) — the partition and
-    the all-to-all are one kernel. The returned tensor then aliases this
-    rank's cached window and stays valid until the next call on the group.
-    exchange="nccl": local partition, then one NCCL all_to_all_single."""
+    window over NVLink (CUDA IPC; raduls_gpu_partition_store_pieces) — the
+    partition and the all-to-all are one kernel. The returned tensor then
+    aliases this rank's cached window and stays valid until the next call on
+    the group. exchange="nccl": local partition by digit, then one NCCL
+    all_to_all_single (host-staged under gloo).
+
+    timings (optional dict) receives plan_s, exchange_ms (device time of the
+    exchange: the fused partition kernel, or the all-to-all), partition_ms
+    (nccl path), local_sort_s, sent_bytes (records leaving this rank * rs),
+    recv_records and exchange ("p2p" or "nccl")."""
     import time
 
     import torch
@@ -372,62 +556,81 @@ def sort_distributed(data, n: int, layout: RecordLayout, ops=None, group=None,
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     rs = layout.record_size
+    cuda = data.is_cuda
+
+    def event():
+        if not cuda:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(torch.cuda.current_stream(data.device))
+        return e
+
+    def elapsed(e0, e1) -> float | None:
+        if e0 is None:
+            return None
+        e1.synchronize()
+        return e0.elapsed_time(e1)
+
     t0 = time.perf_counter()
-    planned = False  # the partition's counts pass already ran (ops.partition_plan)
-    if exchange == "p2p":
-        plan, planned = plan_exchange_sampled(ops, data, n, layout, group)
-        if not planned:  # a key byte varies only off the sample: plan exactly
-            plan = plan_exchange(ops, data, n, layout, group)
-    else:
-        plan = plan_exchange(ops, data, n, layout, group)
     win = None
     if exchange == "p2p":
-        win = _peer_windows(max(int(plan.matrix.sum(axis=0).max()), 1) * rs, group, data.device)
-    if win is not None:
-        matrix = plan.matrix
-        n_out = int(plan.recv_counts.sum())
-        dst = np.array([win.ptrs[r] + int(matrix[:rank, r].sum()) * rs for r in range(world)],
-                       dtype=np.uint64)
-        torch.cuda.synchronize(data.device)
-        dist.barrier(group=group)  # every window free (previous results consumed)
-        if planned:
-            ops.partition_store(data, n, layout, dst)
-        else:
-            counts = ops.partition_to(data, n, layout, plan.p0, plan.bucket_rank, world, dst)
-            if not np.array_equal(counts, plan.send_counts):
+        plan, armed = plan_exchange_sampled(ops, data, n, layout, group)
+        if not armed:  # a key byte varies only off the sample: plan exactly, re-arm the device plan
+            plan = plan_exchange(ops, data, n, layout, group)
+            counts, _ = ops.partition_plan(data, n, layout, plan.p0, plan.digits.bucket_digit,
+                                           plan.digits.n_digits)
+            if not np.array_equal(counts.astype(np.int64), plan.M[rank]):
                 raise RuntimeError("partition counts disagree with the exchanged histograms")
+        win = _peer_windows(max(int(plan.matrix.sum(axis=0).max()), 1) * rs, group, data.device)
+        if win is None:  # IPC unavailable on some rank: the NCCL exchange below
+            exchange = "nccl"
+    else:
+        plan = plan_exchange(ops, data, n, layout, group)
+    n_out = int(plan.recv_counts(rank).sum())
+    t1 = time.perf_counter()
+    info = {"exchange": exchange, "plan_s": t1 - t0, "recv_records": n_out,
+            "sent_bytes": int((plan.send_counts(rank).sum() - plan.send_counts(rank)[rank]) * rs),
+            "hot_split_digits": int(sum(1 for d in range(plan.digits.n_digits)
+                                        if len({k for s in plan.pieces for (dd, k, _) in s if dd == d}) > 1))}
+    if win is not None:
+        dg, ct, ds = _piece_destinations(plan, rank, rs, win.ptrs)
+        if cuda:
+            torch.cuda.synchronize(data.device)
+        dist.barrier(group=group)  # every window free (previous results consumed)
+        e0 = event()
+        ops.partition_store_pieces(data, n, layout, dg, ct, ds)
+        e1 = event()
+        info["exchange_ms"] = elapsed(e0, e1)
         dist.barrier(group=group)  # every rank's stores into every window are complete
         t2 = time.perf_counter()
         recv = torch.as_tensor(_CudaBytes(win.own, max(n_out, 1) * rs), device=data.device)
         tmp = ops.empty(max(n_out, 1) * rs)
         ops.sort(recv, n_out, layout, tmp)
-        t3 = time.perf_counter()
-        if timings is not None:
-            timings.update(plan_partition_exchange_s=t2 - t0, local_sort_s=t3 - t2,
-                           sent_bytes=int((plan.send_counts.sum() - plan.send_counts[rank]) * rs))
-        return recv, n_out
-    # 4. local stable partition into send ranges
-    send, counts = ops.partition(data, n, layout, plan.p0, plan.bucket_rank, world)
-    if not np.array_equal(counts, plan.send_counts):
-        raise RuntimeError("partition counts disagree with the exchanged histograms")
-    t1 = time.perf_counter()
-    # 5. one all-to-all of the records
-    n_out = int(plan.recv_counts.sum())
-    recv = ops.empty(n_out * rs)
-    dist.all_to_all_single(recv, send,
-                           output_split_sizes=[int(c) * rs for c in plan.recv_counts],
-                           input_split_sizes=[int(c) * rs for c in plan.send_counts],
-                           group=group)
-    if recv.is_cuda:
-        torch.cuda.synchronize(recv.device)
-    t2 = time.perf_counter()
-    del send
-    # 6. local sort of the received key range
-    ops.sort(recv, n_out, layout)
+    else:
+        # local stable partition by digit (pieces of a digit stay in rank order)
+        e0 = event()
+        send, counts = ops.partition(data, n, layout, plan.p0, plan.digits.bucket_digit,
+                                     plan.digits.n_digits)
+        e1 = event()
+        if not np.array_equal(np.asarray(counts, dtype=np.int64), plan.M[rank]):
+            raise RuntimeError("partition counts disagree with the exchanged histograms")
+        recv = ops.empty(max(n_out, 1) * rs)
+        e2 = event()
+        _all_to_all(recv[:n_out * rs] if n_out else recv[:0], send[:n * rs],
+                    [int(c) * rs for c in plan.recv_counts(rank)],
+                    [int(c) * rs for c in plan.send_counts(rank)], group)
+        e3 = event()
+        info["partition_ms"] = elapsed(e0, e1)
+        info["exchange_ms"] = elapsed(e2, e3)
+        del send
+        t2 = time.perf_counter()
+        ops.sort(recv, n_out, layout)
+    if cuda:
+        torch.cuda.synchronize(data.device)
     t3 = time.perf_counter()
+    info["local_sort_s"] = t3 - t2
     if timings is not None:
-        timings.update(plan_partition_s=t1 - t0, exchange_s=t2 - t1, local_sort_s=t3 - t2,
-                       sent_bytes=int((plan.send_counts.sum() - plan.send_counts[dist.get_rank(group)]) * rs))
+        timings.update(info)
     return recv, n_out
 
 

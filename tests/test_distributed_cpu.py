@@ -78,6 +78,20 @@ class CpuOps:
         r = data.numpy()[:n * rs].reshape(n, rs)[order]
         return torch.from_numpy(r.reshape(-1).copy()), np.bincount(dest, minlength=world).astype(np.uint64)
 
+    def digit_andor(self, data, n, layout, p0, bucket_digit, hot):
+        rs, ks = layout.record_size, layout.key_size
+        out = np.zeros((len(hot), 8), dtype=np.uint64)
+        out[:, 0::2] = ~np.uint64(0)
+        dig = bucket_digit[self._prefix(data, n, layout, p0)]
+        w = data.numpy()[:n * rs].reshape(n, rs).view("<u8")
+        for d in np.nonzero(hot)[0]:
+            sel = w[dig == d]
+            if len(sel):
+                for k in range((ks + 7) // 8):
+                    out[d, 2 * k] = np.bitwise_and.reduce(sel[:, k])
+                    out[d, 2 * k + 1] = np.bitwise_or.reduce(sel[:, k])
+        return out
+
     def sort(self, data, n, layout, tmp=None):
         import oracle
         rs = layout.record_size
@@ -85,18 +99,49 @@ class CpuOps:
         a[:] = oracle.stable_sort(a.copy(), rs, layout.key_size)
 
 
-def _worker(rank, world, port, rs, ks, dist_kind, q):
+def _input(rank, world, rs, ks, dist_kind, hot=0.0, n_total=40000):
+    """This rank's share of the global input; hot > 0: that fraction of the
+    records (spread over every rank) carries one key."""
+    import oracle
+    n_local = n_total // world
+    a = oracle.generate(n_local, rs, ks, dist_kind, 0x5EED0001, rank * n_local)
+    if hot:
+        r = a.reshape(n_local, rs)
+        rng = np.random.default_rng(1000 + rank)
+        sel = rng.random(n_local) < hot
+        r[sel, :ks] = np.frombuffer(bytes(range(0x40, 0x40 + ks)), dtype=np.uint8)
+    return a
+
+
+def _worker(rank, world, port, rs, ks, dist_kind, q, hot=0.0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    import oracle
-    n_total = 40000
-    n_local = n_total // world
-    a = oracle.generate(n_local, rs, ks, dist_kind, 0x5EED0001, rank * n_local)
+    a = _input(rank, world, rs, ks, dist_kind, hot)
+    n_local = a.size // rs
+    t = {}
     out, n_out = D.sort_distributed(torch.from_numpy(a.copy()), n_local, RecordLayout(rs, ks),
-                                    ops=CpuOps())
-    q.put((rank, out.numpy()[:n_out * rs].copy()))
+                                    ops=CpuOps(), timings=t)
+    q.put((rank, out.numpy()[:n_out * rs].copy(), t))
     dist.destroy_process_group()
+
+
+def _run_world(world, rs, ks, dist_kind, hot=0.0):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, rs, ks, dist_kind, q, hot))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, out, t = q.get(timeout=180)
+        res[r] = (out, t)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
 
 
 def _free_port():
@@ -111,20 +156,131 @@ def _free_port():
 def test_gloo_world2_distributed_sort(rs, ks, dist_kind):
     import oracle
     world = 2
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, rs, ks, dist_kind, q))
-             for r in range(world)]
-    for p in procs:
-        p.start()
-    res = dict(q.get(timeout=120) for _ in range(world))
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    got = np.concatenate([res[r] for r in range(world)])
+    res = _run_world(world, rs, ks, dist_kind)
+    got = np.concatenate([res[r][0] for r in range(world)])
     n_total = 40000
     a = oracle.generate(n_total, rs, ks, dist_kind, 0x5EED0001, 0)
     assert np.array_equal(got, oracle.stable_sort(a, rs, ks))
     # both ranks got work (balanced contiguous ranges)
-    assert all(res[r].size > 0 for r in range(world))
+    assert all(res[r][0].size > 0 for r in range(world))
+    assert all(res[r][1]["exchange"] == "nccl" for r in range(world))
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_gloo_hot_key_is_split_over_ranks(world):
+    """60% of the records share one key: the hot 16-bit bucket holds a single
+    key, so its records are spread over consecutive ranks by count (SURVEY.md
+    §8(e) step 4) instead of landing on one rank; the concatenation is still
+    the stable sort of the concatenated inputs."""
+    import oracle
+    rs, ks = 16, 8
+    res = _run_world(world, rs, ks, 0, hot=0.6)
+    got = np.concatenate([res[r][0] for r in range(world)])
+    a = np.concatenate([_input(r, world, rs, ks, 0, 0.6) for r in range(world)])
+    assert np.array_equal(got, oracle.stable_sort(a, rs, ks))
+    n_total = a.size // rs
+    sizes = [res[r][0].size // rs for r in range(world)]
+    assert max(sizes) <= n_total / world * 1.30 + 1, sizes
+    assert all(res[r][1]["hot_split_digits"] >= 1 for r in range(world))
+
+
+def test_gloo_hot_bucket_with_two_keys_is_not_split():
+    """A hot 16-bit bucket holding two different keys must not be cut by
+    count (the cut could order them wrongly across ranks): it stays whole."""
+    import oracle
+    world, rs, ks = 2, 16, 8
+    ctx_res = _run_world_two_keys(world, rs, ks)
+    got = np.concatenate([ctx_res[r][0] for r in range(world)])
+    a = np.concatenate([_two_key_input(r, world, rs, ks) for r in range(world)])
+    assert np.array_equal(got, oracle.stable_sort(a, rs, ks))
+    assert all(ctx_res[r][1]["hot_split_digits"] == 0 for r in range(world))
+
+
+def _two_key_input(rank, world, rs, ks, n_total=40000):
+    a = _input(rank, world, rs, ks, 0)
+    r = a.reshape(-1, rs)
+    rng = np.random.default_rng(7 + rank)
+    sel = rng.random(len(r)) < 0.6
+    key = np.frombuffer(bytes(range(0x40, 0x40 + ks)), dtype=np.uint8).copy()
+    r[sel, :ks] = key
+    key[ks - 1] ^= 1  # same 16-bit prefix, a different key
+    r[sel & (rng.random(len(r)) < 0.5), :ks] = key
+    return a
+
+
+def _worker_two_keys(rank, world, port, rs, ks, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a = _two_key_input(rank, world, rs, ks)
+    t = {}
+    out, n_out = D.sort_distributed(torch.from_numpy(a.copy()), a.size // rs, RecordLayout(rs, ks),
+                                    ops=CpuOps(), timings=t)
+    q.put((rank, out.numpy()[:n_out * rs].copy(), t))
+    dist.destroy_process_group()
+
+
+def _run_world_two_keys(world, rs, ks):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_two_keys, args=(r, world, port, rs, ks, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, out, t = q.get(timeout=180)
+        res[r] = (out, t)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+def test_assign_pieces_monotone_and_exact():
+    """Host logic of the hot-key split: every record gets exactly one rank,
+    ranks are non-decreasing along (digit, source, position), a splittable
+    digit is cut near the ideal rank boundaries, plain digits stay whole."""
+    rng = np.random.default_rng(3)
+    for world in (2, 3, 4, 8):
+        for _ in range(20):
+            D_ = int(rng.integers(1, 12))
+            M = rng.integers(0, 50, size=(world, D_))
+            hot = rng.integers(0, D_)
+            M[:, hot] += rng.integers(100, 400, size=world)
+            split = np.zeros(D_, dtype=bool)
+            split[hot] = bool(rng.integers(0, 2))
+            pieces, S = D.assign_pieces(M, split, world)
+            assert S.sum() == M.sum()
+            for s in range(world):
+                per_digit = {}
+                for d, k, c in pieces[s]:
+                    per_digit[d] = per_digit.get(d, 0) + c
+                assert all(per_digit.get(d, 0) == M[s, d] for d in range(D_))
+                assert S[s].sum() == M[s].sum()
+            # global rank sequence in (digit, source) order is monotone
+            seq = []
+            for d in range(D_):
+                for s in range(world):
+                    seq += [k for dd, k, c in pieces[s] if dd == d for _ in range(c)]
+            assert all(x <= y for x, y in zip(seq, seq[1:]))
+            for d in range(D_):
+                ranks = {k for s in range(world) for dd, k, _ in pieces[s] if dd == d}
+                if not split[d]:
+                    assert len(ranks) <= 1
+    # one dominating single-key digit over 4 ranks: near-perfect balance
+    M = np.array([[10, 600, 30]] * 4)
+    pieces, S = D.assign_pieces(M, np.array([False, True, False]), 4)
+    loads = S.sum(axis=0)
+    assert loads.max() - loads.min() <= 45, loads
+
+
+def test_make_digits_hot_bucket_gets_own_digit():
+    w = np.ones(D.NBUCKETS)
+    w[1000] = D.NBUCKETS  # ~50% of the weight
+    plan = D.make_digits(w, 4)
+    d = plan.bucket_digit
+    assert np.all(np.diff(d.astype(np.int64)) >= 0)
+    assert d[999] != d[1000] != d[1001]
+    assert plan.hot[d[1000]] and plan.hot.sum() == 1
+    assert plan.n_digits <= 4 + 2
