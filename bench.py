@@ -8,7 +8,10 @@ A "step" is one complete sort of one batch: at N=1 the whole workload
 (default C5: 2^32 records of 16 B, the paper's headline scale, BASELINE.json
 configs[4]) through libraduls_gpu.so; at N>1 (torchrun, one rank per GPU) the
 same total partitioned across ranks by key range (strong scaling) and
-exchanged once with an NCCL all-to-all (paper_1612_02557_b200/distributed.py).
+exchanged once (paper_1612_02557_b200/distributed.py), timed with both
+exchanges — the partition kernel storing straight into peer windows over
+NVLink ("p2p") and a local partition plus an NCCL all-to-all ("nccl") — the
+faster one headlined, both reported with their NVLink fraction.
 
 Timing: inputs are regenerated on the device before every step (untimed:
 the sort is in place); the timed region is the sort call only, bracketed
@@ -19,7 +22,8 @@ roofline of the dominant kernel; `e2e` repeats the measurement through the
 host-memory drop-in (pinned host buffer, H2D + sort + D2H inside the timed
 region); `cpu_baseline` times the reference CPU sorter (oracle/_ref, the
 unmodified reference library compiled here) on a bounded sample on the
-box's host cores.
+box's host cores (the whole config when host RAM holds it); per_config
+adds C1-C4 measured in the same run.
 """
 from __future__ import annotations
 
@@ -129,32 +133,91 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ CPU baseline / reference arm
 
-def cpu_sample(cfg_name: str, n_sample: int):
+def mem_available() -> int:
+    """MemAvailable of this host in bytes (0 if unknown)."""
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def _host_chunks(n: int, threads: int):
+    step = max(1, -(-n // max(1, threads)))
+    return [(a, min(n, a + step)) for a in range(0, n, step)]
+
+
+def host_generate(out, n: int, rs: int, ks: int, dist: int, seed: int, threads: int) -> None:
+    """The §8(d) generator (oracle/liboracle.so, bit-identical to the device
+    k_gen) into the numpy buffer `out`, chunked over host threads (ctypes
+    releases the GIL). Input preparation only: never timed."""
+    import ctypes as C
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+    L = oracle.lib()
+    base = out.ctypes.data
+
+    def one(ab):
+        a, b = ab
+        rc = L.orc_generate(C.cast(base + a * rs, oracle._u8p), b - a, rs, ks, dist, seed, a)
+        if rc:
+            raise ValueError(f"orc_generate rejected layout ({rs},{ks})")
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(one, _host_chunks(n, threads)))
+
+
+def host_sorted(a, n: int, rs: int, ks: int, threads: int) -> bool:
+    """Key order of n records, chunked over threads plus the chunk seams."""
+    import ctypes as C
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+    L = oracle.lib()
+    base = a.ctypes.data
+    ch = _host_chunks(n, threads)
+
+    def one(ab):
+        x, y = ab
+        v = C.c_uint64(0)
+        return bool(L.orc_check_sorted(C.cast(base + x * rs, oracle._u8p), y - x, rs, ks, C.byref(v)))
+
+    with ThreadPoolExecutor(threads) as ex:
+        ok = all(ex.map(one, ch))
+    for (_, y), (x2, _) in zip(ch, ch[1:]):  # seams
+        if bytes(a[(y - 1) * rs:(y - 1) * rs + ks]) > bytes(a[x2 * rs:x2 * rs + ks]):
+            ok = False
+    return ok
+
+
+def run_cpu_reference(cfg_name: str, n_cap: int, steps: int, warmup: int,
+                      threads: int | None = None) -> dict:
+    """The reference CPU sorter (oracle/_ref: the unmodified reference library
+    compiled here; else the plain-C port at T=1) on the first min(n, n_cap)
+    records of a config, `threads` host threads (default: the physical cores,
+    counted as P/tests/acceptance.cpp:52-66 does). Input regenerated before
+    every run (untimed), as P/src/bench.cpp:121-125 re-copies it."""
     import numpy as np
 
     import oracle
     n, rs, ks, dist, seed, _ = CONFIGS[cfg_name]
-    n_s = min(n, n_sample)
-    a = oracle.generate(n_s, rs, ks, dist, seed, 0)
-    return a, n_s, rs, ks, np
-
-
-def run_cpu_reference(cfg_name: str, n_sample: int, steps: int, warmup: int) -> dict:
-    """The reference CPU sorter on the host cores (oracle/_ref when built, else the
-    plain-C port). Returns a dict with records/s over `steps` timed runs."""
-    import oracle
-    a, n_s, rs, ks, np = cpu_sample(cfg_name, n_sample)
-    threads = os.cpu_count() or 1
+    n_s = min(n, n_cap)
+    cores = oracle.host_cores()
+    threads = threads or cores
     kind = "reference" if oracle.ref_available() else "port"
     proxy = ""
     rks = ks
     if kind == "reference" and ks not in (8, 16):
         rks = 16  # the reference rejects ks=24: (32,16) proxy, exact on these inputs (SURVEY §8(c))
         proxy = f" (run as layout ({rs},16): the reference rejects key_size={ks})"
-    work = np.empty_like(a)
+    work = np.empty(n_s * rs, dtype=np.uint8)
     times = []
     for i in range(warmup + steps):
-        work[:] = a
+        host_generate(work, n_s, rs, ks, dist, seed, cores)
         t0 = time.perf_counter()
         if kind == "reference":
             rc = oracle.ref().ref_sort(oracle._ptr(work), n_s, rs, rks, threads)
@@ -165,12 +228,24 @@ def run_cpu_reference(cfg_name: str, n_sample: int, steps: int, warmup: int) -> 
         dt = time.perf_counter() - t0
         if i >= warmup:
             times.append(dt)
-    ok, _ = oracle.check_sorted(work, rs, ks)
+    ok = host_sorted(work, n_s, rs, ks, cores)
+    del work
+    what = "all" if n_s == n else f"first {n_s}"
     return {"value": n_s * len(times) / sum(times), "unit": UNIT,
             "cores": threads if kind == "reference" else 1, "kind": kind,
-            "sample": f"first {n_s} records of the {cfg_name.upper()} generator{proxy}; "
-                      f"median run {statistics.median(times)*1e3:.1f} ms; sorted={ok}",
-            "ms_per_step": 1e3 * sum(times) / len(times), "steps": len(times)}
+            "sample": f"{what} records of the {cfg_name.upper()} generator{proxy}; {len(times)} runs, "
+                      f"median {statistics.median(times)*1e3:.1f} ms; {threads} threads "
+                      f"({cores} physical cores); sorted={ok}",
+            "ms_per_step": 1e3 * sum(times) / len(times), "steps": len(times),
+            "records": n_s, "same_config": n_s == n, "threads": threads}
+
+
+def reference_cap(cfg_name: str) -> int:
+    """The whole config when this host can hold it (data + the reference's own
+    aux buffer + headroom), else a 2^28-record prefix."""
+    n, rs = CONFIGS[cfg_name][0], CONFIGS[cfg_name][1]
+    need = 2 * n * rs + (16 << 30)
+    return n if mem_available() >= need else min(n, 1 << 28)
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -181,11 +256,89 @@ def algorithmic_bytes(stats: dict, rs: int) -> dict:
     record read from the digit array, which the scatter before wrote)."""
     nd = stats.get("hist_digit_records", 0)
     return {
-        "scatter": 2 * rs * stats["scatter_records"],
-        "local_sort": 2 * rs * stats["local_records"],
-        "copy_back": 2 * rs * stats["copy_records"],
-        "tile_hist": rs * stats["hist_records"] + nd,
+        "scatter": 2 * rs * stats.get("scatter_records", 0),
+        "local_sort": 2 * rs * stats.get("local_records", 0),
+        "copy_back": 2 * rs * stats.get("copy_records", 0),
+        "tile_hist": rs * stats.get("hist_records", 0) + nd,
     }
+
+
+def kernel_table(kt: dict, ab: dict) -> dict:
+    return {k: {"launches": l, "ms": round(t, 3),
+                "GBps": round(ab[k] / (t / 1e3) / 1e9, 1) if ab.get(k) and t else None}
+            for k, (l, t) in kt.items()}
+
+
+def dominant(kt: dict, ab: dict, peak: float, peak_src: str) -> dict | None:
+    """Roofline of the kernel class with the most device time (live CUDA events)."""
+    if not kt:
+        return None
+    dom = max(kt, key=lambda k: kt[k][1])
+    dl, dt = kt[dom]
+    db = ab.get(dom, 0)
+    achieved = db / (dt / 1e3) / 1e9 if dt else 0.0
+    return {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+            "algorithmic_bytes_per_launch": db / max(dl, 1), "launches": dl, "peak_source": peak_src}
+
+
+def sort_roofline(ab: dict, total_ms: float, steps: int, peak: float, n: int, rs: int,
+                  n_gpus: int = 1) -> dict:
+    alg = ab.get("scatter", 0) + ab.get("local_sort", 0) + ab.get("copy_back", 0) + \
+        ab.get("partition", 0) + ab.get("partition_exchange", 0)
+    gbs = alg / (total_ms / 1e3) / 1e9
+    return {"achieved": round(gbs, 1), "peak": peak * n_gpus, "unit": "GB/s",
+            "frac": round(gbs / (peak * n_gpus), 4), "algorithmic_bytes_per_step": alg / steps,
+            "passes_per_record": round(alg / steps / (2 * rs * n), 3)}
+
+
+def measure_config(rg, torch, dev, cfg_name: str, steps: int, warmup: int, peak: float,
+                   peak_src: str) -> dict:
+    """One single-GPU config: device-resident sorts timed by CUDA events on the
+    sort's stream, per-kernel times, digest + order verified (untimed)."""
+    n, rs, ks, dist_kind, seed, desc = CONFIGS[cfg_name]
+    lay = rg.RecordLayout(rs, ks)
+    data = torch.empty(n * rs, dtype=torch.uint8, device=dev)
+    tmp = torch.empty_like(data)
+    stream = torch.cuda.current_stream(dev)
+    rg.generate(n, lay, dist=dist_kind, seed=seed, out=data)
+    d_in = rg.digest(data, n, rs)
+    kt: dict = {}
+    st: dict = {}
+    ms = []
+    launches = 0
+    for i in range(warmup + steps):
+        rg.generate(n, lay, dist=dist_kind, seed=seed, out=data)
+        rg.set_profiling(i >= warmup)
+        torch.cuda.synchronize(dev)
+        c0 = rg.launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rg.sort(data, n, lay, tmp=tmp, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if i >= warmup:
+            launches += rg.launch_count() - c0
+            ms.append(e0.elapsed_time(e1))
+            for k, (l, t) in rg.last_kernel_times().items():
+                kt.setdefault(k, [0, 0.0])
+                kt[k][0] += l
+                kt[k][1] += t
+            for k, v in rg.last_stats().items():
+                st[k] = st.get(k, 0) + v
+    rg.set_profiling(False)
+    viol, _ = rg.check_sorted(data, n, lay)
+    ok = viol == 0 and rg.digest(data, n, rs) == d_in
+    del data, tmp
+    torch.cuda.empty_cache()
+    ab = algorithmic_bytes(st, rs)
+    tot = sum(ms)
+    return {"workload": desc, "ms_per_sort": round(tot / len(ms), 3),
+            "value": n * len(ms) / (tot / 1e3), "unit": UNIT, "steps": len(ms), "verified": ok,
+            "roofline": dominant(kt, ab, peak, peak_src),
+            "roofline_sort": sort_roofline(ab, tot, len(ms), peak, n, rs),
+            "kernels": kernel_table(kt, ab), "gpu_launches": launches,
+            "stats_per_step": {k: v // len(ms) for k, v in st.items()}}
 
 
 def main():
@@ -197,8 +350,11 @@ def main():
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-sample", type=int, default=1 << 26)
+    ap.add_argument("--cpu-cap", type=int, default=0,
+                    help="records of the reference run (0: the whole config when host RAM allows)")
+    ap.add_argument("--exchange", default="both", choices=["both", "p2p", "nccl"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "gpu" else args.warmup
 
@@ -210,33 +366,31 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        r = run_cpu_reference(args.config, args.cpu_sample, max(1, args.steps), args.warmup)
-        line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
-                "steps": r["steps"], "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "u8", "data": "synthetic (SURVEY.md §8(d) counter-based generator)",
-                "impl": "reference",
-                "config": {"workload": desc, "n_records": n_total, "record_size": rs,
-                           "key_size": ks, "sample_records": min(n_total, args.cpu_sample)},
-                "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        return 0
+        return reference_arm(args, n_total, rs, ks, desc)
 
     import torch
 
     import paper_1612_02557_b200 as rg
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # RADULS_BENCH_BACKEND=gloo + RADULS_BENCH_DEVICE=0: every rank on one shared
+    # device (the -m gpu test of this N>1 path on a one-GPU box; ranks meet only
+    # at host barriers, no kernel waits on another rank). Default: NCCL, GPU = local rank.
+    backend = os.environ.get("RADULS_BENCH_BACKEND", "nccl")
+    dev_index = int(os.environ.get("RADULS_BENCH_DEVICE", local_rank))
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    coll_dev = dev if backend == "nccl" else torch.device("cpu")
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     lay = rg.RecordLayout(rs, ks)
     n_local = n_total // world
     base = rank * n_local
     if rank == world - 1:
         n_local = n_total - base
+    peak, peak_src = load_peaks()
 
     def barrier():
         if world > 1:
@@ -245,21 +399,31 @@ def main():
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
-    # ---------------- device-resident measurement
+    def gather(obj):
+        if world == 1:
+            return [obj]
+        out = [None] * world
+        torch.distributed.all_gather_object(out, obj)
+        return out
+
+    # ---------------- device-resident measurement (one pass per exchange at N>1)
     data = torch.empty(n_local * rs, dtype=torch.uint8, device=dev)
     tmp = torch.empty_like(data) if world == 1 else None
     stream = torch.cuda.current_stream(dev)
     rg.set_profiling(False)
+    rg.generate(n_local, lay, dist=dist_kind, seed=seed, index_base=base, out=data)
+    digest_in = rg.digest(data, n_local, rs)
 
-    def one_step(timed: bool):
+    def one_step(exchange, timings):
         rg.generate(n_local, lay, dist=dist_kind, seed=seed, index_base=base, out=data)
         torch.cuda.synchronize(dev)
         barrier()
         torch.cuda.synchronize(dev)
+        c0 = rg.launch_count()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -268,135 +432,231 @@ def main():
             out, n_out = data, n_local
         else:
             from paper_1612_02557_b200.distributed import sort_distributed
-            out, n_out = sort_distributed(data, n_local, lay)
+            out, n_out = sort_distributed(data, n_local, lay, timings=timings, exchange=exchange)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
-        return e0.elapsed_time(e1), out, n_out
+        return e0.elapsed_time(e1), out, n_out, rg.launch_count() - c0
 
-    clocks = ClockSampler(local_rank)
-    clocks.start()  # before the warm-up: nvidia-smi's start-up stays outside the timed region
-    for _ in range(args.warmup):
-        _, out, n_out = one_step(False)
-        del out
-    digest_in = None
-    if world == 1:
-        rg.generate(n_local, lay, dist=dist_kind, seed=seed, index_base=base, out=data)
-        digest_in = rg.digest(data, n_local, rs)
-    rg.set_profiling(True)
-    kt_sum: dict[str, list] = {}
-    stats_sum: dict[str, int] = {}
-    step_ms = []
-    t_region0 = time.time()
-    wall0 = time.perf_counter()
-    for _ in range(args.steps):
-        ms, out, n_out = one_step(True)
-        step_ms.append(max_over_ranks(ms))
-        if world == 1:
-            for k, (l, t) in rg.last_kernel_times().items():
-                kt_sum.setdefault(k, [0, 0.0])
-                kt_sum[k][0] += l
-                kt_sum[k][1] += t
+    def measure(exchange):
+        """Warm-up + timed steps; per-rank kernel times, exchange timings,
+        launches; verification of the last step's output (untimed)."""
+        for _ in range(args.warmup):
+            _, out, n_out, _ = one_step(exchange, {})
+            del out
+        rg.set_profiling(True)
+        kt: dict = {}
+        st: dict = {}
+        xs = {"exchange_ms": 0.0, "partition_ms": 0.0, "sent_bytes": 0, "plan_s": 0.0}
+        step_ms = []
+        launches = 0
+        t_region0 = time.time()
+        for _ in range(args.steps):
+            tim: dict = {}
+            ms, out, n_out, nl = one_step(exchange, tim)
+            launches += nl
+            step_ms.append(max_over_ranks(ms))
+            for k, (l, t) in rg.last_kernel_times().items():  # this rank's (local) sort
+                kt.setdefault(k, [0, 0.0])
+                kt[k][0] += l
+                kt[k][1] += t
             for k, v in rg.last_stats().items():
-                stats_sum[k] = stats_sum.get(k, 0) + v
-    wall = time.perf_counter() - wall0
-    clk = clocks.stop((t_region0, time.time()))
-    rg.set_profiling(False)
-    # verify the last step (untimed)
-    viol, _ = rg.check_sorted(out, n_out, lay)
-    verified = viol == 0
-    if world == 1:
-        verified = verified and rg.digest(out, n_out, rs) == digest_in
-    if world > 1:
-        t = torch.tensor([0 if verified else 1], device=dev)
-        torch.distributed.all_reduce(t)
-        verified = int(t.item()) == 0
-    del out
-    total_ms = sum(step_ms)
-    value = n_total * args.steps / (total_ms / 1e3)
+                st[k] = st.get(k, 0) + v
+            for k in ("exchange_ms", "partition_ms", "sent_bytes", "plan_s"):
+                if tim.get(k) is not None:
+                    xs[k] += tim[k]
+            xs["exchange"] = tim.get("exchange")
+        t_region = (t_region0, time.time())
+        rg.set_profiling(False)
+        # verification (untimed): order, digest, and at N>1 the rank seams
+        viol, _ = rg.check_sorted(out, n_out, lay)
+        d_out = rg.digest(out, n_out, rs)
+        first = bytes(out[:ks].cpu().numpy()) if n_out else None
+        last = bytes(out[(n_out - 1) * rs:(n_out - 1) * rs + ks].cpu().numpy()) if n_out else None
+        del out
+        if world > 1 and exchange == "nccl":
+            torch.cuda.empty_cache()
+        mine = {"viol": viol, "d_in": digest_in, "d_out": d_out, "n_out": n_out, "first": first,
+                "last": last, "kt": kt, "st": st, "xs": xs, "launches": launches, "n_local": n_local}
+        return step_ms, t_region, gather(mine)
 
-    # ---------------- roofline of the dominant kernel (live CUDA-event times)
-    peak, peak_src = load_peaks()
-    roofline = None
-    kernels = {}
-    if world == 1 and kt_sum:
-        ab = algorithmic_bytes(stats_sum, rs)
-        for k, (l, t) in kt_sum.items():
-            b = ab.get(k, 0)
-            kernels[k] = {"launches": l, "ms": round(t, 3),
-                          "GBps": round(b / (t / 1e3) / 1e9, 1) if b and t else None}
-        dom = max(kt_sum, key=lambda k: kt_sum[k][1])
-        dl, dt = kt_sum[dom]
-        db = ab.get(dom, 0)
-        achieved = db / (dt / 1e3) / 1e9 if dt else 0.0
-        traffic = None
-        tfile = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
-        if os.path.exists(tfile):
-            try:
-                with open(tfile) as f:
-                    traffic = json.load(f).get(dom)
-            except Exception:  # noqa: BLE001
-                traffic = None
-        roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
-                    "unit": "GB/s", "frac": round(achieved / peak, 4),
-                    "traffic": traffic, "algorithmic_bytes_per_launch": db / max(dl, 1),
-                    "launches": dl, "peak_source": peak_src}
-        sort_alg = ab["scatter"] + ab["local_sort"] + ab["copy_back"]
-        sort_gbs = sort_alg / (total_ms / 1e3) / 1e9
-        roofline_sort = {"achieved": round(sort_gbs, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(sort_gbs / peak, 4),
-                         "algorithmic_bytes_per_step": sort_alg / args.steps,
-                         "passes_per_record": round(sort_alg / args.steps / (2 * rs * n_total), 3)}
-    else:
-        roofline_sort = None
-    gpu_launches = sum(v[0] for v in kt_sum.values()) if kt_sum else None
+    def verify(rows) -> dict:
+        m = (1 << 128) - 1
+        din = sum(r["d_in"][0] + (r["d_in"][1] << 64) for r in rows) & m
+        dout = sum(r["d_out"][0] + (r["d_out"][1] << 64) for r in rows) & m
+        seams = True
+        prev = None
+        for r in rows:
+            if r["n_out"]:
+                if prev is not None and prev > r["first"]:
+                    seams = False
+                prev = r["last"]
+        tot = sum(r["n_out"] for r in rows)
+        ok = all(r["viol"] == 0 for r in rows) and din == dout and seams and tot == n_total
+        return {"ok": ok, "inversions": sum(r["viol"] for r in rows), "digest_equal": din == dout,
+                "rank_seams_ordered": seams, "records_out": tot}
+
+    clocks = ClockSampler(dev_index)
+    clocks.start()  # before the warm-up: nvidia-smi's start-up stays outside the timed region
+    exchanges = [None] if world == 1 else (["p2p", "nccl"] if args.exchange == "both" else [args.exchange])
+    runs = {}
+    regions = []
+    for ex in exchanges:
+        step_ms, region, rows = measure(ex)
+        regions.append(region)
+        runs[ex] = (step_ms, rows)
+    clk = clocks.stop((regions[0][0], regions[-1][1]))
     if world > 1:
-        gpu_launches = None  # counted per rank only in single-GPU runs
+        from paper_1612_02557_b200.distributed import release_peer_windows
+        release_peer_windows()
+
+    def summarise(ex, step_ms, rows) -> dict:
+        total_ms = sum(step_ms)
+        ab_all: dict = {}
+        per_rank = []
+        worst = None
+        for r in rows:
+            ab = algorithmic_bytes(r["st"], rs)
+            kt = {k: tuple(v) for k, v in r["kt"].items()}
+            if ex is not None:  # the partition pass of the exchange: one read + one write of n_local
+                cls = "partition_exchange" if ex == "p2p" else "partition"
+                ms_p = r["xs"]["exchange_ms"] if ex == "p2p" else r["xs"]["partition_ms"]
+                kt[cls] = (args.steps, ms_p)
+                ab[cls] = 2 * rs * r["n_local"] * args.steps
+            for k, v in ab.items():
+                ab_all[k] = ab_all.get(k, 0) + v
+            roof = dominant(kt, ab, peak, peak_src)
+            per_rank.append({"kernel": roof["kernel"], "frac": roof["frac"]} if roof else None)
+            if roof and (worst is None or roof["frac"] < worst[0]["frac"]):
+                worst = (roof, kt, ab)
+        out = {"value": n_total * args.steps / (total_ms / 1e3), "ms_per_step": total_ms / args.steps,
+               "verified": verify(rows),
+               "roofline": worst[0] if worst else None,
+               "roofline_sort": sort_roofline(ab_all, total_ms, args.steps, peak, n_total, rs, world),
+               "kernels": kernel_table(worst[1], worst[2]) if worst else None,
+               "gpu_launches": sum(r["launches"] for r in rows),
+               "stats_per_step": {k: v // args.steps for k, v in rows[0]["st"].items()} or None}
+        if world > 1:
+            out["roofline"]["per_rank_frac"] = [p["frac"] if p else None for p in per_rank]
+            out["roofline"]["rank"] = "slowest rank (lowest frac)"
+            sent = max(r["xs"]["sent_bytes"] for r in rows) / args.steps
+            t_ex = max(r["xs"]["exchange_ms"] for r in rows) / args.steps
+            gbs = sent / (t_ex / 1e3) / 1e9 if t_ex else None
+            out["nvlink"] = {"exchange": ex, "sent_bytes_per_gpu": sent, "t_exchange_ms": round(t_ex, 3),
+                             "GBps": round(gbs, 1) if gbs else None, "peak": 900.0,
+                             "peak_source": "NVLink 5 per direction per GPU (nominal)",
+                             "frac": round(gbs / 900.0, 4) if gbs else None,
+                             "what": ("the fused partition+store kernel (reads local records, stores "
+                                      "each destination's share into its window over NVLink)"
+                                      if ex == "p2p" else "NCCL all_to_all_single"),
+                             "plan_ms": round(1e3 * max(r["xs"]["plan_s"] for r in rows) / args.steps, 3)}
+        return out
+
+    summ = {ex: summarise(ex, *runs[ex]) for ex in exchanges}
+    best = max(summ, key=lambda e: summ[e]["value"])
+    head = summ[best]
 
     del data, tmp
     torch.cuda.empty_cache()
+
+    # ---------------- C1-C4 beside the headline (N=1): same run, same box
+    per_config = None
+    if world == 1 and not args.no_per_config:
+        per_config = {}
+        for name in sorted(CONFIGS):
+            if name == args.config:
+                continue
+            try:
+                per_config[name] = measure_config(rg, torch, dev, name, 3, 2, peak, peak_src)
+            except Exception as ex:  # noqa: BLE001
+                per_config[name] = {"error": str(ex)[:200]}
+
+    # ---------------- CPU baseline (rank 0, N=1): the reference sorter on the host cores
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            r = run_cpu_reference(args.config, args.cpu_cap or reference_cap(args.config), 1, 0)
+            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "same_config")}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
+                   "sample": str(ex)[:200]}
 
     # ---------------- e2e through the host-memory drop-in
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(rg, torch, dev, lay, n_local, base, dist_kind, seed, args.e2e_steps, world,
-                      n_total, max_over_ranks, barrier)
-
-    # ---------------- CPU baseline (rank 0, N=1)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            r = run_cpu_reference(args.config, args.cpu_sample, 3, 1)
-            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
-        except Exception as ex:  # noqa: BLE001
-            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
-                   "sample": str(ex)[:200]}
+                      n_total, max_over_ranks, barrier, best)
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (SURVEY.md §8(d) counter-based generator, regenerated on device "
                     "before each step, untimed)",
             "config": {"workload": desc, "n_records": n_total, "record_size": rs, "key_size": ks,
                        "parallelism": "single GPU" if world == 1 else
-                       f"{world} GPUs: key-range partition + NCCL all-to-all",
+                       f"{world} GPUs: key-range partition, exchange={best} "
+                       "(p2p: partition kernel stores into peer windows over NVLink; "
+                       "nccl: local partition + NCCL all-to-all)",
                        "l2": "inputs >> 126 MB L2 (no flush needed)"},
-            "verified": verified,
-            "wall_s_timed_region": wall,
-            "roofline": roofline, "roofline_sort": roofline_sort, "kernels": kernels or None,
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clk,
-            "stats_per_step": {k: v // args.steps for k, v in stats_sum.items()} or None,
+            "verified": head["verified"]["ok"] if world > 1 else head["verified"]["ok"],
+            "verification": head["verified"],
+            "roofline": head["roofline"], "roofline_sort": head["roofline_sort"],
+            "kernels": head["kernels"],
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": head["gpu_launches"], "clocks": clk,
+            "stats_per_step": head["stats_per_step"],
         }
+        if world > 1:
+            line["nvlink"] = head["nvlink"]
+            line["exchanges"] = {e: {k: summ[e][k] for k in ("value", "ms_per_step", "verified", "roofline",
+                                                              "roofline_sort", "nvlink", "gpu_launches")}
+                                 for e in summ}
+            line["exchange"] = best
+        if per_config:
+            line["per_config"] = per_config
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
 
 
+def reference_arm(args, n_total, rs, ks, desc) -> int:
+    """bench.py --impl reference: the reference CPU sorter on the host cores, on
+    the same config as the GPU arm (the whole config when host RAM allows;
+    timed runs capped so the arm ends in a few minutes), plus a T=1 figure and
+    the C1 pair."""
+    cap = args.cpu_cap or reference_cap(args.config)
+    full = cap >= n_total
+    steps = max(1, min(args.steps, 4)) if full else max(1, args.steps)
+    warmup = min(args.warmup, 1) if full else args.warmup
+    r = run_cpu_reference(args.config, cap, steps, warmup)
+    extra = {}
+    try:  # T=1 (SURVEY.md §8(d)) on C1, and C1 whole at the physical cores: the same-config pair
+        r1 = run_cpu_reference("c1", CONFIGS["c1"][0], 1, 0, threads=1)
+        extra["t1_c1"] = {k: r1[k] for k in ("value", "unit", "threads", "sample")}
+        rc1 = run_cpu_reference("c1", CONFIGS["c1"][0], 3, 1)
+        extra["c1"] = {k: rc1[k] for k in ("value", "unit", "threads", "sample", "ms_per_step")}
+    except Exception as ex:  # noqa: BLE001
+        extra["error"] = str(ex)[:200]
+    line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": r["steps"], "steps_requested": args.steps, "warmup": warmup,
+            "ms_per_step": r["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u8", "data": "synthetic (SURVEY.md §8(d) counter-based generator)",
+            "impl": "reference",
+            "config": {"workload": desc, "n_records": n_total, "record_size": rs,
+                       "key_size": ks, "sample_records": r["records"], "same_config": r["same_config"]},
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "reference_extra": extra}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_e2e(rg, torch, dev, lay, n_local, base, dist_kind, seed, steps, world, n_total,
-            max_over_ranks, barrier):
+            max_over_ranks, barrier, exchange=None):
     """Same metric through the host-memory API: pinned host input, H2D + sort + D2H
     inside the timed region (raduls_gpu_sort_host at N=1; H2D + distributed sort
     + D2H into a pinned result buffer at N>1), after one untimed warm-up call."""
@@ -428,7 +688,7 @@ def run_e2e(rg, torch, dev, lay, n_local, base, dist_kind, seed, steps, world, n
         else:
             from paper_1612_02557_b200.distributed import sort_distributed
             d = host.to(dev, non_blocking=True)
-            out, n_out = sort_distributed(d, n_local, lay)
+            out, n_out = sort_distributed(d, n_local, lay, exchange=exchange)
             del d
             if res.numel() < n_out * rs:  # (skewed keys: a bigger range than planned for)
                 res = torch.empty(n_out * rs, dtype=torch.uint8, pin_memory=True)
@@ -445,7 +705,7 @@ def run_e2e(rg, torch, dev, lay, n_local, base, dist_kind, seed, steps, world, n
             "h2d_bytes_per_step": n_total * rs, "d2h_bytes_per_step": n_total * rs,
             "ms_per_step": 1e3 * sum(times) / len(times), "steps": len(times), "warmup": 1,
             "path": "raduls_gpu_sort_host (pinned host buffer)" if world == 1 else
-                    "H2D + sort_distributed + D2H"}
+                    f"H2D + sort_distributed(exchange={exchange}) + D2H"}
 
 
 if __name__ == "__main__":

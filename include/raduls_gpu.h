@@ -127,6 +127,10 @@ int raduls_gpu_last_kernel_times(raduls_gpu_kernel_time* out, int capacity, int*
  * sort is stable. The LSD baseline and raduls_gpu_split always use 1. */
 int raduls_gpu_rank_mode(int* mode);
 
+/* Kernel launches made by this library in this process so far (every kernel,
+ * every entry point; a relaxed process-wide counter). */
+int raduls_gpu_launch_count(uint64_t* count);
+
 /*
  * Building blocks (tests, benchmarks and the multi-GPU driver). All device
  * pointers; asynchronous on `stream` unless noted.

@@ -23,6 +23,7 @@ from .raduls import (  # noqa: F401
     last_stats,
     local_capacity,
     rank_mode,
+    launch_count,
     lsd_sort,
     set_profiling,
     sort,

@@ -49,6 +49,7 @@ EXPORTED = [
     "raduls_gpu_rank_mode",
     "raduls_gpu_digit_andor",
     "raduls_gpu_partition_store_pieces",
+    "raduls_gpu_launch_count",
 ]
 
 
@@ -129,6 +130,7 @@ def load(build_if_missing: bool = False):
         L.raduls_gpu_ipc_close.argtypes = [_vp]
         L.raduls_gpu_free.argtypes = [_vp]
         L.raduls_gpu_rank_mode.argtypes = [C.POINTER(C.c_int)]
+        L.raduls_gpu_launch_count.argtypes = [_u64p]
         L.raduls_gpu_digit_andor.argtypes = [_vp, _u64, _u32, _u32, _u32, _vp, _u32, _vp, _u64p, _vp]
         L.raduls_gpu_partition_store_pieces.argtypes = [_vp, _u64, _u32, _u32, _u32, _vp, _u64p, _u64p,
                                                         _vp]

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <array>
 #include <cmath>
 #include <cstdio>
@@ -76,6 +77,11 @@ struct CudaError {
     } while (0)
 
 #define RG_LAUNCH_CHECK() RG_CHECK(cudaGetLastError())
+
+// Every kernel launch of the library, process-wide (raduls_gpu_launch_count):
+// bench.py reports how many of this library's kernels ran in its timed region.
+static std::atomic<unsigned long long> g_launches{0};
+static inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 template <typename T>
 struct DevBuf {
@@ -461,14 +467,17 @@ void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t 
         const uint32_t grid = std::min<uint32_t>((ntiles + kNdWarps - 1) / kNdWarps, uint32_t(sm_count()) * 4);
         k_tile_hist_nd<TILE><<<grid, kNdWarps * 32, 0, st>>>(nd_in, ws.segs[cur].p, ws.tile_seg[cur].p,
                                                              ws.tile_cnt.p, c, ntiles);
+        note_launch();
     } else if constexpr (RS == 8) {  // one CTA per tile (see k_tile_hist_reg)
         k_tile_hist_reg<RS, TILE, kMap><<<ntiles, HistRegCfg<RS, TILE>::kThreads, 0, st>>>(
             data, tmp, ws.segs[cur].p, ws.tile_seg[cur].p, ws.tile_cnt.p, ws.seg_andor[cur].p, c, ks, map);
+        note_launch();
     } else {  // persistent, TMA-fed
         const uint32_t hgrid = std::min<uint32_t>(ntiles, uint32_t(sm_count()) * HistCfg<RS>::kCtas);
         k_tile_hist<RS, kMap, kKey1><<<hgrid, HistCfg<RS>::kThreads + 64, HistCfg<RS>::kSmem, st>>>(
             data, tmp, ws.segs[cur].p, ws.tile_seg[cur].p, ws.tile_cnt.p, ws.seg_andor[cur].p, c, ntiles, ks,
             map);
+        note_launch();
     }
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
@@ -477,6 +486,7 @@ void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t 
     pe = ws.prof.begin(K_SCAN, st);
     k_tile_scan<TILE><<<nchunks, 256, 0, st>>>(ws.segs[cur].p, ws.tile_seg[cur].p, ws.tile_cnt.p, ntiles,
                                                ws.tile_off.p, ws.seg_tot[cur].p, ws.status.p, c);
+    note_launch();
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
 }
@@ -493,6 +503,7 @@ bool atomic_rank_ok(Workspace& ws) {
             unsigned int* d_bad = reinterpret_cast<unsigned int*>(ws.acc.p + 2);
             RG_CHECK(cudaMemset(d_bad, 0, sizeof(unsigned int)));
             k_rank_selftest<<<2 * sm_count(), 256>>>(4096, d_bad);
+            note_launch();
             RG_LAUNCH_CHECK();
             unsigned int bad = 1;
             RG_CHECK(cudaMemcpy(&bad, d_bad, sizeof bad, cudaMemcpyDeviceToHost));
@@ -514,14 +525,16 @@ void launch_scatter(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_
     const size_t smem = (kMap || kPeer) ? ScatterCfg<RS>::kSmem : ScatterCfg<RS>::kSmemPlain;
     const bool atomic = !stable_ballot && atomic_rank_ok(ws);
     const int pe = ws.prof.begin(K_SCATTER, st);
-    if (atomic)
+    if (atomic) {
         k_scatter<RS, kMap, kPeer, 0><<<grid, ScatterCfg<RS>::kThreads + 32, smem, st>>>(
             data, tmp, ws.segs[cur].p, ws.seg_tot[cur].p, ws.tile_seg[cur].p, ws.tile_off.p, ntiles,
             &c->scatter_ticket, ks, map, dig_dst, nd, local_cap<RS>(), nd_in, pieces);
-    else
+    } else {
         k_scatter<RS, kMap, kPeer, 1><<<grid, ScatterCfg<RS>::kThreads + 32, smem, st>>>(
             data, tmp, ws.segs[cur].p, ws.seg_tot[cur].p, ws.tile_seg[cur].p, ws.tile_off.p, ntiles,
             &c->scatter_ticket, ks, map, dig_dst, nd, local_cap<RS>(), nd_in, pieces);
+    }
+    note_launch();
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
 }
@@ -537,6 +550,7 @@ void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, 
                                                        : ngroups;
     k_local<RS, false><<<grid, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
         data, tmp, ws.groups.p, ngroups, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
+    note_launch();
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
 }
@@ -552,6 +566,7 @@ void finish_spilled(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ks, Lev
     const uint32_t grid = LocalCfg<RS>::kMinBlocks == 1 ? std::min<uint32_t>(n, uint32_t(sm_count())) : n;
     k_local<RS, true><<<grid, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
         data, tmp, ws.spill.p, n, ks, ctr, nullptr, nullptr, 0);
+    note_launch();
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
     RG_CHECK(cudaStreamSynchronize(st));
@@ -570,6 +585,7 @@ static_assert(sizeof(LevelCounters) % 8 == 0, "LevelCounters published as u64 wo
 void publish(void* h_dst, const void* d_src, size_t bytes, cudaStream_t st) {
     k_publish<<<1, 64, 0, st>>>(static_cast<unsigned long long*>(h_dst),
                                 static_cast<const unsigned long long*>(d_src), uint32_t((bytes + 7) / 8));
+    note_launch();
     RG_LAUNCH_CHECK();
 }
 
@@ -646,18 +662,21 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
     {
         const int pi = ws.prof.begin(K_INIT, st);
         k_init_andor<<<1, 64, 0, st>>>(ws.andor0.p, 1);
+        note_launch();
         RG_LAUNCH_CHECK();
         ws.prof.end(pi, st);
     }
     const uint32_t samples = uint32_t(std::min<uint64_t>(n, 65536));
     int pe = ws.prof.begin(K_SAMPLE, st);
     k_sample_andor<RS><<<64, 256, 0, st>>>(data, n, std::max<uint64_t>(1, n / samples), samples, ws.andor0.p);
+    note_launch();
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
     // no host round trip: the guess goes straight into the level-0 segment,
     // and a check after the histogram flags (rarely) a more significant
     // varying byte; the flag is read with the level-0 plan's counters
     k_set_seg0<<<1, 32, 0, st>>>(ws.andor0.p, ks, n, ws.segs[0].p);
+    note_launch();
     RG_LAUNCH_CHECK();
     const uint32_t nt0 = uint32_t((n + TILE - 1) / TILE);
     int cur = 0;
@@ -666,12 +685,14 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         RG_CHECK(cudaMemsetAsync(ws.tile_seg[0].p, 0, nt0 * sizeof(uint32_t), st));
         const int pi = ws.prof.begin(K_INIT, st);
         k_init_andor<<<1, 64, 0, st>>>(ws.seg_andor[0].p, 1);
+        note_launch();
         RG_LAUNCH_CHECK();
         ws.prof.end(pi, st);
         RG_CHECK(cudaMemsetAsync(dctr, 0, sizeof(LevelCounters), st));
         if (ks <= 8) level_counts<RS, false, true>(ws, data, tmp, 0, nt0, dctr, st);
         else level_counts<RS>(ws, data, tmp, 0, nt0, dctr, st);
         k_check_seg0<<<1, 32, 0, st>>>(ws.seg_andor[0].p, ws.segs[0].p, ks, d_flag);
+        note_launch();
         RG_LAUNCH_CHECK();
     };
     level0_counts();
@@ -710,6 +731,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         A.side = nd_in ? 1u : 0u;
         pe = ws.prof.begin(K_PLAN, st);
         k_plan<<<nseg, 256, 0, st>>>(A);
+        note_launch();
         RG_LAUNCH_CHECK();
         ws.prof.end(pe, st);
         publish(ws.h_ctr + level, c, sizeof(LevelCounters), st);
@@ -739,6 +761,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         if (h.n_copy) {
             pe = ws.prof.begin(K_COPY, st);
             k_copy_back<RS><<<h.n_copy, 256, 0, st>>>(data, tmp, ws.copies.p);
+            note_launch();
             RG_LAUNCH_CHECK();
             ws.prof.end(pe, st);
         }
@@ -815,8 +838,10 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
                 nd_in = nd_in1;
                 nd_half = nd_half1;
                 k_rebase_segs<<<nseg, 256, 0, st>>>(ws.bsegs.p + s0, tb0, ws.segs[cur].p, ws.tile_seg[cur].p, TILE);
+                note_launch();
                 RG_LAUNCH_CHECK();
                 k_init_andor<<<(nseg * 8 + 255) / 256, 256, 0, st>>>(ws.seg_andor[cur].p, nseg);
+                note_launch();
                 RG_LAUNCH_CHECK();
                 RG_CHECK(cudaMemsetAsync(dctr + 1, 0, sizeof(LevelCounters), st));
                 if (ks <= 8) level_counts<RS, false, true>(ws, data, tmp, cur, ntiles, dctr + 1, st, ks, nullptr, nd_in);
@@ -1190,6 +1215,7 @@ void single_segment_counts(Workspace& ws, uint8_t* src, uint64_t n, uint32_t p, 
     const uint32_t nt = uint32_t((n + TILE - 1) / TILE);
     RG_CHECK(cudaMemsetAsync(ws.tile_seg[0].p, 0, nt * sizeof(uint32_t), st));
     k_init_andor<<<1, 64, 0, st>>>(ws.seg_andor[0].p, 1);
+    note_launch();
     RG_LAUNCH_CHECK();
     RG_CHECK(cudaMemsetAsync(ws.ctr.p, 0, sizeof(LevelCounters), st));
     level_counts<RS, kMap>(ws, src, src, 0, nt, ws.ctr.p, st, ks, map);
@@ -1363,6 +1389,7 @@ int raduls_gpu_generate(void* d_out, uint64_t n, uint32_t rs, uint32_t ks, uint3
         GenParams P{n, seed, index_base, ks, dist, ws.thr.p};
         dispatch_rs(rs, [&](auto R) {
             k_gen<decltype(R)::value><<<grid_for(n, 256, 16), 256, 0, st>>>(static_cast<uint8_t*>(d_out), P);
+            note_launch();
         });
         RG_LAUNCH_CHECK();
         RG_CHECK(cudaStreamSynchronize(st));  // thresholds live in pinned scratch
@@ -1382,6 +1409,7 @@ int raduls_gpu_digest(const void* d_data, uint64_t n, uint32_t rs, uint64_t* lo,
             dispatch_rs(rs, [&](auto R) {
                 k_digest<decltype(R)::value><<<grid_for(n, 256, 8), 256, 0, st>>>(
                     static_cast<const uint8_t*>(d_data), n, ws.acc.p);
+                note_launch();
             });
             RG_LAUNCH_CHECK();
         }
@@ -1406,6 +1434,7 @@ int raduls_gpu_check_sorted(const void* d_data, uint64_t n, uint32_t rs, uint32_
             dispatch_rs(rs, [&](auto R) {
                 k_check_sorted<decltype(R)::value><<<grid_for(n, 256, 8), 256, 0, st>>>(
                     static_cast<const uint8_t*>(d_data), n, ks, ws.acc.p);
+                note_launch();
             });
             RG_LAUNCH_CHECK();
         }
@@ -1427,6 +1456,7 @@ int raduls_gpu_prefix_histogram(const void* d_data, uint64_t n, uint32_t rs, uin
             k_prefix_hist<decltype(R)::value><<<grid_for(n, 256, 8), 256, 0, st>>>(
                 static_cast<const uint8_t*>(d_data), n, ks, prefix_byte,
                 reinterpret_cast<unsigned long long*>(d_hist));
+            note_launch();
         });
         RG_LAUNCH_CHECK();
     });
@@ -1448,6 +1478,7 @@ int raduls_gpu_partition(const void* d_src, void* d_dst, uint64_t n, uint32_t rs
         RG_CHECK(cudaMemsetAsync(ws.acc.p, 0, sizeof(unsigned long long), st));
         k_map_to_u8<<<256, 256, 0, st>>>(d_bucket_rank, ws.map8.p, n_ranks,
                                           reinterpret_cast<unsigned int*>(ws.acc.p));
+        note_launch();
         RG_LAUNCH_CHECK();
         RG_CHECK(cudaMemcpyAsync(ws.h_small + 2048, ws.acc.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                  st));
@@ -1484,6 +1515,7 @@ int raduls_gpu_partition_to(const void* d_src, uint64_t n, uint32_t rs, uint32_t
         RG_CHECK(cudaMemsetAsync(ws.acc.p, 0, sizeof(unsigned long long), st));
         k_map_to_u8<<<256, 256, 0, st>>>(d_bucket_rank, ws.map8.p, n_ranks,
                                           reinterpret_cast<unsigned int*>(ws.acc.p));
+        note_launch();
         RG_LAUNCH_CHECK();
         unsigned long long* hd = ws.h_small + 3072;  // pinned staging for the destinations
         for (uint32_t r = 0; r < kRadix; ++r) hd[r] = r < n_ranks ? h_dst[r] : 0ull;
@@ -1509,6 +1541,7 @@ static bool load_rank_map(Workspace& ws, const uint32_t* d_bucket_rank, uint32_t
     ws.map8.ensure(65536);
     RG_CHECK(cudaMemsetAsync(ws.acc.p, 0, sizeof(unsigned long long), st));
     k_map_to_u8<<<256, 256, 0, st>>>(d_bucket_rank, ws.map8.p, n_ranks, reinterpret_cast<unsigned int*>(ws.acc.p));
+    note_launch();
     RG_LAUNCH_CHECK();
     RG_CHECK(cudaMemcpyAsync(ws.h_small + 2048, ws.acc.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
     RG_CHECK(cudaStreamSynchronize(st));
@@ -1677,6 +1710,7 @@ int raduls_gpu_digit_andor(const void* d_src, uint64_t n, uint32_t rs, uint32_t 
         dispatch_rs(rs, [&](auto R) {
             k_digit_andor<decltype(R)::value><<<grid_for(n, 256, 8), 256, 0, st>>>(
                 static_cast<const uint8_t*>(d_src), n, ks, prefix_byte, ws.map8.p, d_hot, d_out);
+            note_launch();
         });
         RG_LAUNCH_CHECK();
         RG_CHECK(cudaMemcpyAsync(init, d_out, kHotSlots * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -1695,12 +1729,14 @@ int raduls_gpu_sample_andor(const void* d_data, uint64_t n, uint32_t rs, uint32_
         std::lock_guard<std::mutex> lk(ws.mu);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         k_init_andor<<<1, 64, 0, st>>>(ws.andor0.p, 1);
+        note_launch();
         RG_LAUNCH_CHECK();
         const uint32_t sm = uint32_t(std::min<uint64_t>(n, std::max<uint32_t>(samples, 1)));
         if (n) {
             dispatch_rs(rs, [&](auto R) {
                 k_sample_andor<decltype(R)::value><<<64, 256, 0, st>>>(
                     static_cast<const uint8_t*>(d_data), n, std::max<uint64_t>(1, n / sm), sm, ws.andor0.p);
+                note_launch();
             });
             RG_LAUNCH_CHECK();
         }
@@ -1722,6 +1758,7 @@ int raduls_gpu_sample_prefix_histogram(const void* d_data, uint64_t n, uint32_t 
             k_sample_prefix_hist<decltype(R)::value><<<grid_for(sm, 256, 4), 256, 0, st>>>(
                 static_cast<const uint8_t*>(d_data), n, std::max<uint64_t>(1, n / sm), sm, ks, prefix_byte,
                 reinterpret_cast<unsigned long long*>(d_hist));
+            note_launch();
         });
         RG_LAUNCH_CHECK();
     });
@@ -1768,11 +1805,13 @@ int raduls_gpu_andor(const void* d_data, uint64_t n, uint32_t rs, uint64_t* h_an
         std::lock_guard<std::mutex> lk(ws.mu);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         k_init_andor<<<1, 64, 0, st>>>(ws.andor0.p, 1);
+        note_launch();
         RG_LAUNCH_CHECK();
         if (n) {
             dispatch_rs(rs, [&](auto R) {
                 k_andor<decltype(R)::value><<<grid_for(n, 256, 8), 256, 0, st>>>(
                     static_cast<const uint8_t*>(d_data), n, ws.andor0.p);
+                note_launch();
             });
             RG_LAUNCH_CHECK();
         }
@@ -1788,6 +1827,12 @@ int raduls_gpu_set_profiling(int on) {
         std::lock_guard<std::mutex> lk(ws.mu);
         ws.prof.on = on != 0;
     });
+}
+
+int raduls_gpu_launch_count(uint64_t* count) {
+    if (!count) return RADULS_GPU_EINVAL;
+    *count = g_launches.load(std::memory_order_relaxed);
+    return RADULS_GPU_OK;
 }
 
 int raduls_gpu_rank_mode(int* mode) {

@@ -33,7 +33,7 @@ __all__ = [
     "RecordLayout", "SchedulerConfig", "TinyPolicy", "BigBinFraction", "ResourceError",
     "CudaError", "sort", "sort_device", "split", "histogram", "generate", "digest",
     "check_sorted", "last_stats", "DIST_UNIFORM", "DIST_SKEW", "local_capacity",
-    "set_profiling", "last_kernel_times", "LsdConfig", "lsd_sort", "rank_mode",
+    "set_profiling", "last_kernel_times", "LsdConfig", "lsd_sort", "rank_mode", "launch_count",
 ]
 
 DIST_UNIFORM = 0
@@ -220,6 +220,13 @@ def rank_mode() -> int:
     m = C.c_int(-1)
     _raise(_lib.load().raduls_gpu_rank_mode(C.byref(m)), "raduls_gpu_rank_mode")
     return m.value
+
+
+def launch_count() -> int:
+    """Kernel launches made by libraduls_gpu.so in this process so far."""
+    c = C.c_uint64(0)
+    _raise(_lib.load().raduls_gpu_launch_count(C.byref(c)), "raduls_gpu_launch_count")
+    return c.value
 
 
 def set_profiling(on: bool) -> None:
