@@ -131,6 +131,13 @@ int raduls_gpu_rank_mode(int* mode);
  * every entry point; a relaxed process-wide counter). */
 int raduls_gpu_launch_count(uint64_t* count);
 
+/* The host drop-ins (raduls_gpu_sort_host, raduls_gpu_lsd_sort_host) stage the
+ * records in two device buffers of n*rec_size bytes. Default (0): freed before
+ * the call returns, as the reference frees its per-call aux buffer
+ * (msd_sorter.hpp:52). 1: kept and reused by later calls of the same or a
+ * smaller size until raduls_gpu_set_host_cache(0) or raduls_gpu_release(). */
+int raduls_gpu_set_host_cache(int on);
+
 /*
  * Building blocks (tests, benchmarks and the multi-GPU driver). All device
  * pointers; asynchronous on `stream` unless noted.
@@ -243,6 +250,19 @@ int raduls_gpu_partition_store(const void* d_src, uint64_t n_recs, uint32_t rec_
  *     counts of every digit must add up to the plan's count for it.
  *     Synchronous.
  */
+/*
+ * Pivots for hot buckets whose records do not share one key: with pivot i
+ * set on digit h_digits[i], a record whose bucket maps to that digit gets
+ * digit d, d + 1 or d + 2 as its key (first key_size bytes, memcmp order) is
+ * below, equal to or above h_keys[i * key_size ...] — so the equal run, one
+ * key, may be cut into pieces by count. A plan then numbers its digits with
+ * d + 1 and d + 2 reserved for the pivot. At most 16 pivots; their digit
+ * triples must not overlap. The pivots apply to every bucket-map call of this
+ * library on the current device (partition, partition_to, partition_plan,
+ * digit_andor) until replaced; n_pivots = 0 clears them.
+ */
+int raduls_gpu_set_pivots(uint32_t n_pivots, const uint32_t* h_digits, const uint8_t* h_keys, uint32_t key_size);
+
 int raduls_gpu_digit_andor(const void* d_src, uint64_t n_recs, uint32_t rec_size, uint32_t key_size,
                            uint32_t prefix_byte, const uint32_t* d_bucket_digit, uint32_t n_digits,
                            const uint8_t* h_hot, uint64_t* h_andor, void* stream);

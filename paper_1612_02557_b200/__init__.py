@@ -24,6 +24,7 @@ from .raduls import (  # noqa: F401
     local_capacity,
     rank_mode,
     launch_count,
+    set_host_cache,
     lsd_sort,
     set_profiling,
     sort,

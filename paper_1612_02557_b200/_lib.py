@@ -50,6 +50,8 @@ EXPORTED = [
     "raduls_gpu_digit_andor",
     "raduls_gpu_partition_store_pieces",
     "raduls_gpu_launch_count",
+    "raduls_gpu_set_host_cache",
+    "raduls_gpu_set_pivots",
 ]
 
 
@@ -131,6 +133,8 @@ def load(build_if_missing: bool = False):
         L.raduls_gpu_free.argtypes = [_vp]
         L.raduls_gpu_rank_mode.argtypes = [C.POINTER(C.c_int)]
         L.raduls_gpu_launch_count.argtypes = [_u64p]
+        L.raduls_gpu_set_host_cache.argtypes = [C.c_int]
+        L.raduls_gpu_set_pivots.argtypes = [_u32, _vp, _vp, _u32]
         L.raduls_gpu_digit_andor.argtypes = [_vp, _u64, _u32, _u32, _u32, _vp, _u32, _vp, _u64p, _vp]
         L.raduls_gpu_partition_store_pieces.argtypes = [_vp, _u64, _u32, _u32, _u32, _vp, _u64p, _u64p,
                                                         _vp]

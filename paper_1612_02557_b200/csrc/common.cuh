@@ -424,6 +424,37 @@ __global__ void __launch_bounds__(256) k_rank_selftest(uint32_t rounds, unsigned
     if (__any_sync(0xFFFFFFFFu, diff) && lane == 0) atomicOr(bad, 1u);
 }
 
+// Multi-GPU partition digits --------------------------------
+//
+// The map buffer: map[b] (b < 65536) = digit of the 16-bit key prefix at bytes
+// (p, p+1); map[kMapPivotSlot + d] = pivot slot + 1 when digit d is a hot
+// bucket cut around a pivot key (0 otherwise); the pivot keys (kMaxPivots x 32
+// B, the key's first ks bytes) follow. A record of a pivot digit gets digit
+// d, d + 1 or d + 2 for a key below, equal to or above the pivot (memcmp
+// order, P/include/raduls/layout.hpp:52-55): the equal run holds one key, so
+// the plan may spread it over ranks by count.
+constexpr uint32_t kMapPivotSlot = 65536;
+constexpr uint32_t kMaxPivots = 16;
+constexpr uint32_t kMapPivotKeys = kMapPivotSlot + 256;
+constexpr uint32_t kMapBytes = kMapPivotKeys + kMaxPivots * 32;
+
+// byte_at(i): key byte i of the record (any i < ks).
+template <typename ByteAt>
+__device__ __forceinline__ uint32_t map_digit(ByteAt byte_at, uint32_t p, uint32_t ks,
+                                              const uint8_t* __restrict__ map) {
+    const uint32_t hi = p < ks ? byte_at(p) : 0u;
+    const uint32_t lo = p + 1 < ks ? byte_at(p + 1) : 0u;
+    const uint32_t d = __ldg(map + ((hi << 8) | lo));
+    const uint32_t pv = __ldg(map + kMapPivotSlot + d);
+    if (pv == 0) return d;
+    const uint8_t* key = map + kMapPivotKeys + (pv - 1) * 32u;
+    for (uint32_t b = 0; b < ks; ++b) {
+        const uint32_t x = byte_at(b), y = __ldg(key + b);
+        if (x != y) return x < y ? d : d + 2;
+    }
+    return d + 1;
+}
+
 // Device segment descriptors -------------------------------------------------
 
 // A contiguous run of records [start, start+size) that still needs ordering by

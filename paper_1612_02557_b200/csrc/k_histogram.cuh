@@ -277,11 +277,8 @@ __global__ void __launch_bounds__(HistCfg<RS>::kThreads + 64, HistCfg<RS>::kCtas
 #pragma unroll
                 for (int q = 0; q < Rec<RS>::kWords; ++q) r.w[q] = 0;
             if constexpr (kMap) {
-                if (valid) {
-                    const uint32_t hi = p < ks ? rec_byte<RS>(r, p) : 0u;
-                    const uint32_t lo = p + 1 < ks ? rec_byte<RS>(r, p + 1) : 0u;
-                    atomicAdd(&hb[__ldg(map + ((hi << 8) | lo))], 1u);
-                }
+                if (valid)
+                    atomicAdd(&hb[map_digit([&](uint32_t b) { return rec_byte<RS>(r, b); }, p, ks, map)], 1u);
             } else {
                 const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
                 const uint32_t word = rec_word32<RS>(r, p >> 2);
@@ -324,8 +321,6 @@ struct HistRegCfg {
                                         : ((kTile + kIt - 1) / kIt + 31) / 32 * 32;
 };
 
-constexpr uint32_t kHistAhead = 592;  // ~ resident histogram CTAs (4 per SM x 148)
-
 template <int RS, int kTile, bool kMap = false>
 __global__ void __launch_bounds__(HistRegCfg<RS, kTile>::kThreads) k_tile_hist_reg(const uint8_t* __restrict__ data,
                                                    const uint8_t* __restrict__ tmp,
@@ -333,8 +328,9 @@ __global__ void __launch_bounds__(HistRegCfg<RS, kTile>::kThreads) k_tile_hist_r
                                                    const uint32_t* __restrict__ tile_seg,
                                                    uint16_t* __restrict__ tile_cnt,
                                                    unsigned long long* __restrict__ seg_andor,
-                                                   LevelCounters* __restrict__ ctr, uint32_t ks = 0,
-                                                   const uint8_t* __restrict__ map = nullptr) {
+                                                   LevelCounters* __restrict__ ctr, uint32_t ks,
+                                                   const uint8_t* __restrict__ map,
+                                                   uint32_t ahead) {  // ~ resident CTAs: 4 per SM
     constexpr int KW = RS / 8;
     constexpr int HT = HistRegCfg<RS, kTile>::kThreads, HW = HT / 32;
     constexpr int IT = (kTile + HT - 1) / HT;
@@ -350,8 +346,8 @@ __global__ void __launch_bounds__(HistRegCfg<RS, kTile>::kThreads) k_tile_hist_r
     const uint32_t p = g.p;
     // 8-B records: pull the tile one resident wave ahead toward L2 (its CTA
     // then starts on L2 hits; measured +4% at C2, a loss at 16 B)
-    if (RS == 8 && threadIdx.x == 0 && tile + kHistAhead < gridDim.x) {
-        const uint32_t t2 = tile + kHistAhead;
+    if (RS == 8 && threadIdx.x == 0 && tile + ahead < gridDim.x) {
+        const uint32_t t2 = tile + ahead;
         const Seg g2 = segs[tile_seg[t2]];
         const uint64_t k2 = uint64_t(t2) - g2.tile_base;
         const uint64_t n2 = min(uint64_t(kTile), g2.size - k2 * kTile);
@@ -379,11 +375,8 @@ __global__ void __launch_bounds__(HistRegCfg<RS, kTile>::kThreads) k_tile_hist_r
         const uint32_t i = uint32_t(j) * HT + threadIdx.x;
         const bool valid = i < tn;
         if constexpr (kMap) {
-            if (valid) {
-                const uint32_t hi = p < ks ? rec_byte<RS>(r[j], p) : 0u;
-                const uint32_t lo = p + 1 < ks ? rec_byte<RS>(r[j], p + 1) : 0u;
-                atomicAdd(&sh[__ldg(map + ((hi << 8) | lo))], 1u);
-            }
+            if (valid)
+                atomicAdd(&sh[map_digit([&](uint32_t b) { return rec_byte<RS>(r[j], b); }, p, ks, map)], 1u);
         } else {
             const uint32_t nvalid = __popc(__ballot_sync(0xFFFFFFFFu, valid));
             const uint32_t word = rec_word32<RS>(r[j], p >> 2);

@@ -760,14 +760,14 @@ template <int RS, bool kFallback>
 __global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBlocks) k_local(
     uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group* __restrict__ groups,
     uint32_t n_groups, uint32_t ks, LevelCounters* __restrict__ ctr, Group* __restrict__ spill,
-    unsigned int* __restrict__ n_spill, uint32_t spill_cap) {
+    unsigned int* __restrict__ n_spill, uint32_t spill_cap, uint32_t ahead) {
     if constexpr (LocalCfg<RS>::kMinBlocks > 1) {
         // two CTAs per SM already overlap one group's start with the other's
         // sort: one group per CTA (measured 4% faster than this loop), the
-        // group one resident wave later prefetched into L2
-        constexpr uint32_t kAhead = 2 * 148;
-        if (threadIdx.x == 0 && blockIdx.x + kAhead < n_groups)
-            prefetch_group_l2<RS>(data, tmp, groups[blockIdx.x + kAhead]);
+        // group one resident wave later (ahead = resident CTAs: 2 per SM)
+        // prefetched into L2
+        if (threadIdx.x == 0 && blockIdx.x + ahead < n_groups)
+            prefetch_group_l2<RS>(data, tmp, groups[blockIdx.x + ahead]);
         local_group<RS, kFallback>(data, tmp, groups[blockIdx.x], ks, ctr, spill, n_spill, spill_cap,
                                    [] {});
         return;

@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(256) k_digit_andor(const uint8_t* __restrict__
     };
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
         const Rec<RS> r = load_rec_stream<RS>(data, i);
-        const uint32_t h = s_hot[__ldg(map + prefix16<RS>(r, pb, ks))];
+        const uint32_t h = s_hot[map_digit([&](uint32_t b) { return rec_byte<RS>(r, b); }, pb, ks, map)];
         if (!h) continue;
         if (h != cur) {
             flush();

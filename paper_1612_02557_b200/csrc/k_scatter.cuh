@@ -100,15 +100,14 @@ __device__ __forceinline__ uint32_t scan256_exclusive(uint32_t v, uint32_t* s_wa
 }
 
 // Digit of a staged record: key byte p (MSD split), or — kMap — the
-// destination rank of its 16-bit key prefix at bytes (p, p+1) through a
-// 65536-entry map (the multi-GPU key-range partition).
+// destination digit of its 16-bit key prefix at bytes (p, p+1) through the
+// partition map (map_digit: 65536 entries + pivot keys; the multi-GPU
+// key-range partition).
 template <int RS, bool kMap>
 __device__ __forceinline__ uint32_t scatter_digit_smem(const uint8_t* rec, uint32_t p, uint32_t ks,
                                                        const uint8_t* __restrict__ map) {
     if constexpr (kMap) {
-        const uint32_t hi = p < ks ? rec[p] : 0u;
-        const uint32_t lo = p + 1 < ks ? rec[p + 1] : 0u;
-        return __ldg(map + ((hi << 8) | lo));
+        return map_digit([&](uint32_t b) { return uint32_t(rec[b]); }, p, ks, map);
     } else {
         return rec[p];
     }

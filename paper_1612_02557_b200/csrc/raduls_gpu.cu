@@ -83,6 +83,11 @@ struct CudaError {
 static std::atomic<unsigned long long> g_launches{0};
 static inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+// Host drop-ins: keep their two N*rs device buffers between calls
+// (raduls_gpu_set_host_cache(1)) or free them before returning (default, like
+// the reference's per-call aux buffer, P/include/raduls/detail/msd_sorter.hpp:52).
+static std::atomic<int> g_host_cache{0};
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
@@ -314,6 +319,10 @@ struct Workspace {
     DevBuf<unsigned int> n_spill;
     DevBuf<CopyRange> copies;
     DevBuf<uint8_t> host_data, host_tmp, map8;
+    // partition pivots (raduls_gpu_set_pivots): the map buffer's pivot region
+    // (kMapBytes - 65536 bytes) as uploaded with every bucket map
+    std::array<uint8_t, kMapBytes - kMapPivotSlot> pivots{};
+    uint32_t n_pivots = 0, pivot_max_digit = 0;
     DevBuf<unsigned long long> dig_dst;  // per-destination byte addresses (raduls_gpu_partition_to)
     DevBuf<Piece> pieces;
     DevBuf<unsigned long long> hot;       // raduls_gpu_digit_andor: slot flags + accumulators                // split digits' destination pieces (raduls_gpu_partition_store_pieces)
@@ -470,7 +479,8 @@ void level_counts(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_t 
         note_launch();
     } else if constexpr (RS == 8) {  // one CTA per tile (see k_tile_hist_reg)
         k_tile_hist_reg<RS, TILE, kMap><<<ntiles, HistRegCfg<RS, TILE>::kThreads, 0, st>>>(
-            data, tmp, ws.segs[cur].p, ws.tile_seg[cur].p, ws.tile_cnt.p, ws.seg_andor[cur].p, c, ks, map);
+            data, tmp, ws.segs[cur].p, ws.tile_seg[cur].p, ws.tile_cnt.p, ws.seg_andor[cur].p, c, ks, map,
+            uint32_t(sm_count()) * 4);
         note_launch();
     } else {  // persistent, TMA-fed
         const uint32_t hgrid = std::min<uint32_t>(ntiles, uint32_t(sm_count()) * HistCfg<RS>::kCtas);
@@ -549,7 +559,8 @@ void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, 
     const uint32_t grid = LocalCfg<RS>::kMinBlocks == 1 ? std::min<uint32_t>(ngroups, uint32_t(sm_count()))
                                                        : ngroups;
     k_local<RS, false><<<grid, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
-        data, tmp, ws.groups.p, ngroups, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap));
+        data, tmp, ws.groups.p, ngroups, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap),
+        uint32_t(sm_count()) * LocalCfg<RS>::kMinBlocks);
     note_launch();
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
@@ -565,7 +576,8 @@ void finish_spilled(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ks, Lev
     const int pe = ws.prof.begin(K_LOCAL, st);
     const uint32_t grid = LocalCfg<RS>::kMinBlocks == 1 ? std::min<uint32_t>(n, uint32_t(sm_count())) : n;
     k_local<RS, true><<<grid, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
-        data, tmp, ws.spill.p, n, ks, ctr, nullptr, nullptr, 0);
+        data, tmp, ws.spill.p, n, ks, ctr, nullptr, nullptr, 0,
+        uint32_t(sm_count()) * LocalCfg<RS>::kMinBlocks);
     note_launch();
     RG_LAUNCH_CHECK();
     ws.prof.end(pe, st);
@@ -953,6 +965,19 @@ int run_per_device(int n, F&& f) {
     return RADULS_GPU_OK;
 }
 
+// Frees the host drop-ins' device buffers when the call ends (normally or by
+// an error) unless the caller opted into caching them.
+struct HostBufs {
+    Workspace& ws;
+    explicit HostBufs(Workspace& w) : ws(w) {}
+    ~HostBufs() {
+        if (g_host_cache.load()) return;
+        cudaDeviceSynchronize();  // the progressive copies may still read host_data
+        ws.host_data.release();
+        ws.host_tmp.release();
+    }
+};
+
 // Device memory a host sort may use: free memory plus the cached host-path
 // buffers (reused), or RADULS_GPU_DEVICE_BUDGET bytes when set (tests force
 // the out-of-core path with it).
@@ -1094,11 +1119,14 @@ static int sort_host_out_of_core(uint8_t* data, uint8_t* htmp, uint64_t n, uint3
         std::vector<uint64_t> hist(kPrefixBuckets);
         RG_CHECK(cudaMemcpy(hist.data(), d_hist, kPrefixBuckets * sizeof(uint64_t), cudaMemcpyDeviceToHost));
         // (2) parts: contiguous bucket ranges of <= P records
+        // A bucket larger than P is a part of its own ("big"): its records
+        // share the 16-bit prefix, and it is sorted afterwards by the same
+        // out-of-core plan applied to its range (the next varying bytes).
         std::vector<uint32_t> map(kPrefixBuckets);
         std::vector<uint64_t> psz(1, 0);
         for (uint32_t b = 0; b < kPrefixBuckets; ++b) {
-            if (hist[b] > P) throw CudaError{RADULS_GPU_ENOMEM};  // one 16-bit prefix outgrows the device
-            if (psz.back() + hist[b] > P) psz.push_back(0);
+            const bool big = hist[b] > P;
+            if (psz.back() && (big || psz.back() + hist[b] > P || psz.back() > P)) psz.push_back(0);
             map[b] = uint32_t(psz.size() - 1);
             psz.back() += hist[b];
         }
@@ -1107,6 +1135,7 @@ static int sort_host_out_of_core(uint8_t* data, uint8_t* htmp, uint64_t n, uint3
         std::vector<uint64_t> poff(K, 0), written(K, 0);
         for (uint32_t k = 1; k < K; ++k) poff[k] = poff[k - 1] + psz[k - 1];
         RG_CHECK(cudaMemcpy(d_map, map.data(), kPrefixBuckets * sizeof(uint32_t), cudaMemcpyHostToDevice));
+        check(raduls_gpu_set_pivots(0, nullptr, nullptr, ks));  // whole buckets only here
         // (3) stable partition of every chunk into the parts' host ranges
         std::vector<uint64_t> cnt(K);
         for (uint64_t off = 0; off < n; off += P) {
@@ -1125,14 +1154,33 @@ static int sort_host_out_of_core(uint8_t* data, uint8_t* htmp, uint64_t n, uint3
         }
         for (uint32_t k = 0; k < K; ++k)
             if (written[k] != psz[k]) throw CudaError{RADULS_GPU_EINTERNAL};
-        // (4) every part: to the device, sorted, to its place in data
-        for (uint32_t k = 0; k < K; ++k) {
-            if (!psz[k]) continue;
-            hs.h2d(A, htmp + poff[k] * rs, psz[k] * rs, st);
-            check(raduls_gpu_sort(A, B, psz[k], rs, ks, st));
-            hs.d2h(data + poff[k] * rs, A, psz[k] * rs, st);
+        // (4) every part: to the device, sorted, to its place in data. From
+        // here on data is overwritten part by part; if anything fails, the
+        // parts not yet written are copied back from htmp unsorted, so data
+        // still holds the input's records (a permutation) when the error returns.
+        uint32_t k = 0;
+        try {
+            for (; k < K; ++k) {
+                if (!psz[k] || psz[k] > P) continue;  // big parts below
+                hs.h2d(A, htmp + poff[k] * rs, psz[k] * rs, st);
+                check(raduls_gpu_sort(A, B, psz[k], rs, ks, st));
+                hs.d2h(data + poff[k] * rs, A, psz[k] * rs, st);
+            }
+            RG_CHECK(cudaStreamSynchronize(st));
+            cudaFree(A), cudaFree(B), A = B = nullptr;  // the big parts' own plans allocate theirs
+            for (k = 0; k < K; ++k) {
+                if (psz[k] <= P) continue;
+                // sort the range in place in htmp with data's (already
+                // consumed) range as its scratch, then move it to data
+                check(sort_host_out_of_core(htmp + poff[k] * rs, data + poff[k] * rs, psz[k], rs, ks, budget));
+                std::memcpy(data + poff[k] * rs, htmp + poff[k] * rs, psz[k] * rs);
+            }
+        } catch (...) {
+            cudaDeviceSynchronize();
+            for (uint32_t q = 0; q < K; ++q)
+                if ((q >= k || psz[q] > P) && psz[q]) std::memcpy(data + poff[q] * rs, htmp + poff[q] * rs, psz[q] * rs);
+            throw;
         }
-        RG_CHECK(cudaStreamSynchronize(st));
     });
 }
 
@@ -1149,6 +1197,7 @@ int raduls_gpu_sort_host(uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t rs, u
     return guarded([&] {
         Workspace& ws = workspace();
         std::lock_guard<std::mutex> lk(ws.mu);
+        HostBufs hb(ws);
         ws.host_data.ensure(bytes);
         ws.host_tmp.ensure(bytes);
         cudaStream_t st = nullptr;
@@ -1308,6 +1357,7 @@ int raduls_gpu_lsd_sort_host(uint8_t* data, uint8_t* /*tmp*/, uint64_t n, uint32
         Workspace& ws = workspace();
         std::lock_guard<std::mutex> lk(ws.mu);
         const size_t bytes = size_t(n) * rs;
+        HostBufs hb(ws);
         ws.host_data.ensure(bytes);
         ws.host_tmp.ensure(bytes);
         cudaStream_t st = nullptr;
@@ -1462,6 +1512,24 @@ int raduls_gpu_prefix_histogram(const void* d_data, uint64_t n, uint32_t rs, uin
     });
 }
 
+// Load the bucket -> rank map (u8) plus the pivot region and check them;
+// false when an entry (or a pivot digit + 2) is >= n_ranks. Asynchronous up to
+// the final check.
+static bool load_rank_map(Workspace& ws, const uint32_t* d_bucket_rank, uint32_t n_ranks, cudaStream_t st) {
+    if (ws.map8.cap < kMapBytes) ws.map8.ensure(kMapBytes);
+    if (ws.n_pivots && ws.pivot_max_digit + 2 >= n_ranks) return false;
+    RG_CHECK(cudaMemsetAsync(ws.acc.p, 0, sizeof(unsigned long long), st));
+    k_map_to_u8<<<256, 256, 0, st>>>(d_bucket_rank, ws.map8.p, n_ranks, reinterpret_cast<unsigned int*>(ws.acc.p));
+    note_launch();
+    RG_LAUNCH_CHECK();
+    unsigned char* hp = reinterpret_cast<unsigned char*>(ws.h_small + 3328);  // pinned staging (6 KB free)
+    std::memcpy(hp, ws.pivots.data(), ws.pivots.size());
+    RG_CHECK(cudaMemcpyAsync(ws.map8.p + kMapPivotSlot, hp, ws.pivots.size(), cudaMemcpyHostToDevice, st));
+    RG_CHECK(cudaMemcpyAsync(ws.h_small + 2048, ws.acc.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    RG_CHECK(cudaStreamSynchronize(st));
+    return uint32_t(ws.h_small[2048]) == 0;
+}
+
 int raduls_gpu_partition(const void* d_src, void* d_dst, uint64_t n, uint32_t rs, uint32_t ks,
                          uint32_t prefix_byte, const uint32_t* d_bucket_rank, uint32_t n_ranks,
                          uint64_t* h_rank_counts, void* stream) {
@@ -1474,16 +1542,7 @@ int raduls_gpu_partition(const void* d_src, void* d_dst, uint64_t n, uint32_t rs
         std::lock_guard<std::mutex> lk(ws.mu);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         if (h_rank_counts) std::memset(h_rank_counts, 0, n_ranks * sizeof(uint64_t));
-        ws.map8.ensure(65536);
-        RG_CHECK(cudaMemsetAsync(ws.acc.p, 0, sizeof(unsigned long long), st));
-        k_map_to_u8<<<256, 256, 0, st>>>(d_bucket_rank, ws.map8.p, n_ranks,
-                                          reinterpret_cast<unsigned int*>(ws.acc.p));
-        note_launch();
-        RG_LAUNCH_CHECK();
-        RG_CHECK(cudaMemcpyAsync(ws.h_small + 2048, ws.acc.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                                 st));
-        RG_CHECK(cudaStreamSynchronize(st));
-        if (uint32_t(ws.h_small[2048])) throw CudaError{RADULS_GPU_EINVAL};  // map entry >= n_ranks
+        if (!load_rank_map(ws, d_bucket_rank, n_ranks, st)) throw CudaError{RADULS_GPU_EINVAL};
         if (!n) return;
         dispatch_rs(rs, [&](auto R) {
             constexpr int RSC = decltype(R)::value;
@@ -1510,20 +1569,11 @@ int raduls_gpu_partition_to(const void* d_src, uint64_t n, uint32_t rs, uint32_t
         std::lock_guard<std::mutex> lk(ws.mu);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         if (h_rank_counts) std::memset(h_rank_counts, 0, n_ranks * sizeof(uint64_t));
-        ws.map8.ensure(65536);
         ws.dig_dst.ensure(kRadix);
-        RG_CHECK(cudaMemsetAsync(ws.acc.p, 0, sizeof(unsigned long long), st));
-        k_map_to_u8<<<256, 256, 0, st>>>(d_bucket_rank, ws.map8.p, n_ranks,
-                                          reinterpret_cast<unsigned int*>(ws.acc.p));
-        note_launch();
-        RG_LAUNCH_CHECK();
+        if (!load_rank_map(ws, d_bucket_rank, n_ranks, st)) throw CudaError{RADULS_GPU_EINVAL};
         unsigned long long* hd = ws.h_small + 3072;  // pinned staging for the destinations
         for (uint32_t r = 0; r < kRadix; ++r) hd[r] = r < n_ranks ? h_dst[r] : 0ull;
         RG_CHECK(cudaMemcpyAsync(ws.dig_dst.p, hd, kRadix * sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
-        RG_CHECK(cudaMemcpyAsync(ws.h_small + 2048, ws.acc.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                                 st));
-        RG_CHECK(cudaStreamSynchronize(st));
-        if (uint32_t(ws.h_small[2048])) throw CudaError{RADULS_GPU_EINVAL};  // map entry >= n_ranks
         if (!n) return;
         dispatch_rs(rs, [&](auto R) {
             constexpr int RSC = decltype(R)::value;
@@ -1534,18 +1584,6 @@ int raduls_gpu_partition_to(const void* d_src, uint64_t n, uint32_t rs, uint32_t
             single_segment_scatter<RSC, true, true>(ws, src, nullptr, n, ks, ws.map8.p, tot, st, ws.dig_dst.p);
         });
     });
-}
-
-// Load the bucket -> rank map (u8) and check it; false when an entry is >= n_ranks.
-static bool load_rank_map(Workspace& ws, const uint32_t* d_bucket_rank, uint32_t n_ranks, cudaStream_t st) {
-    ws.map8.ensure(65536);
-    RG_CHECK(cudaMemsetAsync(ws.acc.p, 0, sizeof(unsigned long long), st));
-    k_map_to_u8<<<256, 256, 0, st>>>(d_bucket_rank, ws.map8.p, n_ranks, reinterpret_cast<unsigned int*>(ws.acc.p));
-    note_launch();
-    RG_LAUNCH_CHECK();
-    RG_CHECK(cudaMemcpyAsync(ws.h_small + 2048, ws.acc.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    RG_CHECK(cudaStreamSynchronize(st));
-    return uint32_t(ws.h_small[2048]) == 0;
 }
 
 int raduls_gpu_partition_plan(const void* d_src, uint64_t n, uint32_t rs, uint32_t ks, uint32_t prefix_byte,
@@ -1829,6 +1867,40 @@ int raduls_gpu_set_profiling(int on) {
     });
 }
 
+int raduls_gpu_set_pivots(uint32_t n_pivots, const uint32_t* digits, const uint8_t* keys, uint32_t ks) {
+    if (n_pivots > kMaxPivots || ks < 1 || ks > 32 || (n_pivots && (!digits || !keys))) return RADULS_GPU_EINVAL;
+    for (uint32_t i = 0; i < n_pivots; ++i) {
+        if (digits[i] + 2 > 255) return RADULS_GPU_EINVAL;
+        for (uint32_t j = 0; j < i; ++j)  // a pivot digit and its two successors belong to one pivot
+            if (digits[i] + 2 >= digits[j] && digits[j] + 2 >= digits[i]) return RADULS_GPU_EINVAL;
+    }
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        ws.pivots.fill(0);
+        ws.pivot_max_digit = 0;
+        for (uint32_t i = 0; i < n_pivots; ++i) {
+            ws.pivots[digits[i]] = uint8_t(i + 1);
+            std::memcpy(ws.pivots.data() + (kMapPivotKeys - kMapPivotSlot) + 32 * i, keys + size_t(i) * ks, ks);
+            ws.pivot_max_digit = std::max(ws.pivot_max_digit, digits[i]);
+        }
+        ws.n_pivots = n_pivots;
+    });
+}
+
+int raduls_gpu_set_host_cache(int on) {
+    g_host_cache.store(on ? 1 : 0);
+    if (!on) {
+        return guarded([&] {
+            Workspace& ws = workspace();
+            std::lock_guard<std::mutex> lk(ws.mu);
+            ws.host_data.release();
+            ws.host_tmp.release();
+        });
+    }
+    return RADULS_GPU_OK;
+}
+
 int raduls_gpu_launch_count(uint64_t* count) {
     if (!count) return RADULS_GPU_EINVAL;
     *count = g_launches.load(std::memory_order_relaxed);
@@ -1991,6 +2063,7 @@ int raduls_gpu_sort_multi(int n_dev, const int* devices, void* const* d_in, cons
             std::vector<uint64_t> got(G, 0), dst(G, 0);
             for (uint32_t q = 0; q < G; ++q)
                 dst[q] = reinterpret_cast<uint64_t>(static_cast<uint8_t*>(d_out[q]) + at[g][q] * rs);
+            if (!r) r = raduls_gpu_set_pivots(0, nullptr, nullptr, ks);  // whole buckets only here
             if (!r) {
                 if (p2p)
                     r = raduls_gpu_partition_to(d_in[g], n_in[g], rs, ks, p0, d_map, G, dst.data(), got.data(),

@@ -84,37 +84,117 @@ def balanced_bucket_map(global_hist: np.ndarray, world: int) -> np.ndarray:
 
 
 HOT_SHARE = 4  # a bucket with more than total / (HOT_SHARE * world) records is hot
+MAX_PIVOTS = 16  # raduls_gpu_set_pivots
+SAMPLE_KEYS = 4096  # keys sampled per rank to find a hot bucket's pivot (its most common key)
 
 
 @dataclass
 class DigitPlan:
-    """The partition's digits: digit = bucket_digit[16-bit prefix at p0].
-    Digits are monotone in the bucket (key order); hot[d] marks a digit that
-    is exactly one hot bucket (a candidate for splitting by count)."""
+    """The partition's digits: digit = bucket_digit[16-bit prefix at p0],
+    except in a pivot bucket, whose records get digit d, d+1 or d+2 for a key
+    below, equal to or above the pivot key (map_digit, csrc/common.cuh).
+    Digits are monotone in key order. hot[d]: a hot bucket's digit whose
+    single-key-ness is unknown (checked with digit_andor before any split);
+    single[d]: a pivot's equal digit — one key by construction."""
     p0: int
     bucket_digit: np.ndarray   # [65536] u32
     n_digits: int
     hot: np.ndarray            # [n_digits] bool
+    single: np.ndarray = None  # [n_digits] bool
+    pivots: list = None        # [(digit d of the "below" part, key bytes)]
+
+    def __post_init__(self):
+        if self.single is None:
+            self.single = np.zeros(self.n_digits, dtype=bool)
+        if self.pivots is None:
+            self.pivots = []
 
 
-def make_digits(weights: np.ndarray, world: int, p0: int = 0, split_hot: bool = True) -> DigitPlan:
+def hot_buckets(weights: np.ndarray, world: int) -> np.ndarray:
+    w = np.asarray(weights, dtype=np.float64)
+    total = w.sum()
+    if world <= 1 or total <= 0:
+        return np.zeros(NBUCKETS, dtype=bool)
+    return w > total / (HOT_SHARE * world)
+
+
+def make_digits(weights: np.ndarray, world: int, p0: int = 0, split_hot: bool = True,
+                pivots: dict | None = None) -> DigitPlan:
     """Digits from global bucket weights (exact counts or sample estimates):
     each rank's contiguous bucket range (balanced_bucket_map) is one digit,
-    except that every hot bucket is a digit of its own."""
+    except that every hot bucket is a digit of its own — three digits
+    (below / equal / above) when `pivots` names a pivot key for it."""
     w = np.asarray(weights, dtype=np.float64)
     rank = balanced_bucket_map(w, world).astype(np.int64)
-    total = w.sum()
-    hot = (w > total / (HOT_SHARE * world)) if (split_hot and world > 1 and total > 0) \
-        else np.zeros(NBUCKETS, dtype=bool)
+    hot = hot_buckets(w, world) if split_hot else np.zeros(NBUCKETS, dtype=bool)
+    piv = np.zeros(NBUCKETS, dtype=bool)
+    if split_hot and pivots:
+        for b in pivots:
+            if hot[b]:
+                piv[b] = True
     change = np.zeros(NBUCKETS, dtype=bool)
     change[1:] = (rank[1:] != rank[:-1]) | hot[1:] | hot[:-1]
-    digit = np.cumsum(change).astype(np.uint32)
-    n_digits = int(digit[-1]) + 1
+    extra = 2 * (np.cumsum(piv) - piv)  # two more digits per earlier pivot bucket
+    digit = (np.cumsum(change) + extra).astype(np.uint32)
+    n_digits = int(digit[-1]) + 1 + (2 if piv[-1] else 0)
     if n_digits > 256:  # too many ranks for separate hot digits: whole buckets only
         return make_digits(weights, world, p0, split_hot=False)
     dhot = np.zeros(n_digits, dtype=bool)
-    dhot[digit[hot]] = True
-    return DigitPlan(p0, digit, n_digits, dhot)
+    single = np.zeros(n_digits, dtype=bool)
+    plist = []
+    for b in np.nonzero(hot)[0]:
+        d = int(digit[b])
+        if piv[b]:
+            single[d + 1] = True
+            plist.append((d, bytes(pivots[int(b)])))
+        else:
+            dhot[d] = True
+    return DigitPlan(p0, digit, n_digits, dhot, single, plist)
+
+
+def prefix16_np(keys: np.ndarray, p0: int, ks: int) -> np.ndarray:
+    """16-bit big-endian key prefix at bytes (p0, p0+1) of [n, >=ks] u8 keys."""
+    hi = keys[:, p0].astype(np.int64) if p0 < ks else np.zeros(len(keys), np.int64)
+    lo = keys[:, p0 + 1].astype(np.int64) if p0 + 1 < ks else np.zeros(len(keys), np.int64)
+    return (hi << 8) | lo
+
+
+def choose_pivots(keys: np.ndarray, p0: int, ks: int, hot: np.ndarray, weights: np.ndarray) -> dict:
+    """Pivot key per hot bucket: the most common key among the sampled keys
+    ([S, ks] u8, every rank's) that fall into it; at most MAX_PIVOTS, the
+    heaviest buckets first."""
+    if not hot.any() or len(keys) == 0:
+        return {}
+    pre = prefix16_np(keys, p0, ks)
+    order = sorted(np.nonzero(hot)[0], key=lambda b: -weights[b])[:MAX_PIVOTS]
+    out = {}
+    for b in order:
+        sel = keys[pre == b]
+        if len(sel) == 0:
+            continue
+        u, c = np.unique(sel[:, :ks], axis=0, return_counts=True)
+        out[int(b)] = u[int(np.argmax(c))].tobytes()
+    return out
+
+
+def map_digits_np(keys: np.ndarray, p0: int, ks: int, digits: "DigitPlan") -> np.ndarray:
+    """Host restatement of map_digit (csrc/common.cuh) for [n, >=ks] u8 keys
+    (the CPU stand-in of the tests and plan checks)."""
+    d = digits.bucket_digit[prefix16_np(keys, p0, ks)].astype(np.int64)
+    for pd, key in digits.pivots:
+        sel = d == pd
+        if not sel.any():
+            continue
+        k = keys[sel, :ks]
+        pk = np.frombuffer(key, dtype=np.uint8)[:ks]
+        neq = k != pk
+        first = np.where(neq.any(axis=1), neq.argmax(axis=1), ks)
+        rows = np.arange(len(k))
+        below = np.zeros(len(k), dtype=bool)
+        m = first < ks
+        below[m] = k[rows[m], first[m]] < pk[first[m]]
+        d[sel] = np.where(first == ks, pd + 1, np.where(below, pd, pd + 2))
+    return d
 
 
 def assign_pieces(M: np.ndarray, splittable: np.ndarray, world: int):
@@ -298,6 +378,28 @@ class DeviceOps:
                                                         dst.ctypes.data_as(_lib._u64p), self.stream()),
                "raduls_gpu_partition_store_pieces")
 
+    def set_pivots(self, digits: DigitPlan, ks: int) -> None:
+        """The plan's pivot keys for every later bucket-map call (raduls_gpu_set_pivots)."""
+        k = len(digits.pivots)
+        dg = np.array([d for d, _ in digits.pivots] or [0], dtype=np.uint32)
+        keys = np.frombuffer(b"".join(key[:ks] for _, key in digits.pivots) or b"\0", dtype=np.uint8).copy()
+        _raise(self.L.raduls_gpu_set_pivots(k, dg.ctypes.data, keys.ctypes.data, ks), "raduls_gpu_set_pivots")
+
+    def sample_keys(self, data, n: int, layout: RecordLayout, samples: int) -> np.ndarray:
+        """Key bytes of a strided sample of min(n, samples) records ([S, ks] u8)."""
+        rs, ks = layout.record_size, layout.key_size
+        s = min(n, samples)
+        if s == 0:
+            return np.zeros((0, ks), dtype=np.uint8)
+        idx = (self.torch.arange(s, device=self.device, dtype=self.torch.int64) * (n // s))
+        return data[:n * rs].view(n, rs)[idx, :ks].cpu().numpy()
+
+    def digit_counts(self, data, n: int, layout: RecordLayout, p0: int, bucket_digit: np.ndarray,
+                     n_digits: int) -> np.ndarray:
+        """Exact records per digit (the partition's own histogram, pivots applied)."""
+        counts, _ = self.partition_plan(data, n, layout, p0, bucket_digit, n_digits)
+        return counts
+
     def sort(self, data, n: int, layout: RecordLayout, tmp=None) -> None:
         _raise(self.L.raduls_gpu_sort(data.data_ptr(), tmp.data_ptr() if tmp is not None else None,
                                       n, layout.record_size, layout.key_size, self.stream()),
@@ -334,8 +436,10 @@ def _key_bytes_constant(andor: np.ndarray, ks: int) -> bool:
 
 
 def _splittable(ops, data, n, layout, digits: DigitPlan, group) -> np.ndarray:
-    """Hot digits whose records (over every rank) share one key."""
-    split = np.zeros(digits.n_digits, dtype=bool)
+    """Digits whose records (over every rank) share one key: a pivot's equal
+    digit by construction, a hot bucket without a pivot when digit_andor
+    proves it."""
+    split = digits.single.copy()
     if not digits.hot.any():
         return split
     ao = ops.digit_andor(data, n, layout, digits.p0, digits.bucket_digit, digits.hot)  # [D, 8]
@@ -349,9 +453,35 @@ def _splittable(ops, data, n, layout, digits: DigitPlan, group) -> np.ndarray:
     return split
 
 
+def _digits_with_pivots(ops, data, n: int, layout: RecordLayout, weights: np.ndarray, world: int,
+                        p0: int, group) -> DigitPlan:
+    """Digits from global bucket weights; every hot bucket is cut around its
+    most common sampled key (a pivot), so that key's run can be spread over
+    ranks by count even when the bucket holds other keys too. Arms the
+    pivots on the device (ops.set_pivots)."""
+    ks = layout.key_size
+    hot = hot_buckets(weights, world)
+    pivots = {}
+    if hot.any() and hasattr(ops, "sample_keys"):
+        k = ops.sample_keys(data, n, layout, SAMPLE_KEYS)
+        row = np.zeros((SAMPLE_KEYS, 32), dtype=np.uint8)
+        row[:len(k), :ks] = k
+        cnt = np.array([len(k)], dtype=np.int64)
+        flat = np.concatenate([cnt.view(np.uint8), row.reshape(-1)])
+        allk = _all_gather_np(flat, _coll_device(data, group), group)
+        keys = np.concatenate([allk[r, 8:].reshape(SAMPLE_KEYS, 32)[:int(allk[r, :8].view(np.int64)[0])]
+                               for r in range(allk.shape[0])])
+        pivots = choose_pivots(keys, p0, ks, hot, weights)
+    digits = make_digits(weights, world, p0, pivots=pivots)
+    if hasattr(ops, "set_pivots"):
+        ops.set_pivots(digits, ks)
+    return digits
+
+
 def plan_exchange(ops, data, n: int, layout: RecordLayout, group=None) -> ExchangePlan:
     """Exact plan: full AND/OR and full 16-bit prefix histograms, all-gathered;
-    per-source digit counts follow from the histograms."""
+    per-source digit counts follow from the histograms (or, with pivots, from
+    the partition's own histogram)."""
     import torch.distributed as dist
     world = dist.get_world_size(group)
     dev = _coll_device(data, group)
@@ -363,11 +493,16 @@ def plan_exchange(ops, data, n: int, layout: RecordLayout, group=None) -> Exchan
     # 2. 16-bit prefix histograms, all-gathered
     h = ops.prefix_hist(data, n, layout, p0).cpu().numpy().astype(np.int64)
     hist = _all_gather_np(h, dev, group).astype(np.int64)  # [world, 65536]
-    # 3. digits, hot single-key digits, exact counts, pieces
-    digits = make_digits(hist.sum(axis=0), world, p0)
+    # 3. digits (hot buckets cut around pivots), single-key digits, exact counts, pieces
+    digits = _digits_with_pivots(ops, data, n, layout, hist.sum(axis=0), world, p0, group)
     split = _splittable(ops, data, n, layout, digits, group)
-    M = np.stack([np.bincount(digits.bucket_digit, weights=hist[r].astype(np.float64),
-                              minlength=digits.n_digits) for r in range(world)]).astype(np.int64)
+    if digits.pivots:
+        mine = np.asarray(ops.digit_counts(data, n, layout, p0, digits.bucket_digit, digits.n_digits),
+                          dtype=np.uint64)
+        M = _all_gather_np(mine, dev, group).astype(np.int64)
+    else:
+        M = np.stack([np.bincount(digits.bucket_digit, weights=hist[r].astype(np.float64),
+                                  minlength=digits.n_digits) for r in range(world)]).astype(np.int64)
     pieces, S = assign_pieces(M, split, world)
     return ExchangePlan(digits, M, pieces, S)
 
@@ -404,7 +539,7 @@ def plan_exchange_sampled(ops, data, n: int, layout: RecordLayout, group=None):
         hr = rows[r, :NBUCKETS].astype(np.float64)
         if hr.sum() > 0:
             weights += hr * (float(rows[r, NBUCKETS]) / hr.sum())
-    digits = make_digits(weights, world, p0)
+    digits = _digits_with_pivots(ops, data, n, layout, weights, world, p0, group)
     split = _splittable(ops, data, n, layout, digits, group)
     # 3. exact per-digit counts and AND/OR from the partition's histogram, all-gathered
     counts, andor = ops.partition_plan(data, n, layout, p0, digits.bucket_digit, digits.n_digits)

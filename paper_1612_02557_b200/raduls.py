@@ -33,7 +33,7 @@ __all__ = [
     "RecordLayout", "SchedulerConfig", "TinyPolicy", "BigBinFraction", "ResourceError",
     "CudaError", "sort", "sort_device", "split", "histogram", "generate", "digest",
     "check_sorted", "last_stats", "DIST_UNIFORM", "DIST_SKEW", "local_capacity",
-    "set_profiling", "last_kernel_times", "LsdConfig", "lsd_sort", "rank_mode", "launch_count",
+    "set_profiling", "last_kernel_times", "LsdConfig", "lsd_sort", "rank_mode", "launch_count", "set_host_cache",
 ]
 
 DIST_UNIFORM = 0
@@ -220,6 +220,12 @@ def rank_mode() -> int:
     m = C.c_int(-1)
     _raise(_lib.load().raduls_gpu_rank_mode(C.byref(m)), "raduls_gpu_rank_mode")
     return m.value
+
+
+def set_host_cache(on: bool) -> None:
+    """Keep the host drop-in's device staging buffers between calls
+    (raduls_gpu_set_host_cache); off (default) frees them before each call returns."""
+    _raise(_lib.load().raduls_gpu_set_host_cache(1 if on else 0), "raduls_gpu_set_host_cache")
 
 
 def launch_count() -> int:

@@ -71,9 +71,29 @@ class CpuOps:
         return torch.from_numpy(np.bincount(self._prefix(data, n, layout, p0),
                                             minlength=D.NBUCKETS).astype(np.int64))
 
+    digits = None  # the plan's pivots (set_pivots), applied like map_digit on the device
+
+    def set_pivots(self, digits, ks):
+        self.digits = digits
+
+    def sample_keys(self, data, n, layout, samples):
+        s = min(n, samples)
+        r = data.numpy()[:n * layout.record_size].reshape(n, layout.record_size)
+        return r[np.arange(s) * (n // s), :layout.key_size].copy() if s else np.zeros((0, layout.key_size), np.uint8)
+
+    def _digits(self, data, n, layout, p0, bucket_digit):
+        r = data.numpy()[:n * layout.record_size].reshape(n, layout.record_size)
+        if self.digits is None or not self.digits.pivots:
+            return bucket_digit[self._prefix(data, n, layout, p0)].astype(np.int64)
+        assert np.array_equal(self.digits.bucket_digit, bucket_digit)
+        return D.map_digits_np(r, p0, layout.key_size, self.digits)
+
+    def digit_counts(self, data, n, layout, p0, bucket_digit, n_digits):
+        return np.bincount(self._digits(data, n, layout, p0, bucket_digit), minlength=n_digits).astype(np.uint64)
+
     def partition(self, data, n, layout, p0, bucket_rank, world):
         rs = layout.record_size
-        dest = bucket_rank[self._prefix(data, n, layout, p0)]
+        dest = self._digits(data, n, layout, p0, bucket_rank)
         order = np.argsort(dest, kind="stable")
         r = data.numpy()[:n * rs].reshape(n, rs)[order]
         return torch.from_numpy(r.reshape(-1).copy()), np.bincount(dest, minlength=world).astype(np.uint64)
@@ -82,7 +102,7 @@ class CpuOps:
         rs, ks = layout.record_size, layout.key_size
         out = np.zeros((len(hot), 8), dtype=np.uint64)
         out[:, 0::2] = ~np.uint64(0)
-        dig = bucket_digit[self._prefix(data, n, layout, p0)]
+        dig = self._digits(data, n, layout, p0, bucket_digit)
         w = data.numpy()[:n * rs].reshape(n, rs).view("<u8")
         for d in np.nonzero(hot)[0]:
             sel = w[dig == d]
@@ -109,6 +129,9 @@ def _input(rank, world, rs, ks, dist_kind, hot=0.0, n_total=40000):
         r = a.reshape(n_local, rs)
         rng = np.random.default_rng(1000 + rank)
         sel = rng.random(n_local) < hot
+        # other keys share the hot key's 16-bit prefix too (at scale a uniform
+        # input always puts some there): the bucket is hot but not single-key
+        r[(rng.random(n_local) < 0.05) & ~sel, :2] = (0x40, 0x41)
         r[sel, :ks] = np.frombuffer(bytes(range(0x40, 0x40 + ks)), dtype=np.uint8)
     return a
 
@@ -168,10 +191,11 @@ def test_gloo_world2_distributed_sort(rs, ks, dist_kind):
 
 @pytest.mark.parametrize("world", [2, 3, 4])
 def test_gloo_hot_key_is_split_over_ranks(world):
-    """60% of the records share one key: the hot 16-bit bucket holds a single
-    key, so its records are spread over consecutive ranks by count (SURVEY.md
-    §8(e) step 4) instead of landing on one rank; the concatenation is still
-    the stable sort of the concatenated inputs."""
+    """60% of the records share one key, and 2% more other keys with the same
+    16-bit prefix: the hot bucket is cut around its most common sampled key
+    (the pivot), whose run — one key — is spread over consecutive ranks by
+    count instead of landing on one rank; the
+    concatenation is still the stable sort of the concatenated inputs."""
     import oracle
     rs, ks = 16, 8
     res = _run_world(world, rs, ks, 0, hot=0.6)
@@ -184,16 +208,18 @@ def test_gloo_hot_key_is_split_over_ranks(world):
     assert all(res[r][1]["hot_split_digits"] >= 1 for r in range(world))
 
 
-def test_gloo_hot_bucket_with_two_keys_is_not_split():
-    """A hot 16-bit bucket holding two different keys must not be cut by
-    count (the cut could order them wrongly across ranks): it stays whole."""
+def test_gloo_hot_bucket_with_two_keys():
+    """A hot 16-bit bucket holding two keys (30% of the records each) must
+    never be cut by count across keys (the cut could order them wrongly
+    across ranks): only the pivot key's own run may be cut; the other key
+    stays whole in its below/above digit. The output is the stable sort."""
     import oracle
     world, rs, ks = 2, 16, 8
     ctx_res = _run_world_two_keys(world, rs, ks)
     got = np.concatenate([ctx_res[r][0] for r in range(world)])
     a = np.concatenate([_two_key_input(r, world, rs, ks) for r in range(world)])
     assert np.array_equal(got, oracle.stable_sort(a, rs, ks))
-    assert all(ctx_res[r][1]["hot_split_digits"] == 0 for r in range(world))
+    assert all(ctx_res[r][1]["hot_split_digits"] <= 1 for r in range(world))
 
 
 def _two_key_input(rank, world, rs, ks, n_total=40000):
@@ -284,3 +310,49 @@ def test_make_digits_hot_bucket_gets_own_digit():
     assert d[999] != d[1000] != d[1001]
     assert plan.hot[d[1000]] and plan.hot.sum() == 1
     assert plan.n_digits <= 4 + 2
+
+
+def test_make_digits_with_pivot_reserves_three_digits():
+    w = np.zeros(D.NBUCKETS)
+    w[:] = 1.0
+    w[1000] = 200000.0  # hot
+    w[40000] = 150000.0  # hot, no pivot given
+    plan = D.make_digits(w, 4, 0, pivots={1000: b"\x03\xe8\x00\x00\x00\x00\x00\x07"})
+    d = plan.bucket_digit.astype(np.int64)
+    assert np.all(np.diff(d) >= 0)
+    assert d[1001] == d[1000] + 3  # below / equal / above
+    assert plan.pivots == [(int(d[1000]), b"\x03\xe8\x00\x00\x00\x00\x00\x07")]
+    assert plan.single[d[1000] + 1] and not plan.single[d[1000]] and not plan.single[d[1000] + 2]
+    assert plan.hot[d[40000]] and not plan.single[d[40000]]
+    assert plan.n_digits == d[-1] + 1
+
+
+def test_map_digits_np_orders_around_pivot():
+    ks = 8
+    keys = np.array([[1, 2, 0, 0, 0, 0, 0, 5], [1, 2, 0, 0, 0, 0, 0, 7], [1, 2, 0, 0, 0, 0, 0, 9],
+                     [1, 2, 9, 0, 0, 0, 0, 0], [1, 3, 0, 0, 0, 0, 0, 0], [0, 0, 0, 0, 0, 0, 0, 0]],
+                    dtype=np.uint8)
+    w = np.ones(D.NBUCKETS)
+    w[0x0102] = 1e6
+    plan = D.make_digits(w, 2, 0, pivots={0x0102: bytes([1, 2, 0, 0, 0, 0, 0, 7])})
+    d = D.map_digits_np(keys, 0, ks, plan)
+    pd = int(plan.bucket_digit[0x0102])
+    assert list(d[:4]) == [pd, pd + 1, pd + 2, pd + 2]
+    assert d[4] >= pd + 3 and d[5] < pd
+    # digit order equals key order
+    order = np.lexsort(keys.T[::-1])
+    assert np.all(np.diff(d[order]) >= 0)
+
+
+def test_choose_pivots_picks_most_common_sampled_key():
+    ks = 8
+    rng = np.random.default_rng(5)
+    keys = rng.integers(0, 256, size=(3000, ks)).astype(np.uint8)
+    hotkey = np.array([7, 7, 1, 2, 3, 4, 5, 6], dtype=np.uint8)
+    keys[:1500] = hotkey
+    keys[1500:1600, :2] = (7, 7)  # same bucket, other keys
+    w = np.bincount(D.prefix16_np(keys, 0, ks), minlength=D.NBUCKETS).astype(np.float64)
+    hot = D.hot_buckets(w, 4)
+    assert hot[0x0707] and hot.sum() == 1
+    piv = D.choose_pivots(keys, 0, ks, hot, w)
+    assert piv == {0x0707: hotkey.tobytes()}

@@ -31,6 +31,10 @@ def _hot_input(data, n_local, rs, ks, rank, hot):
     sel = (torch.rand(n_local, generator=g) < hot).nonzero().flatten().to(data.device)
     key = torch.tensor([0x5A, 0x17, 0x33, 0x00, 0x42, 0x99, 0x01, 0xEE] * 3, dtype=torch.uint8,
                        device=data.device)[:ks]
+    # 3% of the other records get the hot key's 16-bit prefix (as any uniform
+    # input at scale does): the hot bucket is not single-key
+    near = (torch.rand(n_local, generator=g) < 0.03).nonzero().flatten().to(data.device)
+    data.view(n_local, rs)[near, :2] = key[:2]
     data.view(n_local, rs)[sel, :ks] = key
 
 
@@ -179,3 +183,34 @@ def test_bench_multi_rank_line(torch_cuda, tmp_path):
         assert r["nvlink"]["sent_bytes_per_gpu"] > 0 and r["nvlink"]["t_exchange_ms"] > 0
         assert r["roofline"]["frac"] > 0 and len(r["roofline"]["per_rank_frac"]) == 2
     assert line["gpu_launches"] > 0 and line["roofline_sort"]["frac"] > 0
+
+
+@pytest.mark.parametrize("rs,ks", [(16, 8), (32, 24), (8, 8)])
+def test_partition_pivot_digits_match_host(torch_cuda, rs, ks):
+    """The device map_digit (pivot-cut hot buckets, csrc/common.cuh) against
+    its host restatement (distributed.map_digits_np): per-digit counts and the
+    stable partition's bytes, through raduls_gpu_partition with pivots set."""
+    import paper_1612_02557_b200 as rg
+    from paper_1612_02557_b200 import distributed as D
+    n = 200_000
+    lay = rg.RecordLayout(rs, ks)
+    data = rg.generate(n, lay, seed=99)
+    _hot_input(data, n, rs, ks, 0, 0.5)
+    a = data.cpu().numpy().reshape(n, rs)
+    w = np.bincount(D.prefix16_np(a, 0, ks), minlength=D.NBUCKETS).astype(np.float64)
+    hot = D.hot_buckets(w, 4)
+    piv = D.choose_pivots(a[::7, :ks].copy(), 0, ks, hot, w)
+    assert len(piv) == 1
+    plan = D.make_digits(w, 4, 0, pivots=piv)
+    ops = D.DeviceOps()
+    ops.set_pivots(plan, ks)
+    try:
+        out, counts = ops.partition(data, n, lay, 0, plan.bucket_digit, plan.n_digits)
+        want_d = D.map_digits_np(a, 0, ks, plan)
+        assert list(counts.astype(np.int64)) == list(np.bincount(want_d, minlength=plan.n_digits))
+        order = np.argsort(want_d, kind="stable")
+        assert np.array_equal(out[:n * rs].cpu().numpy().reshape(n, rs), a[order])
+        c2 = ops.digit_counts(data, n, lay, 0, plan.bucket_digit, plan.n_digits)
+        assert np.array_equal(c2.astype(np.int64), counts.astype(np.int64))
+    finally:
+        ops.set_pivots(D.make_digits(w, 4, 0), ks)  # clear

@@ -319,6 +319,52 @@ def test_host_sort_out_of_core_late_varying_top_byte(rg, torch_cuda, monkeypatch
     assert np.array_equal(b, want)
 
 
+def test_host_sort_out_of_core_bucket_larger_than_device(rg, torch_cuda, monkeypatch):
+    """One 16-bit key prefix holds more records than a device part: that part
+    is sorted by the same out-of-core plan applied to its range (its next
+    varying bytes), recursively, instead of failing with ENOMEM."""
+    rs, ks, n = 16, 8, 6_000_000
+    a = make_input(n, rs, ks, 0xB16)
+    r = a.reshape(n, rs)
+    hot = np.random.default_rng(3).random(n) < 0.55
+    r[hot, 0], r[hot, 1] = 0x77, 0x33   # ~3.3 M records in one bucket (a part holds ~2.1 M)
+    r[hot[: n // 3].nonzero()[0][:1000], 2] = 0x00  # and a few ties deeper down
+    want = oracle.stable_sort(a, rs, ks)
+    monkeypatch.setenv("RADULS_GPU_DEVICE_BUDGET", str(96 << 20))
+    b = a.copy()
+    rg.sort(b, n, rg.RecordLayout(rs, ks))
+    assert np.array_equal(b, want)
+    c = a.copy()
+    tmp = np.empty_like(a)
+    rc = rg._lib.load().raduls_gpu_sort_host(c.ctypes.data, tmp.ctypes.data, n, rs, ks)
+    assert rc == 0 and np.array_equal(c, want)
+
+
+def test_host_sort_frees_its_device_buffers(rg, torch_cuda):
+    """The host drop-in frees its two n*rs device buffers before returning
+    (the reference frees its per-call aux, msd_sorter.hpp:52), unless the
+    caller opts into caching them (raduls_gpu_set_host_cache)."""
+    rs, ks, n = 16, 8, 1 << 25  # 512 MiB of records: 1 GiB of device buffers
+    a = make_input(n, rs, ks, 77)
+    torch_cuda.cuda.synchronize()
+    free0, _ = torch_cuda.cuda.mem_get_info()
+    b = a.copy()
+    rg.sort(b, n, rg.RecordLayout(rs, ks))
+    free1, _ = torch_cuda.cuda.mem_get_info()
+    assert free1 > free0 - (256 << 20)
+    try:
+        rg.set_host_cache(True)
+        c = a.copy()
+        rg.sort(c, n, rg.RecordLayout(rs, ks))
+        free2, _ = torch_cuda.cuda.mem_get_info()
+        assert free2 < free0 - (900 << 20)
+        assert np.array_equal(b, c)
+    finally:
+        rg.set_host_cache(False)
+    free3, _ = torch_cuda.cuda.mem_get_info()
+    assert free3 > free0 - (256 << 20)
+
+
 @pytest.mark.parametrize("rs,ks", [(8, 8), (16, 8), (24, 16), (32, 24)])
 def test_scatter_tile_boundaries(rg, torch_cuda, rs, ks):
     """Sizes straddling multiples of the scatter tile above the local-sort
