@@ -586,6 +586,17 @@ def main():
     if not args.no_e2e:
         e2e = run_e2e(rg, torch, dev, lay, n_local, base, dist_kind, seed, args.e2e_steps, world,
                       n_total, max_over_ranks, barrier, best)
+        if world == 1 and e2e.get("value"):
+            # the same with the drop-in's device buffers kept between calls
+            # (raduls_gpu_set_host_cache(1)); the headline above uses the
+            # default, which frees them before each call returns
+            rg.set_host_cache(True)
+            try:
+                c = run_e2e(rg, torch, dev, lay, n_local, base, dist_kind, seed, args.e2e_steps, world,
+                            n_total, max_over_ranks, barrier, best)
+                e2e["cached_buffers"] = {"value": c.get("value"), "ms_per_step": c.get("ms_per_step")}
+            finally:
+                rg.set_host_cache(False)
 
     if rank == 0:
         line = {
@@ -704,7 +715,8 @@ def run_e2e(rg, torch, dev, lay, n_local, base, dist_kind, seed, steps, world, n
     return {"value": n_total * len(times) / sum(times), "unit": UNIT,
             "h2d_bytes_per_step": n_total * rs, "d2h_bytes_per_step": n_total * rs,
             "ms_per_step": 1e3 * sum(times) / len(times), "steps": len(times), "warmup": 1,
-            "path": "raduls_gpu_sort_host (pinned host buffer)" if world == 1 else
+            "path": "raduls_gpu_sort_host (pinned host buffer; device buffers allocated and freed "
+                    "inside every call, as the reference's aux)" if world == 1 else
                     f"H2D + sort_distributed(exchange={exchange}) + D2H"}
 
 

@@ -131,6 +131,14 @@ int raduls_gpu_rank_mode(int* mode);
  * every entry point; a relaxed process-wide counter). */
 int raduls_gpu_launch_count(uint64_t* count);
 
+/* Checked build only (libraduls_gpu_checked.so, built with -DRG_CHECKED; the
+ * stand-in for compute-sanitizer): returns 1 and fills out6 = {violations,
+ * first violating address, its check site, its size, barrier timeouts,
+ * checked calls} accumulated over the process; any call that recorded a
+ * violation returned RADULS_GPU_EINTERNAL. The production library returns 0
+ * (zeros). */
+int raduls_gpu_check_report(uint64_t* out6);
+
 /* The host drop-ins (raduls_gpu_sort_host, raduls_gpu_lsd_sort_host) stage the
  * records in two device buffers of n*rec_size bytes. Default (0): freed before
  * the call returns, as the reference frees its per-call aux buffer

@@ -12,7 +12,10 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libraduls_gpu.so")
+# RADULS_GPU_LIB=checked selects the checked build (libraduls_gpu_checked.so,
+# bounds/alignment/deadlock checks and poisoned scratch; tests/test_gpu_checked.py)
+LIB_PATH = os.path.join(HERE, "libraduls_gpu_checked.so" if os.environ.get("RADULS_GPU_LIB") == "checked"
+                        else "libraduls_gpu.so")
 
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, EINTERNAL = 0, 1, 2, 3, 4, 5
 
@@ -52,6 +55,7 @@ EXPORTED = [
     "raduls_gpu_launch_count",
     "raduls_gpu_set_host_cache",
     "raduls_gpu_set_pivots",
+    "raduls_gpu_check_report",
 ]
 
 
@@ -135,6 +139,7 @@ def load(build_if_missing: bool = False):
         L.raduls_gpu_launch_count.argtypes = [_u64p]
         L.raduls_gpu_set_host_cache.argtypes = [C.c_int]
         L.raduls_gpu_set_pivots.argtypes = [_u32, _vp, _vp, _u32]
+        L.raduls_gpu_check_report.argtypes = [_u64p]
         L.raduls_gpu_digit_andor.argtypes = [_vp, _u64, _u32, _u32, _u32, _vp, _u32, _vp, _u64p, _vp]
         L.raduls_gpu_partition_store_pieces.argtypes = [_vp, _u64, _u32, _u32, _u32, _vp, _u64p, _u64p,
                                                         _vp]

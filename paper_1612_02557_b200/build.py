@@ -30,30 +30,39 @@ def _deps() -> list[str]:
     return out
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB):
+LIB_CHECKED = os.path.join(HERE, "libraduls_gpu_checked.so")
+
+
+def needs_build(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(d) > t for d in _deps())
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    if not force and not needs_build():
-        return LIB
+def build(verbose: bool = False, force: bool = False, checked: bool = False) -> str:
+    """libraduls_gpu.so, or (checked=True) libraduls_gpu_checked.so: the same
+    sources with -DRG_CHECKED (bounds/alignment checks on every global record
+    access, bounded mbarrier waits, poisoned scratch and shared memory,
+    optional scheduling jitter; see csrc/common.cuh) — the race/bounds
+    evidence on a pool without compute-sanitizer."""
+    lib = LIB_CHECKED if checked else LIB
+    if not force and not needs_build(lib):
+        return lib
     cmd = [NVCC, *GENCODE, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
            "-shared", "-cudart", "static", "-I", os.path.join(ROOT, "include"),
-           "-o", LIB + ".tmp", *SOURCES]
+           *(["-DRG_CHECKED"] if checked else []),
+           "-o", lib + ".tmp", *SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(lib + ".tmp", lib)
     if verbose:
         sys.stderr.write(res.stderr)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(verbose="--verbose" in sys.argv, force=True)
-    print(LIB)
+    print(build(verbose="--verbose" in sys.argv, force=True, checked="--checked" in sys.argv))

@@ -25,10 +25,81 @@ struct Rec {
     uint32_t w[kWords];
 };
 
+// ---------------------------------------------------------------- checked build
+//
+// RG_CHECKED (python -m paper_1612_02557_b200.build --checked ->
+// libraduls_gpu_checked.so): the stand-in for compute-sanitizer, which this
+// GPU pool does not run. Every global record access (vector loads/stores,
+// TMA bulk copies and L2 prefetches, digit-array stores) is checked against
+// the device ranges the current call registered (its data, tmp, digit arrays,
+// destinations); TMA copies also for the 16-B alignment the hardware needs.
+// mbarrier waits are bounded (a deadlock is counted instead of hanging the
+// GPU); dynamic shared memory and the scratch buffers are poisoned (0xA5)
+// before use, so a read of anything not written first changes the output;
+// and with jitter on, random __nanosleep at every producer/consumer hand-off
+// perturbs warp interleavings so an ordering race shows up as a parity
+// failure. The C-ABI returns RADULS_GPU_EINTERNAL from any call that
+// recorded a violation (raduls_gpu_check_report has the details).
+#ifdef RG_CHECKED
+struct ChkState {
+    unsigned long long lo[32], hi[32];
+    unsigned int n, jitter;
+    unsigned long long fails, first_addr, deadlocks;
+    unsigned int first_site, first_bytes;
+};
+__device__ ChkState g_chk;
+
+__device__ __noinline__ void chk_fail(uint32_t site, const void* p, uint32_t bytes) {
+    if (atomicAdd(&g_chk.fails, 1ull) == 0) {
+        g_chk.first_addr = reinterpret_cast<unsigned long long>(p);
+        g_chk.first_site = site;
+        g_chk.first_bytes = bytes;
+    }
+}
+
+__device__ __forceinline__ void chk_global(const void* p, uint32_t bytes, uint32_t site) {
+    const uint32_t n = *(volatile unsigned int*)&g_chk.n;
+    if (n == 0 || !__isGlobal(p)) return;
+    const unsigned long long a = reinterpret_cast<unsigned long long>(p);
+    for (uint32_t i = 0; i < n; ++i)
+        if (a >= g_chk.lo[i] && a + bytes <= g_chk.hi[i]) return;
+    chk_fail(site, p, bytes);
+}
+
+__device__ __forceinline__ void chk_jitter() {
+    if (*(volatile unsigned int*)&g_chk.jitter) {
+        unsigned long long h = clock64() ^ (uint64_t(blockIdx.x) << 20) ^ threadIdx.x;
+        h *= 0x9E3779B97F4A7C15ull;
+        __nanosleep(uint32_t(h >> 54));  // 0-1023 ns
+    }
+}
+
+__device__ __forceinline__ void chk_poison_smem(uint8_t* smem) {
+    uint32_t sz;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(sz));
+    for (uint32_t i = threadIdx.x * 4u; i + 4u <= sz; i += blockDim.x * 4u)
+        *reinterpret_cast<uint32_t*>(smem + i) = 0xA5A5A5A5u;
+    __syncthreads();
+}
+#define RG_CHK_G(p, bytes, site) ::rg::chk_global((p), (bytes), (site))
+#define RG_CHK_JITTER() ::rg::chk_jitter()
+#define RG_CHK_POISON_SMEM(smem) ::rg::chk_poison_smem(smem)
+#else
+#define RG_CHK_G(p, bytes, site) ((void)0)
+#define RG_CHK_JITTER() ((void)0)
+#define RG_CHK_POISON_SMEM(smem) ((void)0)
+#endif
+// check sites (raduls_gpu_check_report)
+enum : uint32_t {
+    kChkLoad = 1, kChkLoadStream = 2, kChkStore = 3, kChkStoreHint = 4, kChkTmaSrc = 5, kChkTmaAlign = 6,
+    kChkDigitStore = 7, kChkPrefetch = 8
+};
+
 template <int RS>
 __device__ __forceinline__ Rec<RS> load_rec(const uint8_t* base, uint64_t idx) {
     Rec<RS> r;
     const uint8_t* p = base + idx * RS;
+    RG_CHK_G(p, RS, kChkLoad);
     if constexpr (RS % 16 == 0) {
 #pragma unroll
         for (int v = 0; v < RS / 16; ++v) {
@@ -56,6 +127,7 @@ template <int RS>
 __device__ __forceinline__ Rec<RS> load_rec_stream(const uint8_t* base, uint64_t idx) {
     Rec<RS> r;
     const uint8_t* p = base + idx * RS;
+    RG_CHK_G(p, RS, kChkLoadStream);
     if constexpr (RS % 16 == 0) {
 #pragma unroll
         for (int v = 0; v < RS / 16; ++v) {
@@ -85,6 +157,7 @@ __device__ __forceinline__ Rec<RS> load_rec_stream(const uint8_t* base, uint64_t
 template <int RS>
 __device__ __forceinline__ void store_rec(uint8_t* base, uint64_t idx, const Rec<RS>& r) {
     uint8_t* p = base + idx * RS;
+    RG_CHK_G(p, RS, kChkStore);
     if constexpr (RS % 16 == 0) {
 #pragma unroll
         for (int v = 0; v < RS / 16; ++v)
@@ -250,6 +323,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, u
 // completion signalled as transaction bytes on `bar`.
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
                                             unsigned long long* bar) {
+    RG_CHK_G(src, bytes, kChkTmaSrc);
+#ifdef RG_CHECKED
+    if ((smem_u32(dst) | uint32_t(reinterpret_cast<uintptr_t>(src)) | bytes) & 15u) chk_fail(kChkTmaAlign, src, bytes);
+#endif
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
             smem_u32(dst)),
@@ -266,6 +343,11 @@ __device__ __forceinline__ void tma_load_1d_h(void* dst, const void* src, uint32
     if constexpr (kHint == 0) {
         tma_load_1d(dst, src, bytes, bar);
     } else {
+        RG_CHK_G(src, bytes, kChkTmaSrc);
+#ifdef RG_CHECKED
+        if ((smem_u32(dst) | uint32_t(reinterpret_cast<uintptr_t>(src)) | bytes) & 15u)
+            chk_fail(kChkTmaAlign, src, bytes);
+#endif
         uint64_t pol;
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
         asm volatile(
@@ -298,6 +380,7 @@ __device__ __forceinline__ void store_rec_h(uint8_t* base, uint64_t idx, const R
         else
             asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
         uint8_t* p = base + idx * RS;
+        RG_CHK_G(p, RS, kChkStoreHint);
 #pragma unroll
         for (int v = 0; v < RS / 16; ++v)
             asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p + 16 * v),
@@ -324,12 +407,22 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
     const uint32_t a = smem_u32(bar);
     uint32_t ok = 0;
+    RG_CHK_JITTER();
+#ifdef RG_CHECKED
+    uint32_t spins = 0;
+#endif
     do {
         asm volatile(
             "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
             : "=r"(ok)
             : "r"(a), "r"(phase)
             : "memory");
+#ifdef RG_CHECKED
+        if (!ok && ++spins == (1u << 22)) {  // seconds: a lost arrival or transaction
+            atomicAdd(&g_chk.deadlocks, 1ull);
+            return;
+        }
+#endif
     } while (!ok);
 }
 
@@ -339,6 +432,7 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
 
 // Named barrier over the first `nthreads` threads (consumer warps only).
 __device__ __forceinline__ void bar_sync_named(uint32_t id, uint32_t nthreads) {
+    RG_CHK_JITTER();
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 

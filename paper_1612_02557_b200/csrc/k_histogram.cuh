@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(HistCfg<RS>::kThreads + 64, HistCfg<RS>::kCtas
     using C = HistCfg<RS>;
     constexpr int T = C::kThreads, W = C::kWarps, IT = C::kItems, S = C::kStages, KW = RS / 8;
     extern __shared__ __align__(128) uint8_t smem[];
+    RG_CHK_POISON_SMEM(smem);
     __shared__ __align__(16) uint32_t s_h[S][kRadix];
     __shared__ unsigned long long s_and[S][W][KW], s_or[S][W][KW];
     // full: the tile landed (TMA); done: every consumer warp counted it; empty: drained
@@ -353,7 +354,10 @@ __global__ void __launch_bounds__(HistRegCfg<RS, kTile>::kThreads) k_tile_hist_r
         const uint64_t n2 = min(uint64_t(kTile), g2.size - k2 * kTile);
         const uintptr_t a0 = reinterpret_cast<uintptr_t>((g2.parity ? tmp : data) + (g2.start + k2 * kTile) * RS);
         const uintptr_t a = (a0 + 15) & ~uintptr_t(15), e = (a0 + n2 * RS) & ~uintptr_t(15);
-        if (e > a) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(uint32_t(e - a)) : "memory");
+        if (e > a) {
+            RG_CHK_G(reinterpret_cast<const void*>(a), uint32_t(e - a), kChkPrefetch);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(uint32_t(e - a)) : "memory");
+        }
     }
     Rec<RS> r[IT];
 #pragma unroll

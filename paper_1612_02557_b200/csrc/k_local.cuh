@@ -195,6 +195,7 @@ __device__ __forceinline__ void local_group(
     constexpr int T = C::kThreads, W = C::kWarps, IPT = C::kIpt;
     constexpr int KW = RS / 8;
     extern __shared__ __align__(128) uint8_t smem[];
+    RG_CHK_POISON_SMEM(smem);
     // [perm][win][slot][cnt]: win..cnt is one span, the 8-B output's staging area
     uint16_t* perm = reinterpret_cast<uint16_t*>(smem + C::kRecBytes);  // [cap] final order / fpos
     uint32_t* win = reinterpret_cast<uint32_t*>(perm + C::kCap);        // [cap]
@@ -746,6 +747,7 @@ __device__ __forceinline__ void prefetch_group_l2(const uint8_t* data, const uin
     const uintptr_t e = (src + uintptr_t(g.size) * RS) & ~uintptr_t(15);
     for (; a < e; a += 32768) {
         const uint32_t sz = uint32_t(min(uintptr_t(32768), e - a));
+        RG_CHK_G(reinterpret_cast<const void*>(a), sz, kChkPrefetch);
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(sz) : "memory");
     }
 }
@@ -812,6 +814,10 @@ __global__ void __launch_bounds__(256) k_copy_back(uint8_t* __restrict__ data,
     const uint64_t bytes = uint64_t(c.size) * RS;
     const uint8_t* s = tmp + c.start * RS;
     uint8_t* d = data + c.start * RS;
+    if (threadIdx.x == 0) {
+        RG_CHK_G(s, uint32_t(bytes), kChkLoad);
+        RG_CHK_G(d, uint32_t(bytes), kChkStore);
+    }
     if constexpr (RS % 16 == 0) {
         for (uint64_t i = threadIdx.x; i < bytes / 16; i += blockDim.x)
             reinterpret_cast<uint4*>(d)[i] = reinterpret_cast<const uint4*>(s)[i];

@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
     using C = ScatterCfg<RS>;
     constexpr int T = C::kThreads, IT = C::kItems, W = C::kWarps;
     extern __shared__ __align__(128) uint8_t smem[];
+    RG_CHK_POISON_SMEM(smem);
     uint8_t* buf0 = smem;
     constexpr int S = C::kStages;
     // Plain split: the digits can come TMA-loaded from nd_in (this level's
@@ -388,6 +389,7 @@ __global__ void __launch_bounds__(ScatterCfg<RS>::kThreads + 32, ScatterCfg<RS>:
                     store_rec_h<RS, RG_HINT_SCST>(dst, di, v);
                     if (m >> 24) {
                         if constexpr (RG_HINT_NDST == 0) {
+                            RG_CHK_G(nd + ti.seg_start + di, 1, kChkDigitStore),
                             nd[ti.seg_start + di] = uint8_t(rec_byte<RS>(v, p + 1));
                         } else {
                             uint64_t pol;

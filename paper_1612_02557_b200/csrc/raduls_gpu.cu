@@ -88,6 +88,85 @@ static inline void note_launch() { g_launches.fetch_add(1, std::memory_order_rel
 // the reference's per-call aux buffer, P/include/raduls/detail/msd_sorter.hpp:52).
 static std::atomic<int> g_host_cache{0};
 
+// Checked build (RG_CHECKED; see common.cuh): the device ranges the current
+// call may touch, the per-call violation check, the report.
+#ifdef RG_CHECKED
+struct ChkHost {
+    std::mutex mu;
+    std::vector<std::pair<uint64_t, uint64_t>> ranges;
+    unsigned long long report[6] = {};  // fails, first_addr, site, bytes, deadlocks, checked calls
+};
+static ChkHost g_chk_host;
+static void chk_upload(cudaStream_t st) {
+    // RADULS_GPU_CHECK_SHRINK=B (negative control of the tests): every range
+    // B bytes shorter, so a correct sort must be reported
+    static const uint64_t shrink = std::getenv("RADULS_GPU_CHECK_SHRINK")
+                                       ? std::strtoull(std::getenv("RADULS_GPU_CHECK_SHRINK"), nullptr, 10) : 0;
+    for (auto& r : g_chk_host.ranges) r.second = std::max(r.first, r.second - shrink);
+    rg::ChkState h{};
+    const size_t k = std::min<size_t>(g_chk_host.ranges.size(), 32);
+    for (size_t i = 0; i < k; ++i) h.lo[i] = g_chk_host.ranges[i].first, h.hi[i] = g_chk_host.ranges[i].second;
+    h.n = unsigned(k);
+    RG_CHECK(cudaMemcpyToSymbolAsync(rg::g_chk, &h, offsetof(rg::ChkState, fails), 0, cudaMemcpyHostToDevice, st));
+}
+// Replace (reset = true) or extend the registered ranges; enqueued on st.
+static void chk_ranges(cudaStream_t st, std::initializer_list<std::pair<const void*, size_t>> r,
+                       bool reset = true) {
+    std::lock_guard<std::mutex> lk(g_chk_host.mu);
+    if (reset) g_chk_host.ranges.clear();
+    for (auto& x : r)
+        if (x.first && x.second)
+            g_chk_host.ranges.emplace_back(reinterpret_cast<uint64_t>(x.first),
+                                           reinterpret_cast<uint64_t>(x.first) + x.second);
+    chk_upload(st);
+}
+static void chk_begin() {
+    cudaDeviceSynchronize();
+    {
+        std::lock_guard<std::mutex> lk(g_chk_host.mu);
+        g_chk_host.ranges.clear();
+    }
+    rg::ChkState h{};
+    h.jitter = std::getenv("RADULS_GPU_CHECK_JITTER") ? 1u : 0u;
+    cudaMemcpyToSymbol(rg::g_chk, &h, sizeof h);
+}
+// 0, or RADULS_GPU_EINTERNAL after printing the first violation
+static int chk_end() {
+    cudaDeviceSynchronize();
+    rg::ChkState h{};
+    if (cudaMemcpyFromSymbol(&h, rg::g_chk, sizeof h) != cudaSuccess) return RADULS_GPU_ECUDA;
+    std::lock_guard<std::mutex> lk(g_chk_host.mu);
+    g_chk_host.report[5]++;
+    if (!h.fails && !h.deadlocks) return 0;
+    if (!g_chk_host.report[0] && !g_chk_host.report[4]) {
+        g_chk_host.report[1] = h.first_addr;
+        g_chk_host.report[2] = h.first_site;
+        g_chk_host.report[3] = h.first_bytes;
+    }
+    g_chk_host.report[0] += h.fails;
+    g_chk_host.report[4] += h.deadlocks;
+    std::fprintf(stderr, "raduls_gpu[checked]: %llu out-of-range/misaligned accesses (first: site %u, addr 0x%llx, %u B), "
+                 "%llu barrier timeouts\n", h.fails, h.first_site, h.first_addr, h.first_bytes, h.deadlocks);
+    return RADULS_GPU_EINTERNAL;
+}
+static void chk_ranges_vec(cudaStream_t st, const std::vector<std::pair<const void*, size_t>>& r) {
+    std::lock_guard<std::mutex> lk(g_chk_host.mu);
+    g_chk_host.ranges.clear();
+    for (auto& x : r)
+        if (x.first && x.second)
+            g_chk_host.ranges.emplace_back(reinterpret_cast<uint64_t>(x.first),
+                                           reinterpret_cast<uint64_t>(x.first) + x.second);
+    chk_upload(st);
+}
+#define RG_CHK_RANGES_VEC(st, v) chk_ranges_vec((st), (v))
+#define RG_CHK_RANGES(st, ...) chk_ranges((st), __VA_ARGS__)
+#define RG_CHK_RANGES_ADD(st, ...) chk_ranges((st), __VA_ARGS__, false)
+#else
+#define RG_CHK_RANGES(st, ...) ((void)0)
+#define RG_CHK_RANGES_ADD(st, ...) ((void)0)
+#define RG_CHK_RANGES_VEC(st, v) ((void)0)
+#endif
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
@@ -654,6 +733,19 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
     ensure_caps<RS>(ws, n);
     LevelCounters* dctr = ws.ctr.p;
     RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, sizeof(unsigned int), st));
+    RG_CHK_RANGES(st, {{data, size_t(n) * RS}, {tmp, size_t(n) * RS}});
+#ifdef RG_CHECKED
+    {  // poison the scratch: nothing may be read before this sort writes it
+        if (tmp != data) RG_CHECK(cudaMemsetAsync(tmp, 0xA5, size_t(n) * RS, st));
+        RG_CHECK(cudaMemsetAsync(ws.tile_cnt.p, 0xA5, ws.tile_cnt.cap * sizeof(uint16_t), st));
+        RG_CHECK(cudaMemsetAsync(ws.tile_off.p, 0xA5, ws.tile_off.cap * sizeof(uint32_t), st));
+        for (int b = 0; b < 2; ++b)
+            RG_CHECK(cudaMemsetAsync(ws.seg_tot[b].p, 0xA5, ws.seg_tot[b].cap * sizeof(unsigned long long), st));
+        RG_CHECK(cudaMemsetAsync(ws.groups.p, 0xA5, ws.groups.cap * sizeof(Group), st));
+        RG_CHECK(cudaMemsetAsync(ws.copies.p, 0xA5, ws.copies.cap * sizeof(CopyRange), st));
+        if (ws.nd.p) RG_CHECK(cudaMemsetAsync(ws.nd.p, 0xA5, ws.nd.cap, st));
+    }
+#endif
 
     if (n <= uint64_t(local_cap<RS>())) {  // one group sorts everything, in place
         Group g{0, uint32_t(n), 0, 0, 0};
@@ -716,6 +808,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
     // without the 2n extra bytes every level reads whole records.
     constexpr int nd_halves = ScatterCfg<RS>::kNdSmem ? 2 : 1;
     const size_t nd_stride = digit_arrays(ws, n, nd_halves);
+    RG_CHK_RANGES_ADD(st, {{ws.nd.p, nd_stride ? ws.nd.cap : 0}});
     const uint8_t* nd_in = nullptr;  // this level's digits (null: read from the records)
     int nd_half = 0;
     // The level loop from `level` on (its counters at dctr + level); returns the
@@ -883,8 +976,14 @@ template <typename F>
 int guarded(F&& f) {
     cudaGetLastError();  // a stale non-sticky error (e.g. a caller's failed allocation) is not ours
     try {
+#ifdef RG_CHECKED
+        chk_begin();
+        f();
+        return chk_end();
+#else
         f();
         return RADULS_GPU_OK;
+#endif
     } catch (const CudaError& e) {
         return e.code;
     } catch (const std::bad_alloc&) {
@@ -1302,6 +1401,7 @@ template <int RS>
 void lsd_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t ks, cudaStream_t st) {
     uint8_t* src = data;
     uint8_t* dst = tmp;
+    RG_CHK_RANGES(st, {{data, size_t(n) * RS}, {tmp, size_t(n) * RS}});
     for (uint32_t pass = 0; pass < ks; ++pass) {
         const uint32_t byte = ks - 1 - pass;
         unsigned long long* tot = ws.h_small;
@@ -1383,6 +1483,7 @@ int raduls_gpu_split(const void* d_src, void* d_dst, uint64_t n, uint32_t rs,
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         if (h_counts) std::memset(h_counts, 0, 256 * sizeof(uint64_t));
         if (n == 0) return;
+        RG_CHK_RANGES(st, {{d_src, size_t(n) * rs}, {d_dst, size_t(n) * rs}});
         dispatch_rs(rs, [&](auto R) {
             constexpr int RSC = decltype(R)::value;
             uint8_t* src = const_cast<uint8_t*>(static_cast<const uint8_t*>(d_src));
@@ -1437,6 +1538,7 @@ int raduls_gpu_generate(void* d_out, uint64_t n, uint32_t rs, uint32_t ks, uint3
                                      cudaMemcpyHostToDevice, st));
         }
         GenParams P{n, seed, index_base, ks, dist, ws.thr.p};
+        RG_CHK_RANGES(st, {{d_out, size_t(n) * rs}});
         dispatch_rs(rs, [&](auto R) {
             k_gen<decltype(R)::value><<<grid_for(n, 256, 16), 256, 0, st>>>(static_cast<uint8_t*>(d_out), P);
             note_launch();
@@ -1455,6 +1557,7 @@ int raduls_gpu_digest(const void* d_data, uint64_t n, uint32_t rs, uint64_t* lo,
         std::lock_guard<std::mutex> lk(ws.mu);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         RG_CHECK(cudaMemsetAsync(ws.acc.p, 0, 2 * sizeof(unsigned long long), st));
+        RG_CHK_RANGES(st, {{d_data, size_t(n) * rs}});
         if (n) {
             dispatch_rs(rs, [&](auto R) {
                 k_digest<decltype(R)::value><<<grid_for(n, 256, 8), 256, 0, st>>>(
@@ -1480,6 +1583,7 @@ int raduls_gpu_check_sorted(const void* d_data, uint64_t n, uint32_t rs, uint32_
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         unsigned long long init[2] = {0ull, ~0ull};
         RG_CHECK(cudaMemcpyAsync(ws.acc.p, init, sizeof init, cudaMemcpyHostToDevice, st));
+        RG_CHK_RANGES(st, {{d_data, size_t(n) * rs}});
         if (n > 1) {
             dispatch_rs(rs, [&](auto R) {
                 k_check_sorted<decltype(R)::value><<<grid_for(n, 256, 8), 256, 0, st>>>(
@@ -1544,6 +1648,7 @@ int raduls_gpu_partition(const void* d_src, void* d_dst, uint64_t n, uint32_t rs
         if (h_rank_counts) std::memset(h_rank_counts, 0, n_ranks * sizeof(uint64_t));
         if (!load_rank_map(ws, d_bucket_rank, n_ranks, st)) throw CudaError{RADULS_GPU_EINVAL};
         if (!n) return;
+        RG_CHK_RANGES(st, {{d_src, size_t(n) * rs}, {d_dst, size_t(n) * rs}});
         dispatch_rs(rs, [&](auto R) {
             constexpr int RSC = decltype(R)::value;
             uint8_t* src = const_cast<uint8_t*>(static_cast<const uint8_t*>(d_src));
@@ -1575,6 +1680,13 @@ int raduls_gpu_partition_to(const void* d_src, uint64_t n, uint32_t rs, uint32_t
         for (uint32_t r = 0; r < kRadix; ++r) hd[r] = r < n_ranks ? h_dst[r] : 0ull;
         RG_CHECK(cudaMemcpyAsync(ws.dig_dst.p, hd, kRadix * sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
         if (!n) return;
+#ifdef RG_CHECKED
+        {
+            std::vector<std::pair<const void*, size_t>> rr{{d_src, size_t(n) * rs}};
+            for (uint32_t r = 0; r < n_ranks; ++r) rr.emplace_back(reinterpret_cast<const void*>(h_dst[r]), size_t(n) * rs);
+            RG_CHK_RANGES_VEC(st, rr);
+        }
+#endif
         dispatch_rs(rs, [&](auto R) {
             constexpr int RSC = decltype(R)::value;
             uint8_t* src = const_cast<uint8_t*>(static_cast<const uint8_t*>(d_src));
@@ -1602,6 +1714,7 @@ int raduls_gpu_partition_plan(const void* d_src, uint64_t n, uint32_t rs, uint32
         for (int w = 0; w < 8; ++w) h_andor[w] = (w & 1) ? 0ull : ~0ull;
         if (!load_rank_map(ws, d_bucket_rank, n_ranks, st)) throw CudaError{RADULS_GPU_EINVAL};
         if (!n) return;
+        RG_CHK_RANGES(st, {{d_src, size_t(n) * rs}});
         dispatch_rs(rs, [&](auto R) {
             constexpr int RSC = decltype(R)::value;
             uint8_t* src = const_cast<uint8_t*>(static_cast<const uint8_t*>(d_src));
@@ -1638,6 +1751,14 @@ int raduls_gpu_partition_store(const void* d_src, uint64_t n, uint32_t rs, uint3
             if (hd[r] % (rs % 16 == 0 ? 16 : 8)) throw CudaError{RADULS_GPU_EINVAL};
         }
         RG_CHECK(cudaMemcpyAsync(ws.dig_dst.p, hd, kRadix * sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+#ifdef RG_CHECKED
+        {
+            std::vector<std::pair<const void*, size_t>> rr{{d_src, size_t(n) * rs}};
+            for (uint32_t r = 0; r < kRadix; ++r)
+                if (ws.part.tot[r]) rr.emplace_back(reinterpret_cast<const void*>(h_dst[r]), ws.part.tot[r] * rs);
+            RG_CHK_RANGES_VEC(st, rr);
+        }
+#endif
         dispatch_rs(rs, [&](auto R) {
             constexpr int RSC = decltype(R)::value;
             uint8_t* src = const_cast<uint8_t*>(static_cast<const uint8_t*>(d_src));
@@ -1696,6 +1817,15 @@ int raduls_gpu_partition_store_pieces(const void* d_src, uint64_t n, uint32_t rs
         ws.part.pending = false;
         ws.dig_dst.ensure(kRadix);
         RG_CHECK(cudaMemcpyAsync(ws.dig_dst.p, hd, kRadix * sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+#ifdef RG_CHECKED
+        {
+            std::vector<std::pair<const void*, size_t>> rr{{d_src, size_t(n) * rs}};
+            for (uint32_t k = 0; k < n_pieces; ++k)
+                if (h_piece_count[k])
+                    rr.emplace_back(reinterpret_cast<const void*>(h_piece_dst[k]), h_piece_count[k] * rs);
+            RG_CHK_RANGES_VEC(st, rr);
+        }
+#endif
         if (!table.empty()) {
             ws.pieces.ensure(table.size());
             RG_CHECK(cudaMemcpyAsync(ws.pieces.p, table.data(), table.size() * sizeof(Piece), cudaMemcpyHostToDevice,
@@ -1886,6 +2016,18 @@ int raduls_gpu_set_pivots(uint32_t n_pivots, const uint32_t* digits, const uint8
         }
         ws.n_pivots = n_pivots;
     });
+}
+
+int raduls_gpu_check_report(uint64_t* out6) {
+    if (!out6) return RADULS_GPU_EINVAL;
+#ifdef RG_CHECKED
+    std::lock_guard<std::mutex> lk(g_chk_host.mu);
+    for (int i = 0; i < 6; ++i) out6[i] = g_chk_host.report[i];
+    return 1;
+#else
+    for (int i = 0; i < 6; ++i) out6[i] = 0;
+    return 0;
+#endif
 }
 
 int raduls_gpu_set_host_cache(int on) {

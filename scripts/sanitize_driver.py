@@ -1,4 +1,5 @@
-"""Workload for compute-sanitizer (scripts/sanitize.sh): every kernel family of
+"""Workload for compute-sanitizer (scripts/sanitize.sh) and for the checked build
+(RADULS_GPU_LIB=checked; tests/test_gpu_checked.py): every kernel family of
 libraduls_gpu.so on small C1-, C2-, C3- and C4-shaped inputs, checked against
 the oracle so a run that "passes" the tool also sorted correctly.
 
@@ -99,6 +100,11 @@ def main():
     rg.digest(g, 1000, rs)
     rg.check_sorted(g, 1000, lay)
     print("ok utilities", flush=True)
+    import ctypes as C
+    rep = np.zeros(6, dtype=np.uint64)
+    if rg._lib.load().raduls_gpu_check_report(rep.ctypes.data_as(C.POINTER(C.c_uint64))) == 1:
+        print(f"checked build: calls {int(rep[5])} violations {int(rep[0])} timeouts {int(rep[4])}", flush=True)
+        assert rep[0] == 0 and rep[4] == 0, rep
     print("DRIVER OK", flush=True)
 
 
