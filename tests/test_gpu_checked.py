@@ -71,6 +71,9 @@ def test_parity_suite_under_checked_build(torch_cuda):
     res = _run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-k", DESELECT, *PARITY], _env(),
                timeout=3000)
     assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-2000:]
+    import re
+    m = re.search(r"(\d+) passed", res.stdout)
+    assert m and int(m.group(1)) >= 60, res.stdout[-2000:]
 
 
 def test_every_kernel_family_under_jitter(torch_cuda):
