@@ -505,10 +505,11 @@ def main():
         step_ms, region, rows = measure(ex)
         regions.append(region)
         runs[ex] = (step_ms, rows)
+        if world > 1:  # the next exchange (and e2e) gets the memory back
+            from paper_1612_02557_b200.distributed import release_peer_windows
+            release_peer_windows()
+            torch.cuda.empty_cache()
     clk = clocks.stop((regions[0][0], regions[-1][1]))
-    if world > 1:
-        from paper_1612_02557_b200.distributed import release_peer_windows
-        release_peer_windows()
 
     def summarise(ex, step_ms, rows) -> dict:
         total_ms = sum(step_ms)
@@ -672,15 +673,14 @@ def run_e2e(rg, torch, dev, lay, n_local, base, dist_kind, seed, steps, world, n
     inside the timed region (raduls_gpu_sort_host at N=1; H2D + distributed sort
     + D2H into a pinned result buffer at N>1), after one untimed warm-up call."""
     rs = lay.record_size
-    nbytes = n_local * rs
+    # N>1: one pinned buffer per rank for the input and this rank's key range
+    # of the output (which may be a little larger than its input share)
+    cap = n_local if world == 1 else int(n_local * 1.25 + (1 << 20))
     try:
-        host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        host = torch.empty(cap * rs, dtype=torch.uint8, pin_memory=True)
     except RuntimeError as ex:
         return {"value": None, "unit": UNIT, "error": f"pinned alloc failed: {ex}"[:200]}
     times = []
-    res = None  # N>1: pinned result buffer, allocated outside the timed region
-    if world > 1:
-        res = torch.empty(int(n_local * 1.25 + (1 << 20)) * rs, dtype=torch.uint8, pin_memory=True)
     for step in range(steps + 1):  # step 0: untimed warm-up (library buffers, windows)
         # pristine input into the pinned buffer (untimed), generated on the device
         # in 4 GiB chunks so the library's own device buffers still fit
@@ -698,19 +698,19 @@ def run_e2e(rg, torch, dev, lay, n_local, base, dist_kind, seed, steps, world, n
             rg.sort(host.numpy(), n_local, lay)  # raduls_gpu_sort_host: H2D, sort, D2H
         else:
             from paper_1612_02557_b200.distributed import sort_distributed
-            d = host.to(dev, non_blocking=True)
+            d = host[:n_local * rs].to(dev, non_blocking=True)
             out, n_out = sort_distributed(d, n_local, lay, exchange=exchange)
             del d
-            if res.numel() < n_out * rs:  # (skewed keys: a bigger range than planned for)
-                res = torch.empty(n_out * rs, dtype=torch.uint8, pin_memory=True)
-            res[:n_out * rs].copy_(out[:n_out * rs])
+            if host.numel() < n_out * rs:  # (skewed keys: a bigger range than planned for)
+                host = torch.empty(n_out * rs, dtype=torch.uint8, pin_memory=True)
+            host[:n_out * rs].copy_(out[:n_out * rs])
             torch.cuda.synchronize(dev)
             del out
         dt = max_over_ranks(time.perf_counter() - t0)
         if step:
             times.append(dt)
         barrier()
-    del host, res
+    del host
     torch.cuda.empty_cache()
     return {"value": n_total * len(times) / sum(times), "unit": UNIT,
             "h2d_bytes_per_step": n_total * rs, "d2h_bytes_per_step": n_total * rs,
