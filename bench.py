@@ -568,7 +568,8 @@ def main():
             if name == args.config:
                 continue
             try:
-                per_config[name] = measure_config(rg, torch, dev, name, 3, 2, peak, peak_src)
+                time.sleep(3)  # let the HBM/power state settle after the previous config
+                per_config[name] = measure_config(rg, torch, dev, name, 3, 3, peak, peak_src)
             except Exception as ex:  # noqa: BLE001
                 per_config[name] = {"error": str(ex)[:200]}
 
