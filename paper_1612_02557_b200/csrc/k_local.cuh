@@ -68,6 +68,20 @@ struct LocalCfg {
     static constexpr int kCntBytes = (kCntWords * 4 > kWarps * kRadix * 4) ? kCntWords * 4
                                                                              : kWarps * kRadix * 4;
     static constexpr int kRecBytes = kRegRecords ? 0 : ((kCap * RS + 16 + 127) / 128) * 128;
+    // RG_LOC_LIST=1 (shared-memory records): singletons placed during the id
+    // scatter, records of multi-record buckets appended to a CTA list (kList
+    // u16 entries fit beside two CTAs per SM at 16/24 B) and ranked densely
+    // from it. Fewer instructions, but each list entry is a chain of four
+    // dependent shared-memory loads with ~2.5 entries per thread, against
+    // three with seven independent records per thread in the per-record pass:
+    // measured slower (interleaved A/B, one box: C5 local 50.3 vs 47.3 ms, C1
+    // +5%, C4 +9%, C2 unchanged); off by default.
+#ifndef RG_LOC_LIST
+#define RG_LOC_LIST 0
+#endif
+    static constexpr int kList = (kRegRecords || !RG_LOC_LIST) ? 0 : RS == 32 ? kCap : 2560;
+    static constexpr int kTotWords = (kList / 2 > 512) ? kList / 2 : 512;
+    static constexpr int kBmWords = kList ? (1 << kBucketBits) / 32 : 1;
     static constexpr size_t kSmem = size_t(kRecBytes) + size_t(kCap) * (4 + 2 + 2) + kCntBytes;
 };
 
@@ -201,7 +215,9 @@ __device__ __forceinline__ void local_group(
     uint32_t* win = reinterpret_cast<uint32_t*>(perm + C::kCap);        // [cap]
     uint16_t* slot = reinterpret_cast<uint16_t*>(win + C::kCap);        // [cap] bucket order
     uint32_t* cnt = reinterpret_cast<uint32_t*>(slot + C::kCap);        // packed u16 pairs
-    __shared__ uint32_t s_tot[512];
+    __shared__ uint32_t s_tot[C::kTotWords];  // LSD totals / deferred lists / the multi-bucket list (u16)
+    __shared__ uint32_t s_bm[C::kBmWords];     // kList: singleton-bucket bitmap
+    __shared__ uint32_t s_lcnt;                // kList: multi-bucket list length
     __shared__ uint32_t s_scan[65];
     __shared__ uint32_t s_and[W][2 * KW], s_or[W][2 * KW];
     __shared__ uint32_t s_Lw[W][32];  // per-warp copy of the varying key bytes
@@ -254,7 +270,10 @@ __device__ __forceinline__ void local_group(
         s_flag = 0;
         for (int q = 0; q < W; ++q) s_wq[q] = 0;
         s_maxb = 0;
+        s_lcnt = 0;
     }
+    if constexpr (C::kList > 0)
+        for (uint32_t q = threadIdx.x; q < uint32_t(C::kBmWords); q += T) s_bm[q] = 0;
     // bucket counters zeroed now (first used by the histogram, several barriers on)
     for (uint32_t i = threadIdx.x; i < uint32_t(C::kCntWords + 3) / 4; i += T)
         reinterpret_cast<uint4*>(cnt)[i] = make_uint4(0, 0, 0, 0);
@@ -481,21 +500,38 @@ __device__ __forceinline__ void local_group(
         // Packed u16 pairs are summed as u32 (each half stays < 65536).
         uint4* pv = reinterpret_cast<uint4*>(&cw(b0));
         const uint32_t nv = per / 8;
+        // kList: bit b of s_bm = bucket b holds exactly one record
+        auto ones = [](uint32_t w) {  // the two u16 halves == 1 -> bits 0, 1
+            return uint32_t((w & 0xFFFFu) == 1u) | (uint32_t((w >> 16) == 1u) << 1);
+        };
         if (per >= 8) {
-            uint32_t S = 0, M = 0;
+            uint32_t S = 0, M = 0, bits = 0;
             for (uint32_t v = 0; v < nv; ++v) {
                 const uint4 q = pv[v];
                 S += q.x + q.y + q.z + q.w;
                 M = __vmaxu2(M, __vmaxu2(__vmaxu2(q.x, q.y), __vmaxu2(q.z, q.w)));
+                if constexpr (C::kList > 0) {
+                    const uint32_t m8 = ones(q.x) | (ones(q.y) << 2) | (ones(q.z) << 4) | (ones(q.w) << 6);
+                    bits |= m8 << ((v * 8u) & 31u);
+                    if (((v * 8u + 8u) & 31u) == 0u || v + 1 == nv) {
+                        const uint32_t bb0 = b0 + ((v * 8u) & ~31u);
+                        atomicOr(&s_bm[bb0 >> 5], bits << (bb0 & 31u));
+                        bits = 0;
+                    }
+                }
             }
             sum = (S & 0xFFFFu) + (S >> 16);
             mx = max(M & 0xFFFFu, M >> 16);
         } else if (b0 < nbk) {
+            uint32_t bits = 0;
             for (uint32_t b = b0; b < b0 + per; ++b) {
                 const uint32_t c = end_of(b);  // still counts
                 sum += c;
                 mx = c > mx ? c : mx;
+                bits |= uint32_t(c == 1u) << (b - b0);
             }
+            if constexpr (C::kList > 0)
+                if (bits) atomicOr(&s_bm[b0 >> 5], bits << (b0 & 31u));
         }
         uint32_t total;
         uint32_t run = block_scan_excl<false>(sum, s_scan, &total);
@@ -533,24 +569,6 @@ __device__ __forceinline__ void local_group(
     __syncthreads();
 
     if (!kFallback && s_maxb <= kMaxBucket) {
-        // ---- 5. record ids into bucket order (cnt: starts -> ends)
-#pragma unroll
-        for (int j = 0; j < IPT; ++j) {
-            if (uint32_t(j) * T >= n) break;  // block-uniform
-            const uint32_t e = uint32_t(j) * T + threadIdx.x;
-            if (e < n) {
-                uint32_t i;  // the bucket's u16 counter index
-                if constexpr (KEEP) i = bk[j] & 0xFFFFu;
-                else i = i16_of(bucket_of(win[e]));
-                const uint32_t old = atomicAdd(&cnt[i >> 1], 1u << ((i & 1) * 16));
-                slot[(old >> ((i & 1) * 16)) & 0xFFFFu] = uint16_t(e);
-            }
-        }
-        __syncthreads();
-        // ---- 6. order inside buckets (~1 record each). Per record: size-1
-        // bucket -> its start; size-2 -> one comparison; larger buckets (a few
-        // percent) go to a compact list processed densely afterwards, so no
-        // warp iterates to its largest bucket.
         auto less = [&](uint32_t w2, uint32_t e2, uint32_t w, uint32_t e) -> bool {
             if (w2 != w) return w2 < w;
             const int c = beyond ? cmp_rest(e2, e) : 0;
@@ -568,74 +586,147 @@ __device__ __forceinline__ void local_group(
             }
             return rank;
         };
-        // records of buckets over 3 go to a per-warp list (s_tot: 1024 u16 split
-        // over the warps), ranked densely by the same warp after its loop — no
-        // block barrier between the two; s_wq (the lengths) are 0 from the start
-        constexpr uint32_t kWq = 1024 / W;
-        uint16_t* lst = reinterpret_cast<uint16_t*>(s_tot) + warp * kWq;
-        // Buckets of <= 3 records (nearly all): branch-free, so the unrolled
-        // loop overlaps the shared-memory loads of all the thread's records; the
-        // bucket's slots are read clamped (a slot equal to e counts nothing).
-        // Equal windows with key bytes beyond them take the full comparison.
+        // rank of record e (window w) in its bucket [st, en) of <= 3 records:
+        // branch-free; the bucket's slots are read clamped (a slot equal to e
+        // counts nothing); equal windows with key bytes beyond them take the
+        // full comparison
+        auto rank3 = [&](uint32_t e, uint32_t w, uint32_t st, uint32_t en) -> uint32_t {
+            const uint32_t sz = en - st, last = en - 1;
+            // a bucket of one needs no neighbour: its lanes skip the loads
+            uint32_t e1 = e, e2 = e, e3 = e, w1 = w, w2 = w, w3 = w;
+            if (sz > 1) {
+                e1 = slot[st];
+                e2 = slot[min(st + 1, last)];
+                e3 = slot[min(st + 2, last)];
+                w1 = win[e1];
+                w2 = win[e2];
+                w3 = win[e3];
+            }
+            const bool u1 = e1 != e, u2 = e2 != e && e2 != e1, u3 = e3 != e && e3 != e2;
+            // (window, index) order as one 64-bit compare
+            const uint64_t k = (uint64_t(w) << 32) | e;
+            uint32_t rank = 0;
+            rank += u1 && ((uint64_t(w1) << 32) | e1) < k;
+            rank += u2 && ((uint64_t(w2) << 32) | e2) < k;
+            rank += u3 && ((uint64_t(w3) << 32) | e3) < k;
+            const bool tie = (u1 && w1 == w) || (u2 && w2 == w) || (u3 && w3 == w);
+            if (beyond && tie) rank = rank_slow(e, w, st, en);
+            return rank;
+        };
+        bool listed = false;
+        if constexpr (C::kList > 0) {
+            // ---- 5. record ids into bucket order (cnt: starts -> ends). A
+            // record alone in its bucket (~2/3 of them at ~0.44 records per
+            // bucket) is final at its slot: placed now, never ranked. The others
+            // go to a CTA-wide list (warp-aggregated appends), ranked densely
+            // after the barrier -- no pass over all records for the ranking.
+            uint16_t* clst = reinterpret_cast<uint16_t*>(s_tot);
 #pragma unroll
-        for (int j = 0; j < IPT; ++j) {
-            if (uint32_t(j) * T >= n) break;  // block-uniform
-            const uint32_t e = uint32_t(j) * T + threadIdx.x;
-            if (e < n) {
-                uint32_t w, bb, en, st;
-                if constexpr (KEEP) {
-                    w = wv[j];
-                    bb = bk[j] >> 16;
-                    const uint32_t i = bk[j] & 0xFFFFu;  // bucket bb - 1 sits 1 (9 across a pad) below
-                    en = cnt16[i];
-                    st = bb ? cnt16[i - ((bb & 63) ? 1u : 9u)] : 0u;
-                } else {
-                    w = win[e];
-                    bb = bucket_of(w);
-                    en = end_of(bb);
-                    st = bb ? end_of(bb - 1) : 0u;
-                }
-                const uint32_t sz = en - st;
-                if (sz <= 3) {
-                    const uint32_t last = en - 1;
-                    // a bucket of one (most records) needs no neighbour: its
-                    // lanes skip the loads (no shared-memory requests issued)
-                    uint32_t e1 = e, e2 = e, e3 = e, w1 = w, w2 = w, w3 = w;
-                    if (sz > 1) {
-                        e1 = slot[st];
-                        e2 = slot[min(st + 1, last)];
-                        e3 = slot[min(st + 2, last)];
-                        w1 = win[e1];
-                        w2 = win[e2];
-                        w3 = win[e3];
+            for (int j = 0; j < IPT; ++j) {
+                if (uint32_t(j) * T >= n) break;  // block-uniform
+                const uint32_t e = uint32_t(j) * T + threadIdx.x;
+                bool multi = false;
+                if (e < n) {
+                    const uint32_t i = bk[j] & 0xFFFFu, b = (bk[j] >> 16) & 0x1FFFu;
+                    const uint32_t old = atomicAdd(&cnt[i >> 1], 1u << ((i & 1) * 16));
+                    const uint32_t pos = (old >> ((i & 1) * 16)) & 0xFFFFu;
+                    if ((s_bm[b >> 5] >> (b & 31u)) & 1u) {
+                        place(e, pos);
+                    } else {
+                        slot[pos] = uint16_t(e);
+                        multi = true;
                     }
-                    const bool u1 = e1 != e, u2 = e2 != e && e2 != e1, u3 = e3 != e && e3 != e2;
-                    // (window, index) order as one 64-bit compare
-                    const uint64_t k = (uint64_t(w) << 32) | e;
-                    uint32_t rank = 0;
-                    rank += u1 && ((uint64_t(w1) << 32) | e1) < k;
-                    rank += u2 && ((uint64_t(w2) << 32) | e2) < k;
-                    rank += u3 && ((uint64_t(w3) << 32) | e3) < k;
-                    const bool tie = (u1 && w1 == w) || (u2 && w2 == w) || (u3 && w3 == w);
-                    if (beyond && tie) rank = rank_slow(e, w, st, en);
-                    place(e, st + rank);
-                } else {
-                    const uint32_t i = atomicAdd(&s_wq[warp], 1u);
-                    if (i < kWq) lst[i] = uint16_t(e);
-                    else place(e, st + rank_slow(e, w, st, en));  // list full: rank inline
+                }
+                const uint32_t mm = __ballot_sync(0xFFFFFFFFu, multi);
+                if (mm) {
+                    const uint32_t leader = uint32_t(__ffs(mm) - 1);
+                    uint32_t base = 0;
+                    if (uint32_t(lane) == leader) base = atomicAdd(&s_lcnt, uint32_t(__popc(mm)));
+                    base = __shfl_sync(0xFFFFFFFFu, base, leader);
+                    if (multi) {
+                        const uint32_t q = base + __popc(mm & lanemask_lt());
+                        if (q < uint32_t(C::kList)) clst[q] = uint16_t(e);
+                    }
                 }
             }
+            __syncthreads();
+            const uint32_t nl = s_lcnt;
+            if (nl <= uint32_t(C::kList)) {  // block-uniform
+                listed = true;
+                // ---- 6. order inside the multi-record buckets
+                for (uint32_t q = threadIdx.x; q < nl; q += T) {
+                    const uint32_t e = clst[q];
+                    const uint32_t w = win[e];
+                    const uint32_t bb = bucket_of(w);
+                    const uint32_t en = end_of(bb);
+                    const uint32_t st = bb ? end_of(bb - 1) : 0u;
+                    place(e, st + (en - st <= 3 ? rank3(e, w, st, en) : rank_slow(e, w, st, en)));
+                }
+            }
+            // (list overflow: the per-record pass below; every multi-record
+            // bucket's slots are filled, singletons place themselves again)
+        } else {
+            // ---- 5. record ids into bucket order (cnt: starts -> ends)
+#pragma unroll
+            for (int j = 0; j < IPT; ++j) {
+                if (uint32_t(j) * T >= n) break;  // block-uniform
+                const uint32_t e = uint32_t(j) * T + threadIdx.x;
+                if (e < n) {
+                    uint32_t i;  // the bucket's u16 counter index
+                    if constexpr (KEEP) i = bk[j] & 0xFFFFu;
+                    else i = i16_of(bucket_of(win[e]));
+                    const uint32_t old = atomicAdd(&cnt[i >> 1], 1u << ((i & 1) * 16));
+                    slot[(old >> ((i & 1) * 16)) & 0xFFFFu] = uint16_t(e);
+                }
+            }
+            __syncthreads();
         }
-        __syncwarp();
-        {
-            const uint32_t nl = min(s_wq[warp], kWq);
-            for (uint32_t i = lane; i < nl; i += 32) {
-                const uint32_t e = lst[i];
-                const uint32_t w = win[e];
-                const uint32_t bb = bucket_of(w);
-                const uint32_t en = end_of(bb);
-                const uint32_t st = bb ? end_of(bb - 1) : 0u;
-                place(e, st + rank_slow(e, w, st, en));
+        if (!listed) {
+            // ---- 6. order inside buckets (~1 record each), per record: size-1
+            // bucket -> its start; size 2-3 -> rank3; larger buckets (a few
+            // percent) go to a per-warp list (s_tot: 1024 u16 split over the
+            // warps) ranked densely by the same warp after its loop; s_wq (the
+            // lengths) are 0 from the start
+            constexpr uint32_t kWq = 1024 / W;
+            uint16_t* lst = reinterpret_cast<uint16_t*>(s_tot) + warp * kWq;
+#pragma unroll
+            for (int j = 0; j < IPT; ++j) {
+                if (uint32_t(j) * T >= n) break;  // block-uniform
+                const uint32_t e = uint32_t(j) * T + threadIdx.x;
+                if (e < n) {
+                    uint32_t w, bb, en, st;
+                    if constexpr (KEEP) {
+                        w = wv[j];
+                        bb = (bk[j] >> 16) & 0x1FFFu;
+                        const uint32_t i = bk[j] & 0xFFFFu;  // bucket bb - 1 sits 1 (9 across a pad) below
+                        en = cnt16[i];
+                        st = bb ? cnt16[i - ((bb & 63) ? 1u : 9u)] : 0u;
+                    } else {
+                        w = win[e];
+                        bb = bucket_of(w);
+                        en = end_of(bb);
+                        st = bb ? end_of(bb - 1) : 0u;
+                    }
+                    if (en - st <= 3) {
+                        place(e, st + rank3(e, w, st, en));
+                    } else {
+                        const uint32_t i = atomicAdd(&s_wq[warp], 1u);
+                        if (i < kWq) lst[i] = uint16_t(e);
+                        else place(e, st + rank_slow(e, w, st, en));  // list full: rank inline
+                    }
+                }
+            }
+            __syncwarp();
+            {
+                const uint32_t nl = min(s_wq[warp], kWq);
+                for (uint32_t i = lane; i < nl; i += 32) {
+                    const uint32_t e = lst[i];
+                    const uint32_t w = win[e];
+                    const uint32_t bb = bucket_of(w);
+                    const uint32_t en = end_of(bb);
+                    const uint32_t st = bb ? end_of(bb - 1) : 0u;
+                    place(e, st + rank_slow(e, w, st, en));
+                }
             }
         }
         __syncthreads();
