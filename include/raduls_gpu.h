@@ -119,6 +119,16 @@ typedef struct {
 int raduls_gpu_set_profiling(int on);
 int raduls_gpu_last_kernel_times(raduls_gpu_kernel_time* out, int capacity, int* count);
 
+/* raduls_gpu_sort on records that are already partitioned into n_segs
+ * contiguous, key-ordered segments (every key of segment i <= every key of
+ * segment i + 1; h_sizes sum to n): the segments are sorted independently,
+ * as the first MSD level's children, starting at key byte h_first_byte[i]
+ * (key bytes before it must be equal within segment i). The multi-GPU
+ * exchange delivers each rank's range in this form, so the receiver skips
+ * the level the exchange already did. Zero-size segments are allowed. */
+int raduls_gpu_sort_segments(void* d_data, void* d_tmp, uint64_t n_recs, uint32_t rec_size, uint32_t key_size,
+                             uint32_t n_segs, const uint64_t* h_sizes, const uint8_t* h_first_byte, void* stream);
+
 /* How the scatter ranks records inside a warp on the current device (decided
  * on first use): 0 = one shared-memory atomic per record, used only after a
  * device self-test (k_rank_selftest) confirmed that the conflicting lanes of

@@ -56,6 +56,7 @@ EXPORTED = [
     "raduls_gpu_set_host_cache",
     "raduls_gpu_set_pivots",
     "raduls_gpu_check_report",
+    "raduls_gpu_sort_segments",
 ]
 
 
@@ -140,6 +141,7 @@ def load(build_if_missing: bool = False):
         L.raduls_gpu_set_host_cache.argtypes = [C.c_int]
         L.raduls_gpu_set_pivots.argtypes = [_u32, _vp, _vp, _u32]
         L.raduls_gpu_check_report.argtypes = [_u64p]
+        L.raduls_gpu_sort_segments.argtypes = [_vp, _vp, _u64, _u32, _u32, _u32, _u64p, _vp, _vp]
         L.raduls_gpu_digit_andor.argtypes = [_vp, _u64, _u32, _u32, _u32, _vp, _u32, _vp, _u64p, _vp]
         L.raduls_gpu_partition_store_pieces.argtypes = [_vp, _u64, _u32, _u32, _u32, _vp, _u64p, _u64p,
                                                         _vp]

@@ -482,10 +482,10 @@ struct Caps {
 };
 
 template <int RS>
-Caps caps_for(uint64_t n) {
+Caps caps_for(uint64_t n, uint64_t extra_segs = 0) {
     const uint64_t cap_local = local_cap<RS>();
     Caps c;
-    c.seg = size_t(n / (cap_local + 1) + 2);
+    c.seg = size_t(n / (cap_local + 1) + 2 + extra_segs);
     c.tiles = size_t(n / ScatterCfg<RS>::kTile + c.seg + 2);
     c.groups = size_t(3 * (n / cap_local) + c.seg + 2);
     c.copies = size_t(n / kCopyTile + c.seg + 2);
@@ -493,8 +493,8 @@ Caps caps_for(uint64_t n) {
 }
 
 template <int RS>
-void ensure_caps(Workspace& ws, uint64_t n) {
-    const Caps c = caps_for<RS>(n);
+void ensure_caps(Workspace& ws, uint64_t n, uint64_t extra_segs = 0) {
+    const Caps c = caps_for<RS>(n, extra_segs);
     for (int b = 0; b < 2; ++b) {
         ws.segs[b].ensure(c.seg);
         ws.seg_tot[b].ensure(c.seg * kRadix);
@@ -720,17 +720,27 @@ size_t digit_arrays(Workspace& ws, uint64_t n, int halves) {
 // order, covering [0, n) — the host drop-in overlaps their device->host copy
 // with the rest of the sort. Without it (or when the level-0 split does not
 // qualify) the sort runs level by level over all segments.
+// seeds (optional, raduls_gpu_sort_segments): level 0 is the given list of
+// contiguous, key-ordered segments {size, first key byte that may vary}
+// instead of one segment over the whole array.
+struct SegSeed {
+    uint64_t size;
+    uint32_t p;
+};
+
 template <int RS>
 void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t ks,
-               cudaStream_t st, const std::function<void(uint64_t, uint64_t)>* on_final = nullptr) {
+               cudaStream_t st, const std::function<void(uint64_t, uint64_t)>* on_final = nullptr,
+               const std::vector<SegSeed>* seeds = nullptr) {
     constexpr int TILE = ScatterCfg<RS>::kTile;
     raduls_gpu_stats stats{};
     ws.last = stats;
     ws.prof.reset();
     ws.part.pending = false;
     if (n < 2) return;  // msd_sorter.hpp:51
+    if (seeds && seeds->size() == 1 && (*seeds)[0].p == 0) seeds = nullptr;  // the plain sort
     set_attrs<RS>(ws);
-    ensure_caps<RS>(ws, n);
+    ensure_caps<RS>(ws, n, seeds ? seeds->size() : 0);
     LevelCounters* dctr = ws.ctr.p;
     RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, sizeof(unsigned int), st));
     RG_CHK_RANGES(st, {{data, size_t(n) * RS}, {tmp, size_t(n) * RS}});
@@ -747,7 +757,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
     }
 #endif
 
-    if (n <= uint64_t(local_cap<RS>())) {  // one group sorts everything, in place
+    if (n <= uint64_t(local_cap<RS>()) && !seeds) {  // one group sorts everything, in place
         Group g{0, uint32_t(n), 0, 0, 0};
         RG_CHECK(cudaMemcpyAsync(ws.groups.p, &g, sizeof g, cudaMemcpyHostToDevice, st));
         RG_CHECK(cudaMemsetAsync(dctr, 0, sizeof(LevelCounters), st));
@@ -799,9 +809,43 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         note_launch();
         RG_LAUNCH_CHECK();
     };
-    level0_counts();
     uint32_t nseg = 1, ntiles = nt0;
-    const Caps caps = caps_for<RS>(n);
+    if (!seeds) {
+        level0_counts();
+    } else {
+        // level 0 = the caller's segments (bsegs -> segs[0] and the tile map,
+        // as a progressive batch is rebased), AND/OR rows reset, no sampled
+        // guess and no redo flag
+        std::vector<Seg> hs(seeds->size());
+        uint64_t at = 0;
+        uint32_t tb = 0;
+        for (size_t i = 0; i < seeds->size(); ++i) {
+            const uint64_t sz = (*seeds)[i].size;
+            hs[i] = Seg{at, sz, std::min((*seeds)[i].p, ks), 0, tb, 0};
+            at += sz;
+            tb += uint32_t((sz + TILE - 1) / TILE);
+        }
+        if (at != n) throw CudaError{RADULS_GPU_EINVAL};
+        nseg = uint32_t(hs.size());
+        ntiles = tb;
+        ws.bsegs.ensure(nseg);
+        RG_CHECK(cudaMemcpyAsync(ws.bsegs.p, hs.data(), nseg * sizeof(Seg), cudaMemcpyHostToDevice, st));
+        RG_CHECK(cudaMemsetAsync(d_flag, 0, sizeof(unsigned long long), st));
+        RG_CHECK(cudaMemsetAsync(ws.tile_seg[0].p, 0, size_t(ntiles) * sizeof(uint32_t), st));
+        k_rebase_segs<<<nseg, 256, 0, st>>>(ws.bsegs.p, 0, ws.segs[0].p, ws.tile_seg[0].p, TILE);
+        note_launch();
+        RG_LAUNCH_CHECK();
+        k_init_andor<<<(nseg * 8 + 255) / 256, 256, 0, st>>>(ws.seg_andor[0].p, nseg);
+        note_launch();
+        RG_LAUNCH_CHECK();
+        RG_CHECK(cudaMemsetAsync(dctr, 0, sizeof(LevelCounters), st));
+        if (ntiles) {
+            if (ks <= 8) level_counts<RS, false, true>(ws, data, tmp, 0, ntiles, dctr, st);
+            else level_counts<RS>(ws, data, tmp, 0, ntiles, dctr, st);
+        }
+        RG_CHECK(cudaStreamSynchronize(st));  // hs (host) is read by the copy above
+    }
+    const Caps caps = caps_for<RS>(n, seeds ? seeds->size() : 0);
     // Digit arrays: the scatter writes the next key byte of every record whose
     // child is split again, so the next level's histogram reads 1 byte, not
     // rs, and its scatter takes its digits from there too. Best effort:
@@ -901,7 +945,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         const char* e = std::getenv("RADULS_GPU_PROGRESSIVE_BYTES");
         return e ? std::strtoull(e, nullptr, 10) : (uint64_t(256) << 20);
     }();
-    if (on_final && n * RS >= prog_min) {
+    if (on_final && n * RS >= prog_min && !seeds) {
         // Progressive: level 0 over the whole array, then its children (one
         // parent: in digit order = key order, tiles in the same order) in
         // batches of contiguous key ranges, each sorted to the end before the
@@ -1471,6 +1515,43 @@ int raduls_gpu_lsd_sort_host(uint8_t* data, uint8_t* /*tmp*/, uint64_t n, uint32
     });
 }
 
+
+int raduls_gpu_sort_segments(void* d_data, void* d_tmp, uint64_t n, uint32_t rs, uint32_t ks, uint32_t n_segs,
+                             const uint64_t* h_sizes, const uint8_t* h_first_byte, void* stream) {
+    if (!layout_ok(rs, ks) || mul_overflows(n, rs) || n > kMaxRecords || (n_segs && (!h_sizes || !h_first_byte)))
+        return RADULS_GPU_EINVAL;
+    if (n >= 2 && (!d_data || !aligned_ok(d_data, rs) || (d_tmp && !aligned_ok(d_tmp, rs)))) return RADULS_GPU_EINVAL;
+    std::vector<SegSeed> seeds;
+    uint64_t total = 0;
+    for (uint32_t i = 0; i < n_segs; ++i) {
+        total += h_sizes[i];
+        if (h_sizes[i]) seeds.push_back(SegSeed{h_sizes[i], h_first_byte[i]});
+    }
+    if (total != n) return RADULS_GPU_EINVAL;
+    if (n < 2) return RADULS_GPU_OK;
+    return guarded([&] {
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lk(ws.mu);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        uint8_t* tmp = static_cast<uint8_t*>(d_tmp);
+        bool own = false;
+        if (!tmp) {
+            RG_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&tmp), n * rs, st));
+            own = true;
+        }
+        try {
+            dispatch_rs(rs, [&](auto R) {
+                sort_impl<decltype(R)::value>(ws, static_cast<uint8_t*>(d_data), tmp, n, ks, st, nullptr,
+                                              seeds.size() > 1 ? &seeds : nullptr);
+            });
+        } catch (...) {
+            if (own) cudaFreeAsync(tmp, st);
+            throw;
+        }
+        if (own) RG_CHECK(cudaFreeAsync(tmp, st));
+        RG_CHECK(cudaStreamSynchronize(st));
+    });
+}
 
 int raduls_gpu_split(const void* d_src, void* d_dst, uint64_t n, uint32_t rs,
                      uint32_t key_byte_offset, uint64_t* h_counts, void* stream) {

@@ -102,6 +102,7 @@ class DigitPlan:
     hot: np.ndarray            # [n_digits] bool
     single: np.ndarray = None  # [n_digits] bool
     pivots: list = None        # [(digit d of the "below" part, key bytes)]
+    first_byte: np.ndarray = None  # [n_digits] u8: key bytes before it are equal within the digit
 
     def __post_init__(self):
         if self.single is None:
@@ -119,11 +120,16 @@ def hot_buckets(weights: np.ndarray, world: int) -> np.ndarray:
 
 
 def make_digits(weights: np.ndarray, world: int, p0: int = 0, split_hot: bool = True,
-                pivots: dict | None = None) -> DigitPlan:
+                pivots: dict | None = None, ks: int | None = None, align: bool = False) -> DigitPlan:
     """Digits from global bucket weights (exact counts or sample estimates):
     each rank's contiguous bucket range (balanced_bucket_map) is one digit,
     except that every hot bucket is a digit of its own — three digits
-    (below / equal / above) when `pivots` names a pivot key for it."""
+    (below / equal / above) when `pivots` names a pivot key for it.
+
+    align: digits also end where key byte p0 changes (every 256 buckets), as
+    far as 256 digits allow (the lightest byte-p0 boundaries are dropped
+    first), so that within most digits byte p0 is constant and the receiver
+    can sort each digit's run from byte p0 + 1 on (first_byte; needs ks)."""
     w = np.asarray(weights, dtype=np.float64)
     rank = balanced_bucket_map(w, world).astype(np.int64)
     hot = hot_buckets(w, world) if split_hot else np.zeros(NBUCKETS, dtype=bool)
@@ -134,11 +140,19 @@ def make_digits(weights: np.ndarray, world: int, p0: int = 0, split_hot: bool = 
                 piv[b] = True
     change = np.zeros(NBUCKETS, dtype=bool)
     change[1:] = (rank[1:] != rank[:-1]) | hot[1:] | hot[:-1]
+    if align:
+        budget = 256 - (1 + int(change.sum()) + 2 * int(piv.sum()))
+        cand = [b for b in range(256, NBUCKETS, 256) if not change[b]]
+        if budget < len(cand):  # keep the boundaries between the heaviest byte-p0 blocks
+            blk = w.reshape(256, 256).sum(axis=1)
+            cand.sort(key=lambda b: -(blk[(b >> 8) - 1] + blk[b >> 8]))
+            cand = cand[:max(budget, 0)]
+        change[cand] = True
     extra = 2 * (np.cumsum(piv) - piv)  # two more digits per earlier pivot bucket
     digit = (np.cumsum(change) + extra).astype(np.uint32)
     n_digits = int(digit[-1]) + 1 + (2 if piv[-1] else 0)
     if n_digits > 256:  # too many ranks for separate hot digits: whole buckets only
-        return make_digits(weights, world, p0, split_hot=False)
+        return make_digits(weights, world, p0, split_hot=False, ks=ks, align=align)
     dhot = np.zeros(n_digits, dtype=bool)
     single = np.zeros(n_digits, dtype=bool)
     plist = []
@@ -149,7 +163,24 @@ def make_digits(weights: np.ndarray, world: int, p0: int = 0, split_hot: bool = 
             plist.append((d, bytes(pivots[int(b)])))
         else:
             dhot[d] = True
-    return DigitPlan(p0, digit, n_digits, dhot, single, plist)
+    plan = DigitPlan(p0, digit, n_digits, dhot, single, plist)
+    if ks is not None:
+        # first key byte that may vary inside each digit's records
+        fb = np.full(n_digits, p0, dtype=np.int64)
+        b_lo = np.full(n_digits, NBUCKETS, dtype=np.int64)
+        b_hi = np.full(n_digits, -1, dtype=np.int64)
+        np.minimum.at(b_lo, digit.astype(np.int64), np.arange(NBUCKETS))
+        np.maximum.at(b_hi, digit.astype(np.int64), np.arange(NBUCKETS))
+        for d in range(n_digits):
+            if b_hi[d] >= 0 and b_lo[d] == b_hi[d]:
+                fb[d] = p0 + 2  # one 16-bit bucket
+            elif b_hi[d] >= 0 and (b_lo[d] >> 8) == (b_hi[d] >> 8):
+                fb[d] = p0 + 1  # one value of byte p0
+        for d, _ in plist:
+            fb[d] = fb[d + 2] = p0 + 2
+            fb[d + 1] = ks  # the pivot key itself: one key
+        plan.first_byte = np.minimum(fb, ks).astype(np.uint8)
+    return plan
 
 
 def prefix16_np(keys: np.ndarray, p0: int, ks: int) -> np.ndarray:
@@ -400,6 +431,15 @@ class DeviceOps:
         counts, _ = self.partition_plan(data, n, layout, p0, bucket_digit, n_digits)
         return counts
 
+    def sort_segments(self, data, n: int, layout: RecordLayout, sizes, first_bytes, tmp=None) -> None:
+        """raduls_gpu_sort_segments: n records already in key-ordered segments."""
+        sz = np.ascontiguousarray(sizes, dtype=np.uint64)
+        fb = np.ascontiguousarray(first_bytes, dtype=np.uint8)
+        _raise(self.L.raduls_gpu_sort_segments(data.data_ptr(), tmp.data_ptr() if tmp is not None else None,
+                                               n, layout.record_size, layout.key_size, len(sz),
+                                               sz.ctypes.data_as(_lib._u64p), fb.ctypes.data, self.stream()),
+               "raduls_gpu_sort_segments")
+
     def sort(self, data, n: int, layout: RecordLayout, tmp=None) -> None:
         _raise(self.L.raduls_gpu_sort(data.data_ptr(), tmp.data_ptr() if tmp is not None else None,
                                       n, layout.record_size, layout.key_size, self.stream()),
@@ -472,7 +512,7 @@ def _digits_with_pivots(ops, data, n: int, layout: RecordLayout, weights: np.nda
         keys = np.concatenate([allk[r, 8:].reshape(SAMPLE_KEYS, 32)[:int(allk[r, :8].view(np.int64)[0])]
                                for r in range(allk.shape[0])])
         pivots = choose_pivots(keys, p0, ks, hot, weights)
-    digits = make_digits(weights, world, p0, pivots=pivots)
+    digits = make_digits(weights, world, p0, pivots=pivots, ks=ks, align=True)
     if hasattr(ops, "set_pivots"):
         ops.set_pivots(digits, ks)
     return digits
@@ -633,18 +673,32 @@ def release_peer_windows() -> None:
     _windows.clear()
 
 
-def _piece_destinations(plan: ExchangePlan, rank: int, rs: int, bases) -> tuple:
+def _receive_layout(plan: ExchangePlan, world: int):
+    """Digit-major receive windows: receiver k holds its digits in digit
+    order, each digit's records source by source (the stable order). Returns
+    (offsets, segments): offsets[s, d, k] = record offset of source s's piece
+    of digit d in receiver k's window; segments[k] = [(digit, records)] in
+    window order."""
+    G, D = len(plan.pieces), plan.digits.n_digits
+    C = np.zeros((G, D, world), dtype=np.int64)
+    for s_, pcs in enumerate(plan.pieces):
+        for d, k, c in pcs:
+            C[s_, d, k] += c
+    T = C.sum(axis=0)                                   # [D, world]
+    base = np.cumsum(T, axis=0) - T                     # digit-major, per receiver
+    offsets = base[None, :, :] + (np.cumsum(C, axis=0) - C)
+    segments = [[(int(d), int(T[d, k])) for d in np.nonzero(T[:, k])[0]] for k in range(world)]
+    return offsets, segments
+
+
+def _piece_destinations(plan: ExchangePlan, rank: int, rs: int, bases, offsets) -> tuple:
     """This source's pieces with their byte addresses in the receivers'
-    windows: receiver k holds its sources' records source-major, each
-    source's pieces in digit order."""
-    S = plan.matrix
-    run = {k: int(S[:rank, k].sum()) for k in range(S.shape[1])}
+    windows (digit-major, _receive_layout)."""
     dg, ct, ds = [], [], []
     for d, k, c in plan.pieces[rank]:
         dg.append(d)
         ct.append(c)
-        ds.append(bases[k] + run[k] * rs)
-        run[k] += c
+        ds.append(bases[k] + int(offsets[rank, d, k]) * rs)
     return (np.array(dg, dtype=np.uint32), np.array(ct, dtype=np.uint64), np.array(ds, dtype=np.uint64))
 
 
@@ -728,7 +782,8 @@ def sort_distributed(data, n: int, layout: RecordLayout, ops=None, group=None,
             "hot_split_digits": int(sum(1 for d in range(plan.digits.n_digits)
                                         if len({k for s in plan.pieces for (dd, k, _) in s if dd == d}) > 1))}
     if win is not None:
-        dg, ct, ds = _piece_destinations(plan, rank, rs, win.ptrs)
+        offsets, segments = _receive_layout(plan, world)
+        dg, ct, ds = _piece_destinations(plan, rank, rs, win.ptrs, offsets)
         if cuda:
             torch.cuda.synchronize(data.device)
         dist.barrier(group=group)  # every window free (previous results consumed)
@@ -740,7 +795,15 @@ def sort_distributed(data, n: int, layout: RecordLayout, ops=None, group=None,
         t2 = time.perf_counter()
         recv = torch.as_tensor(_CudaBytes(win.own, max(n_out, 1) * rs), device=data.device)
         tmp = ops.empty(max(n_out, 1) * rs)
-        ops.sort(recv, n_out, layout, tmp)
+        # the window holds this rank's digits in key order, each one key range:
+        # the exchange was the first MSD level, the sort continues from there
+        mine = segments[rank]
+        fb = plan.digits.first_byte
+        info["segments"] = len(mine)
+        if fb is not None and hasattr(ops, "sort_segments") and len(mine) > 1:
+            ops.sort_segments(recv, n_out, layout, [c for _, c in mine], [int(fb[d]) for d, _ in mine], tmp)
+        else:
+            ops.sort(recv, n_out, layout, tmp)
     else:
         # local stable partition by digit (pieces of a digit stay in rank order)
         e0 = event()

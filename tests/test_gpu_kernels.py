@@ -209,3 +209,39 @@ def test_sampled_andor_and_prefix_histogram(rg, torch_cuda, rs, ks):
     assert L.raduls_gpu_sample_prefix_histogram(d.data_ptr(), n, rs, ks, pb, samples, hist.data_ptr(), None) == 0
     pref = (recs[:, pb].astype(np.int64) << 8) | recs[:, pb + 1].astype(np.int64)
     assert np.array_equal(hist.cpu().numpy(), np.bincount(pref, minlength=65536))
+
+
+@pytest.mark.parametrize("rs,ks", [(16, 8), (8, 8), (32, 24)])
+def test_sort_segments_matches_oracle(rg, torch_cuda, rs, ks):
+    """raduls_gpu_sort_segments (the multi-GPU receiver's sort): records
+    already grouped into key-ordered segments (here stably by key byte 0),
+    each sorted from key byte 1 on; empty segments, and the 0x42 segment cut
+    into below / equal-key / above parts (the equal part from key byte ks)."""
+    from paper_1612_02557_b200.distributed import DeviceOps
+    n = 400_000
+    a = make_input(n, rs, ks, 31 + rs)
+    r = a.reshape(n, rs)
+    hot = bytes([0x42] * ks)
+    r[: n // 10, :ks] = 0x42  # 10%: one key
+    parts, sizes, fb = [], [], []
+    for v in range(256):
+        seg = r[r[:, 0] == v]  # stable: input order inside
+        if v == 0x42:
+            keys = [bytes(x[:ks]) for x in seg]
+            for sel, f in (([k < hot for k in keys], 1), ([k == hot for k in keys], ks),
+                           ([k > hot for k in keys], 1)):
+                parts.append(seg[np.array(sel, dtype=bool)])
+                sizes.append(int(np.sum(sel)))
+                fb.append(f)
+        else:
+            parts.append(seg)
+            sizes.append(len(seg))
+            fb.append(1)
+    part = np.concatenate(parts).reshape(-1)
+    sizes[5:5] = [0, 0]  # empty segments are allowed anywhere
+    fb[5:5] = [1, 2]
+    assert sum(sizes) == n
+    d = to_dev(torch_cuda, part)
+    DeviceOps().sort_segments(d, n, rg.RecordLayout(rs, ks), sizes, fb)
+    torch_cuda.cuda.synchronize()
+    assert np.array_equal(from_dev(d), oracle.stable_sort(part, rs, ks))
