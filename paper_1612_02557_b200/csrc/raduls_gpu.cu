@@ -17,6 +17,7 @@
 //
 // One device->host read of the level counters per level sizes the next
 // launches. See DESIGN.md for the data layout and the per-kernel rooflines.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -184,6 +185,120 @@ struct DevBuf {
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
+    }
+};
+
+// The host drop-ins' two n*rs device buffers. Mapped through the driver's
+// virtual-memory API (cuMemCreate / cuMemMap, entry points looked up at run
+// time) when available: unmapping one does not wait for the device, so the
+// scratch buffer is released while the result's device->host copies are
+// still running, and the whole release costs ~20 ms instead of cudaFree's
+// device-wide wait plus 20-50 ms (profiles/r2_probe_vmm.txt). Else cudaMalloc.
+struct VmmApi {
+    decltype(&cuMemCreate) create = nullptr;
+    decltype(&cuMemAddressReserve) reserve = nullptr;
+    decltype(&cuMemMap) map = nullptr;
+    decltype(&cuMemSetAccess) access = nullptr;
+    decltype(&cuMemUnmap) unmap = nullptr;
+    decltype(&cuMemRelease) release = nullptr;
+    decltype(&cuMemAddressFree) addr_free = nullptr;
+    decltype(&cuMemGetAllocationGranularity) gran = nullptr;
+    bool ok = false;
+    static const VmmApi& get() {
+        static const VmmApi api = [] {
+            VmmApi a;
+            if (std::getenv("RADULS_GPU_NO_VMM")) return a;
+            auto sym = [](const char* name) -> void* {
+                void* p = nullptr;
+                cudaDriverEntryPointQueryResult q{};
+                if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+                    q != cudaDriverEntryPointSuccess) {
+                    cudaGetLastError();
+                    return nullptr;
+                }
+                return p;
+            };
+            a.create = reinterpret_cast<decltype(a.create)>(sym("cuMemCreate"));
+            a.reserve = reinterpret_cast<decltype(a.reserve)>(sym("cuMemAddressReserve"));
+            a.map = reinterpret_cast<decltype(a.map)>(sym("cuMemMap"));
+            a.access = reinterpret_cast<decltype(a.access)>(sym("cuMemSetAccess"));
+            a.unmap = reinterpret_cast<decltype(a.unmap)>(sym("cuMemUnmap"));
+            a.release = reinterpret_cast<decltype(a.release)>(sym("cuMemRelease"));
+            a.addr_free = reinterpret_cast<decltype(a.addr_free)>(sym("cuMemAddressFree"));
+            a.gran = reinterpret_cast<decltype(a.gran)>(sym("cuMemGetAllocationGranularity"));
+            a.ok = a.create && a.reserve && a.map && a.access && a.unmap && a.release && a.addr_free && a.gran;
+            return a;
+        }();
+        return api;
+    }
+};
+
+struct HostDevBuf {
+    uint8_t* p = nullptr;
+    size_t cap = 0;  // bytes
+    size_t mapped = 0;
+    CUmemGenericAllocationHandle h = 0;
+    bool vmm = false;
+    void ensure(size_t n) {
+        if (n <= cap) return;
+        release();
+        const VmmApi& v = VmmApi::get();
+        if (v.ok) {
+            int dev = 0;
+            RG_CHECK(cudaGetDevice(&dev));
+            CUmemAllocationProp prop{};
+            prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+            prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+            prop.location.id = dev;
+            size_t g = 0;
+            if (v.gran(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) == CUDA_SUCCESS && g) {
+                const size_t sz = (std::max<size_t>(n, 1) + g - 1) / g * g;
+                CUdeviceptr va = 0;
+                CUmemGenericAllocationHandle hh = 0;
+                if (v.reserve(&va, sz, 0, 0, 0) == CUDA_SUCCESS) {
+                    if (v.create(&hh, sz, &prop, 0) == CUDA_SUCCESS) {
+                        CUmemAccessDesc ad{};
+                        ad.location = prop.location;
+                        ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+                        if (v.map(va, sz, 0, hh, 0) == CUDA_SUCCESS) {
+                            if (v.access(va, sz, &ad, 1) == CUDA_SUCCESS) {
+                                p = reinterpret_cast<uint8_t*>(va);
+                                cap = n;
+                                mapped = sz;
+                                h = hh;
+                                vmm = true;
+                                return;
+                            }
+                            v.unmap(va, sz);
+                        }
+                        v.release(hh);
+                    }
+                    v.addr_free(va, sz);
+                }
+                // out of device memory (or no VMM for this device): plain cudaMalloc below
+            }
+        }
+        RG_CHECK(cudaMalloc(&p, std::max<size_t>(n, 1)));
+        cap = n;
+        vmm = false;
+    }
+    // The caller guarantees no queued work still uses the buffer (VMM:
+    // unmapping does not wait; cudaFree waits for the whole device).
+    void release() {
+        if (!p) return;
+        if (vmm) {
+            const VmmApi& v = VmmApi::get();
+            const CUdeviceptr va = reinterpret_cast<CUdeviceptr>(p);
+            v.unmap(va, mapped);
+            v.release(h);
+            v.addr_free(va, mapped);
+        } else {
+            cudaFree(p);
+        }
+        p = nullptr;
+        cap = mapped = 0;
+        h = 0;
+        vmm = false;
     }
 };
 
@@ -397,7 +512,8 @@ struct Workspace {
     DevBuf<Group> groups, spill;
     DevBuf<unsigned int> n_spill;
     DevBuf<CopyRange> copies;
-    DevBuf<uint8_t> host_data, host_tmp, map8;
+    HostDevBuf host_data, host_tmp;
+    DevBuf<uint8_t> map8;
     // partition pivots (raduls_gpu_set_pivots): the map buffer's pivot region
     // (kMapBytes - 65536 bytes) as uploaded with every bucket map
     std::array<uint8_t, kMapBytes - kMapPivotSlot> pivots{};
@@ -1342,13 +1458,13 @@ int raduls_gpu_sort_host(uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t rs, u
         std::lock_guard<std::mutex> lk(ws.mu);
         HostBufs hb(ws);
         ws.host_data.ensure(bytes);
-        ws.host_tmp.ensure(bytes);
         cudaStream_t st = nullptr;
         HostStager& hs = ws.host_stager();
         const bool timing = std::getenv("RADULS_GPU_HOST_TIMING") != nullptr;
         auto now = [] { return std::chrono::steady_clock::now(); };
         const auto t0 = now();
         hs.h2d(ws.host_data.p, data, bytes, st);
+        ws.host_tmp.ensure(bytes);  // (pinned input: mapped while the copy runs)
         if (timing) RG_CHECK(cudaStreamSynchronize(st));
         const auto t1 = now();
         // pinned buffers: each key range is copied back as soon as it is final
@@ -1365,6 +1481,9 @@ int raduls_gpu_sort_host(uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t rs, u
         dispatch_rs(rs, [&](auto R) {
             sort_impl<decltype(R)::value>(ws, ws.host_data.p, ws.host_tmp.p, n, ks, st, pinned ? &fin : nullptr);
         });
+        // every kernel has finished (sort_impl ends synchronised); only the
+        // result's copies may still run: the scratch goes now, under them
+        if (!g_host_cache.load()) ws.host_tmp.release();
         const auto t2 = now();
         if (covered) {  // the sort handed over its ranges (all of them)
             RG_CHECK(cudaStreamSynchronize(hs.copy));
