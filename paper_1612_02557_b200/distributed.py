@@ -166,16 +166,14 @@ def make_digits(weights: np.ndarray, world: int, p0: int = 0, split_hot: bool = 
     plan = DigitPlan(p0, digit, n_digits, dhot, single, plist)
     if ks is not None:
         # first key byte that may vary inside each digit's records
+        # digit is non-decreasing in the bucket: each digit's bucket range
+        dr = np.arange(n_digits)
+        b_lo = np.searchsorted(digit, dr, side="left").astype(np.int64)
+        b_hi = np.searchsorted(digit, dr, side="right").astype(np.int64) - 1
+        has = b_hi >= b_lo
         fb = np.full(n_digits, p0, dtype=np.int64)
-        b_lo = np.full(n_digits, NBUCKETS, dtype=np.int64)
-        b_hi = np.full(n_digits, -1, dtype=np.int64)
-        np.minimum.at(b_lo, digit.astype(np.int64), np.arange(NBUCKETS))
-        np.maximum.at(b_hi, digit.astype(np.int64), np.arange(NBUCKETS))
-        for d in range(n_digits):
-            if b_hi[d] >= 0 and b_lo[d] == b_hi[d]:
-                fb[d] = p0 + 2  # one 16-bit bucket
-            elif b_hi[d] >= 0 and (b_lo[d] >> 8) == (b_hi[d] >> 8):
-                fb[d] = p0 + 1  # one value of byte p0
+        fb[has & ((b_lo >> 8) == (b_hi >> 8))] = p0 + 1  # one value of byte p0
+        fb[has & (b_lo == b_hi)] = p0 + 2                # one 16-bit bucket
         for d, _ in plist:
             fb[d] = fb[d + 2] = p0 + 2
             fb[d + 1] = ks  # the pivot key itself: one key
@@ -249,32 +247,36 @@ def assign_pieces(M: np.ndarray, splittable: np.ndarray, world: int):
         rank = np.minimum((2 * P + C) * world // (2 * N), world - 1)
     plain = ~np.asarray(splittable, dtype=bool)
     S = np.zeros((G, world), dtype=np.int64)
-    pieces = [[] for _ in range(G)]
-    bound = [(k * N + world - 1) // world for k in range(world + 1)]  # first position of rank k
-    for d in range(D):
-        if C[d] == 0:
-            continue
-        if plain[d]:
-            for s in range(G):
-                if M[s, d]:
-                    pieces[s].append((d, int(rank[d]), int(M[s, d])))
-                    S[s, rank[d]] += M[s, d]
-            continue
-        prev = [int(rank[q]) for q in range(d - 1, -1, -1) if plain[q] and C[q]]
-        nxt = [int(rank[q]) for q in range(d + 1, D) if plain[q] and C[q]]
-        r_lo = prev[0] if prev else 0
-        r_hi = nxt[0] if nxt else world - 1
-        start = int(P[d])
-        for s in range(G):
-            a = start
-            b = a + int(M[s, d])
-            start = b
-            for k in range(r_lo, r_hi + 1):
-                lo = a if k == r_lo else max(a, bound[k])
-                hi = b if k == r_hi else min(b, bound[k + 1])
-                if hi > lo:
-                    pieces[s].append((d, k, hi - lo))
-                    S[s, k] += hi - lo
+    # plain digits: whole, to rank[d] (vectorised)
+    Mp = np.where(plain[None, :], M, 0)
+    for r in range(world):
+        S[:, r] = Mp[:, rank == r].sum(axis=1)
+    per = {s_: [] for s_ in range(G)}  # s -> [(d, k, c)]
+    for s_ in range(G):
+        ds = np.nonzero(Mp[s_] > 0)[0]
+        per[s_] = list(zip(ds.tolist(), rank[ds].tolist(), Mp[s_, ds].tolist()))
+    split_ds = [d for d in np.nonzero(~plain & (C > 0))[0]]
+    if split_ds:
+        bound = [(k * N + world - 1) // world for k in range(world + 1)]  # first position of rank k
+        live = np.nonzero(plain & (C > 0))[0]
+        for d in split_ds:
+            i = np.searchsorted(live, d)
+            r_lo = int(rank[live[i - 1]]) if i > 0 else 0
+            r_hi = int(rank[live[i]]) if i < len(live) else world - 1
+            start = int(P[d])
+            for s_ in range(G):
+                a = start
+                b = a + int(M[s_, d])
+                start = b
+                for k in range(r_lo, r_hi + 1):
+                    lo = a if k == r_lo else max(a, bound[k])
+                    hi = b if k == r_hi else min(b, bound[k + 1])
+                    if hi > lo:
+                        per[s_].append((int(d), k, hi - lo))
+                        S[s_, k] += hi - lo
+        for s_ in range(G):
+            per[s_].sort(key=lambda t: (t[0], t[1]))
+    pieces = [per[s_] for s_ in range(G)]
     return pieces, S
 
 
@@ -702,6 +704,15 @@ def _piece_destinations(plan: ExchangePlan, rank: int, rs: int, bases, offsets) 
     return (np.array(dg, dtype=np.uint32), np.array(ct, dtype=np.uint64), np.array(ds, dtype=np.uint64))
 
 
+def _split_digit_count(plan: ExchangePlan) -> int:
+    """Digits whose records go to more than one rank (a hot key spread by count)."""
+    ranks = {}
+    for pcs in plan.pieces:
+        for d, k, _ in pcs:
+            ranks.setdefault(d, set()).add(k)
+    return sum(1 for v in ranks.values() if len(v) > 1)
+
+
 def _all_to_all(recv, send, out_splits, in_splits, group):
     """dist.all_to_all_single; gloo cannot move CUDA tensors, so there the
     exchange is staged through host memory (tests on one shared device)."""
@@ -779,8 +790,7 @@ def sort_distributed(data, n: int, layout: RecordLayout, ops=None, group=None,
     t1 = time.perf_counter()
     info = {"exchange": exchange, "plan_s": t1 - t0, "recv_records": n_out,
             "sent_bytes": int((plan.send_counts(rank).sum() - plan.send_counts(rank)[rank]) * rs),
-            "hot_split_digits": int(sum(1 for d in range(plan.digits.n_digits)
-                                        if len({k for s in plan.pieces for (dd, k, _) in s if dd == d}) > 1))}
+            "hot_split_digits": _split_digit_count(plan)}
     if win is not None:
         offsets, segments = _receive_layout(plan, world)
         dg, ct, ds = _piece_destinations(plan, rank, rs, win.ptrs, offsets)
