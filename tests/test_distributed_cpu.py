@@ -356,3 +356,49 @@ def test_choose_pivots_picks_most_common_sampled_key():
     assert hot[0x0707] and hot.sum() == 1
     piv = D.choose_pivots(keys, 0, ks, hot, w)
     assert piv == {0x0707: hotkey.tobytes()}
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_aligned_digits_and_digit_major_layout(world):
+    """make_digits(align=True): digits end where key byte p0 changes as far as
+    256 digits allow, each digit's first_byte is right (bytes before it are
+    one value over the digit's buckets), and _receive_layout tiles every
+    receiver's window exactly, digit-major, sources in order inside a digit."""
+    rng = np.random.default_rng(world)
+    w = rng.random(D.NBUCKETS) * 1000
+    w[0x1234] = 5e6  # a hot bucket with a pivot
+    plan = D.make_digits(w, world, 0, pivots={0x1234: bytes([0x12, 0x34, 1, 2, 3, 4, 5, 6])}, ks=8,
+                         align=True)
+    assert plan.n_digits <= 256
+    d = plan.bucket_digit.astype(np.int64)
+    assert np.all(np.diff(d) >= 0)
+    for dd in range(plan.n_digits):
+        bs = np.nonzero(d == dd)[0]
+        if len(bs) == 0:
+            continue
+        fb = int(plan.first_byte[dd])
+        if fb >= 1:
+            assert len(set(bs >> 8)) == 1, dd  # byte p0 constant
+        if fb >= 2 and fb < 8:
+            assert len(bs) == 1, dd            # one 16-bit bucket
+    pd = plan.pivots[0][0]
+    assert plan.first_byte[pd + 1] == 8 and plan.single[pd + 1]
+    # most digits are aligned
+    assert (plan.first_byte >= 1).sum() >= 200
+    M = np.stack([np.bincount(plan.bucket_digit, weights=w / world, minlength=plan.n_digits)
+                  for _ in range(world)]).astype(np.int64)
+    pieces, S = D.assign_pieces(M, plan.single, world)
+    ep = D.ExchangePlan(plan, M, pieces, S)
+    off, seg = D._receive_layout(ep, world)
+    for k in range(world):
+        assert sum(c for _, c in seg[k]) == S[:, k].sum()
+        assert [dd for dd, _ in seg[k]] == sorted(dd for dd, _ in seg[k])
+        iv = sorted((int(off[s, dd, kk]), s, dd, c) for s in range(world) for (dd, kk, c) in pieces[s]
+                    if kk == k)
+        pos = 0
+        last = (-1, -1)
+        for a, s, dd, c in iv:
+            assert a == pos
+            assert (dd, s) > last  # digit-major, then source order
+            last = (dd, s)
+            pos += c
