@@ -292,55 +292,6 @@ def sort_roofline(ab: dict, total_ms: float, steps: int, peak: float, n: int, rs
             "passes_per_record": round(alg / steps / (2 * rs * n), 3)}
 
 
-def measure_config(rg, torch, dev, cfg_name: str, steps: int, warmup: int, peak: float,
-                   peak_src: str) -> dict:
-    """One single-GPU config: device-resident sorts timed by CUDA events on the
-    sort's stream, per-kernel times, digest + order verified (untimed)."""
-    n, rs, ks, dist_kind, seed, desc = CONFIGS[cfg_name]
-    lay = rg.RecordLayout(rs, ks)
-    data = torch.empty(n * rs, dtype=torch.uint8, device=dev)
-    tmp = torch.empty_like(data)
-    stream = torch.cuda.current_stream(dev)
-    rg.generate(n, lay, dist=dist_kind, seed=seed, out=data)
-    d_in = rg.digest(data, n, rs)
-    kt: dict = {}
-    st: dict = {}
-    ms = []
-    launches = 0
-    for i in range(warmup + steps):
-        rg.generate(n, lay, dist=dist_kind, seed=seed, out=data)
-        rg.set_profiling(i >= warmup)
-        torch.cuda.synchronize(dev)
-        c0 = rg.launch_count()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        rg.sort(data, n, lay, tmp=tmp, stream=stream)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        if i >= warmup:
-            launches += rg.launch_count() - c0
-            ms.append(e0.elapsed_time(e1))
-            for k, (l, t) in rg.last_kernel_times().items():
-                kt.setdefault(k, [0, 0.0])
-                kt[k][0] += l
-                kt[k][1] += t
-            for k, v in rg.last_stats().items():
-                st[k] = st.get(k, 0) + v
-    rg.set_profiling(False)
-    viol, _ = rg.check_sorted(data, n, lay)
-    ok = viol == 0 and rg.digest(data, n, rs) == d_in
-    del data, tmp
-    torch.cuda.empty_cache()
-    ab = algorithmic_bytes(st, rs)
-    tot = sum(ms)
-    return {"workload": desc, "ms_per_sort": round(tot / len(ms), 3),
-            "value": n * len(ms) / (tot / 1e3), "unit": UNIT, "steps": len(ms), "verified": ok,
-            "roofline": dominant(kt, ab, peak, peak_src),
-            "roofline_sort": sort_roofline(ab, tot, len(ms), peak, n, rs),
-            "kernels": kernel_table(kt, ab), "gpu_launches": launches,
-            "stats_per_step": {k: v // len(ms) for k, v in st.items()}}
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -410,166 +361,177 @@ def main():
         torch.distributed.all_gather_object(out, obj)
         return out
 
-    # ---------------- device-resident measurement (one pass per exchange at N>1)
-    data = torch.empty(n_local * rs, dtype=torch.uint8, device=dev)
-    tmp = torch.empty_like(data) if world == 1 else None
     stream = torch.cuda.current_stream(dev)
     rg.set_profiling(False)
-    rg.generate(n_local, lay, dist=dist_kind, seed=seed, index_base=base, out=data)
-    digest_in = rg.digest(data, n_local, rs)
 
-    def one_step(exchange, timings):
-        rg.generate(n_local, lay, dist=dist_kind, seed=seed, index_base=base, out=data)
-        torch.cuda.synchronize(dev)
-        barrier()
-        torch.cuda.synchronize(dev)
-        c0 = rg.launch_count()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        if world == 1:
-            rg.sort(data, n_local, lay, tmp=tmp, stream=stream)
-            out, n_out = data, n_local
-        else:
-            from paper_1612_02557_b200.distributed import sort_distributed
-            out, n_out = sort_distributed(data, n_local, lay, timings=timings, exchange=exchange)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        barrier()
-        return e0.elapsed_time(e1), out, n_out, rg.launch_count() - c0
+    def run_workload(cfg_name: str, exchanges, steps: int, warmup: int, clocks=None) -> dict:
+        """One configuration, device-resident: per exchange (N>1) warm-up +
+        timed steps, per-rank kernel times, exchange timings, launches, and
+        the verification of the last step's output (untimed). Returns
+        {exchange: summary} (+ "_regions": the timed regions)."""
+        wn_total, wrs, wks, wdist, wseed, _ = CONFIGS[cfg_name]
+        wlay = rg.RecordLayout(wrs, wks)
+        wn_local = wn_total // world
+        wbase = rank * wn_local
+        if rank == world - 1:
+            wn_local = wn_total - wbase
+        data = torch.empty(wn_local * wrs, dtype=torch.uint8, device=dev)
+        tmp = torch.empty_like(data) if world == 1 else None
+        rg.generate(wn_local, wlay, dist=wdist, seed=wseed, index_base=wbase, out=data)
+        digest_in = rg.digest(data, wn_local, wrs)
 
-    def measure(exchange):
-        """Warm-up + timed steps; per-rank kernel times, exchange timings,
-        launches; verification of the last step's output (untimed)."""
-        for _ in range(args.warmup):
-            _, out, n_out, _ = one_step(exchange, {})
+        def one_step(exchange, timings):
+            rg.generate(wn_local, wlay, dist=wdist, seed=wseed, index_base=wbase, out=data)
+            torch.cuda.synchronize(dev)
+            barrier()
+            torch.cuda.synchronize(dev)
+            c0 = rg.launch_count()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            if world == 1:
+                rg.sort(data, wn_local, wlay, tmp=tmp, stream=stream)
+                out, n_out = data, wn_local
+            else:
+                from paper_1612_02557_b200.distributed import sort_distributed
+                out, n_out = sort_distributed(data, wn_local, wlay, timings=timings, exchange=exchange)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            barrier()
+            return e0.elapsed_time(e1), out, n_out, rg.launch_count() - c0
+
+        def measure(exchange):
+            for _ in range(warmup):
+                _, out, n_out, _ = one_step(exchange, {})
+                del out
+            rg.set_profiling(True)
+            kt: dict = {}
+            st: dict = {}
+            xs = {"exchange_ms": 0.0, "partition_ms": 0.0, "sent_bytes": 0, "plan_s": 0.0}
+            step_ms = []
+            launches = 0
+            t_region0 = time.time()
+            for _ in range(steps):
+                tim: dict = {}
+                ms, out, n_out, nl = one_step(exchange, tim)
+                launches += nl
+                step_ms.append(max_over_ranks(ms))
+                for k, (l, t) in rg.last_kernel_times().items():  # this rank's (local) sort
+                    kt.setdefault(k, [0, 0.0])
+                    kt[k][0] += l
+                    kt[k][1] += t
+                for k, v in rg.last_stats().items():
+                    st[k] = st.get(k, 0) + v
+                for k in ("exchange_ms", "partition_ms", "sent_bytes", "plan_s"):
+                    if tim.get(k) is not None:
+                        xs[k] += tim[k]
+            t_region = (t_region0, time.time())
+            rg.set_profiling(False)
+            # verification (untimed): order, digest, and at N>1 the rank seams
+            viol, _ = rg.check_sorted(out, n_out, wlay)
+            d_out = rg.digest(out, n_out, wrs)
+            first = bytes(out[:wks].cpu().numpy()) if n_out else None
+            last = bytes(out[(n_out - 1) * wrs:(n_out - 1) * wrs + wks].cpu().numpy()) if n_out else None
             del out
-        rg.set_profiling(True)
-        kt: dict = {}
-        st: dict = {}
-        xs = {"exchange_ms": 0.0, "partition_ms": 0.0, "sent_bytes": 0, "plan_s": 0.0}
-        step_ms = []
-        launches = 0
-        t_region0 = time.time()
-        for _ in range(args.steps):
-            tim: dict = {}
-            ms, out, n_out, nl = one_step(exchange, tim)
-            launches += nl
-            step_ms.append(max_over_ranks(ms))
-            for k, (l, t) in rg.last_kernel_times().items():  # this rank's (local) sort
-                kt.setdefault(k, [0, 0.0])
-                kt[k][0] += l
-                kt[k][1] += t
-            for k, v in rg.last_stats().items():
-                st[k] = st.get(k, 0) + v
-            for k in ("exchange_ms", "partition_ms", "sent_bytes", "plan_s"):
-                if tim.get(k) is not None:
-                    xs[k] += tim[k]
-            xs["exchange"] = tim.get("exchange")
-        t_region = (t_region0, time.time())
-        rg.set_profiling(False)
-        # verification (untimed): order, digest, and at N>1 the rank seams
-        viol, _ = rg.check_sorted(out, n_out, lay)
-        d_out = rg.digest(out, n_out, rs)
-        first = bytes(out[:ks].cpu().numpy()) if n_out else None
-        last = bytes(out[(n_out - 1) * rs:(n_out - 1) * rs + ks].cpu().numpy()) if n_out else None
-        del out
-        if world > 1 and exchange == "nccl":
-            torch.cuda.empty_cache()
-        mine = {"viol": viol, "d_in": digest_in, "d_out": d_out, "n_out": n_out, "first": first,
-                "last": last, "kt": kt, "st": st, "xs": xs, "launches": launches, "n_local": n_local}
-        return step_ms, t_region, gather(mine)
+            mine = {"viol": viol, "d_in": digest_in, "d_out": d_out, "n_out": n_out, "first": first,
+                    "last": last, "kt": kt, "st": st, "xs": xs, "launches": launches, "n_local": wn_local}
+            return step_ms, t_region, gather(mine)
 
-    def verify(rows) -> dict:
-        m = (1 << 128) - 1
-        din = sum(r["d_in"][0] + (r["d_in"][1] << 64) for r in rows) & m
-        dout = sum(r["d_out"][0] + (r["d_out"][1] << 64) for r in rows) & m
-        seams = True
-        prev = None
-        for r in rows:
-            if r["n_out"]:
-                if prev is not None and prev > r["first"]:
-                    seams = False
-                prev = r["last"]
-        tot = sum(r["n_out"] for r in rows)
-        ok = all(r["viol"] == 0 for r in rows) and din == dout and seams and tot == n_total
-        return {"ok": ok, "inversions": sum(r["viol"] for r in rows), "digest_equal": din == dout,
-                "rank_seams_ordered": seams, "records_out": tot}
+        def verify(rows) -> dict:
+            m = (1 << 128) - 1
+            din = sum(r["d_in"][0] + (r["d_in"][1] << 64) for r in rows) & m
+            dout = sum(r["d_out"][0] + (r["d_out"][1] << 64) for r in rows) & m
+            seams = True
+            prev = None
+            for r in rows:
+                if r["n_out"]:
+                    if prev is not None and prev > r["first"]:
+                        seams = False
+                    prev = r["last"]
+            tot = sum(r["n_out"] for r in rows)
+            ok = all(r["viol"] == 0 for r in rows) and din == dout and seams and tot == wn_total
+            return {"ok": ok, "inversions": sum(r["viol"] for r in rows), "digest_equal": din == dout,
+                    "rank_seams_ordered": seams, "records_out": tot}
+
+        def summarise(ex, step_ms, rows) -> dict:
+            total_ms = sum(step_ms)
+            ab_all: dict = {}
+            per_rank = []
+            worst = None
+            for r in rows:
+                ab = algorithmic_bytes(r["st"], wrs)
+                kt = {k: tuple(v) for k, v in r["kt"].items()}
+                if ex is not None:  # the partition pass of the exchange: one read + one write of n_local
+                    cls = "partition_exchange" if ex == "p2p" else "partition"
+                    ms_p = r["xs"]["exchange_ms"] if ex == "p2p" else r["xs"]["partition_ms"]
+                    kt[cls] = (steps, ms_p)
+                    ab[cls] = 2 * wrs * r["n_local"] * steps
+                for k, v in ab.items():
+                    ab_all[k] = ab_all.get(k, 0) + v
+                roof = dominant(kt, ab, peak, peak_src)
+                per_rank.append({"kernel": roof["kernel"], "frac": roof["frac"]} if roof else None)
+                if roof and (worst is None or roof["frac"] < worst[0]["frac"]):
+                    worst = (roof, kt, ab)
+            out = {"workload": CONFIGS[cfg_name][5],
+                   "value": wn_total * steps / (total_ms / 1e3), "unit": UNIT,
+                   "ms_per_step": total_ms / steps, "steps": steps, "verified": verify(rows),
+                   "roofline": worst[0] if worst else None,
+                   "roofline_sort": sort_roofline(ab_all, total_ms, steps, peak, wn_total, wrs, world),
+                   "kernels": kernel_table(worst[1], worst[2]) if worst else None,
+                   "gpu_launches": sum(r["launches"] for r in rows),
+                   "stats_per_step": {k: v // steps for k, v in rows[0]["st"].items()} or None}
+            if world > 1:
+                out["roofline"]["per_rank_frac"] = [q["frac"] if q else None for q in per_rank]
+                out["roofline"]["rank"] = "slowest rank (lowest frac)"
+                sent = max(r["xs"]["sent_bytes"] for r in rows) / steps
+                t_ex = max(r["xs"]["exchange_ms"] for r in rows) / steps
+                gbs = sent / (t_ex / 1e3) / 1e9 if t_ex else None
+                out["nvlink"] = {"exchange": ex, "sent_bytes_per_gpu": sent, "t_exchange_ms": round(t_ex, 3),
+                                 "GBps": round(gbs, 1) if gbs else None, "peak": 900.0,
+                                 "peak_source": "NVLink 5 per direction per GPU (nominal)",
+                                 "frac": round(gbs / 900.0, 4) if gbs else None,
+                                 "what": ("the fused partition+store kernel (reads local records, stores "
+                                          "each destination's share into its window over NVLink)"
+                                          if ex == "p2p" else "NCCL all_to_all_single"),
+                                 "plan_ms": round(1e3 * max(r["xs"]["plan_s"] for r in rows) / steps, 3)}
+            return out
+
+        res = {}
+        regions = []
+        for ex in exchanges:
+            step_ms, region, rows = measure(ex)
+            regions.append(region)
+            res[ex] = summarise(ex, step_ms, rows)
+            if world > 1:  # the next exchange (and e2e) gets the memory back
+                from paper_1612_02557_b200.distributed import release_peer_windows
+                release_peer_windows()
+                torch.cuda.empty_cache()
+        del data, tmp
+        torch.cuda.empty_cache()
+        res["_regions"] = regions
+        return res
 
     clocks = ClockSampler(dev_index)
     clocks.start()  # before the warm-up: nvidia-smi's start-up stays outside the timed region
     exchanges = [None] if world == 1 else (["p2p", "nccl"] if args.exchange == "both" else [args.exchange])
-    runs = {}
-    regions = []
-    for ex in exchanges:
-        step_ms, region, rows = measure(ex)
-        regions.append(region)
-        runs[ex] = (step_ms, rows)
-        if world > 1:  # the next exchange (and e2e) gets the memory back
-            from paper_1612_02557_b200.distributed import release_peer_windows
-            release_peer_windows()
-            torch.cuda.empty_cache()
+    summ = run_workload(args.config, exchanges, args.steps, args.warmup)
+    regions = summ.pop("_regions")
     clk = clocks.stop((regions[0][0], regions[-1][1]))
-
-    def summarise(ex, step_ms, rows) -> dict:
-        total_ms = sum(step_ms)
-        ab_all: dict = {}
-        per_rank = []
-        worst = None
-        for r in rows:
-            ab = algorithmic_bytes(r["st"], rs)
-            kt = {k: tuple(v) for k, v in r["kt"].items()}
-            if ex is not None:  # the partition pass of the exchange: one read + one write of n_local
-                cls = "partition_exchange" if ex == "p2p" else "partition"
-                ms_p = r["xs"]["exchange_ms"] if ex == "p2p" else r["xs"]["partition_ms"]
-                kt[cls] = (args.steps, ms_p)
-                ab[cls] = 2 * rs * r["n_local"] * args.steps
-            for k, v in ab.items():
-                ab_all[k] = ab_all.get(k, 0) + v
-            roof = dominant(kt, ab, peak, peak_src)
-            per_rank.append({"kernel": roof["kernel"], "frac": roof["frac"]} if roof else None)
-            if roof and (worst is None or roof["frac"] < worst[0]["frac"]):
-                worst = (roof, kt, ab)
-        out = {"value": n_total * args.steps / (total_ms / 1e3), "ms_per_step": total_ms / args.steps,
-               "verified": verify(rows),
-               "roofline": worst[0] if worst else None,
-               "roofline_sort": sort_roofline(ab_all, total_ms, args.steps, peak, n_total, rs, world),
-               "kernels": kernel_table(worst[1], worst[2]) if worst else None,
-               "gpu_launches": sum(r["launches"] for r in rows),
-               "stats_per_step": {k: v // args.steps for k, v in rows[0]["st"].items()} or None}
-        if world > 1:
-            out["roofline"]["per_rank_frac"] = [p["frac"] if p else None for p in per_rank]
-            out["roofline"]["rank"] = "slowest rank (lowest frac)"
-            sent = max(r["xs"]["sent_bytes"] for r in rows) / args.steps
-            t_ex = max(r["xs"]["exchange_ms"] for r in rows) / args.steps
-            gbs = sent / (t_ex / 1e3) / 1e9 if t_ex else None
-            out["nvlink"] = {"exchange": ex, "sent_bytes_per_gpu": sent, "t_exchange_ms": round(t_ex, 3),
-                             "GBps": round(gbs, 1) if gbs else None, "peak": 900.0,
-                             "peak_source": "NVLink 5 per direction per GPU (nominal)",
-                             "frac": round(gbs / 900.0, 4) if gbs else None,
-                             "what": ("the fused partition+store kernel (reads local records, stores "
-                                      "each destination's share into its window over NVLink)"
-                                      if ex == "p2p" else "NCCL all_to_all_single"),
-                             "plan_ms": round(1e3 * max(r["xs"]["plan_s"] for r in rows) / args.steps, 3)}
-        return out
-
-    summ = {ex: summarise(ex, *runs[ex]) for ex in exchanges}
     best = max(summ, key=lambda e: summ[e]["value"])
     head = summ[best]
 
-    del data, tmp
-    torch.cuda.empty_cache()
-
-    # ---------------- C1-C4 beside the headline (N=1): same run, same box
+    # ---------------- C1-C4 beside the headline: same run, same box (N>1: the headline's exchange)
     per_config = None
-    if world == 1 and not args.no_per_config:
+    if not args.no_per_config:
         per_config = {}
         for name in sorted(CONFIGS):
             if name == args.config:
                 continue
             try:
                 time.sleep(3)  # let the HBM/power state settle after the previous config
-                per_config[name] = measure_config(rg, torch, dev, name, 3, 3, peak, peak_src)
+                r = run_workload(name, [best], 3, 3)
+                r.pop("_regions")
+                per_config[name] = r[best]
             except Exception as ex:  # noqa: BLE001
                 per_config[name] = {"error": str(ex)[:200]}
 

@@ -172,7 +172,7 @@ def test_bench_multi_rank_line(torch_cuda, tmp_path):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(root, "bench.py"), "--gpus", "2", "--config", "c1", "--steps", "2",
-           "--warmup", "3", "--no-e2e"]
+           "--warmup", "3", "--no-e2e", "--no-per-config"]
     res = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=root, timeout=600)
     assert res.returncode == 0, res.stderr[-3000:]
     line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
