@@ -57,12 +57,27 @@ struct LocalCfg {
     // 16/24-B records: small CTAs, four per SM, so one group's HBM traffic and
     // barriers overlap other groups' work; 32-B records keep 4608-record groups
     // (BASELINE C4's ~4 K-record bins) at one CTA per SM.
-    static constexpr int kThreads = kRegRecords ? 1024 : 512;
-    static constexpr int kMinBlocks = (RS == 16 || RS == 24) ? 2 : 1;
+    // RG_LOC8_CAP / _THREADS / _BLOCKS / _BITS: the 8-B shape, as knobs for
+    // the measured alternative of a third scatter level at C2 (a smaller cap
+    // makes C2's ~16 K-record bins split once more)
+#ifndef RG_LOC8_CAP
+#define RG_LOC8_CAP 18432
+#endif
+#ifndef RG_LOC8_THREADS
+#define RG_LOC8_THREADS 1024
+#endif
+#ifndef RG_LOC8_BLOCKS
+#define RG_LOC8_BLOCKS 1
+#endif
+#ifndef RG_LOC8_BITS
+#define RG_LOC8_BITS 15
+#endif
+    static constexpr int kThreads = kRegRecords ? RG_LOC8_THREADS : 512;
+    static constexpr int kMinBlocks = (RS == 16 || RS == 24) ? 2 : RS == 8 ? RG_LOC8_BLOCKS : 1;
     static constexpr int kWarps = kThreads / 32;
-    static constexpr int kCap = RS == 8 ? 18432 : RS == 16 ? 3584 : RS == 24 ? 2560 : 4608;
+    static constexpr int kCap = RS == 8 ? RG_LOC8_CAP : RS == 16 ? 3584 : RS == 24 ? 2560 : 4608;
     static constexpr int kIpt = (kCap + kThreads - 1) / kThreads;
-    static constexpr int kBucketBits = RS == 8 ? 15 : 13;
+    static constexpr int kBucketBits = RS == 8 ? RG_LOC8_BITS : 13;
     // packed u16 bucket counters, four pad words per 64 buckets (conflict-free LDS.128 scan)
     static constexpr int kCntWords = (1 << kBucketBits) / 2 + (1 << kBucketBits) / 16;
     static constexpr int kCntBytes = (kCntWords * 4 > kWarps * kRadix * 4) ? kCntWords * 4
