@@ -713,6 +713,56 @@ def _split_digit_count(plan: ExchangePlan) -> int:
     return sum(1 for v in ranks.values() if len(v) > 1)
 
 
+def _exchange_digit_major(recv, send, plan: ExchangePlan, offsets, rank: int, world: int, rs: int,
+                          group) -> None:
+    """The NCCL exchange into a digit-major receive buffer (the layout of
+    _receive_layout): every (source, digit) piece lands at its place, so the
+    receiver continues the MSD sort from the next byte. NCCL: one grouped
+    batch of point-to-point sends and receives (pieces between a pair of
+    ranks posted in the same digit order on both sides); a rank's pieces to
+    itself are device copies. gloo (tests on one shared device or CPU): one
+    all_to_all_single staged through host memory, rearranged on the host."""
+    import torch.distributed as dist
+    mine = plan.pieces[rank]
+    if dist.get_backend(group) == "nccl":
+        ops_ = []
+        pos = 0
+        for d, k, c in mine:
+            if k == rank:
+                o = int(offsets[rank, d, rank])
+                recv[o * rs:(o + c) * rs].copy_(send[pos * rs:(pos + c) * rs])
+            else:
+                ops_.append(dist.P2POp(dist.isend, send[pos * rs:(pos + c) * rs], k, group))
+            pos += c
+        for s_ in range(world):
+            if s_ == rank:
+                continue
+            for d, k, c in plan.pieces[s_]:
+                if k == rank:
+                    o = int(offsets[s_, d, rank])
+                    ops_.append(dist.P2POp(dist.irecv, recv[o * rs:(o + c) * rs], s_, group))
+        if ops_:
+            for r in dist.batch_isend_irecv(ops_):
+                r.wait()
+        return
+    # gloo: source-major all_to_all_single (host-staged for CUDA tensors), then
+    # each source's run of pieces (digit order) moved to its digit-major place
+    n_out = int(plan.recv_counts(rank).sum())
+    n_in = int(plan.send_counts(rank).sum())
+    staged = recv.new_empty(max(n_out, 1) * rs, device="cpu")
+    _all_to_all(staged[:n_out * rs], send[:n_in * rs], [int(c) * rs for c in plan.recv_counts(rank)],
+                [int(c) * rs for c in plan.send_counts(rank)], group)
+    out = staged.new_empty(max(n_out, 1) * rs)
+    at = 0
+    for s_ in range(world):
+        for d, k, c in plan.pieces[s_]:
+            if k == rank:
+                o = int(offsets[s_, d, rank])
+                out[o * rs:(o + c) * rs] = staged[at * rs:(at + c) * rs]
+                at += c
+    recv[:n_out * rs].copy_(out[:n_out * rs])
+
+
 def _all_to_all(recv, send, out_splits, in_splits, group):
     """dist.all_to_all_single; gloo cannot move CUDA tensors, so there the
     exchange is staged through host memory (tests on one shared device)."""
@@ -823,16 +873,21 @@ def sort_distributed(data, n: int, layout: RecordLayout, ops=None, group=None,
         if not np.array_equal(np.asarray(counts, dtype=np.int64), plan.M[rank]):
             raise RuntimeError("partition counts disagree with the exchanged histograms")
         recv = ops.empty(max(n_out, 1) * rs)
+        offsets, segments = _receive_layout(plan, world)
         e2 = event()
-        _all_to_all(recv[:n_out * rs] if n_out else recv[:0], send[:n * rs],
-                    [int(c) * rs for c in plan.recv_counts(rank)],
-                    [int(c) * rs for c in plan.send_counts(rank)], group)
+        _exchange_digit_major(recv, send, plan, offsets, rank, world, rs, group)
         e3 = event()
         info["partition_ms"] = elapsed(e0, e1)
         info["exchange_ms"] = elapsed(e2, e3)
         del send
         t2 = time.perf_counter()
-        ops.sort(recv, n_out, layout)
+        mine = segments[rank]
+        fb = plan.digits.first_byte
+        info["segments"] = len(mine)
+        if fb is not None and hasattr(ops, "sort_segments") and len(mine) > 1:
+            ops.sort_segments(recv, n_out, layout, [c for _, c in mine], [int(fb[d]) for d, _ in mine])
+        else:
+            ops.sort(recv, n_out, layout)
     if cuda:
         torch.cuda.synchronize(data.device)
     t3 = time.perf_counter()
