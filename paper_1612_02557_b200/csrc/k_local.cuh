@@ -221,6 +221,17 @@ __device__ __forceinline__ void local_group(
     unsigned int* __restrict__ n_spill, uint32_t spill_cap, Mid&& mid) {
     using C = LocalCfg<RS>;
     constexpr bool REG = C::kRegRecords;
+    // RG_LOC_DIRECT (shared-memory records): each record is stored to its final
+    // place when it is ranked (its own slot read from shared memory, one
+    // uncoalesced 16-B global store; the group's lines fill up in L2 within
+    // microseconds) instead of through perm and a coalesced output loop that
+    // gathers records at random from shared memory (~10.4 wavefronts per 32
+    // records against 4). Interleaved A/B (profiles/r2_ab_direct*.log): C5
+    // local 44.5 vs 46.7 ms, C3 -3%, C1 -2.3%, C4 unchanged.
+#ifndef RG_LOC_DIRECT
+#define RG_LOC_DIRECT 1
+#endif
+    constexpr bool kDirect = RG_LOC_DIRECT && !REG;
     constexpr int T = C::kThreads, W = C::kWarps, IPT = C::kIpt;
     constexpr int KW = RS / 8;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -591,6 +602,7 @@ __device__ __forceinline__ void local_group(
         };
         auto place = [&](uint32_t e, uint32_t f) {
             if constexpr (REG) perm[e] = uint16_t(f);  // e -> final position
+            else if constexpr (kDirect) store_rec<RS>(dst, f, ld_smem_rec<RS>(recs, e));  // now, uncoalesced
             else perm[f] = uint16_t(e);                // final position -> e
         };
         auto rank_slow = [&](uint32_t e, uint32_t w, uint32_t st, uint32_t en) {
@@ -836,9 +848,11 @@ __device__ __forceinline__ void local_group(
             if (c0 + CC < n) __syncthreads();
         }
     } else {
+        if constexpr (!(kDirect && !kFallback)) {  // (kDirect: every record was stored when placed)
 #pragma unroll kLocOutUnroll<RS>
-        for (uint32_t f = threadIdx.x; f < n; f += T)
-            store_rec<RS>(dst, f, ld_smem_rec<RS>(recs, perm[f]));
+            for (uint32_t f = threadIdx.x; f < n; f += T)
+                store_rec<RS>(dst, f, ld_smem_rec<RS>(recs, perm[f]));
+        }
     }
     if (threadIdx.x == 0) atomicAdd(&ctr->moved_local, (unsigned long long)n);
 }
