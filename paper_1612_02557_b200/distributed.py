@@ -722,9 +722,13 @@ def _exchange_digit_major(recv, send, plan: ExchangePlan, offsets, rank: int, wo
     ranks posted in the same digit order on both sides); a rank's pieces to
     itself are device copies. gloo (tests on one shared device or CPU): one
     all_to_all_single staged through host memory, rearranged on the host."""
+    import os
+
     import torch.distributed as dist
     mine = plan.pieces[rank]
-    if dist.get_backend(group) == "nccl":
+    # RADULS_P2P_OPS=1: the point-to-point form under gloo too (CPU tests of its
+    # piece order and placement; gloo sends host tensors only)
+    if dist.get_backend(group) == "nccl" or (os.environ.get("RADULS_P2P_OPS") == "1" and not send.is_cuda):
         ops_ = []
         pos = 0
         for d, k, c in mine:

@@ -402,3 +402,42 @@ def test_aligned_digits_and_digit_major_layout(world):
             assert (dd, s) > last  # digit-major, then source order
             last = (dd, s)
             pos += c
+
+
+def _worker_p2p_ops(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["RADULS_P2P_OPS"] = "1"
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a = _input(rank, world, 16, 8, 0, 0.3)
+    t = {}
+    out, n_out = D.sort_distributed(torch.from_numpy(a.copy()), a.size // 16, RecordLayout(16, 8),
+                                    ops=CpuOps(), timings=t)
+    q.put((rank, out.numpy()[:n_out * 16].copy(), t))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_point_to_point_exchange_digit_major(world):
+    """The NCCL exchange's point-to-point form (one send/receive per
+    (source, digit) piece into the digit-major receive buffer), run under
+    gloo: with a hot key spread over ranks the concatenation is the stable
+    sort."""
+    import oracle
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_p2p_ops, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, out, t = q.get(timeout=180)
+        res[r] = (out, t)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    got = np.concatenate([res[r][0] for r in range(world)])
+    a = np.concatenate([_input(r, world, 16, 8, 0, 0.3) for r in range(world)])
+    assert np.array_equal(got, oracle.stable_sort(a, 16, 8))
+    assert all(res[r][1]["exchange"] == "nccl" and res[r][1]["segments"] >= 1 for r in range(world))
