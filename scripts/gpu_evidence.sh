@@ -1,10 +1,20 @@
 #!/bin/bash
-# round 2 evidence: driver-shaped bench line, launch list of the bench command, reference arm
+# the round's evidence run: driver-shaped bench line, reference arm, ncu launch
+# list of the bench command, full captures of the local sort and the scatter (C1)
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > gpurun_out/r2_box.txt 2>&1
-timeout 1200 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/r2_bench_c5.json 2> gpurun_out/r2_bench_c5.err
-echo "bench rc=$?" >> gpurun_out/r2_bench_c5.err
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > gpurun_out/ev_box.txt 2>&1
+timeout 1200 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/ev_bench_c5.json 2> gpurun_out/ev_bench_c5.err
+echo "bench rc=$?" >> gpurun_out/ev_bench_c5.err
+timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/ev_bench_ref.json 2> gpurun_out/ev_bench_ref.err
+echo "ref rc=$?" >> gpurun_out/ev_bench_ref.err
 CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-per-config"
 timeout 1800 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 300 --csv \
-   --log-file gpurun_out/r2_launches_bench_c5.csv $CMD > gpurun_out/r2_ncu_bench.log 2>&1
-echo "launch-list rc=$?" >> gpurun_out/r2_ncu_bench.log
+   --log-file gpurun_out/ev_launches_bench_c5.csv $CMD > gpurun_out/ev_ncu_bench.log 2>&1
+echo "launch-list rc=$?" >> gpurun_out/ev_ncu_bench.log
+for K in k_local k_scatter; do
+  timeout 600 ncu --set full --import-source on --clock-control none -k regex:$K -s 2 -c 1 \
+     -o gpurun_out/ev_full_$K -f python scripts/prof_one.py c1 2 > gpurun_out/ev_ncu_full_$K.log 2>&1
+  ncu -i gpurun_out/ev_full_$K.ncu-rep --page raw --csv > gpurun_out/ev_full_${K}_raw.csv 2>&1
+  ncu -i gpurun_out/ev_full_$K.ncu-rep --page source --csv --print-source sass > gpurun_out/ev_full_${K}_sass.csv 2>&1
+done
+rm -f gpurun_out/*.ncu-rep
