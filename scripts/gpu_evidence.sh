@@ -12,7 +12,7 @@ timeout 1800 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byt
    --log-file gpurun_out/ev_launches_bench_c5.csv $CMD > gpurun_out/ev_ncu_bench.log 2>&1
 echo "launch-list rc=$?" >> gpurun_out/ev_ncu_bench.log
 for K in k_local k_scatter; do
-  timeout 600 ncu --set full --import-source on --clock-control none -k regex:$K -s 2 -c 1 \
+  timeout 600 ncu --set full --import-source on --clock-control none -k regex:$K -s $([ $K = k_local ] && echo 1 || echo 2) -c 1 \
      -o gpurun_out/ev_full_$K -f python scripts/prof_one.py c1 2 > gpurun_out/ev_ncu_full_$K.log 2>&1
   ncu -i gpurun_out/ev_full_$K.ncu-rep --page raw --csv > gpurun_out/ev_full_${K}_raw.csv 2>&1
   ncu -i gpurun_out/ev_full_$K.ncu-rep --page source --csv --print-source sass > gpurun_out/ev_full_${K}_sass.csv 2>&1
