@@ -41,11 +41,12 @@ struct Rec {
 // failure. The C-ABI returns RADULS_GPU_EINTERNAL from any call that
 // recorded a violation (raduls_gpu_check_report has the details).
 #ifdef RG_CHECKED
+constexpr unsigned int kChkRanges = 1024;
 struct ChkState {
-    unsigned long long lo[32], hi[32];
-    unsigned int n, jitter;
     unsigned long long fails, first_addr, deadlocks;
     unsigned int first_site, first_bytes;
+    unsigned int n, jitter;
+    unsigned long long lo[kChkRanges], hi[kChkRanges];  // sorted by lo, disjoint (merged on the host)
 };
 __device__ ChkState g_chk;
 
@@ -61,8 +62,13 @@ __device__ __forceinline__ void chk_global(const void* p, uint32_t bytes, uint32
     const uint32_t n = *(volatile unsigned int*)&g_chk.n;
     if (n == 0 || !__isGlobal(p)) return;
     const unsigned long long a = reinterpret_cast<unsigned long long>(p);
-    for (uint32_t i = 0; i < n; ++i)
-        if (a >= g_chk.lo[i] && a + bytes <= g_chk.hi[i]) return;
+    uint32_t l = 0, h = n;  // the last range starting at or below a
+    while (h - l > 1) {
+        const uint32_t m = (l + h) >> 1;
+        if (g_chk.lo[m] <= a) l = m;
+        else h = m;
+    }
+    if (g_chk.lo[l] <= a && a + bytes <= g_chk.hi[l]) return;
     chk_fail(site, p, bytes);
 }
 

@@ -103,12 +103,22 @@ static void chk_upload(cudaStream_t st) {
     // B bytes shorter, so a correct sort must be reported
     static const uint64_t shrink = std::getenv("RADULS_GPU_CHECK_SHRINK")
                                        ? std::strtoull(std::getenv("RADULS_GPU_CHECK_SHRINK"), nullptr, 10) : 0;
-    for (auto& r : g_chk_host.ranges) r.second = std::max(r.first, r.second - shrink);
-    rg::ChkState h{};
-    const size_t k = std::min<size_t>(g_chk_host.ranges.size(), 32);
-    for (size_t i = 0; i < k; ++i) h.lo[i] = g_chk_host.ranges[i].first, h.hi[i] = g_chk_host.ranges[i].second;
+    std::vector<std::pair<uint64_t, uint64_t>> r = g_chk_host.ranges;
+    for (auto& x : r) x.second = std::max(x.first, x.second - shrink);
+    std::sort(r.begin(), r.end());
+    std::vector<std::pair<uint64_t, uint64_t>> m;  // merged: sorted, disjoint
+    for (auto& x : r) {
+        if (!m.empty() && x.first <= m.back().second) m.back().second = std::max(m.back().second, x.second);
+        else m.push_back(x);
+    }
+    static rg::ChkState h;  // (under g_chk_host.mu; copied before it is reused)
+    const size_t k = std::min<size_t>(m.size(), rg::kChkRanges);
+    for (size_t i = 0; i < k; ++i) h.lo[i] = m[i].first, h.hi[i] = m[i].second;
     h.n = unsigned(k);
-    RG_CHECK(cudaMemcpyToSymbolAsync(rg::g_chk, &h, offsetof(rg::ChkState, fails), 0, cudaMemcpyHostToDevice, st));
+    const size_t off = offsetof(rg::ChkState, n);
+    RG_CHECK(cudaMemcpyToSymbol(rg::g_chk, reinterpret_cast<const char*>(&h) + off, sizeof(rg::ChkState) - off, off,
+                                cudaMemcpyHostToDevice));
+    (void)st;
 }
 // Replace (reset = true) or extend the registered ranges; enqueued on st.
 static void chk_ranges(cudaStream_t st, std::initializer_list<std::pair<const void*, size_t>> r,
@@ -127,15 +137,19 @@ static void chk_begin() {
         std::lock_guard<std::mutex> lk(g_chk_host.mu);
         g_chk_host.ranges.clear();
     }
-    rg::ChkState h{};
+    static rg::ChkState h;  // zeros: no ranges, no counts (calls are serialised, g_chk_call)
     h.jitter = std::getenv("RADULS_GPU_CHECK_JITTER") ? 1u : 0u;
-    cudaMemcpyToSymbol(rg::g_chk, &h, sizeof h);
+    cudaMemcpyToSymbol(rg::g_chk, &h, offsetof(rg::ChkState, lo));
 }
+// One checked call at a time per process: the device-side state (ranges,
+// counters) is one per device and the host range list one per process, and
+// a multi-device call runs a host thread per device.
+static std::recursive_mutex g_chk_call;
 // 0, or RADULS_GPU_EINTERNAL after printing the first violation
 static int chk_end() {
     cudaDeviceSynchronize();
-    rg::ChkState h{};
-    if (cudaMemcpyFromSymbol(&h, rg::g_chk, sizeof h) != cudaSuccess) return RADULS_GPU_ECUDA;
+    rg::ChkState h;
+    if (cudaMemcpyFromSymbol(&h, rg::g_chk, offsetof(rg::ChkState, lo)) != cudaSuccess) return RADULS_GPU_ECUDA;
     std::lock_guard<std::mutex> lk(g_chk_host.mu);
     g_chk_host.report[5]++;
     if (!h.fails && !h.deadlocks) return 0;
@@ -1137,6 +1151,7 @@ int guarded(F&& f) {
     cudaGetLastError();  // a stale non-sticky error (e.g. a caller's failed allocation) is not ours
     try {
 #ifdef RG_CHECKED
+        std::lock_guard<std::recursive_mutex> serial(g_chk_call);
         chk_begin();
         f();
         return chk_end();
