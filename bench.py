@@ -269,7 +269,18 @@ def kernel_table(kt: dict, ab: dict) -> dict:
             for k, (l, t) in kt.items()}
 
 
-def dominant(kt: dict, ab: dict, peak: float, peak_src: str) -> dict | None:
+def ncu_traffic(cfg_name: str) -> dict:
+    """DRAM bytes per launch per kernel class from the committed ncu launch list
+    of this config's bench command (scripts/traffic_from_launches.py; the file
+    is regenerated with every evidence run)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg_name}.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def dominant(kt: dict, ab: dict, peak: float, peak_src: str, traffic: dict | None = None) -> dict | None:
     """Roofline of the kernel class with the most device time (live CUDA events)."""
     if not kt:
         return None
@@ -277,8 +288,10 @@ def dominant(kt: dict, ab: dict, peak: float, peak_src: str) -> dict | None:
     dl, dt = kt[dom]
     db = ab.get(dom, 0)
     achieved = db / (dt / 1e3) / 1e9 if dt else 0.0
+    tr = (traffic or {}).get(dom)
     return {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
-            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": tr,
+            "traffic_source": (traffic or {}).get("_source") if tr else None,
             "algorithmic_bytes_per_launch": db / max(dl, 1), "launches": dl, "peak_source": peak_src}
 
 
@@ -468,7 +481,7 @@ def main():
                     ab[cls] = 2 * wrs * r["n_local"] * steps
                 for k, v in ab.items():
                     ab_all[k] = ab_all.get(k, 0) + v
-                roof = dominant(kt, ab, peak, peak_src)
+                roof = dominant(kt, ab, peak, peak_src, ncu_traffic(cfg_name) if world == 1 else None)
                 per_rank.append({"kernel": roof["kernel"], "frac": roof["frac"]} if roof else None)
                 if roof and (worst is None or roof["frac"] < worst[0]["frac"]):
                     worst = (roof, kt, ab)
