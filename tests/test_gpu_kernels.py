@@ -245,3 +245,20 @@ def test_sort_segments_matches_oracle(rg, torch_cuda, rs, ks):
     DeviceOps().sort_segments(d, n, rg.RecordLayout(rs, ks), sizes, fb)
     torch_cuda.cuda.synchronize()
     assert np.array_equal(from_dev(d), oracle.stable_sort(part, rs, ks))
+
+
+def test_sort_segments_many_small_segments(rg, torch_cuda):
+    """Hundreds of small key-ordered segments (below the local-sort capacity,
+    some empty, some of one record), each from key byte 2."""
+    from paper_1612_02557_b200.distributed import DeviceOps
+    rs, ks, n = 16, 8, 200_000
+    a = make_input(n, rs, ks, 777)
+    r = a.reshape(n, rs)
+    pre = (r[:, 0].astype(np.int64) << 8) | r[:, 1]
+    order = np.argsort(pre, kind="stable")
+    part = r[order].reshape(-1).copy()
+    sizes = [int(c) for c in np.bincount(pre, minlength=65536)]  # ~3 records per 16-bit bucket
+    d = to_dev(torch_cuda, part)
+    DeviceOps().sort_segments(d, n, rg.RecordLayout(rs, ks), sizes, [2] * 65536)
+    torch_cuda.cuda.synchronize()
+    assert np.array_equal(from_dev(d), oracle.stable_sort(part, rs, ks))
