@@ -172,6 +172,21 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
     }
     __syncthreads();
     const uint32_t action = s_action;
+    if (action != 0 && g.size <= A.cap_local) {
+        // a segment that fits one local-sort group (only the caller-given
+        // segments of raduls_gpu_sort_segments are this small): sorted as one
+        // group from byte p, no scatter
+        if (tid == 0) {
+            Group gr;
+            gr.start = g.start;
+            gr.size = uint32_t(g.size);
+            gr.p = g.p;
+            gr.parity = g.parity;
+            gr.pad = 0;
+            A.groups[atomicAdd(&A.ctr->n_groups, 1u)] = gr;
+        }
+        return;
+    }
     if (action == 0) {  // all keys equal: finished where it lies
         if (g.parity) emit_copies(A, g.start, g.size, &s_base);
         return;
