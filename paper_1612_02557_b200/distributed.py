@@ -781,6 +781,21 @@ def _all_to_all(recv, send, out_splits, in_splits, group):
                            group=group)
 
 
+def _sort_received(ops, recv, n_out: int, layout: RecordLayout, plan: ExchangePlan, mine, tmp=None) -> int:
+    """Sort this rank's digit-major receive buffer: its digits, in key order,
+    are each one key range whose bytes before first_byte are equal — the
+    exchange was the first MSD level, so the sort continues from there
+    (raduls_gpu_sort_segments). Returns the number of segments."""
+    fb = plan.digits.first_byte
+    if fb is not None and hasattr(ops, "sort_segments") and len(mine) > 1:
+        ops.sort_segments(recv, n_out, layout, [c for _, c in mine], [int(fb[d]) for d, _ in mine], tmp)
+    elif tmp is not None:
+        ops.sort(recv, n_out, layout, tmp)
+    else:
+        ops.sort(recv, n_out, layout)
+    return len(mine)
+
+
 def sort_distributed(data, n: int, layout: RecordLayout, ops=None, group=None,
                      timings: dict | None = None, exchange: str | None = None):
     """Sort `n` local records (uint8 tensor on this rank's device) across the
@@ -792,8 +807,10 @@ def sort_distributed(data, n: int, layout: RecordLayout, ops=None, group=None,
     window over NVLink (CUDA IPC; raduls_gpu_partition_store_pieces) — the
     partition and the all-to-all are one kernel. The returned tensor then
     aliases this rank's cached window and stays valid until the next call on
-    the group. exchange="nccl": local partition by digit, then one NCCL
-    all_to_all_single (host-staged under gloo).
+    the group. exchange="nccl": local partition by digit, then one grouped
+    NCCL batch of per-piece sends and receives (_exchange_digit_major;
+    host-staged under gloo). Either way the receive buffer is digit-major,
+    so the local sort starts from the digits as pre-split segments.
 
     timings (optional dict) receives plan_s, exchange_ms (device time of the
     exchange: the fused partition kernel, or the all-to-all), partition_ms
@@ -858,16 +875,8 @@ def sort_distributed(data, n: int, layout: RecordLayout, ops=None, group=None,
         dist.barrier(group=group)  # every rank's stores into every window are complete
         t2 = time.perf_counter()
         recv = torch.as_tensor(_CudaBytes(win.own, max(n_out, 1) * rs), device=data.device)
-        tmp = ops.empty(max(n_out, 1) * rs)
-        # the window holds this rank's digits in key order, each one key range:
-        # the exchange was the first MSD level, the sort continues from there
-        mine = segments[rank]
-        fb = plan.digits.first_byte
-        info["segments"] = len(mine)
-        if fb is not None and hasattr(ops, "sort_segments") and len(mine) > 1:
-            ops.sort_segments(recv, n_out, layout, [c for _, c in mine], [int(fb[d]) for d, _ in mine], tmp)
-        else:
-            ops.sort(recv, n_out, layout, tmp)
+        info["segments"] = _sort_received(ops, recv, n_out, layout, plan, segments[rank],
+                                          ops.empty(max(n_out, 1) * rs))
     else:
         # local stable partition by digit (pieces of a digit stay in rank order)
         e0 = event()
@@ -885,13 +894,7 @@ def sort_distributed(data, n: int, layout: RecordLayout, ops=None, group=None,
         info["exchange_ms"] = elapsed(e2, e3)
         del send
         t2 = time.perf_counter()
-        mine = segments[rank]
-        fb = plan.digits.first_byte
-        info["segments"] = len(mine)
-        if fb is not None and hasattr(ops, "sort_segments") and len(mine) > 1:
-            ops.sort_segments(recv, n_out, layout, [c for _, c in mine], [int(fb[d]) for d, _ in mine])
-        else:
-            ops.sort(recv, n_out, layout)
+        info["segments"] = _sort_received(ops, recv, n_out, layout, plan, segments[rank])
     if cuda:
         torch.cuda.synchronize(data.device)
     t3 = time.perf_counter()
