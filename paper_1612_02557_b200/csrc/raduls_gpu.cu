@@ -2361,14 +2361,77 @@ int raduls_gpu_sort_multi(int n_dev, const int* devices, void* const* d_in, cons
     for (uint32_t g = 0; g < G; ++g)
         for (uint32_t b = 0; b < kPrefixBuckets; ++b) global[b] += hist[g][b];
     const std::vector<uint32_t> map = balanced_bucket_map_multi(global, G);
+    // digits: each device's bucket range, cut further where key byte p0
+    // changes as far as 256 digits allow (the lightest byte-p0 boundaries
+    // dropped first) — the exchange is then the first MSD level, and each
+    // device sorts its digits as pre-split segments (raduls_gpu_sort_segments)
+    std::vector<uint8_t> cut(kPrefixBuckets, 0);
+    uint32_t ncut = 0;
+    for (uint32_t bk = 1; bk < kPrefixBuckets; ++bk)
+        if (map[bk] != map[bk - 1]) cut[bk] = 1, ++ncut;
+    {
+        std::vector<uint32_t> cand;
+        for (uint32_t bk = 256; bk < kPrefixBuckets; bk += 256)
+            if (!cut[bk]) cand.push_back(bk);
+        const uint32_t budget = 255 - std::min<uint32_t>(ncut, 255);
+        if (cand.size() > budget) {
+            std::vector<double> blk(256, 0.0);
+            for (uint32_t bk = 0; bk < kPrefixBuckets; ++bk) blk[bk >> 8] += double(global[bk]);
+            std::stable_sort(cand.begin(), cand.end(), [&](uint32_t x, uint32_t y) {
+                return blk[(x >> 8) - 1] + blk[x >> 8] > blk[(y >> 8) - 1] + blk[y >> 8];
+            });
+            cand.resize(budget);
+        }
+        for (uint32_t bk : cand) cut[bk] = 1;
+    }
+    std::vector<uint32_t> digit(kPrefixBuckets, 0);
+    for (uint32_t bk = 1; bk < kPrefixBuckets; ++bk) digit[bk] = digit[bk - 1] + cut[bk];
+    const uint32_t D = digit[kPrefixBuckets - 1] + 1;
+    std::vector<uint32_t> drank(D, 0), dlo(D, kPrefixBuckets), dhi(D, 0);
+    for (uint32_t bk = 0; bk < kPrefixBuckets; ++bk) {
+        const uint32_t d = digit[bk];
+        drank[d] = map[bk];
+        dlo[d] = std::min(dlo[d], bk);
+        dhi[d] = std::max(dhi[d], bk);
+    }
+    std::vector<uint8_t> dfirst(D);
+    for (uint32_t d = 0; d < D; ++d) {
+        const uint32_t f = dlo[d] == dhi[d] ? p0 + 2 : (dlo[d] >> 8) == (dhi[d] >> 8) ? p0 + 1 : p0;
+        dfirst[d] = uint8_t(std::min(f, ks));
+    }
+    std::vector<std::vector<uint64_t>> dcnt(G, std::vector<uint64_t>(D, 0));  // [src][digit]
+    for (uint32_t g = 0; g < G; ++g)
+        for (uint32_t bk = 0; bk < kPrefixBuckets; ++bk) dcnt[g][digit[bk]] += hist[g][bk];
     std::vector<std::vector<uint64_t>> cnt(G, std::vector<uint64_t>(G, 0));  // [src][dst]
     for (uint32_t g = 0; g < G; ++g)
-        for (uint32_t b = 0; b < kPrefixBuckets; ++b) cnt[g][map[b]] += hist[g][b];
+        for (uint32_t d = 0; d < D; ++d) cnt[g][drank[d]] += dcnt[g][d];
     std::vector<uint64_t> recv(G, 0);
     for (uint32_t g = 0; g < G; ++g)
         for (uint32_t r = 0; r < G; ++r) recv[r] += cnt[g][r];
     for (uint32_t r = 0; r < G; ++r)
         if (recv[r] > out_capacity_recs || recv[r] > kMaxRecords) return RADULS_GPU_EINVAL;  // nothing written yet
+    // digit-major output: device r holds its digits in order, each digit's
+    // records source by source (the stable order); dat[g][d] = record offset
+    // of source g's run of digit d in d_out[drank[d]]
+    std::vector<std::vector<uint64_t>> dat(G, std::vector<uint64_t>(D, 0));
+    std::vector<std::vector<uint64_t>> seg_size(G);
+    std::vector<std::vector<uint8_t>> seg_first(G);
+    {
+        std::vector<uint64_t> pos(G, 0);
+        for (uint32_t d = 0; d < D; ++d) {
+            const uint32_t r = drank[d];
+            uint64_t tot = 0;
+            for (uint32_t g = 0; g < G; ++g) {
+                dat[g][d] = pos[r] + tot;
+                tot += dcnt[g][d];
+            }
+            pos[r] += tot;
+            if (tot) {
+                seg_size[r].push_back(tot);
+                seg_first[r].push_back(dfirst[d]);
+            }
+        }
+    }
     // 4. peer access between every pair of distinct devices (NVLink P2P)
     bool p2p = true;
     rc = guarded([&] {
@@ -2388,10 +2451,6 @@ int raduls_gpu_sort_multi(int n_dev, const int* devices, void* const* d_in, cons
             }
     });
     if (rc) return rc;
-    // destination of source g's range for device r: after the ranges of sources < g
-    std::vector<std::vector<uint64_t>> at(G, std::vector<uint64_t>(G, 0));
-    for (uint32_t r = 0; r < G; ++r)
-        for (uint32_t g = 1; g < G; ++g) at[g][r] = at[g - 1][r] + cnt[g - 1][r];
     // scratch per device (the partition output when P2P is missing; the local sort's tmp)
     std::vector<uint8_t*> part(G, nullptr);
     auto free_parts = [&] {
@@ -2413,25 +2472,25 @@ int raduls_gpu_sort_multi(int n_dev, const int* devices, void* const* d_in, cons
             if (!n_in[g]) return;
             uint32_t* d_map = nullptr;
             RG_CHECK(cudaMalloc(&d_map, kPrefixBuckets * sizeof(uint32_t)));
-            int r = cudaMemcpy(d_map, map.data(), kPrefixBuckets * sizeof(uint32_t), cudaMemcpyHostToDevice) ==
+            int r = cudaMemcpy(d_map, digit.data(), kPrefixBuckets * sizeof(uint32_t), cudaMemcpyHostToDevice) ==
                             cudaSuccess
                         ? int(RADULS_GPU_OK)
                         : int(RADULS_GPU_ECUDA);
-            std::vector<uint64_t> got(G, 0), dst(G, 0);
-            for (uint32_t q = 0; q < G; ++q)
-                dst[q] = reinterpret_cast<uint64_t>(static_cast<uint8_t*>(d_out[q]) + at[g][q] * rs);
+            std::vector<uint64_t> got(D, 0), dst(D, 0);
+            for (uint32_t d = 0; d < D; ++d)
+                dst[d] = reinterpret_cast<uint64_t>(static_cast<uint8_t*>(d_out[drank[d]]) + dat[g][d] * rs);
             if (!r) r = raduls_gpu_set_pivots(0, nullptr, nullptr, ks);  // whole buckets only here
             if (!r) {
                 if (p2p)
-                    r = raduls_gpu_partition_to(d_in[g], n_in[g], rs, ks, p0, d_map, G, dst.data(), got.data(),
+                    r = raduls_gpu_partition_to(d_in[g], n_in[g], rs, ks, p0, d_map, D, dst.data(), got.data(),
                                                 nullptr);
                 else
-                    r = raduls_gpu_partition(d_in[g], part[g], n_in[g], rs, ks, p0, d_map, G, got.data(), nullptr);
+                    r = raduls_gpu_partition(d_in[g], part[g], n_in[g], rs, ks, p0, d_map, D, got.data(), nullptr);
             }
             cudaFree(d_map);
             if (r) throw CudaError{r};
-            for (uint32_t q = 0; q < G; ++q)
-                if (got[q] != cnt[g][q]) throw CudaError{RADULS_GPU_EINTERNAL};
+            for (uint32_t d = 0; d < D; ++d)
+                if (got[d] != dcnt[g][d]) throw CudaError{RADULS_GPU_EINTERNAL};
             RG_CHECK(cudaDeviceSynchronize());  // peer stores complete before the sort reads them
         });
     });
@@ -2442,13 +2501,14 @@ int raduls_gpu_sort_multi(int n_dev, const int* devices, void* const* d_in, cons
                 RG_CHECK(cudaSetDevice(devices[g]));
                 RG_CHECK(cudaStreamCreateWithFlags(&st[g], cudaStreamNonBlocking));
             }
-            for (uint32_t g = 0; g < G; ++g) {
+            for (uint32_t g = 0; g < G; ++g) {  // the local partition is digit-ordered: one copy per run
                 uint64_t send = 0;
                 RG_CHECK(cudaSetDevice(devices[g]));
-                for (uint32_t r = 0; r < G; ++r) {
-                    const uint64_t k = cnt[g][r];
+                for (uint32_t d = 0; d < D; ++d) {
+                    const uint64_t k = dcnt[g][d];
+                    const uint32_t r = drank[d];
                     if (k)
-                        RG_CHECK(cudaMemcpyPeerAsync(static_cast<uint8_t*>(d_out[r]) + at[g][r] * rs, devices[r],
+                        RG_CHECK(cudaMemcpyPeerAsync(static_cast<uint8_t*>(d_out[r]) + dat[g][d] * rs, devices[r],
                                                      part[g] + send * rs, devices[g], k * rs, st[g]));
                     send += k;
                 }
@@ -2468,7 +2528,8 @@ int raduls_gpu_sort_multi(int n_dev, const int* devices, void* const* d_in, cons
     rc = run_per_device(n_dev, [&](int g) {
         if (cudaSetDevice(devices[g]) != cudaSuccess) return int(RADULS_GPU_ECUDA);
         n_out[g] = recv[g];
-        return raduls_gpu_sort(d_out[g], part[g], recv[g], rs, ks, nullptr);
+        return raduls_gpu_sort_segments(d_out[g], part[g], recv[g], rs, ks, uint32_t(seg_size[g].size()),
+                                        seg_size[g].data(), seg_first[g].data(), nullptr);
     });
     free_parts();
     (void)total;
