@@ -73,14 +73,20 @@ def balanced_bucket_map(global_hist: np.ndarray, world: int) -> np.ndarray:
     """Contiguous bucket ranges per rank, balanced by record count: bucket b
     goes to the rank whose ideal share [r*N/W, (r+1)*N/W) holds the bucket's
     midpoint. Monotone in b, so rank r receives a contiguous key range."""
-    h = global_hist.astype(np.float64)
-    total = h.sum()
+    h = np.asarray(global_hist, dtype=np.float64)
+    c = np.cumsum(h)
+    total = c[-1]
     if total == 0:
         return np.zeros(NBUCKETS, dtype=np.uint32)
-    before = np.cumsum(h) - h
-    mid = before + h / 2.0
-    r = np.floor(mid * world / total).astype(np.int64)
-    return np.clip(r, 0, world - 1).astype(np.uint32)
+    # mid = (prefix before b) + h_b / 2; rank = floor(mid * world / total),
+    # in place and in the same operation order as the C++ planner
+    c -= h
+    c += h / 2.0
+    c *= world
+    c /= total
+    r = c.astype(np.uint32)  # non-negative: truncation is floor
+    np.minimum(r, world - 1, out=r)
+    return r
 
 
 HOT_SHARE = 4  # a bucket with more than total / (HOT_SHARE * world) records is hot
@@ -148,8 +154,14 @@ def make_digits(weights: np.ndarray, world: int, p0: int = 0, split_hot: bool = 
             cand.sort(key=lambda b: -(blk[(b >> 8) - 1] + blk[b >> 8]))
             cand = cand[:max(budget, 0)]
         change[cand] = True
-    extra = 2 * (np.cumsum(piv) - piv)  # two more digits per earlier pivot bucket
-    digit = (np.cumsum(change) + extra).astype(np.uint32)
+    # digit of every bucket from the run lengths between cuts; two more digits
+    # per earlier pivot bucket (its equal and above parts)
+    cuts = np.flatnonzero(change)
+    lengths = np.diff(np.concatenate([[0], cuts, [NBUCKETS]]))
+    runs = np.arange(len(lengths), dtype=np.int64)
+    pruns = np.searchsorted(cuts, np.flatnonzero(piv), side="right")  # the run of each pivot bucket
+    run_digit = runs + 2 * np.searchsorted(pruns, runs, side="left")
+    digit = np.repeat(run_digit.astype(np.uint32), lengths)
     n_digits = int(digit[-1]) + 1 + (2 if piv[-1] else 0)
     if n_digits > 256:  # too many ranks for separate hot digits: whole buckets only
         return make_digits(weights, world, p0, split_hot=False, ks=ks, align=align)
