@@ -38,7 +38,8 @@ def _hot_input(data, n_local, rs, ks, rank, hot):
     data.view(n_local, rs)[sel, :ks] = key
 
 
-def _worker(rank, world, port, cfg, outdir, poke=False, exchange="p2p", hot=0.0, backend="gloo"):
+def _worker(rank, world, port, cfg, outdir, poke=False, exchange="p2p", hot=0.0, backend="gloo",
+            special=""):
     import json
 
     import torch
@@ -60,7 +61,11 @@ def _worker(rank, world, port, cfg, outdir, poke=False, exchange="p2p", hot=0.0,
     if rank == world - 1:
         n_local = n_total - base
     for step in range(2):  # the second step reuses the cached windows
-        data = rg.generate(n_local, lay, dist=dist_kind, seed=seed, index_base=base)
+        if special == "empty_rank1" and rank == 1:
+            n_local = 0
+        data = rg.generate(max(n_local, 1), lay, dist=dist_kind, seed=seed, index_base=base)
+        if special == "one_key":
+            data.view(-1, rs)[:, :ks] = 0x5C
         if hot:
             _hot_input(data, n_local, rs, ks, rank, hot)
         if poke and rank == world - 1:
@@ -68,7 +73,7 @@ def _worker(rank, world, port, cfg, outdir, poke=False, exchange="p2p", hot=0.0,
             # sample: the sampled plan's prefix byte is wrong, the exact
             # AND/OR from the partition's histogram catches it (exact re-plan)
             data[(n_local - 1) * rs] = 1
-        np.save(os.path.join(outdir, f"in{rank}.npy"), data.cpu().numpy())
+        np.save(os.path.join(outdir, f"in{rank}.npy"), data[:n_local * rs].cpu().numpy())
         tim = {}
         out, n_out = sort_distributed(data, n_local, lay, exchange=exchange, timings=tim)
         torch.cuda.synchronize()
@@ -85,7 +90,7 @@ def _run(tmp_path, world, cfg, **kw):
     port = _free_port()
     mp.start_processes(_worker, args=(world, port, cfg, str(tmp_path), kw.get("poke", False),
                                       kw.get("exchange", "p2p"), kw.get("hot", 0.0),
-                                      kw.get("backend", "gloo")),
+                                      kw.get("backend", "gloo"), kw.get("special", "")),
                        nprocs=world, join=True, start_method="spawn")
 
 
@@ -98,7 +103,7 @@ def _check(tmp_path, world, cfg):
     want = oracle.stable_sort(inputs, rs, ks)
     for step in range(2):
         got = np.concatenate([np.load(tmp_path / f"out{r}_{step}.npy") for r in range(world)])
-        assert got.size == n_total * rs
+        assert got.size == inputs.size
         assert np.array_equal(got, want), f"step {step}"
     return [json.load(open(tmp_path / f"tim{r}_1.json")) for r in range(world)], \
         [np.load(tmp_path / f"out{r}_1.npy").size // rs for r in range(world)]
@@ -214,3 +219,15 @@ def test_partition_pivot_digits_match_host(torch_cuda, rs, ks):
         assert np.array_equal(c2.astype(np.int64), counts.astype(np.int64))
     finally:
         ops.set_pivots(D.make_digits(w, 4, 0), ks)  # clear
+
+
+@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
+def test_distributed_empty_rank_and_one_key(torch_cuda, tmp_path, exchange):
+    """A rank with no records, and an input where every key is equal (one
+    single-key bucket holding everything: spread over the ranks by count)."""
+    cfg = (150_000, 16, 8, 0, 0x5EED0001)
+    _run(tmp_path, 3, cfg, exchange=exchange, special="empty_rank1")
+    _check(tmp_path, 3, cfg)
+    _run(tmp_path / "k", 3, cfg, exchange=exchange, special="one_key") if (tmp_path / "k").mkdir() is None else None
+    tim, n_out = _check(tmp_path / "k", 3, cfg)
+    assert max(n_out) <= cfg[0] / 3 + 16  # one key, balanced by count
