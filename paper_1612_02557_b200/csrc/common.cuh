@@ -182,10 +182,26 @@ __device__ __forceinline__ void st_smem_rec(uint8_t* s, uint32_t slot, const Rec
     store_rec<RS>(s, slot, r);
 }
 
+#ifndef RG_LD32_ALT
+#define RG_LD32_ALT 1
+#endif
 template <int RS>
 __device__ __forceinline__ Rec<RS> ld_smem_rec(const uint8_t* s, uint32_t slot) {
     Rec<RS> r;
     const uint8_t* p = s + size_t(slot) * RS;
+    if constexpr (RS == 32 && RG_LD32_ALT) {
+        // 32-B records: lanes of consecutive slots load the first half in
+        // groups of four and the second half in the next four, so each 16-B
+        // load instruction covers all eight 16-B bank groups of a quarter-warp
+        // (plain order: two-way conflicts at the 32-B stride)
+        const uint32_t h = (slot >> 2) & 1u;
+        const uint4 q0 = reinterpret_cast<const uint4*>(p)[h];
+        const uint4 q1 = reinterpret_cast<const uint4*>(p)[h ^ 1u];
+        const uint4 a = h ? q1 : q0, b = h ? q0 : q1;
+        r.w[0] = a.x, r.w[1] = a.y, r.w[2] = a.z, r.w[3] = a.w;
+        r.w[4] = b.x, r.w[5] = b.y, r.w[6] = b.z, r.w[7] = b.w;
+        return r;
+    }
     if constexpr (RS % 16 == 0) {
 #pragma unroll
         for (int v = 0; v < RS / 16; ++v) {
