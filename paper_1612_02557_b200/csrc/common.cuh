@@ -185,11 +185,11 @@ __device__ __forceinline__ void st_smem_rec(uint8_t* s, uint32_t slot, const Rec
 #ifndef RG_LD32_ALT
 #define RG_LD32_ALT 1
 #endif
-template <int RS>
+template <int RS, bool kAlt = true>
 __device__ __forceinline__ Rec<RS> ld_smem_rec(const uint8_t* s, uint32_t slot) {
     Rec<RS> r;
     const uint8_t* p = s + size_t(slot) * RS;
-    if constexpr (RS == 32 && RG_LD32_ALT) {
+    if constexpr (RS == 32 && RG_LD32_ALT && kAlt) {
         // 32-B records: lanes of consecutive slots load the first half in
         // groups of four and the second half in the next four, so each 16-B
         // load instruction covers all eight 16-B bank groups of a quarter-warp

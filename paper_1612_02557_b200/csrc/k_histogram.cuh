@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(HistCfg<RS>::kThreads + 64, HistCfg<RS>::kCtas
             const uint32_t i = uint32_t(warp * IT + j) * 32u + lane;  // warp-striped
             const bool valid = i < tn;
             Rec<RS> r;
-            if (valid) r = ld_smem_rec<RS>(tile, i);
+            if (valid) r = ld_smem_rec<RS, false>(tile, i);  // (the half-swapped order measured +4% here)
             else
 #pragma unroll
                 for (int q = 0; q < Rec<RS>::kWords; ++q) r.w[q] = 0;
