@@ -18,3 +18,4 @@ for K in k_local k_scatter; do
   ncu -i gpurun_out/ev_full_$K.ncu-rep --page source --csv --print-source sass > gpurun_out/ev_full_${K}_sass.csv 2>&1
 done
 rm -f gpurun_out/*.ncu-rep
+python scripts/traffic_from_launches.py gpurun_out/ev_launches_bench_c5.csv > gpurun_out/ev_ncu_traffic_c5.json 2>&1
