@@ -315,7 +315,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-per-config", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-cap", type=int, default=0,
                     help="records of the reference run (0: the whole config when host RAM allows)")
     ap.add_argument("--exchange", default="both", choices=["both", "p2p", "nccl"])
@@ -548,16 +548,6 @@ def main():
             except Exception as ex:  # noqa: BLE001
                 per_config[name] = {"error": str(ex)[:200]}
 
-    # ---------------- CPU baseline (rank 0, N=1): the reference sorter on the host cores
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            r = run_cpu_reference(args.config, args.cpu_cap or reference_cap(args.config), 1, 0)
-            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "same_config")}
-        except Exception as ex:  # noqa: BLE001
-            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
-                   "sample": str(ex)[:200]}
-
     # ---------------- e2e through the host-memory drop-in
     e2e = None
     if not args.no_e2e:
@@ -574,6 +564,16 @@ def main():
                 e2e["cached_buffers"] = {"value": c.get("value"), "ms_per_step": c.get("ms_per_step")}
             finally:
                 rg.set_host_cache(False)
+
+    # ---------------- CPU baseline (rank 0, N=1): the reference sorter on the host cores
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            r = run_cpu_reference(args.config, args.cpu_cap or reference_cap(args.config), 1, 0)
+            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "same_config")}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
+                   "sample": str(ex)[:200]}
 
     if rank == 0:
         line = {
