@@ -102,6 +102,8 @@ typedef struct {
     uint64_t skipped_levels;    /* segment-levels skipped as constant digits (e) */
     uint64_t hist_digit_records; /* records histogrammed from the digit array (1 byte each; the
                                     scatter before wrote that byte) instead of from the records */
+    uint64_t bitmap_spill_groups; /* local-sort groups the bitmap sort handed to the bucket sort
+                                     (duplicate-heavy or clustered keys) */
 } raduls_gpu_stats;
 
 int raduls_gpu_last_stats(raduls_gpu_stats* out);

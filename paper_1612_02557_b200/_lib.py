@@ -71,6 +71,7 @@ class Stats(C.Structure):
         ("fallback_groups", C.c_uint64),
         ("skipped_levels", C.c_uint64),
         ("hist_digit_records", C.c_uint64),
+        ("bitmap_spill_groups", C.c_uint64),
     ]
 
     def as_dict(self) -> dict:

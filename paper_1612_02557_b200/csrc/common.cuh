@@ -622,7 +622,7 @@ struct LevelCounters {
     unsigned long long hist_records;     // records read by this level's tile histogram
     unsigned long long hist_digit_records;  // records histogrammed from the digit array (1 byte each)
     uint32_t n_skip;                     // segments re-queued at a later byte without a split
-    uint32_t pad;
+    uint32_t bm_spill;                   // groups the bitmap local sort handed to the bucket sort
 };
 
 // Decoupled look-back status word: [63:62] flag, [61:0] value.

@@ -1,0 +1,414 @@
+// (d) small-bin sort, bitmap form: the first-line local sort for records held
+// in shared memory (16/24/32 B). Same contract as local_group (k_local.cuh):
+// one CTA sorts one group of <= kCap records that share key bytes [0, p), by
+// key bytes [p, ks), stable, straight into `data`, safe in place.
+//
+// Reference: the tiny-bin sorts (P/include/raduls/small_sorts.hpp:48-191) and
+// finalize() (P/include/raduls/detail/msd_sorter.hpp:76-80).
+//
+// The bucket sort of k_local.cuh spends ~150 of its ~247 thread instructions
+// per record on putting record ids into bucket order and ranking every record
+// against its bucket's neighbours (dependent shared-memory loads). Here the
+// 32-bit key window of every record is mapped linearly (monotone) onto a fine
+// grid of ~64 n cells, one BIT per cell:
+//   * histogram: one atomicOr per record sets its cell's bit. A record that
+//     finds the bit already set (two records in one cell: ~1.6% of random
+//     records) bumps a u16 counter of its 32-cell bitmap word;
+//   * scan: warp-cooperative prefix sum over the words of popc(word) + counter,
+//     the word's start stored as a u16 with bit 15 = "this word holds a
+//     shared cell" (a dirty word);
+//   * rank: a record of a clean word is final at start + popc(bits below its
+//     own) -- two independent shared-memory loads, no neighbour to compare
+//     with, no id scatter -- and is stored to its place at once. Records of
+//     dirty words (all of them, ~3%) go to a short list and are ranked densely
+//     against the list's entries of the same word by (window, key bytes beyond
+//     the window, input index).
+// A group whose dirty records outgrow the list (duplicate-heavy or clustered
+// keys) is handed untouched -- nothing has been written by then -- to the
+// bucket sort (k_local_list below), which may hand it on to the LSD fallback.
+#pragma once
+
+#include "k_local.cuh"
+
+namespace rg {
+
+template <int RS>
+struct BmCfg {
+    using L = LocalCfg<RS>;
+    static_assert(!L::kRegRecords, "shared-memory records only");
+    static constexpr int kThreads = L::kThreads;
+    static constexpr int kMinBlocks = L::kMinBlocks;
+    static constexpr int kWarps = kThreads / 32;
+    static constexpr int kCap = L::kCap;
+    static constexpr int kIpt = L::kIpt;
+    // cells = 2^kFineBits at most: >= 32 per record at a full group
+#ifndef RG_BM_BITS
+#define RG_BM_BITS 0
+#endif
+    static constexpr int kFineBits = RG_BM_BITS ? RG_BM_BITS : (RS == 32 ? 18 : 17);
+    // cells per record aimed at, as a power of two (FB = ceil(log2 n) + kCellLog)
+#ifndef RG_BM_CELL_LOG
+#define RG_BM_CELL_LOG 5
+#endif
+    static constexpr int kCellLog = RG_BM_CELL_LOG;
+    static constexpr int kWords = 1 << (kFineBits - 5);
+    // scan: every warp owns kRows rows of 128 words
+    static constexpr int kRows = kWords / (128 * kWarps) > 0 ? kWords / (128 * kWarps) : 1;
+    static_assert(kRows == 1 || kRows == 2 || kRows == 4, "scan rows per warp");
+    static constexpr int kDirty = 1024;  // records of dirty words (u32 entries)
+    static constexpr int kDw = 512;      // dirty words (8-B descriptors)
+    static constexpr int kRecBytes = L::kRecBytes;
+    static constexpr size_t kSmem =
+        size_t(kRecBytes) + size_t(kWords) * 6 + size_t(kDirty) * 4 + size_t(kDw) * 8;
+};
+
+template <int RS, typename Mid>
+__device__ __forceinline__ void local_group_bm(
+    uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group g, uint32_t ks,
+    LevelCounters* __restrict__ ctr, Group* __restrict__ spill, unsigned int* __restrict__ n_spill,
+    uint32_t spill_cap, Mid&& mid) {
+    using C = BmCfg<RS>;
+    constexpr int T = C::kThreads, W = C::kWarps, IPT = C::kIpt, R = C::kRows;
+    extern __shared__ __align__(128) uint8_t smem[];
+    RG_CHK_POISON_SMEM(smem);
+    uint32_t* bm = reinterpret_cast<uint32_t*>(smem + C::kRecBytes);  // [kWords] cell bits
+    uint32_t* pre = bm + C::kWords;                                   // [kWords] u16: extras, then starts
+    uint2* dw = reinterpret_cast<uint2*>(pre + C::kWords / 2);        // [kDw] {start | cnt << 16, off | cursor << 16}
+    uint32_t* dl = reinterpret_cast<uint32_t*>(dw + C::kDw);          // [kDirty] e | dirty word id << 16
+    __shared__ uint32_t s_scan[W];
+    __shared__ uint32_t s_wmin, s_wmax, s_alloc, s_crowd;
+    __shared__ __align__(8) unsigned long long s_bar;
+
+    const uint32_t n = g.size;
+    const uint8_t* gsrc = (g.parity ? tmp : data) + g.start * RS;
+    uint8_t* dst = data + g.start * RS;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t klim = ks < uint32_t(RS) ? ks : uint32_t(RS);
+    if (n <= 1 || g.p >= klim) {  // nothing to order (no key byte left: the input order stands)
+        if (g.parity)
+            for (uint32_t e = threadIdx.x; e < n; e += T) store_rec<RS>(dst, e, load_rec<RS>(gsrc, e));
+        return;
+    }
+
+    // ---- 1. the group on chip (TMA), bitmap and counters zeroed meanwhile
+    const uint32_t head = uint32_t(reinterpret_cast<uintptr_t>(gsrc) & 15u);
+    const uint8_t* recs = smem + head;
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar, 1);
+        fence_mbar_init();
+        const uint32_t bytes = n * RS;
+        const uint32_t hb = head ? min(8u, bytes) : 0u;
+        const uint32_t body = (bytes - hb) & ~15u;
+        const uint32_t tail = bytes - hb - body;
+        if (hb) *reinterpret_cast<uint2*>(smem + head) = *reinterpret_cast<const uint2*>(gsrc);
+        if (tail)
+            *reinterpret_cast<uint2*>(smem + head + hb + body) =
+                *reinterpret_cast<const uint2*>(gsrc + hb + body);
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&s_bar, body);
+        for (uint32_t o = 0; o < body; o += 32768u)
+            tma_load_1d_h<RG_HINT_LOCAL>(smem + head + hb + o, gsrc + hb + o, min(32768u, body - o), &s_bar);
+        s_wmin = 0xFFFFFFFFu;
+        s_wmax = 0u;
+        s_alloc = 0;
+        s_crowd = 0;
+    }
+    // cells: 2^FB, ~2^kCellLog per record; at least one warp's scan span
+    uint32_t FB = 32u + uint32_t(C::kCellLog) - __clz(n - 1);  // ceil(log2 n) + kCellLog (n >= 2)
+    constexpr uint32_t kMinFB = R == 1 ? 12 : R == 2 ? 13 : 14;  // 128 R words
+    FB = FB < kMinFB ? kMinFB : (FB > uint32_t(C::kFineBits) ? uint32_t(C::kFineBits) : FB);
+    const uint32_t nW = 1u << (FB - 5);  // a multiple of 128 R
+    {
+        // bm and pre are adjacent: [0, nW) words of bm, then [0, nW / 2) words of pre
+        uint4* z = reinterpret_cast<uint4*>(bm);
+#pragma unroll
+        for (int q = 0; q < C::kWords / 4 / T; ++q)
+            if (q * T + threadIdx.x < nW / 4) z[q * T + threadIdx.x] = make_uint4(0, 0, 0, 0);
+        if constexpr (C::kWords / 4 < T)
+            if (threadIdx.x < nW / 4) z[threadIdx.x] = make_uint4(0, 0, 0, 0);
+        uint4* z2 = reinterpret_cast<uint4*>(pre);
+#pragma unroll
+        for (int q = 0; q < (C::kWords / 8 + T - 1) / T; ++q)
+            if (q * T + threadIdx.x < nW / 8) z2[q * T + threadIdx.x] = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+    mbar_wait(&s_bar, 0);
+
+    // ---- 2. windows: key bytes p..p+3 (fewer at the key's end), big-endian,
+    // one byte permute per record; their range. No search for the varying
+    // bytes: a window holding constant bytes only loses resolution, and a
+    // group it cannot resolve is handed to the bucket sort
+    const uint32_t nwin = klim - g.p < 4u ? klim - g.p : 4u;
+    const bool beyond = g.p + 4u < klim;
+    uint32_t Ldef[4] = {g.p, g.p + 1, g.p + 2, g.p + 3};
+    const WindowSel ws = make_window_sel(Ldef, nwin, RS / 4, false);
+    uint32_t wv[IPT];
+    {
+        uint32_t smn = 0xFFFFFFFFu, smx = 0u;
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            if (uint32_t(j) * T >= n) break;  // block-uniform
+            const uint32_t e = uint32_t(j) * T + threadIdx.x;
+            if (e < n) {
+                const uint32_t w = rec_window<RS>(ld_smem_rec<RS>(recs, e), ws);
+                wv[j] = w;
+                smn = min(smn, w);
+                smx = max(smx, w);
+            }
+        }
+        smn = __reduce_min_sync(0xFFFFFFFFu, smn);
+        smx = __reduce_max_sync(0xFFFFFFFFu, smx);
+        if (lane == 0) {
+            atomicMin(&s_wmin, smn);
+            atomicMax(&s_wmax, smx);
+        }
+    }
+    __syncthreads();
+    // cell = umulhi(w - wmin, mul): monotone in w and < 2^FB (mul rounded down
+    // with a 1e-6 margin over the float error; k_local.cuh's bucket geometry)
+    const uint32_t ncell = 1u << FB;
+    const uint32_t wmin = s_wmin;
+    const uint32_t rm1 = s_wmax - wmin;  // range - 1
+    if (rm1 == 0 && !beyond) {           // every key equal: stable order is the input order
+        if (g.parity) {
+#pragma unroll
+            for (int j = 0; j < IPT; ++j) {
+                if (uint32_t(j) * T >= n) break;
+                const uint32_t e = uint32_t(j) * T + threadIdx.x;
+                if (e < n) store_rec<RS>(dst, e, ld_smem_rec<RS>(recs, e));
+            }
+        }
+        return;
+    }
+    const uint32_t mul =
+        rm1 < ncell ? 0u : uint32_t(__fdiv_rz(float(ncell) * 4294967296.0f, float(rm1) + 1.0f) * 0.999999f);
+
+    mid();
+    // ---- 3. one bit per occupied cell; a record finding its cell taken counts
+    // itself in the word's extras (u16 halves of pre)
+    uint32_t fc[IPT];
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        if (uint32_t(j) * T >= n) break;
+        const uint32_t e = uint32_t(j) * T + threadIdx.x;
+        if (e < n) {
+            const uint32_t d = wv[j] - wmin;
+            const uint32_t f = mul ? __umulhi(d, mul) : d;
+            fc[j] = f;
+            const uint32_t bit = 1u << (f & 31u);
+            const uint32_t old = atomicOr(&bm[f >> 5], bit);
+            if (old & bit) atomicAdd(&pre[f >> 6], 1u << ((f >> 1) & 16u));
+        }
+    }
+    __syncthreads();
+
+    // ---- 4. scan over the words of popc(word) + extras. Warp q owns words
+    // [128 R q, 128 R (q + 1)) as R rows of 128; lane l reads words 4 l..4 l + 3
+    // of each row (conflict-free 16-B / 8-B loads); row sums are scanned across
+    // the lanes two rows to a register (u16 halves: sums <= n < 32768). A word
+    // with extras (a shared cell) is dirty: it gets a descriptor {start, count,
+    // first list entry} and its start entry holds 0x8000 | descriptor id.
+    {
+        const bool active = uint32_t(warp) * (128u * R) < nW;
+        const uint4* bm4 = reinterpret_cast<const uint4*>(bm) + warp * (32 * R);
+        uint2* pre2 = reinterpret_cast<uint2*>(pre) + warp * (32 * R);
+        uint32_t sv[R];
+#pragma unroll
+        for (int v = 0; v < R; ++v) {
+            sv[v] = 0;
+            if (active) {
+                const uint4 a = bm4[v * 32 + lane];
+                const uint2 x = pre2[v * 32 + lane];
+                uint32_t s = __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
+                if (x.x | x.y) s += (x.x & 0xFFFFu) + (x.x >> 16) + (x.y & 0xFFFFu) + (x.y >> 16);
+                sv[v] = s;
+            }
+        }
+        constexpr int NP = (R + 1) / 2;
+        uint32_t pk[NP], ik[NP];
+#pragma unroll
+        for (int q = 0; q < NP; ++q) ik[q] = pk[q] = sv[2 * q] | ((2 * q + 1 < R ? sv[2 * q + 1 < R ? 2 * q + 1 : 0] : 0u) << 16);
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, ik[q], off);
+                if (lane >= off) ik[q] += y;
+            }
+        }
+        uint32_t tk[NP], wtot = 0;
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            tk[q] = __shfl_sync(0xFFFFFFFFu, ik[q], 31);
+            wtot += (tk[q] & 0xFFFFu) + (tk[q] >> 16);
+        }
+        if (lane == 0) s_scan[warp] = wtot;
+        __syncthreads();
+        const uint32_t t = lane < W ? s_scan[lane] : 0u;
+        uint32_t rowb = __reduce_add_sync(0xFFFFFFFFu, lane < warp ? t : 0u);
+        if (active) {
+#pragma unroll
+            for (int v = 0; v < R; ++v) {
+                const uint32_t exl = ik[v / 2] - pk[v / 2];  // exclusive over the lanes, per row
+                const uint32_t ex = (v & 1) ? (exl >> 16) : (exl & 0xFFFFu);
+                const uint32_t rt = (v & 1) ? (tk[v / 2] >> 16) : (tk[v / 2] & 0xFFFFu);
+                const uint4 a = bm4[v * 32 + lane];
+                const uint2 x = pre2[v * 32 + lane];
+                const uint32_t c0 = __popc(a.x), c1 = __popc(a.y), c2 = __popc(a.z);
+                uint32_t r0 = rowb + ex, r1 = r0 + c0, r2 = r1 + c1, r3 = r2 + c2;
+                if (x.x | x.y) {  // rare: a dirty word among the four
+                    const uint32_t e0 = x.x & 0xFFFFu, e1 = x.x >> 16, e2 = x.y & 0xFFFFu, e3 = x.y >> 16;
+                    r1 += e0;
+                    r2 += e0 + e1;
+                    r3 += e0 + e1 + e2;
+                    auto dirty = [&](uint32_t start, uint32_t cnt) -> uint32_t {
+                        const uint32_t old = atomicAdd(&s_alloc, cnt | 0x10000u);
+                        const uint32_t id = old >> 16, off = old & 0xFFFFu;
+                        if (id < uint32_t(C::kDw)) dw[id] = make_uint2(start | (cnt << 16), off);
+                        if (cnt > kMaxBucket) s_crowd = 1;  // duplicate-heavy: not for the quadratic ranking
+                        return 0x8000u | (id & 0x7FFFu);
+                    };
+                    if (e0) r0 = dirty(r0, c0 + e0);
+                    if (e1) r1 = dirty(r1, c1 + e1);
+                    if (e2) r2 = dirty(r2, c2 + e2);
+                    if (e3) r3 = dirty(r3, __popc(a.w) + e3);
+                }
+                pre2[v * 32 + lane] = make_uint2(r0 | (r1 << 16), r2 | (r3 << 16));
+                rowb += rt;
+            }
+        }
+    }
+    __syncthreads();
+    const uint32_t nd = s_alloc & 0xFFFFu, ndw = s_alloc >> 16;
+    if (nd > uint32_t(C::kDirty) || ndw > uint32_t(C::kDw) || s_crowd) {
+        // block-uniform; nothing written yet: the bucket sort takes the group
+        if (threadIdx.x == 0) {
+            const uint32_t i = atomicAdd(n_spill, 1u);
+            if (i < spill_cap) spill[i] = g;
+            atomicAdd(&ctr->bm_spill, 1u);
+        }
+        return;
+    }
+
+    // ---- 5. clean words: final position = the word's start + bits below the
+    // record's own; stored at once (one uncoalesced vector store per record,
+    // the group's lines complete in L2). Dirty words: into the word's list run.
+    const uint16_t* pre16 = reinterpret_cast<const uint16_t*>(pre);
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        if (uint32_t(j) * T >= n) break;
+        const uint32_t e = uint32_t(j) * T + threadIdx.x;
+        if (e < n) {
+            const uint32_t f = fc[j], word = f >> 5;
+            const uint32_t pv = pre16[word];
+            const uint32_t m = bm[word];
+            if (pv < 0x8000u) {
+                const uint32_t pos = pv + __popc(m & ((1u << (f & 31u)) - 1u));
+                store_rec<RS>(dst, pos, ld_smem_rec<RS>(recs, e));
+            } else {
+                const uint32_t id = pv & 0x7FFFu;
+                const uint32_t old = atomicAdd(&dw[id].y, 0x10000u);
+                dl[(old & 0xFFFFu) + (old >> 16)] = e | (id << 16);
+            }
+        }
+    }
+    if (nd == 0) {
+        if (threadIdx.x == 0) atomicAdd(&ctr->moved_local, (unsigned long long)n);
+        return;
+    }
+    __syncthreads();
+    // ---- 6. dirty words, densely from the list: each entry ranks itself
+    // among its word's run by (window, key bytes beyond the window, input index)
+    {
+        auto window_of = [&](uint32_t e) { return rec_window<RS>(ld_smem_rec<RS>(recs, e), ws); };
+        auto cmp_rest = [&](uint32_t a, uint32_t b) -> int {
+            for (uint32_t q = g.p + 4u; q < klim; ++q) {
+                const uint32_t x = recs[size_t(a) * RS + q], y = recs[size_t(b) * RS + q];
+                if (x != y) return x < y ? -1 : 1;
+            }
+            return 0;
+        };
+        for (uint32_t i = threadIdx.x; i < nd; i += T) {
+            const uint32_t me = dl[i];
+            const uint32_t e = me & 0xFFFFu;
+            const uint2 d = dw[me >> 16];
+            const uint32_t start = d.x & 0xFFFFu, cnt = d.x >> 16, off = d.y & 0xFFFFu;
+            const uint32_t w = window_of(e);
+            uint32_t rank = 0;
+            for (uint32_t q = off; q < off + cnt; ++q) {
+                if (q == i) continue;
+                const uint32_t e2 = dl[q] & 0xFFFFu;
+                const uint32_t w2 = window_of(e2);
+                bool lt;
+                if (w2 != w) {
+                    lt = w2 < w;
+                } else {
+                    const int c = beyond ? cmp_rest(e2, e) : 0;
+                    lt = c < 0 || (c == 0 && e2 < e);
+                }
+                rank += lt;
+            }
+            store_rec<RS>(dst, start + rank, ld_smem_rec<RS>(recs, e));
+        }
+    }
+    if (threadIdx.x == 0) atomicAdd(&ctr->moved_local, (unsigned long long)n);
+}
+
+// Bitmap local sort launch: the shapes of k_local (two CTAs per SM: a CTA per
+// group, the group one resident wave ahead prefetched into L2; one CTA per
+// SM: persistent, groups round-robin, next descriptor by cp.async).
+template <int RS>
+__global__ void __launch_bounds__(BmCfg<RS>::kThreads, BmCfg<RS>::kMinBlocks) k_local_bm(
+    uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group* __restrict__ groups,
+    uint32_t n_groups, uint32_t ks, LevelCounters* __restrict__ ctr, Group* __restrict__ spill,
+    unsigned int* __restrict__ n_spill, uint32_t spill_cap, uint32_t ahead) {
+    if constexpr (BmCfg<RS>::kMinBlocks > 1) {
+        if (threadIdx.x == 0 && blockIdx.x + ahead < n_groups)
+            prefetch_group_l2<RS>(data, tmp, groups[blockIdx.x + ahead]);
+        local_group_bm<RS>(data, tmp, groups[blockIdx.x], ks, ctr, spill, n_spill, spill_cap, [] {});
+        return;
+    }
+    __shared__ __align__(16) Group s_g[2];
+    uint32_t i = blockIdx.x;
+    if (i >= n_groups) return;
+    if (threadIdx.x == 0) s_g[0] = groups[i];
+    __syncthreads();
+    for (int buf = 0; i < n_groups; buf ^= 1) {
+        const uint32_t nx = i + gridDim.x;
+        const bool more = nx < n_groups;
+        if (threadIdx.x == 0 && more) {
+            for (int q = 0; q < int(sizeof(Group) / 8); ++q)
+                cp_async8(reinterpret_cast<uint8_t*>(&s_g[buf ^ 1]) + 8 * q,
+                          reinterpret_cast<const uint8_t*>(&groups[nx]) + 8 * q);
+        }
+        const Group g = s_g[buf];
+        auto mid = [&] {
+            if (threadIdx.x == 0 && more) {
+                cp_async_wait_all();
+                prefetch_group_l2<RS>(data, tmp, s_g[buf ^ 1]);
+            }
+        };
+        local_group_bm<RS>(data, tmp, g, ks, ctr, spill, n_spill, spill_cap, mid);
+        if (threadIdx.x == 0 && more) cp_async_wait_all();
+        __syncthreads();
+        i = nx;
+    }
+}
+
+// The bucket sort (local_group) over a device-counted list: the groups the
+// bitmap sort handed over. Launched right behind k_local_bm with a fixed grid
+// (no host read of the count); CTAs walk the list with the grid's stride.
+template <int RS>
+__global__ void __launch_bounds__(LocalCfg<RS>::kThreads, LocalCfg<RS>::kMinBlocks) k_local_list(
+    uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group* __restrict__ list,
+    const unsigned int* __restrict__ n_list, uint32_t list_cap, uint32_t ks,
+    LevelCounters* __restrict__ ctr, Group* __restrict__ spill, unsigned int* __restrict__ n_spill,
+    uint32_t spill_cap) {
+    const uint32_t n = min(*n_list, list_cap);
+    for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+        local_group<RS, false>(data, tmp, list[i], ks, ctr, spill, n_spill, spill_cap, [] {});
+        __syncthreads();  // shared memory free for the next group
+    }
+}
+
+}  // namespace rg

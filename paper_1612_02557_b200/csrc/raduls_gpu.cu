@@ -40,6 +40,7 @@
 #include "common.cuh"
 #include "k_histogram.cuh"
 #include "k_local.cuh"
+#include "k_local_bm.cuh"
 #include "k_partition.cuh"
 #include "k_plan.cuh"
 #include "k_scan.cuh"
@@ -523,8 +524,8 @@ struct Workspace {
     DevBuf<uint16_t> tile_cnt;
     DevBuf<uint32_t> tile_off;
     DevBuf<unsigned long long> status;
-    DevBuf<Group> groups, spill;
-    DevBuf<unsigned int> n_spill;
+    DevBuf<Group> groups, spill, spill_bm;
+    DevBuf<unsigned int> n_spill;  // [0]: groups for the LSD fallback, [1]: groups the bitmap sort handed over
     DevBuf<CopyRange> copies;
     HostDevBuf host_data, host_tmp;
     DevBuf<uint8_t> map8;
@@ -636,6 +637,7 @@ void ensure_caps(Workspace& ws, uint64_t n, uint64_t extra_segs = 0) {
     ws.status.ensure((c.tiles / kScanChunk + 1) * kRadix);
     ws.groups.ensure(c.groups);
     ws.spill.ensure(c.groups);
+    if constexpr (RS != 8) ws.spill_bm.ensure(c.groups);
     ws.n_spill.ensure(2);  // (read back as one 8-B word)
     ws.copies.ensure(c.copies);
 }
@@ -647,6 +649,12 @@ void set_attrs(Workspace& ws) {
                                   int(LocalCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_local<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(LocalCfg<RS>::kSmem)));
+    if constexpr (RS != 8) {
+        RG_CHECK(cudaFuncSetAttribute(k_local_bm<RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(BmCfg<RS>::kSmem)));
+        RG_CHECK(cudaFuncSetAttribute(k_local_list<RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(LocalCfg<RS>::kSmem)));
+    }
     RG_CHECK(cudaFuncSetAttribute(k_tile_hist<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(HistCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_tile_hist<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -758,6 +766,17 @@ void launch_scatter(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_
     ws.prof.end(pe, st);
 }
 
+// RADULS_GPU_LOCAL=bucket: the bucket sort alone (k_local.cuh) for every group,
+// as before the bitmap sort existed (tests and A/B).
+#ifndef RG_LOC_BM
+#define RG_LOC_BM 1
+#endif
+bool bitmap_local() {
+    if (!RG_LOC_BM) return false;
+    const char* e = std::getenv("RADULS_GPU_LOCAL");
+    return !(e && std::strcmp(e, "bucket") == 0);
+}
+
 // Launch the local sort over `ngroups` groups already in ws.groups.
 template <int RS>
 void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, uint32_t ks,
@@ -767,6 +786,27 @@ void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, 
     // one CTA per SM: persistent, groups round-robin; two per SM: a CTA per group
     const uint32_t grid = LocalCfg<RS>::kMinBlocks == 1 ? std::min<uint32_t>(ngroups, uint32_t(sm_count()))
                                                        : ngroups;
+    if constexpr (RS != 8) {
+        if (bitmap_local()) {
+            // the bitmap sort first; the groups it hands over (device-counted
+            // list) go to the bucket sort right behind it, no host read between
+            RG_CHECK(cudaMemsetAsync(ws.n_spill.p + 1, 0, sizeof(unsigned int), st));
+            k_local_bm<RS><<<grid, BmCfg<RS>::kThreads, BmCfg<RS>::kSmem, st>>>(
+                data, tmp, ws.groups.p, ngroups, ks, ctr, ws.spill_bm.p, ws.n_spill.p + 1,
+                uint32_t(ws.spill_bm.cap), uint32_t(sm_count()) * BmCfg<RS>::kMinBlocks);
+            note_launch();
+            RG_LAUNCH_CHECK();
+            const uint32_t lgrid =
+                std::min<uint32_t>(ngroups, uint32_t(sm_count()) * LocalCfg<RS>::kMinBlocks);
+            k_local_list<RS><<<lgrid, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
+                data, tmp, ws.spill_bm.p, ws.n_spill.p + 1, uint32_t(ws.spill_bm.cap), ks, ctr, ws.spill.p,
+                ws.n_spill.p, uint32_t(ws.spill.cap));
+            note_launch();
+            RG_LAUNCH_CHECK();
+            ws.prof.end(pe, st);
+            return;
+        }
+    }
     k_local<RS, false><<<grid, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
         data, tmp, ws.groups.p, ngroups, ks, ctr, ws.spill.p, ws.n_spill.p, uint32_t(ws.spill.cap),
         uint32_t(sm_count()) * LocalCfg<RS>::kMinBlocks);
@@ -872,7 +912,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
     set_attrs<RS>(ws);
     ensure_caps<RS>(ws, n, seeds ? seeds->size() : 0);
     LevelCounters* dctr = ws.ctr.p;
-    RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, sizeof(unsigned int), st));
+    RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, 2 * sizeof(unsigned int), st));
     RG_CHK_RANGES(st, {{data, size_t(n) * RS}, {tmp, size_t(n) * RS}});
 #ifdef RG_CHECKED
     {  // poison the scratch: nothing may be read before this sort writes it
@@ -897,6 +937,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         stats.levels = 1;
         stats.local_records = ws.h_ctr[0].moved_local;
         stats.fallback_groups = ws.h_ctr[0].fallback_groups;
+        stats.bitmap_spill_groups = ws.h_ctr[0].bm_spill;
         ws.last = stats;
         return;
     }
@@ -1067,6 +1108,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         for (uint32_t l = l0; l < l1; ++l) {
             stats.local_records += ws.h_ctr[l].moved_local;
             stats.fallback_groups += ws.h_ctr[l].fallback_groups;
+            stats.bitmap_spill_groups += ws.h_ctr[l].bm_spill;
             stats.hist_records += ws.h_ctr[l].hist_records;
             stats.hist_digit_records += ws.h_ctr[l].hist_digit_records;
         }
@@ -1085,7 +1127,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         const bool split = levels == 1 && nseg >= 2 && !last_skip && ws.h_ctr[0].n_scatter_segs == 1;
         read_counters_and_finish<RS>(ws, data, tmp, ks, dctr, 1, st);
         add_level_stats(0, 1);
-        RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, sizeof(unsigned int), st));
+        RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, 2 * sizeof(unsigned int), st));
         if (!split) {  // nothing to batch (level 0 finished it, or skipped a constant byte)
             if (nseg && levels == 1 && ws.h_ctr[0].n_next) {
                 RG_CHECK(cudaMemsetAsync(dctr + 1, 0, sizeof(LevelCounters), st));
@@ -1129,7 +1171,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
                 levels = std::max(levels, lv);
                 read_counters_and_finish<RS>(ws, data, tmp, ks, dctr, lv, st);
                 add_level_stats(1, lv);
-                RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, sizeof(unsigned int), st));
+                RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, 2 * sizeof(unsigned int), st));
                 (*on_final)(p0, p1);
             }
         }
@@ -2301,7 +2343,7 @@ void raduls_gpu_release(void) {
         for (int b = 0; b < 2; ++b) {
             w->segs[b].release(); w->seg_tot[b].release(); w->seg_andor[b].release(); w->tile_seg[b].release();
         }
-        w->tile_cnt.release(); w->tile_off.release(); w->status.release(); w->groups.release(); w->spill.release(); w->n_spill.release();
+        w->tile_cnt.release(); w->tile_off.release(); w->status.release(); w->groups.release(); w->spill.release(); w->spill_bm.release(); w->n_spill.release();
         w->copies.release(); w->host_data.release(); w->host_tmp.release(); w->map8.release(); w->dig_dst.release(); w->pieces.release(); w->hot.release();
         w->nd.release(); w->bsegs.release();
         delete w->stager;
