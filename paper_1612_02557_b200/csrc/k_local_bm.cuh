@@ -32,42 +32,86 @@
 
 namespace rg {
 
-template <int RS>
-struct BmCfg {
-    using L = LocalCfg<RS>;
-    static_assert(!L::kRegRecords, "shared-memory records only");
-    static constexpr int kThreads = L::kThreads;
-    static constexpr int kMinBlocks = L::kMinBlocks;
-    static constexpr int kWarps = kThreads / 32;
-    static constexpr int kCap = L::kCap;
-    static constexpr int kIpt = L::kIpt;
-    // cells = 2^kFineBits at most: >= 32 per record at a full group
+// Shape knobs of the 16-B primary instance (A/B): threads per
+// CTA, CTAs per SM, group capacity. The planner packs small bins into groups
+// of at most this capacity (group_cap<RS>()); a single bin between it and the
+// local-sort capacity (LocalCfg::kCap) is a group of its own, taken by the
+// big instance (V = 1: the bucket sort's shape).
+// Measured (C5 local sort, interleaved A/B): 512 threads x 2 CTAs per SM, cap
+// 3584: 38.7 ms; 384 x 3, cap 2560: 36.8 ms; 256 x 5, cap 1792: 31.9 ms.
+#ifndef RG_BM_THREADS
+#define RG_BM_THREADS 256
+#endif
+#ifndef RG_BM_BLOCKS
+#define RG_BM_BLOCKS 5
+#endif
+#ifndef RG_BM_CAP16
+#define RG_BM_CAP16 1792
+#endif
+#ifndef RG_BM_THREADS32
+#define RG_BM_THREADS32 512
+#endif
 #ifndef RG_BM_BITS
 #define RG_BM_BITS 0
 #endif
-    static constexpr int kFineBits = RG_BM_BITS ? RG_BM_BITS : (RS == 32 ? 18 : 17);
-    // cells per record aimed at, as a power of two (FB = ceil(log2 n) + kCellLog)
 #ifndef RG_BM_CELL_LOG
 #define RG_BM_CELL_LOG 5
 #endif
+
+constexpr int ceil_log2_c(int n) {
+    int b = 0;
+    while ((1 << b) < n) ++b;
+    return b;
+}
+
+template <int RS, int V = 0>
+struct BmCfg {
+    using L = LocalCfg<RS>;
+    static_assert(!L::kRegRecords, "shared-memory records only");
+    static constexpr bool kTuned = RS == 16 && V == 0;
+    static constexpr int kThreads = kTuned ? RG_BM_THREADS : RS == 32 ? RG_BM_THREADS32 : L::kThreads;
+    static constexpr int kMinBlocks = kTuned ? RG_BM_BLOCKS : L::kMinBlocks;
+    static constexpr int kWarps = kThreads / 32;
+    static constexpr int kCap = kTuned ? RG_BM_CAP16 : L::kCap;
+    static_assert(kCap <= L::kCap, "the bucket sort takes over whole groups");
+    static constexpr int kIpt = (kCap + kThreads - 1) / kThreads;
+    // cells per record aimed at, as a power of two: FB = ceil(log2 n) + kCellLog
+    // (measured at 16 B: 2^5 cells per record C5 local 38.1 ms, 2^4 40.1, 2^6 39.7)
     static constexpr int kCellLog = RG_BM_CELL_LOG;
+    // cells = 2^kFineBits at most
+    static constexpr int kFineBits = RG_BM_BITS ? RG_BM_BITS : ceil_log2_c(kCap) + kCellLog;
     static constexpr int kWords = 1 << (kFineBits - 5);
     // scan: every warp owns kRows rows of 128 words
-    static constexpr int kRows = kWords / (128 * kWarps) > 0 ? kWords / (128 * kWarps) : 1;
-    static_assert(kRows == 1 || kRows == 2 || kRows == 4, "scan rows per warp");
-    static constexpr int kDirty = 1024;  // records of dirty words (u32 entries)
-    static constexpr int kDw = 512;      // dirty words (8-B descriptors)
-    static constexpr int kRecBytes = L::kRecBytes;
+    static constexpr int kRows = (kWords + 128 * kWarps - 1) / (128 * kWarps);
+    static_assert(kRows >= 1 && kRows <= 4, "scan rows per warp");
+    static constexpr int kDirty = kCap >= 2048 ? 1024 : 512;  // records of dirty words (u32 entries)
+    static constexpr int kDw = kDirty / 2;                    // dirty words (8-B descriptors)
+    static constexpr int kRecBytes = ((kCap * RS + 16 + 127) / 128) * 128;
     static constexpr size_t kSmem =
         size_t(kRecBytes) + size_t(kWords) * 6 + size_t(kDirty) * 4 + size_t(kDw) * 8;
 };
 
-template <int RS, typename Mid>
+// Whether groups larger than the primary instance's capacity exist (they go to
+// the `med` list, sorted by the big instance).
+template <int RS>
+constexpr bool kBmHasBig = BmCfg<RS, 0>::kCap < LocalCfg<RS>::kCap;
+
+struct GroupList {
+    Group* list;
+    unsigned int* n;
+    uint32_t cap;
+};
+
+__device__ __forceinline__ void push_group(const GroupList& l, const Group& g) {
+    const uint32_t i = atomicAdd(l.n, 1u);
+    if (i < l.cap) l.list[i] = g;
+}
+
+template <int RS, int V, typename Mid>
 __device__ __forceinline__ void local_group_bm(
     uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group g, uint32_t ks,
-    LevelCounters* __restrict__ ctr, Group* __restrict__ spill, unsigned int* __restrict__ n_spill,
-    uint32_t spill_cap, Mid&& mid) {
-    using C = BmCfg<RS>;
+    LevelCounters* __restrict__ ctr, const GroupList spill, const GroupList med, Mid&& mid) {
+    using C = BmCfg<RS, V>;
     constexpr int T = C::kThreads, W = C::kWarps, IPT = C::kIpt, R = C::kRows;
     extern __shared__ __align__(128) uint8_t smem[];
     RG_CHK_POISON_SMEM(smem);
@@ -83,6 +127,12 @@ __device__ __forceinline__ void local_group_bm(
     const uint8_t* gsrc = (g.parity ? tmp : data) + g.start * RS;
     uint8_t* dst = data + g.start * RS;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if constexpr (V == 0 && kBmHasBig<RS>) {
+        if (n > uint32_t(C::kCap)) {  // a single bin above this instance's capacity
+            if (threadIdx.x == 0) push_group(med, g);
+            return;
+        }
+    }
     const uint32_t klim = ks < uint32_t(RS) ? ks : uint32_t(RS);
     if (n <= 1 || g.p >= klim) {  // nothing to order (no key byte left: the input order stands)
         if (g.parity)
@@ -115,17 +165,13 @@ __device__ __forceinline__ void local_group_bm(
     }
     // cells: 2^FB, ~2^kCellLog per record; at least one warp's scan span
     uint32_t FB = 32u + uint32_t(C::kCellLog) - __clz(n - 1);  // ceil(log2 n) + kCellLog (n >= 2)
-    constexpr uint32_t kMinFB = R == 1 ? 12 : R == 2 ? 13 : 14;  // 128 R words
-    FB = FB < kMinFB ? kMinFB : (FB > uint32_t(C::kFineBits) ? uint32_t(C::kFineBits) : FB);
-    const uint32_t nW = 1u << (FB - 5);  // a multiple of 128 R
+    FB = FB < 12u ? 12u : (FB > uint32_t(C::kFineBits) ? uint32_t(C::kFineBits) : FB);
+    const uint32_t nW = 1u << (FB - 5);  // a multiple of 128 (one scan row)
     {
-        // bm and pre are adjacent: [0, nW) words of bm, then [0, nW / 2) words of pre
         uint4* z = reinterpret_cast<uint4*>(bm);
 #pragma unroll
-        for (int q = 0; q < C::kWords / 4 / T; ++q)
+        for (int q = 0; q < (C::kWords / 4 + T - 1) / T; ++q)
             if (q * T + threadIdx.x < nW / 4) z[q * T + threadIdx.x] = make_uint4(0, 0, 0, 0);
-        if constexpr (C::kWords / 4 < T)
-            if (threadIdx.x < nW / 4) z[threadIdx.x] = make_uint4(0, 0, 0, 0);
         uint4* z2 = reinterpret_cast<uint4*>(pre);
 #pragma unroll
         for (int q = 0; q < (C::kWords / 8 + T - 1) / T; ++q)
@@ -203,20 +249,19 @@ __device__ __forceinline__ void local_group_bm(
     __syncthreads();
 
     // ---- 4. scan over the words of popc(word) + extras. Warp q owns words
-    // [128 R q, 128 R (q + 1)) as R rows of 128; lane l reads words 4 l..4 l + 3
+    // [128 R q, 128 R (q + 1)) as R rows of 128 (those below nW); lane l reads words 4 l..4 l + 3
     // of each row (conflict-free 16-B / 8-B loads); row sums are scanned across
     // the lanes two rows to a register (u16 halves: sums <= n < 32768). A word
     // with extras (a shared cell) is dirty: it gets a descriptor {start, count,
     // first list entry} and its start entry holds 0x8000 | descriptor id.
     {
-        const bool active = uint32_t(warp) * (128u * R) < nW;
         const uint4* bm4 = reinterpret_cast<const uint4*>(bm) + warp * (32 * R);
         uint2* pre2 = reinterpret_cast<uint2*>(pre) + warp * (32 * R);
         uint32_t sv[R];
 #pragma unroll
         for (int v = 0; v < R; ++v) {
             sv[v] = 0;
-            if (active) {
+            if ((uint32_t(warp) * R + v) * 128u < nW) {
                 const uint4 a = bm4[v * 32 + lane];
                 const uint2 x = pre2[v * 32 + lane];
                 uint32_t s = __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
@@ -246,9 +291,10 @@ __device__ __forceinline__ void local_group_bm(
         __syncthreads();
         const uint32_t t = lane < W ? s_scan[lane] : 0u;
         uint32_t rowb = __reduce_add_sync(0xFFFFFFFFu, lane < warp ? t : 0u);
-        if (active) {
+        {
 #pragma unroll
             for (int v = 0; v < R; ++v) {
+                if ((uint32_t(warp) * R + v) * 128u >= nW) break;  // warp-uniform
                 const uint32_t exl = ik[v / 2] - pk[v / 2];  // exclusive over the lanes, per row
                 const uint32_t ex = (v & 1) ? (exl >> 16) : (exl & 0xFFFFu);
                 const uint32_t rt = (v & 1) ? (tk[v / 2] >> 16) : (tk[v / 2] & 0xFFFFu);
@@ -283,8 +329,7 @@ __device__ __forceinline__ void local_group_bm(
     if (nd > uint32_t(C::kDirty) || ndw > uint32_t(C::kDw) || s_crowd) {
         // block-uniform; nothing written yet: the bucket sort takes the group
         if (threadIdx.x == 0) {
-            const uint32_t i = atomicAdd(n_spill, 1u);
-            if (i < spill_cap) spill[i] = g;
+            push_group(spill, g);
             atomicAdd(&ctr->bm_spill, 1u);
         }
         return;
@@ -354,18 +399,18 @@ __device__ __forceinline__ void local_group_bm(
     if (threadIdx.x == 0) atomicAdd(&ctr->moved_local, (unsigned long long)n);
 }
 
-// Bitmap local sort launch: the shapes of k_local (two CTAs per SM: a CTA per
-// group, the group one resident wave ahead prefetched into L2; one CTA per
+// Bitmap local sort launch: the shapes of k_local (several CTAs per SM: a CTA
+// per group, the group one resident wave ahead prefetched into L2; one CTA per
 // SM: persistent, groups round-robin, next descriptor by cp.async).
 template <int RS>
 __global__ void __launch_bounds__(BmCfg<RS>::kThreads, BmCfg<RS>::kMinBlocks) k_local_bm(
     uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group* __restrict__ groups,
-    uint32_t n_groups, uint32_t ks, LevelCounters* __restrict__ ctr, Group* __restrict__ spill,
-    unsigned int* __restrict__ n_spill, uint32_t spill_cap, uint32_t ahead) {
+    uint32_t n_groups, uint32_t ks, LevelCounters* __restrict__ ctr, GroupList spill, GroupList med,
+    uint32_t ahead) {
     if constexpr (BmCfg<RS>::kMinBlocks > 1) {
         if (threadIdx.x == 0 && blockIdx.x + ahead < n_groups)
             prefetch_group_l2<RS>(data, tmp, groups[blockIdx.x + ahead]);
-        local_group_bm<RS>(data, tmp, groups[blockIdx.x], ks, ctr, spill, n_spill, spill_cap, [] {});
+        local_group_bm<RS, 0>(data, tmp, groups[blockIdx.x], ks, ctr, spill, med, [] {});
         return;
     }
     __shared__ __align__(16) Group s_g[2];
@@ -388,10 +433,24 @@ __global__ void __launch_bounds__(BmCfg<RS>::kThreads, BmCfg<RS>::kMinBlocks) k_
                 prefetch_group_l2<RS>(data, tmp, s_g[buf ^ 1]);
             }
         };
-        local_group_bm<RS>(data, tmp, g, ks, ctr, spill, n_spill, spill_cap, mid);
+        local_group_bm<RS, 0>(data, tmp, g, ks, ctr, spill, med, mid);
         if (threadIdx.x == 0 && more) cp_async_wait_all();
         __syncthreads();
         i = nx;
+    }
+}
+
+// The big instance over the device-counted `med` list (groups above the
+// primary instance's capacity), launched right behind k_local_bm with a fixed
+// grid; CTAs walk the list with the grid's stride.
+template <int RS>
+__global__ void __launch_bounds__(BmCfg<RS, 1>::kThreads, BmCfg<RS, 1>::kMinBlocks) k_local_bm_med(
+    uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, GroupList med, uint32_t ks,
+    LevelCounters* __restrict__ ctr, GroupList spill) {
+    const uint32_t n = min(*med.n, med.cap);
+    for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+        local_group_bm<RS, 1>(data, tmp, med.list[i], ks, ctr, spill, med, [] {});
+        __syncthreads();  // shared memory free for the next group
     }
 }
 

@@ -33,7 +33,8 @@ struct PlanArgs {
     LevelCounters* ctr;
     uint32_t ks;
     uint32_t tile;       // tile partition (records)
-    uint32_t cap_local;  // local-sort group capacity (records)
+    uint32_t cap_local;  // local-sort capacity (records): larger children go to the next level
+    uint32_t cap_group;  // small children are packed into groups of at most this (<= cap_local)
     uint32_t side;       // this level was histogrammed from the digit array (no AND/OR)
 };
 
@@ -280,9 +281,9 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
     // finds its own end by binary search (P is monotone), a suffix minimum
     // gives the next open digit, and thread 0 walks the ~n/cap-long chain.
     {
-        const uint32_t cap = uint32_t(A.cap_local);
+        const uint32_t cap = uint32_t(A.cap_group);  // (a child above it is a group of its own)
         const unsigned long long c = s_cnt[tid];
-        const bool big = c > cap;
+        const bool big = c > A.cap_local;
         const uint32_t sz = big ? 0u : uint32_t(c);
         // exclusive prefix of the small sizes (block scan over 256 digits)
         uint32_t x = sz;

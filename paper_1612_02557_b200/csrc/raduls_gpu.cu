@@ -524,8 +524,10 @@ struct Workspace {
     DevBuf<uint16_t> tile_cnt;
     DevBuf<uint32_t> tile_off;
     DevBuf<unsigned long long> status;
-    DevBuf<Group> groups, spill, spill_bm;
-    DevBuf<unsigned int> n_spill;  // [0]: groups for the LSD fallback, [1]: groups the bitmap sort handed over
+    DevBuf<Group> groups, spill, spill_bm, spill_med;
+    // [0]: groups for the LSD fallback, [1]: groups the bitmap sort handed to
+    // the bucket sort, [2]: groups above the bitmap sort's primary capacity
+    DevBuf<unsigned int> n_spill;
     DevBuf<CopyRange> copies;
     HostDevBuf host_data, host_tmp;
     DevBuf<uint8_t> map8;
@@ -602,9 +604,19 @@ int grid_for(uint64_t n, int threads, int per_sm) {
 
 // Local-sort group capacity: the register variant for 8-B records (C2 needs
 // ~17 K-record groups), the shared-memory variant otherwise.
+#ifndef RG_LOC_BM
+#define RG_LOC_BM 1
+#endif
 template <int RS>
 constexpr uint32_t local_cap() {
     return LocalCfg<RS>::kCap;
+}
+// Bound on a group packed from several small bins: the bitmap sort's primary
+// capacity (a single bin above it, up to local_cap, is a group of its own).
+template <int RS>
+constexpr uint32_t group_cap() {
+    if constexpr (RG_LOC_BM && RS != 8) return BmCfg<RS>::kCap;
+    else return LocalCfg<RS>::kCap;
 }
 
 // Capacities for a sort of n records.
@@ -618,7 +630,7 @@ Caps caps_for(uint64_t n, uint64_t extra_segs = 0) {
     Caps c;
     c.seg = size_t(n / (cap_local + 1) + 2 + extra_segs);
     c.tiles = size_t(n / ScatterCfg<RS>::kTile + c.seg + 2);
-    c.groups = size_t(3 * (n / cap_local) + c.seg + 2);
+    c.groups = size_t(3 * (n / group_cap<RS>()) + c.seg + 2);
     c.copies = size_t(n / kCopyTile + c.seg + 2);
     return c;
 }
@@ -638,7 +650,8 @@ void ensure_caps(Workspace& ws, uint64_t n, uint64_t extra_segs = 0) {
     ws.groups.ensure(c.groups);
     ws.spill.ensure(c.groups);
     if constexpr (RS != 8) ws.spill_bm.ensure(c.groups);
-    ws.n_spill.ensure(2);  // (read back as one 8-B word)
+    if constexpr (RS != 8) ws.spill_med.ensure(c.groups);
+    ws.n_spill.ensure(4);  // ([0] read back as the low half of one 8-B word)
     ws.copies.ensure(c.copies);
 }
 
@@ -654,6 +667,9 @@ void set_attrs(Workspace& ws) {
                                       int(BmCfg<RS>::kSmem)));
         RG_CHECK(cudaFuncSetAttribute(k_local_list<RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(LocalCfg<RS>::kSmem)));
+        if constexpr (kBmHasBig<RS>)
+            RG_CHECK(cudaFuncSetAttribute(k_local_bm_med<RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(BmCfg<RS, 1>::kSmem)));
     }
     RG_CHECK(cudaFuncSetAttribute(k_tile_hist<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(HistCfg<RS>::kSmem)));
@@ -768,9 +784,6 @@ void launch_scatter(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_
 
 // RADULS_GPU_LOCAL=bucket: the bucket sort alone (k_local.cuh) for every group,
 // as before the bitmap sort existed (tests and A/B).
-#ifndef RG_LOC_BM
-#define RG_LOC_BM 1
-#endif
 bool bitmap_local() {
     if (!RG_LOC_BM) return false;
     const char* e = std::getenv("RADULS_GPU_LOCAL");
@@ -790,12 +803,24 @@ void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, 
         if (bitmap_local()) {
             // the bitmap sort first; the groups it hands over (device-counted
             // list) go to the bucket sort right behind it, no host read between
-            RG_CHECK(cudaMemsetAsync(ws.n_spill.p + 1, 0, sizeof(unsigned int), st));
-            k_local_bm<RS><<<grid, BmCfg<RS>::kThreads, BmCfg<RS>::kSmem, st>>>(
-                data, tmp, ws.groups.p, ngroups, ks, ctr, ws.spill_bm.p, ws.n_spill.p + 1,
-                uint32_t(ws.spill_bm.cap), uint32_t(sm_count()) * BmCfg<RS>::kMinBlocks);
+            RG_CHECK(cudaMemsetAsync(ws.n_spill.p + 1, 0, 2 * sizeof(unsigned int), st));
+            const GroupList spill{ws.spill_bm.p, ws.n_spill.p + 1, uint32_t(ws.spill_bm.cap)};
+            const GroupList med{ws.spill_med.p, ws.n_spill.p + 2, uint32_t(ws.spill_med.cap)};
+            const uint32_t bgrid = BmCfg<RS>::kMinBlocks == 1 ? std::min<uint32_t>(ngroups, uint32_t(sm_count()))
+                                                              : ngroups;
+            k_local_bm<RS><<<bgrid, BmCfg<RS>::kThreads, BmCfg<RS>::kSmem, st>>>(
+                data, tmp, ws.groups.p, ngroups, ks, ctr, spill, med,
+                uint32_t(sm_count()) * BmCfg<RS>::kMinBlocks);
             note_launch();
             RG_LAUNCH_CHECK();
+            if constexpr (kBmHasBig<RS>) {
+                const uint32_t mgrid =
+                    std::min<uint32_t>(ngroups, uint32_t(sm_count()) * BmCfg<RS, 1>::kMinBlocks);
+                k_local_bm_med<RS><<<mgrid, BmCfg<RS, 1>::kThreads, BmCfg<RS, 1>::kSmem, st>>>(
+                    data, tmp, med, ks, ctr, spill);
+                note_launch();
+                RG_LAUNCH_CHECK();
+            }
             const uint32_t lgrid =
                 std::min<uint32_t>(ngroups, uint32_t(sm_count()) * LocalCfg<RS>::kMinBlocks);
             k_local_list<RS><<<lgrid, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
@@ -912,7 +937,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
     set_attrs<RS>(ws);
     ensure_caps<RS>(ws, n, seeds ? seeds->size() : 0);
     LevelCounters* dctr = ws.ctr.p;
-    RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, 2 * sizeof(unsigned int), st));
+    RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, 4 * sizeof(unsigned int), st));
     RG_CHK_RANGES(st, {{data, size_t(n) * RS}, {tmp, size_t(n) * RS}});
 #ifdef RG_CHECKED
     {  // poison the scratch: nothing may be read before this sort writes it
@@ -1048,6 +1073,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         A.ks = ks;
         A.tile = TILE;
         A.cap_local = local_cap<RS>();
+        A.cap_group = group_cap<RS>();
         A.side = nd_in ? 1u : 0u;
         pe = ws.prof.begin(K_PLAN, st);
         k_plan<<<nseg, 256, 0, st>>>(A);
@@ -1127,7 +1153,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         const bool split = levels == 1 && nseg >= 2 && !last_skip && ws.h_ctr[0].n_scatter_segs == 1;
         read_counters_and_finish<RS>(ws, data, tmp, ks, dctr, 1, st);
         add_level_stats(0, 1);
-        RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, 2 * sizeof(unsigned int), st));
+        RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, 4 * sizeof(unsigned int), st));
         if (!split) {  // nothing to batch (level 0 finished it, or skipped a constant byte)
             if (nseg && levels == 1 && ws.h_ctr[0].n_next) {
                 RG_CHECK(cudaMemsetAsync(dctr + 1, 0, sizeof(LevelCounters), st));
@@ -1171,7 +1197,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
                 levels = std::max(levels, lv);
                 read_counters_and_finish<RS>(ws, data, tmp, ks, dctr, lv, st);
                 add_level_stats(1, lv);
-                RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, 2 * sizeof(unsigned int), st));
+                RG_CHECK(cudaMemsetAsync(ws.n_spill.p, 0, 4 * sizeof(unsigned int), st));
                 (*on_final)(p0, p1);
             }
         }
@@ -2343,7 +2369,7 @@ void raduls_gpu_release(void) {
         for (int b = 0; b < 2; ++b) {
             w->segs[b].release(); w->seg_tot[b].release(); w->seg_andor[b].release(); w->tile_seg[b].release();
         }
-        w->tile_cnt.release(); w->tile_off.release(); w->status.release(); w->groups.release(); w->spill.release(); w->spill_bm.release(); w->n_spill.release();
+        w->tile_cnt.release(); w->tile_off.release(); w->status.release(); w->groups.release(); w->spill.release(); w->spill_bm.release(); w->spill_med.release(); w->n_spill.release();
         w->copies.release(); w->host_data.release(); w->host_tmp.release(); w->map8.release(); w->dig_dst.release(); w->pieces.release(); w->hot.release();
         w->nd.release(); w->bsegs.release();
         delete w->stager;
