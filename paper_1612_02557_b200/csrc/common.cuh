@@ -595,7 +595,7 @@ struct Group {
     uint32_t size;
     uint32_t p;
     uint32_t parity;
-    uint32_t pad;
+    uint32_t pad;  // 0, or d0 | d1 << 8 | 1 << 16: key byte p of every record lies in [d0, d1]
 };
 
 // A range of finished records living in tmp that must move home.

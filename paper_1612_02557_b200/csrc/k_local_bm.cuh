@@ -48,6 +48,18 @@ namespace rg {
 #ifndef RG_BM_CAP16
 #define RG_BM_CAP16 1792
 #endif
+// RG_BM_WAIT1: thread 0 alone waits for the group's TMA copy, the block barrier
+// hands the completion on (no spinning warps). RG_BM_PERSIST: the several-
+// CTAs-per-SM shapes run as a resident grid walking the groups with its stride.
+#ifndef RG_BM_WAIT1
+#define RG_BM_WAIT1 0
+#endif
+#ifndef RG_BM_KNOWN
+#define RG_BM_KNOWN 1
+#endif
+#ifndef RG_BM_PERSIST
+#define RG_BM_PERSIST 0
+#endif
 #ifndef RG_BM_THREADS32
 #define RG_BM_THREADS32 512
 #endif
@@ -177,19 +189,59 @@ __device__ __forceinline__ void local_group_bm(
         for (int q = 0; q < (C::kWords / 8 + T - 1) / T; ++q)
             if (q * T + threadIdx.x < nW / 8) z2[q * T + threadIdx.x] = make_uint4(0, 0, 0, 0);
     }
-    __syncthreads();
-    mbar_wait(&s_bar, 0);
+    if constexpr (RG_BM_WAIT1) {
+        if (threadIdx.x == 0) mbar_wait(&s_bar, 0);
+        __syncthreads();
+    } else {
+        __syncthreads();
+        mbar_wait(&s_bar, 0);
+    }
 
-    // ---- 2. windows: key bytes p..p+3 (fewer at the key's end), big-endian,
-    // one byte permute per record; their range. No search for the varying
+    // ---- 2./3. windows: key bytes p..p+3 (fewer at the key's end), big-endian,
+    // one byte permute per record; their range; cell bits. No search for the varying
     // bytes: a window holding constant bytes only loses resolution, and a
     // group it cannot resolve is handed to the bucket sort
     const uint32_t nwin = klim - g.p < 4u ? klim - g.p : 4u;
     const bool beyond = g.p + 4u < klim;
     uint32_t Ldef[4] = {g.p, g.p + 1, g.p + 2, g.p + 3};
     const WindowSel ws = make_window_sel(Ldef, nwin, RS / 4, false);
-    uint32_t wv[IPT];
-    {
+    // The planner's groups carry the digit range [d0, d1] of byte p (pad: d0 |
+    // d1 << 8 | 1 << 16): the window range is known without a min/max pass, so
+    // windows and cell bits are one pass (RG_BM_KNOWN).
+    const bool known = RG_BM_KNOWN && (g.pad & 0x10000u) != 0u;
+    const uint32_t ncell = 1u << FB;
+    uint32_t fc[IPT];
+    // cell = umulhi(w - wmin, mul): monotone in w and < 2^FB (mul rounded down
+    // with a 1e-6 margin over the float error; k_local.cuh's bucket geometry)
+    auto mul_of = [&](uint32_t rm1) {
+        return rm1 < ncell ? 0u
+                           : uint32_t(__fdiv_rz(float(ncell) * 4294967296.0f, float(rm1) + 1.0f) * 0.999999f);
+    };
+    // one bit per occupied cell; a record finding its cell taken counts itself
+    // in the word's extras (u16 halves of pre)
+    auto mark = [&](uint32_t f) {
+        const uint32_t bit = 1u << (f & 31u);
+        const uint32_t old = atomicOr(&bm[f >> 5], bit);
+        if (old & bit) atomicAdd(&pre[f >> 6], 1u << ((f >> 1) & 16u));
+    };
+    if (known) {
+        const uint32_t d0 = g.pad & 0xFFu, d1 = (g.pad >> 8) & 0xFFu;
+        const uint32_t wmin = d0 << 24, rm1 = ((d1 - d0 + 1u) << 24) - 1u;
+        const uint32_t mul = mul_of(rm1);
+        mid();
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            if (uint32_t(j) * T >= n) break;  // block-uniform
+            const uint32_t e = uint32_t(j) * T + threadIdx.x;
+            if (e < n) {
+                const uint32_t d = rec_window<RS>(ld_smem_rec<RS>(recs, e), ws) - wmin;
+                const uint32_t f = min(mul ? __umulhi(d, mul) : d, ncell - 1u);
+                fc[j] = f;
+                mark(f);
+            }
+        }
+    } else {
+        uint32_t wv[IPT];
         uint32_t smn = 0xFFFFFFFFu, smx = 0u;
 #pragma unroll
         for (int j = 0; j < IPT; ++j) {
@@ -208,42 +260,32 @@ __device__ __forceinline__ void local_group_bm(
             atomicMin(&s_wmin, smn);
             atomicMax(&s_wmax, smx);
         }
-    }
-    __syncthreads();
-    // cell = umulhi(w - wmin, mul): monotone in w and < 2^FB (mul rounded down
-    // with a 1e-6 margin over the float error; k_local.cuh's bucket geometry)
-    const uint32_t ncell = 1u << FB;
-    const uint32_t wmin = s_wmin;
-    const uint32_t rm1 = s_wmax - wmin;  // range - 1
-    if (rm1 == 0 && !beyond) {           // every key equal: stable order is the input order
-        if (g.parity) {
+        __syncthreads();
+        const uint32_t wmin = s_wmin;
+        const uint32_t rm1 = s_wmax - wmin;  // range - 1
+        if (rm1 == 0 && !beyond) {           // every key equal: stable order is the input order
+            if (g.parity) {
 #pragma unroll
-            for (int j = 0; j < IPT; ++j) {
-                if (uint32_t(j) * T >= n) break;
-                const uint32_t e = uint32_t(j) * T + threadIdx.x;
-                if (e < n) store_rec<RS>(dst, e, ld_smem_rec<RS>(recs, e));
+                for (int j = 0; j < IPT; ++j) {
+                    if (uint32_t(j) * T >= n) break;
+                    const uint32_t e = uint32_t(j) * T + threadIdx.x;
+                    if (e < n) store_rec<RS>(dst, e, ld_smem_rec<RS>(recs, e));
+                }
             }
+            return;
         }
-        return;
-    }
-    const uint32_t mul =
-        rm1 < ncell ? 0u : uint32_t(__fdiv_rz(float(ncell) * 4294967296.0f, float(rm1) + 1.0f) * 0.999999f);
-
-    mid();
-    // ---- 3. one bit per occupied cell; a record finding its cell taken counts
-    // itself in the word's extras (u16 halves of pre)
-    uint32_t fc[IPT];
+        const uint32_t mul = mul_of(rm1);
+        mid();
 #pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-        if (uint32_t(j) * T >= n) break;
-        const uint32_t e = uint32_t(j) * T + threadIdx.x;
-        if (e < n) {
-            const uint32_t d = wv[j] - wmin;
-            const uint32_t f = mul ? __umulhi(d, mul) : d;
-            fc[j] = f;
-            const uint32_t bit = 1u << (f & 31u);
-            const uint32_t old = atomicOr(&bm[f >> 5], bit);
-            if (old & bit) atomicAdd(&pre[f >> 6], 1u << ((f >> 1) & 16u));
+        for (int j = 0; j < IPT; ++j) {
+            if (uint32_t(j) * T >= n) break;
+            const uint32_t e = uint32_t(j) * T + threadIdx.x;
+            if (e < n) {
+                const uint32_t d = wv[j] - wmin;
+                const uint32_t f = mul ? __umulhi(d, mul) : d;
+                fc[j] = f;
+                mark(f);
+            }
         }
     }
     __syncthreads();
@@ -407,7 +449,7 @@ __global__ void __launch_bounds__(BmCfg<RS>::kThreads, BmCfg<RS>::kMinBlocks) k_
     uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group* __restrict__ groups,
     uint32_t n_groups, uint32_t ks, LevelCounters* __restrict__ ctr, GroupList spill, GroupList med,
     uint32_t ahead) {
-    if constexpr (BmCfg<RS>::kMinBlocks > 1) {
+    if constexpr (BmCfg<RS>::kMinBlocks > 1 && !RG_BM_PERSIST) {
         if (threadIdx.x == 0 && blockIdx.x + ahead < n_groups)
             prefetch_group_l2<RS>(data, tmp, groups[blockIdx.x + ahead]);
         local_group_bm<RS, 0>(data, tmp, groups[blockIdx.x], ks, ctr, spill, med, [] {});

@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
     __shared__ uint32_t s_next_idx[kRadix], s_next_tb[kRadix];
     __shared__ uint32_t s_wbig[8], s_wtiles[8], s_nb_base, s_nt_base;
     __shared__ uint64_t s_gstart[kRadix];
+    __shared__ uint32_t s_gdig[kRadix];
     __shared__ uint32_t s_gsize[kRadix], s_P[kRadix + 1], s_nbig[kRadix], s_open[kRadix], s_end[kRadix];
     __shared__ uint32_t s_wsz[8];
     const uint32_t s = blockIdx.x;
@@ -329,6 +330,7 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
                 const uint32_t e = s_end[d0];
                 s_gstart[ng] = g.start + s_off[d0];
                 s_gsize[ng] = s_P[e] - s_P[d0];
+                s_gdig[ng] = d0 | ((e - 1u) << 8) | 0x10000u;  // byte p of the group's records lies in [d0, e)
                 ++ng;
                 d0 = e < uint32_t(kRadix) ? s_open[e] : uint32_t(kRadix);
             }
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
         gr.size = s_gsize[tid];
         gr.p = g.p;
         gr.parity = cp;
-        gr.pad = 0;
+        gr.pad = s_gdig[tid];
         A.groups[s_base + tid] = gr;
     }
     // tile -> segment map of the big children: one warp per child

@@ -806,8 +806,10 @@ void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, 
             RG_CHECK(cudaMemsetAsync(ws.n_spill.p + 1, 0, 2 * sizeof(unsigned int), st));
             const GroupList spill{ws.spill_bm.p, ws.n_spill.p + 1, uint32_t(ws.spill_bm.cap)};
             const GroupList med{ws.spill_med.p, ws.n_spill.p + 2, uint32_t(ws.spill_med.cap)};
-            const uint32_t bgrid = BmCfg<RS>::kMinBlocks == 1 ? std::min<uint32_t>(ngroups, uint32_t(sm_count()))
-                                                              : ngroups;
+            const uint32_t bgrid =
+                (BmCfg<RS>::kMinBlocks == 1 || RG_BM_PERSIST)
+                    ? std::min<uint32_t>(ngroups, uint32_t(sm_count()) * BmCfg<RS>::kMinBlocks)
+                    : ngroups;
             k_local_bm<RS><<<bgrid, BmCfg<RS>::kThreads, BmCfg<RS>::kSmem, st>>>(
                 data, tmp, ws.groups.p, ngroups, ks, ctr, spill, med,
                 uint32_t(sm_count()) * BmCfg<RS>::kMinBlocks);
