@@ -103,6 +103,91 @@ struct BmCfg {
         size_t(kRecBytes) + size_t(kWords) * 6 + size_t(kDirty) * 4 + size_t(kDw) * 8;
 };
 
+// Scan over the bitmap words of popc(word) + extras -> every word's start (u16
+// in place of its extras). Warp q owns words [128 R q, 128 R (q + 1)) as R rows
+// of 128 (those below nW); lane l reads words 4 l..4 l + 3 of each row
+// (conflict-free 16-B / 8-B loads); row sums are scanned across the lanes two
+// rows to a register (u16 halves: sums <= n < 32768). A word with extras (a
+// shared cell) is dirty: it gets a descriptor {start | count << 16, first list
+// entry} and its start entry holds 0x8000 | descriptor id; *s_alloc counts
+// dirty records (low half) and dirty words (high half). One block barrier
+// inside; the caller syncs after it.
+template <int W, int R, int kDw>
+__device__ __forceinline__ void bm_scan(const uint32_t* bm, uint32_t* pre, uint2* dw, uint32_t nW,
+                                        uint32_t* s_scan, uint32_t* s_alloc, uint32_t* s_crowd) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    {
+        const uint4* bm4 = reinterpret_cast<const uint4*>(bm) + warp * (32 * R);
+        uint2* pre2 = reinterpret_cast<uint2*>(pre) + warp * (32 * R);
+        uint32_t sv[R];
+#pragma unroll
+        for (int v = 0; v < R; ++v) {
+            sv[v] = 0;
+            if ((uint32_t(warp) * R + v) * 128u < nW) {
+                const uint4 a = bm4[v * 32 + lane];
+                const uint2 x = pre2[v * 32 + lane];
+                uint32_t s = __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
+                if (x.x | x.y) s += (x.x & 0xFFFFu) + (x.x >> 16) + (x.y & 0xFFFFu) + (x.y >> 16);
+                sv[v] = s;
+            }
+        }
+        constexpr int NP = (R + 1) / 2;
+        uint32_t pk[NP], ik[NP];
+#pragma unroll
+        for (int q = 0; q < NP; ++q) ik[q] = pk[q] = sv[2 * q] | ((2 * q + 1 < R ? sv[2 * q + 1 < R ? 2 * q + 1 : 0] : 0u) << 16);
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, ik[q], off);
+                if (lane >= off) ik[q] += y;
+            }
+        }
+        uint32_t tk[NP], wtot = 0;
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            tk[q] = __shfl_sync(0xFFFFFFFFu, ik[q], 31);
+            wtot += (tk[q] & 0xFFFFu) + (tk[q] >> 16);
+        }
+        if (lane == 0) s_scan[warp] = wtot;
+        __syncthreads();
+        const uint32_t t = lane < W ? s_scan[lane] : 0u;
+        uint32_t rowb = __reduce_add_sync(0xFFFFFFFFu, lane < warp ? t : 0u);
+        {
+#pragma unroll
+            for (int v = 0; v < R; ++v) {
+                if ((uint32_t(warp) * R + v) * 128u >= nW) break;  // warp-uniform
+                const uint32_t exl = ik[v / 2] - pk[v / 2];  // exclusive over the lanes, per row
+                const uint32_t ex = (v & 1) ? (exl >> 16) : (exl & 0xFFFFu);
+                const uint32_t rt = (v & 1) ? (tk[v / 2] >> 16) : (tk[v / 2] & 0xFFFFu);
+                const uint4 a = bm4[v * 32 + lane];
+                const uint2 x = pre2[v * 32 + lane];
+                const uint32_t c0 = __popc(a.x), c1 = __popc(a.y), c2 = __popc(a.z);
+                uint32_t r0 = rowb + ex, r1 = r0 + c0, r2 = r1 + c1, r3 = r2 + c2;
+                if (x.x | x.y) {  // rare: a dirty word among the four
+                    const uint32_t e0 = x.x & 0xFFFFu, e1 = x.x >> 16, e2 = x.y & 0xFFFFu, e3 = x.y >> 16;
+                    r1 += e0;
+                    r2 += e0 + e1;
+                    r3 += e0 + e1 + e2;
+                    auto dirty = [&](uint32_t start, uint32_t cnt) -> uint32_t {
+                        const uint32_t old = atomicAdd(s_alloc, cnt | 0x10000u);
+                        const uint32_t id = old >> 16, off = old & 0xFFFFu;
+                        if (id < uint32_t(kDw)) dw[id] = make_uint2(start | (cnt << 16), off);
+                        if (cnt > kMaxBucket) *s_crowd = 1;  // duplicate-heavy: not for the quadratic ranking
+                        return 0x8000u | (id & 0x7FFFu);
+                    };
+                    if (e0) r0 = dirty(r0, c0 + e0);
+                    if (e1) r1 = dirty(r1, c1 + e1);
+                    if (e2) r2 = dirty(r2, c2 + e2);
+                    if (e3) r3 = dirty(r3, __popc(a.w) + e3);
+                }
+                pre2[v * 32 + lane] = make_uint2(r0 | (r1 << 16), r2 | (r3 << 16));
+                rowb += rt;
+            }
+        }
+    }
+}
+
 // Whether groups larger than the primary instance's capacity exist (they go to
 // the `med` list, sorted by the big instance).
 template <int RS>
@@ -290,82 +375,8 @@ __device__ __forceinline__ void local_group_bm(
     }
     __syncthreads();
 
-    // ---- 4. scan over the words of popc(word) + extras. Warp q owns words
-    // [128 R q, 128 R (q + 1)) as R rows of 128 (those below nW); lane l reads words 4 l..4 l + 3
-    // of each row (conflict-free 16-B / 8-B loads); row sums are scanned across
-    // the lanes two rows to a register (u16 halves: sums <= n < 32768). A word
-    // with extras (a shared cell) is dirty: it gets a descriptor {start, count,
-    // first list entry} and its start entry holds 0x8000 | descriptor id.
-    {
-        const uint4* bm4 = reinterpret_cast<const uint4*>(bm) + warp * (32 * R);
-        uint2* pre2 = reinterpret_cast<uint2*>(pre) + warp * (32 * R);
-        uint32_t sv[R];
-#pragma unroll
-        for (int v = 0; v < R; ++v) {
-            sv[v] = 0;
-            if ((uint32_t(warp) * R + v) * 128u < nW) {
-                const uint4 a = bm4[v * 32 + lane];
-                const uint2 x = pre2[v * 32 + lane];
-                uint32_t s = __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
-                if (x.x | x.y) s += (x.x & 0xFFFFu) + (x.x >> 16) + (x.y & 0xFFFFu) + (x.y >> 16);
-                sv[v] = s;
-            }
-        }
-        constexpr int NP = (R + 1) / 2;
-        uint32_t pk[NP], ik[NP];
-#pragma unroll
-        for (int q = 0; q < NP; ++q) ik[q] = pk[q] = sv[2 * q] | ((2 * q + 1 < R ? sv[2 * q + 1 < R ? 2 * q + 1 : 0] : 0u) << 16);
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-#pragma unroll
-            for (int q = 0; q < NP; ++q) {
-                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, ik[q], off);
-                if (lane >= off) ik[q] += y;
-            }
-        }
-        uint32_t tk[NP], wtot = 0;
-#pragma unroll
-        for (int q = 0; q < NP; ++q) {
-            tk[q] = __shfl_sync(0xFFFFFFFFu, ik[q], 31);
-            wtot += (tk[q] & 0xFFFFu) + (tk[q] >> 16);
-        }
-        if (lane == 0) s_scan[warp] = wtot;
-        __syncthreads();
-        const uint32_t t = lane < W ? s_scan[lane] : 0u;
-        uint32_t rowb = __reduce_add_sync(0xFFFFFFFFu, lane < warp ? t : 0u);
-        {
-#pragma unroll
-            for (int v = 0; v < R; ++v) {
-                if ((uint32_t(warp) * R + v) * 128u >= nW) break;  // warp-uniform
-                const uint32_t exl = ik[v / 2] - pk[v / 2];  // exclusive over the lanes, per row
-                const uint32_t ex = (v & 1) ? (exl >> 16) : (exl & 0xFFFFu);
-                const uint32_t rt = (v & 1) ? (tk[v / 2] >> 16) : (tk[v / 2] & 0xFFFFu);
-                const uint4 a = bm4[v * 32 + lane];
-                const uint2 x = pre2[v * 32 + lane];
-                const uint32_t c0 = __popc(a.x), c1 = __popc(a.y), c2 = __popc(a.z);
-                uint32_t r0 = rowb + ex, r1 = r0 + c0, r2 = r1 + c1, r3 = r2 + c2;
-                if (x.x | x.y) {  // rare: a dirty word among the four
-                    const uint32_t e0 = x.x & 0xFFFFu, e1 = x.x >> 16, e2 = x.y & 0xFFFFu, e3 = x.y >> 16;
-                    r1 += e0;
-                    r2 += e0 + e1;
-                    r3 += e0 + e1 + e2;
-                    auto dirty = [&](uint32_t start, uint32_t cnt) -> uint32_t {
-                        const uint32_t old = atomicAdd(&s_alloc, cnt | 0x10000u);
-                        const uint32_t id = old >> 16, off = old & 0xFFFFu;
-                        if (id < uint32_t(C::kDw)) dw[id] = make_uint2(start | (cnt << 16), off);
-                        if (cnt > kMaxBucket) s_crowd = 1;  // duplicate-heavy: not for the quadratic ranking
-                        return 0x8000u | (id & 0x7FFFu);
-                    };
-                    if (e0) r0 = dirty(r0, c0 + e0);
-                    if (e1) r1 = dirty(r1, c1 + e1);
-                    if (e2) r2 = dirty(r2, c2 + e2);
-                    if (e3) r3 = dirty(r3, __popc(a.w) + e3);
-                }
-                pre2[v * 32 + lane] = make_uint2(r0 | (r1 << 16), r2 | (r3 << 16));
-                rowb += rt;
-            }
-        }
-    }
+    // ---- 4. scan (bm_scan): word starts; descriptors of the dirty words
+    bm_scan<W, R, C::kDw>(bm, pre, dw, nW, s_scan, &s_alloc, &s_crowd);
     __syncthreads();
     const uint32_t nd = s_alloc & 0xFFFFu, ndw = s_alloc >> 16;
     if (nd > uint32_t(C::kDirty) || ndw > uint32_t(C::kDw) || s_crowd) {
@@ -493,6 +504,289 @@ __global__ void __launch_bounds__(BmCfg<RS, 1>::kThreads, BmCfg<RS, 1>::kMinBloc
     for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
         local_group_bm<RS, 1>(data, tmp, med.list[i], ks, ctr, spill, med, [] {});
         __syncthreads();  // shared memory free for the next group
+    }
+}
+
+// ---------------------------------------------------------------- 8-B records
+//
+// The bitmap sort for 8-B records (BASELINE C2: bins of ~16 K records, one
+// group each): records stay in registers (coalesced global loads), one CTA of
+// 1024 threads per SM, persistent. The cell of a record is recomputed from its
+// registers where needed (no per-record cell array); final positions are kept
+// in registers (u16 pairs), dirty-word records get theirs from the dense list
+// pass; the output is staged through shared memory (over the dead bitmap) in
+// final order and stored coalesced.
+struct Bm8Cfg {
+    static constexpr int RS = 8;
+    static constexpr int kThreads = 1024;
+    static constexpr int kWarps = kThreads / 32;
+    static constexpr int kCap = LocalCfg<8>::kCap;
+    static constexpr int kIpt = (kCap + kThreads - 1) / kThreads;
+    static constexpr int kCellLog = RG_BM_CELL_LOG;
+#ifndef RG_BM8_BITS
+#define RG_BM8_BITS 19
+#endif
+    static constexpr int kFineBits = RG_BM8_BITS;  // 2^19 cells: 28-32 per record at C2's bins
+    static constexpr int kWords = 1 << (kFineBits - 5);
+    static constexpr int kRows = (kWords + 128 * kWarps - 1) / (128 * kWarps);
+    static_assert(kRows >= 1 && kRows <= 4, "scan rows per warp");
+    static constexpr int kDirty = 4096;  // records of dirty words: {e | id << 16, window}
+    static constexpr int kDw = 2048;     // dirty words
+    static constexpr size_t kBmBytes =
+        size_t(kWords) * 6 + size_t(kDw) * 8 + size_t(kDirty) * 8 + size_t(kDirty) * 2;
+    static constexpr size_t kStageBytes = size_t(kCap) * RS;
+    static constexpr size_t kSmem = kBmBytes > kStageBytes ? kBmBytes : kStageBytes;
+    static_assert(kCap < 32768, "positions are u15");
+};
+
+template <typename Mid>
+__device__ __forceinline__ void local_group_bm8(
+    uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group g, uint32_t ks,
+    LevelCounters* __restrict__ ctr, const GroupList spill, Mid&& mid) {
+    using C = Bm8Cfg;
+    constexpr int RS = 8;
+    constexpr int T = C::kThreads, W = C::kWarps, IPT = C::kIpt, R = C::kRows;
+    extern __shared__ __align__(128) uint8_t smem[];
+    RG_CHK_POISON_SMEM(smem);
+    uint32_t* bm = reinterpret_cast<uint32_t*>(smem);              // [kWords] cell bits
+    uint32_t* pre = bm + C::kWords;                                // [kWords] u16: extras, then starts
+    uint2* dw = reinterpret_cast<uint2*>(pre + C::kWords / 2);     // [kDw] {start | cnt << 16, off | cursor << 16}
+    uint2* dl = dw + C::kDw;                                       // [kDirty] {e | dirty word id << 16, window}
+    uint16_t* dfin = reinterpret_cast<uint16_t*>(dl + C::kDirty);  // [kDirty] final position of list entry i
+    __shared__ uint32_t s_scan[W];
+    __shared__ uint32_t s_wmin, s_wmax, s_alloc, s_crowd;
+
+    const uint32_t n = g.size;
+    const uint8_t* gsrc = (g.parity ? tmp : data) + g.start * RS;
+    uint8_t* dst = data + g.start * RS;
+    const int lane = threadIdx.x & 31;
+    const uint32_t klim = ks < uint32_t(RS) ? ks : uint32_t(RS);
+    if (n <= 1 || g.p >= klim) {
+        if (g.parity)
+            for (uint32_t e = threadIdx.x; e < n; e += T) store_rec<RS>(dst, e, load_rec<RS>(gsrc, e));
+        return;
+    }
+
+    // ---- 1. records into registers; bitmap and counters zeroed
+    Rec<RS> r[IPT];
+    {
+        const uint8_t* tsrc = gsrc + size_t(threadIdx.x) * RS;
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            if (uint32_t(j) * T >= n) break;  // block-uniform
+            if (uint32_t(j) * T + threadIdx.x < n) r[j] = load_rec_stream<RS>(tsrc, uint64_t(j) * T);
+        }
+    }
+    if (threadIdx.x == 0) {
+        s_wmin = 0xFFFFFFFFu;
+        s_wmax = 0u;
+        s_alloc = 0;
+        s_crowd = 0;
+    }
+    uint32_t FB = 32u + uint32_t(C::kCellLog) - __clz(n - 1);  // ceil(log2 n) + kCellLog (n >= 2)
+    FB = FB < 12u ? 12u : (FB > uint32_t(C::kFineBits) ? uint32_t(C::kFineBits) : FB);
+    const uint32_t nW = 1u << (FB - 5);
+    {
+        uint4* z = reinterpret_cast<uint4*>(bm);
+#pragma unroll
+        for (int q = 0; q < (C::kWords / 4 + T - 1) / T; ++q)
+            if (q * T + threadIdx.x < nW / 4) z[q * T + threadIdx.x] = make_uint4(0, 0, 0, 0);
+        uint4* z2 = reinterpret_cast<uint4*>(pre);
+#pragma unroll
+        for (int q = 0; q < (C::kWords / 8 + T - 1) / T; ++q)
+            if (q * T + threadIdx.x < nW / 8) z2[q * T + threadIdx.x] = make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();
+
+    // ---- 2./3. windows (key bytes p..p+3, one byte permute), cell bits
+    const uint32_t nwin = klim - g.p < 4u ? klim - g.p : 4u;
+    const bool beyond = g.p + 4u < klim;
+    uint32_t Ldef[4] = {g.p, g.p + 1, g.p + 2, g.p + 3};
+    const WindowSel ws = make_window_sel(Ldef, nwin, RS / 4, true);
+    const bool known = RG_BM_KNOWN && (g.pad & 0x10000u) != 0u;
+    const uint32_t ncell = 1u << FB;
+    auto mul_of = [&](uint32_t rm1) {
+        return rm1 < ncell ? 0u
+                           : uint32_t(__fdiv_rz(float(ncell) * 4294967296.0f, float(rm1) + 1.0f) * 0.999999f);
+    };
+    auto mark = [&](uint32_t f) {
+        const uint32_t bit = 1u << (f & 31u);
+        const uint32_t old = atomicOr(&bm[f >> 5], bit);
+        if (old & bit) atomicAdd(&pre[f >> 6], 1u << ((f >> 1) & 16u));
+    };
+    uint32_t wmin, mul;
+    if (known) {
+        const uint32_t d0 = g.pad & 0xFFu, d1 = (g.pad >> 8) & 0xFFu;
+        wmin = d0 << 24;
+        mul = mul_of(((d1 - d0 + 1u) << 24) - 1u);
+    } else {
+        uint32_t smn = 0xFFFFFFFFu, smx = 0u;
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            if (uint32_t(j) * T >= n) break;
+            if (uint32_t(j) * T + threadIdx.x < n) {
+                const uint32_t w = rec_window<RS>(r[j], ws);
+                smn = min(smn, w);
+                smx = max(smx, w);
+            }
+        }
+        smn = __reduce_min_sync(0xFFFFFFFFu, smn);
+        smx = __reduce_max_sync(0xFFFFFFFFu, smx);
+        if (lane == 0) {
+            atomicMin(&s_wmin, smn);
+            atomicMax(&s_wmax, smx);
+        }
+        __syncthreads();
+        wmin = s_wmin;
+        const uint32_t rm1 = s_wmax - wmin;
+        if (rm1 == 0 && !beyond) {  // every key equal: stable order is the input order
+            if (g.parity) {
+#pragma unroll
+                for (int j = 0; j < IPT; ++j) {
+                    if (uint32_t(j) * T >= n) break;
+                    const uint32_t e = uint32_t(j) * T + threadIdx.x;
+                    if (e < n) store_rec<RS>(dst, e, r[j]);
+                }
+            }
+            return;
+        }
+        mul = mul_of(rm1);
+    }
+    auto cell_of = [&](const Rec<RS>& v) -> uint32_t {
+        const uint32_t d = rec_window<RS>(v, ws) - wmin;
+        return min(mul ? __umulhi(d, mul) : d, ncell - 1u);
+    };
+    mid();
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        if (uint32_t(j) * T >= n) break;
+        if (uint32_t(j) * T + threadIdx.x < n) mark(cell_of(r[j]));
+    }
+    __syncthreads();
+
+    // ---- 4. scan (bm_scan): word starts; descriptors of the dirty words
+    bm_scan<W, R, C::kDw>(bm, pre, dw, nW, s_scan, &s_alloc, &s_crowd);
+    __syncthreads();
+    const uint32_t nd = s_alloc & 0xFFFFu, ndw = s_alloc >> 16;
+    if (nd > uint32_t(C::kDirty) || ndw > uint32_t(C::kDw) || s_crowd) {
+        // block-uniform; nothing written yet: the bucket sort takes the group
+        if (threadIdx.x == 0) {
+            push_group(spill, g);
+            atomicAdd(&ctr->bm_spill, 1u);
+        }
+        return;
+    }
+
+    // ---- 5. final positions into registers (u16 pairs); records of dirty
+    // words go to their word's list run and remember their list slot
+    const uint16_t* pre16 = reinterpret_cast<const uint16_t*>(pre);
+    uint32_t pp[(IPT + 1) / 2];
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        if ((j & 1) == 0) pp[j / 2] = 0;
+        if (uint32_t(j) * T >= n) continue;  // block-uniform
+        const uint32_t e = uint32_t(j) * T + threadIdx.x;
+        if (e < n) {
+            const uint32_t f = cell_of(r[j]), word = f >> 5;
+            const uint32_t pv = pre16[word];
+            const uint32_t m = bm[word];
+            uint32_t pos;
+            if (pv < 0x8000u) {
+                pos = pv + __popc(m & ((1u << (f & 31u)) - 1u));
+            } else {
+                const uint32_t id = pv & 0x7FFFu;
+                const uint32_t old = atomicAdd(&dw[id].y, 0x10000u);
+                const uint32_t slot = (old & 0xFFFFu) + (old >> 16);
+                dl[slot] = make_uint2(e | (id << 16), rec_window<RS>(r[j], ws));
+                pos = 0x8000u | slot;
+            }
+            pp[j / 2] |= pos << ((j & 1) * 16);
+        }
+    }
+    if (nd) {
+        __syncthreads();
+        // ---- 6. dirty words, densely from the list: rank inside the word's run by
+        // (window, key bytes beyond the window, input index)
+        auto cmp_rest = [&](uint32_t a, uint32_t b) -> int {
+            for (uint32_t q = g.p + 4u; q < klim; ++q) {
+                const uint32_t x = gsrc[size_t(a) * RS + q], y = gsrc[size_t(b) * RS + q];
+                if (x != y) return x < y ? -1 : 1;
+            }
+            return 0;
+        };
+        for (uint32_t i = threadIdx.x; i < nd; i += T) {
+            const uint2 me = dl[i];
+            const uint32_t e = me.x & 0xFFFFu, w = me.y;
+            const uint2 d = dw[me.x >> 16];
+            const uint32_t start = d.x & 0xFFFFu, cnt = d.x >> 16, off = d.y & 0xFFFFu;
+            uint32_t rank = 0;
+            for (uint32_t q = off; q < off + cnt; ++q) {
+                if (q == i) continue;
+                const uint2 o = dl[q];
+                const uint32_t e2 = o.x & 0xFFFFu;
+                bool lt;
+                if (o.y != w) {
+                    lt = o.y < w;
+                } else {
+                    const int c = beyond ? cmp_rest(e2, e) : 0;
+                    lt = c < 0 || (c == 0 && e2 < e);
+                }
+                rank += lt;
+            }
+            dfin[i] = uint16_t(start + rank);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            const uint32_t pos = (pp[j / 2] >> ((j & 1) * 16)) & 0xFFFFu;
+            if (pos & 0x8000u) {
+                const uint32_t fin = dfin[pos & 0x7FFFu];
+                pp[j / 2] = (pp[j / 2] & ~(0xFFFFu << ((j & 1) * 16))) | (fin << ((j & 1) * 16));
+            }
+        }
+    }
+    __syncthreads();  // the bitmap structures are dead: the stage takes their place
+
+    // ---- 7. output staged in final order, stored coalesced (all reads of the
+    // source are done: safe in place)
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        if (uint32_t(j) * T >= n) break;
+        if (uint32_t(j) * T + threadIdx.x < n)
+            st_smem_rec<RS>(smem, (pp[j / 2] >> ((j & 1) * 16)) & 0xFFFFu, r[j]);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += T) store_rec<RS>(dst, i, ld_smem_rec<RS>(smem, i));
+    if (threadIdx.x == 0) atomicAdd(&ctr->moved_local, (unsigned long long)n);
+}
+
+__global__ void __launch_bounds__(Bm8Cfg::kThreads, 1) k_local_bm8(
+    uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group* __restrict__ groups,
+    uint32_t n_groups, uint32_t ks, LevelCounters* __restrict__ ctr, GroupList spill) {
+    __shared__ __align__(16) Group s_g[2];
+    uint32_t i = blockIdx.x;
+    if (i >= n_groups) return;
+    if (threadIdx.x == 0) s_g[0] = groups[i];
+    __syncthreads();
+    for (int buf = 0; i < n_groups; buf ^= 1) {
+        const uint32_t nx = i + gridDim.x;
+        const bool more = nx < n_groups;
+        if (threadIdx.x == 0 && more) {
+            for (int q = 0; q < int(sizeof(Group) / 8); ++q)
+                cp_async8(reinterpret_cast<uint8_t*>(&s_g[buf ^ 1]) + 8 * q,
+                          reinterpret_cast<const uint8_t*>(&groups[nx]) + 8 * q);
+        }
+        const Group g = s_g[buf];
+        auto mid = [&] {
+            if (threadIdx.x == 0 && more) {
+                cp_async_wait_all();
+                prefetch_group_l2<8>(data, tmp, s_g[buf ^ 1]);
+            }
+        };
+        local_group_bm8(data, tmp, g, ks, ctr, spill, mid);
+        if (threadIdx.x == 0 && more) cp_async_wait_all();
+        __syncthreads();  // shared memory free for the next group; its descriptor visible
+        i = nx;
     }
 }
 

@@ -607,6 +607,9 @@ int grid_for(uint64_t n, int threads, int per_sm) {
 #ifndef RG_LOC_BM
 #define RG_LOC_BM 1
 #endif
+#ifndef RG_LOC_BM8
+#define RG_LOC_BM8 1
+#endif
 template <int RS>
 constexpr uint32_t local_cap() {
     return LocalCfg<RS>::kCap;
@@ -649,7 +652,7 @@ void ensure_caps(Workspace& ws, uint64_t n, uint64_t extra_segs = 0) {
     ws.status.ensure((c.tiles / kScanChunk + 1) * kRadix);
     ws.groups.ensure(c.groups);
     ws.spill.ensure(c.groups);
-    if constexpr (RS != 8) ws.spill_bm.ensure(c.groups);
+    ws.spill_bm.ensure(c.groups);
     if constexpr (RS != 8) ws.spill_med.ensure(c.groups);
     ws.n_spill.ensure(4);  // ([0] read back as the low half of one 8-B word)
     ws.copies.ensure(c.copies);
@@ -662,11 +665,14 @@ void set_attrs(Workspace& ws) {
                                   int(LocalCfg<RS>::kSmem)));
     RG_CHECK(cudaFuncSetAttribute(k_local<RS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(LocalCfg<RS>::kSmem)));
-    if constexpr (RS != 8) {
+    RG_CHECK(cudaFuncSetAttribute(k_local_list<RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(LocalCfg<RS>::kSmem)));
+    if constexpr (RS == 8) {
+        RG_CHECK(cudaFuncSetAttribute(k_local_bm8, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(Bm8Cfg::kSmem)));
+    } else {
         RG_CHECK(cudaFuncSetAttribute(k_local_bm<RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(BmCfg<RS>::kSmem)));
-        RG_CHECK(cudaFuncSetAttribute(k_local_list<RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(LocalCfg<RS>::kSmem)));
         if constexpr (kBmHasBig<RS>)
             RG_CHECK(cudaFuncSetAttribute(k_local_bm_med<RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           int(BmCfg<RS, 1>::kSmem)));
@@ -799,7 +805,24 @@ void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, 
     // one CTA per SM: persistent, groups round-robin; two per SM: a CTA per group
     const uint32_t grid = LocalCfg<RS>::kMinBlocks == 1 ? std::min<uint32_t>(ngroups, uint32_t(sm_count()))
                                                        : ngroups;
-    if constexpr (RS != 8) {
+    if constexpr (RS == 8) {
+        if (bitmap_local() && RG_LOC_BM8) {
+            RG_CHECK(cudaMemsetAsync(ws.n_spill.p + 1, 0, 2 * sizeof(unsigned int), st));
+            const GroupList spill{ws.spill_bm.p, ws.n_spill.p + 1, uint32_t(ws.spill_bm.cap)};
+            const uint32_t pgrid = std::min<uint32_t>(ngroups, uint32_t(sm_count()));
+            k_local_bm8<<<pgrid, Bm8Cfg::kThreads, Bm8Cfg::kSmem, st>>>(data, tmp, ws.groups.p, ngroups, ks,
+                                                                       ctr, spill);
+            note_launch();
+            RG_LAUNCH_CHECK();
+            k_local_list<RS><<<pgrid, LocalCfg<RS>::kThreads, LocalCfg<RS>::kSmem, st>>>(
+                data, tmp, ws.spill_bm.p, ws.n_spill.p + 1, uint32_t(ws.spill_bm.cap), ks, ctr, ws.spill.p,
+                ws.n_spill.p, uint32_t(ws.spill.cap));
+            note_launch();
+            RG_LAUNCH_CHECK();
+            ws.prof.end(pe, st);
+            return;
+        }
+    } else {
         if (bitmap_local()) {
             // the bitmap sort first; the groups it hands over (device-counted
             // list) go to the bucket sort right behind it, no host read between

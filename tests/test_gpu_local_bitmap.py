@@ -1,6 +1,7 @@
 """The bitmap local sort (csrc/k_local_bm.cuh) and its hand-over chain:
 
     k_local_bm (groups <= the primary capacity)
+         (8-B records: k_local_bm8, records in registers)
       -> k_local_bm_med (single bins above it, 16-B records)
       -> k_local_list   (bucket sort: groups whose shared cells outgrow the lists)
       -> k_local<.., true> (LSD fallback: crowded buckets)
@@ -32,8 +33,9 @@ def _check(rg, torch, a, rs, ks):
     return st
 
 
-@pytest.mark.parametrize("rs,ks", [(16, 8), (16, 16), (24, 16), (32, 24), (32, 8)])
-@pytest.mark.parametrize("n", [2, 3, 31, 127, 128, 129, 1000, 1791, 1792, 1793, 2048, 2500, 3584])
+@pytest.mark.parametrize("rs,ks", [(8, 8), (8, 5), (16, 8), (16, 16), (24, 16), (32, 24), (32, 8)])
+@pytest.mark.parametrize("n", [2, 3, 31, 127, 128, 129, 1000, 1791, 1792, 1793, 2048, 2500, 3584, 16384,
+                               18432])
 def test_single_group_uniform_keys_stay_in_the_bitmap_sort(rg, torch_cuda, rs, ks, n):
     if n > rg.local_capacity(rs):
         pytest.skip("above the local-sort capacity of this record size")
@@ -43,7 +45,7 @@ def test_single_group_uniform_keys_stay_in_the_bitmap_sort(rg, torch_cuda, rs, k
     assert st["local_records"] == n, st
 
 
-@pytest.mark.parametrize("rs,ks", [(16, 8), (24, 16), (32, 24)])
+@pytest.mark.parametrize("rs,ks", [(8, 8), (16, 8), (24, 16), (32, 24)])
 def test_million_uniform_records_no_spill(rg, torch_cuda, rs, ks):
     n = 1 << 20
     a = make_input(n, rs, ks, 0xB17B17 + rs)
@@ -51,7 +53,7 @@ def test_million_uniform_records_no_spill(rg, torch_cuda, rs, ks):
     assert st["bitmap_spill_groups"] == 0, st
 
 
-@pytest.mark.parametrize("rs,ks", [(16, 8), (24, 16), (32, 24)])
+@pytest.mark.parametrize("rs,ks", [(8, 8), (16, 8), (24, 16), (32, 24)])
 @pytest.mark.parametrize("copies", [2, 3, 8])
 def test_every_key_repeated_goes_to_the_bucket_sort(rg, torch_cuda, rs, ks, copies):
     """Each key `copies` times: every cell is shared, the dirty lists overflow
@@ -68,7 +70,8 @@ def test_every_key_repeated_goes_to_the_bucket_sort(rg, torch_cuda, rs, ks, copi
     assert st["bitmap_spill_groups"] > 0, st
 
 
-@pytest.mark.parametrize("rs,ks,n", [(16, 8, 1500), (16, 8, 3000), (24, 16, 2000), (32, 24, 4000)])
+@pytest.mark.parametrize("rs,ks,n", [(8, 8, 12000), (16, 8, 1500), (16, 8, 3000), (24, 16, 2000),
+                                     (32, 24, 4000)])
 def test_few_distinct_keys_reach_the_lsd_fallback(rg, torch_cuda, rs, ks, n):
     """One group whose keys differ only in the last key byte (7 values): every
     window is equal, the one shared cell is crowded -> bucket sort -> crowded
@@ -82,7 +85,7 @@ def test_few_distinct_keys_reach_the_lsd_fallback(rg, torch_cuda, rs, ks, n):
     assert st["bitmap_spill_groups"] == 1 and st["fallback_groups"] == 1, st
 
 
-@pytest.mark.parametrize("rs,ks", [(16, 8), (16, 16), (24, 16), (32, 24)])
+@pytest.mark.parametrize("rs,ks", [(8, 8), (16, 8), (16, 16), (24, 16), (32, 24)])
 def test_shared_cells_resolved_by_bytes_beyond_the_window(rg, torch_cuda, rs, ks):
     """Pairs of records with equal 4-byte windows that differ only in later key
     bytes (and exact duplicates): the dense dirty-word pass must compare the
@@ -143,7 +146,7 @@ def test_bucket_sort_alone_still_matches(rg, torch_cuda, monkeypatch):
     """RADULS_GPU_LOCAL=bucket: the bucket sort takes every group (the local
     sort before the bitmap sort existed)."""
     monkeypatch.setenv("RADULS_GPU_LOCAL", "bucket")
-    for rs, ks, n in [(16, 8, 1 << 18), (32, 24, 1 << 17), (24, 16, 50000)]:
+    for rs, ks, n in [(8, 8, 1 << 18), (16, 8, 1 << 18), (32, 24, 1 << 17), (24, 16, 50000)]:
         a = make_input(n, rs, ks, 0xB0C4 + rs)
         st = _check(rg, torch_cuda, a, rs, ks)
         assert st["bitmap_spill_groups"] == 0, st
