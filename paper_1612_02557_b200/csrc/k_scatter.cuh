@@ -52,12 +52,15 @@ namespace rg {
 #ifndef RG_SC_U4
 #define RG_SC_U4 11
 #endif
+#ifndef RG_SC_ITEMS16
+#define RG_SC_ITEMS16 11
+#endif
 constexpr int kScUnroll = RG_SC_U4;  // write-out loop unroll (11 vs 4: C1 -1%, C2 -1.2%, C5 -0.5%)
 
 template <int RS>
 struct ScatterCfg {
     static constexpr int kThreads = 256;
-    static constexpr int kItems = RS == 8 ? 20 : RS == 16 ? 11 : RS == 24 ? 7 : 6;
+    static constexpr int kItems = RS == 8 ? 20 : RS == 16 ? RG_SC_ITEMS16 : RS == 24 ? 7 : 6;
     static constexpr int kTile = kThreads * kItems;
     static constexpr int kWarps = kThreads / 32;
     static constexpr int kStages = RG_SC_STAGES;  // tile buffers in the TMA ring

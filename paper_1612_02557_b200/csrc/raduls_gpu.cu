@@ -770,7 +770,7 @@ void launch_scatter(Workspace& ws, uint8_t* data, uint8_t* tmp, int cur, uint32_
                     const unsigned long long* dig_dst = nullptr, uint8_t* nd = nullptr,
                     const uint8_t* nd_in = nullptr, bool stable_ballot = false,
                     const Piece* pieces = nullptr) {
-    const uint32_t grid = std::min<uint32_t>(ntiles, uint32_t(sm_count()) * 2);
+    const uint32_t grid = std::min<uint32_t>(ntiles, uint32_t(sm_count()) * ScatterCfg<RS>::kCtas);
     const size_t smem = (kMap || kPeer) ? ScatterCfg<RS>::kSmem : ScatterCfg<RS>::kSmemPlain;
     const bool atomic = !stable_ballot && atomic_rank_ok(ws);
     const int pe = ws.prof.begin(K_SCATTER, st);

@@ -6,8 +6,11 @@ the oracle so a run that "passes" the tool also sorted correctly.
 Kernels reached: k_sample_andor, k_set_seg0/k_check_seg0, k_tile_hist (TMA
 ring, rs 16/24/32), k_tile_hist_reg (rs 8), k_tile_hist_nd (digit-array
 levels), k_tile_scan (look-back), k_plan, k_scatter (plain, digit-array
-TMA at rs 32, map, peer; atomic and ballot ranking), k_local (fast and the
-LSD fallback), k_copy_back, k_publish, k_rank_selftest, k_gen, k_digest,
+TMA at rs 32, map, peer; atomic and ballot ranking), k_local_bm (bitmap local
+sort: clean and dirty words), k_local_bm_med (single bins above the primary
+capacity), k_local_bm8 (8-B records), k_local_list (bucket sort over the
+handed-over groups), k_local (the bucket sort alone with
+RADULS_GPU_LOCAL=bucket, and the LSD fallback), k_copy_back, k_publish, k_rank_selftest, k_gen, k_digest,
 k_check_sorted, k_andor, k_prefix_hist, k_sample_prefix_hist, k_map_to_u8.
 
     python scripts/sanitize_driver.py [--quick]
@@ -50,8 +53,23 @@ def main():
     check_sort(make_input(1 << (18 - sh), 32, 24, 0x5EED0004), 32, 24, "c4-shape")
     # (24,16)
     check_sort(make_input(1 << (17 - sh), 24, 16, 0x5EED0005), 24, 16, "rs24")
-    # duplicate-heavy: crowded local buckets -> the LSD fallback instance
+    # duplicate-heavy: shared cells outgrow the lists -> bucket sort; crowded
+    # buckets -> the LSD fallback instance
     check_sort(make_input(200_000, 16, 8, 9, universe=3000), 16, 8, "fallback")
+    check_sort(make_input(200_000, 8, 8, 9, universe=3000), 8, 8, "fallback-8")
+    check_sort(make_input(150_000, 16, 8, 10, universe=60_000), 16, 8, "pairs")
+    # bins of ~3000 16-B records: groups of their own for the big bitmap instance
+    a = make_input(48 * 3000, 16, 8, 0x3ED)
+    r = a.reshape(-1, 16)
+    r[:, 0] = 0
+    r[:, 1] = np.repeat(np.arange(48, dtype=np.uint8), 3000)[np.random.default_rng(3).permutation(48 * 3000)]
+    check_sort(a, 16, 8, "medium-bins")
+    # the bucket sort alone (every group), as before the bitmap sort
+    os.environ["RADULS_GPU_LOCAL"] = "bucket"
+    check_sort(make_input(1 << (18 - sh), 16, 8, 0x5EED0011), 16, 8, "bucket-16")
+    check_sort(make_input(1 << (18 - sh), 8, 8, 0x5EED0012), 8, 8, "bucket-8")
+    check_sort(make_input(1 << (17 - sh), 32, 24, 0x5EED0013), 32, 24, "bucket-32")
+    del os.environ["RADULS_GPU_LOCAL"]
     # constant trailing key byte after a split -> copy-back of finished bins
     a = make_input(1 << 17, 16, 2, 42)
     r = a.reshape(-1, 16)
