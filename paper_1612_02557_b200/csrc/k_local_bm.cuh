@@ -9,23 +9,34 @@
 // The bucket sort of k_local.cuh spends ~150 of its ~247 thread instructions
 // per record on putting record ids into bucket order and ranking every record
 // against its bucket's neighbours (dependent shared-memory loads). Here the
-// 32-bit key window of every record is mapped linearly (monotone) onto a fine
-// grid of ~64 n cells, one BIT per cell:
-//   * histogram: one atomicOr per record sets its cell's bit. A record that
-//     finds the bit already set (two records in one cell: ~1.6% of random
-//     records) bumps a u16 counter of its 32-cell bitmap word;
-//   * scan: warp-cooperative prefix sum over the words of popc(word) + counter,
-//     the word's start stored as a u16 with bit 15 = "this word holds a
-//     shared cell" (a dirty word);
+// 32-bit window of key bytes p..p+3 of every record is mapped linearly
+// (monotone) onto a fine grid of ~32 n cells, one BIT per cell; the window
+// range comes with the group (the planner knows the digit range of byte p), so
+// windows and cell bits are one pass with no barrier before it:
+//   * cells: one atomicOr per record sets its cell's bit. A record that finds
+//     the bit already set (two records in one cell: ~3% of random records)
+//     bumps a u16 counter ("extras") of its 32-cell bitmap word;
+//   * scan (bm_scan): warp-cooperative prefix sum over the words of
+//     popc(word) + extras; the word's start is stored as a u16 in place of
+//     its extras. A word holding a shared cell (a dirty word) gets a
+//     descriptor {start, count, first entry of its run in a dense list} and
+//     its start entry holds 0x8000 | descriptor id;
 //   * rank: a record of a clean word is final at start + popc(bits below its
 //     own) -- two independent shared-memory loads, no neighbour to compare
 //     with, no id scatter -- and is stored to its place at once. Records of
-//     dirty words (all of them, ~3%) go to a short list and are ranked densely
-//     against the list's entries of the same word by (window, key bytes beyond
-//     the window, input index).
-// A group whose dirty records outgrow the list (duplicate-heavy or clustered
-// keys) is handed untouched -- nothing has been written by then -- to the
-// bucket sort (k_local_list below), which may hand it on to the LSD fallback.
+//     dirty words (all of them, ~5%) append themselves to their word's run and
+//     are ranked densely afterwards, each against the few entries of its own
+//     run, by (window, key bytes beyond the window, input index): stable.
+// No search for the varying key bytes: a window holding constant bytes only
+// loses resolution. A group whose dirty records outgrow the lists, or crowd
+// one word (duplicate-heavy, clustered or constant-byte keys), is handed
+// untouched -- nothing has been written by then -- to the bucket sort
+// (k_local_list below) through a device-counted list; that one searches the
+// varying bytes and may hand the group on to the LSD fallback.
+// Shapes: 16-B records, 256 threads, five CTAs per SM, groups of <= 1792
+// records (a single bin between that and LocalCfg::kCap is a group of its
+// own for the 512-thread instance, k_local_bm_med); 24/32-B records in the
+// bucket sort's shapes; 8-B records in registers (k_local_bm8).
 #pragma once
 
 #include "k_local.cuh"
@@ -56,6 +67,13 @@ namespace rg {
 #endif
 #ifndef RG_BM_KNOWN
 #define RG_BM_KNOWN 1
+#endif
+// RG_BM_CHUNKS (16/32-B records): the group's TMA copy is issued as one bulk
+// copy per loop iteration's records (T records), each with its own mbarrier,
+// and the first pass over the records waits chunk by chunk: it runs while the
+// rest of the group is still arriving.
+#ifndef RG_BM_CHUNKS
+#define RG_BM_CHUNKS 0
 #endif
 #ifndef RG_BM_PERSIST
 #define RG_BM_PERSIST 0
@@ -96,11 +114,10 @@ struct BmCfg {
     // scan: every warp owns kRows rows of 128 words
     static constexpr int kRows = (kWords + 128 * kWarps - 1) / (128 * kWarps);
     static_assert(kRows >= 1 && kRows <= 4, "scan rows per warp");
-    static constexpr int kDirty = kCap >= 2048 ? 1024 : 512;  // records of dirty words (u32 entries)
-    static constexpr int kDw = kDirty / 2;                    // dirty words (8-B descriptors)
+    // the dirty-record list holds every record if need be (u16 entries); a dirty
+    // word's descriptor lives in its own bitmap word
     static constexpr int kRecBytes = ((kCap * RS + 16 + 127) / 128) * 128;
-    static constexpr size_t kSmem =
-        size_t(kRecBytes) + size_t(kWords) * 6 + size_t(kDirty) * 4 + size_t(kDw) * 8;
+    static constexpr size_t kSmem = size_t(kRecBytes) + size_t(kWords) * 6 + ((size_t(kCap) * 2 + 15) / 16) * 16;
 };
 
 // Scan over the bitmap words of popc(word) + extras -> every word's start (u16
@@ -112,8 +129,12 @@ struct BmCfg {
 // entry} and its start entry holds 0x8000 | descriptor id; *s_alloc counts
 // dirty records (low half) and dirty words (high half). One block barrier
 // inside; the caller syncs after it.
-template <int W, int R, int kDw>
-__device__ __forceinline__ void bm_scan(const uint32_t* bm, uint32_t* pre, uint2* dw, uint32_t nW,
+// kInBm: no descriptor table -- a dirty word's own bitmap word (its bits are
+// not needed again: all its records go through the list) becomes its
+// descriptor start | count << 16 | cursor << 24, and its start entry holds
+// 0x8000 | first list entry; *s_alloc then counts dirty records only.
+template <int W, int R, int kDw, bool kInBm = false>
+__device__ __forceinline__ void bm_scan(uint32_t* bm, uint32_t* pre, uint2* dw, uint32_t nW,
                                         uint32_t* s_scan, uint32_t* s_alloc, uint32_t* s_crowd) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     {
@@ -169,17 +190,23 @@ __device__ __forceinline__ void bm_scan(const uint32_t* bm, uint32_t* pre, uint2
                     r1 += e0;
                     r2 += e0 + e1;
                     r3 += e0 + e1 + e2;
-                    auto dirty = [&](uint32_t start, uint32_t cnt) -> uint32_t {
-                        const uint32_t old = atomicAdd(s_alloc, cnt | 0x10000u);
-                        const uint32_t id = old >> 16, off = old & 0xFFFFu;
-                        if (id < uint32_t(kDw)) dw[id] = make_uint2(start | (cnt << 16), off);
+                    auto dirty = [&](uint32_t start, uint32_t cnt, uint32_t c) -> uint32_t {
                         if (cnt > kMaxBucket) *s_crowd = 1;  // duplicate-heavy: not for the quadratic ranking
-                        return 0x8000u | (id & 0x7FFFu);
+                        if constexpr (kInBm) {
+                            const uint32_t off = atomicAdd(s_alloc, cnt);
+                            bm[(uint32_t(warp) * R + v) * 128u + 4u * lane + c] = start | (min(cnt, 255u) << 16);
+                            return 0x8000u | (off & 0x7FFFu);
+                        } else {
+                            const uint32_t old = atomicAdd(s_alloc, cnt | 0x10000u);
+                            const uint32_t id = old >> 16, off = old & 0xFFFFu;
+                            if (id < uint32_t(kDw)) dw[id] = make_uint2(start | (cnt << 16), off);
+                            return 0x8000u | (id & 0x7FFFu);
+                        }
                     };
-                    if (e0) r0 = dirty(r0, c0 + e0);
-                    if (e1) r1 = dirty(r1, c1 + e1);
-                    if (e2) r2 = dirty(r2, c2 + e2);
-                    if (e3) r3 = dirty(r3, __popc(a.w) + e3);
+                    if (e0) r0 = dirty(r0, c0 + e0, 0);
+                    if (e1) r1 = dirty(r1, c1 + e1, 1);
+                    if (e2) r2 = dirty(r2, c2 + e2, 2);
+                    if (e3) r3 = dirty(r3, __popc(a.w) + e3, 3);
                 }
                 pre2[v * 32 + lane] = make_uint2(r0 | (r1 << 16), r2 | (r3 << 16));
                 rowb += rt;
@@ -214,11 +241,12 @@ __device__ __forceinline__ void local_group_bm(
     RG_CHK_POISON_SMEM(smem);
     uint32_t* bm = reinterpret_cast<uint32_t*>(smem + C::kRecBytes);  // [kWords] cell bits
     uint32_t* pre = bm + C::kWords;                                   // [kWords] u16: extras, then starts
-    uint2* dw = reinterpret_cast<uint2*>(pre + C::kWords / 2);        // [kDw] {start | cnt << 16, off | cursor << 16}
-    uint32_t* dl = reinterpret_cast<uint32_t*>(dw + C::kDw);          // [kDirty] e | dirty word id << 16
+    uint16_t* dl = reinterpret_cast<uint16_t*>(pre + C::kWords / 2);  // [kCap] records of dirty words, run by run
     __shared__ uint32_t s_scan[W];
     __shared__ uint32_t s_wmin, s_wmax, s_alloc, s_crowd;
-    __shared__ __align__(8) unsigned long long s_bar;
+    constexpr bool kChunks = RG_BM_CHUNKS && RS % 16 == 0;  // (16-B aligned records: no head bytes)
+    __shared__ __align__(8) unsigned long long s_barv[kChunks ? IPT : 1];
+    unsigned long long& s_bar = s_barv[0];
 
     const uint32_t n = g.size;
     const uint8_t* gsrc = (g.parity ? tmp : data) + g.start * RS;
@@ -240,7 +268,24 @@ __device__ __forceinline__ void local_group_bm(
     // ---- 1. the group on chip (TMA), bitmap and counters zeroed meanwhile
     const uint32_t head = uint32_t(reinterpret_cast<uintptr_t>(gsrc) & 15u);
     const uint8_t* recs = smem + head;
+    const bool chunks = kChunks && head == 0;  // (a base pointer that is only 8-B aligned: one copy)
     if (threadIdx.x == 0) {
+        if (chunks) {
+            const uint32_t bytes = n * RS;
+            constexpr uint32_t CH = uint32_t(T) * RS;  // one loop iteration's records
+#pragma unroll
+            for (int j = 0; j < IPT; ++j)
+                if (uint32_t(j) * CH < bytes) mbar_init(&s_barv[j], 1);
+            fence_mbar_init();
+#pragma unroll
+            for (int j = 0; j < IPT; ++j) {
+                if (uint32_t(j) * CH < bytes) {
+                    const uint32_t sz = min(CH, bytes - uint32_t(j) * CH);
+                    mbar_arrive_expect_tx(&s_barv[j], sz);
+                    tma_load_1d_h<RG_HINT_LOCAL>(smem + j * CH, gsrc + j * CH, sz, &s_barv[j]);
+                }
+            }
+        } else {
         mbar_init(&s_bar, 1);
         fence_mbar_init();
         const uint32_t bytes = n * RS;
@@ -255,6 +300,7 @@ __device__ __forceinline__ void local_group_bm(
         mbar_arrive_expect_tx(&s_bar, body);
         for (uint32_t o = 0; o < body; o += 32768u)
             tma_load_1d_h<RG_HINT_LOCAL>(smem + head + hb + o, gsrc + hb + o, min(32768u, body - o), &s_bar);
+        }
         s_wmin = 0xFFFFFFFFu;
         s_wmax = 0u;
         s_alloc = 0;
@@ -274,7 +320,9 @@ __device__ __forceinline__ void local_group_bm(
         for (int q = 0; q < (C::kWords / 8 + T - 1) / T; ++q)
             if (q * T + threadIdx.x < nW / 8) z2[q * T + threadIdx.x] = make_uint4(0, 0, 0, 0);
     }
-    if constexpr (RG_BM_WAIT1) {
+    if (chunks) {
+        __syncthreads();  // (the first pass waits per chunk)
+    } else if constexpr (RG_BM_WAIT1) {
         if (threadIdx.x == 0) mbar_wait(&s_bar, 0);
         __syncthreads();
     } else {
@@ -309,14 +357,16 @@ __device__ __forceinline__ void local_group_bm(
         const uint32_t old = atomicOr(&bm[f >> 5], bit);
         if (old & bit) atomicAdd(&pre[f >> 6], 1u << ((f >> 1) & 16u));
     };
+    uint32_t wmin, mul;
     if (known) {
         const uint32_t d0 = g.pad & 0xFFu, d1 = (g.pad >> 8) & 0xFFu;
-        const uint32_t wmin = d0 << 24, rm1 = ((d1 - d0 + 1u) << 24) - 1u;
-        const uint32_t mul = mul_of(rm1);
+        wmin = d0 << 24;
+        mul = mul_of(((d1 - d0 + 1u) << 24) - 1u);
         mid();
 #pragma unroll
         for (int j = 0; j < IPT; ++j) {
             if (uint32_t(j) * T >= n) break;  // block-uniform
+            if (chunks) mbar_wait(&s_barv[j], 0);
             const uint32_t e = uint32_t(j) * T + threadIdx.x;
             if (e < n) {
                 const uint32_t d = rec_window<RS>(ld_smem_rec<RS>(recs, e), ws) - wmin;
@@ -331,6 +381,7 @@ __device__ __forceinline__ void local_group_bm(
 #pragma unroll
         for (int j = 0; j < IPT; ++j) {
             if (uint32_t(j) * T >= n) break;  // block-uniform
+            if (chunks) mbar_wait(&s_barv[j], 0);
             const uint32_t e = uint32_t(j) * T + threadIdx.x;
             if (e < n) {
                 const uint32_t w = rec_window<RS>(ld_smem_rec<RS>(recs, e), ws);
@@ -346,7 +397,7 @@ __device__ __forceinline__ void local_group_bm(
             atomicMax(&s_wmax, smx);
         }
         __syncthreads();
-        const uint32_t wmin = s_wmin;
+        wmin = s_wmin;
         const uint32_t rm1 = s_wmax - wmin;  // range - 1
         if (rm1 == 0 && !beyond) {           // every key equal: stable order is the input order
             if (g.parity) {
@@ -359,7 +410,7 @@ __device__ __forceinline__ void local_group_bm(
             }
             return;
         }
-        const uint32_t mul = mul_of(rm1);
+        mul = mul_of(rm1);
         mid();
 #pragma unroll
         for (int j = 0; j < IPT; ++j) {
@@ -367,7 +418,7 @@ __device__ __forceinline__ void local_group_bm(
             const uint32_t e = uint32_t(j) * T + threadIdx.x;
             if (e < n) {
                 const uint32_t d = wv[j] - wmin;
-                const uint32_t f = mul ? __umulhi(d, mul) : d;
+                const uint32_t f = min(mul ? __umulhi(d, mul) : d, ncell - 1u);
                 fc[j] = f;
                 mark(f);
             }
@@ -375,11 +426,11 @@ __device__ __forceinline__ void local_group_bm(
     }
     __syncthreads();
 
-    // ---- 4. scan (bm_scan): word starts; descriptors of the dirty words
-    bm_scan<W, R, C::kDw>(bm, pre, dw, nW, s_scan, &s_alloc, &s_crowd);
+    // ---- 4. scan (bm_scan): word starts; a dirty word's descriptor in its bitmap word
+    bm_scan<W, R, 0, true>(bm, pre, nullptr, nW, s_scan, &s_alloc, &s_crowd);
     __syncthreads();
-    const uint32_t nd = s_alloc & 0xFFFFu, ndw = s_alloc >> 16;
-    if (nd > uint32_t(C::kDirty) || ndw > uint32_t(C::kDw) || s_crowd) {
+    const uint32_t nd = s_alloc;  // records of dirty words (<= n: the list holds them all)
+    if (s_crowd) {
         // block-uniform; nothing written yet: the bucket sort takes the group
         if (threadIdx.x == 0) {
             push_group(spill, g);
@@ -390,7 +441,8 @@ __device__ __forceinline__ void local_group_bm(
 
     // ---- 5. clean words: final position = the word's start + bits below the
     // record's own; stored at once (one uncoalesced vector store per record,
-    // the group's lines complete in L2). Dirty words: into the word's list run.
+    // the group's lines complete in L2). Dirty words: into the word's list run
+    // (cursor in the descriptor's top byte).
     const uint16_t* pre16 = reinterpret_cast<const uint16_t*>(pre);
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
@@ -404,9 +456,8 @@ __device__ __forceinline__ void local_group_bm(
                 const uint32_t pos = pv + __popc(m & ((1u << (f & 31u)) - 1u));
                 store_rec<RS>(dst, pos, ld_smem_rec<RS>(recs, e));
             } else {
-                const uint32_t id = pv & 0x7FFFu;
-                const uint32_t old = atomicAdd(&dw[id].y, 0x10000u);
-                dl[(old & 0xFFFFu) + (old >> 16)] = e | (id << 16);
+                const uint32_t old = atomicAdd(&bm[word], 1u << 24);
+                dl[(pv & 0x7FFFu) + (old >> 24)] = uint16_t(e);
             }
         }
     }
@@ -415,8 +466,9 @@ __device__ __forceinline__ void local_group_bm(
         return;
     }
     __syncthreads();
-    // ---- 6. dirty words, densely from the list: each entry ranks itself
-    // among its word's run by (window, key bytes beyond the window, input index)
+    // ---- 6. dirty words, densely from the list: each entry finds its word again
+    // (window -> cell) and ranks itself among the word's run by (window, key
+    // bytes beyond the window, input index)
     {
         auto window_of = [&](uint32_t e) { return rec_window<RS>(ld_smem_rec<RS>(recs, e), ws); };
         auto cmp_rest = [&](uint32_t a, uint32_t b) -> int {
@@ -427,15 +479,17 @@ __device__ __forceinline__ void local_group_bm(
             return 0;
         };
         for (uint32_t i = threadIdx.x; i < nd; i += T) {
-            const uint32_t me = dl[i];
-            const uint32_t e = me & 0xFFFFu;
-            const uint2 d = dw[me >> 16];
-            const uint32_t start = d.x & 0xFFFFu, cnt = d.x >> 16, off = d.y & 0xFFFFu;
+            const uint32_t e = dl[i];
             const uint32_t w = window_of(e);
+            const uint32_t dd = w - wmin;
+            const uint32_t word = min(mul ? __umulhi(dd, mul) : dd, ncell - 1u) >> 5;
+            const uint32_t desc = bm[word];
+            const uint32_t start = desc & 0xFFFFu, cnt = (desc >> 16) & 0xFFu;
+            const uint32_t off = pre16[word] & 0x7FFFu;
             uint32_t rank = 0;
             for (uint32_t q = off; q < off + cnt; ++q) {
                 if (q == i) continue;
-                const uint32_t e2 = dl[q] & 0xFFFFu;
+                const uint32_t e2 = dl[q];
                 const uint32_t w2 = window_of(e2);
                 bool lt;
                 if (w2 != w) {
@@ -530,10 +584,12 @@ struct Bm8Cfg {
     static constexpr int kWords = 1 << (kFineBits - 5);
     static constexpr int kRows = (kWords + 128 * kWarps - 1) / (128 * kWarps);
     static_assert(kRows >= 1 && kRows <= 4, "scan rows per warp");
-    static constexpr int kDirty = 4096;  // records of dirty words: {e | id << 16, window}
-    static constexpr int kDw = 2048;     // dirty words
-    static constexpr size_t kBmBytes =
-        size_t(kWords) * 6 + size_t(kDw) * 8 + size_t(kDirty) * 8 + size_t(kDirty) * 2;
+    // records of dirty words: {e, window} and their final positions (u16); a
+    // dirty word's descriptor lives in its bitmap word. (The records are in
+    // registers: with the windows in the list the dense pass needs no global
+    // loads -- re-reading them from L2 instead cost C2's local sort +11%.)
+    static constexpr int kDirty = 6144;
+    static constexpr size_t kBmBytes = size_t(kWords) * 6 + size_t(kDirty) * (8 + 2);
     static constexpr size_t kStageBytes = size_t(kCap) * RS;
     static constexpr size_t kSmem = kBmBytes > kStageBytes ? kBmBytes : kStageBytes;
     static_assert(kCap < 32768, "positions are u15");
@@ -550,8 +606,7 @@ __device__ __forceinline__ void local_group_bm8(
     RG_CHK_POISON_SMEM(smem);
     uint32_t* bm = reinterpret_cast<uint32_t*>(smem);              // [kWords] cell bits
     uint32_t* pre = bm + C::kWords;                                // [kWords] u16: extras, then starts
-    uint2* dw = reinterpret_cast<uint2*>(pre + C::kWords / 2);     // [kDw] {start | cnt << 16, off | cursor << 16}
-    uint2* dl = dw + C::kDw;                                       // [kDirty] {e | dirty word id << 16, window}
+    uint2* dl = reinterpret_cast<uint2*>(pre + C::kWords / 2);     // [kDirty] {e, window}, run by run
     uint16_t* dfin = reinterpret_cast<uint16_t*>(dl + C::kDirty);  // [kDirty] final position of list entry i
     __shared__ uint32_t s_scan[W];
     __shared__ uint32_t s_wmin, s_wmax, s_alloc, s_crowd;
@@ -664,11 +719,11 @@ __device__ __forceinline__ void local_group_bm8(
     }
     __syncthreads();
 
-    // ---- 4. scan (bm_scan): word starts; descriptors of the dirty words
-    bm_scan<W, R, C::kDw>(bm, pre, dw, nW, s_scan, &s_alloc, &s_crowd);
+    // ---- 4. scan (bm_scan): word starts; a dirty word's descriptor in its bitmap word
+    bm_scan<W, R, 0, true>(bm, pre, nullptr, nW, s_scan, &s_alloc, &s_crowd);
     __syncthreads();
-    const uint32_t nd = s_alloc & 0xFFFFu, ndw = s_alloc >> 16;
-    if (nd > uint32_t(C::kDirty) || ndw > uint32_t(C::kDw) || s_crowd) {
+    const uint32_t nd = s_alloc;  // records of dirty words
+    if (s_crowd || nd > uint32_t(C::kDirty)) {
         // block-uniform; nothing written yet: the bucket sort takes the group
         if (threadIdx.x == 0) {
             push_group(spill, g);
@@ -694,10 +749,9 @@ __device__ __forceinline__ void local_group_bm8(
             if (pv < 0x8000u) {
                 pos = pv + __popc(m & ((1u << (f & 31u)) - 1u));
             } else {
-                const uint32_t id = pv & 0x7FFFu;
-                const uint32_t old = atomicAdd(&dw[id].y, 0x10000u);
-                const uint32_t slot = (old & 0xFFFFu) + (old >> 16);
-                dl[slot] = make_uint2(e | (id << 16), rec_window<RS>(r[j], ws));
+                const uint32_t old = atomicAdd(&bm[word], 1u << 24);
+                const uint32_t slot = (pv & 0x7FFFu) + (old >> 24);
+                dl[slot] = make_uint2(e, rec_window<RS>(r[j], ws));
                 pos = 0x8000u | slot;
             }
             pp[j / 2] |= pos << ((j & 1) * 16);
@@ -705,8 +759,9 @@ __device__ __forceinline__ void local_group_bm8(
     }
     if (nd) {
         __syncthreads();
-        // ---- 6. dirty words, densely from the list: rank inside the word's run by
-        // (window, key bytes beyond the window, input index)
+        // ---- 6. dirty words, densely from the list: each entry finds its word
+        // (window -> cell) and ranks itself among the word's run by (window, key
+        // bytes beyond the window, input index)
         auto cmp_rest = [&](uint32_t a, uint32_t b) -> int {
             for (uint32_t q = g.p + 4u; q < klim; ++q) {
                 const uint32_t x = gsrc[size_t(a) * RS + q], y = gsrc[size_t(b) * RS + q];
@@ -716,20 +771,22 @@ __device__ __forceinline__ void local_group_bm8(
         };
         for (uint32_t i = threadIdx.x; i < nd; i += T) {
             const uint2 me = dl[i];
-            const uint32_t e = me.x & 0xFFFFu, w = me.y;
-            const uint2 d = dw[me.x >> 16];
-            const uint32_t start = d.x & 0xFFFFu, cnt = d.x >> 16, off = d.y & 0xFFFFu;
+            const uint32_t e = me.x, w = me.y;
+            const uint32_t dd = w - wmin;
+            const uint32_t word = min(mul ? __umulhi(dd, mul) : dd, ncell - 1u) >> 5;
+            const uint32_t desc = bm[word];
+            const uint32_t start = desc & 0xFFFFu, cnt = (desc >> 16) & 0xFFu;
+            const uint32_t off = pre16[word] & 0x7FFFu;
             uint32_t rank = 0;
             for (uint32_t q = off; q < off + cnt; ++q) {
                 if (q == i) continue;
                 const uint2 o = dl[q];
-                const uint32_t e2 = o.x & 0xFFFFu;
                 bool lt;
                 if (o.y != w) {
                     lt = o.y < w;
                 } else {
-                    const int c = beyond ? cmp_rest(e2, e) : 0;
-                    lt = c < 0 || (c == 0 && e2 < e);
+                    const int c = beyond ? cmp_rest(o.x, e) : 0;
+                    lt = c < 0 || (c == 0 && o.x < e);
                 }
                 rank += lt;
             }

@@ -14,9 +14,17 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
         "lts__throughput.avg.pct_of_peak_sustained_elapsed",
         "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
-        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__inst_executed.avg.per_cycle_active"]
-out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True,
-                     text=True, check=True).stdout
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__inst_executed.avg.per_cycle_active",
+        "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
+        "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio"]
+if sys.argv[1].endswith(".csv"):  # already exported: ncu -i X.ncu-rep --page raw --csv
+    out = open(sys.argv[1]).read()
+else:
+    out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr, units, vals = rows[0], rows[1], rows[2]
 ix = {h: i for i, h in enumerate(hdr)}

@@ -10,7 +10,9 @@ import csv
 import json
 import sys
 
-CLASS = {"k_scatter": "scatter", "k_local": "local_sort", "k_tile_hist": "tile_hist",
+CLASS = {"k_scatter": "scatter", "k_local": "local_sort", "k_local_bm": "local_sort", "k_local_bm8": "local_sort",
+         "k_local_bm_med": "local_sort_handover", "k_local_list": "local_sort_handover",
+         "k_tile_hist": "tile_hist",
          "k_tile_hist_nd": "tile_hist", "k_tile_hist_reg": "tile_hist", "k_tile_scan": "tile_scan",
          "k_plan": "plan", "k_copy_back": "copy_back"}
 rows = list(csv.reader(open(sys.argv[1])))

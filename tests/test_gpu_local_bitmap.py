@@ -55,10 +55,11 @@ def test_million_uniform_records_no_spill(rg, torch_cuda, rs, ks):
 
 @pytest.mark.parametrize("rs,ks", [(8, 8), (16, 8), (24, 16), (32, 24)])
 @pytest.mark.parametrize("copies", [2, 3, 8])
-def test_every_key_repeated_goes_to_the_bucket_sort(rg, torch_cuda, rs, ks, copies):
-    """Each key `copies` times: every cell is shared, the dirty lists overflow
-    and the groups are handed to the bucket sort; order among equal keys is the
-    input order (stable)."""
+def test_every_key_repeated_stays_in_the_dirty_word_lists(rg, torch_cuda, rs, ks, copies):
+    """Each key `copies` times: every cell is shared and every word dirty; the
+    lists hold all records of a group (8-B records: up to 6144), so the dense
+    pass orders them — equal keys in input order (stable) — without the
+    bucket sort's LSD fallback."""
     n = 1 << 16
     a = make_input(n, rs, ks, 0xD0B1E + copies + rs)
     r = a.reshape(n, rs)
@@ -66,6 +67,21 @@ def test_every_key_repeated_goes_to_the_bucket_sort(rg, torch_cuda, rs, ks, copi
     for c in range(copies):
         seg = r[c * (n // copies):(c + 1) * (n // copies)]
         seg[:, :ks] = base[: seg.shape[0]]
+    st = _check(rg, torch_cuda, a, rs, ks)
+    assert st["fallback_groups"] == 0, st
+    if rs != 8 and copies <= 3:
+        assert st["bitmap_spill_groups"] == 0, st
+
+
+@pytest.mark.parametrize("rs,ks", [(8, 8), (16, 8)])
+def test_sixty_four_copies_of_each_key_crowd_the_words(rg, torch_cuda, rs, ks):
+    """64 copies of each key: one cell holds more than 32 records, the group
+    is handed to the bucket sort and on to the LSD fallback."""
+    n = 1 << 16
+    a = make_input(n, rs, ks, 0xC40D + rs)
+    r = a.reshape(n, rs)
+    base = r[: n // 64, :ks].copy()
+    r[:, :ks] = np.tile(base, (64, 1))
     st = _check(rg, torch_cuda, a, rs, ks)
     assert st["bitmap_spill_groups"] > 0, st
 
