@@ -1375,7 +1375,7 @@ const char* raduls_gpu_strerror(int code) {
 
 int raduls_gpu_layout_valid(uint32_t rs, uint32_t ks) { return layout_ok(rs, ks) ? 1 : 0; }
 
-uint32_t raduls_gpu_version(void) { return 0x000100u; }
+uint32_t raduls_gpu_version(void) { return 0x000200u; }  // 0x0200: raduls_gpu_stats + bitmap_spill_groups
 
 int raduls_gpu_sort(void* d_data, void* d_tmp, uint64_t n, uint32_t rs, uint32_t ks, void* stream) {
     if (!layout_ok(rs, ks) || mul_overflows(n, rs) || n > kMaxRecords) return RADULS_GPU_EINVAL;

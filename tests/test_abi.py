@@ -70,7 +70,7 @@ def test_invalid_arguments_rejected_without_gpu():
 def test_version_and_stats_struct():
     L = _lib.load()
     assert L.raduls_gpu_version() >= 0x000100
-    assert C.sizeof(_lib.Stats) == 4 + 4 + 7 * 8
+    assert C.sizeof(_lib.Stats) == 4 + 4 + 8 * 8  # (round 2: + bitmap_spill_groups)
 
 
 def test_lsd_rejects_bad_config_and_layouts_without_gpu():
