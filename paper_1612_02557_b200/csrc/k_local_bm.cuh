@@ -18,9 +18,10 @@
 //     bumps a u16 counter ("extras") of its 32-cell bitmap word;
 //   * scan (bm_scan): warp-cooperative prefix sum over the words of
 //     popc(word) + extras; the word's start is stored as a u16 in place of
-//     its extras. A word holding a shared cell (a dirty word) gets a
-//     descriptor {start, count, first entry of its run in a dense list} and
-//     its start entry holds 0x8000 | descriptor id;
+//     its extras. A word holding a shared cell (a dirty word) turns its own
+//     bitmap word into a descriptor {start, count, cursor} and its start
+//     entry into 0x8000 | the first entry of its run in a dense list (u16
+//     record ids; the list can hold every record of the group);
 //   * rank: a record of a clean word is final at start + popc(bits below its
 //     own) -- two independent shared-memory loads, no neighbour to compare
 //     with, no id scatter -- and is stored to its place at once. Records of
@@ -28,8 +29,8 @@
 //     are ranked densely afterwards, each against the few entries of its own
 //     run, by (window, key bytes beyond the window, input index): stable.
 // No search for the varying key bytes: a window holding constant bytes only
-// loses resolution. A group whose dirty records outgrow the lists, or crowd
-// one word (duplicate-heavy, clustered or constant-byte keys), is handed
+// loses resolution. A group with more than kMaxBucket records in one word
+// (duplicate-heavy, clustered or constant-byte keys) is handed
 // untouched -- nothing has been written by then -- to the bucket sort
 // (k_local_list below) through a device-counted list; that one searches the
 // varying bytes and may hand the group on to the LSD fallback.
@@ -125,17 +126,15 @@ struct BmCfg {
 // of 128 (those below nW); lane l reads words 4 l..4 l + 3 of each row
 // (conflict-free 16-B / 8-B loads); row sums are scanned across the lanes two
 // rows to a register (u16 halves: sums <= n < 32768). A word with extras (a
-// shared cell) is dirty: it gets a descriptor {start | count << 16, first list
-// entry} and its start entry holds 0x8000 | descriptor id; *s_alloc counts
-// dirty records (low half) and dirty words (high half). One block barrier
+// shared cell) is dirty: its own bitmap word (its bits are not needed again:
+// all its records go through the list) becomes its descriptor start | count
+// << 16 | cursor << 24, and its start entry holds 0x8000 | the first list
+// entry of its run; *s_alloc counts the records of dirty words, *s_crowd is
+// set when one word holds more than kMaxBucket records. One block barrier
 // inside; the caller syncs after it.
-// kInBm: no descriptor table -- a dirty word's own bitmap word (its bits are
-// not needed again: all its records go through the list) becomes its
-// descriptor start | count << 16 | cursor << 24, and its start entry holds
-// 0x8000 | first list entry; *s_alloc then counts dirty records only.
-template <int W, int R, int kDw, bool kInBm = false>
-__device__ __forceinline__ void bm_scan(uint32_t* bm, uint32_t* pre, uint2* dw, uint32_t nW,
-                                        uint32_t* s_scan, uint32_t* s_alloc, uint32_t* s_crowd) {
+template <int W, int R>
+__device__ __forceinline__ void bm_scan(uint32_t* bm, uint32_t* pre, uint32_t nW, uint32_t* s_scan,
+                                        uint32_t* s_alloc, uint32_t* s_crowd) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     {
         const uint4* bm4 = reinterpret_cast<const uint4*>(bm) + warp * (32 * R);
@@ -192,16 +191,9 @@ __device__ __forceinline__ void bm_scan(uint32_t* bm, uint32_t* pre, uint2* dw, 
                     r3 += e0 + e1 + e2;
                     auto dirty = [&](uint32_t start, uint32_t cnt, uint32_t c) -> uint32_t {
                         if (cnt > kMaxBucket) *s_crowd = 1;  // duplicate-heavy: not for the quadratic ranking
-                        if constexpr (kInBm) {
-                            const uint32_t off = atomicAdd(s_alloc, cnt);
-                            bm[(uint32_t(warp) * R + v) * 128u + 4u * lane + c] = start | (min(cnt, 255u) << 16);
-                            return 0x8000u | (off & 0x7FFFu);
-                        } else {
-                            const uint32_t old = atomicAdd(s_alloc, cnt | 0x10000u);
-                            const uint32_t id = old >> 16, off = old & 0xFFFFu;
-                            if (id < uint32_t(kDw)) dw[id] = make_uint2(start | (cnt << 16), off);
-                            return 0x8000u | (id & 0x7FFFu);
-                        }
+                        const uint32_t off = atomicAdd(s_alloc, cnt);
+                        bm[(uint32_t(warp) * R + v) * 128u + 4u * lane + c] = start | (min(cnt, 255u) << 16);
+                        return 0x8000u | (off & 0x7FFFu);
                     };
                     if (e0) r0 = dirty(r0, c0 + e0, 0);
                     if (e1) r1 = dirty(r1, c1 + e1, 1);
@@ -427,7 +419,7 @@ __device__ __forceinline__ void local_group_bm(
     __syncthreads();
 
     // ---- 4. scan (bm_scan): word starts; a dirty word's descriptor in its bitmap word
-    bm_scan<W, R, 0, true>(bm, pre, nullptr, nW, s_scan, &s_alloc, &s_crowd);
+    bm_scan<W, R>(bm, pre, nW, s_scan, &s_alloc, &s_crowd);
     __syncthreads();
     const uint32_t nd = s_alloc;  // records of dirty words (<= n: the list holds them all)
     if (s_crowd) {
@@ -720,7 +712,7 @@ __device__ __forceinline__ void local_group_bm8(
     __syncthreads();
 
     // ---- 4. scan (bm_scan): word starts; a dirty word's descriptor in its bitmap word
-    bm_scan<W, R, 0, true>(bm, pre, nullptr, nW, s_scan, &s_alloc, &s_crowd);
+    bm_scan<W, R>(bm, pre, nW, s_scan, &s_alloc, &s_crowd);
     __syncthreads();
     const uint32_t nd = s_alloc;  // records of dirty words
     if (s_crowd || nd > uint32_t(C::kDirty)) {

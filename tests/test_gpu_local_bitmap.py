@@ -3,7 +3,7 @@
     k_local_bm (groups <= the primary capacity)
          (8-B records: k_local_bm8, records in registers)
       -> k_local_bm_med (single bins above it, 16-B records)
-      -> k_local_list   (bucket sort: groups whose shared cells outgrow the lists)
+      -> k_local_list   (bucket sort: groups with a crowded bitmap word)
       -> k_local<.., true> (LSD fallback: crowded buckets)
 
 Every case is compared byte for byte with the oracle's stable sort
