@@ -25,7 +25,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 # the parity suite minus the 8-64 GiB full-size configs (minutes under the checks)
 PARITY = ["tests/test_gpu_parity.py", "tests/test_gpu_kernels.py", "tests/test_gpu_lsd.py",
-          "tests/test_gpu_local_edges.py", "tests/test_gpu_local_bitmap.py", "tests/test_gpu_digit_array.py", "tests/test_gpu_progressive.py",
+          "tests/test_gpu_local_edges.py", "tests/test_gpu_local_bitmap.py", "tests/test_gpu_fuzz.py", "tests/test_gpu_digit_array.py", "tests/test_gpu_progressive.py",
           "tests/test_gpu_distributed.py", "tests/test_gpu_multi.py"]
 DESELECT = ("not full_size and not c5_full and not concurrent and not frees_its and not allocation_failure "
             "and not bench")
