@@ -10,11 +10,12 @@
 // per record on putting record ids into bucket order and ranking every record
 // against its bucket's neighbours (dependent shared-memory loads). Here the
 // 32-bit window of key bytes p..p+3 of every record is mapped linearly
-// (monotone) onto a fine grid of ~32 n cells, one BIT per cell; the window
+// (monotone) onto a fine grid of ~16 n cells (8-B records: ~32 n), one BIT per
+// cell; the window
 // range comes with the group (the planner knows the digit range of byte p), so
 // windows and cell bits are one pass with no barrier before it:
 //   * cells: one atomicOr per record sets its cell's bit. A record that finds
-//     the bit already set (two records in one cell: ~3% of random records)
+//     the bit already set (two records in one cell: ~6% of random records)
 //     bumps a u16 counter ("extras") of its 32-cell bitmap word;
 //   * scan (bm_scan): warp-cooperative prefix sum over the words of
 //     popc(word) + extras; the word's start is stored as a u16 in place of
@@ -25,7 +26,7 @@
 //   * rank: a record of a clean word is final at start + popc(bits below its
 //     own) -- two independent shared-memory loads, no neighbour to compare
 //     with, no id scatter -- and is stored to its place at once. Records of
-//     dirty words (all of them, ~5%) append themselves to their word's run and
+//     dirty words (all of them, ~12%) append themselves to their word's run and
 //     are ranked densely afterwards, each against the few entries of its own
 //     run, by (window, key bytes beyond the window, input index): stable.
 // No search for the varying key bytes: a window holding constant bytes only
@@ -34,7 +35,7 @@
 // untouched -- nothing has been written by then -- to the bucket sort
 // (k_local_list below) through a device-counted list; that one searches the
 // varying bytes and may hand the group on to the LSD fallback.
-// Shapes: 16-B records, 256 threads, five CTAs per SM, groups of <= 1792
+// Shapes: 16-B records, 256 threads, six CTAs per SM, groups of <= 1728
 // records (a single bin between that and LocalCfg::kCap is a group of its
 // own for the 512-thread instance, k_local_bm_med); 24/32-B records in the
 // bucket sort's shapes; 8-B records in registers (k_local_bm8).
@@ -49,16 +50,18 @@ namespace rg {
 // of at most this capacity (group_cap<RS>()); a single bin between it and the
 // local-sort capacity (LocalCfg::kCap) is a group of its own, taken by the
 // big instance (V = 1: the bucket sort's shape).
-// Measured (C5 local sort, interleaved A/B): 512 threads x 2 CTAs per SM, cap
-// 3584: 38.7 ms; 384 x 3, cap 2560: 36.8 ms; 256 x 5, cap 1792: 31.9 ms.
+// Measured (C5 local sort, interleaved A/B, 32 cells per record): 512 threads
+// x 2 CTAs per SM, cap 3584: 38.7 ms; 384 x 3, cap 2560: 36.8 ms; 256 x 5, cap
+// 1792: 31.9 ms. With 16 cells per record the bitmap shrinks and six CTAs of
+// <= 1728 records fit: C5 30.05 vs 30.9 ms, C1 0.549 vs 0.594 ms.
 #ifndef RG_BM_THREADS
 #define RG_BM_THREADS 256
 #endif
 #ifndef RG_BM_BLOCKS
-#define RG_BM_BLOCKS 5
+#define RG_BM_BLOCKS 6
 #endif
 #ifndef RG_BM_CAP16
-#define RG_BM_CAP16 1792
+#define RG_BM_CAP16 1728
 #endif
 // RG_BM_WAIT1: thread 0 alone waits for the group's TMA copy, the block barrier
 // hands the completion on (no spinning warps). RG_BM_PERSIST: the several-
@@ -85,8 +88,14 @@ namespace rg {
 #ifndef RG_BM_BITS
 #define RG_BM_BITS 0
 #endif
+// cells per record aimed at (log2): shared-memory records 2^4 (measured 2^3 /
+// 2^4 / 2^5: C5 local 33.0 / 30.4 / 30.9 ms, C4 5.94 / 5.14 / 5.34); 8-B
+// records 2^5 (2^4: C2 local 8.13 vs 7.85 ms)
 #ifndef RG_BM_CELL_LOG
-#define RG_BM_CELL_LOG 5
+#define RG_BM_CELL_LOG 4
+#endif
+#ifndef RG_BM8_CELL_LOG
+#define RG_BM8_CELL_LOG 5
 #endif
 
 constexpr int ceil_log2_c(int n) {
@@ -107,7 +116,6 @@ struct BmCfg {
     static_assert(kCap <= L::kCap, "the bucket sort takes over whole groups");
     static constexpr int kIpt = (kCap + kThreads - 1) / kThreads;
     // cells per record aimed at, as a power of two: FB = ceil(log2 n) + kCellLog
-    // (measured at 16 B: 2^5 cells per record C5 local 38.1 ms, 2^4 40.1, 2^6 39.7)
     static constexpr int kCellLog = RG_BM_CELL_LOG;
     // cells = 2^kFineBits at most
     static constexpr int kFineBits = RG_BM_BITS ? RG_BM_BITS : ceil_log2_c(kCap) + kCellLog;
@@ -568,7 +576,7 @@ struct Bm8Cfg {
     static constexpr int kWarps = kThreads / 32;
     static constexpr int kCap = LocalCfg<8>::kCap;
     static constexpr int kIpt = (kCap + kThreads - 1) / kThreads;
-    static constexpr int kCellLog = RG_BM_CELL_LOG;
+    static constexpr int kCellLog = RG_BM8_CELL_LOG;
 #ifndef RG_BM8_BITS
 #define RG_BM8_BITS 19
 #endif
