@@ -35,7 +35,7 @@
 // untouched -- nothing has been written by then -- to the bucket sort
 // (k_local_list below) through a device-counted list; that one searches the
 // varying bytes and may hand the group on to the LSD fallback.
-// Shapes: 16-B records, 256 threads, six CTAs per SM, groups of <= 1728
+// Shapes: 16-B records, 256 threads, five CTAs per SM, groups of <= 2048
 // records (a single bin between that and LocalCfg::kCap is a group of its
 // own for the 512-thread instance, k_local_bm_med); 24/32-B records in the
 // bucket sort's shapes; 8-B records in registers (k_local_bm8).
@@ -52,16 +52,18 @@ namespace rg {
 // big instance (V = 1: the bucket sort's shape).
 // Measured (C5 local sort, interleaved A/B, 32 cells per record): 512 threads
 // x 2 CTAs per SM, cap 3584: 38.7 ms; 384 x 3, cap 2560: 36.8 ms; 256 x 5, cap
-// 1792: 31.9 ms. With 16 cells per record the bitmap shrinks and six CTAs of
-// <= 1728 records fit: C5 30.05 vs 30.9 ms, C1 0.549 vs 0.594 ms.
+// 1792: 31.9 ms. With 16 cells per record the bitmap shrinks: six CTAs of <=
+// 1728 records C5 30.05 vs 30.9 ms, C1 0.549 vs 0.594 ms; five CTAs of <= 2048
+// records (the largest group whose grid stays 2^15 cells) C1 0.533, C3 4.66 vs
+// 4.86 (its 1800-record bins stay in this instance), C5 30.4 vs 30.6 ms.
 #ifndef RG_BM_THREADS
 #define RG_BM_THREADS 256
 #endif
 #ifndef RG_BM_BLOCKS
-#define RG_BM_BLOCKS 6
+#define RG_BM_BLOCKS 5
 #endif
 #ifndef RG_BM_CAP16
-#define RG_BM_CAP16 1728
+#define RG_BM_CAP16 2048
 #endif
 // RG_BM_WAIT1: thread 0 alone waits for the group's TMA copy, the block barrier
 // hands the completion on (no spinning warps). RG_BM_PERSIST: the several-
@@ -81,6 +83,16 @@ namespace rg {
 #endif
 #ifndef RG_BM_PERSIST
 #define RG_BM_PERSIST 0
+#endif
+// the big 16-B instance (V = 1): threads, CTAs per SM, bitmap bits (0: as the primary)
+#ifndef RG_BM_MED_THREADS
+#define RG_BM_MED_THREADS 512
+#endif
+#ifndef RG_BM_MED_BLOCKS
+#define RG_BM_MED_BLOCKS 2
+#endif
+#ifndef RG_BM_MED_BITS
+#define RG_BM_MED_BITS 0
 #endif
 #ifndef RG_BM_THREADS32
 #define RG_BM_THREADS32 512
@@ -109,8 +121,11 @@ struct BmCfg {
     using L = LocalCfg<RS>;
     static_assert(!L::kRegRecords, "shared-memory records only");
     static constexpr bool kTuned = RS == 16 && V == 0;
-    static constexpr int kThreads = kTuned ? RG_BM_THREADS : RS == 32 ? RG_BM_THREADS32 : L::kThreads;
-    static constexpr int kMinBlocks = kTuned ? RG_BM_BLOCKS : L::kMinBlocks;
+    static constexpr bool kMed = RS == 16 && V == 1;
+    static constexpr int kThreads = kTuned ? RG_BM_THREADS
+                                    : kMed ? RG_BM_MED_THREADS
+                                           : RS == 32 ? RG_BM_THREADS32 : L::kThreads;
+    static constexpr int kMinBlocks = kTuned ? RG_BM_BLOCKS : kMed ? RG_BM_MED_BLOCKS : L::kMinBlocks;
     static constexpr int kWarps = kThreads / 32;
     static constexpr int kCap = kTuned ? RG_BM_CAP16 : L::kCap;
     static_assert(kCap <= L::kCap, "the bucket sort takes over whole groups");
@@ -118,7 +133,8 @@ struct BmCfg {
     // cells per record aimed at, as a power of two: FB = ceil(log2 n) + kCellLog
     static constexpr int kCellLog = RG_BM_CELL_LOG;
     // cells = 2^kFineBits at most
-    static constexpr int kFineBits = RG_BM_BITS ? RG_BM_BITS : ceil_log2_c(kCap) + kCellLog;
+    static constexpr int kFineBits = (kMed && RG_BM_MED_BITS) ? RG_BM_MED_BITS
+                                     : RG_BM_BITS ? RG_BM_BITS : ceil_log2_c(kCap) + kCellLog;
     static constexpr int kWords = 1 << (kFineBits - 5);
     // scan: every warp owns kRows rows of 128 words
     static constexpr int kRows = (kWords + 128 * kWarps - 1) / (128 * kWarps);
@@ -251,7 +267,7 @@ __device__ __forceinline__ void local_group_bm(
     const uint32_t n = g.size;
     const uint8_t* gsrc = (g.parity ? tmp : data) + g.start * RS;
     uint8_t* dst = data + g.start * RS;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     if constexpr (V == 0 && kBmHasBig<RS>) {
         if (n > uint32_t(C::kCap)) {  // a single bin above this instance's capacity
             if (threadIdx.x == 0) push_group(med, g);

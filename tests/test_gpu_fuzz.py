@@ -62,7 +62,7 @@ def test_random_shapes_match_the_oracle(rg, torch_cuda, case):
     rng = np.random.default_rng(0xF022 + case)
     rs, ks = LAYOUTS[case % len(LAYOUTS)]
     cap = rg.local_capacity(rs)
-    n = int(rng.choice([2, 17, 255, 1727, 1729, cap - 1, cap, cap + 1, 2 * cap + 5, 20_000, 70_000,
+    n = int(rng.choice([2, 17, 255, 2047, 2049, cap - 1, cap, cap + 1, 2 * cap + 5, 20_000, 70_000,
                         150_000, 400_000]))
     a = make_input(n, rs, ks, 0xF0220000 + case)
     name = _shape(rng, a, n, rs, ks)

@@ -34,7 +34,7 @@ def _check(rg, torch, a, rs, ks):
 
 
 @pytest.mark.parametrize("rs,ks", [(8, 8), (8, 5), (16, 8), (16, 16), (24, 16), (32, 24), (32, 8)])
-@pytest.mark.parametrize("n", [2, 3, 31, 127, 128, 129, 1000, 1727, 1728, 1729, 1792, 2048, 2500, 3584, 16384,
+@pytest.mark.parametrize("n", [2, 3, 31, 127, 128, 129, 1000, 1727, 1728, 1729, 2047, 2048, 2049, 2500, 3584, 16384,
                                18432])
 def test_single_group_uniform_keys_stay_in_the_bitmap_sort(rg, torch_cuda, rs, ks, n):
     if n > rg.local_capacity(rs):
@@ -129,7 +129,7 @@ def test_key_ends_inside_the_window(rg, torch_cuda):
 
 
 def test_medium_bins_take_the_big_instance(rg, torch_cuda):
-    """16-B records: bins of ~3000 records (above the primary capacity of 1728,
+    """16-B records: bins of ~3000 records (above the primary capacity of 2048,
     within the local-sort capacity) are groups of their own, sorted by the
     big instance over the device-counted list."""
     rs, ks = 16, 8
