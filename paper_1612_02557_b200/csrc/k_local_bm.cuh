@@ -74,6 +74,10 @@ namespace rg {
 #ifndef RG_BM_KNOWN
 #define RG_BM_KNOWN 1
 #endif
+// L2 eviction hint of the final record stores (0 none, 1 evict_first, 2 evict_last)
+#ifndef RG_HINT_LOCST
+#define RG_HINT_LOCST 0
+#endif
 // RG_BM_CHUNKS (16/32-B records): the group's TMA copy is issued as one bulk
 // copy per loop iteration's records (T records), each with its own mbarrier,
 // and the first pass over the records waits chunk by chunk: it runs while the
@@ -470,7 +474,7 @@ __device__ __forceinline__ void local_group_bm(
             const uint32_t m = bm[word];
             if (pv < 0x8000u) {
                 const uint32_t pos = pv + __popc(m & ((1u << (f & 31u)) - 1u));
-                store_rec<RS>(dst, pos, ld_smem_rec<RS>(recs, e));
+                store_rec_h<RS, RG_HINT_LOCST>(dst, pos, ld_smem_rec<RS>(recs, e));
             } else {
                 const uint32_t old = atomicAdd(&bm[word], 1u << 24);
                 dl[(pv & 0x7FFFu) + (old >> 24)] = uint16_t(e);
