@@ -610,6 +610,15 @@ int grid_for(uint64_t n, int threads, int per_sm) {
 #ifndef RG_LOC_BM8
 #define RG_LOC_BM8 1
 #endif
+// L2 prefetch distance of the bitmap local sort, in resident waves (NUM / DEN).
+// Measured (C5 local sort): 2 waves 30.4 ms, 1 wave 28.4, 1/2 wave 28.0-28.1,
+// 1/4 wave 28.1.
+#ifndef RG_BM_AHEAD_NUM
+#define RG_BM_AHEAD_NUM 1
+#endif
+#ifndef RG_BM_AHEAD_DEN
+#define RG_BM_AHEAD_DEN 2
+#endif
 template <int RS>
 constexpr uint32_t local_cap() {
     return LocalCfg<RS>::kCap;
@@ -835,7 +844,7 @@ void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, 
                     : ngroups;
             k_local_bm<RS><<<bgrid, BmCfg<RS>::kThreads, BmCfg<RS>::kSmem, st>>>(
                 data, tmp, ws.groups.p, ngroups, ks, ctr, spill, med,
-                uint32_t(sm_count()) * BmCfg<RS>::kMinBlocks);
+                uint32_t(sm_count()) * BmCfg<RS>::kMinBlocks * RG_BM_AHEAD_NUM / RG_BM_AHEAD_DEN);
             note_launch();
             RG_LAUNCH_CHECK();
             if constexpr (kBmHasBig<RS>) {
