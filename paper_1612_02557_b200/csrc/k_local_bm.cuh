@@ -527,7 +527,7 @@ __device__ __forceinline__ void local_group_bm(
 }
 
 // Bitmap local sort launch: the shapes of k_local (several CTAs per SM: a CTA
-// per group, the group one resident wave ahead prefetched into L2; one CTA per
+// per group, the group half a resident wave ahead prefetched into L2; one CTA per
 // SM: persistent, groups round-robin, next descriptor by cp.async).
 template <int RS>
 __global__ void __launch_bounds__(BmCfg<RS>::kThreads, BmCfg<RS>::kMinBlocks) k_local_bm(
