@@ -73,6 +73,18 @@ def test_version_and_stats_struct():
     assert C.sizeof(_lib.Stats) == 4 + 4 + 8 * 8  # (round 2: + bitmap_spill_groups)
 
 
+def test_stats_struct_fields_match_the_header():
+    """The ctypes mirror of raduls_gpu_stats has the header's fields, in order
+    and with the header's widths (an ABI drift would misread every counter)."""
+    txt = open(HEADER).read()
+    body = re.search(r"typedef struct \{(.*?)\} raduls_gpu_stats;", txt, flags=re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = re.findall(r"(uint32_t|uint64_t)\s+(\w+)\s*;", body)
+    want = [(name, C.c_uint32 if t == "uint32_t" else C.c_uint64) for t, name in fields]
+    assert want == list(_lib.Stats._fields_)
+    assert want[-1][0] == "bitmap_spill_groups"
+
+
 def test_lsd_rejects_bad_config_and_layouts_without_gpu():
     """test_lsd.cpp:69-77: lane sizes 63 and 0, layout (8, 16) -> invalid_argument."""
     L = _lib.load()
