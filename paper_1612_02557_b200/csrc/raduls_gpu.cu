@@ -1574,11 +1574,15 @@ int raduls_gpu_sort_host(uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t rs, u
         Workspace& ws = workspace();
         std::lock_guard<std::mutex> lk(ws.mu);
         HostBufs hb(ws);
-        ws.host_data.ensure(bytes);
-        cudaStream_t st = nullptr;
-        HostStager& hs = ws.host_stager();
         const bool timing = std::getenv("RADULS_GPU_HOST_TIMING") != nullptr;
         auto now = [] { return std::chrono::steady_clock::now(); };
+        const auto ta = now();
+        ws.host_data.ensure(bytes);
+        if (timing)
+            std::fprintf(stderr, "raduls_gpu_sort_host: data buffer %.1f ms\n",
+                         std::chrono::duration<double, std::milli>(now() - ta).count());
+        cudaStream_t st = nullptr;
+        HostStager& hs = ws.host_stager();
         const auto t0 = now();
         hs.h2d(ws.host_data.p, data, bytes, st);
         ws.host_tmp.ensure(bytes);  // (pinned input: mapped while the copy runs)
