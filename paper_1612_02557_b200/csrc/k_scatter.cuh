@@ -11,11 +11,15 @@
 //   * warp 8 (producer) claims tiles in order through a global ticket, skips tiles of segments the planner did not split,
 //     and TMA-loads each tile (cp.async.bulk, mbarrier transaction count) into
 //     one of two shared-memory buffers;
-//   * warps 0-7 (consumers) rank the tile's records by digit with a ballot
-//     multisplit (warp_rank: peers of a digit from eight ballots, rank =
-//     warp-private counter + popc(peers & lanemask_lt) -- stable by
-//     construction: warp-striped input order, digit-major/warp-minor
-//     offsets), build a slot map in digit order, and write the records out in
+//   * warps 0-7 (consumers) rank the tile's records by digit inside their warp
+//     (warp_rank, common.cuh; warp-striped input order, warp-private counters,
+//     digit-major/warp-minor offsets): kRank 1 -- peers of a digit from eight
+//     ballots, rank = counter + popc(peers & lanemask_lt), stable by
+//     construction; kRank 0 -- one shared-memory atomic per record, stable only
+//     if the hardware serves the lanes of one atomic in lane order, so it is
+//     launched only after k_rank_selftest confirmed that on the device
+//     (atomic_rank_ok, raduls_gpu.cu; C5 scatter 73.6 vs 94.7 ms). They then
+//     build a slot map in digit order, and write the records out in
 //     that order: consecutive slots of one digit go to consecutive destinations,
 //     so every digit run becomes one contiguous span of 16-B (8-B) vector
 //     stores — the GPU analogue of the 256-B write-combining lanes.
