@@ -37,8 +37,8 @@
 // varying bytes and may hand the group on to the LSD fallback.
 // Shapes: 16-B records, 256 threads, five CTAs per SM, groups of <= 2048
 // records (a single bin between that and LocalCfg::kCap is a group of its
-// own for the 512-thread instance, k_local_bm_med); 24/32-B records in the
-// bucket sort's shapes; 8-B records in registers (k_local_bm8).
+// own for the 512-thread instance, k_local_bm_med); 24-B records alike with
+// groups of <= 1280; 32-B records in the bucket sort's shape; 8-B records in registers (k_local_bm8).
 #pragma once
 
 #include "k_local.cuh"
@@ -98,6 +98,16 @@ namespace rg {
 #ifndef RG_BM_MED_BITS
 #define RG_BM_MED_BITS 0
 #endif
+// 24-B primary instance: RG_BM_THREADS threads, RG_BM_BLOCKS24 CTAs per SM,
+// groups of <= RG_BM_CAP24 records (0: the bucket sort's shape, 512 threads x 2,
+// cap 2560). Measured on 2^28 x 24 B: local sort 2.50 (1280 x 5) / 2.52 (1024 x
+// 6) vs 3.36 ms; a single bin above the capacity goes to the 512-thread instance.
+#ifndef RG_BM_CAP24
+#define RG_BM_CAP24 1280
+#endif
+#ifndef RG_BM_BLOCKS24
+#define RG_BM_BLOCKS24 5
+#endif
 #ifndef RG_BM_THREADS32
 #define RG_BM_THREADS32 512
 #endif
@@ -125,13 +135,16 @@ struct BmCfg {
     using L = LocalCfg<RS>;
     static_assert(!L::kRegRecords, "shared-memory records only");
     static constexpr bool kTuned = RS == 16 && V == 0;
+    static constexpr bool kTuned24 = RS == 24 && V == 0 && RG_BM_CAP24 != 0;
     static constexpr bool kMed = RS == 16 && V == 1;
-    static constexpr int kThreads = kTuned ? RG_BM_THREADS
+    static constexpr int kThreads = (kTuned || kTuned24) ? RG_BM_THREADS
                                     : kMed ? RG_BM_MED_THREADS
                                            : RS == 32 ? RG_BM_THREADS32 : L::kThreads;
-    static constexpr int kMinBlocks = kTuned ? RG_BM_BLOCKS : kMed ? RG_BM_MED_BLOCKS : L::kMinBlocks;
+    static constexpr int kMinBlocks = kTuned ? RG_BM_BLOCKS
+                                      : kTuned24 ? RG_BM_BLOCKS24
+                                                 : kMed ? RG_BM_MED_BLOCKS : L::kMinBlocks;
     static constexpr int kWarps = kThreads / 32;
-    static constexpr int kCap = kTuned ? RG_BM_CAP16 : L::kCap;
+    static constexpr int kCap = kTuned ? RG_BM_CAP16 : kTuned24 ? RG_BM_CAP24 : L::kCap;
     static_assert(kCap <= L::kCap, "the bucket sort takes over whole groups");
     static constexpr int kIpt = (kCap + kThreads - 1) / kThreads;
     // cells per record aimed at, as a power of two: FB = ceil(log2 n) + kCellLog

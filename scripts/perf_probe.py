@@ -19,6 +19,8 @@ CONFIGS = {
     "c3": (1 << 29, 16, 8, 1, 0x5EED0003),
     "c4": (1 << 28, 32, 24, 0, 0x5EED0004),
     "c5": (1 << 32, 16, 8, 0, 0x5EED0005),
+    # not a BASELINE config: 24-B records (a reference layout) for shape A/Bs
+    "x24": (1 << 28, 24, 16, 0, 0x5EED0024),
 }
 
 

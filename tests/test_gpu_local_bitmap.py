@@ -34,7 +34,7 @@ def _check(rg, torch, a, rs, ks):
 
 
 @pytest.mark.parametrize("rs,ks", [(8, 8), (8, 5), (16, 8), (16, 16), (24, 16), (32, 24), (32, 8)])
-@pytest.mark.parametrize("n", [2, 3, 31, 127, 128, 129, 1000, 1727, 1728, 1729, 2047, 2048, 2049, 2500, 3584, 16384,
+@pytest.mark.parametrize("n", [2, 3, 31, 127, 128, 129, 1000, 1279, 1280, 1281, 1728, 2047, 2048, 2049, 2500, 3584, 16384,
                                18432])
 def test_single_group_uniform_keys_stay_in_the_bitmap_sort(rg, torch_cuda, rs, ks, n):
     if n > rg.local_capacity(rs):
@@ -143,6 +143,21 @@ def test_medium_bins_take_the_big_instance(rg, torch_cuda):
     st = _check(rg, torch_cuda, a, rs, ks)
     assert st["bitmap_spill_groups"] == 0, st
     assert st["local_records"] == n, st
+
+
+def test_medium_bins_24_byte_records(rg, torch_cuda):
+    """24-B records: bins of ~2000 records (above the primary capacity of 1280,
+    within the local-sort capacity of 2560) take the big instance."""
+    rs, ks = 24, 16
+    bins = 40
+    n = bins * 2000
+    a = make_input(n, rs, ks, 0x24ED)
+    r = a.reshape(n, rs)
+    rng = np.random.default_rng(4)
+    r[:, 0] = 7
+    r[:, 1] = np.repeat(np.arange(bins, dtype=np.uint8), 2000)[rng.permutation(n)]
+    st = _check(rg, torch_cuda, a, rs, ks)
+    assert st["bitmap_spill_groups"] == 0 and st["local_records"] == n, st
 
 
 def test_clustered_windows_inside_the_digit_range(rg, torch_cuda):
