@@ -98,6 +98,9 @@ namespace rg {
 #ifndef RG_BM_MED_BITS
 #define RG_BM_MED_BITS 0
 #endif
+#ifndef RG_BM_MED_PREFETCH
+#define RG_BM_MED_PREFETCH 1
+#endif
 // 24-B primary instance: RG_BM_THREADS threads, RG_BM_BLOCKS24 CTAs per SM,
 // groups of <= RG_BM_CAP24 records (0: the bucket sort's shape, 512 threads x 2,
 // cap 2560). Measured on 2^28 x 24 B: local sort 2.50 (1280 x 5) / 2.52 (1024 x
@@ -589,7 +592,11 @@ __global__ void __launch_bounds__(BmCfg<RS, 1>::kThreads, BmCfg<RS, 1>::kMinBloc
     LevelCounters* __restrict__ ctr, GroupList spill) {
     const uint32_t n = min(*med.n, med.cap);
     for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
-        local_group_bm<RS, 1>(data, tmp, med.list[i], ks, ctr, spill, med, [] {});
+        const uint32_t nx = i + gridDim.x;
+        auto mid = [&] {  // the CTA's next group toward L2 while this one is sorted
+            if (RG_BM_MED_PREFETCH && threadIdx.x == 0 && nx < n) prefetch_group_l2<RS>(data, tmp, med.list[nx]);
+        };
+        local_group_bm<RS, 1>(data, tmp, med.list[i], ks, ctr, spill, med, mid);
         __syncthreads();  // shared memory free for the next group
     }
 }
