@@ -623,6 +623,8 @@ struct LevelCounters {
     unsigned long long hist_digit_records;  // records histogrammed from the digit array (1 byte each)
     uint32_t n_skip;                     // segments re-queued at a later byte without a split
     uint32_t bm_spill;                   // groups the bitmap local sort handed to the bucket sort
+    uint32_t n_big_groups;               // groups above the bitmap sort's primary capacity (single bins)
+    uint32_t pad;
 };
 
 // Decoupled look-back status word: [63:62] flag, [61:0] value.

@@ -114,6 +114,16 @@ namespace rg {
 #ifndef RG_BM_THREADS32
 #define RG_BM_THREADS32 512
 #endif
+// 32-B primary instance in the small two-tier shape (0: off -- one 512-thread CTA
+// per SM takes every group). Measured: 2^26 x 32 B (1024-record bins) local sort
+// 1.01 vs 1.28 ms; C4's 4096-record bins are all above it, and the host then
+// launches the big instance over the whole list (n_big_groups from the planner).
+#ifndef RG_BM_CAP32
+#define RG_BM_CAP32 1280
+#endif
+#ifndef RG_BM_BLOCKS32
+#define RG_BM_BLOCKS32 4
+#endif
 #ifndef RG_BM_BITS
 #define RG_BM_BITS 0
 #endif
@@ -138,16 +148,16 @@ struct BmCfg {
     using L = LocalCfg<RS>;
     static_assert(!L::kRegRecords, "shared-memory records only");
     static constexpr bool kTuned = RS == 16 && V == 0;
-    static constexpr bool kTuned24 = RS == 24 && V == 0 && RG_BM_CAP24 != 0;
+    static constexpr bool kTuned24 = (RS == 24 && V == 0 && RG_BM_CAP24 != 0) || (RS == 32 && V == 0 && RG_BM_CAP32 != 0);
     static constexpr bool kMed = RS == 16 && V == 1;
     static constexpr int kThreads = (kTuned || kTuned24) ? RG_BM_THREADS
                                     : kMed ? RG_BM_MED_THREADS
                                            : RS == 32 ? RG_BM_THREADS32 : L::kThreads;
     static constexpr int kMinBlocks = kTuned ? RG_BM_BLOCKS
-                                      : kTuned24 ? RG_BM_BLOCKS24
+                                      : kTuned24 ? (RS == 24 ? RG_BM_BLOCKS24 : RG_BM_BLOCKS32)
                                                  : kMed ? RG_BM_MED_BLOCKS : L::kMinBlocks;
     static constexpr int kWarps = kThreads / 32;
-    static constexpr int kCap = kTuned ? RG_BM_CAP16 : kTuned24 ? RG_BM_CAP24 : L::kCap;
+    static constexpr int kCap = kTuned ? RG_BM_CAP16 : kTuned24 ? (RS == 24 ? RG_BM_CAP24 : RG_BM_CAP32) : L::kCap;
     static_assert(kCap <= L::kCap, "the bucket sort takes over whole groups");
     static constexpr int kIpt = (kCap + kThreads - 1) / kThreads;
     // cells per record aimed at, as a power of two: FB = ceil(log2 n) + kCellLog
@@ -545,15 +555,17 @@ __device__ __forceinline__ void local_group_bm(
 // Bitmap local sort launch: the shapes of k_local (several CTAs per SM: a CTA
 // per group, the group half a resident wave ahead prefetched into L2; one CTA per
 // SM: persistent, groups round-robin, next descriptor by cp.async).
-template <int RS>
-__global__ void __launch_bounds__(BmCfg<RS>::kThreads, BmCfg<RS>::kMinBlocks) k_local_bm(
+// V = 1: the big instance over the whole group list (the host launches it
+// instead when most groups are single bins above the primary capacity).
+template <int RS, int V = 0>
+__global__ void __launch_bounds__(BmCfg<RS, V>::kThreads, BmCfg<RS, V>::kMinBlocks) k_local_bm(
     uint8_t* __restrict__ data, uint8_t* __restrict__ tmp, const Group* __restrict__ groups,
     uint32_t n_groups, uint32_t ks, LevelCounters* __restrict__ ctr, GroupList spill, GroupList med,
     uint32_t ahead) {
-    if constexpr (BmCfg<RS>::kMinBlocks > 1 && !RG_BM_PERSIST) {
+    if constexpr (BmCfg<RS, V>::kMinBlocks > 1 && !RG_BM_PERSIST) {
         if (threadIdx.x == 0 && blockIdx.x + ahead < n_groups)
             prefetch_group_l2<RS>(data, tmp, groups[blockIdx.x + ahead]);
-        local_group_bm<RS, 0>(data, tmp, groups[blockIdx.x], ks, ctr, spill, med, [] {});
+        local_group_bm<RS, V>(data, tmp, groups[blockIdx.x], ks, ctr, spill, med, [] {});
         return;
     }
     __shared__ __align__(16) Group s_g[2];
@@ -576,7 +588,7 @@ __global__ void __launch_bounds__(BmCfg<RS>::kThreads, BmCfg<RS>::kMinBlocks) k_
                 prefetch_group_l2<RS>(data, tmp, s_g[buf ^ 1]);
             }
         };
-        local_group_bm<RS, 0>(data, tmp, g, ks, ctr, spill, med, mid);
+        local_group_bm<RS, V>(data, tmp, g, ks, ctr, spill, med, mid);
         if (threadIdx.x == 0 && more) cp_async_wait_all();
         __syncthreads();
         i = nx;

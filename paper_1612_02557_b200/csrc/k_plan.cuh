@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
             gr.parity = g.parity;
             gr.pad = 0;
             A.groups[atomicAdd(&A.ctr->n_groups, 1u)] = gr;
+            if (g.size > A.cap_group) atomicAdd(&A.ctr->n_big_groups, 1u);
         }
         return;
     }
@@ -325,17 +326,19 @@ __global__ void __launch_bounds__(256) k_plan(PlanArgs A) {
         }
         __syncthreads();
         if (tid == 0) {
-            uint32_t ng = 0;
+            uint32_t ng = 0, nbig = 0;
             for (uint32_t d0 = s_open[0]; d0 < uint32_t(kRadix);) {
                 const uint32_t e = s_end[d0];
                 s_gstart[ng] = g.start + s_off[d0];
                 s_gsize[ng] = s_P[e] - s_P[d0];
                 s_gdig[ng] = d0 | ((e - 1u) << 8) | 0x10000u;  // byte p of the group's records lies in [d0, e)
+                nbig += s_gsize[ng] > A.cap_group;
                 ++ng;
                 d0 = e < uint32_t(kRadix) ? s_open[e] : uint32_t(kRadix);
             }
             s_ngroups = ng;
             s_base = ng ? atomicAdd(&A.ctr->n_groups, ng) : 0u;
+            if (nbig) atomicAdd(&A.ctr->n_big_groups, nbig);
         }
     }
     __syncthreads();

@@ -682,9 +682,12 @@ void set_attrs(Workspace& ws) {
     } else {
         RG_CHECK(cudaFuncSetAttribute(k_local_bm<RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(BmCfg<RS>::kSmem)));
-        if constexpr (kBmHasBig<RS>)
+        if constexpr (kBmHasBig<RS>) {
             RG_CHECK(cudaFuncSetAttribute(k_local_bm_med<RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           int(BmCfg<RS, 1>::kSmem)));
+            RG_CHECK(cudaFuncSetAttribute(k_local_bm<RS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(BmCfg<RS, 1>::kSmem)));
+        }
     }
     RG_CHECK(cudaFuncSetAttribute(k_tile_hist<RS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(HistCfg<RS>::kSmem)));
@@ -808,7 +811,7 @@ bool bitmap_local() {
 // Launch the local sort over `ngroups` groups already in ws.groups.
 template <int RS>
 void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, uint32_t ks,
-                  LevelCounters* ctr, cudaStream_t st) {
+                  LevelCounters* ctr, cudaStream_t st, uint32_t n_big = 0) {
     if (!ngroups) return;
     const int pe = ws.prof.begin(K_LOCAL, st);
     // one CTA per SM: persistent, groups round-robin; two per SM: a CTA per group
@@ -842,18 +845,35 @@ void launch_local(Workspace& ws, uint8_t* data, uint8_t* tmp, uint32_t ngroups, 
                 (BmCfg<RS>::kMinBlocks == 1 || RG_BM_PERSIST)
                     ? std::min<uint32_t>(ngroups, uint32_t(sm_count()) * BmCfg<RS>::kMinBlocks)
                     : ngroups;
-            k_local_bm<RS><<<bgrid, BmCfg<RS>::kThreads, BmCfg<RS>::kSmem, st>>>(
-                data, tmp, ws.groups.p, ngroups, ks, ctr, spill, med,
-                uint32_t(sm_count()) * BmCfg<RS>::kMinBlocks * RG_BM_AHEAD_NUM / RG_BM_AHEAD_DEN);
-            note_launch();
-            RG_LAUNCH_CHECK();
-            if constexpr (kBmHasBig<RS>) {
-                const uint32_t mgrid =
-                    std::min<uint32_t>(ngroups, uint32_t(sm_count()) * BmCfg<RS, 1>::kMinBlocks);
-                k_local_bm_med<RS><<<mgrid, BmCfg<RS, 1>::kThreads, BmCfg<RS, 1>::kSmem, st>>>(
-                    data, tmp, med, ks, ctr, spill);
+            // most groups are single bins above the primary capacity: the big
+            // instance takes the whole list itself (no hand-over pass)
+            bool big_first = false;
+            if constexpr (kBmHasBig<RS>) big_first = 2ull * n_big > ngroups;
+            if (big_first) {
+                if constexpr (kBmHasBig<RS>) {
+                    const uint32_t ggrid = BmCfg<RS, 1>::kMinBlocks == 1
+                                               ? std::min<uint32_t>(ngroups, uint32_t(sm_count()))
+                                               : ngroups;
+                    k_local_bm<RS, 1><<<ggrid, BmCfg<RS, 1>::kThreads, BmCfg<RS, 1>::kSmem, st>>>(
+                        data, tmp, ws.groups.p, ngroups, ks, ctr, spill, med,
+                        uint32_t(sm_count()) * BmCfg<RS, 1>::kMinBlocks);
+                    note_launch();
+                    RG_LAUNCH_CHECK();
+                }
+            } else {
+                k_local_bm<RS><<<bgrid, BmCfg<RS>::kThreads, BmCfg<RS>::kSmem, st>>>(
+                    data, tmp, ws.groups.p, ngroups, ks, ctr, spill, med,
+                    uint32_t(sm_count()) * BmCfg<RS>::kMinBlocks * RG_BM_AHEAD_NUM / RG_BM_AHEAD_DEN);
                 note_launch();
                 RG_LAUNCH_CHECK();
+                if constexpr (kBmHasBig<RS>) {
+                    const uint32_t mgrid =
+                        std::min<uint32_t>(ngroups, uint32_t(sm_count()) * BmCfg<RS, 1>::kMinBlocks);
+                    k_local_bm_med<RS><<<mgrid, BmCfg<RS, 1>::kThreads, BmCfg<RS, 1>::kSmem, st>>>(
+                        data, tmp, med, ks, ctr, spill);
+                    note_launch();
+                    RG_LAUNCH_CHECK();
+                }
             }
             const uint32_t lgrid =
                 std::min<uint32_t>(ngroups, uint32_t(sm_count()) * LocalCfg<RS>::kMinBlocks);
@@ -990,7 +1010,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
         Group g{0, uint32_t(n), 0, 0, 0};
         RG_CHECK(cudaMemcpyAsync(ws.groups.p, &g, sizeof g, cudaMemcpyHostToDevice, st));
         RG_CHECK(cudaMemsetAsync(dctr, 0, sizeof(LevelCounters), st));
-        launch_local<RS>(ws, data, tmp, 1, ks, dctr, st);
+        launch_local<RS>(ws, data, tmp, 1, ks, dctr, st, n > uint64_t(group_cap<RS>()) ? 1u : 0u);
         read_counters_and_finish<RS>(ws, data, tmp, ks, dctr, 1, st);
         ws.prof.collect();
         stats.levels = 1;
@@ -1137,7 +1157,7 @@ void sort_impl(Workspace& ws, uint8_t* data, uint8_t* tmp, uint64_t n, uint32_t 
                                       nd_halves == 2 ? nd_in : nullptr);
             stats.scatter_launches++;
         }
-        launch_local<RS>(ws, data, tmp, h.n_groups, ks, c, st);
+        launch_local<RS>(ws, data, tmp, h.n_groups, ks, c, st, h.n_big_groups);
         if (h.n_copy) {
             pe = ws.prof.begin(K_COPY, st);
             k_copy_back<RS><<<h.n_copy, 256, 0, st>>>(data, tmp, ws.copies.p);

@@ -21,6 +21,7 @@ CONFIGS = {
     "c5": (1 << 32, 16, 8, 0, 0x5EED0005),
     # not a BASELINE config: 24-B records (a reference layout) for shape A/Bs
     "x24": (1 << 28, 24, 16, 0, 0x5EED0024),
+    "x32": (1 << 26, 32, 24, 0, 0x5EED0032),
 }
 
 

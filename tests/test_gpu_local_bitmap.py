@@ -160,6 +160,25 @@ def test_medium_bins_24_byte_records(rg, torch_cuda):
     assert st["bitmap_spill_groups"] == 0 and st["local_records"] == n, st
 
 
+@pytest.mark.parametrize("rs,ks,big,cnt", [(16, 8, 3000, 10), (24, 16, 2000, 10), (32, 24, 3000, 10),
+                                            (32, 24, 3000, 200)])
+def test_mixed_small_and_medium_bins(rg, torch_cuda, rs, ks, big, cnt):
+    """`cnt` bins of `big` records (single-bin groups above the primary capacity)
+    among 246 small bins: with few of them the primary instance runs first and
+    hands them to the big instance's list; when they are the majority of the
+    groups the host launches the big instance over the whole list."""
+    small = 246 - cnt if cnt < 246 else 0
+    sizes = [big] * cnt + [37] * small
+    n = sum(sizes)
+    a = make_input(n, rs, ks, 0x317ED + rs + cnt)
+    r = a.reshape(n, rs)
+    rng = np.random.default_rng(9)
+    r[:, 0] = 3
+    r[:, 1] = np.repeat(np.arange(len(sizes), dtype=np.uint8), sizes)[rng.permutation(n)]
+    st = _check(rg, torch_cuda, a, rs, ks)
+    assert st["bitmap_spill_groups"] == 0 and st["local_records"] == n, st
+
+
 def test_clustered_windows_inside_the_digit_range(rg, torch_cuda):
     """The planner hands the group its digit range, so the cell grid spans
     whole digits: windows clustered in a sliver of that range share cells and
